@@ -1,0 +1,228 @@
+// oracle/ref_capi.cpp — C entry points into the COMPILED REFERENCE.
+//
+// TEST INFRASTRUCTURE ONLY: built by oracle/Makefile against the unmodified
+// reference sources under /root/reference/proj/src into oracle/_ref/. Only
+// tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+// --impl reference) load it, as the checker / the reference CPU arm. Nothing in
+// the product links it.
+//
+// Every function calls the reference's public API only:
+//   TruncatedOperator (operators.hpp:28-54), apply_truncated_dense (:58-62),
+//   apply_smooth_dense (:66-70), apply_full_dense (:73-75), apply_split (:94-96),
+//   match_polynomial / split (kernel.hpp:63-66), random_vector (bench.hpp:24).
+// BASELINE-only features (fractional |r|^-alpha kernels, per-node delta(x),
+// C(x) and (kappa(x)+kappa(y))/2 weighting) are expressed through the
+// reference's own coefficient_fn hook (kernel.hpp:101) with an InverseS
+// profile and a Constant horizon delta_max (SURVEY.md §8(c) "Feature envelope").
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "nonloc/bench.hpp"
+#include "nonloc/kernel.hpp"
+#include "nonloc/operators.hpp"
+#include "nonloc/tree.hpp"
+
+using namespace nonloc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return 1;
+  if (dynamic_cast<const std::domain_error*>(&e)) return 2;
+  if (dynamic_cast<const std::out_of_range*>(&e)) return 3;
+  return 4;
+}
+
+KernelSpec make_spec(int dim, int family, int order, int horizon_kind,
+                     double delta0, double coeff, int symmetry) {
+  KernelSpec spec;
+  spec.dim = dim;
+  switch (family) {
+    case 0: spec.profile = RadialProfile::inverse_s(); break;
+    case 1: spec.profile = RadialProfile::conical(); break;
+    case 2: spec.profile = RadialProfile::regularized(order); break;
+    case 3: spec.profile = RadialProfile::truncated_polynomial(order); break;
+    default: throw std::invalid_argument("unknown family");
+  }
+  spec.horizon = {horizon_kind == 0 ? HorizonKind::Constant : HorizonKind::GaussianBump, delta0};
+  spec.coefficient_value = coeff;
+  spec.symmetry = symmetry == 0 ? SymmetryClass::NonDivergence : SymmetryClass::Divergence;
+  return spec;
+}
+
+double secs(std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_random_vector(int64_t n, uint64_t seed, double* out) {
+  try {
+    const auto v = random_vector(n, seed);
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_match_polynomial(int K, double c, double* coeffs) {
+  try {
+    const auto p = match_polynomial(RadialProfile::inverse_s(c), K);
+    for (int j = 0; j <= K; ++j) coeffs[j] = p.coeffs[j];
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_split(int K, double c, double* poly, double* tail, int* ntail) {
+  try {
+    const auto sk = split(RadialProfile::inverse_s(c), K);
+    for (int j = 0; j <= K; ++j) poly[j] = sk.polynomial.coeffs[j];
+    *ntail = static_cast<int>(sk.tail.size());
+    for (std::size_t j = 0; j < sk.tail.size(); ++j) tail[j] = sk.tail[j];
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_kappa(int K, double c, int64_t n, const double* s, double* out) {
+  try {
+    const auto sk = split(RadialProfile::inverse_s(c), K);
+    for (int64_t i = 0; i < n; ++i) out[i] = sk.kappa(s[i]);
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// Fast truncated apply (Steps 1-3). counters = {recur_calls, step2_ops, step3_ops};
+// times = {step1_seconds, apply_seconds (mean over reps)}.
+int ref_truncated_fast(int dim, int n, int K, int horizon_kind, double delta0,
+                       double coeff, const double* u, double* out,
+                       int64_t* counters, double* times, int reps) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    const KernelSpec spec = make_spec(dim, 3, K, horizon_kind, delta0, coeff, 0);
+    const auto t0 = std::chrono::steady_clock::now();
+    TruncatedOperator op(spec, g);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::vector<double> r;
+    if (reps < 1) reps = 1;
+    for (int k = 0; k < reps; ++k) r = op.apply(std::span<const double>(u, g.total));
+    const auto t2 = std::chrono::steady_clock::now();
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+    if (counters) {
+      counters[0] = op.recur_calls();
+      counters[1] = op.step2_ops() / reps;
+      counters[2] = op.step3_ops() / reps;
+    }
+    if (times) { times[0] = secs(t0, t1); times[1] = secs(t1, t2) / reps; }
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_truncated_dense(int dim, int n, int K, int horizon_kind, double delta0,
+                        double coeff, int rule, int form, const double* u,
+                        double* out, int64_t* pairs) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    const KernelSpec spec = make_spec(dim, 3, K, horizon_kind, delta0, coeff, 0);
+    const auto r = apply_truncated_dense(
+        spec, g, rule == 0 ? InclusionRule::Leaf : InclusionRule::Point,
+        std::span<const double>(u, g.total),
+        form == 0 ? ApplyForm::Mass : ApplyForm::Difference, pairs);
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_smooth_dense(int dim, int n, int K, int horizon_kind, double delta0,
+                     double coeff, const double* u, double* out, int64_t* pairs) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    const KernelSpec spec = make_spec(dim, 0, 0, horizon_kind, delta0, coeff, 0);
+    const SplitKernel sk = split(spec.profile, K);
+    const auto r = apply_smooth_dense(sk, spec, g, std::span<const double>(u, g.total), pairs);
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// family: 0 InverseS, 1 Conical, 2 Regularized(order), 3 Truncated(order).
+int ref_full_dense(int dim, int n, int family, int order, int horizon_kind,
+                   double delta0, double coeff, int symmetry, const double* u,
+                   double* out, int64_t* pairs) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    const KernelSpec spec = make_spec(dim, family, order, horizon_kind, delta0, coeff, symmetry);
+    const auto r = apply_full_dense(spec, g, std::span<const double>(u, g.total), pairs);
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// truncated: 0 FastLeafMass, 1 DensePointDifference (backend always Dense).
+int ref_apply_split(int dim, int n, int K, int horizon_kind, double delta0,
+                    double coeff, int truncated, const double* u, double* out) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    const KernelSpec spec = make_spec(dim, 0, 0, horizon_kind, delta0, coeff, 0);
+    SplitApplyOptions opt;
+    opt.backend = SmoothBackend::Dense;
+    opt.truncated = truncated == 0 ? TruncatedPath::FastLeafMass : TruncatedPath::DensePointDifference;
+    const auto r = apply_split(spec, g, K, std::span<const double>(u, g.total), opt);
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// BASELINE operator through the reference's apply_full_dense (Point rule,
+// Difference form, clipped exterior):
+//   out_i = h^d sum_{k!=i, |y-x|<delta_i} C_i * kw(x,y) * |y-x|^-alpha (u_k-u_i)
+// with kw = (kappa_i+kappa_k)/2 when kappa != NULL else 1. delta/cx are per-node
+// arrays (row-major). Expressed as InverseS (c=1), Constant horizon delta_max,
+// coefficient_fn(x,y) = [r<delta(x)] * omega(x,y) * delta_max^{d+1} * r, which
+// eval_omega (kernel.cpp:275-287) turns back into omega(x,y).
+int ref_full_dense_general(int dim, int n, const double* delta, double delta_max,
+                           const double* cx, const double* kappa, double alpha,
+                           const double* u, double* out, int64_t* pairs) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    KernelSpec spec;
+    spec.dim = dim;
+    spec.profile = RadialProfile::inverse_s(1.0);
+    spec.horizon = {HorizonKind::Constant, delta_max};
+    double dpow = delta_max;  // delta_max^{d+1}
+    for (int j = 0; j < dim; ++j) dpow *= delta_max;
+    const auto index_of = [g](const Point& p) {
+      std::int64_t flat = 0;
+      for (int j = 0; j < g.dim; ++j)
+        flat = flat * g.n + static_cast<std::int64_t>(std::floor(p[j] * g.n));
+      return flat;
+    };
+    spec.coefficient_fn = [=](const Point& x, const Point& y) {
+      double r2 = 0.0;
+      for (int j = 0; j < dim; ++j) { const double d = y[j] - x[j]; r2 += d * d; }
+      const double r = std::sqrt(r2);
+      const std::int64_t ix = index_of(x), iy = index_of(y);
+      if (!(r < delta[ix])) return 0.0;
+      double c = cx ? cx[ix] : 1.0;
+      if (kappa) c *= 0.5 * (kappa[ix] + kappa[iy]);
+      return c * std::pow(r, -alpha) * dpow * r;
+    };
+    const auto r = apply_full_dense(spec, g, std::span<const double>(u, g.total), pairs);
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+}  // extern "C"
