@@ -1,0 +1,158 @@
+/* include/nlgpu.h — C-ABI of the B200-native nonlocal-apply hot path.
+ *
+ * This is the drop-in boundary. Plain C types, plain
+ * pointers and sizes; no torch, no C++ types. A plan owns its device buffers;
+ * host-pointer entry points do the H2D/D2H copies themselves (blocking), the
+ * *_dev entry points take device pointers and a cudaStream_t (as void*) and
+ * are asynchronous on that stream (Krylov-resident use).
+ *
+ * Reference interfaces each entry point replaces (/root/reference/proj/...):
+ *   nlg_plan_create      TruncatedOperator::TruncatedOperator  include/nonloc/operators.hpp:32
+ *                        (Step 1: caches delta_, coeff_  src/operators.cpp:102-124), and the
+ *                        KernelSpec/Grid setup of apply_*_dense  operators.hpp:58-75
+ *   nlg_apply_fast       TruncatedOperator::apply               operators.hpp:34, operators.cpp:126-167
+ *                        (and, for the BASELINE kernels, the fast apply the reference lacks)
+ *   nlg_apply_direct     apply_truncated_dense                  operators.hpp:58-62, operators.cpp:169-204
+ *                        apply_smooth_dense                     operators.hpp:66-70, operators.cpp:206-234
+ *                        apply_full_dense                       operators.hpp:73-75, operators.cpp:236-260
+ *   nlg_counters         TruncatedOperator::{step2,step3}_ops / pair_count out-params
+ *                        operators.hpp:39-42, operators.cpp:193,225,253
+ *   nlg_match_polynomial match_polynomial                       kernel.hpp:63-64, kernel.cpp:184-207
+ *   nlg_split            split                                  kernel.hpp:66, kernel.cpp:209-245
+ *   nlg_last_error       the what() text of the reference's exceptions
+ *                        (std::invalid_argument / domain_error / out_of_range / runtime_error)
+ */
+#ifndef NLGPU_H
+#define NLGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NLG_ABI_VERSION 1
+
+typedef struct nlg_plan nlg_plan;
+
+/* Status codes; the C++ shim rethrows them as the reference's exception types
+ * (include/nonloc/*.hpp, SURVEY §8(b) "Errors"). */
+typedef enum {
+  NLG_OK = 0,
+  NLG_EINVAL = 1,      /* std::invalid_argument (config / size errors)       */
+  NLG_EDOMAIN = 2,     /* std::domain_error (singular evaluation at s = 0)   */
+  NLG_ERANGE = 3,      /* std::out_of_range (bad node index)                 */
+  NLG_ERUNTIME = 4,    /* std::runtime_error                                 */
+  NLG_ECUDA = 5,       /* CUDA error            -> std::runtime_error        */
+  NLG_ENCCL = 6,       /* collective error      -> std::runtime_error        */
+  NLG_EUNSUPPORTED = 7 /* valid request this build does not implement -> invalid_argument */
+} nlg_status;
+
+enum { NLG_LEAF = 0, NLG_POINT = 1 };            /* InclusionRule (operators.hpp:16) */
+enum { NLG_MASS = 0, NLG_DIFFERENCE = 1 };       /* ApplyForm (operators.hpp:20)     */
+enum { NLG_CLIP = 0, NLG_COLLAR = 1 };           /* exterior: clipped window (operators.cpp:36-38)
+                                                    or zero volume-constraint collar */
+enum {
+  NLG_TRUNCATED = 0,   /* gamma(s) = p(s), even polynomial in s (kernel.cpp:106-112)      */
+  NLG_INVERSE_S = 1,   /* gamma(s) = c/s                                                   */
+  NLG_CONICAL = 2,     /* gamma(s) = c/s (1-s)                                             */
+  NLG_KAPPA = 3,       /* gamma(s) = kappa(s), the split remainder (kernel.cpp:114-126)    */
+  NLG_FRACTIONAL = 4,  /* omega(x,y) = C(x) kw(x,y) |y-x|^-alpha (BASELINE cfg0/1/2/4)    */
+  NLG_PERIDYNAMIC = 5  /* vector: -h^d sum C(x)/|y-x| (e.(u_y-u_x)) e (BASELINE cfg3)      */
+};
+/* Which reference routine's bookkeeping a direct apply follows. */
+enum {
+  NLG_ROUTE_TRUNCATED = 0, /* apply_truncated_dense: self included, Mass/Difference, Leaf/Point */
+  NLG_ROUTE_SMOOTH = 1,    /* apply_smooth_dense:   self skipped, Point, Difference            */
+  NLG_ROUTE_FULL = 2       /* apply_full_dense:     self skipped, Point, Difference, eval_omega */
+};
+
+/* Operator description. Mirrors KernelSpec + Grid (kernel.hpp:97-108,
+ * geometry.hpp:18-26) flattened to POD: x-dependent parts arrive as host
+ * arrays evaluated at the nodes (delta_ / coeff_ of operators.cpp:119-120).
+ * Arrays are row-major (axis 0 slowest, geometry.cpp:86-97) over the plan's
+ * INPUT rows (see row_begin / row_end), or NULL for the scalar value. */
+typedef struct nlg_desc {
+  int dim;               /* 1, 2 or 3                                          */
+  int64_t n;             /* nodes per axis, h = 1/n, x_k = (k+1/2)h            */
+  int family;            /* NLG_TRUNCATED .. NLG_PERIDYNAMIC                   */
+  int route;             /* NLG_ROUTE_* (profile families only)                */
+  const double* poly;    /* TRUNCATED / KAPPA: p(s) = sum_j poly[j] s^{2j}     */
+  int npoly;
+  const double* tail;    /* KAPPA: tail(s) = sum_j tail[j] s^j                 */
+  int ntail;
+  int order;             /* KAPPA: K of the (1-s)^{K+1} factor                 */
+  double c;              /* profile constant                                   */
+  double alpha;          /* FRACTIONAL exponent (d + 2s)                       */
+  int rule;              /* NLG_LEAF / NLG_POINT                               */
+  int form;              /* NLG_MASS / NLG_DIFFERENCE                          */
+  int exterior;          /* NLG_CLIP / NLG_COLLAR                              */
+  int divergence;        /* horizon(x,y) = (delta(x)+delta(y))/2 (kernel.cpp:270-273) */
+  const double* delta;   /* delta(x_i) per node, or NULL -> delta0             */
+  double delta0;
+  double reach;          /* window radius (HorizonField::max_radius); <=0: max delta */
+  const double* coeff;   /* C(x_i) per node, or NULL -> coeff0                 */
+  double coeff0;
+  const double* kappa;   /* kappa(x_i) for (kappa(x)+kappa(y))/2 weighting, or NULL */
+  /* Slab sharding along axis 0. The plan produces output rows
+   * [row_begin, row_end) of axis 0; all per-node arrays above and the u passed
+   * to apply cover the INPUT rows [row_begin - halo_lo, row_end + halo_hi),
+   * where halo_lo/halo_hi come from nlg_plan_info(). row_end = 0 means the
+   * whole grid (no sharding). Per-node arrays must then cover the input rows,
+   * so call nlg_halo_rows() first to size them. */
+  int64_t row_begin;
+  int64_t row_end;
+  int device;            /* CUDA device ordinal                                */
+} nlg_desc;
+
+typedef struct nlg_info {
+  int64_t halo_lo, halo_hi;  /* input rows below / above the output slab       */
+  int64_t n_in, n_out;       /* nodes in the input / output slab               */
+  int fast_method;           /* 0 tiled direct quadrature, 1 span prefix sums
+                                (polynomial kernels), 2 exponential-sum scans
+                                (1-D fractional)                               */
+  int exp_terms;             /* far-field terms of the 1-D exponential sum     */
+  int near_cells;            /* near-field radius (cells) of the 1-D scan path */
+  double far_rel_err;        /* fitted kernel error of the exponential sum     */
+} nlg_info;
+
+/* Halo rows a slab [row_begin,row_end) needs for this operator, before the
+ * per-node arrays exist (uses delta0 / reach / the max of delta). */
+nlg_status nlg_halo_rows(const nlg_desc* desc, double delta_max, int64_t* halo);
+
+nlg_status nlg_plan_create(const nlg_desc* desc, nlg_plan** out);
+void nlg_plan_destroy(nlg_plan* plan);
+nlg_status nlg_plan_info(const nlg_plan* plan, nlg_info* info);
+
+/* Host pointers, blocking. u covers the input rows (components planes
+ * [dim][n_in] for PERIDYNAMIC); out covers the output rows. */
+nlg_status nlg_apply_fast(nlg_plan* plan, const double* u, double* out);
+nlg_status nlg_apply_direct(nlg_plan* plan, const double* u, double* out, int64_t* pair_count);
+
+/* Device pointers, asynchronous on `stream` (cudaStream_t, may be NULL). */
+nlg_status nlg_apply_fast_dev(nlg_plan* plan, const double* u_dev, double* out_dev, void* stream);
+nlg_status nlg_apply_direct_dev(nlg_plan* plan, const double* u_dev, double* out_dev,
+                                int64_t* pair_count_dev, void* stream);
+
+/* Direct apply at a subset of output nodes (flat indices into the output
+ * slab); used for sampled parity at BASELINE sizes. Host pointers, blocking. */
+nlg_status nlg_apply_direct_at(nlg_plan* plan, const double* u, const int64_t* targets,
+                               int64_t ntargets, double* out);
+
+/* Counters in the reference's semantics: pairs summed by the last direct apply
+ * (operators.cpp:193,225,253); number of fast applies issued. */
+nlg_status nlg_counters(const nlg_plan* plan, int64_t* pairs, int64_t* fast_applies);
+
+/* Kernel algebra (host setup, exact rationals for K <= 4 like kernel.cpp:26-51). */
+nlg_status nlg_match_polynomial(int K, double c, double* coeffs /* K+1 */);
+nlg_status nlg_split(int K, double c, double* poly /* K+1 */, double* tail /* >= K+1 */,
+                     int* ntail);
+
+/* Thread-local text of the last error; "" if none. */
+const char* nlg_last_error(void);
+int nlg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NLGPU_H */

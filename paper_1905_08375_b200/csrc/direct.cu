@@ -1,0 +1,260 @@
+// paper_1905_08375_b200/csrc/direct.cu — direct-sum applies (the in-repo
+// GPU oracle and the compute-bound fp64 kernel).
+//
+// One thread per target node; the thread walks the window around its node
+// (a superset of window_around, operators.cpp:31-42) and applies the exact
+// inclusion predicate of the route it reproduces:
+//   KIND 0  apply_truncated_dense  operators.cpp:169-204 (Leaf/Point, Mass/Difference, self included)
+//   KIND 1  apply_smooth_dense     operators.cpp:206-234 (Point, self skipped, kappa profile)
+//   KIND 2  apply_full_dense       operators.cpp:236-260 with eval_omega kernel.cpp:275-287
+//   KIND 3  BASELINE fractional    omega = C(x) kw(x,y) |y-x|^-alpha, Point rule
+//   KIND 4  BASELINE peridynamics  -h^d sum C(x)/|r| (e.(u_y-u_x)) e, Point rule
+// Exterior: clip (reference) or zero collar (u = 0 outside, kappa_y := kappa_x,
+// delta_y := delta_x outside).
+#include "plan.hpp"
+
+namespace nlg {
+
+namespace {
+
+struct DirectArgs {
+  Geom g;
+  Profile p;
+  const double* u;
+  const double* delta;
+  double delta0;
+  const double* coeff;
+  double coeff0;
+  const double* kappa;
+  double reach;
+  int rule, form, exterior, divergence;
+  const int64_t* targets;
+  int64_t ntargets;
+  double* out;
+  unsigned long long* pairs;
+};
+
+template <int DIM>
+__device__ __forceinline__ void unflatten(const Geom& g, int64_t t, int64_t* k) {
+  // output-slab flat index -> global multi-index
+  int64_t rest = t % g.stride0;
+  k[0] = g.row_begin + t / g.stride0;
+#pragma unroll
+  for (int j = DIM - 1; j >= 1; --j) {
+    k[j] = rest % g.n;
+    rest /= g.n;
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ int64_t in_index(const Geom& g, const int64_t* k) {
+  int64_t rest = 0;
+#pragma unroll
+  for (int j = 1; j < DIM; ++j) rest = rest * g.n + k[j];
+  return (k[0] - g.in_begin) * g.stride0 + rest;
+}
+
+template <int DIM, int KIND>
+__global__ void __launch_bounds__(256) direct_kernel(DirectArgs a) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long my_pairs = 0;
+  if (t < a.ntargets) {
+    const Geom& g = a.g;
+    const int64_t tt = a.targets ? a.targets[t] : t;
+    int64_t ki[3] = {0, 0, 0};
+    unflatten<DIM>(g, tt, ki);
+    const int64_t ii = in_index<DIM>(g, ki);
+    const double h = g.h;
+    double x[3];
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) x[j] = coord(ki[j], h);
+    const double delta = a.delta ? a.delta[ii] : a.delta0;
+    const double ci = a.coeff ? a.coeff[ii] : a.coeff0;
+    const double kap_i = a.kappa ? a.kappa[ii] : 1.0;
+    const bool collar = a.exterior == 1 && (KIND >= 2);
+    const double radius = (KIND == 2 && a.reach > 0.0) ? a.reach : delta;
+    const int64_t W = static_cast<int64_t>(floor(radius / h)) + 2;
+    int64_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) {
+      lo[j] = ki[j] - W;
+      hi[j] = ki[j] + W;
+      if (!collar) {
+        lo[j] = lo[j] < 0 ? 0 : lo[j];
+        hi[j] = hi[j] > g.n - 1 ? g.n - 1 : hi[j];
+      }
+    }
+    constexpr int NC = KIND == 4 ? DIM : 1;
+    double ui[NC];
+    const int64_t nin = (g.in_end - g.in_begin) * g.stride0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) ui[c] = a.u[c * nin + ii];
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    const double r2max = __dmul_rn(delta, delta);
+
+    int64_t k[3] = {0, 0, 0};
+    for (k[0] = lo[0]; k[0] <= hi[0]; ++k[0]) {
+      for (k[1] = (DIM > 1 ? lo[1] : 0); k[1] <= (DIM > 1 ? hi[1] : 0); ++k[1]) {
+        for (k[2] = (DIM > 2 ? lo[2] : 0); k[2] <= (DIM > 2 ? hi[2] : 0); ++k[2]) {
+          bool in_dom = true;
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) in_dom = in_dom && k[j] >= 0 && k[j] < g.n;
+          bool self = true;
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) self = self && k[j] == ki[j];
+          double y[3];
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) y[j] = coord(k[j], h);
+          // dist (operators.cpp:71-78), exact op order
+          double r2 = 0.0;
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) {
+            const double d = __dsub_rn(y[j], x[j]);
+            r2 = __dadd_rn(r2, __dmul_rn(d, d));
+          }
+          const double r = __dsqrt_rn(r2);
+          const int64_t kk = in_dom ? in_index<DIM>(g, k) : -1;
+          if (KIND == 0) {
+            bool in;
+            if (a.rule == 1) {
+              in = r < delta;
+            } else {
+              // cube_intersects_ball on the leaf box (geometry.cpp:63-76)
+              double dmin = 0.0;
+#pragma unroll
+              for (int j = 0; j < DIM; ++j) {
+                const double blo = __dmul_rn(static_cast<double>(k[j]), h);
+                const double bhi = __dmul_rn(static_cast<double>(k[j] + 1), h);
+                if (blo > x[j]) {
+                  const double d = __dsub_rn(blo, x[j]);
+                  dmin = __dadd_rn(dmin, __dmul_rn(d, d));
+                } else if (bhi < x[j]) {
+                  const double d = __dsub_rn(bhi, x[j]);
+                  dmin = __dadd_rn(dmin, __dmul_rn(d, d));
+                }
+              }
+              in = dmin < r2max;
+            }
+            if (!in) continue;
+            ++my_pairs;
+            const double v = poly_eval(a.p, __ddiv_rn(r, delta));
+            acc[0] += a.form == 0 ? v * a.u[kk] : v * (a.u[kk] - ui[0]);
+          } else if (KIND == 1) {
+            if (self) continue;
+            if (r >= delta) continue;
+            ++my_pairs;
+            const double front = __ddiv_rn(1.0, delta_power(DIM, delta));
+            acc[0] += ci * front * kappa_eval(a.p, __ddiv_rn(r, delta)) * (a.u[kk] - ui[0]);
+          } else if (KIND == 2) {
+            if (self) continue;
+            double dl = delta;
+            if (a.divergence) {
+              const double dk = in_dom ? (a.delta ? a.delta[kk] : a.delta0) : delta;
+              dl = __dmul_rn(0.5, __dadd_rn(delta, dk));
+            }
+            if (r >= dl) continue;
+            double c = ci;
+            if (a.kappa) c = c * (0.5 * (kap_i + (in_dom ? a.kappa[kk] : kap_i)));
+            const double w = __dmul_rn(__ddiv_rn(c, delta_power(DIM, dl)),
+                                       profile_eval(a.p, __ddiv_rn(r, dl)));
+            if (w == 0.0) continue;
+            ++my_pairs;
+            acc[0] += w * ((in_dom ? a.u[kk] : 0.0) - ui[0]);
+          } else if (KIND == 3) {
+            if (self) continue;
+            if (!(r < delta)) continue;
+            ++my_pairs;
+            double c = ci;
+            if (a.kappa) c = c * (0.5 * (kap_i + (in_dom ? a.kappa[kk] : kap_i)));
+            const double w = c * pow(r, -a.p.alpha);
+            acc[0] += w * ((in_dom ? a.u[kk] : 0.0) - ui[0]);
+          } else {
+            if (self) continue;
+            if (!(r < delta)) continue;
+            ++my_pairs;
+            double e[3];
+            double proj = 0.0;
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+              e[j] = __ddiv_rn(__dsub_rn(y[j], x[j]), r);
+              const double du = (in_dom ? a.u[j * nin + kk] : 0.0) - ui[j];
+              proj += e[j] * du;
+            }
+            const double w = __ddiv_rn(ci, r);
+#pragma unroll
+            for (int j = 0; j < NC; ++j) acc[j] += w * proj * e[j];
+          }
+        }
+      }
+    }
+    const int64_t nout = a.targets ? a.ntargets : (g.row_end - g.row_begin) * g.stride0;
+    if (KIND == 0) {
+      const double front = __ddiv_rn(ci, delta_power(DIM, delta));
+      a.out[t] = a.form == 0 ? front * (g.hd * acc[0] - ball_volume(DIM, delta) * ui[0])
+                             : front * g.hd * acc[0];
+    } else if (KIND == 4) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) a.out[c * nout + t] = -g.hd * acc[c];
+    } else {
+      a.out[t] = g.hd * acc[0];
+    }
+  }
+  if (a.pairs) {
+    my_pairs = warp_sum(my_pairs);
+    if ((threadIdx.x & 31) == 0 && my_pairs) atomicAdd(a.pairs, my_pairs);
+  }
+}
+
+template <int DIM>
+void launch_dim(int kind, const DirectArgs& a, cudaStream_t s) {
+  const int threads = 256;
+  const unsigned blocks = static_cast<unsigned>((a.ntargets + threads - 1) / threads);
+  if (blocks == 0) return;
+  switch (kind) {
+    case 0: direct_kernel<DIM, 0><<<blocks, threads, 0, s>>>(a); break;
+    case 1: direct_kernel<DIM, 1><<<blocks, threads, 0, s>>>(a); break;
+    case 2: direct_kernel<DIM, 2><<<blocks, threads, 0, s>>>(a); break;
+    case 3: direct_kernel<DIM, 3><<<blocks, threads, 0, s>>>(a); break;
+    default: direct_kernel<DIM, 4><<<blocks, threads, 0, s>>>(a); break;
+  }
+}
+
+}  // namespace
+
+int direct_kind(const Plan& P) {
+  if (P.family == 5) return 4;
+  if (P.family == 4) return 3;
+  return P.route;  // 0 truncated, 1 smooth, 2 full
+}
+
+void launch_direct(const Plan& P, const double* u, double* out, const int64_t* targets,
+                   int64_t ntargets, unsigned long long* pairs, cudaStream_t s) {
+  DirectArgs a;
+  a.g = P.geom;
+  a.p = P.prof;
+  a.u = u;
+  a.delta = P.d_delta;
+  a.delta0 = P.delta0;
+  a.coeff = P.d_coeff;
+  a.coeff0 = P.coeff0;
+  a.kappa = P.d_kappa;
+  a.reach = P.reach;
+  a.rule = P.rule;
+  a.form = P.form;
+  a.exterior = P.exterior;
+  a.divergence = P.divergence;
+  a.targets = targets;
+  a.ntargets = targets ? ntargets : P.n_out;
+  a.out = out;
+  a.pairs = pairs;
+  const int kind = direct_kind(P);
+  switch (P.geom.dim) {
+    case 1: launch_dim<1>(kind, a, s); break;
+    case 2: launch_dim<2>(kind, a, s); break;
+    default: launch_dim<3>(kind, a, s); break;
+  }
+}
+
+}  // namespace nlg

@@ -1,0 +1,378 @@
+// paper_1905_08375_b200/csrc/plan.cu — the C-ABI (include/nlgpu.h).
+//
+// nlg_plan_create is Step 1 of the reference (TruncatedOperator ctor,
+// operators.cpp:102-124): it validates the spec, uploads the per-node delta /
+// C / kappa arrays the reference caches (delta_, coeff_, operators.cpp:119-120)
+// and prepares the fast method. There is no panel list: the GPU replaces
+// Algorithm 1 by spans / scans computed on the fly.
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "plan.hpp"
+
+struct nlg_plan {
+  nlg::Plan p;
+};
+
+namespace nlg {
+namespace {
+
+thread_local std::string g_last_error;
+
+nlg_status fail(nlg_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+template <typename F>
+nlg_status guard(F&& f) {
+  try {
+    g_last_error.clear();
+    f();
+    return NLG_OK;
+  } catch (const Error& e) {
+    return fail(e.code, e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(NLG_ERUNTIME, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(NLG_ERUNTIME, e.what());
+  }
+}
+
+void require(bool ok, const char* msg, nlg_status code = NLG_EINVAL) {
+  if (!ok) throw Error{code, msg};
+}
+
+int64_t ipow(int64_t n, int d) {
+  int64_t r = 1;
+  for (int j = 0; j < d; ++j) r *= n;
+  return r;
+}
+
+// Window radius (cells) of a node with horizon `radius`: the direct kernel
+// walks +-(floor(radius/h) + 2), a superset of window_around (operators.cpp:31-42).
+int64_t window_cells(double radius, double h) {
+  return static_cast<int64_t>(std::floor(radius / h)) + 2;
+}
+
+double desc_radius(const nlg_desc& d, double delta_max) {
+  double r = delta_max;
+  if (d.family <= 3 && d.route == NLG_ROUTE_FULL && d.reach > 0) r = std::max(r, d.reach);
+  return r;
+}
+
+void validate(const nlg_desc& d) {
+  require(d.dim >= 1 && d.dim <= 3, "grid dimension must be 1, 2 or 3");
+  require(d.n >= 2, "grid n must be >= 2");
+  require(d.family >= 0 && d.family <= 5, "unknown kernel family");
+  require(d.route >= 0 && d.route <= 2, "unknown route");
+  require(d.rule == 0 || d.rule == 1, "unknown inclusion rule");
+  require(d.form == 0 || d.form == 1, "unknown apply form");
+  require(d.exterior == 0 || d.exterior == 1, "unknown exterior mode");
+  if (d.family == NLG_TRUNCATED || d.family == NLG_KAPPA) {
+    require(d.poly && d.npoly >= 1 && d.npoly <= kMaxPoly, "polynomial coefficients required");
+  }
+  if (d.family == NLG_KAPPA) require(d.tail && d.ntail >= 1 && d.ntail <= kMaxTail, "kappa tail required");
+  if (d.family == NLG_TRUNCATED && d.route != NLG_ROUTE_TRUNCATED && d.route != NLG_ROUTE_FULL)
+    throw Error{NLG_EINVAL, "truncated profile: route must be TRUNCATED or FULL"};
+  if (d.family == NLG_FRACTIONAL || d.family == NLG_PERIDYNAMIC)
+    require(d.rule == NLG_POINT && d.form == NLG_DIFFERENCE,
+            "fractional / peridynamic kernels use the Point rule, Difference form");
+  if (d.route == NLG_ROUTE_TRUNCATED && d.family <= 3)
+    require(d.family == NLG_TRUNCATED, "operation requires a PolynomialTruncated profile");
+  const int64_t rb = d.row_begin, re = d.row_end == 0 ? d.n : d.row_end;
+  require(rb >= 0 && rb < re && re <= d.n, "invalid slab rows");
+}
+
+}  // namespace
+}  // namespace nlg
+
+using namespace nlg;
+
+extern "C" {
+
+const char* nlg_last_error(void) { return g_last_error.c_str(); }
+int nlg_abi_version(void) { return NLG_ABI_VERSION; }
+
+nlg_status nlg_halo_rows(const nlg_desc* desc, double delta_max, int64_t* halo) {
+  return guard([&] {
+    require(desc && halo, "null argument");
+    validate(*desc);
+    const double h = 1.0 / static_cast<double>(desc->n);
+    const double dm = std::max(std::max(delta_max, desc->delta0), desc->reach);
+    *halo = window_cells(desc_radius(*desc, dm), h);
+  });
+}
+
+nlg_status nlg_plan_create(const nlg_desc* desc, nlg_plan** out) {
+  nlg_plan* plan = nullptr;
+  nlg_status st = guard([&] {
+    require(desc && out, "null argument");
+    const nlg_desc& d = *desc;
+    validate(d);
+    plan = new nlg_plan();
+    Plan& P = plan->p;
+    P.family = d.family;
+    P.route = d.route;
+    P.rule = d.rule;
+    P.form = d.form;
+    P.exterior = d.exterior;
+    P.divergence = d.divergence;
+    P.device = d.device;
+    P.delta0 = d.delta0;
+    P.coeff0 = d.coeff0;
+    P.reach = d.reach;
+    Profile& pr = P.prof;
+    std::memset(&pr, 0, sizeof(pr));
+    pr.family = d.family;
+    pr.route = d.route;
+    pr.npoly = d.poly ? d.npoly : 0;
+    pr.ntail = d.tail ? d.ntail : 0;
+    pr.order = d.order;
+    pr.c = d.c;
+    pr.alpha = d.alpha;
+    for (int j = 0; j < pr.npoly; ++j) pr.poly[j] = d.poly[j];
+    for (int j = 0; j < pr.ntail; ++j) pr.tail[j] = d.tail[j];
+
+    Geom& g = P.geom;
+    g.dim = d.dim;
+    g.n = d.n;
+    g.h = 1.0 / static_cast<double>(d.n);
+    g.hd = g.h;
+    for (int j = 1; j < d.dim; ++j) g.hd *= g.h;
+    g.stride0 = ipow(d.n, d.dim - 1);
+    g.row_begin = d.row_begin;
+    g.row_end = d.row_end == 0 ? d.n : d.row_end;
+
+    // Halo rows: sharded plans (row range != whole grid) read their input
+    // rows [rb - H, re + H); H comes from the global horizon bound, which the
+    // caller states in `reach` when delta is an array (nlg_halo_rows gives the
+    // same H, so the caller can size its arrays first).
+    const bool sharded = !(g.row_begin == 0 && g.row_end == d.n);
+    if (sharded && d.delta) require(d.reach > 0.0, "sharded plan with a delta array needs reach = max delta");
+    const int64_t halo = window_cells(desc_radius(d, std::max(d.delta0, d.reach)), g.h);
+    {
+      const int64_t lo = std::min<int64_t>(halo, g.row_begin);
+      const int64_t hi = std::min<int64_t>(halo, d.n - g.row_end);
+      const int64_t cnt = (g.row_end + hi - (g.row_begin - lo)) * g.stride0;
+      double dm = d.delta0;
+      if (d.delta)
+        for (int64_t i = 0; i < cnt; ++i) dm = std::max(dm, d.delta[i]);
+      P.delta_max = dm;
+      if (sharded && d.delta) require(dm <= d.reach, "reach must bound every delta");
+    }
+    require(P.delta_max > 0.0, "radius must be positive");
+    P.halo_lo = std::min<int64_t>(halo, g.row_begin);
+    P.halo_hi = std::min<int64_t>(halo, d.n - g.row_end);
+    g.in_begin = g.row_begin - P.halo_lo;
+    g.in_end = g.row_end + P.halo_hi;
+    P.n_in = (g.in_end - g.in_begin) * g.stride0;
+    P.n_out = (g.row_end - g.row_begin) * g.stride0;
+
+    NLG_CUDA(cudaSetDevice(P.device));
+    NLG_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+    const size_t bytes_in = sizeof(double) * static_cast<size_t>(P.n_in);
+    if (d.delta) {
+      NLG_CUDA(cudaMalloc(&P.d_delta, bytes_in));
+      NLG_CUDA(cudaMemcpy(P.d_delta, d.delta, bytes_in, cudaMemcpyHostToDevice));
+    }
+    if (d.coeff) {
+      NLG_CUDA(cudaMalloc(&P.d_coeff, bytes_in));
+      NLG_CUDA(cudaMemcpy(P.d_coeff, d.coeff, bytes_in, cudaMemcpyHostToDevice));
+    }
+    if (d.kappa) {
+      NLG_CUDA(cudaMalloc(&P.d_kappa, bytes_in));
+      NLG_CUDA(cudaMemcpy(P.d_kappa, d.kappa, bytes_in, cudaMemcpyHostToDevice));
+    }
+    NLG_CUDA(cudaMalloc(&P.d_pairs, sizeof(unsigned long long)));
+
+    // fast method selection
+    if (P.family == NLG_TRUNCATED && P.route == NLG_ROUTE_TRUNCATED && pr.npoly == 1) {
+      P.fast_method = 1;
+      spans_setup(P);
+    } else if (P.family == NLG_FRACTIONAL && g.dim == 1) {
+      P.fast_method = 2;
+      expsum_setup(P);
+    } else {
+      P.fast_method = 0;
+    }
+    NLG_CUDA(cudaStreamSynchronize(P.stream));
+    *out = plan;
+  });
+  if (st != NLG_OK && plan) {
+    nlg_plan_destroy(plan);
+  }
+  return st;
+}
+
+void nlg_plan_destroy(nlg_plan* plan) {
+  if (!plan) return;
+  Plan& P = plan->p;
+  cudaSetDevice(P.device);
+  if (P.stream) cudaStreamSynchronize(P.stream);
+  spans_free(P);
+  expsum_free(P);
+  cudaFree(P.d_delta);
+  cudaFree(P.d_coeff);
+  cudaFree(P.d_kappa);
+  cudaFree(P.d_u);
+  cudaFree(P.d_out);
+  cudaFree(P.d_pairs);
+  cudaFree(P.d_targets);
+  if (P.stream) cudaStreamDestroy(P.stream);
+  delete plan;
+}
+
+nlg_status nlg_plan_info(const nlg_plan* plan, nlg_info* info) {
+  return guard([&] {
+    require(plan && info, "null argument");
+    const Plan& P = plan->p;
+    info->halo_lo = P.halo_lo;
+    info->halo_hi = P.halo_hi;
+    info->n_in = P.n_in;
+    info->n_out = P.n_out;
+    info->fast_method = P.fast_method;
+    info->exp_terms = P.es.terms;
+    info->near_cells = P.es.near;
+    info->far_rel_err = P.es.rel_err;
+  });
+}
+
+namespace {
+
+int components(const Plan& P) { return P.family == NLG_PERIDYNAMIC ? P.geom.dim : 1; }
+
+void ensure_staging(Plan& P) {
+  const int nc = components(P);
+  if (!P.d_u) NLG_CUDA(cudaMalloc(&P.d_u, sizeof(double) * nc * P.n_in));
+  if (!P.d_out) NLG_CUDA(cudaMalloc(&P.d_out, sizeof(double) * nc * P.n_out));
+}
+
+void fast_dev(Plan& P, const double* u, double* out, cudaStream_t s) {
+  switch (P.fast_method) {
+    case 1: spans_apply(P, u, out, s); break;
+    case 2: expsum_apply(P, u, out, s); break;
+    default: launch_direct(P, u, out, nullptr, 0, nullptr, s); break;
+  }
+  NLG_CUDA(cudaGetLastError());
+  ++P.fast_applies;
+}
+
+}  // namespace
+
+nlg_status nlg_apply_fast(nlg_plan* plan, const double* u, double* out) {
+  return guard([&] {
+    require(plan && u && out, "null argument");
+    Plan& P = plan->p;
+    NLG_CUDA(cudaSetDevice(P.device));
+    ensure_staging(P);
+    const int nc = components(P);
+    NLG_CUDA(cudaMemcpyAsync(P.d_u, u, sizeof(double) * nc * P.n_in, cudaMemcpyHostToDevice, P.stream));
+    fast_dev(P, P.d_u, P.d_out, P.stream);
+    NLG_CUDA(cudaMemcpyAsync(out, P.d_out, sizeof(double) * nc * P.n_out, cudaMemcpyDeviceToHost, P.stream));
+    NLG_CUDA(cudaStreamSynchronize(P.stream));
+  });
+}
+
+nlg_status nlg_apply_fast_dev(nlg_plan* plan, const double* u_dev, double* out_dev, void* stream) {
+  return guard([&] {
+    require(plan && u_dev && out_dev, "null argument");
+    Plan& P = plan->p;
+    NLG_CUDA(cudaSetDevice(P.device));
+    fast_dev(P, u_dev, out_dev, static_cast<cudaStream_t>(stream));
+  });
+}
+
+nlg_status nlg_apply_direct(nlg_plan* plan, const double* u, double* out, int64_t* pair_count) {
+  return guard([&] {
+    require(plan && u && out, "null argument");
+    Plan& P = plan->p;
+    NLG_CUDA(cudaSetDevice(P.device));
+    ensure_staging(P);
+    const int nc = components(P);
+    NLG_CUDA(cudaMemcpyAsync(P.d_u, u, sizeof(double) * nc * P.n_in, cudaMemcpyHostToDevice, P.stream));
+    NLG_CUDA(cudaMemsetAsync(P.d_pairs, 0, sizeof(unsigned long long), P.stream));
+    launch_direct(P, P.d_u, P.d_out, nullptr, 0, P.d_pairs, P.stream);
+    NLG_CUDA(cudaGetLastError());
+    unsigned long long pairs = 0;
+    NLG_CUDA(cudaMemcpyAsync(out, P.d_out, sizeof(double) * nc * P.n_out, cudaMemcpyDeviceToHost, P.stream));
+    NLG_CUDA(cudaMemcpyAsync(&pairs, P.d_pairs, sizeof(pairs), cudaMemcpyDeviceToHost, P.stream));
+    NLG_CUDA(cudaStreamSynchronize(P.stream));
+    P.last_pairs = static_cast<int64_t>(pairs);
+    if (pair_count) *pair_count += P.last_pairs;
+  });
+}
+
+nlg_status nlg_apply_direct_dev(nlg_plan* plan, const double* u_dev, double* out_dev,
+                                int64_t* pair_count_dev, void* stream) {
+  return guard([&] {
+    require(plan && u_dev && out_dev, "null argument");
+    Plan& P = plan->p;
+    NLG_CUDA(cudaSetDevice(P.device));
+    launch_direct(P, u_dev, out_dev, nullptr, 0,
+                  reinterpret_cast<unsigned long long*>(pair_count_dev),
+                  static_cast<cudaStream_t>(stream));
+    NLG_CUDA(cudaGetLastError());
+  });
+}
+
+nlg_status nlg_apply_direct_at(nlg_plan* plan, const double* u, const int64_t* targets,
+                               int64_t ntargets, double* out) {
+  return guard([&] {
+    require(plan && u && targets && out && ntargets >= 0, "null argument");
+    Plan& P = plan->p;
+    for (int64_t t = 0; t < ntargets; ++t)
+      if (targets[t] < 0 || targets[t] >= P.n_out) throw Error{NLG_ERANGE, "node index out of range"};
+    NLG_CUDA(cudaSetDevice(P.device));
+    ensure_staging(P);
+    if (P.targets_cap < ntargets) {
+      cudaFree(P.d_targets);
+      P.d_targets = nullptr;
+      NLG_CUDA(cudaMalloc(&P.d_targets, sizeof(int64_t) * std::max<int64_t>(ntargets, 1)));
+      P.targets_cap = ntargets;
+    }
+    const int nc = components(P);
+    double* d_o = nullptr;
+    NLG_CUDA(cudaMalloc(&d_o, sizeof(double) * nc * std::max<int64_t>(ntargets, 1)));
+    NLG_CUDA(cudaMemcpyAsync(P.d_u, u, sizeof(double) * nc * P.n_in, cudaMemcpyHostToDevice, P.stream));
+    NLG_CUDA(cudaMemcpyAsync(P.d_targets, targets, sizeof(int64_t) * ntargets, cudaMemcpyHostToDevice, P.stream));
+    launch_direct(P, P.d_u, d_o, P.d_targets, ntargets, nullptr, P.stream);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out, d_o, sizeof(double) * nc * ntargets, cudaMemcpyDeviceToHost, P.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(P.stream);
+    cudaFree(d_o);
+    if (e != cudaSuccess) throw Error{NLG_ECUDA, cudaGetErrorString(e)};
+  });
+}
+
+nlg_status nlg_counters(const nlg_plan* plan, int64_t* pairs, int64_t* fast_applies) {
+  return guard([&] {
+    require(plan, "null argument");
+    if (pairs) *pairs = plan->p.last_pairs;
+    if (fast_applies) *fast_applies = plan->p.fast_applies;
+  });
+}
+
+nlg_status nlg_match_polynomial(int K, double c, double* coeffs) {
+  return guard([&] {
+    require(coeffs, "null argument");
+    const auto p = match_polynomial(K, c);
+    for (size_t j = 0; j < p.size(); ++j) coeffs[j] = p[j];
+  });
+}
+
+nlg_status nlg_split(int K, double c, double* poly, double* tail, int* ntail) {
+  return guard([&] {
+    require(poly && tail && ntail, "null argument");
+    std::vector<double> p, t;
+    split_kernel(K, c, p, t);
+    for (size_t j = 0; j < p.size(); ++j) poly[j] = p[j];
+    for (size_t j = 0; j < t.size(); ++j) tail[j] = t[j];
+    *ntail = static_cast<int>(t.size());
+  });
+}
+
+}  // extern "C"

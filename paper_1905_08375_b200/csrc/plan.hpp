@@ -1,0 +1,97 @@
+// paper_1905_08375_b200/csrc/plan.hpp — the plan object behind nlg_plan.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/nlgpu.h"
+#include "common.cuh"
+
+namespace nlg {
+
+// Error plumbing: CUDA failures become NLG_ECUDA with the CUDA error string.
+struct Error {
+  nlg_status code;
+  std::string msg;
+};
+
+#define NLG_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      throw ::nlg::Error{NLG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+// 1-D exponential-sum far field (fast method 2).
+struct ExpSum {
+  int terms = 0;          // M
+  int near = 0;           // P: offsets 1..P summed directly
+  int64_t dmax = 0;       // largest horizon offset (cells)
+  double rel_err = 0.0;   // fitted max relative kernel error on [P+1, dmax]
+  std::vector<double> rate;   // t_m  (lambda_m = exp(-t_m))
+  std::vector<double> weight; // c_m
+};
+
+struct Plan {
+  int family = 0, route = 0, rule = 0, form = 0, exterior = 0, divergence = 0;
+  Profile prof{};
+  Geom geom{};
+  double delta0 = 0, coeff0 = 1, reach = 0, delta_max = 0;
+  int64_t n_in = 0, n_out = 0;
+  int64_t halo_lo = 0, halo_hi = 0;
+  int device = 0;
+  int fast_method = 0;
+  cudaStream_t stream = nullptr;
+
+  // per-node static fields over the input rows (device)
+  double* d_delta = nullptr;
+  double* d_coeff = nullptr;
+  double* d_kappa = nullptr;
+
+  // staging for the host entry points
+  double* d_u = nullptr;
+  double* d_out = nullptr;
+  unsigned long long* d_pairs = nullptr;
+  int64_t* d_targets = nullptr;
+  int64_t targets_cap = 0;
+
+  // fast method 1 (span prefix sums)
+  double* d_pref_hi = nullptr;   // local exclusive prefix, [rows][len]
+  double* d_pref_lo = nullptr;
+  double* d_seg_hi = nullptr;    // segment totals -> exclusive offsets
+  double* d_seg_lo = nullptr;
+  int64_t scan_rows = 0, scan_len = 0, scan_nseg = 0;
+
+  // fast method 2 (1-D exponential-sum scans)
+  ExpSum es;
+  double* d_es = nullptr;        // packed device tables
+  double* d_diag = nullptr;      // u-independent far-field diagonal per output node
+  double* d_carry = nullptr;     // block carries [fields][dirs][M][nblocks]
+  double* d_agg = nullptr;
+  int64_t es_nblocks = 0;
+  int* d_dcells = nullptr;       // per input node: horizon offset D_i (cells)
+
+  int64_t last_pairs = 0;
+  int64_t fast_applies = 0;
+};
+
+// kernels
+void launch_direct(const Plan& P, const double* u, double* out, const int64_t* targets,
+                   int64_t ntargets, unsigned long long* pairs, cudaStream_t s);
+int direct_kind(const Plan& P);
+void spans_setup(Plan& P);
+void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s);
+void spans_free(Plan& P);
+void expsum_setup(Plan& P);
+void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s);
+void expsum_free(Plan& P);
+
+// host algebra (algebra.cpp)
+std::vector<double> match_polynomial(int K, double c);
+void split_kernel(int K, double c, std::vector<double>& poly, std::vector<double>& tail);
+ExpSum fit_exponential_sum(double alpha, int near, int64_t dmax, double tol);
+
+}  // namespace nlg
