@@ -148,6 +148,13 @@ nlg_status nlg_match_polynomial(int K, double c, double* coeffs /* K+1 */);
 nlg_status nlg_split(int K, double c, double* poly /* K+1 */, double* tail /* >= K+1 */,
                      int* ntail);
 
+/* Far-field exponential sum used by the 1-D fast path (host, for tests and
+ * diagnostics): d^-alpha ~= sum_m weight[m] exp(-rate[m] d) on d in
+ * [near+1, dmax]. rate/weight must hold 64 entries; *rel_err is the max
+ * relative error over every integer d in the window. */
+nlg_status nlg_expsum_fit(double alpha, int near, int64_t dmax, double* rate, double* weight,
+                          int* terms, double* rel_err);
+
 /* Thread-local text of the last error; "" if none. */
 const char* nlg_last_error(void);
 int nlg_abi_version(void);

@@ -52,6 +52,7 @@ EXPORTS = {
     "nlg_counters": ([C.c_void_p, _ip, _ip], C.c_int),
     "nlg_match_polynomial": ([C.c_int, C.c_double, _dp], C.c_int),
     "nlg_split": ([C.c_int, C.c_double, _dp, _dp, C.POINTER(C.c_int)], C.c_int),
+    "nlg_expsum_fit": ([C.c_double, C.c_int, C.c_int64, _dp, _dp, C.POINTER(C.c_int), _dp], C.c_int),
     "nlg_last_error": ([], C.c_char_p),
     "nlg_abi_version": ([], C.c_int),
 }

@@ -6,6 +6,7 @@
 //   coefficients are the correctly rounded quotients the reference produces.
 // split_kernel: kappa(s) = c/s - p(s) written as c (1-s)^{K+1} tail(s) / s
 //   (kernel.cpp:209-245): tail = (1 - s p1(s)) / (1-s)^{K+1}, exact division.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <stdexcept>
@@ -110,6 +111,134 @@ void split_kernel(int K, double c, std::vector<double>& poly, std::vector<double
   for (const Q& r : num)
     tail.push_back(c * static_cast<double>(static_cast<long long>(r.p)) /
                    static_cast<double>(static_cast<long long>(r.q)));
+}
+
+}  // namespace nlg
+
+// ---------------------------------------------------------------------------
+// Exponential-sum fit of the far-field weights w_d = d^-alpha, d in [P+1, dmax]
+//   w_d ~= sum_m c_m exp(-t_m d)
+// 1. Trapezoid rule on r^-a = 1/Gamma(a) int exp(a s - r e^s) ds with step ds
+//    (exponentially convergent in 1/ds), truncated where terms fall below 1e-17.
+// 2. Terms with t_m dmax < cut are "ultra-slow": over the window they are a
+//    smooth near-polynomial function R(d). They are replaced by nslow
+//    exponentials with rates {0, geometric in [0.05, cut]/dmax} fitted to R by
+//    relatively-weighted least squares (Householder QR).
+// The fitted max relative error over EVERY integer d in the window is measured
+// and returned; the plan refuses the fast path if it exceeds `tol`.
+// ---------------------------------------------------------------------------
+
+namespace nlg {
+namespace {
+
+// Least squares min ||A x - b|| by Householder QR; A is m x n row-major.
+std::vector<double> lstsq(std::vector<double> A, std::vector<double> b, int m, int n) {
+  for (int k = 0; k < n; ++k) {
+    double nrm = 0.0;
+    for (int i = k; i < m; ++i) nrm += A[i * n + k] * A[i * n + k];
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0) continue;
+    const double alpha = A[k * n + k] > 0 ? -nrm : nrm;
+    std::vector<double> v(m - k);
+    for (int i = k; i < m; ++i) v[i - k] = A[i * n + k];
+    v[0] -= alpha;
+    double vn = 0.0;
+    for (double x : v) vn += x * x;
+    if (vn == 0.0) continue;
+    for (int j = k; j < n; ++j) {
+      double s = 0.0;
+      for (int i = k; i < m; ++i) s += v[i - k] * A[i * n + j];
+      s = 2.0 * s / vn;
+      for (int i = k; i < m; ++i) A[i * n + j] -= s * v[i - k];
+    }
+    double s = 0.0;
+    for (int i = k; i < m; ++i) s += v[i - k] * b[i];
+    s = 2.0 * s / vn;
+    for (int i = k; i < m; ++i) b[i] -= s * v[i - k];
+  }
+  std::vector<double> x(n, 0.0);
+  for (int k = n - 1; k >= 0; --k) {
+    double s = b[k];
+    for (int j = k + 1; j < n; ++j) s -= A[k * n + j] * x[j];
+    x[k] = A[k * n + k] != 0.0 ? s / A[k * n + k] : 0.0;
+  }
+  return x;
+}
+
+}  // namespace
+
+ExpSum fit_exponential_sum(double alpha, int near, int64_t dmax, double tol) {
+  ExpSum es;
+  es.near = near;
+  es.dmax = dmax;
+  const double d0 = near + 1.0;
+  const double D = static_cast<double>(dmax);
+  if (dmax <= near) return es;  // no far field
+  const double lg = std::lgamma(alpha);
+  const double ds = 0.3, cut = 0.5;
+  const int nslow = 6;
+  const double smin = std::log(1e-16) / alpha - std::log(D) - 2.0;
+  const double smax = std::log(38.0 / d0);
+  std::vector<double> ut, uc;  // ultra-slow trapezoid terms
+  for (long k = static_cast<long>(std::floor(smin / ds)); k * ds <= smax + ds; ++k) {
+    const double s = k * ds;
+    const double t = std::exp(s);
+    const double c = ds * std::exp(alpha * s - lg);
+    if (t * D < cut) {
+      ut.push_back(t);
+      uc.push_back(c);
+    } else {
+      es.rate.push_back(t);
+      es.weight.push_back(c);
+    }
+  }
+  // fit the ultra-slow remainder R(d) on log-spaced samples, weight 1/w(d)
+  std::vector<double> srates{0.0};
+  for (int j = 0; j < nslow - 1; ++j)
+    srates.push_back(0.05 * std::pow(cut / 0.05, j / double(nslow - 2)) / D);
+  const int ns = static_cast<int>(srates.size());
+  std::vector<double> xs;
+  for (int q = 0; q < 3000; ++q) {
+    const double x = std::round(d0 * std::pow(D / d0, q / 2999.0));
+    if (xs.empty() || x != xs.back()) xs.push_back(x);
+  }
+  const int m = static_cast<int>(xs.size());
+  std::vector<double> A(static_cast<size_t>(m) * ns), b(m);
+  for (int i = 0; i < m; ++i) {
+    const double wi = std::pow(xs[i], alpha);  // 1 / w(d)
+    double r = 0.0;
+    for (size_t k = 0; k < ut.size(); ++k) r += uc[k] * std::exp(-ut[k] * xs[i]);
+    b[i] = r * wi;
+    for (int j = 0; j < ns; ++j) A[i * ns + j] = std::exp(-srates[j] * xs[i]) * wi;
+  }
+  const auto cs = lstsq(A, b, m, ns);
+  for (int j = 0; j < ns; ++j) {
+    es.rate.push_back(srates[j]);
+    es.weight.push_back(cs[j]);
+  }
+  // order by rate (slow terms last is irrelevant; kernels sort by use)
+  std::vector<int> idx(es.rate.size());
+  for (size_t i = 0; i < idx.size(); ++i) idx[i] = static_cast<int>(i);
+  std::sort(idx.begin(), idx.end(), [&](int a, int b2) { return es.rate[a] < es.rate[b2]; });
+  std::vector<double> r2, w2;
+  for (int i : idx) {
+    r2.push_back(es.rate[i]);
+    w2.push_back(es.weight[i]);
+  }
+  es.rate = r2;
+  es.weight = w2;
+  es.terms = static_cast<int>(es.rate.size());
+  // measure on every integer of the window
+  double worst = 0.0;
+  for (int64_t d = near + 1; d <= dmax; ++d) {
+    const double x = static_cast<double>(d);
+    double s = 0.0;
+    for (int k = 0; k < es.terms; ++k) s += es.weight[k] * std::exp(-es.rate[k] * x);
+    worst = std::max(worst, std::fabs(s * std::pow(x, alpha) - 1.0));
+  }
+  es.rel_err = worst;
+  (void)tol;
+  return es;
 }
 
 }  // namespace nlg

@@ -1,14 +1,567 @@
-// paper_1905_08375_b200/csrc/expsum.cu — fast method 2 (1-D fractional,
-// exponential-sum scans). Placeholder until the scan kernels land: the plan
-// runs the GPU direct quadrature (method 0).
+// paper_1905_08375_b200/csrc/expsum.cu — fast method 2: the 1-D fractional
+// operator (BASELINE cfg0/cfg1) by exponential-sum recurrence scans.
+//
+// Operator (Point rule, Difference form; reference semantics of
+// apply_full_dense, operators.cpp:236-260, with omega = C(x) kw |y-x|^-alpha):
+//   out_i = h sum_{0<|d|<=D_i^+-} C_i kw(i,i+d) |d h|^-alpha (u_{i+d} - u_i)
+// With w_d = |d|^-alpha and s_i = h^{1-alpha} C_i (x 1/2 when kappa-weighted):
+//   out_i = s_i [ kappa_i F[u]_i + F[kappa u]_i - u_i diag_i ]      (kappa)
+//   out_i = s_i [ F[u]_i - u_i diag_i ]                              (no kappa)
+//   F[f]_i = sum_{0<|d|<=D_i^+-} w_d f_{i+d}     (f = 0 outside the domain)
+// diag_i (u-independent) is summed exactly at plan time (collar: exterior
+// nodes enter diag with kappa_y := kappa_x). F splits into
+//   near |d| <= P : direct, shared-memory tile (es_near_combine)
+//   far  |d| >  P : w_d ~= sum_m c_m lambda_m^d (lambda_m = e^{-t_m}), so
+//     sum_{d=P+1}^{D} w_d f_{i+d} = sum_m c_m [lambda^{P+1} G_m(i+P+1) - lambda^{D+1} G_m(i+D+1)],
+//     G_m(j) = f_j + lambda_m G_m(j+1)  (suffix recurrence; the left side is
+//     the mirrored prefix recurrence).
+// The recurrences are linear scans: per 512-node warp segment the segment
+// aggregate (es_aggregate), a carry scan over segments (es_carry), then the
+// main pass (es_main) re-scans in registers (lanes own 16 nodes, warp-shuffle
+// scan across lanes) and accumulates the near-window term into its own
+// targets and scatters the far-window term of the slow exponentials to the
+// target whose horizon ends at this node (j = i + D_i + 1, one writer per
+// target).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "plan.hpp"
 
 namespace nlg {
 
-void expsum_setup(Plan& P) { P.fast_method = 0; }
-void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
-  launch_direct(P, u, out, nullptr, 0, nullptr, s);
+namespace {
+
+constexpr int kQ = 16;               // nodes per lane
+constexpr int kSegLen = 32 * kQ;     // nodes per warp segment
+constexpr int kNear = 32;            // P: offsets 1..P summed directly
+constexpr int kPowE = 32;            // |lambda exponent offsets| in the shared table
+constexpr int kMaxTerms = 64;
+constexpr int kWarpsPerCta = 4;
+
+// Packed per-term constants (device, read-only):
+struct TermTab {
+  const double* lam;      // lambda_m
+  const double* lam16;    // lambda^{16}, lambda^{32}, .. lambda^{256} : [5][M]
+  const double* cn;       // c_m lambda^{P+1}
+  const double* cw;       // c_m
+  const double* rate;     // t_m
+  const double* lam_inv;  // 1/lambda_m
+  const double* pw;       // [Mslow][2 kPowE + 1] lambda^e, e in [-kPowE, kPowE]
+  int M, Mslow;
+};
+
+struct PassArgs {
+  TermTab tt;
+  const double* u;       // input slab
+  const double* kappa;   // may be null
+  int field;             // 0: u, 1: kappa*u
+  int mirror;            // 0: right (suffix), 1: left (prefix, mirrored indexing)
+  int64_t n_in, n_out, o0;   // o0: input index of the first output target
+  int64_t q0;            // positions-space index of segment 0 (= o0' + P + 1)
+  int64_t nseg;
+  const int* tinfo;      // positions space: (tfirst << 2) | count, -1 none
+  const int* dtarget;    // D of each output target in this direction [n_out] (output order)
+  double* agg;           // [M][nseg]
+  double* carry;         // [M][nseg + 1]  G at segment starts, carry[nseg] = 0
+  double* facc;          // [n_out]  near-window exp-sum term (+=)
+  double* ffar;          // [n_out]  far-window exp-sum term (-=)
+};
+
+__device__ __forceinline__ int64_t to_input(const PassArgs& a, int64_t p) {
+  return a.mirror ? (a.n_in - 1 - p) : p;
 }
-void expsum_free(Plan&) {}
+
+__device__ __forceinline__ double field_at(const PassArgs& a, int64_t p) {
+  if (p < 0 || p >= a.n_in) return 0.0;
+  const int64_t x = to_input(a, p);
+  const double u = a.u[x];
+  return a.field == 0 ? u : u * a.kappa[x];
+}
+
+// warp suffix scan: S_l = a_l + L16 S_{l+1}, with the carry folded into lane 31
+__device__ __forceinline__ double warp_suffix_scan(double a, const double* lamp, int m, int M, int lane) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int off = 1 << k;
+    const double v = __shfl_down_sync(0xffffffffu, a, off);
+    if (lane + off < 32) a = fma(lamp[k * M + m], v, a);
+  }
+  return a;
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerCta) es_aggregate(PassArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t seg = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
+  if (seg >= a.nseg) return;
+  const int64_t p0 = a.q0 + seg * kSegLen + lane * kQ;
+  double f[kQ];
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) f[q] = field_at(a, p0 + q);
+  const int M = a.tt.M;
+  for (int m = 0; m < M; ++m) {
+    const double lam = a.tt.lam[m];
+    double s = f[kQ - 1];
+#pragma unroll
+    for (int q = kQ - 2; q >= 0; --q) s = fma(lam, s, f[q]);
+    s = warp_suffix_scan(s, a.tt.lam16, m, M, lane);
+    if (lane == 0) a.agg[m * a.nseg + seg] = s;
+  }
+}
+
+// One block per term: carry[s] = G(start of segment s) = agg[s] + L512 carry[s+1].
+__global__ void __launch_bounds__(1024) es_carry(PassArgs a, const double* lam512) {
+  const int m = blockIdx.x;
+  const int64_t ns = a.nseg;
+  const double L = lam512[m];
+  const double* ag = a.agg + m * ns;
+  double* cr = a.carry + m * (ns + 1);
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  const int64_t per = (ns + nt - 1) / nt;
+  const int64_t s0 = tid * per, s1 = min(ns, s0 + per);
+  // chunk as an affine map: G(start s0) = A + Mu * G(start s1)
+  double A = 0.0, Mu = 1.0;
+  for (int64_t s = s1 - 1; s >= s0; --s) {
+    A = fma(L, A, ag[s]);
+    Mu *= L;
+  }
+  // block suffix scan of affine maps (Kogge-Stone through shared memory)
+  __shared__ double sA[1024], sM[1024];
+  sA[tid] = A;
+  sM[tid] = Mu;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    double nA = sA[tid], nM = sM[tid];
+    if (tid + off < nt) {
+      const double rA = sA[tid + off], rM = sM[tid + off];
+      nA = fma(nM, rA, nA);
+      nM = nM * rM;
+    }
+    __syncthreads();
+    sA[tid] = nA;
+    sM[tid] = nM;
+    __syncthreads();
+  }
+  // G at the end of my chunk = A of the next thread's composed suffix map (G beyond = 0)
+  double g = (tid + 1 < nt) ? sA[tid + 1] : 0.0;
+  if (s0 < s1) {
+    if (s1 == ns) g = 0.0;
+    cr[s1] = g;
+    for (int64_t s = s1 - 1; s >= s0; --s) {
+      g = fma(L, g, ag[s]);
+      cr[s] = g;
+    }
+  }
+  if (tid == 0 && ns == 0) cr[0] = 0.0;
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerCta) es_main(PassArgs a) {
+  const int M = a.tt.M, Ms = a.tt.Mslow;
+  extern __shared__ double pw[];  // [Ms][2 kPowE + 1]
+  for (int i = threadIdx.x; i < Ms * (2 * kPowE + 1); i += blockDim.x) pw[i] = a.tt.pw[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t seg = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
+  const int64_t nsegT = (a.n_out + kSegLen - 1) / kSegLen;
+  if (seg >= nsegT) return;
+  const int64_t p0 = a.q0 + seg * kSegLen + lane * kQ;       // my first position
+  const int64_t t0 = p0 - (kNear + 1);                       // my first target (positions space)
+  double f[kQ], acc[kQ], fa[kQ], fb[kQ];
+  int e[kQ], cnt[kQ], tf[kQ];
+  bool tvalid[kQ];
+  int base = 0x7fffffff;
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    const int64_t p = p0 + q;
+    f[q] = field_at(a, p);
+    acc[q] = 0.0;
+    fa[q] = 0.0;
+    fb[q] = 0.0;
+    const int ti = (p < a.n_in) ? a.tinfo[p] : -1;
+    cnt[q] = ti < 0 ? 0 : (ti & 3);
+    tf[q] = ti < 0 ? 0 : (ti >> 2);
+    // positions-space target index t -> lambda exponent p - t
+    const int dlt = static_cast<int>(p - tf[q]);
+    e[q] = dlt;
+    if (cnt[q] > 0 && dlt < base) base = dlt;
+    // my own near-window target t0 + q
+    const int64_t t = t0 + q;
+    const int64_t tin = to_input(a, t);
+    const int64_t oi = tin - a.o0;
+    tvalid[q] = t >= 0 && oi >= 0 && oi < a.n_out && a.dtarget[oi] > kNear;
+  }
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) e[q] -= base;
+  for (int m = 0; m < M; ++m) {
+    const double lam = a.tt.lam[m];
+    const double cg = a.carry[m * (a.nseg + 1) + seg + 1];  // G at my warp segment's end
+    double s = f[kQ - 1];
+#pragma unroll
+    for (int q = kQ - 2; q >= 0; --q) s = fma(lam, s, f[q]);
+    if (lane == 31) s = fma(a.tt.lam16[m], cg, s);  // fold the segment carry into the last lane
+    s = warp_suffix_scan(s, a.tt.lam16, m, M, lane);
+    double g = __shfl_down_sync(0xffffffffu, s, 1);
+    if (lane == 31) g = cg;
+    const double cn = a.tt.cn[m];
+    if (m < Ms) {
+      // far-window coefficient base: c_m lambda^{base}
+      const double bm = (base == 0x7fffffff) ? 0.0 : a.tt.cw[m] * exp(-a.tt.rate[m] * static_cast<double>(base));
+      const double linv = a.tt.lam_inv[m];
+      const double* pwm = pw + m * (2 * kPowE + 1) + kPowE;
+#pragma unroll
+      for (int q = kQ - 1; q >= 0; --q) {
+        g = fma(lam, g, f[q]);
+        acc[q] = fma(cn, g, acc[q]);
+        if (cnt[q] > 0) {
+          const int ee = e[q];
+          const double pe = (ee >= -kPowE && ee <= kPowE) ? pwm[ee] : exp(-a.tt.rate[m] * ee);
+          const double ca = bm * pe;
+          fa[q] = fma(ca, g, fa[q]);
+          if (cnt[q] > 1) fb[q] = fma(ca * linv, g, fb[q]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = kQ - 1; q >= 0; --q) {
+        g = fma(lam, g, f[q]);
+        acc[q] = fma(cn, g, acc[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    if (tvalid[q]) {
+      const int64_t oi = to_input(a, t0 + q) - a.o0;
+      a.facc[oi] += acc[q];
+    }
+    if (cnt[q] > 0) {
+      const int64_t oa = to_input(a, tf[q]) - a.o0;
+      a.ffar[oa] -= fa[q];
+      if (cnt[q] > 1) {
+        const int64_t ob = to_input(a, tf[q] + 1) - a.o0;
+        a.ffar[ob] -= fb[q];
+      }
+    }
+  }
+}
+
+struct CombineArgs {
+  const double* u;
+  const double* kappa;
+  int64_t n_in, n_out, o0;
+  const int* dplus;
+  const int* dminus;
+  const double* wnear;   // w_1..w_P at [1..P]
+  const double* scale;   // s_i
+  const double* diag;
+  const double* facc;    // [fields][n_out]
+  const double* ffar;
+  double* out;
+};
+
+constexpr int kCombineThreads = 256;
+
+__global__ void __launch_bounds__(kCombineThreads) es_near_combine(CombineArgs a) {
+  __shared__ double su[kCombineThreads + 2 * kNear];
+  __shared__ double sk[kCombineThreads + 2 * kNear];
+  __shared__ double sw[kNear + 1];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kCombineThreads;
+  const int tid = threadIdx.x;
+  const bool kw = a.kappa != nullptr;
+  for (int k = tid; k < kCombineThreads + 2 * kNear; k += kCombineThreads) {
+    const int64_t x = a.o0 + i0 - kNear + k;
+    const bool in = x >= 0 && x < a.n_in;
+    const double uu = in ? a.u[x] : 0.0;
+    su[k] = uu;
+    if (kw) sk[k] = in ? uu * a.kappa[x] : 0.0;
+  }
+  if (tid <= kNear) sw[tid] = a.wnear[tid];
+  __syncthreads();
+  const int64_t i = i0 + tid;
+  if (i >= a.n_out) return;
+  const int dp = min(a.dplus[i], kNear), dm = min(a.dminus[i], kNear);
+  double nu = 0.0, nk = 0.0;
+  const int c = tid + kNear;
+  for (int d = 1; d <= dp; ++d) {
+    nu = fma(sw[d], su[c + d], nu);
+    if (kw) nk = fma(sw[d], sk[c + d], nk);
+  }
+  for (int d = 1; d <= dm; ++d) {
+    nu = fma(sw[d], su[c - d], nu);
+    if (kw) nk = fma(sw[d], sk[c - d], nk);
+  }
+  const double ui = su[c];
+  double r;
+  if (kw) {
+    const double ki = a.kappa[a.o0 + i];
+    const double fu = nu + a.facc[i] + a.ffar[i];
+    const double fk = nk + a.facc[a.n_out + i] + a.ffar[a.n_out + i];
+    r = a.scale[i] * (fma(ki, fu, fk) - ui * a.diag[i]);
+  } else {
+    const double fu = nu + a.facc[i] + a.ffar[i];
+    r = a.scale[i] * (fu - ui * a.diag[i]);
+  }
+  a.out[i] = r;
+}
+
+// Plan-time exact diagonal: sum_{0<|d|<=D^+-, in domain or collar} w_d (kappa_i + kappa_{i+d})
+// (kappa case, exterior kappa := kappa_i) or sum w_d (no kappa).
+__global__ void es_diag(const double* kappa, const double* wtab, const int* dplus, const int* dminus,
+                        int64_t n_in, int64_t n_out, int64_t o0, int collar, double* diag) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_out) return;
+  const int64_t x = o0 + i;
+  const double ki = kappa ? kappa[x] : 0.0;
+  double s = 0.0;
+  for (int side = 0; side < 2; ++side) {
+    const int D = side ? dminus[i] : dplus[i];
+    for (int d = 1; d <= D; ++d) {
+      const int64_t y = side ? x - d : x + d;
+      const bool in = y >= 0 && y < n_in;
+      if (!in && !collar) break;
+      const double w = wtab[d];
+      s += kappa ? w * (ki + (in ? kappa[y] : ki)) : w;
+    }
+  }
+  diag[i] = s;
+}
+
+template <typename T>
+T* upload(const std::vector<T>& v) {
+  T* d = nullptr;
+  NLG_CUDA(cudaMalloc(&d, sizeof(T) * std::max<size_t>(v.size(), 1)));
+  if (!v.empty()) NLG_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return d;
+}
+
+}  // namespace
+
+// Device-side state of the exponential-sum plan (declared in plan.hpp).
+struct ExpSumState {
+  int M = 0, Mslow = 0;
+  double *lam = nullptr, *lamp = nullptr, *cn = nullptr, *cw = nullptr, *rate = nullptr,
+         *lam_inv = nullptr, *pw = nullptr, *lam512 = nullptr;
+  int *dplus = nullptr, *dminus = nullptr, *tinfoR = nullptr, *tinfoL = nullptr;
+  double *wnear = nullptr, *scale = nullptr, *diag = nullptr;
+  double *agg = nullptr, *carry = nullptr, *facc = nullptr, *ffar = nullptr;
+  int64_t nsegR = 0, nsegL = 0, o0R = 0, o0L = 0;
+  int fields = 1;
+  double* kappa_dev = nullptr;
+};
+
+namespace {
+
+// exact per-node horizon extents D^+- (Point rule dist < delta with the
+// reference's operation order, operators.cpp:71-78, geometry.cpp:78-84)
+int64_t extent(int64_t g, int dir, double delta, double h, int64_t cap) {
+  const double x = (static_cast<double>(g) + 0.5) * h;
+  auto in = [&](int64_t d) {
+    const double y = (static_cast<double>(g + dir * d) + 0.5) * h;
+    const double dd = y - x;
+    return std::sqrt(dd * dd) < delta;
+  };
+  int64_t e = std::min<int64_t>(static_cast<int64_t>(std::floor(delta / h)) + 1, cap);
+  while (e > 0 && !in(e)) --e;
+  while (e < cap && in(e + 1)) ++e;
+  return e;
+}
+
+// positions -> targets map for one direction; returns false if some node
+// would own more than two targets or the map is not monotone.
+bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirror, std::vector<int>& tinfo) {
+  tinfo.assign(static_cast<size_t>(n_in), -1);
+  const int64_t n_out = static_cast<int64_t>(D.size());
+  int64_t last_p = -1;
+  for (int64_t k = 0; k < n_out; ++k) {
+    // walk targets in positions-space order
+    const int64_t oi = mirror ? (n_out - 1 - k) : k;
+    if (D[oi] <= kNear) continue;
+    const int64_t tin = o0 + oi;
+    const int64_t t = mirror ? (n_in - 1 - tin) : tin;
+    const int64_t p = t + D[oi] + 1;
+    if (p < last_p) return false;
+    last_p = p;
+    if (p >= n_in) continue;  // beyond the slab: contributes nothing
+    int& slot = tinfo[p];
+    if (slot < 0) {
+      if (t >= (int64_t(1) << 29)) return false;
+      slot = static_cast<int>(t << 2) | 1;
+    } else {
+      const int c = slot & 3;
+      if (c >= 2 || (slot >> 2) + c != t) return false;
+      slot += 1;
+    }
+  }
+  return true;
+}
+
+}  // namespace
+
+void expsum_setup_impl(Plan& P, const nlg_desc& d) {
+  const Geom& g = P.geom;
+  const double h = g.h;
+  const int64_t n_in = P.n_in, n_out = P.n_out, o0 = P.halo_lo;
+  // horizon extents per output target
+  std::vector<int> dplus(n_out), dminus(n_out);
+  int64_t dmax = 0;
+  for (int64_t i = 0; i < n_out; ++i) {
+    const int64_t x = o0 + i;
+    const double delta = d.delta ? d.delta[x] : d.delta0;
+    const int64_t gi = g.in_begin + x;
+    dplus[i] = static_cast<int>(extent(gi, +1, delta, h, 1 << 30));
+    dminus[i] = static_cast<int>(extent(gi, -1, delta, h, 1 << 30));
+    dmax = std::max<int64_t>(dmax, std::max(dplus[i], dminus[i]));
+  }
+  // the scan path pays off only for wide horizons
+  if (dmax < 8 * kNear) return;
+  ExpSum es = fit_exponential_sum(d.alpha, kNear, dmax, 1e-11);
+  if (es.terms == 0 || es.terms > kMaxTerms || es.rel_err > 1e-11) return;
+  std::vector<int> tR, tL;
+  if (!build_tinfo(dplus, n_in, o0, false, tR) || !build_tinfo(dminus, n_in, o0, true, tL)) return;
+
+  auto* S = new ExpSumState();
+  P.es_state = S;
+  P.es = es;
+  const int M = es.terms;
+  int64_t dmin = dmax;
+  for (int64_t i = 0; i < n_out; ++i) dmin = std::min<int64_t>(dmin, std::min(dplus[i], dminus[i]));
+  int Ms = 0;
+  for (int m = 0; m < M; ++m)
+    if (es.rate[m] * static_cast<double>(std::max<int64_t>(dmin, kNear + 1) + 1) <= 40.0) Ms = m + 1;
+  S->M = M;
+  S->Mslow = Ms;
+  std::vector<double> lam(M), lamp(5 * M), cn(M), linv(M), l512(M);
+  for (int m = 0; m < M; ++m) {
+    const double t = es.rate[m];
+    lam[m] = std::exp(-t);
+    for (int k = 0; k < 5; ++k) lamp[k * M + m] = std::exp(-t * kQ * double(1 << k));
+    cn[m] = es.weight[m] * std::exp(-t * (kNear + 1));
+    linv[m] = std::exp(t);
+    l512[m] = std::exp(-t * kSegLen);
+  }
+  std::vector<double> pw(static_cast<size_t>(std::max(Ms, 1)) * (2 * kPowE + 1));
+  for (int m = 0; m < Ms; ++m)
+    for (int e = -kPowE; e <= kPowE; ++e) pw[m * (2 * kPowE + 1) + e + kPowE] = std::exp(-es.rate[m] * e);
+  S->lam = upload(lam);
+  S->lamp = upload(lamp);
+  S->cn = upload(cn);
+  S->cw = upload(es.weight);
+  S->rate = upload(es.rate);
+  S->lam_inv = upload(linv);
+  S->lam512 = upload(l512);
+  S->pw = upload(pw);
+  S->dplus = upload(dplus);
+  S->dminus = upload(dminus);
+  S->tinfoR = upload(tR);
+  S->tinfoL = upload(tL);
+  // weights |d|^-alpha, d = 0..dmax (w_0 unused)
+  std::vector<double> wt(static_cast<size_t>(dmax) + 1, 0.0);
+  for (int64_t k = 1; k <= dmax; ++k) wt[k] = std::pow(static_cast<double>(k), -d.alpha);
+  std::vector<double> wn(wt.begin(), wt.begin() + std::min<int64_t>(dmax, kNear) + 1);
+  wn.resize(kNear + 1, 0.0);
+  S->wnear = upload(wn);
+  double* wtab = upload(wt);
+  // scale s_i = h^{1-alpha} C_i (x 1/2 with kappa)
+  const double hs = std::pow(h, 1.0 - d.alpha);
+  std::vector<double> sc(n_out);
+  for (int64_t i = 0; i < n_out; ++i) {
+    const double c = d.coeff ? d.coeff[o0 + i] : d.coeff0;
+    sc[i] = (d.kappa ? 0.5 : 1.0) * hs * c;
+  }
+  S->scale = upload(sc);
+  S->fields = d.kappa ? 2 : 1;
+  S->kappa_dev = P.d_kappa;
+  NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * n_out));
+  es_diag<<<static_cast<unsigned>((n_out + 255) / 256), 256, 0, P.stream>>>(
+      P.d_kappa, wtab, S->dplus, S->dminus, n_in, n_out, o0, P.exterior == 1, S->diag);
+  NLG_CUDA(cudaGetLastError());
+  NLG_CUDA(cudaStreamSynchronize(P.stream));
+  cudaFree(wtab);
+  // scan geometry per direction (positions space)
+  const int64_t o0R = o0, o0L = n_in - o0 - n_out;
+  const int64_t nsegT = (n_out + kSegLen - 1) / kSegLen;
+  auto nseg_of = [&](int64_t oo) {
+    const int64_t q0 = oo + kNear + 1;
+    const int64_t span = std::max<int64_t>(n_in - q0, 0);
+    return std::max<int64_t>((span + kSegLen - 1) / kSegLen, nsegT);
+  };
+  S->o0R = o0R;
+  S->o0L = o0L;
+  S->nsegR = nseg_of(o0R);
+  S->nsegL = nseg_of(o0L);
+  const int64_t ns = std::max(S->nsegR, S->nsegL);
+  NLG_CUDA(cudaMalloc(&S->agg, sizeof(double) * M * ns));
+  NLG_CUDA(cudaMalloc(&S->carry, sizeof(double) * M * (ns + 1)));
+  NLG_CUDA(cudaMalloc(&S->facc, sizeof(double) * S->fields * n_out));
+  NLG_CUDA(cudaMalloc(&S->ffar, sizeof(double) * S->fields * n_out));
+  P.fast_method = 2;
+}
+
+void expsum_setup(Plan& P, const nlg_desc& d) {
+  P.fast_method = 0;
+  expsum_setup_impl(P, d);
+}
+
+void expsum_free(Plan& P) {
+  ExpSumState* S = P.es_state;
+  if (!S) return;
+  for (double* p : {S->lam, S->lamp, S->cn, S->cw, S->rate, S->lam_inv, S->pw, S->lam512, S->wnear,
+                    S->scale, S->diag, S->agg, S->carry, S->facc, S->ffar})
+    cudaFree(p);
+  for (int* p : {S->dplus, S->dminus, S->tinfoR, S->tinfoL}) cudaFree(p);
+  delete S;
+  P.es_state = nullptr;
+}
+
+void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
+  ExpSumState* S = P.es_state;
+  const int64_t n_out = P.n_out;
+  NLG_CUDA(cudaMemsetAsync(S->facc, 0, sizeof(double) * S->fields * n_out, s));
+  NLG_CUDA(cudaMemsetAsync(S->ffar, 0, sizeof(double) * S->fields * n_out, s));
+  TermTab tt{S->lam, S->lamp, S->cn, S->cw, S->rate, S->lam_inv, S->pw, S->M, S->Mslow};
+  const int64_t nsegT = (n_out + kSegLen - 1) / kSegLen;
+  const size_t pw_bytes = sizeof(double) * std::max(S->Mslow, 1) * (2 * kPowE + 1);
+  for (int field = 0; field < S->fields; ++field) {
+    for (int mirror = 0; mirror < 2; ++mirror) {
+      PassArgs a;
+      a.tt = tt;
+      a.u = u;
+      a.kappa = S->kappa_dev;
+      a.field = field;
+      a.mirror = mirror;
+      a.n_in = P.n_in;
+      a.n_out = n_out;
+      a.o0 = P.halo_lo;
+      const int64_t oo = mirror ? S->o0L : S->o0R;
+      a.q0 = oo + kNear + 1;
+      a.nseg = mirror ? S->nsegL : S->nsegR;
+      a.tinfo = mirror ? S->tinfoL : S->tinfoR;
+      a.dtarget = mirror ? S->dminus : S->dplus;
+      a.agg = S->agg;
+      a.carry = S->carry;
+      a.facc = S->facc + field * n_out;
+      a.ffar = S->ffar + field * n_out;
+      es_aggregate<<<static_cast<unsigned>((a.nseg + kWarpsPerCta - 1) / kWarpsPerCta), 32 * kWarpsPerCta, 0, s>>>(a);
+      es_carry<<<S->M, 1024, 0, s>>>(a, S->lam512);
+      es_main<<<static_cast<unsigned>((nsegT + kWarpsPerCta - 1) / kWarpsPerCta), 32 * kWarpsPerCta, pw_bytes, s>>>(a);
+    }
+  }
+  CombineArgs c;
+  c.u = u;
+  c.kappa = S->fields == 2 ? S->kappa_dev : nullptr;
+  c.n_in = P.n_in;
+  c.n_out = n_out;
+  c.o0 = P.halo_lo;
+  c.dplus = S->dplus;
+  c.dminus = S->dminus;
+  c.wnear = S->wnear;
+  c.scale = S->scale;
+  c.diag = S->diag;
+  c.facc = S->facc;
+  c.ffar = S->ffar;
+  c.out = out;
+  es_near_combine<<<static_cast<unsigned>((n_out + kCombineThreads - 1) / kCombineThreads), kCombineThreads, 0, s>>>(c);
+}
 
 }  // namespace nlg

@@ -193,8 +193,7 @@ nlg_status nlg_plan_create(const nlg_desc* desc, nlg_plan** out) {
       P.fast_method = 1;
       spans_setup(P);
     } else if (P.family == NLG_FRACTIONAL && g.dim == 1) {
-      P.fast_method = 2;
-      expsum_setup(P);
+      expsum_setup(P, d);
     } else {
       P.fast_method = 0;
     }
@@ -372,6 +371,22 @@ nlg_status nlg_split(int K, double c, double* poly, double* tail, int* ntail) {
     for (size_t j = 0; j < p.size(); ++j) poly[j] = p[j];
     for (size_t j = 0; j < t.size(); ++j) tail[j] = t[j];
     *ntail = static_cast<int>(t.size());
+  });
+}
+
+nlg_status nlg_expsum_fit(double alpha, int near, int64_t dmax, double* rate, double* weight,
+                          int* terms, double* rel_err) {
+  return guard([&] {
+    require(rate && weight && terms && rel_err, "null argument");
+    require(alpha > 0 && near >= 1 && dmax > near, "invalid exponential-sum window");
+    const ExpSum es = fit_exponential_sum(alpha, near, dmax, 0.0);
+    require(es.terms <= 64, "too many exponential terms", NLG_ERUNTIME);
+    for (int m = 0; m < es.terms; ++m) {
+      rate[m] = es.rate[m];
+      weight[m] = es.weight[m];
+    }
+    *terms = es.terms;
+    *rel_err = es.rel_err;
   });
 }
 

@@ -35,6 +35,8 @@ struct ExpSum {
   std::vector<double> weight; // c_m
 };
 
+struct ExpSumState;
+
 struct Plan {
   int family = 0, route = 0, rule = 0, form = 0, exterior = 0, divergence = 0;
   Profile prof{};
@@ -67,12 +69,7 @@ struct Plan {
 
   // fast method 2 (1-D exponential-sum scans)
   ExpSum es;
-  double* d_es = nullptr;        // packed device tables
-  double* d_diag = nullptr;      // u-independent far-field diagonal per output node
-  double* d_carry = nullptr;     // block carries [fields][dirs][M][nblocks]
-  double* d_agg = nullptr;
-  int64_t es_nblocks = 0;
-  int* d_dcells = nullptr;       // per input node: horizon offset D_i (cells)
+  ExpSumState* es_state = nullptr;
 
   int64_t last_pairs = 0;
   int64_t fast_applies = 0;
@@ -85,7 +82,7 @@ int direct_kind(const Plan& P);
 void spans_setup(Plan& P);
 void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void spans_free(Plan& P);
-void expsum_setup(Plan& P);
+void expsum_setup(Plan& P, const nlg_desc& d);
 void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void expsum_free(Plan& P);
 
