@@ -257,7 +257,9 @@ struct CombineArgs {
   const double* diag;
   const double* facc;    // [fields][n_out]
   const double* ffar;
-  double* out;
+  const double* ext;     // mode 1: exact exterior (collar) part of diag, or null
+  double* out;           // mode 0: out; mode 1: diag
+  int mode;
 };
 
 constexpr int kCombineThreads = 256;
@@ -291,40 +293,23 @@ __global__ void __launch_bounds__(kCombineThreads) es_near_combine(CombineArgs a
     nu = fma(sw[d], su[c - d], nu);
     if (kw) nk = fma(sw[d], sk[c - d], nk);
   }
-  const double ui = su[c];
-  double r;
+  // X = kappa_i F[u] + F[kappa u]  (or F[u]); the plan-time pass (mode 1)
+  // evaluates the same expression with u = 1, so diag is consistent with the
+  // fast far field and constants are annihilated exactly (clip).
+  double X;
   if (kw) {
     const double ki = a.kappa[a.o0 + i];
     const double fu = nu + a.facc[i] + a.ffar[i];
     const double fk = nk + a.facc[a.n_out + i] + a.ffar[a.n_out + i];
-    r = a.scale[i] * (fma(ki, fu, fk) - ui * a.diag[i]);
+    X = fma(ki, fu, fk);
   } else {
-    const double fu = nu + a.facc[i] + a.ffar[i];
-    r = a.scale[i] * (fu - ui * a.diag[i]);
+    X = nu + a.facc[i] + a.ffar[i];
   }
-  a.out[i] = r;
-}
-
-// Plan-time exact diagonal: sum_{0<|d|<=D^+-, in domain or collar} w_d (kappa_i + kappa_{i+d})
-// (kappa case, exterior kappa := kappa_i) or sum w_d (no kappa).
-__global__ void es_diag(const double* kappa, const double* wtab, const int* dplus, const int* dminus,
-                        int64_t n_in, int64_t n_out, int64_t o0, int collar, double* diag) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n_out) return;
-  const int64_t x = o0 + i;
-  const double ki = kappa ? kappa[x] : 0.0;
-  double s = 0.0;
-  for (int side = 0; side < 2; ++side) {
-    const int D = side ? dminus[i] : dplus[i];
-    for (int d = 1; d <= D; ++d) {
-      const int64_t y = side ? x - d : x + d;
-      const bool in = y >= 0 && y < n_in;
-      if (!in && !collar) break;
-      const double w = wtab[d];
-      s += kappa ? w * (ki + (in ? kappa[y] : ki)) : w;
-    }
+  if (a.mode == 1) {
+    a.out[i] = a.ext ? X + a.ext[i] : X;
+  } else {
+    a.out[i] = a.scale[i] * (X - su[c] * a.diag[i]);
   }
-  diag[i] = s;
 }
 
 template <typename T>
@@ -398,6 +383,8 @@ bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirro
 
 }  // namespace
 
+void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode, const double* ext);
+
 void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   const Geom& g = P.geom;
   const double h = g.h;
@@ -414,7 +401,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
     dmax = std::max<int64_t>(dmax, std::max(dplus[i], dminus[i]));
   }
   // the scan path pays off only for wide horizons
-  if (dmax < 8 * kNear) return;
+  if (dmax < 4 * kNear) return;
   ExpSum es = fit_exponential_sum(d.alpha, kNear, dmax, 1e-11);
   if (es.terms == 0 || es.terms > kMaxTerms || es.rel_err > 1e-11) return;
   std::vector<int> tR, tL;
@@ -461,7 +448,6 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   std::vector<double> wn(wt.begin(), wt.begin() + std::min<int64_t>(dmax, kNear) + 1);
   wn.resize(kNear + 1, 0.0);
   S->wnear = upload(wn);
-  double* wtab = upload(wt);
   // scale s_i = h^{1-alpha} C_i (x 1/2 with kappa)
   const double hs = std::pow(h, 1.0 - d.alpha);
   std::vector<double> sc(n_out);
@@ -472,12 +458,6 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   S->scale = upload(sc);
   S->fields = d.kappa ? 2 : 1;
   S->kappa_dev = P.d_kappa;
-  NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * n_out));
-  es_diag<<<static_cast<unsigned>((n_out + 255) / 256), 256, 0, P.stream>>>(
-      P.d_kappa, wtab, S->dplus, S->dminus, n_in, n_out, o0, P.exterior == 1, S->diag);
-  NLG_CUDA(cudaGetLastError());
-  NLG_CUDA(cudaStreamSynchronize(P.stream));
-  cudaFree(wtab);
   // scan geometry per direction (positions space)
   const int64_t o0R = o0, o0L = n_in - o0 - n_out;
   const int64_t nsegT = (n_out + kSegLen - 1) / kSegLen;
@@ -495,6 +475,38 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   NLG_CUDA(cudaMalloc(&S->carry, sizeof(double) * M * (ns + 1)));
   NLG_CUDA(cudaMalloc(&S->facc, sizeof(double) * S->fields * n_out));
   NLG_CUDA(cudaMalloc(&S->ffar, sizeof(double) * S->fields * n_out));
+  NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * n_out));
+  // exterior (zero collar) part of diag, exact: sum_{d > edge distance} w_d,
+  // times (kappa_i + kappa_i) when kappa-weighted (kappa_y := kappa_x outside)
+  double* ext_dev = nullptr;
+  if (P.exterior == 1) {
+    std::vector<double> W(static_cast<size_t>(dmax) + 1, 0.0);  // W[D] = sum_{d=1..D} w_d
+    for (int64_t k = 1; k <= dmax; ++k) W[k] = W[k - 1] + wt[k];
+    std::vector<double> ext(n_out, 0.0);
+    const int64_t N = g.n;
+    for (int64_t i = 0; i < n_out; ++i) {
+      const int64_t gi = g.in_begin + o0 + i;
+      double e = 0.0;
+      const int64_t room_r = N - 1 - gi, room_l = gi;   // in-domain offsets available
+      if (dplus[i] > room_r) e += W[dplus[i]] - W[room_r];
+      if (dminus[i] > room_l) e += W[dminus[i]] - W[room_l];
+      const double ki = d.kappa ? d.kappa[o0 + i] : 1.0;
+      ext[i] = d.kappa ? e * (ki + ki) : e;
+    }
+    ext_dev = upload(ext);
+  }
+  // diag = the fast operator's own X for u = 1 (consistent far field) + exterior
+  double* ones = nullptr;
+  NLG_CUDA(cudaMalloc(&ones, sizeof(double) * n_in));
+  {
+    std::vector<double> o(static_cast<size_t>(n_in), 1.0);
+    NLG_CUDA(cudaMemcpy(ones, o.data(), sizeof(double) * n_in, cudaMemcpyHostToDevice));
+  }
+  P.fast_method = 2;
+  expsum_run(P, ones, S->diag, P.stream, 1, ext_dev);
+  NLG_CUDA(cudaStreamSynchronize(P.stream));
+  cudaFree(ones);
+  cudaFree(ext_dev);
   P.fast_method = 2;
 }
 
@@ -514,7 +526,7 @@ void expsum_free(Plan& P) {
   P.es_state = nullptr;
 }
 
-void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
+void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode, const double* ext) {
   ExpSumState* S = P.es_state;
   const int64_t n_out = P.n_out;
   NLG_CUDA(cudaMemsetAsync(S->facc, 0, sizeof(double) * S->fields * n_out, s));
@@ -560,8 +572,14 @@ void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   c.diag = S->diag;
   c.facc = S->facc;
   c.ffar = S->ffar;
+  c.ext = ext;
   c.out = out;
+  c.mode = mode;
   es_near_combine<<<static_cast<unsigned>((n_out + kCombineThreads - 1) / kCombineThreads), kCombineThreads, 0, s>>>(c);
+}
+
+void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
+  expsum_run(P, u, out, s, 0, nullptr);
 }
 
 }  // namespace nlg

@@ -21,7 +21,7 @@ def op_for(N, w, **kw):
     return N.NonlocalOperator(w.dim, w.n, **{**w.op_kwargs(), **kw})
 
 
-@pytest.mark.parametrize("n", [1 << 14, 1 << 16, 1 << 18])
+@pytest.mark.parametrize("n", [1 << 15, 1 << 16, 1 << 18])
 @pytest.mark.parametrize("exterior", [0, 1])
 def test_cfg1_family_fast_vs_direct(N, orc, n, exterior):
     from paper_1905_08375_b200 import configs
