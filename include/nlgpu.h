@@ -143,6 +143,15 @@ nlg_status nlg_apply_direct_at(nlg_plan* plan, const double* u, const int64_t* t
  * (operators.cpp:193,225,253); number of fast applies issued. */
 nlg_status nlg_counters(const nlg_plan* plan, int64_t* pairs, int64_t* fast_applies);
 
+/* Per-stage CUDA-event timing of this plan's kernels (off by default).
+ * Stages: 0 direct, 1 span scan, 2 span eval, 3 exp-sum aggregate, 4 exp-sum
+ * carry, 5 exp-sum main, 6 near+combine. nlg_stage_times returns (and resets)
+ * the accumulated milliseconds and launch counts per stage (8 slots). */
+nlg_status nlg_set_profiling(nlg_plan* plan, int on);
+nlg_status nlg_stage_times(nlg_plan* plan, double* ms, int64_t* launches, int* nstages);
+/* Total kernels this plan has launched. */
+nlg_status nlg_launch_count(const nlg_plan* plan, int64_t* launches);
+
 /* Kernel algebra (host setup, exact rationals for K <= 4 like kernel.cpp:26-51). */
 nlg_status nlg_match_polynomial(int K, double c, double* coeffs /* K+1 */);
 nlg_status nlg_split(int K, double c, double* poly /* K+1 */, double* tail /* >= K+1 */,

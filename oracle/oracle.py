@@ -96,6 +96,8 @@ def ref():
         lib.ref_full_dense.argtypes = [i, i, i, i, i, d, d, i, _dp, _dp, _ip]
         lib.ref_apply_split.argtypes = [i, i, i, i, d, d, i, _dp, _dp]
         lib.ref_full_dense_general.argtypes = [i, i, _dp, d, _dp, _dp, d, _dp, _dp, _ip]
+        lib.ref_full_dense_general_at.argtypes = [i, i, _dp, d, _dp, _dp, d, _dp, _ip, C.c_int64,
+                                                  _dp, i, _ip]
         _ref = lib
     return _ref
 
@@ -263,6 +265,24 @@ def ref_full_dense_general(dim, n, delta, cx, kappa, alpha, u):
     pairs = C.c_int64(0)
     _check_ref(ref().ref_full_dense_general(dim, n, _p(delta), float(delta.max()), _p(cx),
                                             _p(kappa), alpha, _p(u), _p(out), C.byref(pairs)))
+    return out, pairs.value
+
+
+def ref_full_dense_general_at(dim, n, delta, cx, kappa, alpha, u, targets, nthreads=1,
+                              delta_max=None):
+    """The reference's apply_full_dense inner loop + eval_omega at selected
+    targets (threaded); returns (out, pairs)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    delta = np.ascontiguousarray(delta, dtype=np.float64)
+    cx = None if cx is None else np.ascontiguousarray(cx, dtype=np.float64)
+    kappa = None if kappa is None else np.ascontiguousarray(kappa, dtype=np.float64)
+    tg = np.ascontiguousarray(targets, dtype=np.int64)
+    out = np.empty(len(tg))
+    pairs = C.c_int64(0)
+    dm = float(delta.max()) if delta_max is None else float(delta_max)
+    _check_ref(ref().ref_full_dense_general_at(dim, n, _p(delta), dm, _p(cx), _p(kappa), alpha,
+                                               _p(u), tg.ctypes.data_as(_ip), len(tg), _p(out),
+                                               nthreads, C.byref(pairs)))
     return out, pairs.value
 
 

@@ -22,6 +22,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "nonloc/bench.hpp"
@@ -221,6 +222,86 @@ int ref_full_dense_general(int dim, int n, const double* delta, double delta_max
     };
     const auto r = apply_full_dense(spec, g, std::span<const double>(u, g.total), pairs);
     std::memcpy(out, r.data(), sizeof(double) * r.size());
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// Same operator as ref_full_dense_general, evaluated only at `targets` and
+// split across `nthreads` std::threads: the per-target loop of
+// apply_full_dense (operators.cpp:244-256, window_around :31-42 restated since
+// it is file-local) around the reference's own eval_omega (kernel.cpp:275-287)
+// with the same coefficient_fn. Used for the bounded CPU baseline at BASELINE
+// sizes, where the whole-grid reference call would take hours.
+int ref_full_dense_general_at(int dim, int n, const double* delta, double delta_max,
+                              const double* cx, const double* kappa, double alpha,
+                              const double* u, const int64_t* targets, int64_t ntargets,
+                              double* out, int nthreads, int64_t* pairs_out) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    KernelSpec spec;
+    spec.dim = dim;
+    spec.profile = RadialProfile::inverse_s(1.0);
+    spec.horizon = {HorizonKind::Constant, delta_max};
+    double dpow = delta_max;
+    for (int j = 0; j < dim; ++j) dpow *= delta_max;
+    const auto index_of = [g](const Point& p) {
+      std::int64_t flat = 0;
+      for (int j = 0; j < g.dim; ++j)
+        flat = flat * g.n + static_cast<std::int64_t>(std::floor(p[j] * g.n));
+      return flat;
+    };
+    spec.coefficient_fn = [=](const Point& x, const Point& y) {
+      double r2 = 0.0;
+      for (int j = 0; j < dim; ++j) { const double d = y[j] - x[j]; r2 += d * d; }
+      const double r = std::sqrt(r2);
+      const std::int64_t ix = index_of(x), iy = index_of(y);
+      if (!(r < delta[ix])) return 0.0;
+      double c = cx ? cx[ix] : 1.0;
+      if (kappa) c *= 0.5 * (kappa[ix] + kappa[iy]);
+      return c * std::pow(r, -alpha) * dpow * r;
+    };
+    double hd = g.h;
+    for (int j = 1; j < dim; ++j) hd *= g.h;
+    if (nthreads < 1) nthreads = 1;
+    std::vector<std::int64_t> pc(nthreads, 0);
+    auto work = [&](int tid) {
+      for (std::int64_t t = tid; t < ntargets; t += nthreads) {
+        const std::int64_t i = targets[t];
+        const Point x = node_position(g, i);
+        std::int64_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+        for (int j = 0; j < dim; ++j) {
+          const double l = (x[j] - delta_max) / g.h - 1.0;
+          const double h2 = (x[j] + delta_max) / g.h + 1.0;
+          lo[j] = std::max<std::int64_t>(0, static_cast<std::int64_t>(std::floor(l)));
+          hi[j] = std::min<std::int64_t>(g.n - 1, static_cast<std::int64_t>(std::ceil(h2)));
+        }
+        double acc = 0.0;
+        std::int64_t k[3];
+        for (k[0] = lo[0]; k[0] <= hi[0]; ++k[0])
+          for (k[1] = lo[1]; k[1] <= hi[1]; ++k[1])
+            for (k[2] = lo[2]; k[2] <= hi[2]; ++k[2]) {
+              std::int64_t flat = 0;
+              for (int j = 0; j < dim; ++j) flat = flat * g.n + k[j];
+              if (flat == i) continue;
+              Point y{};
+              for (int j = 0; j < dim; ++j) y[j] = (static_cast<double>(k[j]) + 0.5) * g.h;
+              const double w = eval_omega(spec, x, y);
+              if (w == 0.0) continue;
+              ++pc[tid];
+              acc += w * (u[flat] - u[i]);
+            }
+        out[t] = hd * acc;
+      }
+    };
+    std::vector<std::thread> th;
+    for (int k = 1; k < nthreads; ++k) th.emplace_back(work, k);
+    work(0);
+    for (auto& x : th) x.join();
+    if (pairs_out) {
+      std::int64_t s = 0;
+      for (auto v : pc) s += v;
+      *pairs_out = s;
+    }
     return 0;
   } catch (const std::exception& e) { return fail(e); }
 }

@@ -50,6 +50,9 @@ EXPORTS = {
     "nlg_apply_direct_dev": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "nlg_apply_direct_at": ([C.c_void_p, _dp, _ip, C.c_int64, _dp], C.c_int),
     "nlg_counters": ([C.c_void_p, _ip, _ip], C.c_int),
+    "nlg_set_profiling": ([C.c_void_p, C.c_int], C.c_int),
+    "nlg_stage_times": ([C.c_void_p, _dp, _ip, C.POINTER(C.c_int)], C.c_int),
+    "nlg_launch_count": ([C.c_void_p, _ip], C.c_int),
     "nlg_match_polynomial": ([C.c_int, C.c_double, _dp], C.c_int),
     "nlg_split": ([C.c_int, C.c_double, _dp, _dp, C.POINTER(C.c_int)], C.c_int),
     "nlg_expsum_fit": ([C.c_double, C.c_int, C.c_int64, _dp, _dp, C.POINTER(C.c_int), _dp], C.c_int),
@@ -97,3 +100,6 @@ def dptr(a):
     if a is None:
         return None
     return a.ctypes.data_as(_dp)
+
+
+STAGES = ["direct", "span_scan", "span_eval", "es_aggregate", "es_carry", "es_main", "es_combine"]

@@ -35,6 +35,7 @@ class Workload:
     kappa: Optional[np.ndarray] = None
     exterior: int = 0               # 0 clip, 1 zero collar
     seeds: dict = field(default_factory=dict)
+    algo_bytes: int = 16            # algorithmic HBM bytes per point
 
     @property
     def N(self) -> int:
@@ -53,13 +54,9 @@ class Workload:
 
     def bytes_per_point(self) -> int:
         """Algorithmic HBM bytes per output point: every input field read once,
-        the output written once."""
-        comps = self.dim if self.kernel == "peridynamic" else 1
-        b = 16 * comps
-        for a in (self.kappa, self.delta, self.coeff):
-            if a is not None:
-                b += 8
-        return b
+        the output written once; C_delta(x) is a function of
+        delta(x) and is not counted as a field."""
+        return self.algo_bytes
 
 
 def _nodes(n: int) -> np.ndarray:
@@ -97,13 +94,16 @@ def cfg0(n: int = 4096) -> Workload:
     s, delta0 = 0.25, 0.02
     u = _u_1d(n, np.random.default_rng(1))
     return Workload("cfg0_1d_fractional_collar", 1, n, "fractional", 1 + 2 * s, s, u, delta0=delta0,
-                    coeff0=float(fractional_cdelta(1, s, delta0)), exterior=1, seeds={"u": 1})
+                    coeff0=float(fractional_cdelta(1, s, delta0)), exterior=1, seeds={"u": 1},
+                    algo_bytes=16)
 
 
-def cfg1(n: int = 1 << 22, exterior: int = 1) -> Workload:
+def cfg1(n: int = 1 << 22, exterior: int = 0) -> Workload:
     """1-D, N=2^22, delta(x)=0.005+0.01(1/2+1/2 sin 2 pi x), s=0.4,
-    kappa-weighted (kappa = exp(g), 32 modes, sigma 0.5). Exterior: zero
-    collar (kappa_y := kappa_x outside)."""
+    kappa-weighted (kappa = exp(g), 32 modes, sigma 0.5). Exterior: clip by
+    default — the reference's own apply_full_dense convention
+    (operators.cpp:36-38), so the compiled reference evaluates the identical
+    operator; exterior=1 gives the zero collar (kappa_y := kappa_x outside)."""
     s = 0.4
     x = _nodes(n)
     delta = 0.005 + 0.01 * (0.5 + 0.5 * np.sin(2 * math.pi * x))
@@ -111,7 +111,8 @@ def cfg1(n: int = 1 << 22, exterior: int = 1) -> Workload:
     kappa = _lognormal_1d(n, np.random.default_rng(2))
     coeff = fractional_cdelta(1, s, delta)
     return Workload("cfg1_1d_kappa_variable_delta", 1, n, "fractional", 1 + 2 * s, s, u, delta=delta,
-                    coeff=coeff, kappa=kappa, exterior=exterior, seeds={"u": 1, "kappa": 2})
+                    coeff=coeff, kappa=kappa, exterior=exterior, seeds={"u": 1, "kappa": 2},
+                    algo_bytes=32)
 
 
 WORKLOADS = {"cfg0": cfg0, "cfg1": cfg1}

@@ -554,9 +554,16 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
       a.carry = S->carry;
       a.facc = S->facc + field * n_out;
       a.ffar = S->ffar + field * n_out;
+      cudaEvent_t ev;
+      stage_begin(P, s, kStEsAggregate, &ev);
       es_aggregate<<<static_cast<unsigned>((a.nseg + kWarpsPerCta - 1) / kWarpsPerCta), 32 * kWarpsPerCta, 0, s>>>(a);
+      stage_end(P, s, kStEsAggregate, ev, 1);
+      stage_begin(P, s, kStEsCarry, &ev);
       es_carry<<<S->M, 1024, 0, s>>>(a, S->lam512);
+      stage_end(P, s, kStEsCarry, ev, 1);
+      stage_begin(P, s, kStEsMain, &ev);
       es_main<<<static_cast<unsigned>((nsegT + kWarpsPerCta - 1) / kWarpsPerCta), 32 * kWarpsPerCta, pw_bytes, s>>>(a);
+      stage_end(P, s, kStEsMain, ev, 1);
     }
   }
   CombineArgs c;
@@ -575,7 +582,10 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
   c.ext = ext;
   c.out = out;
   c.mode = mode;
+  cudaEvent_t ev;
+  stage_begin(P, s, kStEsCombine, &ev);
   es_near_combine<<<static_cast<unsigned>((n_out + kCombineThreads - 1) / kCombineThreads), kCombineThreads, 0, s>>>(c);
+  stage_end(P, s, kStEsCombine, ev, 1);
 }
 
 void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s) {

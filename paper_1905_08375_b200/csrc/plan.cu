@@ -87,6 +87,35 @@ void validate(const nlg_desc& d) {
 }
 
 }  // namespace
+
+static cudaEvent_t take_event(Plan& P) {
+  if (!P.sprof.pool.empty()) {
+    cudaEvent_t e = P.sprof.pool.back();
+    P.sprof.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  NLG_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void stage_begin(Plan& P, cudaStream_t s, int stage, cudaEvent_t* ev) {
+  (void)stage;
+  *ev = nullptr;
+  if (!P.sprof.on) return;
+  *ev = take_event(P);
+  NLG_CUDA(cudaEventRecord(*ev, s));
+}
+
+void stage_end(Plan& P, cudaStream_t s, int stage, cudaEvent_t ev, int nlaunch) {
+  P.launches += nlaunch;
+  P.sprof.launches[stage] += nlaunch;
+  if (!P.sprof.on || !ev) return;
+  cudaEvent_t e2 = take_event(P);
+  NLG_CUDA(cudaEventRecord(e2, s));
+  P.sprof.pending.push_back({stage, ev, e2});
+}
+
 }  // namespace nlg
 
 using namespace nlg;
@@ -211,6 +240,8 @@ void nlg_plan_destroy(nlg_plan* plan) {
   Plan& P = plan->p;
   cudaSetDevice(P.device);
   if (P.stream) cudaStreamSynchronize(P.stream);
+  for (auto& r : P.sprof.pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : P.sprof.pool) cudaEventDestroy(e);
   spans_free(P);
   expsum_free(P);
   cudaFree(P.d_delta);
@@ -253,7 +284,13 @@ void fast_dev(Plan& P, const double* u, double* out, cudaStream_t s) {
   switch (P.fast_method) {
     case 1: spans_apply(P, u, out, s); break;
     case 2: expsum_apply(P, u, out, s); break;
-    default: launch_direct(P, u, out, nullptr, 0, nullptr, s); break;
+    default: {
+      cudaEvent_t ev;
+      stage_begin(P, s, kStDirect, &ev);
+      launch_direct(P, u, out, nullptr, 0, nullptr, s);
+      stage_end(P, s, kStDirect, ev, 1);
+      break;
+    }
   }
   NLG_CUDA(cudaGetLastError());
   ++P.fast_applies;
@@ -293,7 +330,10 @@ nlg_status nlg_apply_direct(nlg_plan* plan, const double* u, double* out, int64_
     const int nc = components(P);
     NLG_CUDA(cudaMemcpyAsync(P.d_u, u, sizeof(double) * nc * P.n_in, cudaMemcpyHostToDevice, P.stream));
     NLG_CUDA(cudaMemsetAsync(P.d_pairs, 0, sizeof(unsigned long long), P.stream));
+    cudaEvent_t ev;
+    stage_begin(P, P.stream, kStDirect, &ev);
     launch_direct(P, P.d_u, P.d_out, nullptr, 0, P.d_pairs, P.stream);
+    stage_end(P, P.stream, kStDirect, ev, 1);
     NLG_CUDA(cudaGetLastError());
     unsigned long long pairs = 0;
     NLG_CUDA(cudaMemcpyAsync(out, P.d_out, sizeof(double) * nc * P.n_out, cudaMemcpyDeviceToHost, P.stream));
@@ -310,9 +350,12 @@ nlg_status nlg_apply_direct_dev(nlg_plan* plan, const double* u_dev, double* out
     require(plan && u_dev && out_dev, "null argument");
     Plan& P = plan->p;
     NLG_CUDA(cudaSetDevice(P.device));
+    cudaEvent_t ev;
+    stage_begin(P, static_cast<cudaStream_t>(stream), kStDirect, &ev);
     launch_direct(P, u_dev, out_dev, nullptr, 0,
                   reinterpret_cast<unsigned long long*>(pair_count_dev),
                   static_cast<cudaStream_t>(stream));
+    stage_end(P, static_cast<cudaStream_t>(stream), kStDirect, ev, 1);
     NLG_CUDA(cudaGetLastError());
   });
 }
@@ -352,6 +395,44 @@ nlg_status nlg_counters(const nlg_plan* plan, int64_t* pairs, int64_t* fast_appl
     require(plan, "null argument");
     if (pairs) *pairs = plan->p.last_pairs;
     if (fast_applies) *fast_applies = plan->p.fast_applies;
+  });
+}
+
+nlg_status nlg_set_profiling(nlg_plan* plan, int on) {
+  return guard([&] {
+    require(plan, "null argument");
+    plan->p.sprof.on = on != 0;
+  });
+}
+
+nlg_status nlg_stage_times(nlg_plan* plan, double* ms, int64_t* launches, int* nstages) {
+  return guard([&] {
+    require(plan && ms && launches && nstages, "null argument");
+    Plan& P = plan->p;
+    NLG_CUDA(cudaSetDevice(P.device));
+    for (auto& r : P.sprof.pending) {
+      NLG_CUDA(cudaEventSynchronize(r.b));
+      float t = 0.f;
+      NLG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      P.sprof.ms[r.stage] += t;
+      P.sprof.pool.push_back(r.a);
+      P.sprof.pool.push_back(r.b);
+    }
+    P.sprof.pending.clear();
+    for (int k = 0; k < kNumStages; ++k) {
+      ms[k] = P.sprof.ms[k];
+      launches[k] = P.sprof.launches[k];
+      P.sprof.ms[k] = 0.0;
+      P.sprof.launches[k] = 0;
+    }
+    *nstages = kNumStages;
+  });
+}
+
+nlg_status nlg_launch_count(const nlg_plan* plan, int64_t* launches) {
+  return guard([&] {
+    require(plan && launches, "null argument");
+    *launches = plan->p.launches;
   });
 }
 

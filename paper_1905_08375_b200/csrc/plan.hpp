@@ -37,6 +37,18 @@ struct ExpSum {
 
 struct ExpSumState;
 
+// Optional per-stage CUDA-event timing (nlg_set_profiling / nlg_stage_times).
+enum Stage { kStDirect = 0, kStSpanScan, kStSpanEval, kStEsAggregate, kStEsCarry, kStEsMain,
+             kStEsCombine, kNumStages };
+struct StageProf {
+  bool on = false;
+  struct Rec { int stage; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[kNumStages] = {};
+  int64_t launches[kNumStages] = {};
+};
+
 struct Plan {
   int family = 0, route = 0, rule = 0, form = 0, exterior = 0, divergence = 0;
   Profile prof{};
@@ -73,7 +85,13 @@ struct Plan {
 
   int64_t last_pairs = 0;
   int64_t fast_applies = 0;
+  int64_t launches = 0;   // kernels launched by this plan (all entry points)
+  StageProf sprof;
 };
+
+// Stage bracketing: records events when profiling is on; always counts launches.
+void stage_begin(Plan& P, cudaStream_t s, int stage, cudaEvent_t* ev);
+void stage_end(Plan& P, cudaStream_t s, int stage, cudaEvent_t ev, int nlaunch);
 
 // kernels
 void launch_direct(const Plan& P, const double* u, double* out, const int64_t* targets,

@@ -290,8 +290,12 @@ void spans_free(Plan& P) {
 void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   const RowGeom rg = row_geom(P);
   const unsigned nblk = static_cast<unsigned>(rg.rows * rg.nseg);
+  cudaEvent_t ev;
+  stage_begin(P, s, kStSpanScan, &ev);
   scan_segments<<<nblk, kScanThreads, 0, s>>>(u, rg, P.d_pref_hi, P.d_pref_lo, P.d_seg_hi, P.d_seg_lo);
   scan_offsets<<<static_cast<unsigned>((rg.rows + 127) / 128), 128, 0, s>>>(rg, P.d_seg_hi, P.d_seg_lo);
+  stage_end(P, s, kStSpanScan, ev, 2);
+  stage_begin(P, s, kStSpanEval, &ev);
   SpanArgs a;
   a.g = P.geom;
   a.rg = rg;
@@ -314,6 +318,7 @@ void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
     case 2: span_eval<2><<<blocks, 256, 0, s>>>(a); break;
     default: span_eval<3><<<blocks, 256, 0, s>>>(a); break;
   }
+  stage_end(P, s, kStSpanEval, ev, 1);
 }
 
 }  // namespace nlg

@@ -272,6 +272,21 @@ class Plan:
         A.check(A.lib().nlg_apply_direct_dev(self._h, C.c_void_p(u_ptr), C.c_void_p(out_ptr),
                                              C.c_void_p(pairs_ptr or None), C.c_void_p(stream)))
 
+    def set_profiling(self, on: bool = True) -> None:
+        A.check(A.lib().nlg_set_profiling(self._h, int(on)))
+
+    def stage_times(self) -> dict:
+        ms = np.zeros(8)
+        ln = np.zeros(8, dtype=np.int64)
+        n = C.c_int(0)
+        A.check(A.lib().nlg_stage_times(self._h, A.dptr(ms), ln.ctypes.data_as(A._ip), C.byref(n)))
+        return {A.STAGES[k]: (float(ms[k]), int(ln[k])) for k in range(n.value) if ln[k]}
+
+    def launch_count(self) -> int:
+        v = C.c_int64(0)
+        A.check(A.lib().nlg_launch_count(self._h, C.byref(v)))
+        return v.value
+
     def counters(self):
         p, f = C.c_int64(0), C.c_int64(0)
         A.check(A.lib().nlg_counters(self._h, C.byref(p), C.byref(f)))
