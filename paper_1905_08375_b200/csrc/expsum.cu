@@ -32,7 +32,7 @@ namespace nlg {
 
 namespace {
 
-constexpr int kQ = 16;               // nodes per lane
+constexpr int kQ = 8;                // nodes per lane
 constexpr int kSegLen = 32 * kQ;     // nodes per warp segment
 constexpr int kNear = 32;            // P: offsets 1..P summed directly
 constexpr int kPowE = 32;            // |lambda exponent offsets| in the shared table
@@ -42,7 +42,7 @@ constexpr int kWarpsPerCta = 4;
 // Packed per-term constants (device, read-only):
 struct TermTab {
   const double* lam;      // lambda_m
-  const double* lam16;    // lambda^{16}, lambda^{32}, .. lambda^{256} : [5][M]
+  const double* lam16;    // lambda^{kQ}, lambda^{2 kQ}, .. lambda^{16 kQ} : [5][M]
   const double* cn;       // c_m lambda^{P+1}
   const double* cw;       // c_m
   const double* rate;     // t_m
@@ -90,7 +90,45 @@ __device__ __forceinline__ double warp_suffix_scan(double a, const double* lamp,
   return a;
 }
 
+// Per-term constants staged in shared memory (broadcast reads in the loops).
+struct TermC {
+  double lam, cn, l16[5], cw, rate, linv;
+};
+
+__device__ __forceinline__ void load_terms(const PassArgs& a, TermC* tc) {
+  for (int m = threadIdx.x; m < a.tt.M; m += blockDim.x) {
+    TermC t;
+    t.lam = a.tt.lam[m];
+    t.cn = a.tt.cn[m];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) t.l16[k] = a.tt.lam16[k * a.tt.M + m];
+    t.cw = a.tt.cw[m];
+    t.rate = a.tt.rate[m];
+    t.linv = a.tt.lam_inv[m];
+    tc[m] = t;
+  }
+}
+
+// warp suffix scan of two independent terms (ILP 2)
+__device__ __forceinline__ void warp_suffix_scan2(double& a1, double& a2, const TermC* t1,
+                                                  const TermC* t2, int lane) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int off = 1 << k;
+    const double v1 = __shfl_down_sync(0xffffffffu, a1, off);
+    const double v2 = __shfl_down_sync(0xffffffffu, a2, off);
+    if (lane + off < 32) {
+      a1 = fma(t1->l16[k], v1, a1);
+      a2 = fma(t2->l16[k], v2, a2);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(32 * kWarpsPerCta) es_aggregate(PassArgs a) {
+  extern __shared__ double smem[];
+  TermC* tc = reinterpret_cast<TermC*>(smem);
+  load_terms(a, tc);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t seg = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
   if (seg >= a.nseg) return;
@@ -99,13 +137,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) es_aggregate(PassArgs a) {
 #pragma unroll
   for (int q = 0; q < kQ; ++q) f[q] = field_at(a, p0 + q);
   const int M = a.tt.M;
-  for (int m = 0; m < M; ++m) {
-    const double lam = a.tt.lam[m];
-    double s = f[kQ - 1];
+  for (int m = 0; m < M; m += 2) {
+    const int m2 = m + 1 < M ? m + 1 : m;
+    const TermC* t1 = tc + m;
+    const TermC* t2 = tc + m2;
+    const double l1 = t1->lam, l2 = t2->lam;
+    double s1 = f[kQ - 1], s2 = f[kQ - 1];
 #pragma unroll
-    for (int q = kQ - 2; q >= 0; --q) s = fma(lam, s, f[q]);
-    s = warp_suffix_scan(s, a.tt.lam16, m, M, lane);
-    if (lane == 0) a.agg[m * a.nseg + seg] = s;
+    for (int q = kQ - 2; q >= 0; --q) {
+      s1 = fma(l1, s1, f[q]);
+      s2 = fma(l2, s2, f[q]);
+    }
+    warp_suffix_scan2(s1, s2, t1, t2, lane);
+    if (lane == 0) {
+      a.agg[m * a.nseg + seg] = s1;
+      if (m2 != m) a.agg[m2 * a.nseg + seg] = s2;
+    }
   }
 }
 
@@ -156,91 +203,142 @@ __global__ void __launch_bounds__(1024) es_carry(PassArgs a, const double* lam51
   if (tid == 0 && ns == 0) cr[0] = 0.0;
 }
 
+// lambda^e for a small exponent offset e (targets per position drift slowly)
+__device__ __forceinline__ double lam_pow(double lam, int e) {
+  double p = 1.0;
+  for (int k = 0; k < e; ++k) p *= lam;   // e in [0, 15], almost always 0 or 1
+  return p;
+}
+
+// SLOW = false: the fast terms m in [Ms, M) (near-window term only);
+// SLOW = true : the slow terms m in [0, Ms) (near-window term + far scatter).
+template <bool SLOW>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) es_main(PassArgs a) {
   const int M = a.tt.M, Ms = a.tt.Mslow;
-  extern __shared__ double pw[];  // [Ms][2 kPowE + 1]
-  for (int i = threadIdx.x; i < Ms * (2 * kPowE + 1); i += blockDim.x) pw[i] = a.tt.pw[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t seg = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
+  const int mb = SLOW ? 0 : Ms, me = SLOW ? Ms : M;
+  extern __shared__ double smem[];
+  TermC* tc = reinterpret_cast<TermC*>(smem);
+  double* cs = smem + (sizeof(TermC) / sizeof(double)) * M;   // [warps][M] segment carries
+  load_terms(a, tc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t seg = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp;
   const int64_t nsegT = (a.n_out + kSegLen - 1) / kSegLen;
-  if (seg >= nsegT) return;
+  double* mycs = cs + warp * M;
+  if (seg < nsegT)
+    for (int m = lane; m < M; m += 32) mycs[m] = a.carry[m * (a.nseg + 1) + seg + 1];
+  __syncthreads();
+  if (seg >= nsegT || mb >= me) return;
   const int64_t p0 = a.q0 + seg * kSegLen + lane * kQ;       // my first position
   const int64_t t0 = p0 - (kNear + 1);                       // my first target (positions space)
-  double f[kQ], acc[kQ], fa[kQ], fb[kQ];
-  int e[kQ], cnt[kQ], tf[kQ];
-  bool tvalid[kQ];
+  double f[kQ], acc[kQ], fa[SLOW ? kQ : 1];
+  double fb = 0.0;   // the (at most one, checked at plan time) two-target node of this lane
+  unsigned cnt1 = 0, cnt2 = 0, tval = 0;  // bitmasks: >=1 target, 2 targets, own target valid
+  unsigned epk0 = 0;                      // far exponent offsets in [0, 15], nibbles
   int base = 0x7fffffff;
 #pragma unroll
   for (int q = 0; q < kQ; ++q) {
     const int64_t p = p0 + q;
     f[q] = field_at(a, p);
     acc[q] = 0.0;
-    fa[q] = 0.0;
-    fb[q] = 0.0;
-    const int ti = (p < a.n_in) ? a.tinfo[p] : -1;
-    cnt[q] = ti < 0 ? 0 : (ti & 3);
-    tf[q] = ti < 0 ? 0 : (ti >> 2);
-    // positions-space target index t -> lambda exponent p - t
-    const int dlt = static_cast<int>(p - tf[q]);
-    e[q] = dlt;
-    if (cnt[q] > 0 && dlt < base) base = dlt;
-    // my own near-window target t0 + q
+    if (SLOW) {
+      fa[q] = 0.0;
+      const int ti = (p < a.n_in) ? a.tinfo[p] : -1;
+      const int c = ti < 0 ? 0 : (ti & 3);
+      if (c >= 1) {
+        cnt1 |= 1u << q;
+        base = min(base, static_cast<int>(p - (ti >> 2)));
+      }
+      if (c >= 2) cnt2 |= 1u << q;
+    }
     const int64_t t = t0 + q;
-    const int64_t tin = to_input(a, t);
-    const int64_t oi = tin - a.o0;
-    tvalid[q] = t >= 0 && oi >= 0 && oi < a.n_out && a.dtarget[oi] > kNear;
+    const int64_t oi = to_input(a, t) - a.o0;
+    if (t >= 0 && oi >= 0 && oi < a.n_out && a.dtarget[oi] > kNear) tval |= 1u << q;
   }
+  if (SLOW) {
 #pragma unroll
-  for (int q = 0; q < kQ; ++q) e[q] -= base;
-  for (int m = 0; m < M; ++m) {
-    const double lam = a.tt.lam[m];
-    const double cg = a.carry[m * (a.nseg + 1) + seg + 1];  // G at my warp segment's end
-    double s = f[kQ - 1];
+    for (int q = 0; q < kQ; ++q) {
+      if (cnt1 & (1u << q)) {
+        const int64_t p = p0 + q;
+        const unsigned v = static_cast<unsigned>(min(max(static_cast<int>(p - (a.tinfo[p] >> 2)) - base, 0), 15));
+        epk0 |= v << (4 * q);
+      }
+    }
+  }
+  const bool any_far = SLOW && cnt1 != 0;
+  const int qd = cnt2 ? __ffs(cnt2) - 1 : -1;
+
+  for (int m = mb; m < me; m += 2) {
+    const int m2 = m + 1 < me ? m + 1 : m;
+    const double w2 = m2 != m ? 1.0 : 0.0;   // a lone last term is paired with itself, weight 0
+    const TermC* t1 = tc + m;
+    const TermC* t2 = tc + m2;
+    const double l1 = t1->lam, l2 = t2->lam;
+    const double cg1 = mycs[m], cg2 = mycs[m2];
+    double s1 = f[kQ - 1], s2 = f[kQ - 1];
 #pragma unroll
-    for (int q = kQ - 2; q >= 0; --q) s = fma(lam, s, f[q]);
-    if (lane == 31) s = fma(a.tt.lam16[m], cg, s);  // fold the segment carry into the last lane
-    s = warp_suffix_scan(s, a.tt.lam16, m, M, lane);
-    double g = __shfl_down_sync(0xffffffffu, s, 1);
-    if (lane == 31) g = cg;
-    const double cn = a.tt.cn[m];
-    if (m < Ms) {
-      // far-window coefficient base: c_m lambda^{base}
-      const double bm = (base == 0x7fffffff) ? 0.0 : a.tt.cw[m] * exp(-a.tt.rate[m] * static_cast<double>(base));
-      const double linv = a.tt.lam_inv[m];
-      const double* pwm = pw + m * (2 * kPowE + 1) + kPowE;
+    for (int q = kQ - 2; q >= 0; --q) {
+      s1 = fma(l1, s1, f[q]);
+      s2 = fma(l2, s2, f[q]);
+    }
+    if (lane == 31) {  // fold the segment carry into the last lane
+      s1 = fma(t1->l16[0], cg1, s1);
+      s2 = fma(t2->l16[0], cg2, s2);
+    }
+    warp_suffix_scan2(s1, s2, t1, t2, lane);
+    double g1 = __shfl_down_sync(0xffffffffu, s1, 1);
+    double g2 = __shfl_down_sync(0xffffffffu, s2, 1);
+    if (lane == 31) {
+      g1 = cg1;
+      g2 = cg2;
+    }
+    const double cn1 = t1->cn, cn2 = t2->cn * w2;
+    if (SLOW && any_far) {
+      // far-window coefficients c_m lambda^{p - t} = (c_m lambda^{base}) lambda^{e_q}
+      const double b1 = t1->cw * exp(-t1->rate * static_cast<double>(base));
+      const double b2 = w2 * t2->cw * exp(-t2->rate * static_cast<double>(base));
+      const double i1 = t1->linv, i2 = t2->linv;
 #pragma unroll
       for (int q = kQ - 1; q >= 0; --q) {
-        g = fma(lam, g, f[q]);
-        acc[q] = fma(cn, g, acc[q]);
-        if (cnt[q] > 0) {
-          const int ee = e[q];
-          const double pe = (ee >= -kPowE && ee <= kPowE) ? pwm[ee] : exp(-a.tt.rate[m] * ee);
-          const double ca = bm * pe;
-          fa[q] = fma(ca, g, fa[q]);
-          if (cnt[q] > 1) fb[q] = fma(ca * linv, g, fb[q]);
+        g1 = fma(l1, g1, f[q]);
+        g2 = fma(l2, g2, f[q]);
+        acc[q] = fma(cn1, g1, acc[q]);
+        acc[q] = fma(cn2, g2, acc[q]);
+        if (cnt1 & (1u << q)) {
+          const int eq = static_cast<int>((epk0 >> (4 * q)) & 15u);
+          const double c1 = b1 * lam_pow(l1, eq);
+          const double c2 = b2 * lam_pow(l2, eq);
+          fa[q] = fma(c1, g1, fa[q]);
+          fa[q] = fma(c2, g2, fa[q]);
+          if (q == qd) {
+            fb = fma(c1 * i1, g1, fb);
+            fb = fma(c2 * i2, g2, fb);
+          }
         }
       }
     } else {
 #pragma unroll
       for (int q = kQ - 1; q >= 0; --q) {
-        g = fma(lam, g, f[q]);
-        acc[q] = fma(cn, g, acc[q]);
+        g1 = fma(l1, g1, f[q]);
+        g2 = fma(l2, g2, f[q]);
+        acc[q] = fma(cn1, g1, acc[q]);
+        acc[q] = fma(cn2, g2, acc[q]);
       }
     }
   }
 #pragma unroll
   for (int q = 0; q < kQ; ++q) {
-    if (tvalid[q]) {
+    if (tval & (1u << q)) {
       const int64_t oi = to_input(a, t0 + q) - a.o0;
       a.facc[oi] += acc[q];
     }
-    if (cnt[q] > 0) {
-      const int64_t oa = to_input(a, tf[q]) - a.o0;
+    if (SLOW && (cnt1 & (1u << q))) {
+      const int64_t p = p0 + q;
+      const int tf = a.tinfo[p] >> 2;
+      const int64_t oa = to_input(a, tf) - a.o0;
       a.ffar[oa] -= fa[q];
-      if (cnt[q] > 1) {
-        const int64_t ob = to_input(a, tf[q] + 1) - a.o0;
-        a.ffar[ob] -= fb[q];
+      if (q == qd) {
+        const int64_t ob = to_input(a, tf + 1) - a.o0;
+        a.ffar[ob] -= fb;
       }
     }
   }
@@ -262,53 +360,99 @@ struct CombineArgs {
   int mode;
 };
 
-constexpr int kCombineThreads = 256;
+constexpr int kCombineThreads = 128;
+constexpr int kCR = 8;                                     // targets per thread
+constexpr int kCTile = kCombineThreads * kCR;              // targets per CTA
+constexpr int kCWin = kCTile + 2 * kNear;                  // source nodes per CTA
+__host__ __device__ constexpr int cpad(int i) { return i + i / 8; }    // conflict-free lanes
 
+// Near field (|d| <= P) by register blocking: a thread owns 16 consecutive
+// targets, streams the 16 + 2P sources once from shared memory and applies the
+// 64 weights from registers (compile-time tap indices), then combines with the
+// far-field arrays:  out = s_i (X - u_i diag_i),  X = kappa_i F[u] + F[kappa u].
+template <bool KW>
 __global__ void __launch_bounds__(kCombineThreads) es_near_combine(CombineArgs a) {
-  __shared__ double su[kCombineThreads + 2 * kNear];
-  __shared__ double sk[kCombineThreads + 2 * kNear];
-  __shared__ double sw[kNear + 1];
-  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kCombineThreads;
+  extern __shared__ double sx[];        // [2][cpad(kCWin)] : u, kappa*u
+  double* su = sx;
+  double* sk = sx + cpad(kCWin) + 1;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kCTile;
   const int tid = threadIdx.x;
-  const bool kw = a.kappa != nullptr;
-  for (int k = tid; k < kCombineThreads + 2 * kNear; k += kCombineThreads) {
+  for (int k = tid; k < kCWin; k += kCombineThreads) {
     const int64_t x = a.o0 + i0 - kNear + k;
     const bool in = x >= 0 && x < a.n_in;
     const double uu = in ? a.u[x] : 0.0;
-    su[k] = uu;
-    if (kw) sk[k] = in ? uu * a.kappa[x] : 0.0;
+    su[cpad(k)] = uu;
+    if (KW) sk[cpad(k)] = in ? uu * a.kappa[x] : 0.0;
   }
-  if (tid <= kNear) sw[tid] = a.wnear[tid];
   __syncthreads();
-  const int64_t i = i0 + tid;
-  if (i >= a.n_out) return;
-  const int dp = min(a.dplus[i], kNear), dm = min(a.dminus[i], kNear);
-  double nu = 0.0, nk = 0.0;
-  const int c = tid + kNear;
-  for (int d = 1; d <= dp; ++d) {
-    nu = fma(sw[d], su[c + d], nu);
-    if (kw) nk = fma(sw[d], sk[c + d], nk);
+  double w[kNear + 1];
+#pragma unroll
+  for (int d = 1; d <= kNear; ++d) w[d] = a.wnear[d];
+  const int64_t t0 = i0 + static_cast<int64_t>(tid) * kCR;    // my first target (output index)
+  if (t0 >= a.n_out) return;
+  const int base = tid * kCR;                                  // window index of target t0 - P
+  bool uniform = t0 + kCR <= a.n_out;
+  if (uniform)
+#pragma unroll
+    for (int j = 0; j < kCR; ++j) uniform = uniform && a.dplus[t0 + j] >= kNear && a.dminus[t0 + j] >= kNear;
+  double nu[kCR], nk[kCR];
+#pragma unroll
+  for (int j = 0; j < kCR; ++j) {
+    nu[j] = 0.0;
+    nk[j] = 0.0;
   }
-  for (int d = 1; d <= dm; ++d) {
-    nu = fma(sw[d], su[c - d], nu);
-    if (kw) nk = fma(sw[d], sk[c - d], nk);
-  }
-  // X = kappa_i F[u] + F[kappa u]  (or F[u]); the plan-time pass (mode 1)
-  // evaluates the same expression with u = 1, so diag is consistent with the
-  // fast far field and constants are annihilated exactly (clip).
-  double X;
-  if (kw) {
-    const double ki = a.kappa[a.o0 + i];
-    const double fu = nu + a.facc[i] + a.ffar[i];
-    const double fk = nk + a.facc[a.n_out + i] + a.ffar[a.n_out + i];
-    X = fma(ki, fu, fk);
+  if (uniform) {
+#pragma unroll
+    for (int r = 0; r < kCR + 2 * kNear; ++r) {      // source node t0 - P + r
+      const double xu = su[cpad(base + r)];
+      const double xk = KW ? sk[cpad(base + r)] : 0.0;
+#pragma unroll
+      for (int j = 0; j < kCR; ++j) {
+        const int d = r - kNear - j;                  // source offset from target j
+        if (d != 0 && d >= -kNear && d <= kNear) {
+          const double wd = w[d < 0 ? -d : d];
+          nu[j] = fma(wd, xu, nu[j]);
+          if (KW) nk[j] = fma(wd, xk, nk[j]);
+        }
+      }
+    }
   } else {
-    X = nu + a.facc[i] + a.ffar[i];
+#pragma unroll
+    for (int j = 0; j < kCR; ++j) {
+      if (t0 + j >= a.n_out) continue;
+      const int c = base + kNear + j;
+      const int dp = min(a.dplus[t0 + j], kNear), dm = min(a.dminus[t0 + j], kNear);
+      for (int d = 1; d <= dp; ++d) {
+        nu[j] = fma(a.wnear[d], su[cpad(c + d)], nu[j]);
+        if (KW) nk[j] = fma(a.wnear[d], sk[cpad(c + d)], nk[j]);
+      }
+      for (int d = 1; d <= dm; ++d) {
+        nu[j] = fma(a.wnear[d], su[cpad(c - d)], nu[j]);
+        if (KW) nk[j] = fma(a.wnear[d], sk[cpad(c - d)], nk[j]);
+      }
+    }
   }
-  if (a.mode == 1) {
-    a.out[i] = a.ext ? X + a.ext[i] : X;
-  } else {
-    a.out[i] = a.scale[i] * (X - su[c] * a.diag[i]);
+#pragma unroll
+  for (int j = 0; j < kCR; ++j) {
+    const int64_t i = t0 + j;
+    if (i >= a.n_out) continue;
+    // X = kappa_i F[u] + F[kappa u]  (or F[u]); the plan-time pass (mode 1)
+    // evaluates the same expression with u = 1, so diag is consistent with the
+    // fast far field and constants are annihilated exactly (clip).
+    double X;
+    if (KW) {
+      const double ki = a.kappa[a.o0 + i];
+      const double fu = nu[j] + a.facc[i] + a.ffar[i];
+      const double fk = nk[j] + a.facc[a.n_out + i] + a.ffar[a.n_out + i];
+      X = fma(ki, fu, fk);
+    } else {
+      X = nu[j] + a.facc[i] + a.ffar[i];
+    }
+    if (a.mode == 1) {
+      a.out[i] = a.ext ? X + a.ext[i] : X;
+    } else {
+      a.out[i] = a.scale[i] * (X - su[cpad(base + kNear + j)] * a.diag[i]);
+    }
   }
 }
 
@@ -354,7 +498,8 @@ int64_t extent(int64_t g, int dir, double delta, double h, int64_t cap) {
 
 // positions -> targets map for one direction; returns false if some node
 // would own more than two targets or the map is not monotone.
-bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirror, std::vector<int>& tinfo) {
+bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirror, std::vector<int>& tinfo,
+                 int64_t q0) {
   tinfo.assign(static_cast<size_t>(n_in), -1);
   const int64_t n_out = static_cast<int64_t>(D.size());
   int64_t last_p = -1;
@@ -377,6 +522,21 @@ bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirro
       if (c >= 2 || (slot >> 2) + c != t) return false;
       slot += 1;
     }
+  }
+  // es_main keeps one second-target accumulator per 16-node lane block
+  for (int64_t b = std::max<int64_t>(q0, 0); b < n_in; b += kQ) {
+    int doubles = 0;
+    for (int64_t p = b; p < std::min(n_in, b + kQ); ++p)
+      if (tinfo[p] >= 0 && (tinfo[p] & 3) == 2) ++doubles;
+    if (doubles > 1) return false;
+    int lo = 1 << 30, hi = -(1 << 30);
+    for (int64_t p = b; p < std::min(n_in, b + kQ); ++p)
+      if (tinfo[p] >= 0) {
+        const int dl = static_cast<int>(p - (tinfo[p] >> 2));
+        lo = std::min(lo, dl);
+        hi = std::max(hi, dl);
+      }
+    if (hi - lo > 15) return false;
   }
   return true;
 }
@@ -405,7 +565,9 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   ExpSum es = fit_exponential_sum(d.alpha, kNear, dmax, 1e-11);
   if (es.terms == 0 || es.terms > kMaxTerms || es.rel_err > 1e-11) return;
   std::vector<int> tR, tL;
-  if (!build_tinfo(dplus, n_in, o0, false, tR) || !build_tinfo(dminus, n_in, o0, true, tL)) return;
+  if (!build_tinfo(dplus, n_in, o0, false, tR, o0 + kNear + 1) ||
+      !build_tinfo(dminus, n_in, o0, true, tL, (n_in - o0 - n_out) + kNear + 1))
+    return;
 
   auto* S = new ExpSumState();
   P.es_state = S;
@@ -533,7 +695,8 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
   NLG_CUDA(cudaMemsetAsync(S->ffar, 0, sizeof(double) * S->fields * n_out, s));
   TermTab tt{S->lam, S->lamp, S->cn, S->cw, S->rate, S->lam_inv, S->pw, S->M, S->Mslow};
   const int64_t nsegT = (n_out + kSegLen - 1) / kSegLen;
-  const size_t pw_bytes = sizeof(double) * std::max(S->Mslow, 1) * (2 * kPowE + 1);
+  const size_t tc_bytes = sizeof(TermC) * S->M;
+  const size_t main_bytes = tc_bytes + sizeof(double) * kWarpsPerCta * S->M;
   for (int field = 0; field < S->fields; ++field) {
     for (int mirror = 0; mirror < 2; ++mirror) {
       PassArgs a;
@@ -556,14 +719,16 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
       a.ffar = S->ffar + field * n_out;
       cudaEvent_t ev;
       stage_begin(P, s, kStEsAggregate, &ev);
-      es_aggregate<<<static_cast<unsigned>((a.nseg + kWarpsPerCta - 1) / kWarpsPerCta), 32 * kWarpsPerCta, 0, s>>>(a);
+      es_aggregate<<<static_cast<unsigned>((a.nseg + kWarpsPerCta - 1) / kWarpsPerCta), 32 * kWarpsPerCta, tc_bytes, s>>>(a);
       stage_end(P, s, kStEsAggregate, ev, 1);
       stage_begin(P, s, kStEsCarry, &ev);
       es_carry<<<S->M, 1024, 0, s>>>(a, S->lam512);
       stage_end(P, s, kStEsCarry, ev, 1);
       stage_begin(P, s, kStEsMain, &ev);
-      es_main<<<static_cast<unsigned>((nsegT + kWarpsPerCta - 1) / kWarpsPerCta), 32 * kWarpsPerCta, pw_bytes, s>>>(a);
-      stage_end(P, s, kStEsMain, ev, 1);
+      const unsigned gm = static_cast<unsigned>((nsegT + kWarpsPerCta - 1) / kWarpsPerCta);
+      es_main<true><<<gm, 32 * kWarpsPerCta, main_bytes, s>>>(a);
+      es_main<false><<<gm, 32 * kWarpsPerCta, main_bytes, s>>>(a);
+      stage_end(P, s, kStEsMain, ev, 2);
     }
   }
   CombineArgs c;
@@ -584,7 +749,12 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
   c.mode = mode;
   cudaEvent_t ev;
   stage_begin(P, s, kStEsCombine, &ev);
-  es_near_combine<<<static_cast<unsigned>((n_out + kCombineThreads - 1) / kCombineThreads), kCombineThreads, 0, s>>>(c);
+  const unsigned gc = static_cast<unsigned>((n_out + kCTile - 1) / kCTile);
+  const size_t cbytes = sizeof(double) * 2 * (cpad(kCWin) + 1);
+  if (c.kappa)
+    es_near_combine<true><<<gc, kCombineThreads, cbytes, s>>>(c);
+  else
+    es_near_combine<false><<<gc, kCombineThreads, cbytes, s>>>(c);
   stage_end(P, s, kStEsCombine, ev, 1);
 }
 
