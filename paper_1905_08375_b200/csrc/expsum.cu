@@ -203,15 +203,14 @@ __global__ void __launch_bounds__(1024) es_carry(PassArgs a, const double* lam51
   if (tid == 0 && ns == 0) cr[0] = 0.0;
 }
 
-// lambda^e for a small exponent offset e (targets per position drift slowly)
-__device__ __forceinline__ double lam_pow(double lam, int e) {
-  double p = 1.0;
-  for (int k = 0; k < e; ++k) p *= lam;   // e in [0, 15], almost always 0 or 1
-  return p;
-}
-
 // SLOW = false: the fast terms m in [Ms, M) (near-window term only);
 // SLOW = true : the slow terms m in [0, Ms) (near-window term + far scatter).
+// Far scatter: target t (horizon end p = t + D_t + 1) needs
+//   sum_m c_m lambda_m^{p - t} G_m(p) = sum_m (c_m lambda_m^{base}) lambda_m^{e} G_m(p),
+// with base = the lane's smallest p - t and e in {0, 1} (checked at plan time:
+// horizons change by at most one cell across a lane block). Two accumulators
+// A0 (e = 0) and A1 (e = 1) per node cover both cases and the second target of a
+// two-target node (exponent e - 1).
 template <bool SLOW>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) es_main(PassArgs a) {
   const int M = a.tt.M, Ms = a.tt.Mslow;
@@ -230,10 +229,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) es_main(PassArgs a) {
   if (seg >= nsegT || mb >= me) return;
   const int64_t p0 = a.q0 + seg * kSegLen + lane * kQ;       // my first position
   const int64_t t0 = p0 - (kNear + 1);                       // my first target (positions space)
-  double f[kQ], acc[kQ], fa[SLOW ? kQ : 1];
-  double fb = 0.0;   // the (at most one, checked at plan time) two-target node of this lane
-  unsigned cnt1 = 0, cnt2 = 0, tval = 0;  // bitmasks: >=1 target, 2 targets, own target valid
-  unsigned epk0 = 0;                      // far exponent offsets in [0, 15], nibbles
+  double f[kQ], acc[kQ], A0[SLOW ? kQ : 1], A1[SLOW ? kQ : 1];
+  unsigned cnt1 = 0, tval = 0;   // bitmasks: node ends >= 1 horizon; own target valid
+  int qd = -1;                   // the (at most one) node of this lane ending two horizons
   int base = 0x7fffffff;
 #pragma unroll
   for (int q = 0; q < kQ; ++q) {
@@ -241,31 +239,21 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) es_main(PassArgs a) {
     f[q] = field_at(a, p);
     acc[q] = 0.0;
     if (SLOW) {
-      fa[q] = 0.0;
+      A0[q] = 0.0;
+      A1[q] = 0.0;
       const int ti = (p < a.n_in) ? a.tinfo[p] : -1;
       const int c = ti < 0 ? 0 : (ti & 3);
       if (c >= 1) {
         cnt1 |= 1u << q;
-        base = min(base, static_cast<int>(p - (ti >> 2)));
+        base = min(base, static_cast<int>(p - (ti >> 2)) - (c - 1));
       }
-      if (c >= 2) cnt2 |= 1u << q;
+      if (c >= 2) qd = q;
     }
     const int64_t t = t0 + q;
     const int64_t oi = to_input(a, t) - a.o0;
     if (t >= 0 && oi >= 0 && oi < a.n_out && a.dtarget[oi] > kNear) tval |= 1u << q;
   }
-  if (SLOW) {
-#pragma unroll
-    for (int q = 0; q < kQ; ++q) {
-      if (cnt1 & (1u << q)) {
-        const int64_t p = p0 + q;
-        const unsigned v = static_cast<unsigned>(min(max(static_cast<int>(p - (a.tinfo[p] >> 2)) - base, 0), 15));
-        epk0 |= v << (4 * q);
-      }
-    }
-  }
   const bool any_far = SLOW && cnt1 != 0;
-  const int qd = cnt2 ? __ffs(cnt2) - 1 : -1;
 
   for (int m = mb; m < me; m += 2) {
     const int m2 = m + 1 < me ? m + 1 : m;
@@ -293,27 +281,19 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) es_main(PassArgs a) {
     }
     const double cn1 = t1->cn, cn2 = t2->cn * w2;
     if (SLOW && any_far) {
-      // far-window coefficients c_m lambda^{p - t} = (c_m lambda^{base}) lambda^{e_q}
       const double b1 = t1->cw * exp(-t1->rate * static_cast<double>(base));
       const double b2 = w2 * t2->cw * exp(-t2->rate * static_cast<double>(base));
-      const double i1 = t1->linv, i2 = t2->linv;
+      const double b1l = b1 * l1, b2l = b2 * l2;
 #pragma unroll
       for (int q = kQ - 1; q >= 0; --q) {
         g1 = fma(l1, g1, f[q]);
         g2 = fma(l2, g2, f[q]);
         acc[q] = fma(cn1, g1, acc[q]);
         acc[q] = fma(cn2, g2, acc[q]);
-        if (cnt1 & (1u << q)) {
-          const int eq = static_cast<int>((epk0 >> (4 * q)) & 15u);
-          const double c1 = b1 * lam_pow(l1, eq);
-          const double c2 = b2 * lam_pow(l2, eq);
-          fa[q] = fma(c1, g1, fa[q]);
-          fa[q] = fma(c2, g2, fa[q]);
-          if (q == qd) {
-            fb = fma(c1 * i1, g1, fb);
-            fb = fma(c2 * i2, g2, fb);
-          }
-        }
+        A0[q] = fma(b1, g1, A0[q]);
+        A0[q] = fma(b2, g2, A0[q]);
+        A1[q] = fma(b1l, g1, A1[q]);
+        A1[q] = fma(b2l, g2, A1[q]);
       }
     } else {
 #pragma unroll
@@ -333,12 +313,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) es_main(PassArgs a) {
     }
     if (SLOW && (cnt1 & (1u << q))) {
       const int64_t p = p0 + q;
-      const int tf = a.tinfo[p] >> 2;
+      const int ti = a.tinfo[p];
+      const int tf = ti >> 2;
+      const int e = static_cast<int>(p - tf) - base;      // 0 or 1 (plan-time check)
       const int64_t oa = to_input(a, tf) - a.o0;
-      a.ffar[oa] -= fa[q];
-      if (q == qd) {
+      a.ffar[oa] -= e ? A1[q] : A0[q];
+      if (q == qd) {                                      // second target tf + 1: exponent e - 1
         const int64_t ob = to_input(a, tf + 1) - a.o0;
-        a.ffar[ob] -= fb;
+        a.ffar[ob] -= (e - 1) ? A1[q] : A0[q];
       }
     }
   }
@@ -533,10 +515,11 @@ bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirro
     for (int64_t p = b; p < std::min(n_in, b + kQ); ++p)
       if (tinfo[p] >= 0) {
         const int dl = static_cast<int>(p - (tinfo[p] >> 2));
-        lo = std::min(lo, dl);
+        const int c = tinfo[p] & 3;
+        lo = std::min(lo, dl - (c - 1));
         hi = std::max(hi, dl);
       }
-    if (hi - lo > 15) return false;
+    if (hi - lo > 1) return false;   // es_main keeps exponent offsets {0, 1}
   }
   return true;
 }
