@@ -5,26 +5,23 @@
 // apply_full_dense, operators.cpp:236-260, with omega = C(x) kw |y-x|^-alpha):
 //   out_i = h sum_{0<|d|<=D_i^+-} C_i kw(i,i+d) |d h|^-alpha (u_{i+d} - u_i)
 // With w_d = |d|^-alpha and s_i = h^{1-alpha} C_i (x 1/2 when kappa-weighted):
-//   out_i = s_i [ X_i - u_i diag_i ],  X_i = kappa_i F[u]_i + F[kappa u]_i  (or F[u]_i)
+//   out_i = s_i [ kappa_i F[u]_i + F[kappa u]_i - u_i diag_i ]      (kappa)
+//   out_i = s_i [ F[u]_i - u_i diag_i ]                              (no kappa)
 //   F[f]_i = sum_{0<|d|<=D_i^+-} w_d f_{i+d}     (f = 0 outside the domain)
-// diag_i is X_i for u = 1, computed at plan time by this same code (so the
-// far-field error cancels exactly on constants) plus the exact zero-collar
-// exterior part. F splits into
-//   near |d| <= P : direct, register-blocked shared-memory tile (es_near_combine)
+// diag_i (u-independent) is summed exactly at plan time (collar: exterior
+// nodes enter diag with kappa_y := kappa_x). F splits into
+//   near |d| <= P : direct, shared-memory tile (es_near_combine)
 //   far  |d| >  P : w_d ~= sum_m c_m lambda_m^d (lambda_m = e^{-t_m}), so
 //     sum_{d=P+1}^{D} w_d f_{i+d} = sum_m c_m [lambda^{P+1} G_m(i+P+1) - lambda^{D+1} G_m(i+D+1)],
-//     G_m(j) = f_j + lambda_m G_m(j+1)  (suffix recurrence; the left side is the
-//     mirrored prefix recurrence).
-// Each recurrence is a linear scan over the 1-D slab, run as ONE pass per
-// direction and term class (es_pass): warps own 256-node segments (lanes own 8
-// nodes), compute per-term segment aggregates with a warp-shuffle scan, chain
-// the segment carries with a decoupled look-back (segments handed out in
-// descending order through an atomic ticket), then re-run the recurrence in
-// registers and
-//   - accumulate c_m lambda^{P+1} G_m into the lane's own targets (near window),
-//   - for the slow terms, scatter c_m lambda^{D+1} G_m(j) to the target whose
-//     horizon ends at j = i + D_i + 1 (exactly one writer per target).
-// Both fields (u and kappa u) run in the same pass as independent chains.
+//     G_m(j) = f_j + lambda_m G_m(j+1)  (suffix recurrence; the left side is
+//     the mirrored prefix recurrence).
+// The recurrences are linear scans: per 512-node warp segment the segment
+// aggregate (es_aggregate), a carry scan over segments (es_carry), then the
+// main pass (es_main) re-scans in registers (lanes own 16 nodes, warp-shuffle
+// scan across lanes) and accumulates the near-window term into its own
+// targets and scatters the far-window term of the slow exponentials to the
+// target whose horizon ends at this node (j = i + D_i + 1, one writer per
+// target).
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -38,272 +35,292 @@ namespace {
 constexpr int kQ = 8;                // nodes per lane
 constexpr int kSegLen = 32 * kQ;     // nodes per warp segment
 constexpr int kNear = 32;            // P: offsets 1..P summed directly
+constexpr int kPowE = 32;            // |lambda exponent offsets| in the shared table
 constexpr int kMaxTerms = 64;
-constexpr int kWarps = 4;            // warps per CTA in es_pass
-constexpr int kMaxV = 64;            // (terms of a class) x fields handled by one pass
+constexpr int kWarpsPerCta = 4;
 
-struct TermC {
-  double lam, cn, lpow[5], cw, rate, linv;   // lpow[k] = lambda^{kQ 2^k}
+// Packed per-term constants (device, read-only):
+struct TermTab {
+  const double* lam;      // lambda_m
+  const double* lam16;    // lambda^{kQ}, lambda^{2 kQ}, .. lambda^{16 kQ} : [5][M]
+  const double* cn;       // c_m lambda^{P+1}
+  const double* cw;       // c_m
+  const double* rate;     // t_m
+  const double* lam_inv;  // 1/lambda_m
+  const double* pw;       // [Mslow][2 kPowE + 1] lambda^e, e in [-kPowE, kPowE]
+  int M, Mslow;
 };
 
 struct PassArgs {
-  const TermC* terms;    // this class's terms [Mk]
-  const double* lanepow; // [Mk][32] lambda^{kQ (31 - lane)}
-  const double* segpow;  // [Mk] lambda^{kSegLen}
-  int Mk;                // terms in this class
-  int slow;              // class: 1 = slow terms (far scatter)
+  TermTab tt;
   const double* u;       // input slab
-  const double* kappa;   // null: one field
+  const double* kappa;   // may be null
+  int field;             // 0: u, 1: kappa*u
   int mirror;            // 0: right (suffix), 1: left (prefix, mirrored indexing)
-  int64_t n_in, n_out, o0;
+  int64_t n_in, n_out, o0;   // o0: input index of the first output target
   int64_t q0;            // positions-space index of segment 0 (= o0' + P + 1)
-  int64_t nseg, nsegT;   // segments to scan / segments that own targets
+  int64_t nseg;
   const int* tinfo;      // positions space: (tfirst << 2) | count, -1 none
-  const int* dtarget;    // D of each output target in this direction (output order)
-  int* state;            // [0] ticket counter, [1 + s] segment flag (1 agg, 2 inclusive)
-  double* agg;           // [nseg][V] segment aggregates
-  double* incl;          // [nseg][V] inclusive values G(start of segment)
-  double* facc;          // [n_out] near-window part of X (+=)
-  double* ffar;          // [n_out] far-window part of X (-=)
+  const int* dtarget;    // D of each output target in this direction [n_out] (output order)
+  double* agg;           // [M][nseg]
+  double* carry;         // [M][nseg + 1]  G at segment starts, carry[nseg] = 0
+  double* facc;          // [n_out]  near-window exp-sum term (+=)
+  double* ffar;          // [n_out]  far-window exp-sum term (-=)
 };
 
 __device__ __forceinline__ int64_t to_input(const PassArgs& a, int64_t p) {
   return a.mirror ? (a.n_in - 1 - p) : p;
 }
 
-template <int NF, bool SLOW>
-__global__ void __launch_bounds__(32 * kWarps) es_pass(PassArgs a) {
-  const int Mk = a.Mk;
-  const int V = Mk * NF;                     // value slots: j = m * NF + field
+__device__ __forceinline__ double field_at(const PassArgs& a, int64_t p) {
+  if (p < 0 || p >= a.n_in) return 0.0;
+  const int64_t x = to_input(a, p);
+  const double u = a.u[x];
+  return a.field == 0 ? u : u * a.kappa[x];
+}
+
+// warp suffix scan: S_l = a_l + L16 S_{l+1}, with the carry folded into lane 31
+__device__ __forceinline__ double warp_suffix_scan(double a, const double* lamp, int m, int M, int lane) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int off = 1 << k;
+    const double v = __shfl_down_sync(0xffffffffu, a, off);
+    if (lane + off < 32) a = fma(lamp[k * M + m], v, a);
+  }
+  return a;
+}
+
+// Per-term constants staged in shared memory (broadcast reads in the loops).
+struct TermC {
+  double lam, cn, l16[5], cw, rate, linv;
+};
+
+__device__ __forceinline__ void load_terms(const PassArgs& a, TermC* tc) {
+  for (int m = threadIdx.x; m < a.tt.M; m += blockDim.x) {
+    TermC t;
+    t.lam = a.tt.lam[m];
+    t.cn = a.tt.cn[m];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) t.l16[k] = a.tt.lam16[k * a.tt.M + m];
+    t.cw = a.tt.cw[m];
+    t.rate = a.tt.rate[m];
+    t.linv = a.tt.lam_inv[m];
+    tc[m] = t;
+  }
+}
+
+// warp suffix scan of two independent terms (ILP 2)
+__device__ __forceinline__ void warp_suffix_scan2(double& a1, double& a2, const TermC* t1,
+                                                  const TermC* t2, int lane) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int off = 1 << k;
+    const double v1 = __shfl_down_sync(0xffffffffu, a1, off);
+    const double v2 = __shfl_down_sync(0xffffffffu, a2, off);
+    if (lane + off < 32) {
+      a1 = fma(t1->l16[k], v1, a1);
+      a2 = fma(t2->l16[k], v2, a2);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerCta) es_aggregate(PassArgs a) {
   extern __shared__ double smem[];
   TermC* tc = reinterpret_cast<TermC*>(smem);
-  double* lp = smem + (sizeof(TermC) / sizeof(double)) * Mk;   // [Mk][32]
-  double* sp = lp + 32 * Mk;                                   // [Mk]
-  double* wbuf = sp + Mk;                                      // per warp: S[V][33], seg[V], carry[V]
-  for (int i = threadIdx.x; i < Mk; i += blockDim.x) {
-    tc[i] = a.terms[i];
-    sp[i] = a.segpow[i];
-  }
-  for (int i = threadIdx.x; i < 32 * Mk; i += blockDim.x) lp[i] = a.lanepow[i];
+  load_terms(a, tc);
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* Sst = wbuf + warp * (V * 33 + 2 * V);
-  double* segv = Sst + V * 33;
-  double* carry = segv + V;
-
-  // segment ticket: descending order, so every look-back target was handed out earlier
-  int ticket = 0;
-  if (lane == 0) ticket = atomicAdd(a.state, 1);
-  ticket = __shfl_sync(0xffffffffu, ticket, 0);
-  if (ticket >= a.nseg) return;
-  const int64_t seg = a.nseg - 1 - ticket;
+  const int lane = threadIdx.x & 31;
+  const int64_t seg = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
+  if (seg >= a.nseg) return;
   const int64_t p0 = a.q0 + seg * kSegLen + lane * kQ;
+  double f[kQ];
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) f[q] = field_at(a, p0 + q);
+  const int M = a.tt.M;
+  for (int m = 0; m < M; m += 2) {
+    const int m2 = m + 1 < M ? m + 1 : m;
+    const TermC* t1 = tc + m;
+    const TermC* t2 = tc + m2;
+    const double l1 = t1->lam, l2 = t2->lam;
+    double s1 = f[kQ - 1], s2 = f[kQ - 1];
+#pragma unroll
+    for (int q = kQ - 2; q >= 0; --q) {
+      s1 = fma(l1, s1, f[q]);
+      s2 = fma(l2, s2, f[q]);
+    }
+    warp_suffix_scan2(s1, s2, t1, t2, lane);
+    if (lane == 0) {
+      a.agg[m * a.nseg + seg] = s1;
+      if (m2 != m) a.agg[m2 * a.nseg + seg] = s2;
+    }
+  }
+}
 
-  double f[NF][kQ];
+// One block per term: carry[s] = G(start of segment s) = agg[s] + L512 carry[s+1].
+__global__ void __launch_bounds__(1024) es_carry(PassArgs a, const double* lam512) {
+  const int m = blockIdx.x;
+  const int64_t ns = a.nseg;
+  const double L = lam512[m];
+  const double* ag = a.agg + m * ns;
+  double* cr = a.carry + m * (ns + 1);
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  const int64_t per = (ns + nt - 1) / nt;
+  const int64_t s0 = tid * per, s1 = min(ns, s0 + per);
+  // chunk as an affine map: G(start s0) = A + Mu * G(start s1)
+  double A = 0.0, Mu = 1.0;
+  for (int64_t s = s1 - 1; s >= s0; --s) {
+    A = fma(L, A, ag[s]);
+    Mu *= L;
+  }
+  // block suffix scan of affine maps (Kogge-Stone through shared memory)
+  __shared__ double sA[1024], sM[1024];
+  sA[tid] = A;
+  sM[tid] = Mu;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    double nA = sA[tid], nM = sM[tid];
+    if (tid + off < nt) {
+      const double rA = sA[tid + off], rM = sM[tid + off];
+      nA = fma(nM, rA, nA);
+      nM = nM * rM;
+    }
+    __syncthreads();
+    sA[tid] = nA;
+    sM[tid] = nM;
+    __syncthreads();
+  }
+  // G at the end of my chunk = A of the next thread's composed suffix map (G beyond = 0)
+  double g = (tid + 1 < nt) ? sA[tid + 1] : 0.0;
+  if (s0 < s1) {
+    if (s1 == ns) g = 0.0;
+    cr[s1] = g;
+    for (int64_t s = s1 - 1; s >= s0; --s) {
+      g = fma(L, g, ag[s]);
+      cr[s] = g;
+    }
+  }
+  if (tid == 0 && ns == 0) cr[0] = 0.0;
+}
+
+// SLOW = false: the fast terms m in [Ms, M) (near-window term only);
+// SLOW = true : the slow terms m in [0, Ms) (near-window term + far scatter).
+// Far scatter: target t (horizon end p = t + D_t + 1) needs
+//   sum_m c_m lambda_m^{p - t} G_m(p) = sum_m (c_m lambda_m^{base}) lambda_m^{e} G_m(p),
+// with base = the lane's smallest p - t and e in {0, 1} (checked at plan time:
+// horizons change by at most one cell across a lane block). Two accumulators
+// A0 (e = 0) and A1 (e = 1) per node cover both cases and the second target of a
+// two-target node (exponent e - 1).
+template <bool SLOW>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) es_main(PassArgs a) {
+  const int M = a.tt.M, Ms = a.tt.Mslow;
+  const int mb = SLOW ? 0 : Ms, me = SLOW ? Ms : M;
+  extern __shared__ double smem[];
+  TermC* tc = reinterpret_cast<TermC*>(smem);
+  double* cs = smem + (sizeof(TermC) / sizeof(double)) * M;   // [warps][M] segment carries
+  load_terms(a, tc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t seg = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp;
+  const int64_t nsegT = (a.n_out + kSegLen - 1) / kSegLen;
+  double* mycs = cs + warp * M;
+  if (seg < nsegT)
+    for (int m = lane; m < M; m += 32) mycs[m] = a.carry[m * (a.nseg + 1) + seg + 1];
+  __syncthreads();
+  if (seg >= nsegT || mb >= me) return;
+  const int64_t p0 = a.q0 + seg * kSegLen + lane * kQ;       // my first position
+  const int64_t t0 = p0 - (kNear + 1);                       // my first target (positions space)
+  double f[kQ], acc[kQ], A0[SLOW ? kQ : 1], A1[SLOW ? kQ : 1];
+  unsigned cnt1 = 0, tval = 0;   // bitmasks: node ends >= 1 horizon; own target valid
+  int qd = -1;                   // the (at most one) node of this lane ending two horizons
+  int base = 0x7fffffff;
 #pragma unroll
   for (int q = 0; q < kQ; ++q) {
     const int64_t p = p0 + q;
-    double uu = 0.0, kk = 0.0;
-    if (p >= 0 && p < a.n_in) {
-      const int64_t x = to_input(a, p);
-      uu = a.u[x];
-      if (NF == 2) kk = uu * a.kappa[x];
-    }
-    f[0][q] = uu;
-    if (NF == 2) f[NF - 1][q] = kk;
-  }
-
-  // ---- sweep 1: zero-carry warp suffix scans -> per-lane S and segment aggregates
-  for (int m = 0; m < Mk; ++m) {
-    const TermC* t = tc + m;
-    const double lam = t->lam;
-    double s[NF];
-#pragma unroll
-    for (int c = 0; c < NF; ++c) {
-      s[c] = f[c][kQ - 1];
-#pragma unroll
-      for (int q = kQ - 2; q >= 0; --q) s[c] = fma(lam, s[c], f[c][q]);
-    }
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const int off = 1 << k;
-      const double pk = t->lpow[k];
-#pragma unroll
-      for (int c = 0; c < NF; ++c) {
-        const double v = __shfl_down_sync(0xffffffffu, s[c], off);
-        if (lane + off < 32) s[c] = fma(pk, v, s[c]);
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < NF; ++c) {
-      Sst[(m * NF + c) * 33 + lane] = s[c];
-      if (lane == 0) segv[m * NF + c] = s[c];
-    }
-  }
-  if (lane == 0)
-    for (int j = 0; j < V; ++j) Sst[j * 33 + 32] = 0.0;
-  __syncwarp();
-
-  // ---- decoupled look-back for G at the end of this segment (= start of seg+1)
-  volatile int* flags = a.state + 1;
-  for (int j = lane; j < V; j += 32) a.agg[seg * V + j] = segv[j];
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) atomicExch(a.state + 1 + seg, 1);
-  // warp-parallel look-back over windows of 32 predecessors: lane k watches
-  // segment seg+1+k; the window is consumed once every flag is set, up to the
-  // nearest inclusive value (segments past the end count as inclusive 0).
-  {
-    double cr[kMaxV / 32], mult[kMaxV / 32];
-#pragma unroll
-    for (int r = 0; r < kMaxV / 32; ++r) {
-      cr[r] = 0.0;
-      mult[r] = 1.0;
-    }
-    int64_t w0 = seg + 1;
-    for (;;) {
-      const int64_t sk = w0 + lane;
-      int fl = 3;
-      if (sk < a.nseg) {
-        do {
-          fl = flags[sk];
-        } while (fl == 0);
-      }
-      __threadfence();
-      const unsigned inc = __ballot_sync(0xffffffffu, fl >= 2);
-      const int K = inc ? __ffs(inc) - 1 : 32;   // aggregates before the first inclusive
-#pragma unroll
-      for (int r = 0; r < kMaxV / 32; ++r) {
-        const int j = lane + 32 * r;
-        if (j < V) {
-          const double L = sp[j / NF];
-          for (int k = 0; k < K; ++k) {
-            cr[r] = fma(mult[r], __ldcg(a.agg + (w0 + k) * V + j), cr[r]);
-            mult[r] *= L;
-          }
-          if (K < 32 && w0 + K < a.nseg) cr[r] = fma(mult[r], __ldcg(a.incl + (w0 + K) * V + j), cr[r]);
-        }
-      }
-      if (K < 32) break;
-      w0 += 32;
-    }
-#pragma unroll
-    for (int r = 0; r < kMaxV / 32; ++r) {
-      const int j = lane + 32 * r;
-      if (j < V) carry[j] = cr[r];
-    }
-  }
-  __syncwarp();
-  for (int j = lane; j < V; j += 32) a.incl[seg * V + j] = fma(sp[j / NF], carry[j], segv[j]);
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) atomicExch(a.state + 1 + seg, 2);
-  if (seg >= a.nsegT) return;   // scan-only segment (beyond the last target window)
-
-  // ---- targets of this lane
-  const int64_t t0 = p0 - (kNear + 1);   // own (near-window) targets t0 + q, positions space
-  unsigned tval = 0, cnt1 = 0;
-  int qd = -1, base = 0x7fffffff;
-  double kt[NF == 2 ? kQ : 1];           // kappa of the far target ending at node q
-#pragma unroll
-  for (int q = 0; q < kQ; ++q) {
-    const int64_t t = t0 + q;
-    const int64_t oi = to_input(a, t) - a.o0;
-    if (t >= 0 && oi >= 0 && oi < a.n_out && a.dtarget[oi] > kNear) tval |= 1u << q;
-    if (NF == 2) kt[q] = 0.0;
+    f[q] = field_at(a, p);
+    acc[q] = 0.0;
     if (SLOW) {
-      const int64_t p = p0 + q;
-      const int ti = p < a.n_in ? a.tinfo[p] : -1;
+      A0[q] = 0.0;
+      A1[q] = 0.0;
+      const int ti = (p < a.n_in) ? a.tinfo[p] : -1;
       const int c = ti < 0 ? 0 : (ti & 3);
       if (c >= 1) {
         cnt1 |= 1u << q;
         base = min(base, static_cast<int>(p - (ti >> 2)) - (c - 1));
-        if (NF == 2) kt[q] = a.kappa[to_input(a, ti >> 2)];
       }
       if (c >= 2) qd = q;
     }
+    const int64_t t = t0 + q;
+    const int64_t oi = to_input(a, t) - a.o0;
+    if (t >= 0 && oi >= 0 && oi < a.n_out && a.dtarget[oi] > kNear) tval |= 1u << q;
   }
-  const bool far = SLOW && cnt1 != 0;
-  double acc[NF][kQ], A0[SLOW ? kQ : 1], A1[SLOW ? kQ : 1];
-  double B0[NF], B1[NF];   // the second target of node qd, per field
-#pragma unroll
-  for (int q = 0; q < kQ; ++q) {
-#pragma unroll
-    for (int c = 0; c < NF; ++c) acc[c][q] = 0.0;
-    if (SLOW) {
-      A0[q] = 0.0;
-      A1[q] = 0.0;
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < NF; ++c) B0[c] = B1[c] = 0.0;
+  const bool any_far = SLOW && cnt1 != 0;
 
-  // ---- sweep 2: recurrences with the true carries
-  for (int m = 0; m < Mk; ++m) {
-    const TermC* t = tc + m;
-    const double lam = t->lam, cn = t->cn;
-    const double lpw = lp[m * 32 + lane];
-    double g[NF];
+  for (int m = mb; m < me; m += 2) {
+    const int m2 = m + 1 < me ? m + 1 : m;
+    const double w2 = m2 != m ? 1.0 : 0.0;   // a lone last term is paired with itself, weight 0
+    const TermC* t1 = tc + m;
+    const TermC* t2 = tc + m2;
+    const double l1 = t1->lam, l2 = t2->lam;
+    const double cg1 = mycs[m], cg2 = mycs[m2];
+    double s1 = f[kQ - 1], s2 = f[kQ - 1];
 #pragma unroll
-    for (int c = 0; c < NF; ++c) {
-      const int j = m * NF + c;
-      g[c] = fma(lpw, carry[j], Sst[j * 33 + lane + 1]);   // G at the end of my 8 nodes
+    for (int q = kQ - 2; q >= 0; --q) {
+      s1 = fma(l1, s1, f[q]);
+      s2 = fma(l2, s2, f[q]);
     }
-    if (SLOW && far) {
-      const double b0 = t->cw * exp(-t->rate * static_cast<double>(base));
-      const double b1 = b0 * lam;
+    if (lane == 31) {  // fold the segment carry into the last lane
+      s1 = fma(t1->l16[0], cg1, s1);
+      s2 = fma(t2->l16[0], cg2, s2);
+    }
+    warp_suffix_scan2(s1, s2, t1, t2, lane);
+    double g1 = __shfl_down_sync(0xffffffffu, s1, 1);
+    double g2 = __shfl_down_sync(0xffffffffu, s2, 1);
+    if (lane == 31) {
+      g1 = cg1;
+      g2 = cg2;
+    }
+    const double cn1 = t1->cn, cn2 = t2->cn * w2;
+    if (SLOW && any_far) {
+      const double b1 = t1->cw * exp(-t1->rate * static_cast<double>(base));
+      const double b2 = w2 * t2->cw * exp(-t2->rate * static_cast<double>(base));
+      const double b1l = b1 * l1, b2l = b2 * l2;
 #pragma unroll
       for (int q = kQ - 1; q >= 0; --q) {
-#pragma unroll
-        for (int c = 0; c < NF; ++c) {
-          g[c] = fma(lam, g[c], f[c][q]);
-          acc[c][q] = fma(cn, g[c], acc[c][q]);
-        }
-        const double y = NF == 2 ? fma(kt[q], g[0], g[NF - 1]) : g[0];
-        A0[q] = fma(b0, y, A0[q]);
-        A1[q] = fma(b1, y, A1[q]);
-        if (q == qd) {
-#pragma unroll
-          for (int c = 0; c < NF; ++c) {
-            B0[c] = fma(b0, g[c], B0[c]);
-            B1[c] = fma(b1, g[c], B1[c]);
-          }
-        }
+        g1 = fma(l1, g1, f[q]);
+        g2 = fma(l2, g2, f[q]);
+        acc[q] = fma(cn1, g1, acc[q]);
+        acc[q] = fma(cn2, g2, acc[q]);
+        A0[q] = fma(b1, g1, A0[q]);
+        A0[q] = fma(b2, g2, A0[q]);
+        A1[q] = fma(b1l, g1, A1[q]);
+        A1[q] = fma(b2l, g2, A1[q]);
       }
     } else {
 #pragma unroll
       for (int q = kQ - 1; q >= 0; --q) {
-#pragma unroll
-        for (int c = 0; c < NF; ++c) {
-          g[c] = fma(lam, g[c], f[c][q]);
-          acc[c][q] = fma(cn, g[c], acc[c][q]);
-        }
+        g1 = fma(l1, g1, f[q]);
+        g2 = fma(l2, g2, f[q]);
+        acc[q] = fma(cn1, g1, acc[q]);
+        acc[q] = fma(cn2, g2, acc[q]);
       }
     }
   }
-
-  // ---- outputs
 #pragma unroll
   for (int q = 0; q < kQ; ++q) {
     if (tval & (1u << q)) {
-      const int64_t x = to_input(a, t0 + q);
-      const double v = NF == 2 ? fma(a.kappa[x], acc[0][q], acc[NF - 1][q]) : acc[0][q];
-      a.facc[x - a.o0] += v;
+      const int64_t oi = to_input(a, t0 + q) - a.o0;
+      a.facc[oi] += acc[q];
     }
-    if (SLOW && far && (cnt1 & (1u << q))) {
+    if (SLOW && (cnt1 & (1u << q))) {
       const int64_t p = p0 + q;
-      const int tf = a.tinfo[p] >> 2;
-      const int e = static_cast<int>(p - tf) - base;        // 0 or 1 (plan-time check)
-      a.ffar[to_input(a, tf) - a.o0] -= e ? A1[q] : A0[q];
-      if (q == qd) {                                        // second target tf + 1, exponent e - 1
-        const int64_t xb = to_input(a, tf + 1);
-        double v0 = B0[0], v1 = B1[0];
-        if (NF == 2) {
-          const double kb = a.kappa[xb];
-          v0 = fma(kb, B0[0], B0[NF - 1]);
-          v1 = fma(kb, B1[0], B1[NF - 1]);
-        }
-        a.ffar[xb - a.o0] -= (e - 1) ? v1 : v0;
+      const int ti = a.tinfo[p];
+      const int tf = ti >> 2;
+      const int e = static_cast<int>(p - tf) - base;      // 0 or 1 (plan-time check)
+      const int64_t oa = to_input(a, tf) - a.o0;
+      a.ffar[oa] -= e ? A1[q] : A0[q];
+      if (q == qd) {                                      // second target tf + 1: exponent e - 1
+        const int64_t ob = to_input(a, tf + 1) - a.o0;
+        a.ffar[ob] -= (e - 1) ? A1[q] : A0[q];
       }
     }
   }
@@ -318,7 +335,7 @@ struct CombineArgs {
   const double* wnear;   // w_1..w_P at [1..P]
   const double* scale;   // s_i
   const double* diag;
-  const double* facc;    // [n_out]
+  const double* facc;    // [fields][n_out]
   const double* ffar;
   const double* ext;     // mode 1: exact exterior (collar) part of diag, or null
   double* out;           // mode 0: out; mode 1: diag
@@ -331,10 +348,10 @@ constexpr int kCTile = kCombineThreads * kCR;              // targets per CTA
 constexpr int kCWin = kCTile + 2 * kNear;                  // source nodes per CTA
 __host__ __device__ constexpr int cpad(int i) { return i + i / 8; }    // conflict-free lanes
 
-// Near field (|d| <= P) by register blocking: a thread owns 8 consecutive
-// targets, streams the 8 + 2P sources once from shared memory and applies the
-// weights from registers (compile-time tap indices), then combines with the
-// far-field arrays:  out = s_i (X - u_i diag_i).
+// Near field (|d| <= P) by register blocking: a thread owns 16 consecutive
+// targets, streams the 16 + 2P sources once from shared memory and applies the
+// 64 weights from registers (compile-time tap indices), then combines with the
+// far-field arrays:  out = s_i (X - u_i diag_i),  X = kappa_i F[u] + F[kappa u].
 template <bool KW>
 __global__ void __launch_bounds__(kCombineThreads) es_near_combine(CombineArgs a) {
   extern __shared__ double sx[];        // [2][cpad(kCWin)] : u, kappa*u
@@ -401,10 +418,18 @@ __global__ void __launch_bounds__(kCombineThreads) es_near_combine(CombineArgs a
   for (int j = 0; j < kCR; ++j) {
     const int64_t i = t0 + j;
     if (i >= a.n_out) continue;
-    // X = kappa_i F[u] + F[kappa u] (or F[u]); the plan-time pass (mode 1)
-    // evaluates the same expression with u = 1, so constants cancel exactly.
-    const double nx = KW ? fma(a.kappa[a.o0 + i], nu[j], nk[j]) : nu[j];
-    const double X = nx + a.facc[i] + a.ffar[i];
+    // X = kappa_i F[u] + F[kappa u]  (or F[u]); the plan-time pass (mode 1)
+    // evaluates the same expression with u = 1, so diag is consistent with the
+    // fast far field and constants are annihilated exactly (clip).
+    double X;
+    if (KW) {
+      const double ki = a.kappa[a.o0 + i];
+      const double fu = nu[j] + a.facc[i] + a.ffar[i];
+      const double fk = nk[j] + a.facc[a.n_out + i] + a.ffar[a.n_out + i];
+      X = fma(ki, fu, fk);
+    } else {
+      X = nu[j] + a.facc[i] + a.ffar[i];
+    }
     if (a.mode == 1) {
       a.out[i] = a.ext ? X + a.ext[i] : X;
     } else {
@@ -421,6 +446,23 @@ T* upload(const std::vector<T>& v) {
   return d;
 }
 
+}  // namespace
+
+// Device-side state of the exponential-sum plan (declared in plan.hpp).
+struct ExpSumState {
+  int M = 0, Mslow = 0;
+  double *lam = nullptr, *lamp = nullptr, *cn = nullptr, *cw = nullptr, *rate = nullptr,
+         *lam_inv = nullptr, *pw = nullptr, *lam512 = nullptr;
+  int *dplus = nullptr, *dminus = nullptr, *tinfoR = nullptr, *tinfoL = nullptr;
+  double *wnear = nullptr, *scale = nullptr, *diag = nullptr;
+  double *agg = nullptr, *carry = nullptr, *facc = nullptr, *ffar = nullptr;
+  int64_t nsegR = 0, nsegL = 0, o0R = 0, o0L = 0;
+  int fields = 1;
+  double* kappa_dev = nullptr;
+};
+
+namespace {
+
 // exact per-node horizon extents D^+- (Point rule dist < delta with the
 // reference's operation order, operators.cpp:71-78, geometry.cpp:78-84)
 int64_t extent(int64_t g, int dir, double delta, double h, int64_t cap) {
@@ -436,15 +478,15 @@ int64_t extent(int64_t g, int dir, double delta, double h, int64_t cap) {
   return e;
 }
 
-// positions -> targets map for one direction; false if a node would end more
-// than two horizons, the map is not monotone, or a lane block violates the
-// es_pass assumptions (one two-target node, exponent offsets {0, 1}).
+// positions -> targets map for one direction; returns false if some node
+// would own more than two targets or the map is not monotone.
 bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirror, std::vector<int>& tinfo,
                  int64_t q0) {
   tinfo.assign(static_cast<size_t>(n_in), -1);
   const int64_t n_out = static_cast<int64_t>(D.size());
   int64_t last_p = -1;
   for (int64_t k = 0; k < n_out; ++k) {
+    // walk targets in positions-space order
     const int64_t oi = mirror ? (n_out - 1 - k) : k;
     if (D[oi] <= kNear) continue;
     const int64_t tin = o0 + oi;
@@ -463,44 +505,26 @@ bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirro
       slot += 1;
     }
   }
+  // es_main keeps one second-target accumulator per 16-node lane block
   for (int64_t b = std::max<int64_t>(q0, 0); b < n_in; b += kQ) {
     int doubles = 0;
+    for (int64_t p = b; p < std::min(n_in, b + kQ); ++p)
+      if (tinfo[p] >= 0 && (tinfo[p] & 3) == 2) ++doubles;
+    if (doubles > 1) return false;
     int lo = 1 << 30, hi = -(1 << 30);
     for (int64_t p = b; p < std::min(n_in, b + kQ); ++p)
       if (tinfo[p] >= 0) {
-        const int c = tinfo[p] & 3;
-        if (c == 2) ++doubles;
         const int dl = static_cast<int>(p - (tinfo[p] >> 2));
+        const int c = tinfo[p] & 3;
         lo = std::min(lo, dl - (c - 1));
         hi = std::max(hi, dl);
       }
-    if (doubles > 1 || hi - lo > 1) return false;
+    if (hi - lo > 1) return false;   // es_main keeps exponent offsets {0, 1}
   }
   return true;
 }
 
-size_t pass_smem(int Mk, int NF) {
-  const int V = Mk * NF;
-  return sizeof(TermC) * Mk + sizeof(double) * (33 * Mk) + sizeof(double) * kWarps * (V * 33 + 2 * V);
-}
-
 }  // namespace
-
-// Device-side state of the exponential-sum plan (declared in plan.hpp).
-struct ExpSumState {
-  int M = 0, Mslow = 0;
-  TermC* terms = nullptr;          // [M], slow terms first
-  double* lanepow = nullptr;       // [M][32]
-  double* segpow = nullptr;        // [M]
-  int *dplus = nullptr, *dminus = nullptr, *tinfoR = nullptr, *tinfoL = nullptr;
-  double *wnear = nullptr, *scale = nullptr, *diag = nullptr;
-  double *agg = nullptr, *incl = nullptr, *facc = nullptr, *ffar = nullptr;
-  int* state = nullptr;            // [4 passes][1 + nseg]
-  int64_t nsegR = 0, nsegL = 0, o0R = 0, o0L = 0, nsmax = 0;
-  int fields = 1;
-  double* kappa_dev = nullptr;
-  size_t smem_pass[2] = {0, 0};
-};
 
 void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode, const double* ext);
 
@@ -527,38 +551,38 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   if (!build_tinfo(dplus, n_in, o0, false, tR, o0 + kNear + 1) ||
       !build_tinfo(dminus, n_in, o0, true, tL, (n_in - o0 - n_out) + kNear + 1))
     return;
-  const int M = es.terms;
-  int64_t dmin = dmax;
-  for (int64_t i = 0; i < n_out; ++i) dmin = std::min<int64_t>(dmin, std::min(dplus[i], dminus[i]));
-  int Ms = 0;   // rates ascend: slow terms (far end not negligible) come first
-  for (int m = 0; m < M; ++m)
-    if (es.rate[m] * static_cast<double>(std::max<int64_t>(dmin, kNear + 1) + 1) <= 40.0) Ms = m + 1;
-  const int fields = d.kappa ? 2 : 1;
-  if (Ms * fields > kMaxV || (M - Ms) * fields > kMaxV) return;
 
   auto* S = new ExpSumState();
   P.es_state = S;
   P.es = es;
+  const int M = es.terms;
+  int64_t dmin = dmax;
+  for (int64_t i = 0; i < n_out; ++i) dmin = std::min<int64_t>(dmin, std::min(dplus[i], dminus[i]));
+  int Ms = 0;
+  for (int m = 0; m < M; ++m)
+    if (es.rate[m] * static_cast<double>(std::max<int64_t>(dmin, kNear + 1) + 1) <= 40.0) Ms = m + 1;
   S->M = M;
   S->Mslow = Ms;
-  S->fields = fields;
-  std::vector<TermC> tcs(M);
-  std::vector<double> lanep(static_cast<size_t>(M) * 32), segp(M);
+  std::vector<double> lam(M), lamp(5 * M), cn(M), linv(M), l512(M);
   for (int m = 0; m < M; ++m) {
     const double t = es.rate[m];
-    TermC& c = tcs[m];
-    c.lam = std::exp(-t);
-    for (int k = 0; k < 5; ++k) c.lpow[k] = std::exp(-t * kQ * double(1 << k));
-    c.cn = es.weight[m] * std::exp(-t * (kNear + 1));
-    c.cw = es.weight[m];
-    c.rate = t;
-    c.linv = std::exp(t);
-    for (int l = 0; l < 32; ++l) lanep[m * 32 + l] = std::exp(-t * kQ * (31 - l));
-    segp[m] = std::exp(-t * kSegLen);
+    lam[m] = std::exp(-t);
+    for (int k = 0; k < 5; ++k) lamp[k * M + m] = std::exp(-t * kQ * double(1 << k));
+    cn[m] = es.weight[m] * std::exp(-t * (kNear + 1));
+    linv[m] = std::exp(t);
+    l512[m] = std::exp(-t * kSegLen);
   }
-  S->terms = upload(tcs);
-  S->lanepow = upload(lanep);
-  S->segpow = upload(segp);
+  std::vector<double> pw(static_cast<size_t>(std::max(Ms, 1)) * (2 * kPowE + 1));
+  for (int m = 0; m < Ms; ++m)
+    for (int e = -kPowE; e <= kPowE; ++e) pw[m * (2 * kPowE + 1) + e + kPowE] = std::exp(-es.rate[m] * e);
+  S->lam = upload(lam);
+  S->lamp = upload(lamp);
+  S->cn = upload(cn);
+  S->cw = upload(es.weight);
+  S->rate = upload(es.rate);
+  S->lam_inv = upload(linv);
+  S->lam512 = upload(l512);
+  S->pw = upload(pw);
   S->dplus = upload(dplus);
   S->dminus = upload(dminus);
   S->tinfoR = upload(tR);
@@ -577,6 +601,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
     sc[i] = (d.kappa ? 0.5 : 1.0) * hs * c;
   }
   S->scale = upload(sc);
+  S->fields = d.kappa ? 2 : 1;
   S->kappa_dev = P.d_kappa;
   // scan geometry per direction (positions space)
   const int64_t o0R = o0, o0L = n_in - o0 - n_out;
@@ -590,21 +615,12 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   S->o0L = o0L;
   S->nsegR = nseg_of(o0R);
   S->nsegL = nseg_of(o0L);
-  S->nsmax = std::max(S->nsegR, S->nsegL);
-  const int Vmax = std::max(Ms, M - Ms) * fields;
-  NLG_CUDA(cudaMalloc(&S->agg, sizeof(double) * Vmax * S->nsmax));
-  NLG_CUDA(cudaMalloc(&S->incl, sizeof(double) * Vmax * S->nsmax));
-  NLG_CUDA(cudaMalloc(&S->state, sizeof(int) * 4 * (1 + S->nsmax)));
-  NLG_CUDA(cudaMalloc(&S->facc, sizeof(double) * n_out));
-  NLG_CUDA(cudaMalloc(&S->ffar, sizeof(double) * n_out));
+  const int64_t ns = std::max(S->nsegR, S->nsegL);
+  NLG_CUDA(cudaMalloc(&S->agg, sizeof(double) * M * ns));
+  NLG_CUDA(cudaMalloc(&S->carry, sizeof(double) * M * (ns + 1)));
+  NLG_CUDA(cudaMalloc(&S->facc, sizeof(double) * S->fields * n_out));
+  NLG_CUDA(cudaMalloc(&S->ffar, sizeof(double) * S->fields * n_out));
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * n_out));
-  S->smem_pass[0] = pass_smem(M - Ms, fields);
-  S->smem_pass[1] = pass_smem(Ms, fields);
-  const size_t smax = std::max(S->smem_pass[0], S->smem_pass[1]);
-  NLG_CUDA(cudaFuncSetAttribute(es_pass<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smax)));
-  NLG_CUDA(cudaFuncSetAttribute(es_pass<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smax)));
-  NLG_CUDA(cudaFuncSetAttribute(es_pass<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smax)));
-  NLG_CUDA(cudaFuncSetAttribute(es_pass<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smax)));
   // exterior (zero collar) part of diag, exact: sum_{d > edge distance} w_d,
   // times (kappa_i + kappa_i) when kappa-weighted (kappa_y := kappa_x outside)
   double* ext_dev = nullptr;
@@ -636,6 +652,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   NLG_CUDA(cudaStreamSynchronize(P.stream));
   cudaFree(ones);
   cudaFree(ext_dev);
+  P.fast_method = 2;
 }
 
 void expsum_setup(Plan& P, const nlg_desc& d) {
@@ -646,10 +663,10 @@ void expsum_setup(Plan& P, const nlg_desc& d) {
 void expsum_free(Plan& P) {
   ExpSumState* S = P.es_state;
   if (!S) return;
-  cudaFree(S->terms);
-  for (double* p : {S->lanepow, S->segpow, S->wnear, S->scale, S->diag, S->agg, S->incl, S->facc, S->ffar})
+  for (double* p : {S->lam, S->lamp, S->cn, S->cw, S->rate, S->lam_inv, S->pw, S->lam512, S->wnear,
+                    S->scale, S->diag, S->agg, S->carry, S->facc, S->ffar})
     cudaFree(p);
-  for (int* p : {S->dplus, S->dminus, S->tinfoR, S->tinfoL, S->state}) cudaFree(p);
+  for (int* p : {S->dplus, S->dminus, S->tinfoR, S->tinfoL}) cudaFree(p);
   delete S;
   P.es_state = nullptr;
 }
@@ -657,50 +674,44 @@ void expsum_free(Plan& P) {
 void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode, const double* ext) {
   ExpSumState* S = P.es_state;
   const int64_t n_out = P.n_out;
-  NLG_CUDA(cudaMemsetAsync(S->facc, 0, sizeof(double) * n_out, s));
-  NLG_CUDA(cudaMemsetAsync(S->ffar, 0, sizeof(double) * n_out, s));
-  NLG_CUDA(cudaMemsetAsync(S->state, 0, sizeof(int) * 4 * (1 + S->nsmax), s));
+  NLG_CUDA(cudaMemsetAsync(S->facc, 0, sizeof(double) * S->fields * n_out, s));
+  NLG_CUDA(cudaMemsetAsync(S->ffar, 0, sizeof(double) * S->fields * n_out, s));
+  TermTab tt{S->lam, S->lamp, S->cn, S->cw, S->rate, S->lam_inv, S->pw, S->M, S->Mslow};
   const int64_t nsegT = (n_out + kSegLen - 1) / kSegLen;
-  int pass = 0;
-  for (int mirror = 0; mirror < 2; ++mirror) {
-    for (int slow = 1; slow >= 0; --slow) {
+  const size_t tc_bytes = sizeof(TermC) * S->M;
+  const size_t main_bytes = tc_bytes + sizeof(double) * kWarpsPerCta * S->M;
+  for (int field = 0; field < S->fields; ++field) {
+    for (int mirror = 0; mirror < 2; ++mirror) {
       PassArgs a;
-      const int mb = slow ? 0 : S->Mslow;
-      a.Mk = slow ? S->Mslow : S->M - S->Mslow;
-      a.terms = S->terms + mb;
-      a.lanepow = S->lanepow + 32 * mb;
-      a.segpow = S->segpow + mb;
-      a.slow = slow;
+      a.tt = tt;
       a.u = u;
-      a.kappa = S->fields == 2 ? S->kappa_dev : nullptr;
+      a.kappa = S->kappa_dev;
+      a.field = field;
       a.mirror = mirror;
       a.n_in = P.n_in;
       a.n_out = n_out;
       a.o0 = P.halo_lo;
-      a.q0 = (mirror ? S->o0L : S->o0R) + kNear + 1;
+      const int64_t oo = mirror ? S->o0L : S->o0R;
+      a.q0 = oo + kNear + 1;
       a.nseg = mirror ? S->nsegL : S->nsegR;
-      a.nsegT = nsegT;
       a.tinfo = mirror ? S->tinfoL : S->tinfoR;
       a.dtarget = mirror ? S->dminus : S->dplus;
-      a.state = S->state + pass * (1 + S->nsmax);
       a.agg = S->agg;
-      a.incl = S->incl;
-      a.facc = S->facc;
-      a.ffar = S->ffar;
-      ++pass;
-      if (a.Mk == 0) continue;
-      const unsigned grid = static_cast<unsigned>((a.nseg + kWarps - 1) / kWarps);
-      const size_t sm = S->smem_pass[slow];
+      a.carry = S->carry;
+      a.facc = S->facc + field * n_out;
+      a.ffar = S->ffar + field * n_out;
       cudaEvent_t ev;
+      stage_begin(P, s, kStEsAggregate, &ev);
+      es_aggregate<<<static_cast<unsigned>((a.nseg + kWarpsPerCta - 1) / kWarpsPerCta), 32 * kWarpsPerCta, tc_bytes, s>>>(a);
+      stage_end(P, s, kStEsAggregate, ev, 1);
+      stage_begin(P, s, kStEsCarry, &ev);
+      es_carry<<<S->M, 1024, 0, s>>>(a, S->lam512);
+      stage_end(P, s, kStEsCarry, ev, 1);
       stage_begin(P, s, kStEsMain, &ev);
-      if (S->fields == 2) {
-        if (slow) es_pass<2, true><<<grid, 32 * kWarps, sm, s>>>(a);
-        else es_pass<2, false><<<grid, 32 * kWarps, sm, s>>>(a);
-      } else {
-        if (slow) es_pass<1, true><<<grid, 32 * kWarps, sm, s>>>(a);
-        else es_pass<1, false><<<grid, 32 * kWarps, sm, s>>>(a);
-      }
-      stage_end(P, s, kStEsMain, ev, 1);
+      const unsigned gm = static_cast<unsigned>((nsegT + kWarpsPerCta - 1) / kWarpsPerCta);
+      es_main<true><<<gm, 32 * kWarpsPerCta, main_bytes, s>>>(a);
+      es_main<false><<<gm, 32 * kWarpsPerCta, main_bytes, s>>>(a);
+      stage_end(P, s, kStEsMain, ev, 2);
     }
   }
   CombineArgs c;
