@@ -154,6 +154,7 @@ nlg_status nlg_launch_count(const nlg_plan* plan, int64_t* launches);
 
 /* Kernel algebra (host setup, exact rationals for K <= 4 like kernel.cpp:26-51). */
 nlg_status nlg_match_polynomial(int K, double c, double* coeffs /* K+1 */);
+nlg_status nlg_match_polynomial_exact(int K, int64_t* num, int64_t* den);   /* c = 1, K <= 6 */
 nlg_status nlg_split(int K, double c, double* poly /* K+1 */, double* tail /* >= K+1 */,
                      int* ntail);
 

@@ -54,6 +54,7 @@ EXPORTS = {
     "nlg_stage_times": ([C.c_void_p, _dp, _ip, C.POINTER(C.c_int)], C.c_int),
     "nlg_launch_count": ([C.c_void_p, _ip], C.c_int),
     "nlg_match_polynomial": ([C.c_int, C.c_double, _dp], C.c_int),
+    "nlg_match_polynomial_exact": ([C.c_int, _ip, _ip], C.c_int),
     "nlg_split": ([C.c_int, C.c_double, _dp, _dp, C.POINTER(C.c_int)], C.c_int),
     "nlg_expsum_fit": ([C.c_double, C.c_int, C.c_int64, _dp, _dp, C.POINTER(C.c_int), _dp], C.c_int),
     "nlg_last_error": ([], C.c_char_p),

@@ -91,6 +91,14 @@ std::vector<double> match_polynomial(int K, double c) {
   return out;
 }
 
+void match_polynomial_exact(int K, int64_t* num, int64_t* den) {
+  const auto ex = matching_exact(K);
+  for (int j = 0; j <= K; ++j) {
+    num[j] = static_cast<int64_t>(ex[j].p);
+    den[j] = static_cast<int64_t>(ex[j].q);
+  }
+}
+
 void split_kernel(int K, double c, std::vector<double>& poly, std::vector<double>& tail) {
   poly = match_polynomial(K, c);
   const auto p1 = matching_exact(K);

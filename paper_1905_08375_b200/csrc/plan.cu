@@ -444,6 +444,14 @@ nlg_status nlg_match_polynomial(int K, double c, double* coeffs) {
   });
 }
 
+nlg_status nlg_match_polynomial_exact(int K, int64_t* num, int64_t* den) {
+  return guard([&] {
+    require(num && den, "null argument");
+    require(K >= 0 && K <= 6, "matching order must be in [0, 6]");
+    match_polynomial_exact(K, num, den);
+  });
+}
+
 nlg_status nlg_split(int K, double c, double* poly, double* tail, int* ntail) {
   return guard([&] {
     require(poly && tail && ntail, "null argument");

@@ -106,6 +106,7 @@ void expsum_free(Plan& P);
 
 // host algebra (algebra.cpp)
 std::vector<double> match_polynomial(int K, double c);
+void match_polynomial_exact(int K, int64_t* num, int64_t* den);
 void split_kernel(int K, double c, std::vector<double>& poly, std::vector<double>& tail);
 ExpSum fit_exponential_sum(double alpha, int near, int64_t dmax, double tol);
 

@@ -1,0 +1,132 @@
+"""Slab sharding along axis 0.
+
+CPU (not gpu): world_size-2 gloo processes exchange u halos through
+paper_1905_08375_b200.slabs and each rank evaluates its rows with the oracle
+from ONLY its input slab; the result must equal the whole-grid oracle.
+GPU: sharded plans (row_begin/row_end) for every fast method, run one after
+another on one device, reassemble to the unsharded result."""
+import os
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _worker(rank, world, port, dim, n, delta, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    import oracle as O
+    from paper_1905_08375_b200.slabs import Slab
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    N = n ** dim
+    stride = n ** (dim - 1)
+    u = O.random_vector(N, 5)
+    halo = int(np.floor(delta * n)) + 2
+    sl = Slab(n, stride, halo, rank, world)
+    u_in = torch.zeros(sl.n_in, dtype=torch.float64)
+    own = sl.output_slice()
+    u_in[sl.halo_lo * stride: sl.halo_lo * stride + sl.n_out] = torch.from_numpy(u[own])
+    sl.exchange(u_in)
+    # rebuild a full-grid array that is zero outside this rank's input slab
+    v = np.zeros(N)
+    v[sl.in_begin * stride: sl.in_end * stride] = u_in.numpy()
+    tg = np.arange(own.start, own.stop)
+    got, _ = O.apply(dim, n, v, targets=tg, family=O.FRACTIONAL, alpha=1.5, delta0=delta)
+    ref, _ = O.apply(dim, n, u, targets=tg, family=O.FRACTIONAL, alpha=1.5, delta0=delta)
+    q.put((rank, O.rel_inf(got, ref), bool(np.array_equal(u_in.numpy(), u[sl.in_begin * stride: sl.in_end * stride]))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dim,n,delta", [(1, 512, 0.05), (2, 32, 0.2)])
+def test_gloo_halo_exchange_world2(dim, n, delta):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + dim * 7 + n % 97
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, dim, n, delta, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, err, exact in res:
+        assert exact, f"rank {rank}: halo rows differ"
+        assert err == 0.0, f"rank {rank}: rel {err}"
+
+
+def test_slab_rows_partition():
+    from paper_1905_08375_b200.slabs import slab_rows
+    for n in (7, 64, 4096, 768):
+        for w in (1, 2, 3, 4, 8):
+            rows = [slab_rows(n, w, r) for r in range(w)]
+            assert rows[0][0] == 0 and rows[-1][1] == n
+            assert all(rows[i][1] == rows[i + 1][0] for i in range(w - 1))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["cfg1_small", "trunc2d", "frac2d", "peri2d"])
+def test_sharded_plans_match_unsharded(case, orc):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1905_08375_b200 import nonloc as N, configs
+    from paper_1905_08375_b200.slabs import Slab
+    if case == "cfg1_small":
+        w = configs.cfg1(1 << 16)
+        kw = w.op_kwargs()
+        dim, n, u, comps = 1, w.n, w.u, 1
+    elif case == "trunc2d":
+        dim, n, comps = 2, 64, 1
+        u = orc.random_vector(n * n, 3)
+        kw = None
+    elif case == "frac2d":
+        dim, n, comps = 2, 64, 1
+        rng = np.random.default_rng(2)
+        u = rng.standard_normal(n * n)
+        kw = dict(kernel="fractional", alpha=3.0, delta=(4 + 8 * rng.random(n * n)) / n,
+                  coeff=1 + rng.random(n * n), kappa=np.exp(0.5 * rng.standard_normal(n * n)))
+    else:
+        dim, n, comps = 2, 64, 2
+        rng = np.random.default_rng(3)
+        u = rng.standard_normal(2 * n * n)
+        kw = dict(kernel="peridynamic", delta=(3 + 5 * rng.random(n * n)) / n, coeff=1 + 9 * (rng.random(n * n) < .3))
+    N_ = n ** dim
+    stride = n ** (dim - 1)
+    if kw is None:
+        full = N.Plan(dim=dim, n=n, family=0, route=0, poly=np.array([1.0]), rule=0, form=0, delta0=0.2)
+        ref = full.apply_fast(u)
+    else:
+        ref = N.NonlocalOperator(dim, n, **kw).apply(u)
+    world = 3
+    parts = []
+    for r in range(world):
+        if kw is None:
+            halo = N.halo_rows(dim=dim, n=n, family=0, delta_max=0.2, route=0, rule=0, form=0)
+        else:
+            dmax = float(np.max(kw["delta"])) if kw.get("delta") is not None else kw["delta0"]
+            halo = N.halo_rows(dim=dim, n=n, family=4 if kw["kernel"] == "fractional" else 5, delta_max=dmax)
+        sl = Slab(n, stride, halo, r, world)
+        if kw is None:
+            p = N.Plan(dim=dim, n=n, family=0, route=0, poly=np.array([1.0]), rule=0, form=0, delta0=0.2,
+                       row_begin=sl.row_begin, row_end=sl.row_end)
+        else:
+            k2 = dict(kw)
+            for key in ("delta", "coeff", "kappa"):
+                if k2.get(key) is not None:
+                    k2[key] = sl.input_slice(k2[key])
+            p = N.NonlocalOperator(dim, n, row_begin=sl.row_begin, row_end=sl.row_end, reach=dmax, **k2).plan
+        assert p.info.halo_lo == sl.halo_lo and p.info.halo_hi == sl.halo_hi
+        if comps == 1:
+            ui = sl.input_slice(u)
+        else:
+            ui = np.concatenate([sl.input_slice(u[c * N_:(c + 1) * N_]) for c in range(comps)])
+        parts.append(p.apply_fast(ui).reshape(comps, -1))
+    got = np.concatenate(parts, axis=1).reshape(-1)
+    assert orc.rel_inf(got, ref) <= 1e-12
