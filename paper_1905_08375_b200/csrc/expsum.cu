@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) es_main(PassArgs a) {
   load_terms(a, tc);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t seg = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp;
-  const int64_t nsegT = (a.n_out + kSegLen - 1) / kSegLen;
+  // slow class: every segment (far-window ends may lie past the target
+  // segments when the slab has a halo); fast class: target segments only
+  const int64_t nsegT = SLOW ? a.nseg : (a.n_out + kSegLen - 1) / kSegLen;
   double* mycs = cs + warp * M;
   if (seg < nsegT)
     for (int m = lane; m < M; m += 32) mycs[m] = a.carry[m * (a.nseg + 1) + seg + 1];
@@ -708,8 +710,9 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
       es_carry<<<S->M, 1024, 0, s>>>(a, S->lam512);
       stage_end(P, s, kStEsCarry, ev, 1);
       stage_begin(P, s, kStEsMain, &ev);
+      const unsigned gs = static_cast<unsigned>((a.nseg + kWarpsPerCta - 1) / kWarpsPerCta);
       const unsigned gm = static_cast<unsigned>((nsegT + kWarpsPerCta - 1) / kWarpsPerCta);
-      es_main<true><<<gm, 32 * kWarpsPerCta, main_bytes, s>>>(a);
+      es_main<true><<<gs, 32 * kWarpsPerCta, main_bytes, s>>>(a);
       es_main<false><<<gm, 32 * kWarpsPerCta, main_bytes, s>>>(a);
       stage_end(P, s, kStEsMain, ev, 2);
     }
