@@ -5,23 +5,29 @@
 // apply_full_dense, operators.cpp:236-260, with omega = C(x) kw |y-x|^-alpha):
 //   out_i = h sum_{0<|d|<=D_i^+-} C_i kw(i,i+d) |d h|^-alpha (u_{i+d} - u_i)
 // With w_d = |d|^-alpha and s_i = h^{1-alpha} C_i (x 1/2 when kappa-weighted):
-//   out_i = s_i [ kappa_i F[u]_i + F[kappa u]_i - u_i diag_i ]      (kappa)
-//   out_i = s_i [ F[u]_i - u_i diag_i ]                              (no kappa)
+//   out_i = s_i [ X_i - u_i diag_i ],  X_i = kappa_i F[u]_i + F[kappa u]_i  (or F[u]_i)
 //   F[f]_i = sum_{0<|d|<=D_i^+-} w_d f_{i+d}     (f = 0 outside the domain)
-// diag_i (u-independent) is summed exactly at plan time (collar: exterior
-// nodes enter diag with kappa_y := kappa_x). F splits into
-//   near |d| <= P : direct, shared-memory tile (es_near_combine)
+// diag_i is X_i for u = 1, computed at plan time by this same code (so the
+// far-field error cancels exactly on constants) plus the exact zero-collar
+// exterior part. F splits into
+//   near |d| <= P : direct, register-blocked shared-memory tile (es_near_combine)
 //   far  |d| >  P : w_d ~= sum_m c_m lambda_m^d (lambda_m = e^{-t_m}), so
 //     sum_{d=P+1}^{D} w_d f_{i+d} = sum_m c_m [lambda^{P+1} G_m(i+P+1) - lambda^{D+1} G_m(i+D+1)],
-//     G_m(j) = f_j + lambda_m G_m(j+1)  (suffix recurrence; the left side is
-//     the mirrored prefix recurrence).
-// The recurrences are linear scans: per 512-node warp segment the segment
-// aggregate (es_aggregate), a carry scan over segments (es_carry), then the
-// main pass (es_main) re-scans in registers (lanes own 16 nodes, warp-shuffle
-// scan across lanes) and accumulates the near-window term into its own
-// targets and scatters the far-window term of the slow exponentials to the
-// target whose horizon ends at this node (j = i + D_i + 1, one writer per
-// target).
+//     G_m(j) = f_j + lambda_m G_m(j+1)  (suffix recurrence; the left side is the
+//     mirrored prefix recurrence).
+//
+// Scan organisation (one pass per direction and term class; the slow class
+// holds the terms whose far-window factor lambda^{D+1} is not negligible):
+//   es_agg   : per 64-node segment, the segment aggregate of every term
+//   es_carry : per term, a block scan of the segment aggregates -> G at every
+//              segment end
+//   es_main  : per segment, the recurrence re-run from its carry
+// A thread owns one (segment, group of 8 terms) pair and walks its 64 nodes
+// sequentially: 8 terms x fields independent FMA chains, no warp scans. The
+// four groups of a segment sit in adjacent lanes and reduce with two shuffles.
+// es_main accumulates c_m lambda^{P+1} G_m(j) into target j - P - 1 (near
+// window) and, for the slow class, c_m lambda^{j-t} G_m(j) into the target t
+// whose horizon ends at j (j = t + D_t + 1, exactly one writer per target).
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -32,298 +38,290 @@ namespace nlg {
 
 namespace {
 
-constexpr int kQ = 8;                // nodes per lane
-constexpr int kSegLen = 32 * kQ;     // nodes per warp segment
+constexpr int kL = 64;               // nodes per segment
+constexpr int kG = 8;                // terms per group (per thread)
+constexpr int kGroups = 4;           // groups per class (adjacent lanes)
+constexpr int kClassMax = kG * kGroups;
 constexpr int kNear = 32;            // P: offsets 1..P summed directly
-constexpr int kPowE = 32;            // |lambda exponent offsets| in the shared table
-constexpr int kMaxTerms = 64;
-constexpr int kWarpsPerCta = 4;
+constexpr int kThreads = 128;        // 32 segments x 4 groups per CTA
 
-// Packed per-term constants (device, read-only):
-struct TermTab {
-  const double* lam;      // lambda_m
-  const double* lam16;    // lambda^{kQ}, lambda^{2 kQ}, .. lambda^{16 kQ} : [5][M]
-  const double* cn;       // c_m lambda^{P+1}
-  const double* cw;       // c_m
-  const double* rate;     // t_m
-  const double* lam_inv;  // 1/lambda_m
-  const double* pw;       // [Mslow][2 kPowE + 1] lambda^e, e in [-kPowE, kPowE]
-  int M, Mslow;
+// Term constants of one class, padded to kClassMax (padding: lam = cn = cw = 0).
+struct ClassTab {
+  const double* lam;
+  const double* cn;      // c_m lambda^{P+1}
+  const double* cw;      // c_m
+  const double* rate;    // t_m
+  const double* linv;    // 1 / lambda_m
+  const double* segpow;  // lambda^{kL}
+  int Mk;                // real terms in the class
 };
 
 struct PassArgs {
-  TermTab tt;
-  const double* u;       // input slab
-  const double* kappa;   // may be null
-  int field;             // 0: u, 1: kappa*u
+  ClassTab ct;
+  const double* u;
+  const double* kappa;   // null: one field
   int mirror;            // 0: right (suffix), 1: left (prefix, mirrored indexing)
-  int64_t n_in, n_out, o0;   // o0: input index of the first output target
+  int64_t n_in, n_out, o0;
   int64_t q0;            // positions-space index of segment 0 (= o0' + P + 1)
-  int64_t nseg;
+  int64_t nseg;          // segments covering [q0, n_in)
   const int* tinfo;      // positions space: (tfirst << 2) | count, -1 none
-  const int* dtarget;    // D of each output target in this direction [n_out] (output order)
-  double* agg;           // [M][nseg]
-  double* carry;         // [M][nseg + 1]  G at segment starts, carry[nseg] = 0
-  double* facc;          // [n_out]  near-window exp-sum term (+=)
-  double* ffar;          // [n_out]  far-window exp-sum term (-=)
+  const int* dtarget;    // D of each output target in this direction (output order)
+  double* agg;           // [kClassMax * NF][nseg]
+  double* carry;         // [kClassMax * NF][nseg]  G at the end of each segment
+  double* facc;          // [n_out] near-window part of X (+=)
+  double* ffar;          // [n_out] far-window part of X (-=)
 };
 
 __device__ __forceinline__ int64_t to_input(const PassArgs& a, int64_t p) {
   return a.mirror ? (a.n_in - 1 - p) : p;
 }
 
-__device__ __forceinline__ double field_at(const PassArgs& a, int64_t p) {
-  if (p < 0 || p >= a.n_in) return 0.0;
-  const int64_t x = to_input(a, p);
-  const double u = a.u[x];
-  return a.field == 0 ? u : u * a.kappa[x];
-}
-
-// warp suffix scan: S_l = a_l + L16 S_{l+1}, with the carry folded into lane 31
-__device__ __forceinline__ double warp_suffix_scan(double a, const double* lamp, int m, int M, int lane) {
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const int off = 1 << k;
-    const double v = __shfl_down_sync(0xffffffffu, a, off);
-    if (lane + off < 32) a = fma(lamp[k * M + m], v, a);
-  }
-  return a;
-}
-
-// Per-term constants staged in shared memory (broadcast reads in the loops).
-struct TermC {
-  double lam, cn, l16[5], cw, rate, linv;
-};
-
-__device__ __forceinline__ void load_terms(const PassArgs& a, TermC* tc) {
-  for (int m = threadIdx.x; m < a.tt.M; m += blockDim.x) {
-    TermC t;
-    t.lam = a.tt.lam[m];
-    t.cn = a.tt.cn[m];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) t.l16[k] = a.tt.lam16[k * a.tt.M + m];
-    t.cw = a.tt.cw[m];
-    t.rate = a.tt.rate[m];
-    t.linv = a.tt.lam_inv[m];
-    tc[m] = t;
+template <int NF>
+__device__ __forceinline__ void load_field(const PassArgs& a, int64_t p, double (&f)[NF]) {
+  f[0] = 0.0;
+  if (NF == 2) f[NF - 1] = 0.0;
+  if (p >= 0 && p < a.n_in) {
+    const int64_t x = to_input(a, p);
+    const double uu = __ldg(a.u + x);
+    f[0] = uu;
+    if (NF == 2) f[NF - 1] = uu * __ldg(a.kappa + x);
   }
 }
 
-// warp suffix scan of two independent terms (ILP 2)
-__device__ __forceinline__ void warp_suffix_scan2(double& a1, double& a2, const TermC* t1,
-                                                  const TermC* t2, int lane) {
+constexpr int kC = 4;                // nodes per prefetch chunk
+
+template <int NF>
+__device__ __forceinline__ void load_chunk(const PassArgs& a, int64_t p, double (&f)[kC][NF]) {
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const int off = 1 << k;
-    const double v1 = __shfl_down_sync(0xffffffffu, a1, off);
-    const double v2 = __shfl_down_sync(0xffffffffu, a2, off);
-    if (lane + off < 32) {
-      a1 = fma(t1->l16[k], v1, a1);
-      a2 = fma(t2->l16[k], v2, a2);
-    }
-  }
+  for (int k = 0; k < kC; ++k) load_field<NF>(a, p + k, f[k]);
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerCta) es_aggregate(PassArgs a) {
-  extern __shared__ double smem[];
-  TermC* tc = reinterpret_cast<TermC*>(smem);
-  load_terms(a, tc);
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t seg = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
+template <int NF>
+__global__ void __launch_bounds__(kThreads) es_agg(PassArgs a) {
+  const int lane = threadIdx.x & 31, grp = lane & 3;
+  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 2;
   if (seg >= a.nseg) return;
-  const int64_t p0 = a.q0 + seg * kSegLen + lane * kQ;
-  double f[kQ];
+  const int mb = grp * kG;
+  double lam[kG], s[kG][NF];
 #pragma unroll
-  for (int q = 0; q < kQ; ++q) f[q] = field_at(a, p0 + q);
-  const int M = a.tt.M;
-  for (int m = 0; m < M; m += 2) {
-    const int m2 = m + 1 < M ? m + 1 : m;
-    const TermC* t1 = tc + m;
-    const TermC* t2 = tc + m2;
-    const double l1 = t1->lam, l2 = t2->lam;
-    double s1 = f[kQ - 1], s2 = f[kQ - 1];
+  for (int m = 0; m < kG; ++m) {
+    lam[m] = a.ct.lam[mb + m];
 #pragma unroll
-    for (int q = kQ - 2; q >= 0; --q) {
-      s1 = fma(l1, s1, f[q]);
-      s2 = fma(l2, s2, f[q]);
-    }
-    warp_suffix_scan2(s1, s2, t1, t2, lane);
-    if (lane == 0) {
-      a.agg[m * a.nseg + seg] = s1;
-      if (m2 != m) a.agg[m2 * a.nseg + seg] = s2;
-    }
+    for (int c = 0; c < NF; ++c) s[m][c] = 0.0;
   }
+  const int64_t p0 = a.q0 + seg * kL;
+  double cur[kC][NF], nxt[kC][NF];
+  load_chunk<NF>(a, p0 + kL - kC, cur);
+  for (int ch = kL / kC - 1; ch >= 0; --ch) {
+    if (ch > 0) load_chunk<NF>(a, p0 + (ch - 1) * kC, nxt);   // prefetch the next chunk down
+#pragma unroll
+    for (int k = kC - 1; k >= 0; --k)
+#pragma unroll
+      for (int m = 0; m < kG; ++m)
+#pragma unroll
+        for (int c = 0; c < NF; ++c) s[m][c] = fma(lam[m], s[m][c], cur[k][c]);
+#pragma unroll
+    for (int k = 0; k < kC; ++k)
+#pragma unroll
+      for (int c = 0; c < NF; ++c) cur[k][c] = nxt[k][c];
+  }
+#pragma unroll
+  for (int m = 0; m < kG; ++m)
+#pragma unroll
+    for (int c = 0; c < NF; ++c) a.agg[((mb + m) * NF + c) * a.nseg + seg] = s[m][c];
 }
 
-// One block per term: carry[s] = G(start of segment s) = agg[s] + L512 carry[s+1].
-__global__ void __launch_bounds__(1024) es_carry(PassArgs a, const double* lam512) {
-  const int m = blockIdx.x;
+// One block per value j = m * NF + c: carry[j][s] = G(end of segment s)
+//   G(start s) = agg[s] + L G(start s+1),  L = lambda^{kL}.
+// Rounds of 1024 x 16 segments from the top down: coalesced loads into shared
+// memory, a per-thread 16-long chunk, a block scan of affine maps, and the
+// round's carry-in from the round above.
+constexpr int kCarryThreads = 512, kCarryPer = 8;
+
+__global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int NF) {
+  const int j = blockIdx.x;
+  const int m = j / NF;
+  if (m >= a.ct.Mk) return;
   const int64_t ns = a.nseg;
-  const double L = lam512[m];
-  const double* ag = a.agg + m * ns;
-  double* cr = a.carry + m * (ns + 1);
+  const double L = a.ct.segpow[m];
+  const double* ag = a.agg + static_cast<int64_t>(j) * ns;
+  double* cr = a.carry + static_cast<int64_t>(j) * ns;
   const int tid = threadIdx.x;
-  const int nt = blockDim.x;
-  const int64_t per = (ns + nt - 1) / nt;
-  const int64_t s0 = tid * per, s1 = min(ns, s0 + per);
-  // chunk as an affine map: G(start s0) = A + Mu * G(start s1)
-  double A = 0.0, Mu = 1.0;
-  for (int64_t s = s1 - 1; s >= s0; --s) {
-    A = fma(L, A, ag[s]);
-    Mu *= L;
-  }
-  // block suffix scan of affine maps (Kogge-Stone through shared memory)
-  __shared__ double sA[1024], sM[1024];
-  sA[tid] = A;
-  sM[tid] = Mu;
-  __syncthreads();
-  for (int off = 1; off < nt; off <<= 1) {
-    double nA = sA[tid], nM = sM[tid];
-    if (tid + off < nt) {
-      const double rA = sA[tid + off], rM = sM[tid + off];
-      nA = fma(nM, rA, nA);
-      nM = nM * rM;
+  __shared__ double buf[kCarryThreads * kCarryPer + kCarryThreads * kCarryPer / 32];
+  __shared__ double sA[kCarryThreads], sM[kCarryThreads];
+  const int64_t round = static_cast<int64_t>(kCarryThreads) * kCarryPer;
+  double gin = 0.0;                            // G at the top of the current round
+  for (int64_t r1 = ns; r1 > 0; r1 -= round) {
+    const int64_t r0 = r1 > round ? r1 - round : 0;
+    const int cnt = static_cast<int>(r1 - r0);
+    for (int k = tid; k < round; k += kCarryThreads) {
+      const double v = k < cnt ? __ldg(ag + r0 + k) : 0.0;
+      buf[k + k / 32] = v;
     }
     __syncthreads();
-    sA[tid] = nA;
-    sM[tid] = nM;
-    __syncthreads();
-  }
-  // G at the end of my chunk = A of the next thread's composed suffix map (G beyond = 0)
-  double g = (tid + 1 < nt) ? sA[tid + 1] : 0.0;
-  if (s0 < s1) {
-    if (s1 == ns) g = 0.0;
-    cr[s1] = g;
-    for (int64_t s = s1 - 1; s >= s0; --s) {
-      g = fma(L, g, ag[s]);
-      cr[s] = g;
+    // my chunk: local indices [tid*kCarryPer, (tid+1)*kCarryPer)
+    double A = 0.0, Mu = 1.0;
+#pragma unroll
+    for (int k = kCarryPer - 1; k >= 0; --k) {
+      const int li = tid * kCarryPer + k;
+      const bool in = li < cnt;
+      A = in ? fma(L, A, buf[li + li / 32]) : A;
+      Mu = in ? Mu * L : Mu;
     }
+    sA[tid] = A;
+    sM[tid] = Mu;
+    __syncthreads();
+    for (int off = 1; off < kCarryThreads; off <<= 1) {
+      double nA = sA[tid], nM = sM[tid];
+      if (tid + off < kCarryThreads) {
+        nA = fma(nM, sA[tid + off], nA);
+        nM *= sM[tid + off];
+      }
+      __syncthreads();
+      sA[tid] = nA;
+      sM[tid] = nM;
+      __syncthreads();
+    }
+    // G at the end of my chunk: next thread's composed map applied to gin
+    double g = tid + 1 < kCarryThreads ? fma(sM[tid + 1], gin, sA[tid + 1]) : gin;
+#pragma unroll
+    for (int k = kCarryPer - 1; k >= 0; --k) {
+      const int li = tid * kCarryPer + k;
+      if (li < cnt) {
+        cr[r0 + li] = g;
+        g = fma(L, g, buf[li + li / 32]);
+      }
+    }
+    const double gtop = fma(sM[0], gin, sA[0]);   // G(start of this round)
+    __syncthreads();
+    gin = gtop;
   }
-  if (tid == 0 && ns == 0) cr[0] = 0.0;
 }
 
-// SLOW = false: the fast terms m in [Ms, M) (near-window term only);
-// SLOW = true : the slow terms m in [0, Ms) (near-window term + far scatter).
-// Far scatter: target t (horizon end p = t + D_t + 1) needs
-//   sum_m c_m lambda_m^{p - t} G_m(p) = sum_m (c_m lambda_m^{base}) lambda_m^{e} G_m(p),
-// with base = the lane's smallest p - t and e in {0, 1} (checked at plan time:
-// horizons change by at most one cell across a lane block). Two accumulators
-// A0 (e = 0) and A1 (e = 1) per node cover both cases and the second target of a
-// two-target node (exponent e - 1).
-template <bool SLOW>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) es_main(PassArgs a) {
-  const int M = a.tt.M, Ms = a.tt.Mslow;
-  const int mb = SLOW ? 0 : Ms, me = SLOW ? Ms : M;
-  extern __shared__ double smem[];
-  TermC* tc = reinterpret_cast<TermC*>(smem);
-  double* cs = smem + (sizeof(TermC) / sizeof(double)) * M;   // [warps][M] segment carries
-  load_terms(a, tc);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t seg = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp;
-  // slow class: every segment (far-window ends may lie past the target
-  // segments when the slab has a halo); fast class: target segments only
-  const int64_t nsegT = SLOW ? a.nseg : (a.n_out + kSegLen - 1) / kSegLen;
-  double* mycs = cs + warp * M;
-  if (seg < nsegT)
-    for (int m = lane; m < M; m += 32) mycs[m] = a.carry[m * (a.nseg + 1) + seg + 1];
-  __syncthreads();
-  if (seg >= nsegT || mb >= me) return;
-  const int64_t p0 = a.q0 + seg * kSegLen + lane * kQ;       // my first position
-  const int64_t t0 = p0 - (kNear + 1);                       // my first target (positions space)
-  double f[kQ], acc[kQ], A0[SLOW ? kQ : 1], A1[SLOW ? kQ : 1];
-  unsigned cnt1 = 0, tval = 0;   // bitmasks: node ends >= 1 horizon; own target valid
-  int qd = -1;                   // the (at most one) node of this lane ending two horizons
-  int base = 0x7fffffff;
+template <int NF, bool SLOW>
+__global__ void __launch_bounds__(kThreads) es_main(PassArgs a) {
+  const int lane = threadIdx.x & 31, grp = lane & 3;
+  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 2;
+  const bool live = seg < a.nseg;          // whole groups of 4 lanes share `live`
+  const int mb = grp * kG;
+  double lam[kG], cn[kG], g[kG][NF];
+  double cw[SLOW ? kG : 1], li[SLOW ? kG : 1], coef[SLOW ? kG : 1];
 #pragma unroll
-  for (int q = 0; q < kQ; ++q) {
-    const int64_t p = p0 + q;
-    f[q] = field_at(a, p);
-    acc[q] = 0.0;
+  for (int m = 0; m < kG; ++m) {
+    lam[m] = a.ct.lam[mb + m];
+    cn[m] = a.ct.cn[mb + m];
+#pragma unroll
+    for (int c = 0; c < NF; ++c)
+      g[m][c] = live ? a.carry[((mb + m) * NF + c) * a.nseg + seg] : 0.0;
     if (SLOW) {
-      A0[q] = 0.0;
-      A1[q] = 0.0;
-      const int ti = (p < a.n_in) ? a.tinfo[p] : -1;
-      const int c = ti < 0 ? 0 : (ti & 3);
-      if (c >= 1) {
-        cnt1 |= 1u << q;
-        base = min(base, static_cast<int>(p - (ti >> 2)) - (c - 1));
-      }
-      if (c >= 2) qd = q;
+      cw[m] = a.ct.cw[mb + m];
+      li[m] = a.ct.linv[mb + m];
+      coef[m] = 0.0;
     }
-    const int64_t t = t0 + q;
+  }
+  int ecur = -1;                            // exponent of coef (p - t), -1: unset
+  const int64_t p0 = a.q0 + (live ? seg : 0) * kL;
+  // per-node side data, prefetched one chunk ahead with the field values:
+  //   own near-window target t = p - P - 1 (output index or -1), far-target info
+  double cur[kC][NF], nxt[kC][NF];
+  int64_t own_c[kC], own_n[kC];
+  int ti_c[kC], ti_n[kC];
+  auto side = [&](int64_t pp, int64_t& own, int& ti) {
+    own = -1;
+    ti = -1;
+    if (!live) return;
+    const int64_t t = pp - (kNear + 1);
     const int64_t oi = to_input(a, t) - a.o0;
-    if (t >= 0 && oi >= 0 && oi < a.n_out && a.dtarget[oi] > kNear) tval |= 1u << q;
-  }
-  const bool any_far = SLOW && cnt1 != 0;
-
-  for (int m = mb; m < me; m += 2) {
-    const int m2 = m + 1 < me ? m + 1 : m;
-    const double w2 = m2 != m ? 1.0 : 0.0;   // a lone last term is paired with itself, weight 0
-    const TermC* t1 = tc + m;
-    const TermC* t2 = tc + m2;
-    const double l1 = t1->lam, l2 = t2->lam;
-    const double cg1 = mycs[m], cg2 = mycs[m2];
-    double s1 = f[kQ - 1], s2 = f[kQ - 1];
+    if (grp == 0 && t >= 0 && oi >= 0 && oi < a.n_out && __ldg(a.dtarget + oi) > kNear) own = oi;
+    if (SLOW && pp < a.n_in) ti = __ldg(a.tinfo + pp);
+  };
+  load_chunk<NF>(a, p0 + kL - kC, cur);
 #pragma unroll
-    for (int q = kQ - 2; q >= 0; --q) {
-      s1 = fma(l1, s1, f[q]);
-      s2 = fma(l2, s2, f[q]);
-    }
-    if (lane == 31) {  // fold the segment carry into the last lane
-      s1 = fma(t1->l16[0], cg1, s1);
-      s2 = fma(t2->l16[0], cg2, s2);
-    }
-    warp_suffix_scan2(s1, s2, t1, t2, lane);
-    double g1 = __shfl_down_sync(0xffffffffu, s1, 1);
-    double g2 = __shfl_down_sync(0xffffffffu, s2, 1);
-    if (lane == 31) {
-      g1 = cg1;
-      g2 = cg2;
-    }
-    const double cn1 = t1->cn, cn2 = t2->cn * w2;
-    if (SLOW && any_far) {
-      const double b1 = t1->cw * exp(-t1->rate * static_cast<double>(base));
-      const double b2 = w2 * t2->cw * exp(-t2->rate * static_cast<double>(base));
-      const double b1l = b1 * l1, b2l = b2 * l2;
+  for (int k = 0; k < kC; ++k) side(p0 + kL - kC + k, own_c[k], ti_c[k]);
+  for (int ch = kL / kC - 1; ch >= 0; --ch) {
+    if (ch > 0) {
+      load_chunk<NF>(a, p0 + (ch - 1) * kC, nxt);
 #pragma unroll
-      for (int q = kQ - 1; q >= 0; --q) {
-        g1 = fma(l1, g1, f[q]);
-        g2 = fma(l2, g2, f[q]);
-        acc[q] = fma(cn1, g1, acc[q]);
-        acc[q] = fma(cn2, g2, acc[q]);
-        A0[q] = fma(b1, g1, A0[q]);
-        A0[q] = fma(b2, g2, A0[q]);
-        A1[q] = fma(b1l, g1, A1[q]);
-        A1[q] = fma(b2l, g2, A1[q]);
+      for (int k = 0; k < kC; ++k) side(p0 + (ch - 1) * kC + k, own_n[k], ti_n[k]);
+    }
+#pragma unroll
+    for (int k = kC - 1; k >= 0; --k) {
+      const int64_t p = p0 + ch * kC + k;
+      double ac[NF];
+#pragma unroll
+      for (int c = 0; c < NF; ++c) ac[c] = 0.0;
+#pragma unroll
+      for (int m = 0; m < kG; ++m)
+#pragma unroll
+        for (int c = 0; c < NF; ++c) {
+          g[m][c] = fma(lam[m], g[m][c], cur[k][c]);
+          ac[c] = fma(cn[m], g[m][c], ac[c]);
+        }
+#pragma unroll
+      for (int c = 0; c < NF; ++c) {
+        ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], 1);
+        ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], 2);
       }
-    } else {
+      if (own_c[k] >= 0)
 #pragma unroll
-      for (int q = kQ - 1; q >= 0; --q) {
-        g1 = fma(l1, g1, f[q]);
-        g2 = fma(l2, g2, f[q]);
-        acc[q] = fma(cn1, g1, acc[q]);
-        acc[q] = fma(cn2, g2, acc[q]);
+        for (int c = 0; c < NF; ++c) a.facc[c * a.n_out + own_c[k]] += ac[c];
+      if (SLOW) {
+        const int ti = ti_c[k];
+        const int cnt = ti < 0 ? 0 : (ti & 3);
+        double y[NF], z[NF];
+#pragma unroll
+        for (int c = 0; c < NF; ++c) y[c] = z[c] = 0.0;
+        if (cnt) {
+          const int e = static_cast<int>(p - (ti >> 2));      // = D_t + 1
+          if (e != ecur) {
+#pragma unroll
+            for (int m = 0; m < kG; ++m) {
+              if (e == ecur + 1) coef[m] *= lam[m];
+              else if (e == ecur - 1) coef[m] *= li[m];
+              else coef[m] = cw[m] * exp(-__ldg(a.ct.rate + mb + m) * static_cast<double>(e));
+            }
+            ecur = e;
+          }
+#pragma unroll
+          for (int m = 0; m < kG; ++m)
+#pragma unroll
+            for (int c = 0; c < NF; ++c) y[c] = fma(coef[m], g[m][c], y[c]);
+          if (cnt == 2) {
+#pragma unroll
+            for (int m = 0; m < kG; ++m)
+#pragma unroll
+              for (int c = 0; c < NF; ++c) z[c] = fma(coef[m] * li[m], g[m][c], z[c]);
+          }
+        }
+        // the 4 group lanes of a segment see the same p, hence the same cnt
+        if (__any_sync(0xffffffffu, cnt != 0)) {
+#pragma unroll
+          for (int c = 0; c < NF; ++c) {
+            y[c] += __shfl_xor_sync(0xffffffffu, y[c], 1);
+            y[c] += __shfl_xor_sync(0xffffffffu, y[c], 2);
+            z[c] += __shfl_xor_sync(0xffffffffu, z[c], 1);
+            z[c] += __shfl_xor_sync(0xffffffffu, z[c], 2);
+          }
+          if (cnt && grp == 0) {
+            const int tf = ti >> 2;
+            const int64_t oa = to_input(a, tf) - a.o0;
+#pragma unroll
+            for (int c = 0; c < NF; ++c) a.ffar[c * a.n_out + oa] -= y[c];
+            if (cnt == 2) {
+              const int64_t ob = to_input(a, tf + 1) - a.o0;
+#pragma unroll
+              for (int c = 0; c < NF; ++c) a.ffar[c * a.n_out + ob] -= z[c];
+            }
+          }
+        }
       }
     }
-  }
 #pragma unroll
-  for (int q = 0; q < kQ; ++q) {
-    if (tval & (1u << q)) {
-      const int64_t oi = to_input(a, t0 + q) - a.o0;
-      a.facc[oi] += acc[q];
-    }
-    if (SLOW && (cnt1 & (1u << q))) {
-      const int64_t p = p0 + q;
-      const int ti = a.tinfo[p];
-      const int tf = ti >> 2;
-      const int e = static_cast<int>(p - tf) - base;      // 0 or 1 (plan-time check)
-      const int64_t oa = to_input(a, tf) - a.o0;
-      a.ffar[oa] -= e ? A1[q] : A0[q];
-      if (q == qd) {                                      // second target tf + 1: exponent e - 1
-        const int64_t ob = to_input(a, tf + 1) - a.o0;
-        a.ffar[ob] -= (e - 1) ? A1[q] : A0[q];
-      }
+    for (int k = 0; k < kC; ++k) {
+#pragma unroll
+      for (int c = 0; c < NF; ++c) cur[k][c] = nxt[k][c];
+      own_c[k] = own_n[k];
+      ti_c[k] = ti_n[k];
     }
   }
 }
@@ -338,7 +336,7 @@ struct CombineArgs {
   const double* scale;   // s_i
   const double* diag;
   const double* facc;    // [fields][n_out]
-  const double* ffar;
+  const double* ffar;    // [fields][n_out]
   const double* ext;     // mode 1: exact exterior (collar) part of diag, or null
   double* out;           // mode 0: out; mode 1: diag
   int mode;
@@ -350,10 +348,10 @@ constexpr int kCTile = kCombineThreads * kCR;              // targets per CTA
 constexpr int kCWin = kCTile + 2 * kNear;                  // source nodes per CTA
 __host__ __device__ constexpr int cpad(int i) { return i + i / 8; }    // conflict-free lanes
 
-// Near field (|d| <= P) by register blocking: a thread owns 16 consecutive
-// targets, streams the 16 + 2P sources once from shared memory and applies the
-// 64 weights from registers (compile-time tap indices), then combines with the
-// far-field arrays:  out = s_i (X - u_i diag_i),  X = kappa_i F[u] + F[kappa u].
+// Near field (|d| <= P) by register blocking: a thread owns 8 consecutive
+// targets, streams the 8 + 2P sources once from shared memory and applies the
+// weights from registers (compile-time tap indices), then combines with the
+// far-field arrays:  out = s_i (X - u_i diag_i).
 template <bool KW>
 __global__ void __launch_bounds__(kCombineThreads) es_near_combine(CombineArgs a) {
   extern __shared__ double sx[];        // [2][cpad(kCWin)] : u, kappa*u
@@ -420,18 +418,10 @@ __global__ void __launch_bounds__(kCombineThreads) es_near_combine(CombineArgs a
   for (int j = 0; j < kCR; ++j) {
     const int64_t i = t0 + j;
     if (i >= a.n_out) continue;
-    // X = kappa_i F[u] + F[kappa u]  (or F[u]); the plan-time pass (mode 1)
-    // evaluates the same expression with u = 1, so diag is consistent with the
-    // fast far field and constants are annihilated exactly (clip).
-    double X;
-    if (KW) {
-      const double ki = a.kappa[a.o0 + i];
-      const double fu = nu[j] + a.facc[i] + a.ffar[i];
-      const double fk = nk[j] + a.facc[a.n_out + i] + a.ffar[a.n_out + i];
-      X = fma(ki, fu, fk);
-    } else {
-      X = nu[j] + a.facc[i] + a.ffar[i];
-    }
+    // X = kappa_i F[u] + F[kappa u] (or F[u]); the plan-time pass (mode 1)
+    // evaluates the same expression with u = 1, so constants cancel exactly.
+    const double fu = nu[j] + a.facc[i] + a.ffar[i];
+    const double X = KW ? fma(a.kappa[a.o0 + i], fu, nk[j] + a.facc[a.n_out + i] + a.ffar[a.n_out + i]) : fu;
     if (a.mode == 1) {
       a.out[i] = a.ext ? X + a.ext[i] : X;
     } else {
@@ -448,23 +438,6 @@ T* upload(const std::vector<T>& v) {
   return d;
 }
 
-}  // namespace
-
-// Device-side state of the exponential-sum plan (declared in plan.hpp).
-struct ExpSumState {
-  int M = 0, Mslow = 0;
-  double *lam = nullptr, *lamp = nullptr, *cn = nullptr, *cw = nullptr, *rate = nullptr,
-         *lam_inv = nullptr, *pw = nullptr, *lam512 = nullptr;
-  int *dplus = nullptr, *dminus = nullptr, *tinfoR = nullptr, *tinfoL = nullptr;
-  double *wnear = nullptr, *scale = nullptr, *diag = nullptr;
-  double *agg = nullptr, *carry = nullptr, *facc = nullptr, *ffar = nullptr;
-  int64_t nsegR = 0, nsegL = 0, o0R = 0, o0L = 0;
-  int fields = 1;
-  double* kappa_dev = nullptr;
-};
-
-namespace {
-
 // exact per-node horizon extents D^+- (Point rule dist < delta with the
 // reference's operation order, operators.cpp:71-78, geometry.cpp:78-84)
 int64_t extent(int64_t g, int dir, double delta, double h, int64_t cap) {
@@ -480,15 +453,13 @@ int64_t extent(int64_t g, int dir, double delta, double h, int64_t cap) {
   return e;
 }
 
-// positions -> targets map for one direction; returns false if some node
-// would own more than two targets or the map is not monotone.
-bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirror, std::vector<int>& tinfo,
-                 int64_t q0) {
+// positions -> targets map for one direction; false if a node would end more
+// than two horizons or the map is not monotone (the scan path then declines).
+bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirror, std::vector<int>& tinfo) {
   tinfo.assign(static_cast<size_t>(n_in), -1);
   const int64_t n_out = static_cast<int64_t>(D.size());
   int64_t last_p = -1;
   for (int64_t k = 0; k < n_out; ++k) {
-    // walk targets in positions-space order
     const int64_t oi = mirror ? (n_out - 1 - k) : k;
     if (D[oi] <= kNear) continue;
     const int64_t tin = o0 + oi;
@@ -507,26 +478,22 @@ bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirro
       slot += 1;
     }
   }
-  // es_main keeps one second-target accumulator per 16-node lane block
-  for (int64_t b = std::max<int64_t>(q0, 0); b < n_in; b += kQ) {
-    int doubles = 0;
-    for (int64_t p = b; p < std::min(n_in, b + kQ); ++p)
-      if (tinfo[p] >= 0 && (tinfo[p] & 3) == 2) ++doubles;
-    if (doubles > 1) return false;
-    int lo = 1 << 30, hi = -(1 << 30);
-    for (int64_t p = b; p < std::min(n_in, b + kQ); ++p)
-      if (tinfo[p] >= 0) {
-        const int dl = static_cast<int>(p - (tinfo[p] >> 2));
-        const int c = tinfo[p] & 3;
-        lo = std::min(lo, dl - (c - 1));
-        hi = std::max(hi, dl);
-      }
-    if (hi - lo > 1) return false;   // es_main keeps exponent offsets {0, 1}
-  }
   return true;
 }
 
 }  // namespace
+
+// Device-side state of the exponential-sum plan (declared in plan.hpp).
+struct ExpSumState {
+  int M = 0, Mslow = 0, fields = 1;
+  double* tabs = nullptr;          // [2 classes][6 arrays][kClassMax]
+  int Mk[2] = {0, 0};
+  int *dplus = nullptr, *dminus = nullptr, *tinfoR = nullptr, *tinfoL = nullptr;
+  double *wnear = nullptr, *scale = nullptr, *diag = nullptr;
+  double *agg = nullptr, *carry = nullptr, *facc = nullptr, *ffar = nullptr;
+  int64_t nsegR = 0, nsegL = 0, o0R = 0, o0L = 0;
+  double* kappa_dev = nullptr;
+};
 
 void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode, const double* ext);
 
@@ -548,43 +515,42 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   // the scan path pays off only for wide horizons
   if (dmax < 4 * kNear) return;
   ExpSum es = fit_exponential_sum(d.alpha, kNear, dmax, 1e-11);
-  if (es.terms == 0 || es.terms > kMaxTerms || es.rel_err > 1e-11) return;
+  if (es.terms == 0 || es.rel_err > 1e-11) return;
   std::vector<int> tR, tL;
-  if (!build_tinfo(dplus, n_in, o0, false, tR, o0 + kNear + 1) ||
-      !build_tinfo(dminus, n_in, o0, true, tL, (n_in - o0 - n_out) + kNear + 1))
-    return;
+  if (!build_tinfo(dplus, n_in, o0, false, tR) || !build_tinfo(dminus, n_in, o0, true, tL)) return;
+  const int M = es.terms;
+  int64_t dmin = dmax;
+  for (int64_t i = 0; i < n_out; ++i) dmin = std::min<int64_t>(dmin, std::min(dplus[i], dminus[i]));
+  int Ms = 0;   // rates ascend: slow terms (far end not negligible) come first
+  for (int m = 0; m < M; ++m)
+    if (es.rate[m] * static_cast<double>(std::max<int64_t>(dmin, kNear + 1) + 1) <= 40.0) Ms = m + 1;
+  if (Ms > kClassMax || M - Ms > kClassMax) return;
 
   auto* S = new ExpSumState();
   P.es_state = S;
   P.es = es;
-  const int M = es.terms;
-  int64_t dmin = dmax;
-  for (int64_t i = 0; i < n_out; ++i) dmin = std::min<int64_t>(dmin, std::min(dplus[i], dminus[i]));
-  int Ms = 0;
-  for (int m = 0; m < M; ++m)
-    if (es.rate[m] * static_cast<double>(std::max<int64_t>(dmin, kNear + 1) + 1) <= 40.0) Ms = m + 1;
   S->M = M;
   S->Mslow = Ms;
-  std::vector<double> lam(M), lamp(5 * M), cn(M), linv(M), l512(M);
-  for (int m = 0; m < M; ++m) {
-    const double t = es.rate[m];
-    lam[m] = std::exp(-t);
-    for (int k = 0; k < 5; ++k) lamp[k * M + m] = std::exp(-t * kQ * double(1 << k));
-    cn[m] = es.weight[m] * std::exp(-t * (kNear + 1));
-    linv[m] = std::exp(t);
-    l512[m] = std::exp(-t * kSegLen);
+  S->fields = d.kappa ? 2 : 1;
+  S->Mk[0] = Ms;          // class 0: slow
+  S->Mk[1] = M - Ms;      // class 1: fast
+  // per-class constant tables, padded with inert terms (lambda = c = 0)
+  std::vector<double> tab(2 * 6 * kClassMax, 0.0);
+  for (int cls = 0; cls < 2; ++cls) {
+    const int mb = cls == 0 ? 0 : Ms;
+    for (int k = 0; k < S->Mk[cls]; ++k) {
+      const int m = mb + k;
+      const double t = es.rate[m];
+      double* T = tab.data() + cls * 6 * kClassMax;
+      T[0 * kClassMax + k] = std::exp(-t);
+      T[1 * kClassMax + k] = es.weight[m] * std::exp(-t * (kNear + 1));
+      T[2 * kClassMax + k] = es.weight[m];
+      T[3 * kClassMax + k] = t;
+      T[4 * kClassMax + k] = std::exp(t);
+      T[5 * kClassMax + k] = std::exp(-t * kL);
+    }
   }
-  std::vector<double> pw(static_cast<size_t>(std::max(Ms, 1)) * (2 * kPowE + 1));
-  for (int m = 0; m < Ms; ++m)
-    for (int e = -kPowE; e <= kPowE; ++e) pw[m * (2 * kPowE + 1) + e + kPowE] = std::exp(-es.rate[m] * e);
-  S->lam = upload(lam);
-  S->lamp = upload(lamp);
-  S->cn = upload(cn);
-  S->cw = upload(es.weight);
-  S->rate = upload(es.rate);
-  S->lam_inv = upload(linv);
-  S->lam512 = upload(l512);
-  S->pw = upload(pw);
+  S->tabs = upload(tab);
   S->dplus = upload(dplus);
   S->dminus = upload(dminus);
   S->tinfoR = upload(tR);
@@ -603,23 +569,21 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
     sc[i] = (d.kappa ? 0.5 : 1.0) * hs * c;
   }
   S->scale = upload(sc);
-  S->fields = d.kappa ? 2 : 1;
   S->kappa_dev = P.d_kappa;
-  // scan geometry per direction (positions space)
-  const int64_t o0R = o0, o0L = n_in - o0 - n_out;
-  const int64_t nsegT = (n_out + kSegLen - 1) / kSegLen;
+  // scan geometry per direction (positions space); the last segments may own
+  // no near-window target but still end far windows and feed the carries
+  S->o0R = o0;
+  S->o0L = n_in - o0 - n_out;
   auto nseg_of = [&](int64_t oo) {
     const int64_t q0 = oo + kNear + 1;
-    const int64_t span = std::max<int64_t>(n_in - q0, 0);
-    return std::max<int64_t>((span + kSegLen - 1) / kSegLen, nsegT);
+    return std::max<int64_t>((std::max<int64_t>(n_in - q0, 0) + kL - 1) / kL, 1);
   };
-  S->o0R = o0R;
-  S->o0L = o0L;
-  S->nsegR = nseg_of(o0R);
-  S->nsegL = nseg_of(o0L);
+  S->nsegR = nseg_of(S->o0R);
+  S->nsegL = nseg_of(S->o0L);
   const int64_t ns = std::max(S->nsegR, S->nsegL);
-  NLG_CUDA(cudaMalloc(&S->agg, sizeof(double) * M * ns));
-  NLG_CUDA(cudaMalloc(&S->carry, sizeof(double) * M * (ns + 1)));
+  const size_t vals = static_cast<size_t>(kClassMax) * S->fields * ns;
+  NLG_CUDA(cudaMalloc(&S->agg, sizeof(double) * vals));
+  NLG_CUDA(cudaMalloc(&S->carry, sizeof(double) * vals));
   NLG_CUDA(cudaMalloc(&S->facc, sizeof(double) * S->fields * n_out));
   NLG_CUDA(cudaMalloc(&S->ffar, sizeof(double) * S->fields * n_out));
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * n_out));
@@ -654,7 +618,6 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   NLG_CUDA(cudaStreamSynchronize(P.stream));
   cudaFree(ones);
   cudaFree(ext_dev);
-  P.fast_method = 2;
 }
 
 void expsum_setup(Plan& P, const nlg_desc& d) {
@@ -665,9 +628,7 @@ void expsum_setup(Plan& P, const nlg_desc& d) {
 void expsum_free(Plan& P) {
   ExpSumState* S = P.es_state;
   if (!S) return;
-  for (double* p : {S->lam, S->lamp, S->cn, S->cw, S->rate, S->lam_inv, S->pw, S->lam512, S->wnear,
-                    S->scale, S->diag, S->agg, S->carry, S->facc, S->ffar})
-    cudaFree(p);
+  for (double* p : {S->tabs, S->wnear, S->scale, S->diag, S->agg, S->carry, S->facc, S->ffar}) cudaFree(p);
   for (int* p : {S->dplus, S->dminus, S->tinfoR, S->tinfoL}) cudaFree(p);
   delete S;
   P.es_state = nullptr;
@@ -676,50 +637,53 @@ void expsum_free(Plan& P) {
 void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode, const double* ext) {
   ExpSumState* S = P.es_state;
   const int64_t n_out = P.n_out;
-  NLG_CUDA(cudaMemsetAsync(S->facc, 0, sizeof(double) * S->fields * n_out, s));
-  NLG_CUDA(cudaMemsetAsync(S->ffar, 0, sizeof(double) * S->fields * n_out, s));
-  TermTab tt{S->lam, S->lamp, S->cn, S->cw, S->rate, S->lam_inv, S->pw, S->M, S->Mslow};
-  const int64_t nsegT = (n_out + kSegLen - 1) / kSegLen;
-  const size_t tc_bytes = sizeof(TermC) * S->M;
-  const size_t main_bytes = tc_bytes + sizeof(double) * kWarpsPerCta * S->M;
-  for (int field = 0; field < S->fields; ++field) {
-    for (int mirror = 0; mirror < 2; ++mirror) {
+  const int NF = S->fields;
+  NLG_CUDA(cudaMemsetAsync(S->facc, 0, sizeof(double) * NF * n_out, s));
+  NLG_CUDA(cudaMemsetAsync(S->ffar, 0, sizeof(double) * NF * n_out, s));
+  for (int mirror = 0; mirror < 2; ++mirror) {
+    for (int cls = 0; cls < 2; ++cls) {
+      if (S->Mk[cls] == 0) continue;
       PassArgs a;
-      a.tt = tt;
+      const double* T = S->tabs + cls * 6 * kClassMax;
+      a.ct = {T, T + kClassMax, T + 2 * kClassMax, T + 3 * kClassMax, T + 4 * kClassMax, T + 5 * kClassMax,
+              S->Mk[cls]};
       a.u = u;
-      a.kappa = S->kappa_dev;
-      a.field = field;
+      a.kappa = NF == 2 ? S->kappa_dev : nullptr;
       a.mirror = mirror;
       a.n_in = P.n_in;
       a.n_out = n_out;
       a.o0 = P.halo_lo;
-      const int64_t oo = mirror ? S->o0L : S->o0R;
-      a.q0 = oo + kNear + 1;
+      a.q0 = (mirror ? S->o0L : S->o0R) + kNear + 1;
       a.nseg = mirror ? S->nsegL : S->nsegR;
       a.tinfo = mirror ? S->tinfoL : S->tinfoR;
       a.dtarget = mirror ? S->dminus : S->dplus;
       a.agg = S->agg;
       a.carry = S->carry;
-      a.facc = S->facc + field * n_out;
-      a.ffar = S->ffar + field * n_out;
+      a.facc = S->facc;
+      a.ffar = S->ffar;
+      const unsigned grid = static_cast<unsigned>((a.nseg * kGroups + kThreads - 1) / kThreads);
       cudaEvent_t ev;
       stage_begin(P, s, kStEsAggregate, &ev);
-      es_aggregate<<<static_cast<unsigned>((a.nseg + kWarpsPerCta - 1) / kWarpsPerCta), 32 * kWarpsPerCta, tc_bytes, s>>>(a);
+      if (NF == 2) es_agg<2><<<grid, kThreads, 0, s>>>(a);
+      else es_agg<1><<<grid, kThreads, 0, s>>>(a);
       stage_end(P, s, kStEsAggregate, ev, 1);
       stage_begin(P, s, kStEsCarry, &ev);
-      es_carry<<<S->M, 1024, 0, s>>>(a, S->lam512);
+      es_carry<<<kClassMax * NF, kCarryThreads, 0, s>>>(a, NF);
       stage_end(P, s, kStEsCarry, ev, 1);
       stage_begin(P, s, kStEsMain, &ev);
-      const unsigned gs = static_cast<unsigned>((a.nseg + kWarpsPerCta - 1) / kWarpsPerCta);
-      const unsigned gm = static_cast<unsigned>((nsegT + kWarpsPerCta - 1) / kWarpsPerCta);
-      es_main<true><<<gs, 32 * kWarpsPerCta, main_bytes, s>>>(a);
-      es_main<false><<<gm, 32 * kWarpsPerCta, main_bytes, s>>>(a);
-      stage_end(P, s, kStEsMain, ev, 2);
+      if (NF == 2) {
+        if (cls == 0) es_main<2, true><<<grid, kThreads, 0, s>>>(a);
+        else es_main<2, false><<<grid, kThreads, 0, s>>>(a);
+      } else {
+        if (cls == 0) es_main<1, true><<<grid, kThreads, 0, s>>>(a);
+        else es_main<1, false><<<grid, kThreads, 0, s>>>(a);
+      }
+      stage_end(P, s, kStEsMain, ev, 1);
     }
   }
   CombineArgs c;
   c.u = u;
-  c.kappa = S->fields == 2 ? S->kappa_dev : nullptr;
+  c.kappa = NF == 2 ? S->kappa_dev : nullptr;
   c.n_in = P.n_in;
   c.n_out = n_out;
   c.o0 = P.halo_lo;
@@ -737,10 +701,8 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
   stage_begin(P, s, kStEsCombine, &ev);
   const unsigned gc = static_cast<unsigned>((n_out + kCTile - 1) / kCTile);
   const size_t cbytes = sizeof(double) * 2 * (cpad(kCWin) + 1);
-  if (c.kappa)
-    es_near_combine<true><<<gc, kCombineThreads, cbytes, s>>>(c);
-  else
-    es_near_combine<false><<<gc, kCombineThreads, cbytes, s>>>(c);
+  if (c.kappa) es_near_combine<true><<<gc, kCombineThreads, cbytes, s>>>(c);
+  else es_near_combine<false><<<gc, kCombineThreads, cbytes, s>>>(c);
   stage_end(P, s, kStEsCombine, ev, 1);
 }
 
