@@ -198,16 +198,19 @@ __global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int NF) {
   }
 }
 
-template <int NF, bool SLOW>
+// LANES lanes share a segment, each owning G = kClassMax / LANES terms (the
+// slow class uses 8 lanes x 4 terms to keep its far-scatter state in registers).
+template <int NF, bool SLOW, int LANES>
 __global__ void __launch_bounds__(kThreads) es_main(PassArgs a) {
-  const int lane = threadIdx.x & 31, grp = lane & 3;
-  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 2;
-  const bool live = seg < a.nseg;          // whole groups of 4 lanes share `live`
-  const int mb = grp * kG;
-  double lam[kG], cn[kG], g[kG][NF];
-  double cw[SLOW ? kG : 1], li[SLOW ? kG : 1], coef[SLOW ? kG : 1];
+  constexpr int G = kClassMax / LANES;
+  const int lane = threadIdx.x & 31, grp = lane & (LANES - 1);
+  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) / LANES;
+  const bool live = seg < a.nseg;          // whole lane groups share `live`
+  const int mb = grp * G;
+  double lam[G], cn[G], g[G][NF];
+  double cw[SLOW ? G : 1], li[SLOW ? G : 1], coef[SLOW ? G : 1];
 #pragma unroll
-  for (int m = 0; m < kG; ++m) {
+  for (int m = 0; m < G; ++m) {
     lam[m] = a.ct.lam[mb + m];
     cn[m] = a.ct.cn[mb + m];
 #pragma unroll
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(kThreads) es_main(PassArgs a) {
 #pragma unroll
       for (int c = 0; c < NF; ++c) ac[c] = 0.0;
 #pragma unroll
-      for (int m = 0; m < kG; ++m)
+      for (int m = 0; m < G; ++m)
 #pragma unroll
         for (int c = 0; c < NF; ++c) {
           g[m][c] = fma(lam[m], g[m][c], cur[k][c]);
@@ -259,12 +262,12 @@ __global__ void __launch_bounds__(kThreads) es_main(PassArgs a) {
         }
 #pragma unroll
       for (int c = 0; c < NF; ++c) {
-        ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], 1);
-        ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], 2);
+#pragma unroll
+        for (int o = 1; o < LANES; o <<= 1) ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], o);
       }
       if (own_c[k] >= 0)
 #pragma unroll
-        for (int c = 0; c < NF; ++c) a.facc[c * a.n_out + own_c[k]] += ac[c];
+        for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + own_c[k], ac[c]);   // RED, no stall
       if (SLOW) {
         const int ti = ti_c[k];
         const int cnt = ti < 0 ? 0 : (ti & 3);
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(kThreads) es_main(PassArgs a) {
           const int e = static_cast<int>(p - (ti >> 2));      // = D_t + 1
           if (e != ecur) {
 #pragma unroll
-            for (int m = 0; m < kG; ++m) {
+            for (int m = 0; m < G; ++m) {
               if (e == ecur + 1) coef[m] *= lam[m];
               else if (e == ecur - 1) coef[m] *= li[m];
               else coef[m] = cw[m] * exp(-__ldg(a.ct.rate + mb + m) * static_cast<double>(e));
@@ -283,12 +286,12 @@ __global__ void __launch_bounds__(kThreads) es_main(PassArgs a) {
             ecur = e;
           }
 #pragma unroll
-          for (int m = 0; m < kG; ++m)
+          for (int m = 0; m < G; ++m)
 #pragma unroll
             for (int c = 0; c < NF; ++c) y[c] = fma(coef[m], g[m][c], y[c]);
           if (cnt == 2) {
 #pragma unroll
-            for (int m = 0; m < kG; ++m)
+            for (int m = 0; m < G; ++m)
 #pragma unroll
               for (int c = 0; c < NF; ++c) z[c] = fma(coef[m] * li[m], g[m][c], z[c]);
           }
@@ -297,20 +300,21 @@ __global__ void __launch_bounds__(kThreads) es_main(PassArgs a) {
         if (__any_sync(0xffffffffu, cnt != 0)) {
 #pragma unroll
           for (int c = 0; c < NF; ++c) {
-            y[c] += __shfl_xor_sync(0xffffffffu, y[c], 1);
-            y[c] += __shfl_xor_sync(0xffffffffu, y[c], 2);
-            z[c] += __shfl_xor_sync(0xffffffffu, z[c], 1);
-            z[c] += __shfl_xor_sync(0xffffffffu, z[c], 2);
+#pragma unroll
+            for (int o = 1; o < LANES; o <<= 1) {
+              y[c] += __shfl_xor_sync(0xffffffffu, y[c], o);
+              z[c] += __shfl_xor_sync(0xffffffffu, z[c], o);
+            }
           }
           if (cnt && grp == 0) {
             const int tf = ti >> 2;
             const int64_t oa = to_input(a, tf) - a.o0;
 #pragma unroll
-            for (int c = 0; c < NF; ++c) a.ffar[c * a.n_out + oa] -= y[c];
+            for (int c = 0; c < NF; ++c) atomicAdd(a.ffar + c * a.n_out + oa, -y[c]);
             if (cnt == 2) {
               const int64_t ob = to_input(a, tf + 1) - a.o0;
 #pragma unroll
-              for (int c = 0; c < NF; ++c) a.ffar[c * a.n_out + ob] -= z[c];
+              for (int c = 0; c < NF; ++c) atomicAdd(a.ffar + c * a.n_out + ob, -z[c]);
             }
           }
         }
@@ -671,12 +675,13 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
       es_carry<<<kClassMax * NF, kCarryThreads, 0, s>>>(a, NF);
       stage_end(P, s, kStEsCarry, ev, 1);
       stage_begin(P, s, kStEsMain, &ev);
+      const unsigned grid8 = static_cast<unsigned>((a.nseg * 8 + kThreads - 1) / kThreads);
       if (NF == 2) {
-        if (cls == 0) es_main<2, true><<<grid, kThreads, 0, s>>>(a);
-        else es_main<2, false><<<grid, kThreads, 0, s>>>(a);
+        if (cls == 0) es_main<2, true, 8><<<grid8, kThreads, 0, s>>>(a);
+        else es_main<2, false, 4><<<grid, kThreads, 0, s>>>(a);
       } else {
-        if (cls == 0) es_main<1, true><<<grid, kThreads, 0, s>>>(a);
-        else es_main<1, false><<<grid, kThreads, 0, s>>>(a);
+        if (cls == 0) es_main<1, true, 8><<<grid8, kThreads, 0, s>>>(a);
+        else es_main<1, false, 4><<<grid, kThreads, 0, s>>>(a);
       }
       stage_end(P, s, kStEsMain, ev, 1);
     }
