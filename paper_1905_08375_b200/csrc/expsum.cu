@@ -88,18 +88,34 @@ __device__ __forceinline__ void load_field(const PassArgs& a, int64_t p, double 
   }
 }
 
-constexpr int kC = 4;                // nodes per prefetch chunk
+// Shared-memory staging: a CTA covers SPC consecutive segments; their field
+// values (and per-node side data) are loaded once, coalesced, into shared
+// memory with a 65-double segment stride (the segments of a warp then hit
+// distinct banks), and the sequential walks read them from there.
+constexpr int kLP = kL + 1;
 
 template <int NF>
-__device__ __forceinline__ void load_chunk(const PassArgs& a, int64_t p, double (&f)[kC][NF]) {
+__device__ __forceinline__ void stage_fields(const PassArgs& a, int64_t P0, int npos, double* sf) {
+  for (int i = threadIdx.x; i < npos; i += blockDim.x) {
+    double f[NF];
+    load_field<NF>(a, P0 + i, f);
+    const int si = (i / kL) * kLP + (i % kL);
 #pragma unroll
-  for (int k = 0; k < kC; ++k) load_field<NF>(a, p + k, f[k]);
+    for (int c = 0; c < NF; ++c) sf[c * (npos / kL) * kLP + si] = f[c];
+  }
 }
 
 template <int NF>
 __global__ void __launch_bounds__(kThreads) es_agg(PassArgs a) {
+  constexpr int SPC = kThreads / 4;          // segments per CTA (4 lanes x 8 terms each)
+  __shared__ double sf[NF * SPC * kLP];
   const int lane = threadIdx.x & 31, grp = lane & 3;
-  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 2;
+  const int sl = threadIdx.x >> 2;
+  const int64_t seg0 = static_cast<int64_t>(blockIdx.x) * SPC;
+  const int64_t P0 = a.q0 + seg0 * kL;
+  stage_fields<NF>(a, P0, SPC * kL, sf);
+  __syncthreads();
+  const int64_t seg = seg0 + sl;
   if (seg >= a.nseg) return;
   const int mb = grp * kG;
   double lam[kG], s[kG][NF];
@@ -109,22 +125,18 @@ __global__ void __launch_bounds__(kThreads) es_agg(PassArgs a) {
 #pragma unroll
     for (int c = 0; c < NF; ++c) s[m][c] = 0.0;
   }
-  const int64_t p0 = a.q0 + seg * kL;
-  double cur[kC][NF], nxt[kC][NF];
-  load_chunk<NF>(a, p0 + kL - kC, cur);
-  for (int ch = kL / kC - 1; ch >= 0; --ch) {
-    if (ch > 0) load_chunk<NF>(a, p0 + (ch - 1) * kC, nxt);   // prefetch the next chunk down
+  const double* my = sf + sl * kLP;
+#pragma unroll 4
+  for (int q = kL - 1; q >= 0; --q) {
+    double f[NF];
 #pragma unroll
-    for (int k = kC - 1; k >= 0; --k)
+    for (int c = 0; c < NF; ++c) f[c] = my[c * SPC * kLP + q];
 #pragma unroll
-      for (int m = 0; m < kG; ++m)
+    for (int m = 0; m < kG; ++m)
 #pragma unroll
-        for (int c = 0; c < NF; ++c) s[m][c] = fma(lam[m], s[m][c], cur[k][c]);
-#pragma unroll
-    for (int k = 0; k < kC; ++k)
-#pragma unroll
-      for (int c = 0; c < NF; ++c) cur[k][c] = nxt[k][c];
+      for (int c = 0; c < NF; ++c) s[m][c] = fma(lam[m], s[m][c], f[c]);
   }
+  (void)lane;
 #pragma unroll
   for (int m = 0; m < kG; ++m)
 #pragma unroll
@@ -203,9 +215,27 @@ __global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int NF) {
 template <int NF, bool SLOW, int LANES>
 __global__ void __launch_bounds__(kThreads) es_main(PassArgs a) {
   constexpr int G = kClassMax / LANES;
+  constexpr int SPC = kThreads / LANES;       // segments per CTA
+  constexpr int NP = SPC * kL;                // nodes per CTA
+  __shared__ double sf[NF * SPC * kLP];
+  __shared__ int sown[SPC * kLP];             // own near-window target (output index) or -1
+  __shared__ int sti[SLOW ? SPC * kLP : 1];   // far-target info (tfirst << 2 | count) or -1
   const int lane = threadIdx.x & 31, grp = lane & (LANES - 1);
-  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) / LANES;
-  const bool live = seg < a.nseg;          // whole lane groups share `live`
+  const int sl = threadIdx.x / LANES;
+  const int64_t seg0 = static_cast<int64_t>(blockIdx.x) * SPC;
+  const int64_t P0 = a.q0 + seg0 * kL;
+  stage_fields<NF>(a, P0, NP, sf);
+  for (int i = threadIdx.x; i < NP; i += kThreads) {
+    const int64_t p = P0 + i;
+    const int si = (i / kL) * kLP + (i % kL);
+    const int64_t t = p - (kNear + 1);
+    const int64_t oi = to_input(a, t) - a.o0;
+    sown[si] = (t >= 0 && oi >= 0 && oi < a.n_out && __ldg(a.dtarget + oi) > kNear) ? static_cast<int>(oi) : -1;
+    if (SLOW) sti[si] = p < a.n_in ? __ldg(a.tinfo + p) : -1;
+  }
+  __syncthreads();
+  const int64_t seg = seg0 + sl;
+  const bool live = seg < a.nseg;            // whole lane groups share `live`
   const int mb = grp * G;
   double lam[G], cn[G], g[G][NF];
   double cw[SLOW ? G : 1], li[SLOW ? G : 1], coef[SLOW ? G : 1];
@@ -222,112 +252,85 @@ __global__ void __launch_bounds__(kThreads) es_main(PassArgs a) {
       coef[m] = 0.0;
     }
   }
-  int ecur = -1;                            // exponent of coef (p - t), -1: unset
-  const int64_t p0 = a.q0 + (live ? seg : 0) * kL;
-  // per-node side data, prefetched one chunk ahead with the field values:
-  //   own near-window target t = p - P - 1 (output index or -1), far-target info
-  double cur[kC][NF], nxt[kC][NF];
-  int64_t own_c[kC], own_n[kC];
-  int ti_c[kC], ti_n[kC];
-  auto side = [&](int64_t pp, int64_t& own, int& ti) {
-    own = -1;
-    ti = -1;
-    if (!live) return;
-    const int64_t t = pp - (kNear + 1);
-    const int64_t oi = to_input(a, t) - a.o0;
-    if (grp == 0 && t >= 0 && oi >= 0 && oi < a.n_out && __ldg(a.dtarget + oi) > kNear) own = oi;
-    if (SLOW && pp < a.n_in) ti = __ldg(a.tinfo + pp);
-  };
-  load_chunk<NF>(a, p0 + kL - kC, cur);
+  int ecur = -1;                              // exponent of coef (p - t), -1: unset
+  const double* myf = sf + sl * kLP;
+  const int* myown = sown + sl * kLP;
+  const int* myti = sti + (SLOW ? sl * kLP : 0);
+  const int64_t p0 = P0 + static_cast<int64_t>(sl) * kL;
+#pragma unroll 2
+  for (int q = kL - 1; q >= 0; --q) {
+    double ac[NF];
 #pragma unroll
-  for (int k = 0; k < kC; ++k) side(p0 + kL - kC + k, own_c[k], ti_c[k]);
-  for (int ch = kL / kC - 1; ch >= 0; --ch) {
-    if (ch > 0) {
-      load_chunk<NF>(a, p0 + (ch - 1) * kC, nxt);
+    for (int c = 0; c < NF; ++c) ac[c] = 0.0;
 #pragma unroll
-      for (int k = 0; k < kC; ++k) side(p0 + (ch - 1) * kC + k, own_n[k], ti_n[k]);
-    }
-#pragma unroll
-    for (int k = kC - 1; k >= 0; --k) {
-      const int64_t p = p0 + ch * kC + k;
-      double ac[NF];
-#pragma unroll
-      for (int c = 0; c < NF; ++c) ac[c] = 0.0;
-#pragma unroll
-      for (int m = 0; m < G; ++m)
-#pragma unroll
-        for (int c = 0; c < NF; ++c) {
-          g[m][c] = fma(lam[m], g[m][c], cur[k][c]);
-          ac[c] = fma(cn[m], g[m][c], ac[c]);
-        }
+    for (int m = 0; m < G; ++m)
 #pragma unroll
       for (int c = 0; c < NF; ++c) {
-#pragma unroll
-        for (int o = 1; o < LANES; o <<= 1) ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], o);
+        g[m][c] = fma(lam[m], g[m][c], myf[c * NP / kL * kLP + q]);
+        ac[c] = fma(cn[m], g[m][c], ac[c]);
       }
-      if (own_c[k] >= 0)
 #pragma unroll
-        for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + own_c[k], ac[c]);   // RED, no stall
-      if (SLOW) {
-        const int ti = ti_c[k];
-        const int cnt = ti < 0 ? 0 : (ti & 3);
-        double y[NF], z[NF];
+    for (int c = 0; c < NF; ++c) {
 #pragma unroll
-        for (int c = 0; c < NF; ++c) y[c] = z[c] = 0.0;
-        if (cnt) {
-          const int e = static_cast<int>(p - (ti >> 2));      // = D_t + 1
-          if (e != ecur) {
+      for (int o = 1; o < LANES; o <<= 1) ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], o);
+    }
+    const int own = myown[q];
+    if (live && grp == 0 && own >= 0)
 #pragma unroll
-            for (int m = 0; m < G; ++m) {
-              if (e == ecur + 1) coef[m] *= lam[m];
-              else if (e == ecur - 1) coef[m] *= li[m];
-              else coef[m] = cw[m] * exp(-__ldg(a.ct.rate + mb + m) * static_cast<double>(e));
-            }
-            ecur = e;
+      for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + own, ac[c]);   // RED, no stall
+    if (SLOW) {
+      const int ti = live ? myti[q] : -1;
+      const int cnt = ti < 0 ? 0 : (ti & 3);
+      double y[NF], z[NF];
+#pragma unroll
+      for (int c = 0; c < NF; ++c) y[c] = z[c] = 0.0;
+      if (cnt) {
+        const int e = static_cast<int>(p0 + q - (ti >> 2));      // = D_t + 1
+        if (e != ecur) {
+#pragma unroll
+          for (int m = 0; m < G; ++m) {
+            if (e == ecur + 1) coef[m] *= lam[m];
+            else if (e == ecur - 1) coef[m] *= li[m];
+            else coef[m] = cw[m] * exp(-__ldg(a.ct.rate + mb + m) * static_cast<double>(e));
           }
+          ecur = e;
+        }
+#pragma unroll
+        for (int m = 0; m < G; ++m)
+#pragma unroll
+          for (int c = 0; c < NF; ++c) y[c] = fma(coef[m], g[m][c], y[c]);
+        if (cnt == 2) {
 #pragma unroll
           for (int m = 0; m < G; ++m)
 #pragma unroll
-            for (int c = 0; c < NF; ++c) y[c] = fma(coef[m], g[m][c], y[c]);
-          if (cnt == 2) {
+            for (int c = 0; c < NF; ++c) z[c] = fma(coef[m] * li[m], g[m][c], z[c]);
+        }
+      }
+      // the lanes of a segment see the same node, hence the same cnt
+      if (__any_sync(0xffffffffu, cnt != 0)) {
 #pragma unroll
-            for (int m = 0; m < G; ++m)
+        for (int c = 0; c < NF; ++c) {
 #pragma unroll
-              for (int c = 0; c < NF; ++c) z[c] = fma(coef[m] * li[m], g[m][c], z[c]);
+          for (int o = 1; o < LANES; o <<= 1) {
+            y[c] += __shfl_xor_sync(0xffffffffu, y[c], o);
+            z[c] += __shfl_xor_sync(0xffffffffu, z[c], o);
           }
         }
-        // the 4 group lanes of a segment see the same p, hence the same cnt
-        if (__any_sync(0xffffffffu, cnt != 0)) {
+        if (cnt && grp == 0) {
+          const int tf = ti >> 2;
+          const int64_t oa = to_input(a, tf) - a.o0;
 #pragma unroll
-          for (int c = 0; c < NF; ++c) {
+          for (int c = 0; c < NF; ++c) atomicAdd(a.ffar + c * a.n_out + oa, -y[c]);
+          if (cnt == 2) {
+            const int64_t ob = to_input(a, tf + 1) - a.o0;
 #pragma unroll
-            for (int o = 1; o < LANES; o <<= 1) {
-              y[c] += __shfl_xor_sync(0xffffffffu, y[c], o);
-              z[c] += __shfl_xor_sync(0xffffffffu, z[c], o);
-            }
-          }
-          if (cnt && grp == 0) {
-            const int tf = ti >> 2;
-            const int64_t oa = to_input(a, tf) - a.o0;
-#pragma unroll
-            for (int c = 0; c < NF; ++c) atomicAdd(a.ffar + c * a.n_out + oa, -y[c]);
-            if (cnt == 2) {
-              const int64_t ob = to_input(a, tf + 1) - a.o0;
-#pragma unroll
-              for (int c = 0; c < NF; ++c) atomicAdd(a.ffar + c * a.n_out + ob, -z[c]);
-            }
+            for (int c = 0; c < NF; ++c) atomicAdd(a.ffar + c * a.n_out + ob, -z[c]);
           }
         }
       }
     }
-#pragma unroll
-    for (int k = 0; k < kC; ++k) {
-#pragma unroll
-      for (int c = 0; c < NF; ++c) cur[k][c] = nxt[k][c];
-      own_c[k] = own_n[k];
-      ti_c[k] = ti_n[k];
-    }
   }
+  (void)lane;
 }
 
 struct CombineArgs {
@@ -665,7 +668,7 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
       a.carry = S->carry;
       a.facc = S->facc;
       a.ffar = S->ffar;
-      const unsigned grid = static_cast<unsigned>((a.nseg * kGroups + kThreads - 1) / kThreads);
+      const unsigned grid = static_cast<unsigned>((a.nseg * 4 + kThreads - 1) / kThreads);
       cudaEvent_t ev;
       stage_begin(P, s, kStEsAggregate, &ev);
       if (NF == 2) es_agg<2><<<grid, kThreads, 0, s>>>(a);
