@@ -143,42 +143,57 @@ __global__ void __launch_bounds__(kThreads) es_agg(PassArgs a) {
     for (int c = 0; c < NF; ++c) a.agg[((mb + m) * NF + c) * a.nseg + seg] = s[m][c];
 }
 
-// One block per value j = m * NF + c: carry[j][s] = G(end of segment s)
-//   G(start s) = agg[s] + L G(start s+1),  L = lambda^{kL}.
-// Rounds of 1024 x 16 segments from the top down: coalesced loads into shared
-// memory, a per-thread 16-long chunk, a block scan of affine maps, and the
-// round's carry-in from the round above.
+// Segment carries by a three-level scan (all fully parallel except a short
+// per-term block scan over chunks of kChunk segments):
+//   es_chunk  : per (term value j, chunk), the chunk aggregate from its segment aggregates
+//   es_carry  : per j, block scan of chunk aggregates -> G at every chunk end
+//   es_expand : per (j, chunk), walk its segments down from the chunk-end G
+// with G(start s) = agg[s] + L G(start s+1), L = lambda^{kL}.
+constexpr int kChunk = 32;                       // segments per chunk
 constexpr int kCarryThreads = 512, kCarryPer = 8;
 
-__global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int NF) {
+__global__ void es_chunk(PassArgs a, int NF, int64_t nchunk, double* cagg) {
+  const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int V = kClassMax * NF;
+  const int j = static_cast<int>(id % V);
+  const int64_t k = id / V;
+  if (k >= nchunk || j / NF >= a.ct.Mk) return;
+  const double L = a.ct.segpow[j / NF];
+  const double* ag = a.agg + static_cast<int64_t>(j) * a.nseg;
+  const int64_t s0 = k * kChunk, s1 = min(a.nseg, s0 + kChunk);
+  double A = 0.0;
+  for (int64_t s = s1 - 1; s >= s0; --s) A = fma(L, A, __ldg(ag + s));
+  cagg[static_cast<int64_t>(j) * nchunk + k] = A;
+}
+
+// One block per value j: gchunk[j][k] = G(end of chunk k); chunk multiplier
+// Lc = L^{kChunk} (a short last chunk only matters at the very top, where G = 0).
+__global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int NF, int64_t nchunk, const double* cagg,
+                                                          double* gchunk) {
   const int j = blockIdx.x;
   const int m = j / NF;
   if (m >= a.ct.Mk) return;
-  const int64_t ns = a.nseg;
-  const double L = a.ct.segpow[m];
-  const double* ag = a.agg + static_cast<int64_t>(j) * ns;
-  double* cr = a.carry + static_cast<int64_t>(j) * ns;
+  double Lc = 1.0;
+  for (int k = 0; k < kChunk; ++k) Lc *= a.ct.segpow[m];
+  const double* ag = cagg + static_cast<int64_t>(j) * nchunk;
+  double* gc = gchunk + static_cast<int64_t>(j) * nchunk;
   const int tid = threadIdx.x;
   __shared__ double buf[kCarryThreads * kCarryPer + kCarryThreads * kCarryPer / 32];
   __shared__ double sA[kCarryThreads], sM[kCarryThreads];
   const int64_t round = static_cast<int64_t>(kCarryThreads) * kCarryPer;
   double gin = 0.0;                            // G at the top of the current round
-  for (int64_t r1 = ns; r1 > 0; r1 -= round) {
+  for (int64_t r1 = nchunk; r1 > 0; r1 -= round) {
     const int64_t r0 = r1 > round ? r1 - round : 0;
     const int cnt = static_cast<int>(r1 - r0);
-    for (int k = tid; k < round; k += kCarryThreads) {
-      const double v = k < cnt ? __ldg(ag + r0 + k) : 0.0;
-      buf[k + k / 32] = v;
-    }
+    for (int k = tid; k < round; k += kCarryThreads) buf[k + k / 32] = k < cnt ? __ldg(ag + r0 + k) : 0.0;
     __syncthreads();
-    // my chunk: local indices [tid*kCarryPer, (tid+1)*kCarryPer)
     double A = 0.0, Mu = 1.0;
 #pragma unroll
     for (int k = kCarryPer - 1; k >= 0; --k) {
       const int li = tid * kCarryPer + k;
       const bool in = li < cnt;
-      A = in ? fma(L, A, buf[li + li / 32]) : A;
-      Mu = in ? Mu * L : Mu;
+      A = in ? fma(Lc, A, buf[li + li / 32]) : A;
+      Mu = in ? Mu * Lc : Mu;
     }
     sA[tid] = A;
     sM[tid] = Mu;
@@ -194,19 +209,35 @@ __global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int NF) {
       sM[tid] = nM;
       __syncthreads();
     }
-    // G at the end of my chunk: next thread's composed map applied to gin
     double g = tid + 1 < kCarryThreads ? fma(sM[tid + 1], gin, sA[tid + 1]) : gin;
 #pragma unroll
     for (int k = kCarryPer - 1; k >= 0; --k) {
       const int li = tid * kCarryPer + k;
       if (li < cnt) {
-        cr[r0 + li] = g;
-        g = fma(L, g, buf[li + li / 32]);
+        gc[r0 + li] = g;
+        g = fma(Lc, g, buf[li + li / 32]);
       }
     }
-    const double gtop = fma(sM[0], gin, sA[0]);   // G(start of this round)
+    const double gtop = fma(sM[0], gin, sA[0]);
     __syncthreads();
     gin = gtop;
+  }
+}
+
+__global__ void es_expand(PassArgs a, int NF, int64_t nchunk, const double* gchunk) {
+  const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int V = kClassMax * NF;
+  const int j = static_cast<int>(id % V);
+  const int64_t k = id / V;
+  if (k >= nchunk || j / NF >= a.ct.Mk) return;
+  const double L = a.ct.segpow[j / NF];
+  const double* ag = a.agg + static_cast<int64_t>(j) * a.nseg;
+  double* cr = a.carry + static_cast<int64_t>(j) * a.nseg;
+  const int64_t s0 = k * kChunk, s1 = min(a.nseg, s0 + kChunk);
+  double g = gchunk[static_cast<int64_t>(j) * nchunk + k];
+  for (int64_t s = s1 - 1; s >= s0; --s) {
+    cr[s] = g;
+    g = fma(L, g, __ldg(ag + s));
   }
 }
 
@@ -498,6 +529,7 @@ struct ExpSumState {
   int *dplus = nullptr, *dminus = nullptr, *tinfoR = nullptr, *tinfoL = nullptr;
   double *wnear = nullptr, *scale = nullptr, *diag = nullptr;
   double *agg = nullptr, *carry = nullptr, *facc = nullptr, *ffar = nullptr;
+  double *cagg = nullptr, *gchunk = nullptr;
   int64_t nsegR = 0, nsegL = 0, o0R = 0, o0L = 0;
   double* kappa_dev = nullptr;
 };
@@ -591,6 +623,9 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   const size_t vals = static_cast<size_t>(kClassMax) * S->fields * ns;
   NLG_CUDA(cudaMalloc(&S->agg, sizeof(double) * vals));
   NLG_CUDA(cudaMalloc(&S->carry, sizeof(double) * vals));
+  const size_t cvals = static_cast<size_t>(kClassMax) * S->fields * ((ns + kChunk - 1) / kChunk);
+  NLG_CUDA(cudaMalloc(&S->cagg, sizeof(double) * cvals));
+  NLG_CUDA(cudaMalloc(&S->gchunk, sizeof(double) * cvals));
   NLG_CUDA(cudaMalloc(&S->facc, sizeof(double) * S->fields * n_out));
   NLG_CUDA(cudaMalloc(&S->ffar, sizeof(double) * S->fields * n_out));
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * n_out));
@@ -635,7 +670,8 @@ void expsum_setup(Plan& P, const nlg_desc& d) {
 void expsum_free(Plan& P) {
   ExpSumState* S = P.es_state;
   if (!S) return;
-  for (double* p : {S->tabs, S->wnear, S->scale, S->diag, S->agg, S->carry, S->facc, S->ffar}) cudaFree(p);
+  for (double* p : {S->tabs, S->wnear, S->scale, S->diag, S->agg, S->carry, S->facc, S->ffar, S->cagg, S->gchunk})
+    cudaFree(p);
   for (int* p : {S->dplus, S->dminus, S->tinfoR, S->tinfoL}) cudaFree(p);
   delete S;
   P.es_state = nullptr;
@@ -675,8 +711,15 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
       else es_agg<1><<<grid, kThreads, 0, s>>>(a);
       stage_end(P, s, kStEsAggregate, ev, 1);
       stage_begin(P, s, kStEsCarry, &ev);
-      es_carry<<<kClassMax * NF, kCarryThreads, 0, s>>>(a, NF);
-      stage_end(P, s, kStEsCarry, ev, 1);
+      {
+        const int64_t nchunk = (a.nseg + kChunk - 1) / kChunk;
+        const int64_t work = nchunk * kClassMax * NF;
+        const unsigned gw = static_cast<unsigned>((work + 255) / 256);
+        es_chunk<<<gw, 256, 0, s>>>(a, NF, nchunk, S->cagg);
+        es_carry<<<kClassMax * NF, kCarryThreads, 0, s>>>(a, NF, nchunk, S->cagg, S->gchunk);
+        es_expand<<<gw, 256, 0, s>>>(a, NF, nchunk, S->gchunk);
+      }
+      stage_end(P, s, kStEsCarry, ev, 3);
       stage_begin(P, s, kStEsMain, &ev);
       const unsigned grid8 = static_cast<unsigned>((a.nseg * 8 + kThreads - 1) / kThreads);
       if (NF == 2) {
