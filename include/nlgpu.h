@@ -108,9 +108,10 @@ typedef struct nlg_desc {
 typedef struct nlg_info {
   int64_t halo_lo, halo_hi;  /* input rows below / above the output slab       */
   int64_t n_in, n_out;       /* nodes in the input / output slab               */
-  int fast_method;           /* 0 tiled direct quadrature, 1 span prefix sums
+  int fast_method;           /* 0 direct quadrature, 1 span prefix sums
                                 (polynomial kernels), 2 exponential-sum scans
-                                (1-D fractional)                               */
+                                (1-D fractional), 3 offset-table stencil
+                                (2-D/3-D fractional, 2-D peridynamics)         */
   int exp_terms;             /* far-field terms of the 1-D exponential sum     */
   int near_cells;            /* near-field radius (cells) of the 1-D scan path */
   double far_rel_err;        /* fitted kernel error of the exponential sum     */
@@ -145,7 +146,7 @@ nlg_status nlg_counters(const nlg_plan* plan, int64_t* pairs, int64_t* fast_appl
 
 /* Per-stage CUDA-event timing of this plan's kernels (off by default).
  * Stages: 0 direct, 1 span scan, 2 span eval, 3 exp-sum aggregate, 4 exp-sum
- * carry, 5 exp-sum main, 6 near+combine. nlg_stage_times returns (and resets)
+ * carry, 5 exp-sum main, 6 near+combine, 7 stencil. nlg_stage_times returns (and resets)
  * the accumulated milliseconds and launch counts per stage (8 slots). */
 nlg_status nlg_set_profiling(nlg_plan* plan, int on);
 nlg_status nlg_stage_times(nlg_plan* plan, double* ms, int64_t* launches, int* nstages);

@@ -103,4 +103,4 @@ def dptr(a):
     return a.ctypes.data_as(_dp)
 
 
-STAGES = ["direct", "span_scan", "span_eval", "es_aggregate", "es_carry", "es_main", "es_combine"]
+STAGES = ["direct", "span_scan", "span_eval", "es_aggregate", "es_carry", "es_main", "es_combine", "stencil"]

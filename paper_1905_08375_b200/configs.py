@@ -115,4 +115,120 @@ def cfg1(n: int = 1 << 22, exterior: int = 0) -> Workload:
                     algo_bytes=32)
 
 
-WORKLOADS = {"cfg0": cfg0, "cfg1": cfg1}
+# ---------------------------------------------------------------------------
+# 2-D / 3-D workloads. Fields are sums of seeded Fourier modes evaluated with
+# torch (on the GPU when one is present — 768^3 has 4.5e8 nodes), returned as
+# numpy arrays so the plan and the oracle read identical inputs.
+# ---------------------------------------------------------------------------
+
+def _torch_dev():
+    import torch
+    return torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
+
+
+def _modes(rng, count, kmax, dim, decay=1.0):
+    ks = rng.integers(-kmax, kmax + 1, size=(count, dim))
+    ks[np.all(ks == 0, axis=1)] = 1
+    amp = rng.standard_normal(count) / np.linalg.norm(ks, axis=1) ** decay
+    ph = rng.uniform(0.0, 2 * math.pi, count)
+    return ks, amp, ph
+
+
+def _field(n, dim, ks, amp, ph):
+    """sum_m amp_m sin(2 pi k_m . x + ph_m) on the cell centres, row-major."""
+    import torch
+    dev = _torch_dev()
+    x = (torch.arange(n, device=dev, dtype=torch.float64) + 0.5) / n
+    shape = [n] * dim
+    out = torch.zeros(shape, device=dev, dtype=torch.float64)
+    for k, a, p in zip(ks, amp, ph):
+        arg = torch.full(shape, float(p), device=dev, dtype=torch.float64)
+        for j in range(dim):
+            view = [1] * dim
+            view[j] = n
+            arg = arg + (2 * math.pi * float(k[j])) * x.view(view)
+        out += float(a) * torch.sin(arg)
+    return out.reshape(-1).cpu().numpy()
+
+
+def _noise(n_total, rng):
+    return 1e-3 * rng.uniform(-1.0, 1.0, n_total)
+
+
+def _lognormal(n, dim, rng, sigma=0.5, modes=32):
+    ks, amp, ph = _modes(rng, modes, 4, dim)
+    g = _field(n, dim, ks, amp, ph)
+    return np.exp((g - g.mean()) / g.std() * sigma)
+
+
+def cfg2(n: int = 4096) -> Workload:
+    """2-D, 4096^2, delta(x) = h (8 + 4 sin(2 pi k.x + phi)) in [4h, 12h],
+    s = 0.5 (|r|^-3), kappa lognormal (sigma 0.5), u = 64 modes + noise."""
+    s, dim = 0.5, 2
+    h = 1.0 / n
+    rd = np.random.default_rng(3)
+    k = rd.integers(1, 5, size=(1, dim))
+    delta = h * (8.0 + 4.0 * _field(n, dim, k, np.ones(1), rd.uniform(0, 2 * math.pi, 1)))
+    ru = np.random.default_rng(1)
+    ks, amp, ph = _modes(ru, 64, 8, dim)
+    u = _field(n, dim, ks, amp, ph) + _noise(n ** dim, ru)
+    kappa = _lognormal(n, dim, np.random.default_rng(2))
+    coeff = fractional_cdelta(dim, s, delta)
+    return Workload("cfg2_2d_kappa_variable_delta", dim, n, "fractional", dim + 2 * s, s, u, delta=delta,
+                    coeff=coeff, kappa=kappa, exterior=0, seeds={"u": 1, "kappa": 2, "delta": 3},
+                    algo_bytes=32)
+
+
+def cfg3(n: int = 4096) -> Workload:
+    """2-D bond-based peridynamics, 4096^2, u in R^2 (SoA planes), circular
+    inclusion (centre U([.3,.7]^2), radius U(.1,.25)); delta in [3h,5h] inside,
+    [5h,8h] outside (smooth within each material); c_in = 10 c_out."""
+    dim = 2
+    h = 1.0 / n
+    rg = np.random.default_rng(4)
+    cen = rg.uniform(0.3, 0.7, 2)
+    rad = rg.uniform(0.1, 0.25)
+    x = (np.arange(n) + 0.5) / n
+    inside = ((x[:, None] - cen[0]) ** 2 + (x[None, :] - cen[1]) ** 2 < rad * rad).reshape(-1)
+    rd = np.random.default_rng(3)
+    k = rd.integers(1, 5, size=(1, dim))
+    wave = _field(n, dim, k, np.ones(1), rd.uniform(0, 2 * math.pi, 1))
+    delta = np.where(inside, h * (4.0 + wave), h * (6.5 + 1.5 * wave))
+    coeff = np.where(inside, 10.0, 1.0)
+    ru = np.random.default_rng(1)
+    comps = []
+    for _ in range(2):
+        ks, amp, ph = _modes(ru, 64, 8, dim)
+        comps.append(_field(n, dim, ks, amp, ph))
+    u = np.concatenate(comps)
+    return Workload("cfg3_2d_peridynamics_inclusion", dim, n, "peridynamic", 1.0, 0.0, u, delta=delta,
+                    coeff=coeff, exterior=0, seeds={"u": 1, "delta": 3, "inclusion": 4}, algo_bytes=48)
+
+
+def cfg4(n: int = 768, variable: bool = False) -> Workload:
+    """3-D, 768^3 (non power of two), delta = 6h (A) or h (6 + 2 sin(.)) in
+    [4h, 8h] (B); s = 0.25 (|r|^-3.5), kappa lognormal, u = 128 modes."""
+    s, dim = 0.25, 3
+    h = 1.0 / n
+    if variable:
+        rd = np.random.default_rng(3)
+        k = rd.integers(1, 4, size=(1, dim))
+        delta = h * (6.0 + 2.0 * _field(n, dim, k, np.ones(1), rd.uniform(0, 2 * math.pi, 1)))
+        coeff = fractional_cdelta(dim, s, delta)
+        d0 = 0.0
+        c0 = 1.0
+    else:
+        delta, d0 = None, 6.0 * h
+        coeff, c0 = None, float(fractional_cdelta(dim, s, 6.0 * h))
+    ru = np.random.default_rng(1)
+    ks, amp, ph = _modes(ru, 128, 8, dim)
+    u = _field(n, dim, ks, amp, ph)
+    kappa = _lognormal(n, dim, np.random.default_rng(2))
+    name = "cfg4B_3d_kappa_variable_delta" if variable else "cfg4A_3d_kappa_delta6h"
+    return Workload(name, dim, n, "fractional", dim + 2 * s, s, u, delta=delta, delta0=d0, coeff=coeff,
+                    coeff0=c0, kappa=kappa, exterior=0, seeds={"u": 1, "kappa": 2, "delta": 3},
+                    algo_bytes=32 if variable else 24)
+
+
+WORKLOADS = {"cfg0": cfg0, "cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4,
+             "cfg4b": lambda n=768: cfg4(n, variable=True)}

@@ -223,6 +223,8 @@ nlg_status nlg_plan_create(const nlg_desc* desc, nlg_plan** out) {
       spans_setup(P);
     } else if (P.family == NLG_FRACTIONAL && g.dim == 1) {
       expsum_setup(P, d);
+    } else if ((P.family == NLG_FRACTIONAL || P.family == NLG_PERIDYNAMIC) && g.dim >= 2) {
+      stencil_setup(P, d);
     } else {
       P.fast_method = 0;
     }
@@ -244,6 +246,7 @@ void nlg_plan_destroy(nlg_plan* plan) {
   for (auto e : P.sprof.pool) cudaEventDestroy(e);
   spans_free(P);
   expsum_free(P);
+  stencil_free(P);
   cudaFree(P.d_delta);
   cudaFree(P.d_coeff);
   cudaFree(P.d_kappa);
@@ -284,6 +287,13 @@ void fast_dev(Plan& P, const double* u, double* out, cudaStream_t s) {
   switch (P.fast_method) {
     case 1: spans_apply(P, u, out, s); break;
     case 2: expsum_apply(P, u, out, s); break;
+    case 3: {
+      cudaEvent_t ev;
+      stage_begin(P, s, kStStencil, &ev);
+      stencil_apply(P, u, out, s);
+      stage_end(P, s, kStStencil, ev, P.d_kappa && P.family == NLG_FRACTIONAL ? 2 : 1);
+      break;
+    }
     default: {
       cudaEvent_t ev;
       stage_begin(P, s, kStDirect, &ev);

@@ -36,10 +36,11 @@ struct ExpSum {
 };
 
 struct ExpSumState;
+struct StencilState;
 
 // Optional per-stage CUDA-event timing (nlg_set_profiling / nlg_stage_times).
 enum Stage { kStDirect = 0, kStSpanScan, kStSpanEval, kStEsAggregate, kStEsCarry, kStEsMain,
-             kStEsCombine, kNumStages };
+             kStEsCombine, kStStencil, kNumStages };
 struct StageProf {
   bool on = false;
   struct Rec { int stage; cudaEvent_t a, b; };
@@ -83,6 +84,9 @@ struct Plan {
   ExpSum es;
   ExpSumState* es_state = nullptr;
 
+  // fast method 3 (2-D/3-D offset-table stencil)
+  StencilState* st_state = nullptr;
+
   int64_t last_pairs = 0;
   int64_t fast_applies = 0;
   int64_t launches = 0;   // kernels launched by this plan (all entry points)
@@ -103,6 +107,9 @@ void spans_free(Plan& P);
 void expsum_setup(Plan& P, const nlg_desc& d);
 void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void expsum_free(Plan& P);
+void stencil_setup(Plan& P, const nlg_desc& d);
+void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s);
+void stencil_free(Plan& P);
 
 // host algebra (algebra.cpp)
 std::vector<double> match_polynomial(int K, double c);
