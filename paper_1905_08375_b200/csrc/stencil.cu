@@ -79,9 +79,10 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
   const Geom& g = a.g;
   const int64_t n = g.n;
   // target: x along threadIdx.x; remaining axes from blockIdx / threadIdx.y
-  const int64_t ix = static_cast<int64_t>(blockIdx.x) * kTX + threadIdx.x;
+  const int64_t bx = (n + kTX - 1) / kTX;
+  const int64_t ix = (static_cast<int64_t>(blockIdx.x) % bx) * kTX + threadIdx.x;
   const int64_t rowsOut = (g.row_end - g.row_begin) * (DIM == 3 ? n : 1);
-  const int64_t r = static_cast<int64_t>(blockIdx.y) * kTY + threadIdx.y;   // output row (axis0 [, axis1])
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) / bx) * kTY + threadIdx.y;   // output row (axis0 [, axis1])
   const bool live = ix < n && r < rowsOut;
   int64_t ki[3] = {0, 0, 0};
   ki[DIM - 1] = live ? ix : 0;
@@ -209,6 +210,248 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
   }
 }
 
+// ---- apply (MODE 0): register-blocked R targets per thread ---------------
+// 2-D: a CTA of 32 x (4*R) targets stages its (32+2H) x (4R+2H) neighbourhood
+// once in shared memory (zeros outside the domain: clip and collar apply paths
+// coincide, the collar lives in diag). A thread owns R targets in one column
+// (consecutive rows); every source node it loads (one 16-byte shared load) is
+// used by all R targets, each with its own exact half spans (tie band resolved
+// by the float predicate at the span ends only) and a broadcast weight read.
+// 3-D: the same blocking along axis 0 with the sources read through L1.
+constexpr int kR = 4;
+constexpr int kT2X = 32, kT2Y = 4;       // threads; targets per CTA: 32 x (4 kR)
+
+struct Span {
+  int xm, xp;   // half spans (-1: empty row)
+};
+
+template <int DIM>
+__device__ __forceinline__ Span row_span(bool live, int mlo, int mhi, int base2, const int64_t* ki,
+                                         const int* dpre, double h, double delta) {
+  Span sp{-1, -1};
+  if (!live || base2 > mhi) return sp;
+  auto inset = [&](int dx) {
+    const int m = base2 + dx * dx;
+    if (m == 0 || m > mhi) return m == 0 ? false : false;
+    if (m < mlo) return true;
+    int d[3] = {dpre[0], dpre[1], dpre[2]};
+    d[DIM - 1] = dx;
+    return point_in<DIM>(ki, d, h, delta);
+  };
+  const int X = static_cast<int>(floor(sqrt(static_cast<double>(mhi - base2))));
+  int xp = X, xm = X;
+  while (xp > 0 && !inset(xp)) --xp;
+  while (xm > 0 && !inset(-xm)) --xm;
+  if (base2 != 0 && !inset(0)) return sp;   // row does not reach the centre column
+  sp.xm = xm;
+  sp.xp = xp;
+  return sp;
+}
+
+template <int KIND, bool KW>
+__global__ void __launch_bounds__(kT2X * kT2Y) stencil2d_kernel(StArgs a) {
+  extern __shared__ double sm[];
+  const int H = a.H;
+  constexpr int TY = kT2Y * kR;                            // target rows per CTA
+  const int TW = kT2X + 2 * H, TH = TY + 2 * H;
+  double2* tile = reinterpret_cast<double2*>(sm);          // (u, kappa u) or (ux, uy); .y = 0 if unused
+  double* wt = sm + 2 * static_cast<size_t>(TW) * TH;
+  const int tid = threadIdx.y * kT2X + threadIdx.x;
+  for (int i = tid; i < a.tab_len; i += kT2X * kT2Y) wt[i] = a.tab[i];
+  const Geom& g = a.g;
+  const int64_t n = g.n;
+  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kT2X;
+  const int64_t y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * TY;
+  const int64_t nin_total = (g.in_end - g.in_begin) * g.stride0;
+  for (int i = tid; i < TW * TH; i += kT2X * kT2Y) {
+    const int ty = i / TW, tx = i % TW;
+    const int64_t gy = y0 - H + ty, gx = x0 - H + tx;
+    const bool in = gy >= 0 && gy < n && gx >= 0 && gx < n && gy >= g.in_begin && gy < g.in_end;
+    const int64_t k = (gy - g.in_begin) * n + gx;
+    double2 v = make_double2(0.0, 0.0);
+    if (in) {
+      if (KIND == 1) v = make_double2(__ldg(a.u + k), __ldg(a.u + nin_total + k));
+      else if (KW) v = a.pk[k];
+      else v.x = __ldg(a.u + k);
+    }
+    tile[i] = v;
+  }
+  __syncthreads();
+  const int64_t ix = x0 + threadIdx.x;
+  const int ty0 = threadIdx.y * kR;                        // my first target row within the CTA
+  const double h = g.h;
+  bool live[kR];
+  double delta[kR];
+  int mlo[kR], mhi[kR];
+  int Rw = 0;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int64_t iy = y0 + ty0 + r;
+    live[r] = ix < n && iy < g.row_end;
+    const int64_t ii = (iy - g.in_begin) * n + ix;
+    delta[r] = live[r] ? (a.delta ? a.delta[ii] : a.delta0) : 0.0;
+    const double e = delta[r] / h, e2 = e * e;
+    mlo[r] = live[r] ? static_cast<int>(ceil(e2 * (1.0 - 1e-12))) : 0;
+    mhi[r] = live[r] ? static_cast<int>(floor(e2 * (1.0 + 1e-12))) : -1;
+    if (live[r]) Rw = max(Rw, static_cast<int>(floor(e)) + 1);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) Rw = max(Rw, __shfl_xor_sync(0xffffffffu, Rw, o));
+  const int W1 = H + 1, W2 = 2 * H + 1;
+  double acc0[kR], acc1[kR];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) acc0[r] = acc1[r] = 0.0;
+  const int cx = threadIdx.x + H;
+  // source rows sy (relative to my first target row), covering every target's ball
+  for (int sy = -Rw; sy <= kR - 1 + Rw; ++sy) {
+    Span sp[kR];
+    int Xw = -1;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int dy = sy - r;
+      const int64_t ki[3] = {y0 + ty0 + r, ix, 0};
+      const int dpre[3] = {dy, 0, 0};
+      sp[r] = row_span<2>(live[r], mlo[r], mhi[r], dy * dy, ki, dpre, h, delta[r]);
+      Xw = max(Xw, max(sp[r].xm, sp[r].xp));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Xw = max(Xw, __shfl_xor_sync(0xffffffffu, Xw, o));
+    if (Xw < 0) continue;
+    const double2* trow = tile + (ty0 + sy + H) * TW + cx;
+    for (int dx = -Xw; dx <= Xw; ++dx) {
+      const double2 v = trow[dx];
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        const int dy = sy - r;
+        const bool in = dx >= -sp[r].xm && dx <= sp[r].xp && (dx != 0 || dy != 0);
+        if (KIND == 0) {
+          const double w = wt[(dy < 0 ? -dy : dy) * W1 + (dx < 0 ? -dx : dx)];
+          if (in) {
+            acc0[r] = fma(w, v.x, acc0[r]);
+            if (KW) acc1[r] = fma(w, v.y, acc1[r]);
+          }
+        } else {
+          const int t = (dy + H) * W2 + (dx + H);
+          const double mxx = wt[t], mxy = wt[W2 * W2 + t], myy = wt[2 * W2 * W2 + t];
+          if (in) {
+            acc0[r] = fma(mxx, v.x, fma(mxy, v.y, acc0[r]));
+            acc1[r] = fma(mxy, v.x, fma(myy, v.y, acc1[r]));
+          }
+        }
+      }
+    }
+  }
+  const int64_t nout = (g.row_end - g.row_begin) * n;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    if (!live[r]) continue;
+    const int64_t iy = y0 + ty0 + r;
+    const int64_t ii = (iy - g.in_begin) * n + ix;
+    const int64_t oi = (iy - g.row_begin) * n + ix;
+    const double2 c = tile[(ty0 + r + H) * TW + cx];
+    if (KIND == 0) {
+      const double X = KW ? fma(a.kappa[ii], acc0[r], acc1[r]) : acc0[r];
+      a.out[oi] = a.scale[oi] * (X - c.x * a.diag[oi]);
+    } else {
+      const double dxx = a.diag[oi], dxy = a.diag[nout + oi], dyy = a.diag[2 * nout + oi];
+      const double sc = a.scale[oi];
+      a.out[oi] = sc * (acc0[r] - (dxx * c.x + dxy * c.y));
+      a.out[nout + oi] = sc * (acc1[r] - (dxy * c.x + dyy * c.y));
+    }
+  }
+}
+
+// 3-D fractional apply: R targets along axis 0 per thread, sources via L1.
+template <bool KW>
+__global__ void __launch_bounds__(128) stencil3d_kernel(StArgs a) {
+  extern __shared__ double wt[];
+  for (int i = threadIdx.x; i < a.tab_len; i += blockDim.x) wt[i] = a.tab[i];
+  __syncthreads();
+  const Geom& g = a.g;
+  const int64_t n = g.n;
+  const int H = a.H, W1 = H + 1;
+  // threads: x fastest (32 lanes), then y (4 warps); CTA covers 32 x 4 x kR targets
+  const int64_t bx = (n + 31) / 32, by = (n + 3) / 4;
+  const int64_t b = blockIdx.x;
+  const int64_t ix = (b % bx) * 32 + (threadIdx.x & 31);
+  const int64_t iy = ((b / bx) % by) * 4 + (threadIdx.x >> 5);
+  const int64_t z0 = g.row_begin + (b / (bx * by)) * kR;
+  const double h = g.h;
+  const int64_t plane = n * n;
+  bool live[kR];
+  double delta[kR];
+  int mlo[kR], mhi[kR];
+  int Rw = 0;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int64_t iz = z0 + r;
+    live[r] = ix < n && iy < n && iz < g.row_end;
+    const int64_t ii = (iz - g.in_begin) * plane + iy * n + ix;
+    delta[r] = live[r] ? (a.delta ? a.delta[ii] : a.delta0) : 0.0;
+    const double e = delta[r] / h, e2 = e * e;
+    mlo[r] = live[r] ? static_cast<int>(ceil(e2 * (1.0 - 1e-12))) : 0;
+    mhi[r] = live[r] ? static_cast<int>(floor(e2 * (1.0 + 1e-12))) : -1;
+    if (live[r]) Rw = max(Rw, static_cast<int>(floor(e)) + 1);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) Rw = max(Rw, __shfl_xor_sync(0xffffffffu, Rw, o));
+  double acc0[kR], acc1[kR];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) acc0[r] = acc1[r] = 0.0;
+  for (int sz = -Rw; sz <= kR - 1 + Rw; ++sz) {
+    const int64_t gz = z0 + sz;
+    if (gz < 0 || gz >= n) continue;              // zero field outside the domain
+    for (int dy = -Rw; dy <= Rw; ++dy) {
+      const int64_t gy = iy + dy;
+      const bool rowok = gy >= 0 && gy < n;
+      Span sp[kR];
+      int Xw = -1;
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        const int dz = sz - r;
+        const int64_t ki[3] = {z0 + r, iy, ix};
+        const int dpre[3] = {dz, dy, 0};
+        sp[r] = row_span<3>(live[r] && rowok, mlo[r], mhi[r], dz * dz + dy * dy, ki, dpre, h, delta[r]);
+        Xw = max(Xw, max(sp[r].xm, sp[r].xp));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) Xw = max(Xw, __shfl_xor_sync(0xffffffffu, Xw, o));
+      if (Xw < 0) continue;
+      const int64_t rowoff = (gz - g.in_begin) * plane + (rowok ? gy : 0) * n;
+      const int ay = dy < 0 ? -dy : dy;
+      for (int dx = -Xw; dx <= Xw; ++dx) {
+        const int64_t gx = ix + dx;
+        double2 v = make_double2(0.0, 0.0);
+        if (rowok && gx >= 0 && gx < n) {
+          if (KW) v = a.pk[rowoff + gx];
+          else v.x = __ldg(a.u + rowoff + gx);
+        }
+        const int ax = dx < 0 ? -dx : dx;
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          const int dz = sz - r;
+          const bool in = dx >= -sp[r].xm && dx <= sp[r].xp && (dx != 0 || dy != 0 || dz != 0);
+          const double w = wt[((dz < 0 ? -dz : dz) * W1 + ay) * W1 + ax];
+          if (in) {
+            acc0[r] = fma(w, v.x, acc0[r]);
+            if (KW) acc1[r] = fma(w, v.y, acc1[r]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    if (!live[r]) continue;
+    const int64_t iz = z0 + r;
+    const int64_t ii = (iz - g.in_begin) * plane + iy * n + ix;
+    const int64_t oi = (iz - g.row_begin) * plane + iy * n + ix;
+    const double ui = KW ? a.pk[ii].x : a.u[ii];
+    const double X = KW ? fma(a.kappa[ii], acc0[r], acc1[r]) : acc0[r];
+    a.out[oi] = a.scale[oi] * (X - ui * a.diag[oi]);
+  }
+}
+
 __global__ void pack_kernel(const double* u, const double* kappa, int64_t n, double2* pk) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) {
@@ -229,12 +472,33 @@ template <int DIM, int KIND, int MODE, bool KW>
 void launch_t(const StArgs& a, cudaStream_t s, size_t smem) {
   const int64_t n = a.g.n;
   const int64_t rows = (a.g.row_end - a.g.row_begin) * (DIM == 3 ? n : 1);
-  dim3 grid(static_cast<unsigned>((n + kTX - 1) / kTX), static_cast<unsigned>((rows + kTY - 1) / kTY));
-  stencil_kernel<DIM, KIND, MODE, KW><<<grid, dim3(kTX, kTY), smem, s>>>(a);
+  const int64_t bx = (n + kTX - 1) / kTX, by = (rows + kTY - 1) / kTY;
+  stencil_kernel<DIM, KIND, MODE, KW><<<static_cast<unsigned>(bx * by), dim3(kTX, kTY), smem, s>>>(a);
+}
+
+size_t tile2d_bytes(const StArgs& a) {
+  return sizeof(double) * (2 * static_cast<size_t>(kT2X + 2 * a.H) * (kT2Y * kR + 2 * a.H)) +
+         sizeof(double) * a.tab_len;
 }
 
 void launch(const StArgs& a, cudaStream_t s, size_t smem) {
   const int dim = a.g.dim;
+  const int64_t n = a.g.n;
+  if (dim == 2 && a.mode == 0) {
+    dim3 grid(static_cast<unsigned>((n + kT2X - 1) / kT2X),
+              static_cast<unsigned>((a.g.row_end - a.g.row_begin + kT2Y * kR - 1) / (kT2Y * kR)));
+    const size_t sb = tile2d_bytes(a);
+    if (a.kind == 1) stencil2d_kernel<1, false><<<grid, dim3(kT2X, kT2Y), sb, s>>>(a);
+    else if (a.kw) stencil2d_kernel<0, true><<<grid, dim3(kT2X, kT2Y), sb, s>>>(a);
+    else stencil2d_kernel<0, false><<<grid, dim3(kT2X, kT2Y), sb, s>>>(a);
+    return;
+  }
+  if (dim == 3 && a.mode == 0) {
+    const int64_t blocks = ((n + 31) / 32) * ((n + 3) / 4) * ((a.g.row_end - a.g.row_begin + kR - 1) / kR);
+    if (a.kw) stencil3d_kernel<true><<<static_cast<unsigned>(blocks), 128, smem, s>>>(a);
+    else stencil3d_kernel<false><<<static_cast<unsigned>(blocks), 128, smem, s>>>(a);
+    return;
+  }
   if (a.kind == 1) {
     if (a.mode == 0) launch_t<2, 1, 0, false>(a, s, smem);
     else launch_t<2, 1, 1, false>(a, s, smem);
@@ -326,6 +590,9 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * P.n_out * (peri ? 3 : 1)));
   if (frac && d.kappa) NLG_CUDA(cudaMalloc(&S->pack, sizeof(double2) * P.n_in));
   P.st_state = S;
+  NLG_CUDA(cudaFuncSetAttribute(stencil2d_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  NLG_CUDA(cudaFuncSetAttribute(stencil2d_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  NLG_CUDA(cudaFuncSetAttribute(stencil2d_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   // diag: MODE 1 over the same sets and tables
   const StArgs a = make_args(P, *S, 1, nullptr, S->diag);
   launch(a, P.stream, S->tab_bytes);
