@@ -210,58 +210,73 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
   }
 }
 
-// ---- apply (MODE 0): register-blocked R targets per thread ---------------
-// 2-D: a CTA of 32 x (4*R) targets stages its (32+2H) x (4R+2H) neighbourhood
-// once in shared memory (zeros outside the domain: clip and collar apply paths
-// coincide, the collar lives in diag). A thread owns R targets in one column
-// (consecutive rows); every source node it loads (one 16-byte shared load) is
-// used by all R targets, each with its own exact half spans (tie band resolved
-// by the float predicate at the span ends only) and a broadcast weight read.
-// 3-D: the same blocking along axis 0 with the sources read through L1.
-constexpr int kR = 4;
-constexpr int kT2X = 32, kT2Y = 4;       // threads; targets per CTA: 32 x (4 kR)
+// ---- apply (MODE 0) ---------------------------------------------------------
+// One thread per target; the thread walks its own ball row by row with exact
+// half spans (integer bound from a single-precision sqrt with an integer fix-
+// up; the tie band around (delta/h)^2 is resolved by the float predicate at the
+// span ends only), so the pair loop is value-load, weight-load, FMA(s) with no
+// per-pair predicate. 2-D: the CTA's (32+2H) x (8+2H) neighbourhood is staged
+// in shared memory (zeros outside the domain: clip and collar apply paths
+// coincide, the collar lives in diag). 3-D: sources through L1.
+constexpr int kT2X = 32, kT2Y = 8;
 
-struct Span {
-  int xm, xp;   // half spans (-1: empty row)
-};
+__device__ __forceinline__ int isqrt_floor(int m) {
+  if (m < 0) return -1;
+  int x = static_cast<int>(sqrtf(static_cast<float>(m)));
+  while (x * x > m) --x;
+  while ((x + 1) * (x + 1) <= m) ++x;
+  return x;
+}
 
 template <int DIM>
-__device__ __forceinline__ Span row_span(bool live, int mlo, int mhi, int base2, const int64_t* ki,
-                                         const int* dpre, double h, double delta) {
-  Span sp{-1, -1};
-  if (!live || base2 > mhi) return sp;
-  auto inset = [&](int dx) {
-    const int m = base2 + dx * dx;
-    if (m == 0 || m > mhi) return m == 0 ? false : false;
+struct Ball {
+  int mlo, mhi;
+  int64_t ki[3];
+  double h, delta;
+  __device__ __forceinline__ bool in(const int* d) const {
+    int m = 0;
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) m += d[j] * d[j];
+    if (m == 0 || m > mhi) return false;
     if (m < mlo) return true;
-    int d[3] = {dpre[0], dpre[1], dpre[2]};
-    d[DIM - 1] = dx;
     return point_in<DIM>(ki, d, h, delta);
-  };
-  const int X = static_cast<int>(floor(sqrt(static_cast<double>(mhi - base2))));
-  int xp = X, xm = X;
-  while (xp > 0 && !inset(xp)) --xp;
-  while (xm > 0 && !inset(-xm)) --xm;
-  if (base2 != 0 && !inset(0)) return sp;   // row does not reach the centre column
-  sp.xm = xm;
-  sp.xp = xp;
-  return sp;
-}
+  }
+  // exact half spans of the row with the leading offsets d[0..DIM-2]; false if empty
+  __device__ __forceinline__ bool span(int* d, int& xm, int& xp) const {
+    int base2 = 0;
+#pragma unroll
+    for (int j = 0; j < DIM - 1; ++j) base2 += d[j] * d[j];
+    const int X = isqrt_floor(mhi - base2);
+    if (X < 0) return false;
+    xp = X;
+    xm = X;
+    if (base2 + X * X >= mlo) {                         // ends sit in the tie band
+      d[DIM - 1] = xp;
+      while (xp > 0 && !in(d)) { --xp; d[DIM - 1] = xp; }
+      d[DIM - 1] = -xm;
+      while (xm > 0 && !in(d)) { --xm; d[DIM - 1] = -xm; }
+    }
+    if (base2 != 0) {
+      d[DIM - 1] = 0;
+      if (!in(d)) return false;
+    }
+    return true;
+  }
+};
 
 template <int KIND, bool KW>
 __global__ void __launch_bounds__(kT2X * kT2Y) stencil2d_kernel(StArgs a) {
   extern __shared__ double sm[];
   const int H = a.H;
-  constexpr int TY = kT2Y * kR;                            // target rows per CTA
-  const int TW = kT2X + 2 * H, TH = TY + 2 * H;
-  double2* tile = reinterpret_cast<double2*>(sm);          // (u, kappa u) or (ux, uy); .y = 0 if unused
+  const int TW = kT2X + 2 * H, TH = kT2Y + 2 * H;
+  double2* tile = reinterpret_cast<double2*>(sm);          // (u, kappa u) or (ux, uy)
   double* wt = sm + 2 * static_cast<size_t>(TW) * TH;
   const int tid = threadIdx.y * kT2X + threadIdx.x;
   for (int i = tid; i < a.tab_len; i += kT2X * kT2Y) wt[i] = a.tab[i];
   const Geom& g = a.g;
   const int64_t n = g.n;
   const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kT2X;
-  const int64_t y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * TY;
+  const int64_t y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * kT2Y;
   const int64_t nin_total = (g.in_end - g.in_begin) * g.stride0;
   for (int i = tid; i < TW * TH; i += kT2X * kT2Y) {
     const int ty = i / TW, tx = i % TW;
@@ -277,91 +292,70 @@ __global__ void __launch_bounds__(kT2X * kT2Y) stencil2d_kernel(StArgs a) {
     tile[i] = v;
   }
   __syncthreads();
-  const int64_t ix = x0 + threadIdx.x;
-  const int ty0 = threadIdx.y * kR;                        // my first target row within the CTA
-  const double h = g.h;
-  bool live[kR];
-  double delta[kR];
-  int mlo[kR], mhi[kR];
-  int Rw = 0;
-#pragma unroll
-  for (int r = 0; r < kR; ++r) {
-    const int64_t iy = y0 + ty0 + r;
-    live[r] = ix < n && iy < g.row_end;
-    const int64_t ii = (iy - g.in_begin) * n + ix;
-    delta[r] = live[r] ? (a.delta ? a.delta[ii] : a.delta0) : 0.0;
-    const double e = delta[r] / h, e2 = e * e;
-    mlo[r] = live[r] ? static_cast<int>(ceil(e2 * (1.0 - 1e-12))) : 0;
-    mhi[r] = live[r] ? static_cast<int>(floor(e2 * (1.0 + 1e-12))) : -1;
-    if (live[r]) Rw = max(Rw, static_cast<int>(floor(e)) + 1);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) Rw = max(Rw, __shfl_xor_sync(0xffffffffu, Rw, o));
+  const int64_t ix = x0 + threadIdx.x, iy = y0 + threadIdx.y;
+  if (ix >= n || iy >= g.row_end) return;
+  const int64_t ii = (iy - g.in_begin) * n + ix;
+  Ball<2> B;
+  B.h = g.h;
+  B.delta = a.delta ? a.delta[ii] : a.delta0;
+  B.ki[0] = iy;
+  B.ki[1] = ix;
+  const double e = B.delta / B.h, e2 = e * e;
+  B.mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
+  B.mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+  const int Ry = isqrt_floor(B.mhi);
   const int W1 = H + 1, W2 = 2 * H + 1;
-  double acc0[kR], acc1[kR];
-#pragma unroll
-  for (int r = 0; r < kR; ++r) acc0[r] = acc1[r] = 0.0;
-  const int cx = threadIdx.x + H;
-  // source rows sy (relative to my first target row), covering every target's ball
-  for (int sy = -Rw; sy <= kR - 1 + Rw; ++sy) {
-    Span sp[kR];
-    int Xw = -1;
-#pragma unroll
-    for (int r = 0; r < kR; ++r) {
-      const int dy = sy - r;
-      const int64_t ki[3] = {y0 + ty0 + r, ix, 0};
-      const int dpre[3] = {dy, 0, 0};
-      sp[r] = row_span<2>(live[r], mlo[r], mhi[r], dy * dy, ki, dpre, h, delta[r]);
-      Xw = max(Xw, max(sp[r].xm, sp[r].xp));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) Xw = max(Xw, __shfl_xor_sync(0xffffffffu, Xw, o));
-    if (Xw < 0) continue;
-    const double2* trow = tile + (ty0 + sy + H) * TW + cx;
-    for (int dx = -Xw; dx <= Xw; ++dx) {
-      const double2 v = trow[dx];
-#pragma unroll
-      for (int r = 0; r < kR; ++r) {
-        const int dy = sy - r;
-        const bool in = dx >= -sp[r].xm && dx <= sp[r].xp && (dx != 0 || dy != 0);
-        if (KIND == 0) {
-          const double w = wt[(dy < 0 ? -dy : dy) * W1 + (dx < 0 ? -dx : dx)];
-          if (in) {
-            acc0[r] = fma(w, v.x, acc0[r]);
-            if (KW) acc1[r] = fma(w, v.y, acc1[r]);
-          }
-        } else {
-          const int t = (dy + H) * W2 + (dx + H);
-          const double mxx = wt[t], mxy = wt[W2 * W2 + t], myy = wt[2 * W2 * W2 + t];
-          if (in) {
-            acc0[r] = fma(mxx, v.x, fma(mxy, v.y, acc0[r]));
-            acc1[r] = fma(mxy, v.x, fma(myy, v.y, acc1[r]));
-          }
-        }
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  const int cx = threadIdx.x + H, cy = threadIdx.y + H;
+  for (int dy = -Ry; dy <= Ry; ++dy) {
+    int d[2] = {dy, 0};
+    int xm, xp;
+    if (!B.span(d, xm, xp)) continue;
+    const double2* trow = tile + (cy + dy) * TW + cx;
+    const int ay = dy < 0 ? -dy : dy;
+    if (KIND == 0) {
+      const double* wrow = wt + ay * W1;
+      // left half (dx = -xm .. -1) and right half (dx = 0 .. xp), self skipped
+      for (int k = 1; k <= xm; ++k) {
+        const double w = wrow[k];
+        const double2 v = trow[-k];
+        acc0 = fma(w, v.x, acc0);
+        if (KW) acc1 = fma(w, v.y, acc1);
+      }
+      for (int k = dy == 0 ? 1 : 0; k <= xp; ++k) {
+        const double w = wrow[k];
+        const double2 v = trow[k];
+        acc2 = fma(w, v.x, acc2);
+        if (KW) acc3 = fma(w, v.y, acc3);
+      }
+    } else {
+      const int t0 = (dy + H) * W2 + H;
+      for (int dx = -xm; dx <= xp; ++dx) {
+        if (dx == 0 && dy == 0) continue;
+        const int t = t0 + dx;
+        const double mxx = wt[t], mxy = wt[W2 * W2 + t], myy = wt[2 * W2 * W2 + t];
+        const double2 v = trow[dx];
+        acc0 = fma(mxx, v.x, fma(mxy, v.y, acc0));
+        acc1 = fma(mxy, v.x, fma(myy, v.y, acc1));
       }
     }
   }
   const int64_t nout = (g.row_end - g.row_begin) * n;
-#pragma unroll
-  for (int r = 0; r < kR; ++r) {
-    if (!live[r]) continue;
-    const int64_t iy = y0 + ty0 + r;
-    const int64_t ii = (iy - g.in_begin) * n + ix;
-    const int64_t oi = (iy - g.row_begin) * n + ix;
-    const double2 c = tile[(ty0 + r + H) * TW + cx];
-    if (KIND == 0) {
-      const double X = KW ? fma(a.kappa[ii], acc0[r], acc1[r]) : acc0[r];
-      a.out[oi] = a.scale[oi] * (X - c.x * a.diag[oi]);
-    } else {
-      const double dxx = a.diag[oi], dxy = a.diag[nout + oi], dyy = a.diag[2 * nout + oi];
-      const double sc = a.scale[oi];
-      a.out[oi] = sc * (acc0[r] - (dxx * c.x + dxy * c.y));
-      a.out[nout + oi] = sc * (acc1[r] - (dxy * c.x + dyy * c.y));
-    }
+  const int64_t oi = (iy - g.row_begin) * n + ix;
+  const double2 c = tile[cy * TW + cx];
+  if (KIND == 0) {
+    const double A = acc0 + acc2, Bk = acc1 + acc3;
+    const double X = KW ? fma(a.kappa[ii], A, Bk) : A;
+    a.out[oi] = a.scale[oi] * (X - c.x * a.diag[oi]);
+  } else {
+    const double dxx = a.diag[oi], dxy = a.diag[nout + oi], dyy = a.diag[2 * nout + oi];
+    const double sc = a.scale[oi];
+    a.out[oi] = sc * (acc0 - (dxx * c.x + dxy * c.y));
+    a.out[nout + oi] = sc * (acc1 - (dxy * c.x + dyy * c.y));
   }
 }
 
-// 3-D fractional apply: R targets along axis 0 per thread, sources via L1.
+// 3-D fractional apply, one thread per target, sources through L1.
 template <bool KW>
 __global__ void __launch_bounds__(128) stencil3d_kernel(StArgs a) {
   extern __shared__ double wt[];
@@ -370,86 +364,67 @@ __global__ void __launch_bounds__(128) stencil3d_kernel(StArgs a) {
   const Geom& g = a.g;
   const int64_t n = g.n;
   const int H = a.H, W1 = H + 1;
-  // threads: x fastest (32 lanes), then y (4 warps); CTA covers 32 x 4 x kR targets
   const int64_t bx = (n + 31) / 32, by = (n + 3) / 4;
   const int64_t b = blockIdx.x;
   const int64_t ix = (b % bx) * 32 + (threadIdx.x & 31);
   const int64_t iy = ((b / bx) % by) * 4 + (threadIdx.x >> 5);
-  const int64_t z0 = g.row_begin + (b / (bx * by)) * kR;
-  const double h = g.h;
+  const int64_t iz = g.row_begin + b / (bx * by);
+  if (ix >= n || iy >= n || iz >= g.row_end) return;
   const int64_t plane = n * n;
-  bool live[kR];
-  double delta[kR];
-  int mlo[kR], mhi[kR];
-  int Rw = 0;
-#pragma unroll
-  for (int r = 0; r < kR; ++r) {
-    const int64_t iz = z0 + r;
-    live[r] = ix < n && iy < n && iz < g.row_end;
-    const int64_t ii = (iz - g.in_begin) * plane + iy * n + ix;
-    delta[r] = live[r] ? (a.delta ? a.delta[ii] : a.delta0) : 0.0;
-    const double e = delta[r] / h, e2 = e * e;
-    mlo[r] = live[r] ? static_cast<int>(ceil(e2 * (1.0 - 1e-12))) : 0;
-    mhi[r] = live[r] ? static_cast<int>(floor(e2 * (1.0 + 1e-12))) : -1;
-    if (live[r]) Rw = max(Rw, static_cast<int>(floor(e)) + 1);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) Rw = max(Rw, __shfl_xor_sync(0xffffffffu, Rw, o));
-  double acc0[kR], acc1[kR];
-#pragma unroll
-  for (int r = 0; r < kR; ++r) acc0[r] = acc1[r] = 0.0;
-  for (int sz = -Rw; sz <= kR - 1 + Rw; ++sz) {
-    const int64_t gz = z0 + sz;
-    if (gz < 0 || gz >= n) continue;              // zero field outside the domain
-    for (int dy = -Rw; dy <= Rw; ++dy) {
+  const int64_t ii = (iz - g.in_begin) * plane + iy * n + ix;
+  Ball<3> B;
+  B.h = g.h;
+  B.delta = a.delta ? a.delta[ii] : a.delta0;
+  B.ki[0] = iz;
+  B.ki[1] = iy;
+  B.ki[2] = ix;
+  const double e = B.delta / B.h, e2 = e * e;
+  B.mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
+  B.mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+  const int Rz = isqrt_floor(B.mhi);
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  for (int dz = -Rz; dz <= Rz; ++dz) {
+    const int64_t gz = iz + dz;
+    if (gz < 0 || gz >= n) continue;
+    const int Ry = isqrt_floor(B.mhi - dz * dz);
+    const int az = dz < 0 ? -dz : dz;
+    for (int dy = -Ry; dy <= Ry; ++dy) {
       const int64_t gy = iy + dy;
-      const bool rowok = gy >= 0 && gy < n;
-      Span sp[kR];
-      int Xw = -1;
-#pragma unroll
-      for (int r = 0; r < kR; ++r) {
-        const int dz = sz - r;
-        const int64_t ki[3] = {z0 + r, iy, ix};
-        const int dpre[3] = {dz, dy, 0};
-        sp[r] = row_span<3>(live[r] && rowok, mlo[r], mhi[r], dz * dz + dy * dy, ki, dpre, h, delta[r]);
-        Xw = max(Xw, max(sp[r].xm, sp[r].xp));
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) Xw = max(Xw, __shfl_xor_sync(0xffffffffu, Xw, o));
-      if (Xw < 0) continue;
-      const int64_t rowoff = (gz - g.in_begin) * plane + (rowok ? gy : 0) * n;
-      const int ay = dy < 0 ? -dy : dy;
-      for (int dx = -Xw; dx <= Xw; ++dx) {
-        const int64_t gx = ix + dx;
-        double2 v = make_double2(0.0, 0.0);
-        if (rowok && gx >= 0 && gx < n) {
-          if (KW) v = a.pk[rowoff + gx];
-          else v.x = __ldg(a.u + rowoff + gx);
+      if (gy < 0 || gy >= n) continue;
+      int d[3] = {dz, dy, 0};
+      int xm, xp;
+      if (!B.span(d, xm, xp)) continue;
+      if (xm > ix) xm = static_cast<int>(ix);                     // clip to the domain (zero field)
+      if (xp > n - 1 - ix) xp = static_cast<int>(n - 1 - ix);
+      const int64_t row = (gz - g.in_begin) * plane + gy * n + ix;
+      const double* wrow = wt + (az * W1 + (dy < 0 ? -dy : dy)) * W1;
+      for (int k = 1; k <= xm; ++k) {
+        const double w = wrow[k];
+        if (KW) {
+          const double2 v = a.pk[row - k];
+          acc0 = fma(w, v.x, acc0);
+          acc1 = fma(w, v.y, acc1);
+        } else {
+          acc0 = fma(w, __ldg(a.u + row - k), acc0);
         }
-        const int ax = dx < 0 ? -dx : dx;
-#pragma unroll
-        for (int r = 0; r < kR; ++r) {
-          const int dz = sz - r;
-          const bool in = dx >= -sp[r].xm && dx <= sp[r].xp && (dx != 0 || dy != 0 || dz != 0);
-          const double w = wt[((dz < 0 ? -dz : dz) * W1 + ay) * W1 + ax];
-          if (in) {
-            acc0[r] = fma(w, v.x, acc0[r]);
-            if (KW) acc1[r] = fma(w, v.y, acc1[r]);
-          }
+      }
+      for (int k = (dz == 0 && dy == 0) ? 1 : 0; k <= xp; ++k) {
+        const double w = wrow[k];
+        if (KW) {
+          const double2 v = a.pk[row + k];
+          acc2 = fma(w, v.x, acc2);
+          acc3 = fma(w, v.y, acc3);
+        } else {
+          acc2 = fma(w, __ldg(a.u + row + k), acc2);
         }
       }
     }
   }
-#pragma unroll
-  for (int r = 0; r < kR; ++r) {
-    if (!live[r]) continue;
-    const int64_t iz = z0 + r;
-    const int64_t ii = (iz - g.in_begin) * plane + iy * n + ix;
-    const int64_t oi = (iz - g.row_begin) * plane + iy * n + ix;
-    const double ui = KW ? a.pk[ii].x : a.u[ii];
-    const double X = KW ? fma(a.kappa[ii], acc0[r], acc1[r]) : acc0[r];
-    a.out[oi] = a.scale[oi] * (X - ui * a.diag[oi]);
-  }
+  const int64_t oi = (iz - g.row_begin) * plane + iy * n + ix;
+  const double ui = KW ? a.pk[ii].x : a.u[ii];
+  const double A = acc0 + acc2, Bk = acc1 + acc3;
+  const double X = KW ? fma(a.kappa[ii], A, Bk) : A;
+  a.out[oi] = a.scale[oi] * (X - ui * a.diag[oi]);
 }
 
 __global__ void pack_kernel(const double* u, const double* kappa, int64_t n, double2* pk) {
@@ -477,7 +452,7 @@ void launch_t(const StArgs& a, cudaStream_t s, size_t smem) {
 }
 
 size_t tile2d_bytes(const StArgs& a) {
-  return sizeof(double) * (2 * static_cast<size_t>(kT2X + 2 * a.H) * (kT2Y * kR + 2 * a.H)) +
+  return sizeof(double) * (2 * static_cast<size_t>(kT2X + 2 * a.H) * (kT2Y + 2 * a.H)) +
          sizeof(double) * a.tab_len;
 }
 
@@ -486,7 +461,7 @@ void launch(const StArgs& a, cudaStream_t s, size_t smem) {
   const int64_t n = a.g.n;
   if (dim == 2 && a.mode == 0) {
     dim3 grid(static_cast<unsigned>((n + kT2X - 1) / kT2X),
-              static_cast<unsigned>((a.g.row_end - a.g.row_begin + kT2Y * kR - 1) / (kT2Y * kR)));
+              static_cast<unsigned>((a.g.row_end - a.g.row_begin + kT2Y - 1) / kT2Y));
     const size_t sb = tile2d_bytes(a);
     if (a.kind == 1) stencil2d_kernel<1, false><<<grid, dim3(kT2X, kT2Y), sb, s>>>(a);
     else if (a.kw) stencil2d_kernel<0, true><<<grid, dim3(kT2X, kT2Y), sb, s>>>(a);
@@ -494,7 +469,7 @@ void launch(const StArgs& a, cudaStream_t s, size_t smem) {
     return;
   }
   if (dim == 3 && a.mode == 0) {
-    const int64_t blocks = ((n + 31) / 32) * ((n + 3) / 4) * ((a.g.row_end - a.g.row_begin + kR - 1) / kR);
+    const int64_t blocks = ((n + 31) / 32) * ((n + 3) / 4) * (a.g.row_end - a.g.row_begin);
     if (a.kw) stencil3d_kernel<true><<<static_cast<unsigned>(blocks), 128, smem, s>>>(a);
     else stencil3d_kernel<false><<<static_cast<unsigned>(blocks), 128, smem, s>>>(a);
     return;
