@@ -222,7 +222,8 @@ nlg_status nlg_plan_create(const nlg_desc* desc, nlg_plan** out) {
       P.fast_method = 1;
       spans_setup(P);
     } else if (P.family == NLG_FRACTIONAL && g.dim == 1) {
-      expsum_setup(P, d);
+      expsum_setup(P, d);                       // wide horizons: exponential-sum scans
+      if (P.fast_method == 0) stencil_setup(P, d);   // narrow ones: 1-D stencil
     } else if ((P.family == NLG_FRACTIONAL || P.family == NLG_PERIDYNAMIC) && g.dim >= 2) {
       stencil_setup(P, d);
     } else {

@@ -79,15 +79,20 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
   const Geom& g = a.g;
   const int64_t n = g.n;
   // target: x along threadIdx.x; remaining axes from blockIdx / threadIdx.y
-  const int64_t bx = (n + kTX - 1) / kTX;
+  const int64_t nx = DIM == 1 ? (g.row_end - g.row_begin) : n;   // targets along the fastest axis
+  const int64_t bx = (nx + kTX - 1) / kTX;
   const int64_t ix = (static_cast<int64_t>(blockIdx.x) % bx) * kTX + threadIdx.x;
-  const int64_t rowsOut = (g.row_end - g.row_begin) * (DIM == 3 ? n : 1);
+  const int64_t rowsOut = DIM == 1 ? 1 : (g.row_end - g.row_begin) * (DIM == 3 ? n : 1);
   const int64_t r = (static_cast<int64_t>(blockIdx.x) / bx) * kTY + threadIdx.y;   // output row (axis0 [, axis1])
-  const bool live = ix < n && r < rowsOut;
+  const bool live = ix < nx && r < rowsOut;
   int64_t ki[3] = {0, 0, 0};
-  ki[DIM - 1] = live ? ix : 0;
-  if (DIM == 2) ki[0] = g.row_begin + (live ? r : 0);
-  else {
+  if (DIM == 1) {
+    ki[0] = g.row_begin + (live ? ix : 0);
+  } else if (DIM == 2) {
+    ki[1] = live ? ix : 0;
+    ki[0] = g.row_begin + (live ? r : 0);
+  } else {
+    ki[2] = live ? ix : 0;
     ki[0] = g.row_begin + (live ? r / n : 0);
     ki[1] = live ? r % n : 0;
   }
@@ -117,7 +122,7 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
   int d[3] = {0, 0, 0};
   const int zlo = DIM == 3 ? -Rw : 0, zhi = DIM == 3 ? Rw : 0;
   for (int dz = zlo; dz <= zhi; ++dz) {
-    for (int dy = -Rw; dy <= Rw; ++dy) {
+    for (int dy = (DIM == 1 ? 0 : -Rw); dy <= (DIM == 1 ? 0 : Rw); ++dy) {
       const int base2 = (DIM == 3 ? dz * dz : 0) + dy * dy;
       // this lane's half span on the row (covering the tie band), warp max
       int X = -1;
@@ -126,22 +131,24 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) Xw = max(Xw, __shfl_xor_sync(0xffffffffu, Xw, o));
       if (Xw < 0) continue;
-      int64_t krow[3];
+      int64_t krow[3] = {0, 0, 0};
       if (DIM == 2) {
         krow[0] = ki[0] + dy;
-        krow[1] = 0;
-      } else {
+      } else if (DIM == 3) {
         krow[0] = ki[0] + dz;
         krow[1] = ki[1] + dy;
       }
-      const bool row_in = DIM == 2 ? (krow[0] >= 0 && krow[0] < n) : (krow[0] >= 0 && krow[0] < n && krow[1] >= 0 && krow[1] < n);
-      const int64_t rowoff = DIM == 2 ? (krow[0] - g.in_begin) * n : ((krow[0] - g.in_begin) * n + krow[1]) * n;
+      const bool row_in = DIM == 1 ? true
+                          : DIM == 2 ? (krow[0] >= 0 && krow[0] < n)
+                                     : (krow[0] >= 0 && krow[0] < n && krow[1] >= 0 && krow[1] < n);
+      const int64_t rowoff = DIM == 1 ? -g.in_begin
+                             : DIM == 2 ? (krow[0] - g.in_begin) * n : ((krow[0] - g.in_begin) * n + krow[1]) * n;
       const int ay = dy < 0 ? -dy : dy, az = dz < 0 ? -dz : dz;
       for (int dx = -Xw; dx <= Xw; ++dx) {
         const int m = base2 + dx * dx;
         bool in = live && m > 0 && m <= mhi && (dx >= -X && dx <= X);
         if (in && m >= mlo) {
-          if (DIM == 2) { d[0] = dy; d[1] = dx; } else { d[0] = dz; d[1] = dy; d[2] = dx; }
+          if (DIM == 1) { d[0] = dx; } else if (DIM == 2) { d[0] = dy; d[1] = dx; } else { d[0] = dz; d[1] = dy; d[2] = dx; }
           in = point_in<DIM>(ki, d, h, delta);
         }
         const int64_t kx = ki[DIM - 1] + dx;
@@ -149,7 +156,7 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
         if (!in) continue;
         if (KIND == 0) {
           const int ax = dx < 0 ? -dx : dx;
-          const double w = DIM == 2 ? stab[ay * W1 + ax] : stab[(az * W1 + ay) * W1 + ax];
+          const double w = DIM == 1 ? stab[ax] : DIM == 2 ? stab[ay * W1 + ax] : stab[(az * W1 + ay) * W1 + ax];
           if (MODE == 0) {
             if (!dom) continue;
             const int64_t kk = rowoff + kx;
@@ -355,6 +362,67 @@ __global__ void __launch_bounds__(kT2X * kT2Y) stencil2d_kernel(StArgs a) {
   }
 }
 
+// 1-D fractional apply (horizons below the scan threshold, e.g. cfg0): one
+// thread per target over a shared-memory tile of the CTA's neighbourhood.
+constexpr int k1T = 256;
+
+template <bool KW>
+__global__ void __launch_bounds__(k1T) stencil1d_kernel(StArgs a) {
+  extern __shared__ double sm[];
+  const int H = a.H;
+  const int TW = k1T + 2 * H;
+  double2* tile = reinterpret_cast<double2*>(sm);
+  double* wt = sm + 2 * static_cast<size_t>(TW);
+  for (int i = threadIdx.x; i < a.tab_len; i += k1T) wt[i] = a.tab[i];
+  const Geom& g = a.g;
+  const int64_t n = g.n;
+  const int64_t x0 = g.row_begin + static_cast<int64_t>(blockIdx.x) * k1T;
+  for (int i = threadIdx.x; i < TW; i += k1T) {
+    const int64_t gx = x0 - H + i;
+    const bool in = gx >= 0 && gx < n && gx >= g.in_begin && gx < g.in_end;
+    const int64_t k = gx - g.in_begin;
+    double2 v = make_double2(0.0, 0.0);
+    if (in) {
+      if (KW) v = a.pk[k];
+      else v.x = __ldg(a.u + k);
+    }
+    tile[i] = v;
+  }
+  __syncthreads();
+  const int64_t ix = x0 + threadIdx.x;
+  if (ix >= g.row_end) return;
+  const int64_t ii = ix - g.in_begin;
+  Ball<1> B;
+  B.h = g.h;
+  B.delta = a.delta ? a.delta[ii] : a.delta0;
+  B.ki[0] = ix;
+  const double e = B.delta / B.h, e2 = e * e;
+  B.mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
+  B.mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+  int d[1] = {0};
+  int xm, xp;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  const double2* trow = tile + threadIdx.x + H;
+  if (B.span(d, xm, xp)) {
+    for (int k = 1; k <= xm; ++k) {
+      const double w = wt[k];
+      const double2 v = trow[-k];
+      acc0 = fma(w, v.x, acc0);
+      if (KW) acc1 = fma(w, v.y, acc1);
+    }
+    for (int k = 1; k <= xp; ++k) {
+      const double w = wt[k];
+      const double2 v = trow[k];
+      acc2 = fma(w, v.x, acc2);
+      if (KW) acc3 = fma(w, v.y, acc3);
+    }
+  }
+  const int64_t oi = ix - g.row_begin;
+  const double A = acc0 + acc2, Bk = acc1 + acc3;
+  const double X = KW ? fma(a.kappa[ii], A, Bk) : A;
+  a.out[oi] = a.scale[oi] * (X - trow[0].x * a.diag[oi]);
+}
+
 // 3-D fractional apply, one thread per target, sources through L1.
 template <bool KW>
 __global__ void __launch_bounds__(128) stencil3d_kernel(StArgs a) {
@@ -446,8 +514,9 @@ T* upload_vec(const std::vector<T>& v) {
 template <int DIM, int KIND, int MODE, bool KW>
 void launch_t(const StArgs& a, cudaStream_t s, size_t smem) {
   const int64_t n = a.g.n;
-  const int64_t rows = (a.g.row_end - a.g.row_begin) * (DIM == 3 ? n : 1);
-  const int64_t bx = (n + kTX - 1) / kTX, by = (rows + kTY - 1) / kTY;
+  const int64_t nx = DIM == 1 ? (a.g.row_end - a.g.row_begin) : n;
+  const int64_t rows = DIM == 1 ? 1 : (a.g.row_end - a.g.row_begin) * (DIM == 3 ? n : 1);
+  const int64_t bx = (nx + kTX - 1) / kTX, by = (rows + kTY - 1) / kTY;
   stencil_kernel<DIM, KIND, MODE, KW><<<static_cast<unsigned>(bx * by), dim3(kTX, kTY), smem, s>>>(a);
 }
 
@@ -459,6 +528,17 @@ size_t tile2d_bytes(const StArgs& a) {
 void launch(const StArgs& a, cudaStream_t s, size_t smem) {
   const int dim = a.g.dim;
   const int64_t n = a.g.n;
+  if (dim == 1) {
+    if (a.mode == 0) {
+      const unsigned grid = static_cast<unsigned>((a.g.row_end - a.g.row_begin + k1T - 1) / k1T);
+      const size_t sb = sizeof(double) * (2 * static_cast<size_t>(k1T + 2 * a.H) + a.tab_len);
+      if (a.kw) stencil1d_kernel<true><<<grid, k1T, sb, s>>>(a);
+      else stencil1d_kernel<false><<<grid, k1T, sb, s>>>(a);
+    } else {
+      if (a.kw) launch_t<1, 0, 1, true>(a, s, smem); else launch_t<1, 0, 1, false>(a, s, smem);
+    }
+    return;
+  }
   if (dim == 2 && a.mode == 0) {
     dim3 grid(static_cast<unsigned>((n + kT2X - 1) / kT2X),
               static_cast<unsigned>((a.g.row_end - a.g.row_begin + kT2Y - 1) / kT2Y));
@@ -515,24 +595,27 @@ StArgs make_args(const Plan& P, const StencilState& S, int mode, const double* u
 // horizon of at most 16 cells (tables in shared memory).
 void stencil_setup(Plan& P, const nlg_desc& d) {
   const Geom& g = P.geom;
-  if (g.dim < 2) return;
   const bool frac = d.family == NLG_FRACTIONAL, peri = d.family == NLG_PERIDYNAMIC;
   if (!frac && !(peri && g.dim == 2)) return;
   const int H = static_cast<int>(std::floor(P.delta_max / g.h)) + 2;
-  if (H > 16) return;
+  if (g.dim >= 2 && H > 16) return;
+  if (g.dim == 1 && H > 2048) return;
   auto* S = new StencilState();
   S->dim = g.dim;
   S->kind = peri ? 1 : 0;
   S->H = H;
   if (frac) {
     const int W1 = H + 1;
-    std::vector<double> w(static_cast<size_t>(g.dim == 2 ? W1 * W1 : W1 * W1 * W1), 0.0);
+    const size_t tl = g.dim == 1 ? W1 : g.dim == 2 ? W1 * W1 : W1 * W1 * W1;
+    std::vector<double> w(tl, 0.0);
     for (int az = 0; az <= (g.dim == 3 ? H : 0); ++az)
-      for (int ay = 0; ay <= H; ++ay)
+      for (int ay = 0; ay <= (g.dim >= 2 ? H : 0); ++ay)
         for (int ax = 0; ax <= H; ++ax) {
           const int m = az * az + ay * ay + ax * ax;
           if (m == 0) continue;
-          const size_t idx = g.dim == 2 ? static_cast<size_t>(ay * W1 + ax) : static_cast<size_t>((az * W1 + ay) * W1 + ax);
+          const size_t idx = g.dim == 1 ? static_cast<size_t>(ax)
+                             : g.dim == 2 ? static_cast<size_t>(ay * W1 + ax)
+                                          : static_cast<size_t>((az * W1 + ay) * W1 + ax);
           w[idx] = std::pow(static_cast<double>(m), -0.5 * d.alpha);
         }
     S->wtab = upload_vec(w);
