@@ -22,6 +22,7 @@
 // are shared-memory broadcasts.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "plan.hpp"
@@ -36,6 +37,7 @@ struct StencilState {
   double* scale = nullptr;              // [n_out]
   double* pack = nullptr;               // [n_in] double2 (u, kappa u) for kappa-weighted fractional
   size_t tab_bytes = 0;
+  int ws = 0;                           // weight row stride (2-D: padded to a multiple of 4)
 };
 
 namespace {
@@ -52,6 +54,7 @@ struct StArgs {
   const double* kappa;
   const double* tab;      // weights (device)
   int tab_len;
+  int ws, wp;             // weight row stride, peridynamic plane stride (doubles)
   const double* diag;
   const double* scale;
   double* out;            // [comps][n_out]
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
   for (int o = 16; o > 0; o >>= 1) Rw = max(Rw, __shfl_xor_sync(0xffffffffu, Rw, o));
   const int64_t nin_total = (g.in_end - g.in_begin) * g.stride0;
   const double ki_kappa = (KW && live) ? a.kappa[ii] : 1.0;
-  const int W1 = a.H + 1, W2 = 2 * a.H + 1;
+  const int W1 = a.H + 1;
 
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;   // A, B (fractional) / out_x, out_y (peri) / diag parts
   int d[3] = {0, 0, 0};
@@ -156,7 +159,9 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
         if (!in) continue;
         if (KIND == 0) {
           const int ax = dx < 0 ? -dx : dx;
-          const double w = DIM == 1 ? stab[ax] : DIM == 2 ? stab[ay * W1 + ax] : stab[(az * W1 + ay) * W1 + ax];
+          const int ny = DIM >= 2 ? W1 : 1;
+          const double w = stab[((DIM == 3 ? az : 0) * ny + (DIM >= 2 ? ay : 0)) * a.ws + dx + a.H];
+          (void)ax;
           if (MODE == 0) {
             if (!dom) continue;
             const int64_t kk = rowoff + kx;
@@ -174,8 +179,8 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
           }
         } else {
           // peridynamic 2-D: M(d) = d d^T / |d|^3, tables by signed offset
-          const int t = (dy + a.H) * W2 + (dx + a.H);
-          const double mxx = stab[t], mxy = stab[W2 * W2 + t], myy = stab[2 * W2 * W2 + t];
+          const int t = (dy + a.H) * a.ws + (dx + a.H);
+          const double mxx = stab[t], mxy = stab[a.wp + t], myy = stab[2 * a.wp + t];
           if (MODE == 0) {
             if (!dom) continue;
             const int64_t kk = rowoff + kx;
@@ -219,27 +224,36 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
 
 // ---- apply (MODE 0) ---------------------------------------------------------
 // One thread per target; the thread walks its own ball row by row with exact
-// half spans (integer bound from a single-precision sqrt with an integer fix-
-// up; the tie band around (delta/h)^2 is resolved by the float predicate at the
-// span ends only), so the pair loop is value-load, weight-load, FMA(s) with no
-// per-pair predicate. 2-D: the CTA's (32+2H) x (8+2H) neighbourhood is staged
-// in shared memory (zeros outside the domain: clip and collar apply paths
-// coincide, the collar lives in diag). 3-D: sources through L1.
-constexpr int kT2X = 32, kT2Y = 8;
+// half spans (integer bound from a single-precision sqrt; only when the tie
+// band around (delta/h)^2 is non-empty are the span ends re-checked with the
+// reference's float predicate), and each row is ONE loop over [-xm, xp] with a
+// symmetric weight row (the origin weight is 0, so the self term needs no
+// branch): value load, weight load, FMA(s). 2-D: the CTA's (32+2H) x (8+2H)
+// neighbourhood is staged in shared memory (zeros outside the domain: clip and
+// collar apply paths coincide, the collar lives in diag). 3-D: sources via L1.
 
 __device__ __forceinline__ int isqrt_floor(int m) {
   if (m < 0) return -1;
   int x = static_cast<int>(sqrtf(static_cast<float>(m)));
-  while (x * x > m) --x;
-  while ((x + 1) * (x + 1) <= m) ++x;
+  if (x * x > m) --x;
+  else if ((x + 1) * (x + 1) <= m) ++x;
   return x;
 }
 
 template <int DIM>
 struct Ball {
   int mlo, mhi;
+  bool tie;          // non-empty tie band [mlo, mhi]
   int64_t ki[3];
   double h, delta;
+  __device__ __forceinline__ void init(double dl, double hh) {
+    delta = dl;
+    h = hh;
+    const double e = dl / hh, e2 = e * e;
+    mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
+    mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+    tie = mlo <= mhi;
+  }
   __device__ __forceinline__ bool in(const int* d) const {
     int m = 0;
 #pragma unroll
@@ -248,7 +262,7 @@ struct Ball {
     if (m < mlo) return true;
     return point_in<DIM>(ki, d, h, delta);
   }
-  // exact half spans of the row with the leading offsets d[0..DIM-2]; false if empty
+  // exact half spans of the row with leading offsets d[0..DIM-2]; false if empty
   __device__ __forceinline__ bool span(int* d, int& xm, int& xp) const {
     int base2 = 0;
 #pragma unroll
@@ -257,108 +271,334 @@ struct Ball {
     if (X < 0) return false;
     xp = X;
     xm = X;
-    if (base2 + X * X >= mlo) {                         // ends sit in the tie band
+    if (tie && base2 + X * X >= mlo) {
       d[DIM - 1] = xp;
       while (xp > 0 && !in(d)) { --xp; d[DIM - 1] = xp; }
       d[DIM - 1] = -xm;
       while (xm > 0 && !in(d)) { --xm; d[DIM - 1] = -xm; }
-    }
-    if (base2 != 0) {
-      d[DIM - 1] = 0;
-      if (!in(d)) return false;
+      if (base2 != 0) {
+        d[DIM - 1] = 0;
+        if (!in(d)) return false;
+      }
     }
     return true;
   }
 };
 
+template <bool KW>
+__device__ __forceinline__ void row_sum(const double2* v, const double* w, int xm, int xp, double& a0, double& a1) {
+  double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
+  int k = -xm;
+#pragma unroll 2
+  for (; k + 1 <= xp; k += 2) {
+    const double2 va = v[k], vb = v[k + 1];
+    const double wa = w[k], wb = w[k + 1];
+    s0 = fma(wa, va.x, s0);
+    t0 = fma(wb, vb.x, t0);
+    if (KW) {
+      s1 = fma(wa, va.y, s1);
+      t1 = fma(wb, vb.y, t1);
+    }
+  }
+  if (k <= xp) {
+    const double2 va = v[k];
+    s0 = fma(w[k], va.x, s0);
+    if (KW) s1 = fma(w[k], va.y, s1);
+  }
+  a0 += s0 + t0;
+  if (KW) a1 += s1 + t1;
+}
+
+// 2-D apply, register-blocked: a warp owns one target row of kRX * 32
+// consecutive nodes, each lane kRX adjacent targets. For every ball row the
+// warp sweeps the warp-uniform offset range [-XW, XW] (XW the widest half span
+// of its targets on that row); per offset k it reads ONE weight w(dy, k)
+// (shared-memory broadcast) and ONE new source value — the lane's window of
+// kRX sources slides by one — and issues kRX unmasked FMA pairs. The sweep
+// starts exactly at -XW: the tile keeps columns split by (column mod 4) into
+// four planes (window loads of a warp are contiguous, no bank conflicts) and
+// the start phase (-XW mod 4) is a template parameter, so every load offset is
+// static. Afterwards each target removes the offsets of the sweep outside its
+// own span (|k| > X_r; rare, delta varies slowly) and adds the offsets of its
+// tie band ((delta/h)^2 within 1e-12), decided by the reference's float
+// predicate.
+// warp patch: kLX lanes x kRX targets along x, kLY rows; CTA: kWY warps along y
+constexpr int kRX = 4, kLX = 8, kLY = 4, kWY = 8;
+constexpr int kBX = kLX * kRX, kBY = kLY * kWY;
+
+__host__ __device__ inline int tile2d_q(int H) { return kLX + 2 + H / 2; }
+__host__ __device__ inline int isq_len(int H) { return (H + 1) * (H + 1) + 1; }
+constexpr int kRowMax = 16;                      // |dy| bound of the per-warp row plan (H <= 16)
+
 template <int KIND, bool KW>
-__global__ void __launch_bounds__(kT2X * kT2Y) stencil2d_kernel(StArgs a) {
-  extern __shared__ double sm[];
-  const int H = a.H;
-  const int TW = kT2X + 2 * H, TH = kT2Y + 2 * H;
-  double2* tile = reinterpret_cast<double2*>(sm);          // (u, kappa u) or (ux, uy)
-  double* wt = sm + 2 * static_cast<size_t>(TW) * TH;
-  const int tid = threadIdx.y * kT2X + threadIdx.x;
-  for (int i = tid; i < a.tab_len; i += kT2X * kT2Y) wt[i] = a.tab[i];
+struct Acc2 {
+  double a0[kRX], a1[kRX];
+};
+
+// one ball row: chunks of 4 offsets from k = -XW; ph = (H - XW) & 3
+template <int KIND, bool KW, int PH>
+__device__ __forceinline__ void sweep_row(Acc2<KIND, KW>& A, const double2* __restrict__ tp, int Q,
+                                          const double* __restrict__ wq, int wplane, int nsteps) {
+  // tp: plane 0 of the lane's quad containing the window start; wq: aligned
+  // weight quad containing the start offset; window element i sits at quad
+  // offset (PH + i) >> 2, plane (PH + i) & 3
+  double2 cur[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) cur[i] = tp[((PH + i) & 3) * Q + ((PH + i) >> 2)];
+  double wa[4], wn[4];
+  double xa[4], xn[4], ya[4], yn[4];
+  auto ldw = [&](const double* p, double* w) {
+    const double2 lo = *reinterpret_cast<const double2*>(p), hi = *reinterpret_cast<const double2*>(p + 2);
+    w[0] = lo.x; w[1] = lo.y; w[2] = hi.x; w[3] = hi.y;
+  };
+  ldw(wq, wa);
+  if (KIND == 1) {
+    ldw(wq + wplane, xa);
+    ldw(wq + 2 * wplane, ya);
+  }
+  // one chunk: offsets s = 0..3 of the current quad pair; MASK drops s >= left
+  auto chunk = [&](auto mask_tag, int left) {
+    constexpr bool MASK = decltype(mask_tag)::value;
+    tp += 1;
+    double2 nxt[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) nxt[i] = tp[((PH + i) & 3) * Q + ((PH + i) >> 2)];
+    ldw(wq + 4, wn);
+    if (KIND == 1) {
+      ldw(wq + 4 + wplane, xn);
+      ldw(wq + 4 + 2 * wplane, yn);
+    }
+    const double2 win[8] = {cur[0], cur[1], cur[2], cur[3], nxt[0], nxt[1], nxt[2], nxt[3]};
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int wi = PH + s;                       // weight index in (wa, wn)
+      const bool on = !MASK || s < left;
+      if (KIND == 0) {
+        double w = wi < 4 ? wa[wi & 3] : wn[wi & 3];
+        if (MASK) w = on ? w : 0.0;
+#pragma unroll
+        for (int r = 0; r < kRX; ++r) {
+          A.a0[r] = fma(w, win[s + r].x, A.a0[r]);
+          if (KW) A.a1[r] = fma(w, win[s + r].y, A.a1[r]);
+        }
+      } else {
+        double mxx = wi < 4 ? wa[wi & 3] : wn[wi & 3];
+        double mxy = wi < 4 ? xa[wi & 3] : xn[wi & 3];
+        double myy = wi < 4 ? ya[wi & 3] : yn[wi & 3];
+        if (MASK) {
+          mxx = on ? mxx : 0.0;
+          mxy = on ? mxy : 0.0;
+          myy = on ? myy : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < kRX; ++r) {
+          const double2 v = win[s + r];
+          A.a0[r] = fma(mxx, v.x, fma(mxy, v.y, A.a0[r]));
+          A.a1[r] = fma(mxy, v.x, fma(myy, v.y, A.a1[r]));
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      cur[i] = nxt[i];
+      wa[i] = wn[i];
+      if (KIND == 1) {
+        xa[i] = xn[i];
+        ya[i] = yn[i];
+      }
+    }
+    wq += 4;
+  };
+  int left = nsteps;
+  for (; left >= 8; left -= 8) {          // two chunks per trip: the window rotation is register renaming
+    chunk(std::false_type{}, 4);
+    chunk(std::false_type{}, 4);
+  }
+  if (left >= 4) {
+    chunk(std::false_type{}, 4);
+    left -= 4;
+  }
+  if (left > 0) chunk(std::true_type{}, left);
+}
+
+template <int KIND, bool KW>
+__global__ void __launch_bounds__(32 * kWY, KIND == 1 ? 2 : 3) stencil2d_kernel(StArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int H = a.H, Q = tile2d_q(H), TH = kBY + 2 * H, TW = 4 * Q;
+  double2* tile = reinterpret_cast<double2*>(sm);          // [TH][4 planes][Q]
+  double* wt = sm + 2 * static_cast<size_t>(TH) * TW;
+  int* isq = reinterpret_cast<int*>(wt + a.tab_len);       // isqrt table for 0..(H+1)^2
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int i = tid; i < a.tab_len; i += 32 * kWY) wt[i] = a.tab[i];
+  for (int i = tid; i < isq_len(H); i += 32 * kWY) {
+    int x = static_cast<int>(sqrtf(static_cast<float>(i)));
+    while (x * x > i) --x;
+    while ((x + 1) * (x + 1) <= i) ++x;
+    isq[i] = x;
+  }
   const Geom& g = a.g;
   const int64_t n = g.n;
-  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kT2X;
-  const int64_t y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * kT2Y;
+  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kBX;
+  const int64_t y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * kBY;
   const int64_t nin_total = (g.in_end - g.in_begin) * g.stride0;
-  for (int i = tid; i < TW * TH; i += kT2X * kT2Y) {
-    const int ty = i / TW, tx = i % TW;
-    const int64_t gy = y0 - H + ty, gx = x0 - H + tx;
-    const bool in = gy >= 0 && gy < n && gx >= 0 && gx < n && gy >= g.in_begin && gy < g.in_end;
-    const int64_t k = (gy - g.in_begin) * n + gx;
-    double2 v = make_double2(0.0, 0.0);
-    if (in) {
-      if (KIND == 1) v = make_double2(__ldg(a.u + k), __ldg(a.u + nin_total + k));
-      else if (KW) v = a.pk[k];
-      else v.x = __ldg(a.u + k);
+  // staging: lane i of a 32-column group takes column 4 (i & 7) + (i >> 3), so
+  // each quarter warp stores consecutive slots of one plane (conflict-free)
+  const int cl = 4 * (threadIdx.x & 7) + (threadIdx.x >> 3);
+  for (int ty = threadIdx.y; ty < TH; ty += kWY) {
+    const int64_t gy = y0 - H + ty;
+    const bool yin = gy >= 0 && gy < n && gy >= g.in_begin && gy < g.in_end;
+    const int64_t rowk = (gy - g.in_begin) * n;
+    double2* trow = tile + static_cast<size_t>(ty) * TW;
+    for (int c0 = 0; c0 < TW; c0 += 32) {
+      const int c = c0 + cl;
+      if (c >= TW) continue;
+      const int64_t gx = x0 - H + c;
+      double2 v = make_double2(0.0, 0.0);
+      if (yin && gx >= 0 && gx < n) {
+        const int64_t k = rowk + gx;
+        if (KIND == 1) v = make_double2(__ldg(a.u + k), __ldg(a.u + nin_total + k));
+        else if (KW) v = a.pk[k];
+        else v.x = __ldg(a.u + k);
+      }
+      trow[(c & 3) * Q + (c >> 2)] = v;
     }
-    tile[i] = v;
   }
   __syncthreads();
-  const int64_t ix = x0 + threadIdx.x, iy = y0 + threadIdx.y;
-  if (ix >= n || iy >= g.row_end) return;
-  const int64_t ii = (iy - g.in_begin) * n + ix;
-  Ball<2> B;
-  B.h = g.h;
-  B.delta = a.delta ? a.delta[ii] : a.delta0;
-  B.ki[0] = iy;
-  B.ki[1] = ix;
-  const double e = B.delta / B.h, e2 = e * e;
-  B.mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
-  B.mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
-  const int Ry = isqrt_floor(B.mhi);
-  const int W1 = H + 1, W2 = 2 * H + 1;
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-  const int cx = threadIdx.x + H, cy = threadIdx.y + H;
-  for (int dy = -Ry; dy <= Ry; ++dy) {
-    int d[2] = {dy, 0};
-    int xm, xp;
-    if (!B.span(d, xm, xp)) continue;
-    const double2* trow = tile + (cy + dy) * TW + cx;
-    const int ay = dy < 0 ? -dy : dy;
+  const int tx = threadIdx.x & (kLX - 1);                   // lane column
+  const int wy = threadIdx.y * kLY + (threadIdx.x >> 3);    // target row within the CTA
+  // targets of this lane
+  const int64_t iy = y0 + wy;
+  const bool yok = iy < g.row_end;
+  int M[kRX], mlo[kRX], mhi[kRX];
+  unsigned tiem = 0;
+  int Mx = -1;
+#pragma unroll
+  for (int r = 0; r < kRX; ++r) {
+    const int64_t ix = x0 + kRX * tx + r;
+    M[r] = -1;
+    mlo[r] = 1;
+    mhi[r] = 0;
+    if (yok && ix < n) {
+      const int64_t ii = (iy - g.in_begin) * n + ix;
+      const double e = (a.delta ? a.delta[ii] : a.delta0) / g.h, e2 = e * e;
+      mlo[r] = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
+      mhi[r] = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+      M[r] = mlo[r] <= mhi[r] ? mlo[r] - 1 : mhi[r];
+      if (mlo[r] <= mhi[r]) tiem |= 1u << r;
+    }
+    Mx = max(Mx, M[r]);
+  }
+  auto isqrt_t = [&](int m) { return m < 0 ? -1 : isq[m]; };
+  const int RyW = __reduce_max_sync(0xffffffffu, isqrt_t(Mx));
+  Acc2<KIND, KW> A;
+#pragma unroll
+  for (int r = 0; r < kRX; ++r) A.a0[r] = A.a1[r] = 0.0;
+  const int cy = wy + H;
+  // tile value of this lane's target r at offset (dy, k)
+  auto tv = [&](int dy, int r, int k) {
+    const int c = kRX * tx + r + H + k;
+    return tile[static_cast<size_t>(cy + dy) * TW + (c & 3) * Q + (c >> 2)];
+  };
+  auto add = [&](int r, int dy, int k, int wrow, double sg) {
+    const double2 v = tv(dy, r, k);
     if (KIND == 0) {
-      const double* wrow = wt + ay * W1;
-      // left half (dx = -xm .. -1) and right half (dx = 0 .. xp), self skipped
-      for (int k = 1; k <= xm; ++k) {
-        const double w = wrow[k];
-        const double2 v = trow[-k];
-        acc0 = fma(w, v.x, acc0);
-        if (KW) acc1 = fma(w, v.y, acc1);
-      }
-      for (int k = dy == 0 ? 1 : 0; k <= xp; ++k) {
-        const double w = wrow[k];
-        const double2 v = trow[k];
-        acc2 = fma(w, v.x, acc2);
-        if (KW) acc3 = fma(w, v.y, acc3);
-      }
+      const double w = sg * wt[wrow + k + H];
+      A.a0[r] = fma(w, v.x, A.a0[r]);
+      if (KW) A.a1[r] = fma(w, v.y, A.a1[r]);
     } else {
-      const int t0 = (dy + H) * W2 + H;
-      for (int dx = -xm; dx <= xp; ++dx) {
-        if (dx == 0 && dy == 0) continue;
-        const int t = t0 + dx;
-        const double mxx = wt[t], mxy = wt[W2 * W2 + t], myy = wt[2 * W2 * W2 + t];
-        const double2 v = trow[dx];
-        acc0 = fma(mxx, v.x, fma(mxy, v.y, acc0));
-        acc1 = fma(mxy, v.x, fma(myy, v.y, acc1));
+      const int t = wrow + k + H;
+      const double mxx = sg * wt[t], mxy = sg * wt[a.wp + t], myy = sg * wt[2 * a.wp + t];
+      A.a0[r] = fma(mxx, v.x, fma(mxy, v.y, A.a0[r]));
+      A.a1[r] = fma(mxy, v.x, fma(myy, v.y, A.a1[r]));
+    }
+  };
+  // row plan of the warp, computed for all rows first (independent chains):
+  // XW = widest half span, XN = narrowest over live targets
+  int2* rowp = reinterpret_cast<int2*>(isq + ((isq_len(H) + 1) & ~1)) + threadIdx.y * (2 * kRowMax + 1) + kRowMax;
+  const int lane = threadIdx.x;
+  for (int dy = -RyW; dy <= RyW; ++dy) {
+    const int dy2 = dy * dy;
+    int Xl = -1, Xs = 1 << 20;
+#pragma unroll
+    for (int r = 0; r < kRX; ++r) {
+      const int X = isqrt_t(M[r] - dy2);
+      Xl = max(Xl, X);
+      if (M[r] >= 0) Xs = min(Xs, X);
+    }
+    const int XW = __reduce_max_sync(0xffffffffu, Xl);
+    const int XN = __reduce_min_sync(0xffffffffu, Xs);
+    if (lane == 0) rowp[dy] = make_int2(XW, XN);
+  }
+  __syncwarp();
+  for (int dy = -RyW; dy <= RyW; ++dy) {
+    const int2 rp = rowp[dy];
+    const int XW = rp.x, XN = rp.y;
+    if (XW < 0) continue;
+    const int wrow = (KIND == 0 ? (dy < 0 ? -dy : dy) : dy + H) * a.ws;
+    const int st = H - XW;                       // tile column of the window start minus 4 tx
+    const double2* tp = tile + static_cast<size_t>(cy + dy) * TW + tx + (st >> 2);
+    const double* wq = wt + wrow + (st & ~3);
+    const int nsteps = 2 * XW + 1;
+    switch (st & 3) {
+      case 0: sweep_row<KIND, KW, 0>(A, tp, Q, wq, a.wp, nsteps); break;
+      case 1: sweep_row<KIND, KW, 1>(A, tp, Q, wq, a.wp, nsteps); break;
+      case 2: sweep_row<KIND, KW, 2>(A, tp, Q, wq, a.wp, nsteps); break;
+      default: sweep_row<KIND, KW, 3>(A, tp, Q, wq, a.wp, nsteps); break;
+    }
+    if (XN >= XW) continue;
+    // remove the sweep's offsets outside each target's own span: warp-uniform
+    // offsets k = XN+1..XW, per-target selects
+    int X[kRX];
+#pragma unroll
+    for (int r = 0; r < kRX; ++r) X[r] = isqrt_t(M[r] - dy * dy);
+    for (int k = max(XN + 1, 0); k <= XW; ++k) {
+#pragma unroll
+      for (int r = 0; r < kRX; ++r) {
+        const double sg = X[r] < k ? -1.0 : 0.0;
+        add(r, dy, k, wrow, sg);
+        if (k > 0) add(r, dy, -k, wrow, sg);
       }
     }
   }
+  // tie band: at most one |d|^2 per row, at x = +-X; the float predicate decides
+  if (tiem) {
+    for (int r = 0; r < kRX; ++r) {
+      if (!(tiem >> r & 1u)) continue;
+      const int64_t ix = x0 + kRX * tx + r;
+      const int64_t ii = (iy - g.in_begin) * n + ix;
+      const double delta = a.delta ? a.delta[ii] : a.delta0;
+      const int64_t ki[2] = {iy, ix};
+      const int Ry = isqrt_floor(mhi[r]);
+      for (int dy = -Ry; dy <= Ry; ++dy) {
+        const int X = isqrt_floor(mhi[r] - dy * dy);
+        const int m = dy * dy + X * X;
+        if (m < mlo[r] || m == 0) continue;
+        const int wrow = (KIND == 0 ? (dy < 0 ? -dy : dy) : dy + H) * a.ws;
+        for (int sx = -X; sx <= X; sx += (X > 0 ? 2 * X : 1)) {
+          const int d[2] = {dy, sx};
+          if (point_in<2>(ki, d, g.h, delta)) add(r, dy, sx, wrow, 1.0);
+        }
+      }
+    }
+  }
+  if (!yok) return;
   const int64_t nout = (g.row_end - g.row_begin) * n;
-  const int64_t oi = (iy - g.row_begin) * n + ix;
-  const double2 c = tile[cy * TW + cx];
-  if (KIND == 0) {
-    const double A = acc0 + acc2, Bk = acc1 + acc3;
-    const double X = KW ? fma(a.kappa[ii], A, Bk) : A;
-    a.out[oi] = a.scale[oi] * (X - c.x * a.diag[oi]);
-  } else {
-    const double dxx = a.diag[oi], dxy = a.diag[nout + oi], dyy = a.diag[2 * nout + oi];
-    const double sc = a.scale[oi];
-    a.out[oi] = sc * (acc0 - (dxx * c.x + dxy * c.y));
-    a.out[nout + oi] = sc * (acc1 - (dxy * c.x + dyy * c.y));
+#pragma unroll
+  for (int r = 0; r < kRX; ++r) {
+    const int64_t ix = x0 + kRX * tx + r;
+    if (ix >= n) break;
+    const int64_t ii = (iy - g.in_begin) * n + ix;
+    const int64_t oi = (iy - g.row_begin) * n + ix;
+    const double2 u = tv(0, r, 0);
+    if (KIND == 0) {
+      const double X = KW ? fma(a.kappa[ii], A.a0[r], A.a1[r]) : A.a0[r];
+      a.out[oi] = a.scale[oi] * (X - u.x * a.diag[oi]);
+    } else {
+      const double dxx = a.diag[oi], dxy = a.diag[nout + oi], dyy = a.diag[2 * nout + oi];
+      const double sc = a.scale[oi];
+      a.out[oi] = sc * (A.a0[r] - (dxx * u.x + dxy * u.y));
+      a.out[nout + oi] = sc * (A.a1[r] - (dxy * u.x + dyy * u.y));
+    }
   }
 }
 
@@ -393,33 +633,15 @@ __global__ void __launch_bounds__(k1T) stencil1d_kernel(StArgs a) {
   if (ix >= g.row_end) return;
   const int64_t ii = ix - g.in_begin;
   Ball<1> B;
-  B.h = g.h;
-  B.delta = a.delta ? a.delta[ii] : a.delta0;
+  B.init(a.delta ? a.delta[ii] : a.delta0, g.h);
   B.ki[0] = ix;
-  const double e = B.delta / B.h, e2 = e * e;
-  B.mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
-  B.mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
   int d[1] = {0};
   int xm, xp;
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  double acc0 = 0.0, acc1 = 0.0;
   const double2* trow = tile + threadIdx.x + H;
-  if (B.span(d, xm, xp)) {
-    for (int k = 1; k <= xm; ++k) {
-      const double w = wt[k];
-      const double2 v = trow[-k];
-      acc0 = fma(w, v.x, acc0);
-      if (KW) acc1 = fma(w, v.y, acc1);
-    }
-    for (int k = 1; k <= xp; ++k) {
-      const double w = wt[k];
-      const double2 v = trow[k];
-      acc2 = fma(w, v.x, acc2);
-      if (KW) acc3 = fma(w, v.y, acc3);
-    }
-  }
+  if (B.span(d, xm, xp)) row_sum<KW>(trow, wt + H, xm, xp, acc0, acc1);
   const int64_t oi = ix - g.row_begin;
-  const double A = acc0 + acc2, Bk = acc1 + acc3;
-  const double X = KW ? fma(a.kappa[ii], A, Bk) : A;
+  const double X = KW ? fma(a.kappa[ii], acc0, acc1) : acc0;
   a.out[oi] = a.scale[oi] * (X - trow[0].x * a.diag[oi]);
 }
 
@@ -431,7 +653,7 @@ __global__ void __launch_bounds__(128) stencil3d_kernel(StArgs a) {
   __syncthreads();
   const Geom& g = a.g;
   const int64_t n = g.n;
-  const int H = a.H, W1 = H + 1;
+  const int H = a.H, W1 = H + 1, W2 = 2 * H + 1;
   const int64_t bx = (n + 31) / 32, by = (n + 3) / 4;
   const int64_t b = blockIdx.x;
   const int64_t ix = (b % bx) * 32 + (threadIdx.x & 31);
@@ -441,16 +663,13 @@ __global__ void __launch_bounds__(128) stencil3d_kernel(StArgs a) {
   const int64_t plane = n * n;
   const int64_t ii = (iz - g.in_begin) * plane + iy * n + ix;
   Ball<3> B;
-  B.h = g.h;
-  B.delta = a.delta ? a.delta[ii] : a.delta0;
+  B.init(a.delta ? a.delta[ii] : a.delta0, g.h);
   B.ki[0] = iz;
   B.ki[1] = iy;
   B.ki[2] = ix;
-  const double e = B.delta / B.h, e2 = e * e;
-  B.mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
-  B.mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
   const int Rz = isqrt_floor(B.mhi);
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  double acc0 = 0.0, acc1 = 0.0;
+  const double2* pk = a.pk;
   for (int dz = -Rz; dz <= Rz; ++dz) {
     const int64_t gz = iz + dz;
     if (gz < 0 || gz >= n) continue;
@@ -462,36 +681,22 @@ __global__ void __launch_bounds__(128) stencil3d_kernel(StArgs a) {
       int d[3] = {dz, dy, 0};
       int xm, xp;
       if (!B.span(d, xm, xp)) continue;
-      if (xm > ix) xm = static_cast<int>(ix);                     // clip to the domain (zero field)
+      if (xm > ix) xm = static_cast<int>(ix);                      // clip to the domain (zero field)
       if (xp > n - 1 - ix) xp = static_cast<int>(n - 1 - ix);
       const int64_t row = (gz - g.in_begin) * plane + gy * n + ix;
-      const double* wrow = wt + (az * W1 + (dy < 0 ? -dy : dy)) * W1;
-      for (int k = 1; k <= xm; ++k) {
-        const double w = wrow[k];
-        if (KW) {
-          const double2 v = a.pk[row - k];
-          acc0 = fma(w, v.x, acc0);
-          acc1 = fma(w, v.y, acc1);
-        } else {
-          acc0 = fma(w, __ldg(a.u + row - k), acc0);
-        }
-      }
-      for (int k = (dz == 0 && dy == 0) ? 1 : 0; k <= xp; ++k) {
-        const double w = wrow[k];
-        if (KW) {
-          const double2 v = a.pk[row + k];
-          acc2 = fma(w, v.x, acc2);
-          acc3 = fma(w, v.y, acc3);
-        } else {
-          acc2 = fma(w, __ldg(a.u + row + k), acc2);
-        }
+      const double* wrow = wt + (az * W1 + (dy < 0 ? -dy : dy)) * W2 + H;
+      if (KW) {
+        row_sum<true>(pk + row, wrow, xm, xp, acc0, acc1);
+      } else {
+        double s0 = 0.0;
+        for (int k = -xm; k <= xp; ++k) s0 = fma(wrow[k], __ldg(a.u + row + k), s0);
+        acc0 += s0;
       }
     }
   }
   const int64_t oi = (iz - g.row_begin) * plane + iy * n + ix;
   const double ui = KW ? a.pk[ii].x : a.u[ii];
-  const double A = acc0 + acc2, Bk = acc1 + acc3;
-  const double X = KW ? fma(a.kappa[ii], A, Bk) : A;
+  const double X = KW ? fma(a.kappa[ii], acc0, acc1) : acc0;
   a.out[oi] = a.scale[oi] * (X - ui * a.diag[oi]);
 }
 
@@ -521,8 +726,8 @@ void launch_t(const StArgs& a, cudaStream_t s, size_t smem) {
 }
 
 size_t tile2d_bytes(const StArgs& a) {
-  return sizeof(double) * (2 * static_cast<size_t>(kT2X + 2 * a.H) * (kT2Y + 2 * a.H)) +
-         sizeof(double) * a.tab_len;
+  return sizeof(double2) * static_cast<size_t>(kBY + 2 * a.H) * 4 * tile2d_q(a.H) + sizeof(double) * a.tab_len +
+         sizeof(int) * ((isq_len(a.H) + 1) & ~1) + sizeof(int2) * kWY * (2 * kRowMax + 1);
 }
 
 void launch(const StArgs& a, cudaStream_t s, size_t smem) {
@@ -540,12 +745,12 @@ void launch(const StArgs& a, cudaStream_t s, size_t smem) {
     return;
   }
   if (dim == 2 && a.mode == 0) {
-    dim3 grid(static_cast<unsigned>((n + kT2X - 1) / kT2X),
-              static_cast<unsigned>((a.g.row_end - a.g.row_begin + kT2Y - 1) / kT2Y));
+    dim3 grid(static_cast<unsigned>((n + kBX - 1) / kBX),
+              static_cast<unsigned>((a.g.row_end - a.g.row_begin + kBY - 1) / kBY));
     const size_t sb = tile2d_bytes(a);
-    if (a.kind == 1) stencil2d_kernel<1, false><<<grid, dim3(kT2X, kT2Y), sb, s>>>(a);
-    else if (a.kw) stencil2d_kernel<0, true><<<grid, dim3(kT2X, kT2Y), sb, s>>>(a);
-    else stencil2d_kernel<0, false><<<grid, dim3(kT2X, kT2Y), sb, s>>>(a);
+    if (a.kind == 1) stencil2d_kernel<1, false><<<grid, dim3(32, kWY), sb, s>>>(a);
+    else if (a.kw) stencil2d_kernel<0, true><<<grid, dim3(32, kWY), sb, s>>>(a);
+    else stencil2d_kernel<0, false><<<grid, dim3(32, kWY), sb, s>>>(a);
     return;
   }
   if (dim == 3 && a.mode == 0) {
@@ -583,12 +788,43 @@ StArgs make_args(const Plan& P, const StencilState& S, int mode, const double* u
   a.kappa = P.d_kappa;
   a.tab = S.kind == 0 ? S.wtab : S.mtab;
   a.tab_len = static_cast<int>(S.tab_bytes / sizeof(double));
+  a.ws = S.ws;
+  a.wp = (2 * S.H + 1) * S.ws;
   a.diag = S.diag;
   a.scale = S.scale;
   a.out = out;
   return a;
 }
 
+}  // namespace
+
+namespace {
+template <typename K>
+void smem_attr(K k) {
+  NLG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  NLG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+}
+void allow_smem() {
+  smem_attr(stencil2d_kernel<0, true>);
+  smem_attr(stencil2d_kernel<0, false>);
+  smem_attr(stencil2d_kernel<1, false>);
+  smem_attr(stencil1d_kernel<true>);
+  smem_attr(stencil1d_kernel<false>);
+  smem_attr(stencil3d_kernel<true>);
+  smem_attr(stencil3d_kernel<false>);
+  smem_attr(stencil_kernel<1, 0, 1, true>);
+  smem_attr(stencil_kernel<1, 0, 1, false>);
+  smem_attr(stencil_kernel<2, 0, 0, true>);
+  smem_attr(stencil_kernel<2, 0, 0, false>);
+  smem_attr(stencil_kernel<2, 0, 1, true>);
+  smem_attr(stencil_kernel<2, 0, 1, false>);
+  smem_attr(stencil_kernel<2, 1, 0, false>);
+  smem_attr(stencil_kernel<2, 1, 1, false>);
+  smem_attr(stencil_kernel<3, 0, 0, true>);
+  smem_attr(stencil_kernel<3, 0, 0, false>);
+  smem_attr(stencil_kernel<3, 0, 1, true>);
+  smem_attr(stencil_kernel<3, 0, 1, false>);
+}
 }  // namespace
 
 // Method 3 applies when the operator is a BASELINE kernel in 2-D/3-D with a
@@ -604,25 +840,25 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   S->dim = g.dim;
   S->kind = peri ? 1 : 0;
   S->H = H;
+  // 2-D rows are read as aligned quads up to index 2H+7
+  S->ws = g.dim == 2 ? ((2 * H + 8 + 3) & ~3) : 2 * H + 1;
   if (frac) {
-    const int W1 = H + 1;
-    const size_t tl = g.dim == 1 ? W1 : g.dim == 2 ? W1 * W1 : W1 * W1 * W1;
-    std::vector<double> w(tl, 0.0);
-    for (int az = 0; az <= (g.dim == 3 ? H : 0); ++az)
-      for (int ay = 0; ay <= (g.dim >= 2 ? H : 0); ++ay)
-        for (int ax = 0; ax <= H; ++ax) {
-          const int m = az * az + ay * ay + ax * ax;
+    // symmetric rows: w[(az * W1 + ay) * W2 + dx + H] = |(az, ay, dx)|^-alpha, w = 0 at the origin
+    const int W1 = H + 1, W2 = S->ws;
+    const int nz = g.dim == 3 ? W1 : 1, ny = g.dim >= 2 ? W1 : 1;
+    std::vector<double> w(static_cast<size_t>(nz) * ny * W2, 0.0);
+    for (int az = 0; az < nz; ++az)
+      for (int ay = 0; ay < ny; ++ay)
+        for (int dx = -H; dx <= H; ++dx) {
+          const int m = az * az + ay * ay + dx * dx;
           if (m == 0) continue;
-          const size_t idx = g.dim == 1 ? static_cast<size_t>(ax)
-                             : g.dim == 2 ? static_cast<size_t>(ay * W1 + ax)
-                                          : static_cast<size_t>((az * W1 + ay) * W1 + ax);
-          w[idx] = std::pow(static_cast<double>(m), -0.5 * d.alpha);
+          w[(static_cast<size_t>(az) * ny + ay) * W2 + dx + H] = std::pow(static_cast<double>(m), -0.5 * d.alpha);
         }
     S->wtab = upload_vec(w);
     S->tab_bytes = w.size() * sizeof(double);
   } else {
-    const int W2 = 2 * H + 1;
-    std::vector<double> t(static_cast<size_t>(3 * W2 * W2), 0.0);
+    const int W2 = S->ws, P = (2 * H + 1) * W2;
+    std::vector<double> t(static_cast<size_t>(3 * P), 0.0);
     for (int dy = -H; dy <= H; ++dy)
       for (int dx = -H; dx <= H; ++dx) {
         const double r2 = static_cast<double>(dx * dx + dy * dy);
@@ -630,8 +866,8 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
         const double r3 = r2 * std::sqrt(r2);
         const int k = (dy + H) * W2 + (dx + H);
         t[k] = dy * dy / r3;                 // axis 0 = "x" component of the SoA planes
-        t[W2 * W2 + k] = dx * dy / r3;
-        t[2 * W2 * W2 + k] = dx * dx / r3;
+        t[P + k] = dx * dy / r3;
+        t[2 * P + k] = dx * dx / r3;
       }
     S->mtab = upload_vec(t);
     S->tab_bytes = t.size() * sizeof(double);
@@ -648,9 +884,7 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * P.n_out * (peri ? 3 : 1)));
   if (frac && d.kappa) NLG_CUDA(cudaMalloc(&S->pack, sizeof(double2) * P.n_in));
   P.st_state = S;
-  NLG_CUDA(cudaFuncSetAttribute(stencil2d_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-  NLG_CUDA(cudaFuncSetAttribute(stencil2d_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-  NLG_CUDA(cudaFuncSetAttribute(stencil2d_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  allow_smem();
   // diag: MODE 1 over the same sets and tables
   const StArgs a = make_args(P, *S, 1, nullptr, S->diag);
   launch(a, P.stream, S->tab_bytes);
