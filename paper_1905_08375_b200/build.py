@@ -43,6 +43,7 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
     headers.append(os.path.join(ROOT, "include", "nlgpu.h"))
     objs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+    common += os.environ.get("NLG_NVCC_EXTRA", "").split()   # experiment builds (e.g. -DNLG_R2FRAC=4)
     for f in cu:
         src = os.path.join(CSRC, f)
         obj = os.path.join(objdir, f + ".o")

@@ -309,82 +309,82 @@ __device__ __forceinline__ void row_sum(const double2* v, const double* w, int x
   if (KW) a1 += s1 + t1;
 }
 
-// 2-D apply, register-blocked: a warp owns one target row of kRX * 32
-// consecutive nodes, each lane kRX adjacent targets. For every ball row the
-// warp sweeps the warp-uniform offset range [-XW, XW] (XW the widest half span
-// of its targets on that row); per offset k it reads ONE weight w(dy, k)
-// (shared-memory broadcast) and ONE new source value — the lane's window of
-// kRX sources slides by one — and issues kRX unmasked FMA pairs. The sweep
-// starts exactly at -XW: the tile keeps columns split by (column mod 4) into
-// four planes (window loads of a warp are contiguous, no bank conflicts) and
-// the start phase (-XW mod 4) is a template parameter, so every load offset is
-// static. Afterwards each target removes the offsets of the sweep outside its
-// own span (|k| > X_r; rare, delta varies slowly) and adds the offsets of its
-// tie band ((delta/h)^2 within 1e-12), decided by the reference's float
-// predicate.
-// warp patch: kLX lanes x kRX targets along x, kLY rows; CTA: kWY warps along y
-constexpr int kRX = 4, kLX = 8, kLY = 4, kWY = 8;
-constexpr int kBX = kLX * kRX, kBY = kLY * kWY;
+// 2-D apply, register-blocked. A warp owns a patch of kLY target rows x
+// kLX * kRX columns; each lane kRX adjacent targets of one row. For every ball
+// row the warp sweeps the warp-uniform offset range [-XW, XW] (XW the widest
+// half span among its targets on that row); per offset k it reads ONE weight
+// w(dy, k) (shared-memory broadcast) and ONE new source value — the lane's
+// window of kRX sources slides by one — and issues kRX unmasked FMA pairs.
+// The fractional weight is even in dy, and so is every target's span, so rows
+// +dy and -dy are swept together on the pre-added sources (half the FMAs).
+// The sweep starts exactly at -XW: tile columns are split by (column mod 4)
+// into four planes and the start phase (-XW mod 4) is a template parameter, so
+// every load offset is static; the odd row stride keeps the two rows a
+// quarter warp reads on disjoint banks. Afterwards each target removes the
+// offsets of the sweep outside its own span (|k| > X_r, uniform loop over the
+// warp's narrowest..widest span) and adds the offsets of its tie band
+// ((delta/h)^2 within 1e-12) decided by the reference's float predicate.
+// R targets per lane: a warp covers 32/R lanes x R targets = 32 columns by R
+// rows, a CTA 32/R warps stacked along y = 32 x 32 targets.
+constexpr int kBX = 32, kBY = 32;
+#ifndef NLG_R2FRAC
+#define NLG_R2FRAC 8
+#endif
+#ifndef NLG_R2PERI
+#define NLG_R2PERI 4
+#endif
+constexpr int kR2Frac = NLG_R2FRAC, kR2Peri = NLG_R2PERI;   // targets per lane
 
-__host__ __device__ inline int tile2d_q(int H) { return kLX + 2 + H / 2; }
+__host__ __device__ inline int tile2d_q(int H) { return kBX / 4 + 2 + H / 2; }   // slots per plane
+__host__ __device__ inline int tile2d_rs(int H) { return 4 * tile2d_q(H) + 1; }  // row stride in slots (odd)
 __host__ __device__ inline int isq_len(int H) { return (H + 1) * (H + 1) + 1; }
-constexpr int kRowMax = 16;                      // |dy| bound of the per-warp row plan (H <= 16)
 
-template <int KIND, bool KW>
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool in) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(in ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool in) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(in ? 8 : 0) : "memory");
+}
+
+__device__ __forceinline__ double2 dadd2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+
+template <int KIND, bool KW, int R>
 struct Acc2 {
-  double a0[kRX], a1[kRX];
+  double a0[R], a1[R];
 };
 
-// one ball row: chunks of 4 offsets from k = -XW; ph = (H - XW) & 3
-template <int KIND, bool KW, int PH>
-__device__ __forceinline__ void sweep_row(Acc2<KIND, KW>& A, const double2* __restrict__ tp, int Q,
-                                          const double* __restrict__ wq, int wplane, int nsteps) {
-  // tp: plane 0 of the lane's quad containing the window start; wq: aligned
-  // weight quad containing the start offset; window element i sits at quad
-  // offset (PH + i) >> 2, plane (PH + i) & 3
-  double2 cur[4];
+// One ball row (PAIR: rows +dy and -dy on pre-added sources), 2*XW+1 offsets
+// from k = -XW. tp / tm: plane-0 slot of the lane's start quad in the row(s);
+// window element i (i < 4) sits at slot offset o[i] = ((ph + i) & 3) Q +
+// ((ph + i) >> 2), element i + 4 one slot further; wk: weight of the first
+// offset (offsets advance by one double).
+template <int KIND, bool KW, int kRX, bool PAIR>
+__device__ __forceinline__ void sweep_row(Acc2<KIND, KW, kRX>& A, const double2* __restrict__ tp,
+                                          const double2* __restrict__ tm, const int* o,
+                                          const double* __restrict__ wk, int wplane, int nsteps) {
+  auto ld = [&](int off) { return PAIR ? dadd2(tp[off], tm[off]) : tp[off]; };
+  double2 W[kRX + 4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) cur[i] = tp[((PH + i) & 3) * Q + ((PH + i) >> 2)];
-  double wa[4], wn[4];
-  double xa[4], xn[4], ya[4], yn[4];
-  auto ldw = [&](const double* p, double* w) {
-    const double2 lo = *reinterpret_cast<const double2*>(p), hi = *reinterpret_cast<const double2*>(p + 2);
-    w[0] = lo.x; w[1] = lo.y; w[2] = hi.x; w[3] = hi.y;
-  };
-  ldw(wq, wa);
-  if (KIND == 1) {
-    ldw(wq + wplane, xa);
-    ldw(wq + 2 * wplane, ya);
-  }
-  // one chunk: offsets s = 0..3 of the current quad pair; MASK drops s >= left
+  for (int i = 0; i < kRX; ++i) W[i] = ld(o[i & 3] + (i >> 2));
   auto chunk = [&](auto mask_tag, int left) {
     constexpr bool MASK = decltype(mask_tag)::value;
-    tp += 1;
-    double2 nxt[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) nxt[i] = tp[((PH + i) & 3) * Q + ((PH + i) >> 2)];
-    ldw(wq + 4, wn);
-    if (KIND == 1) {
-      ldw(wq + 4 + wplane, xn);
-      ldw(wq + 4 + 2 * wplane, yn);
-    }
-    const double2 win[8] = {cur[0], cur[1], cur[2], cur[3], nxt[0], nxt[1], nxt[2], nxt[3]};
+    for (int j = 0; j < 4; ++j) W[kRX + j] = ld(o[j] + kRX / 4);
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      const int wi = PH + s;                       // weight index in (wa, wn)
       const bool on = !MASK || s < left;
       if (KIND == 0) {
-        double w = wi < 4 ? wa[wi & 3] : wn[wi & 3];
+        double w = wk[s];
         if (MASK) w = on ? w : 0.0;
 #pragma unroll
         for (int r = 0; r < kRX; ++r) {
-          A.a0[r] = fma(w, win[s + r].x, A.a0[r]);
-          if (KW) A.a1[r] = fma(w, win[s + r].y, A.a1[r]);
+          A.a0[r] = fma(w, W[s + r].x, A.a0[r]);
+          if (KW) A.a1[r] = fma(w, W[s + r].y, A.a1[r]);
         }
       } else {
-        double mxx = wi < 4 ? wa[wi & 3] : wn[wi & 3];
-        double mxy = wi < 4 ? xa[wi & 3] : xn[wi & 3];
-        double myy = wi < 4 ? ya[wi & 3] : yn[wi & 3];
+        double mxx = wk[s], mxy = wk[wplane + s], myy = wk[2 * wplane + s];
         if (MASK) {
           mxx = on ? mxx : 0.0;
           mxy = on ? mxy : 0.0;
@@ -392,25 +392,20 @@ __device__ __forceinline__ void sweep_row(Acc2<KIND, KW>& A, const double2* __re
         }
 #pragma unroll
         for (int r = 0; r < kRX; ++r) {
-          const double2 v = win[s + r];
+          const double2 v = W[s + r];
           A.a0[r] = fma(mxx, v.x, fma(mxy, v.y, A.a0[r]));
           A.a1[r] = fma(mxy, v.x, fma(myy, v.y, A.a1[r]));
         }
       }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      cur[i] = nxt[i];
-      wa[i] = wn[i];
-      if (KIND == 1) {
-        xa[i] = xn[i];
-        ya[i] = yn[i];
-      }
-    }
-    wq += 4;
+    for (int i = 0; i < kRX; ++i) W[i] = W[i + 4];
+    tp += 1;
+    if (PAIR) tm += 1;
+    wk += 4;
   };
   int left = nsteps;
-  for (; left >= 8; left -= 8) {          // two chunks per trip: the window rotation is register renaming
+  for (; left >= 8; left -= 8) {          // two chunks per trip: the window shift is register renaming
     chunk(std::false_type{}, 4);
     chunk(std::false_type{}, 4);
   }
@@ -421,14 +416,16 @@ __device__ __forceinline__ void sweep_row(Acc2<KIND, KW>& A, const double2* __re
   if (left > 0) chunk(std::true_type{}, left);
 }
 
-template <int KIND, bool KW>
-__global__ void __launch_bounds__(32 * kWY, KIND == 1 ? 2 : 3) stencil2d_kernel(StArgs a) {
+template <int KIND, bool KW, int kRX>
+__global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil2d_kernel(StArgs a) {
+  constexpr int kLX = 32 / kRX, kLY = kRX, kWY = 32 / kRX;
   extern __shared__ __align__(16) double sm[];
-  const int H = a.H, Q = tile2d_q(H), TH = kBY + 2 * H, TW = 4 * Q;
-  double2* tile = reinterpret_cast<double2*>(sm);          // [TH][4 planes][Q]
-  double* wt = sm + 2 * static_cast<size_t>(TH) * TW;
+  const int H = a.H, Q = tile2d_q(H), RS = tile2d_rs(H), TH = kBY + 2 * H, TWc = 4 * Q;
+  double2* tile = reinterpret_cast<double2*>(sm);          // [TH][RS slots: 4 planes x Q, +1 pad]
+  double* wt = sm + 2 * static_cast<size_t>(TH + 1) * RS;  // row TH: zeros (partner of row 0)
   int* isq = reinterpret_cast<int*>(wt + a.tab_len);       // isqrt table for 0..(H+1)^2
   const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int i = tid; i < RS; i += 32 * kWY) tile[static_cast<size_t>(TH) * RS + i] = make_double2(0.0, 0.0);
   for (int i = tid; i < a.tab_len; i += 32 * kWY) wt[i] = a.tab[i];
   for (int i = tid; i < isq_len(H); i += 32 * kWY) {
     int x = static_cast<int>(sqrtf(static_cast<float>(i)));
@@ -441,143 +438,179 @@ __global__ void __launch_bounds__(32 * kWY, KIND == 1 ? 2 : 3) stencil2d_kernel(
   const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kBX;
   const int64_t y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * kBY;
   const int64_t nin_total = (g.in_end - g.in_begin) * g.stride0;
-  // staging: lane i of a 32-column group takes column 4 (i & 7) + (i >> 3), so
-  // each quarter warp stores consecutive slots of one plane (conflict-free)
+  // staging with cp.async (every load of a thread in flight at once; zero fill
+  // outside the domain / slab): lane i of a 32-column group takes column
+  // 4 (i & 7) + (i >> 3), so each quarter warp fills consecutive slots of one plane
   const int cl = 4 * (threadIdx.x & 7) + (threadIdx.x >> 3);
   for (int ty = threadIdx.y; ty < TH; ty += kWY) {
     const int64_t gy = y0 - H + ty;
     const bool yin = gy >= 0 && gy < n && gy >= g.in_begin && gy < g.in_end;
     const int64_t rowk = (gy - g.in_begin) * n;
-    double2* trow = tile + static_cast<size_t>(ty) * TW;
-    for (int c0 = 0; c0 < TW; c0 += 32) {
+    double2* trow = tile + static_cast<size_t>(ty) * RS;
+    for (int c0 = 0; c0 < TWc; c0 += 32) {
       const int c = c0 + cl;
-      if (c >= TW) continue;
+      if (c >= TWc) continue;
       const int64_t gx = x0 - H + c;
-      double2 v = make_double2(0.0, 0.0);
-      if (yin && gx >= 0 && gx < n) {
-        const int64_t k = rowk + gx;
-        if (KIND == 1) v = make_double2(__ldg(a.u + k), __ldg(a.u + nin_total + k));
-        else if (KW) v = a.pk[k];
-        else v.x = __ldg(a.u + k);
+      const bool in = yin && gx >= 0 && gx < n;
+      const int64_t k = in ? rowk + gx : 0;
+      double* dst = reinterpret_cast<double*>(trow + (c & 3) * Q + (c >> 2));
+      if (KIND == 1) {
+        cp_async8(dst, a.u + k, in);
+        cp_async8(dst + 1, a.u + nin_total + k, in);
+      } else if (KW) {
+        cp_async8(dst, a.u + k, in);
+        cp_async8(dst + 1, a.kappa + k, in);
+      } else {
+        cp_async8(dst, a.u + k, in);
+        cp_async8(dst + 1, a.u + k, false);
       }
-      trow[(c & 3) * Q + (c >> 2)] = v;
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  if (KW) {   // (u, kappa) -> (u, kappa u) on the thread's own slots
+    for (int ty = threadIdx.y; ty < TH; ty += kWY) {
+      double2* trow = tile + static_cast<size_t>(ty) * RS;
+      for (int c0 = 0; c0 < TWc; c0 += 32) {
+        const int c = c0 + cl;
+        if (c >= TWc) continue;
+        double2* dst = trow + (c & 3) * Q + (c >> 2);
+        const double2 v = *dst;
+        dst->y = v.y * v.x;
+      }
     }
   }
   __syncthreads();
   const int tx = threadIdx.x & (kLX - 1);                   // lane column
-  const int wy = threadIdx.y * kLY + (threadIdx.x >> 3);    // target row within the CTA
-  // targets of this lane
+  const int wy = threadIdx.y * kLY + threadIdx.x / kLX;     // target row within the CTA
   const int64_t iy = y0 + wy;
   const bool yok = iy < g.row_end;
-  int M[kRX], mlo[kRX], mhi[kRX];
+  const double inv_h = 1.0 / g.h;
+  // targets of this lane: M = largest |d|^2 surely inside (below the tie band)
+  int M[kRX];
   unsigned tiem = 0;
-  int Mx = -1;
+  int Mx = -1, Mn = 1 << 20;
 #pragma unroll
   for (int r = 0; r < kRX; ++r) {
     const int64_t ix = x0 + kRX * tx + r;
     M[r] = -1;
-    mlo[r] = 1;
-    mhi[r] = 0;
     if (yok && ix < n) {
       const int64_t ii = (iy - g.in_begin) * n + ix;
-      const double e = (a.delta ? a.delta[ii] : a.delta0) / g.h, e2 = e * e;
-      mlo[r] = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
-      mhi[r] = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
-      M[r] = mlo[r] <= mhi[r] ? mlo[r] - 1 : mhi[r];
-      if (mlo[r] <= mhi[r]) tiem |= 1u << r;
+      const double e = (a.delta ? a.delta[ii] : a.delta0) * inv_h, e2 = e * e;
+      const int mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
+      const int mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+      M[r] = mlo <= mhi ? mlo - 1 : mhi;
+      if (mlo <= mhi) tiem |= 1u << r;
+      Mn = min(Mn, M[r]);
     }
     Mx = max(Mx, M[r]);
   }
   auto isqrt_t = [&](int m) { return m < 0 ? -1 : isq[m]; };
-  const int RyW = __reduce_max_sync(0xffffffffu, isqrt_t(Mx));
-  Acc2<KIND, KW> A;
+  // row plan of the warp: isqrt is monotone, so the widest / narrowest half
+  // span on a row come from the warp's largest / smallest live M
+  const int MW = __reduce_max_sync(0xffffffffu, Mx);
+  const int MN = __reduce_min_sync(0xffffffffu, Mn);
+  Acc2<KIND, KW, kRX> A;
 #pragma unroll
   for (int r = 0; r < kRX; ++r) A.a0[r] = A.a1[r] = 0.0;
   const int cy = wy + H;
   // tile value of this lane's target r at offset (dy, k)
   auto tv = [&](int dy, int r, int k) {
     const int c = kRX * tx + r + H + k;
-    return tile[static_cast<size_t>(cy + dy) * TW + (c & 3) * Q + (c >> 2)];
+    return tile[static_cast<size_t>(cy + dy) * RS + (c & 3) * Q + (c >> 2)];
   };
-  auto add = [&](int r, int dy, int k, int wrow, double sg) {
+  auto wrow_of = [&](int dy) { return (KIND == 0 ? (dy < 0 ? -dy : dy) : dy + H) * a.ws; };
+  auto add = [&](int r, int dy, int k, double sg) {
     const double2 v = tv(dy, r, k);
+    const int t = wrow_of(dy) + k + H;
     if (KIND == 0) {
-      const double w = sg * wt[wrow + k + H];
+      const double w = sg * wt[t];
       A.a0[r] = fma(w, v.x, A.a0[r]);
       if (KW) A.a1[r] = fma(w, v.y, A.a1[r]);
     } else {
-      const int t = wrow + k + H;
       const double mxx = sg * wt[t], mxy = sg * wt[a.wp + t], myy = sg * wt[2 * a.wp + t];
       A.a0[r] = fma(mxx, v.x, fma(mxy, v.y, A.a0[r]));
       A.a1[r] = fma(mxy, v.x, fma(myy, v.y, A.a1[r]));
     }
   };
-  // row plan of the warp, computed for all rows first (independent chains):
-  // XW = widest half span, XN = narrowest over live targets
-  int2* rowp = reinterpret_cast<int2*>(isq + ((isq_len(H) + 1) & ~1)) + threadIdx.y * (2 * kRowMax + 1) + kRowMax;
-  const int lane = threadIdx.x;
-  for (int dy = -RyW; dy <= RyW; ++dy) {
-    const int dy2 = dy * dy;
-    int Xl = -1, Xs = 1 << 20;
+  // KIND 0 sweeps rows +ay / -ay together; row 0 pairs with the zero row TH
+  auto sweep = [&](int dy, int dm, int XW) {
+    const int st = H - XW;                       // start column relative to the lane's first target - H
+    const int ph = st & 3;
+    int o[4];
 #pragma unroll
-    for (int r = 0; r < kRX; ++r) {
-      const int X = isqrt_t(M[r] - dy2);
-      Xl = max(Xl, X);
-      if (M[r] >= 0) Xs = min(Xs, X);
-    }
-    const int XW = __reduce_max_sync(0xffffffffu, Xl);
-    const int XN = __reduce_min_sync(0xffffffffu, Xs);
-    if (lane == 0) rowp[dy] = make_int2(XW, XN);
-  }
-  __syncwarp();
-  for (int dy = -RyW; dy <= RyW; ++dy) {
-    const int2 rp = rowp[dy];
-    const int XW = rp.x, XN = rp.y;
+    for (int j = 0; j < 4; ++j) o[j] = ((ph + j) & 3) * Q + ((ph + j) >> 2);
+    const double2* tp = tile + static_cast<size_t>(cy + dy) * RS + (kRX / 4) * tx + (st >> 2);
+    const double2* tm = tile + static_cast<size_t>(dm) * RS + (kRX / 4) * tx + (st >> 2);
+    const double* wk = wt + wrow_of(dy) + st;
+    if (KIND == 0) sweep_row<KIND, KW, kRX, true>(A, tp, tm, o, wk, a.wp, 2 * XW + 1);
+    else sweep_row<KIND, KW, kRX, false>(A, tp, tm, o, wk, a.wp, 2 * XW + 1);
+  };
+  const int RyW = isqrt_t(MW);
+  for (int ay = 0; ay <= RyW; ++ay) {
+    const int XW = isqrt_t(MW - ay * ay), XN = MN > MW ? XW : isqrt_t(MN - ay * ay);
     if (XW < 0) continue;
-    const int wrow = (KIND == 0 ? (dy < 0 ? -dy : dy) : dy + H) * a.ws;
-    const int st = H - XW;                       // tile column of the window start minus 4 tx
-    const double2* tp = tile + static_cast<size_t>(cy + dy) * TW + tx + (st >> 2);
-    const double* wq = wt + wrow + (st & ~3);
-    const int nsteps = 2 * XW + 1;
-    switch (st & 3) {
-      case 0: sweep_row<KIND, KW, 0>(A, tp, Q, wq, a.wp, nsteps); break;
-      case 1: sweep_row<KIND, KW, 1>(A, tp, Q, wq, a.wp, nsteps); break;
-      case 2: sweep_row<KIND, KW, 2>(A, tp, Q, wq, a.wp, nsteps); break;
-      default: sweep_row<KIND, KW, 3>(A, tp, Q, wq, a.wp, nsteps); break;
+    if (KIND == 0) {
+      sweep(ay, ay == 0 ? TH : cy - ay, XW);
+    } else {
+      sweep(ay, 0, XW);
+      if (ay > 0) sweep(-ay, 0, XW);
     }
     if (XN >= XW) continue;
-    // remove the sweep's offsets outside each target's own span: warp-uniform
-    // offsets k = XN+1..XW, per-target selects
+    // remove the sweep's offsets outside each target's own span (warp-uniform
+    // offsets k = XN+1..XW, per-target selects); spans are even in dy
     int X[kRX];
 #pragma unroll
-    for (int r = 0; r < kRX; ++r) X[r] = isqrt_t(M[r] - dy * dy);
+    for (int r = 0; r < kRX; ++r) X[r] = isqrt_t(M[r] - ay * ay);
     for (int k = max(XN + 1, 0); k <= XW; ++k) {
 #pragma unroll
       for (int r = 0; r < kRX; ++r) {
+        if (!__any_sync(0xffffffffu, X[r] < k)) continue;
         const double sg = X[r] < k ? -1.0 : 0.0;
-        add(r, dy, k, wrow, sg);
-        if (k > 0) add(r, dy, -k, wrow, sg);
+        for (int sd = (ay == 0 ? 0 : -ay); sd <= ay; sd += (ay == 0 ? 1 : 2 * ay)) {
+          add(r, sd, k, sg);
+          if (k > 0) add(r, sd, -k, sg);
+        }
       }
     }
   }
-  // tie band: at most one |d|^2 per row, at x = +-X; the float predicate decides
-  if (tiem) {
-    for (int r = 0; r < kRX; ++r) {
-      if (!(tiem >> r & 1u)) continue;
-      const int64_t ix = x0 + kRX * tx + r;
-      const int64_t ii = (iy - g.in_begin) * n + ix;
-      const double delta = a.delta ? a.delta[ii] : a.delta0;
-      const int64_t ki[2] = {iy, ix};
-      const int Ry = isqrt_floor(mhi[r]);
-      for (int dy = -Ry; dy <= Ry; ++dy) {
-        const int X = isqrt_floor(mhi[r] - dy * dy);
-        const int m = dy * dy + X * X;
-        if (m < mlo[r] || m == 0) continue;
-        const int wrow = (KIND == 0 ? (dy < 0 ? -dy : dy) : dy + H) * a.ws;
-        for (int sx = -X; sx <= X; sx += (X > 0 ? 2 * X : 1)) {
-          const int d[2] = {dy, sx};
-          if (point_in<2>(ki, d, g.h, delta)) add(r, dy, sx, wrow, 1.0);
+  // tie band: at most one |d|^2 per row, at x = +-X; the float predicate
+  // decides. Rare: a dynamic loop over the lane's tie targets into scalars,
+  // then one static scatter (keeps the accumulators in registers).
+  while (tiem) {
+    const int rr = __ffs(tiem) - 1;
+    tiem &= tiem - 1;
+    const int64_t ix = x0 + kRX * tx + rr;
+    const int64_t ii = (iy - g.in_begin) * n + ix;
+    const double delta = a.delta ? a.delta[ii] : a.delta0;
+    const double e = delta * inv_h, e2 = e * e;
+    const int mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
+    const int mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+    const int64_t ki[2] = {iy, ix};
+    const int Ry = isqrt_floor(mhi);
+    double t0 = 0.0, t1 = 0.0;
+    for (int dy = -Ry; dy <= Ry; ++dy) {
+      const int X = isqrt_floor(mhi - dy * dy);
+      const int m = dy * dy + X * X;
+      if (m < mlo || m == 0) continue;
+      for (int sx = -X; sx <= X; sx += (X > 0 ? 2 * X : 1)) {
+        const int d[2] = {dy, sx};
+        if (!point_in<2>(ki, d, g.h, delta)) continue;
+        const double2 v = tv(dy, rr, sx);
+        const int t = wrow_of(dy) + sx + H;
+        if (KIND == 0) {
+          t0 = fma(wt[t], v.x, t0);
+          if (KW) t1 = fma(wt[t], v.y, t1);
+        } else {
+          t0 = fma(wt[t], v.x, fma(wt[a.wp + t], v.y, t0));
+          t1 = fma(wt[a.wp + t], v.x, fma(wt[2 * a.wp + t], v.y, t1));
         }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kRX; ++r) {
+      if (r == rr) {
+        A.a0[r] += t0;
+        A.a1[r] += t1;
       }
     }
   }
@@ -726,8 +759,8 @@ void launch_t(const StArgs& a, cudaStream_t s, size_t smem) {
 }
 
 size_t tile2d_bytes(const StArgs& a) {
-  return sizeof(double2) * static_cast<size_t>(kBY + 2 * a.H) * 4 * tile2d_q(a.H) + sizeof(double) * a.tab_len +
-         sizeof(int) * ((isq_len(a.H) + 1) & ~1) + sizeof(int2) * kWY * (2 * kRowMax + 1);
+  return sizeof(double2) * static_cast<size_t>(kBY + 2 * a.H + 1) * tile2d_rs(a.H) + sizeof(double) * a.tab_len +
+         sizeof(int) * isq_len(a.H);
 }
 
 void launch(const StArgs& a, cudaStream_t s, size_t smem) {
@@ -748,9 +781,9 @@ void launch(const StArgs& a, cudaStream_t s, size_t smem) {
     dim3 grid(static_cast<unsigned>((n + kBX - 1) / kBX),
               static_cast<unsigned>((a.g.row_end - a.g.row_begin + kBY - 1) / kBY));
     const size_t sb = tile2d_bytes(a);
-    if (a.kind == 1) stencil2d_kernel<1, false><<<grid, dim3(32, kWY), sb, s>>>(a);
-    else if (a.kw) stencil2d_kernel<0, true><<<grid, dim3(32, kWY), sb, s>>>(a);
-    else stencil2d_kernel<0, false><<<grid, dim3(32, kWY), sb, s>>>(a);
+    if (a.kind == 1) stencil2d_kernel<1, false, kR2Peri><<<grid, dim3(32, 32 / kR2Peri), sb, s>>>(a);
+    else if (a.kw) stencil2d_kernel<0, true, kR2Frac><<<grid, dim3(32, 32 / kR2Frac), sb, s>>>(a);
+    else stencil2d_kernel<0, false, kR2Frac><<<grid, dim3(32, 32 / kR2Frac), sb, s>>>(a);
     return;
   }
   if (dim == 3 && a.mode == 0) {
@@ -805,9 +838,9 @@ void smem_attr(K k) {
   NLG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 }
 void allow_smem() {
-  smem_attr(stencil2d_kernel<0, true>);
-  smem_attr(stencil2d_kernel<0, false>);
-  smem_attr(stencil2d_kernel<1, false>);
+  smem_attr(stencil2d_kernel<0, true, kR2Frac>);
+  smem_attr(stencil2d_kernel<0, false, kR2Frac>);
+  smem_attr(stencil2d_kernel<1, false, kR2Peri>);
   smem_attr(stencil1d_kernel<true>);
   smem_attr(stencil1d_kernel<false>);
   smem_attr(stencil3d_kernel<true>);
@@ -840,8 +873,8 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   S->dim = g.dim;
   S->kind = peri ? 1 : 0;
   S->H = H;
-  // 2-D rows are read as aligned quads up to index 2H+7
-  S->ws = g.dim == 2 ? ((2 * H + 8 + 3) & ~3) : 2 * H + 1;
+  // 2-D rows are read as aligned quads up to index 2H+11
+  S->ws = g.dim == 2 ? ((2 * H + 12 + 3) & ~3) : 2 * H + 1;
   if (frac) {
     // symmetric rows: w[(az * W1 + ay) * W2 + dx + H] = |(az, ay, dx)|^-alpha, w = 0 at the origin
     const int W1 = H + 1, W2 = S->ws;
@@ -882,7 +915,7 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   }
   S->scale = upload_vec(sc);
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * P.n_out * (peri ? 3 : 1)));
-  if (frac && d.kappa) NLG_CUDA(cudaMalloc(&S->pack, sizeof(double2) * P.n_in));
+  if (frac && d.kappa && g.dim != 2) NLG_CUDA(cudaMalloc(&S->pack, sizeof(double2) * P.n_in));
   P.st_state = S;
   allow_smem();
   // diag: MODE 1 over the same sets and tables
@@ -895,7 +928,7 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
 
 void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   StencilState* S = P.st_state;
-  if (S->pack) {
+  if (S->pack && S->dim != 2) {
     pack_kernel<<<static_cast<unsigned>((P.n_in + 255) / 256), 256, 0, s>>>(
         u, P.d_kappa, P.n_in, reinterpret_cast<double2*>(S->pack));
   }
