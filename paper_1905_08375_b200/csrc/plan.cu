@@ -292,7 +292,7 @@ void fast_dev(Plan& P, const double* u, double* out, cudaStream_t s) {
       cudaEvent_t ev;
       stage_begin(P, s, kStStencil, &ev);
       stencil_apply(P, u, out, s);
-      stage_end(P, s, kStStencil, ev, P.d_kappa && P.family == NLG_FRACTIONAL && P.geom.dim != 2 ? 2 : 1);
+      stage_end(P, s, kStStencil, ev, P.d_kappa && P.family == NLG_FRACTIONAL && P.geom.dim == 1 ? 2 : 1);
       break;
     }
     default: {

@@ -62,6 +62,15 @@ struct StArgs {
 
 __device__ __forceinline__ double node_c(int64_t k, double h) { return coord(k, h); }
 
+// smallest double x with sqrt_rn(x) >= delta: the reference's predicate
+// sqrt(r2) < delta is r2 < T exactly (sqrt_rn is monotone)
+__device__ __forceinline__ double sqrt_threshold(double delta) {
+  double t = __dmul_rn(delta, delta);   // positive: neighbours are +-1 in the bit pattern
+  while (t > 0.0 && __dsqrt_rn(t) >= delta) t = __longlong_as_double(__double_as_longlong(t) - 1);
+  while (__dsqrt_rn(t) < delta) t = __longlong_as_double(__double_as_longlong(t) + 1);
+  return t;
+}
+
 // exact Point-rule membership for an offset (the tie band only)
 template <int DIM>
 __device__ __forceinline__ bool point_in(const int64_t* ki, const int* d, double h, double delta) {
@@ -333,7 +342,10 @@ constexpr int kBX = 32, kBY = 32;
 #ifndef NLG_R2PERI
 #define NLG_R2PERI 4
 #endif
-constexpr int kR2Frac = NLG_R2FRAC, kR2Peri = NLG_R2PERI;   // targets per lane
+#ifndef NLG_R3FRAC
+#define NLG_R3FRAC 8
+#endif
+constexpr int kR2Frac = NLG_R2FRAC, kR2Peri = NLG_R2PERI, kR3Frac = NLG_R3FRAC;   // targets per lane
 
 __host__ __device__ inline int tile2d_q(int H) { return kBX / 4 + 2 + H / 2; }   // slots per plane
 __host__ __device__ inline int tile2d_rs(int H) { return 4 * tile2d_q(H) + 1; }  // row stride in slots (odd)
@@ -416,75 +428,56 @@ __device__ __forceinline__ void sweep_row(Acc2<KIND, KW, kRX>& A, const double2*
   if (left > 0) chunk(std::true_type{}, left);
 }
 
-template <int KIND, bool KW, int kRX>
-__global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil2d_kernel(StArgs a) {
+// DIM 2: one tile of kBY x kBX targets. DIM 3: the same tile in one target
+// plane z, the source planes z + dz visited one at a time (staged in shared
+// memory, the in-plane sweep as in 2-D with |d|^2 budgets reduced by dz^2);
+// the grid runs z fastest so the blocks in flight share their source planes
+// in L2.
+template <int DIM, int KIND, bool KW, int kRX>
+__global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kernel(StArgs a) {
   constexpr int kLX = 32 / kRX, kLY = kRX, kWY = 32 / kRX;
   extern __shared__ __align__(16) double sm[];
   const int H = a.H, Q = tile2d_q(H), RS = tile2d_rs(H), TH = kBY + 2 * H, TWc = 4 * Q;
   double2* tile = reinterpret_cast<double2*>(sm);          // [TH][RS slots: 4 planes x Q, +1 pad]
   double* wt = sm + 2 * static_cast<size_t>(TH + 1) * RS;  // row TH: zeros (partner of row 0)
-  int* isq = reinterpret_cast<int*>(wt + a.tab_len);       // isqrt table for 0..(H+1)^2
+  // weights in shared memory: the whole table (2-D) or the rows of the current |dz| (3-D)
+  const int wlen = DIM == 2 ? a.tab_len : (H + 1) * a.ws;
+  int* isq = reinterpret_cast<int*>(wt + wlen);            // isqrt table for 0..(H+1)^2
+  int* bmax = isq + isq_len(H);                            // block max of M (3-D plane range)
   const int tid = threadIdx.y * 32 + threadIdx.x;
   for (int i = tid; i < RS; i += 32 * kWY) tile[static_cast<size_t>(TH) * RS + i] = make_double2(0.0, 0.0);
-  for (int i = tid; i < a.tab_len; i += 32 * kWY) wt[i] = a.tab[i];
+  if (DIM == 2)
+    for (int i = tid; i < wlen; i += 32 * kWY) wt[i] = a.tab[i];
   for (int i = tid; i < isq_len(H); i += 32 * kWY) {
     int x = static_cast<int>(sqrtf(static_cast<float>(i)));
     while (x * x > i) --x;
     while ((x + 1) * (x + 1) <= i) ++x;
     isq[i] = x;
   }
+  if (tid == 0) *bmax = -1;
   const Geom& g = a.g;
   const int64_t n = g.n;
-  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kBX;
-  const int64_t y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * kBY;
+  // tile origin: 2-D (x0, y0) from the grid; 3-D z fastest, then the x-y tile
+  int64_t x0, y0, z = 0;
+  if (DIM == 2) {
+    x0 = static_cast<int64_t>(blockIdx.x) * kBX;
+    y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * kBY;
+  } else {
+    const int64_t ntx = (n + kBX - 1) / kBX;
+    z = g.row_begin + blockIdx.x;
+    x0 = (blockIdx.y % ntx) * kBX;
+    y0 = (blockIdx.y / ntx) * kBY;
+  }
+  const int64_t ystop = DIM == 2 ? g.row_end : n;
   const int64_t nin_total = (g.in_end - g.in_begin) * g.stride0;
-  // staging with cp.async (every load of a thread in flight at once; zero fill
-  // outside the domain / slab): lane i of a 32-column group takes column
-  // 4 (i & 7) + (i >> 3), so each quarter warp fills consecutive slots of one plane
-  const int cl = 4 * (threadIdx.x & 7) + (threadIdx.x >> 3);
-  for (int ty = threadIdx.y; ty < TH; ty += kWY) {
-    const int64_t gy = y0 - H + ty;
-    const bool yin = gy >= 0 && gy < n && gy >= g.in_begin && gy < g.in_end;
-    const int64_t rowk = (gy - g.in_begin) * n;
-    double2* trow = tile + static_cast<size_t>(ty) * RS;
-    for (int c0 = 0; c0 < TWc; c0 += 32) {
-      const int c = c0 + cl;
-      if (c >= TWc) continue;
-      const int64_t gx = x0 - H + c;
-      const bool in = yin && gx >= 0 && gx < n;
-      const int64_t k = in ? rowk + gx : 0;
-      double* dst = reinterpret_cast<double*>(trow + (c & 3) * Q + (c >> 2));
-      if (KIND == 1) {
-        cp_async8(dst, a.u + k, in);
-        cp_async8(dst + 1, a.u + nin_total + k, in);
-      } else if (KW) {
-        cp_async8(dst, a.u + k, in);
-        cp_async8(dst + 1, a.kappa + k, in);
-      } else {
-        cp_async8(dst, a.u + k, in);
-        cp_async8(dst + 1, a.u + k, false);
-      }
-    }
-  }
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  if (KW) {   // (u, kappa) -> (u, kappa u) on the thread's own slots
-    for (int ty = threadIdx.y; ty < TH; ty += kWY) {
-      double2* trow = tile + static_cast<size_t>(ty) * RS;
-      for (int c0 = 0; c0 < TWc; c0 += 32) {
-        const int c = c0 + cl;
-        if (c >= TWc) continue;
-        double2* dst = trow + (c & 3) * Q + (c >> 2);
-        const double2 v = *dst;
-        dst->y = v.y * v.x;
-      }
-    }
-  }
-  __syncthreads();
   const int tx = threadIdx.x & (kLX - 1);                   // lane column
   const int wy = threadIdx.y * kLY + threadIdx.x / kLX;     // target row within the CTA
   const int64_t iy = y0 + wy;
-  const bool yok = iy < g.row_end;
+  const bool yok = iy < ystop;
   const double inv_h = 1.0 / g.h;
+  auto in_index = [&](int64_t ix) {
+    return DIM == 2 ? (iy - g.in_begin) * n + ix : ((z - g.in_begin) * n + iy) * n + ix;
+  };
   // targets of this lane: M = largest |d|^2 surely inside (below the tie band)
   int M[kRX];
   unsigned tiem = 0;
@@ -494,7 +487,7 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil2d_kernel
     const int64_t ix = x0 + kRX * tx + r;
     M[r] = -1;
     if (yok && ix < n) {
-      const int64_t ii = (iy - g.in_begin) * n + ix;
+      const int64_t ii = in_index(ix);
       const double e = (a.delta ? a.delta[ii] : a.delta0) * inv_h, e2 = e * e;
       const int mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
       const int mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
@@ -504,24 +497,48 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil2d_kernel
     }
     Mx = max(Mx, M[r]);
   }
-  auto isqrt_t = [&](int m) { return m < 0 ? -1 : isq[m]; };
-  // row plan of the warp: isqrt is monotone, so the widest / narrowest half
-  // span on a row come from the warp's largest / smallest live M
   const int MW = __reduce_max_sync(0xffffffffu, Mx);
   const int MN = __reduce_min_sync(0xffffffffu, Mn);
+  const bool tie_const = a.delta == nullptr;
+  int m0c = -1;
+  double Tc = 0.0;
+  if (tie_const) {
+    const double e = a.delta0 * inv_h, e2 = e * e;
+    const int mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
+    const int mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+    if (mlo <= mhi) {
+      m0c = mlo;
+      Tc = sqrt_threshold(a.delta0);
+    }
+  }
+  __syncthreads();
+  if (DIM == 3) {
+    int Mt = Mx;                                 // tie bands sit at M + 1
+#pragma unroll
+    for (int r = 0; r < kRX; ++r)
+      if (tiem >> r & 1u) Mt = max(Mt, M[r] + 1);
+    Mt = __reduce_max_sync(0xffffffffu, Mt);
+    if ((threadIdx.x & 31) == 0) atomicMax(bmax, Mt);
+  }
+  __syncthreads();
+  auto isqrt_t = [&](int m) { return m < 0 ? -1 : isq[m]; };
+  const int Rz = DIM == 3 ? isqrt_t(*bmax) : 0;
   Acc2<KIND, KW, kRX> A;
 #pragma unroll
   for (int r = 0; r < kRX; ++r) A.a0[r] = A.a1[r] = 0.0;
   const int cy = wy + H;
-  // tile value of this lane's target r at offset (dy, k)
   auto tv = [&](int dy, int r, int k) {
     const int c = kRX * tx + r + H + k;
     return tile[static_cast<size_t>(cy + dy) * RS + (c & 3) * Q + (c >> 2)];
   };
-  auto wrow_of = [&](int dy) { return (KIND == 0 ? (dy < 0 ? -dy : dy) : dy + H) * a.ws; };
-  auto add = [&](int r, int dy, int k, double sg) {
+  auto wrow_of = [&](int az, int dy) {
+    (void)az;
+    const int ay = dy < 0 ? -dy : dy;
+    return (KIND == 0 ? ay : dy + H) * a.ws;
+  };
+  auto add = [&](int r, int az, int dy, int k, double sg) {
     const double2 v = tv(dy, r, k);
-    const int t = wrow_of(dy) + k + H;
+    const int t = wrow_of(az, dy) + k + H;
     if (KIND == 0) {
       const double w = sg * wt[t];
       A.a0[r] = fma(w, v.x, A.a0[r]);
@@ -533,7 +550,7 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil2d_kernel
     }
   };
   // KIND 0 sweeps rows +ay / -ay together; row 0 pairs with the zero row TH
-  auto sweep = [&](int dy, int dm, int XW) {
+  auto sweep = [&](int az, int dy, int dm, int XW) {
     const int st = H - XW;                       // start column relative to the lane's first target - H
     const int ph = st & 3;
     int o[4];
@@ -541,96 +558,183 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil2d_kernel
     for (int j = 0; j < 4; ++j) o[j] = ((ph + j) & 3) * Q + ((ph + j) >> 2);
     const double2* tp = tile + static_cast<size_t>(cy + dy) * RS + (kRX / 4) * tx + (st >> 2);
     const double2* tm = tile + static_cast<size_t>(dm) * RS + (kRX / 4) * tx + (st >> 2);
-    const double* wk = wt + wrow_of(dy) + st;
+    const double* wk = wt + wrow_of(az, dy) + st;
     if (KIND == 0) sweep_row<KIND, KW, kRX, true>(A, tp, tm, o, wk, a.wp, 2 * XW + 1);
     else sweep_row<KIND, KW, kRX, false>(A, tp, tm, o, wk, a.wp, 2 * XW + 1);
   };
-  const int RyW = isqrt_t(MW);
-  for (int ay = 0; ay <= RyW; ++ay) {
-    const int XW = isqrt_t(MW - ay * ay), XN = MN > MW ? XW : isqrt_t(MN - ay * ay);
-    if (XW < 0) continue;
-    if (KIND == 0) {
-      sweep(ay, ay == 0 ? TH : cy - ay, XW);
-    } else {
-      sweep(ay, 0, XW);
-      if (ay > 0) sweep(-ay, 0, XW);
+  // staging with cp.async (every load of a thread in flight at once; zero fill
+  // outside the domain / slab): lane i of a 32-column group takes column
+  // 4 (i & 7) + (i >> 3), so each quarter warp fills consecutive slots of one plane
+  const int cl = 4 * (threadIdx.x & 7) + (threadIdx.x >> 3);
+  auto stage = [&](int64_t gz, int az) {
+    if (DIM == 3)
+      for (int i = tid; i < wlen; i += 32 * kWY) wt[i] = a.tab[static_cast<size_t>(az) * wlen + i];
+    const bool zin = DIM == 2 || (gz >= 0 && gz < n && gz >= g.in_begin && gz < g.in_end);
+    for (int ty = threadIdx.y; ty < TH; ty += kWY) {
+      const int64_t gy = y0 - H + ty;
+      const bool yin = zin && gy >= 0 && gy < n && (DIM == 3 || (gy >= g.in_begin && gy < g.in_end));
+      const int64_t rowk = DIM == 2 ? (gy - g.in_begin) * n : ((gz - g.in_begin) * n + gy) * n;
+      double2* trow = tile + static_cast<size_t>(ty) * RS;
+      for (int c0 = 0; c0 < TWc; c0 += 32) {
+        const int c = c0 + cl;
+        if (c >= TWc) continue;
+        const int64_t gx = x0 - H + c;
+        const bool in = yin && gx >= 0 && gx < n;
+        const int64_t k = in ? rowk + gx : 0;
+        double* dst = reinterpret_cast<double*>(trow + (c & 3) * Q + (c >> 2));
+        if (KIND == 1) {
+          cp_async8(dst, a.u + k, in);
+          cp_async8(dst + 1, a.u + nin_total + k, in);
+        } else if (KW) {
+          cp_async8(dst, a.u + k, in);
+          cp_async8(dst + 1, a.kappa + k, in);
+        } else {
+          cp_async8(dst, a.u + k, in);
+          cp_async8(dst + 1, a.u + k, false);
+        }
+      }
     }
-    if (XN >= XW) continue;
-    // remove the sweep's offsets outside each target's own span (warp-uniform
-    // offsets k = XN+1..XW, per-target selects); spans are even in dy
-    int X[kRX];
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (KW) {   // (u, kappa) -> (u, kappa u) on the thread's own slots
+      for (int ty = threadIdx.y; ty < TH; ty += kWY) {
+        double2* trow = tile + static_cast<size_t>(ty) * RS;
+        for (int c0 = 0; c0 < TWc; c0 += 32) {
+          const int c = c0 + cl;
+          if (c >= TWc) continue;
+          double2* dst = trow + (c & 3) * Q + (c >> 2);
+          const double2 v = *dst;
+          dst->y = v.y * v.x;
+        }
+      }
+    }
+    __syncthreads();
+  };
+  for (int dz = -Rz; dz <= Rz; ++dz) {
+    const int az = dz < 0 ? -dz : dz, dz2 = dz * dz;
+    if (DIM == 3) __syncthreads();               // the previous plane is consumed
+    stage(z + dz, az);
+    const int mW = MW - dz2, mN = MN - dz2;
+    const int RyW = isqrt_t(mW);
+    for (int ay = 0; ay <= RyW; ++ay) {
+      const int XW = isqrt_t(mW - ay * ay), XN = MN > MW ? XW : isqrt_t(mN - ay * ay);
+      if (XW < 0) continue;
+      if (KIND == 0) {
+        sweep(az, ay, ay == 0 ? TH : cy - ay, XW);
+      } else {
+        sweep(az, ay, 0, XW);
+        if (ay > 0) sweep(az, -ay, 0, XW);
+      }
+      if (XN >= XW) continue;
+      // remove the sweep's offsets outside each target's own span (warp-uniform
+      // offsets k = XN+1..XW, per-target selects); spans are even in dy
+      int X[kRX];
 #pragma unroll
-    for (int r = 0; r < kRX; ++r) X[r] = isqrt_t(M[r] - ay * ay);
-    for (int k = max(XN + 1, 0); k <= XW; ++k) {
+      for (int r = 0; r < kRX; ++r) X[r] = isqrt_t(M[r] - dz2 - ay * ay);
+      for (int k = max(XN + 1, 0); k <= XW; ++k) {
+#pragma unroll
+        for (int r = 0; r < kRX; ++r) {
+          if (!__any_sync(0xffffffffu, X[r] < k)) continue;
+          const double sg = X[r] < k ? -1.0 : 0.0;
+          for (int sd = (ay == 0 ? 0 : -ay); sd <= ay; sd += (ay == 0 ? 1 : 2 * ay)) {
+            add(r, az, sd, k, sg);
+            if (k > 0) add(r, az, sd, -k, sg);
+          }
+        }
+      }
+    }
+    // tie band of this plane: |d|^2 = m0 exactly, decided by the reference's
+    // float predicate. Constant horizon: every target shares m0 and the
+    // threshold, so the warp walks the lattice points of the sphere uniformly
+    // and each target tests r2 < T on its own coordinates.
+    if (tie_const) {
+      const int rem0 = m0c - dz2;
+      if (m0c >= 0 && rem0 >= 0) {
+        const int Ry = isq[rem0];
+        const double ddz = DIM == 3 ? __dsub_rn(coord(z + dz, g.h), coord(z, g.h)) : 0.0;
+        for (int dy = -Ry; dy <= Ry; ++dy) {
+          const int rem = rem0 - dy * dy, X = isq[rem];
+          if (X * X != rem || (dz == 0 && dy == 0 && X == 0)) continue;
+          const double ddy = __dsub_rn(coord(iy + dy, g.h), coord(iy, g.h));
+          const double base = DIM == 3 ? __dadd_rn(__dmul_rn(ddz, ddz), __dmul_rn(ddy, ddy)) : __dmul_rn(ddy, ddy);
+          for (int sx = -X; sx <= X; sx += (X > 0 ? 2 * X : 1)) {
+#pragma unroll
+            for (int r = 0; r < kRX; ++r) {
+              const int64_t ix = x0 + kRX * tx + r;
+              const double ddx = __dsub_rn(coord(ix + sx, g.h), coord(ix, g.h));
+              const bool in = M[r] >= 0 && __dadd_rn(base, __dmul_rn(ddx, ddx)) < Tc;
+              add(r, az, dy, sx, in ? 1.0 : 0.0);
+            }
+          }
+        }
+      }
+      continue;
+    }
+    // variable horizon: ties are rare; a dynamic loop over the lane's tie
+    // targets into scalars, then one static scatter (keeps the accumulators in
+    // registers)
+    unsigned tm = tiem;
+    while (tm) {
+      const int rr = __ffs(tm) - 1;
+      tm &= tm - 1;
+      const int64_t ix = x0 + kRX * tx + rr;
+      const double delta = a.delta ? a.delta[in_index(ix)] : a.delta0;
+      const double e = delta * inv_h, e2 = e * e;
+      const int mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
+      const int mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+      const int64_t ki[3] = {DIM == 2 ? iy : z, DIM == 2 ? ix : iy, ix};
+      const int Ry = isqrt_floor(mhi - dz2);
+      double t0 = 0.0, t1 = 0.0;
+      for (int dy = -Ry; dy <= Ry; ++dy) {
+        const int X = isqrt_floor(mhi - dz2 - dy * dy);
+        const int m = dz2 + dy * dy + X * X;
+        if (m < mlo || m == 0) continue;
+        for (int sx = -X; sx <= X; sx += (X > 0 ? 2 * X : 1)) {
+          bool in;
+          if (DIM == 2) {
+            const int d[2] = {dy, sx};
+            in = point_in<2>(ki, d, g.h, delta);
+          } else {
+            const int d[3] = {dz, dy, sx};
+            in = point_in<3>(ki, d, g.h, delta);
+          }
+          if (!in) continue;
+          const double2 v = tv(dy, rr, sx);
+          const int t = wrow_of(az, dy) + sx + H;
+          if (KIND == 0) {
+            t0 = fma(wt[t], v.x, t0);
+            if (KW) t1 = fma(wt[t], v.y, t1);
+          } else {
+            t0 = fma(wt[t], v.x, fma(wt[a.wp + t], v.y, t0));
+            t1 = fma(wt[a.wp + t], v.x, fma(wt[2 * a.wp + t], v.y, t1));
+          }
+        }
+      }
 #pragma unroll
       for (int r = 0; r < kRX; ++r) {
-        if (!__any_sync(0xffffffffu, X[r] < k)) continue;
-        const double sg = X[r] < k ? -1.0 : 0.0;
-        for (int sd = (ay == 0 ? 0 : -ay); sd <= ay; sd += (ay == 0 ? 1 : 2 * ay)) {
-          add(r, sd, k, sg);
-          if (k > 0) add(r, sd, -k, sg);
+        if (r == rr) {
+          A.a0[r] += t0;
+          A.a1[r] += t1;
         }
-      }
-    }
-  }
-  // tie band: at most one |d|^2 per row, at x = +-X; the float predicate
-  // decides. Rare: a dynamic loop over the lane's tie targets into scalars,
-  // then one static scatter (keeps the accumulators in registers).
-  while (tiem) {
-    const int rr = __ffs(tiem) - 1;
-    tiem &= tiem - 1;
-    const int64_t ix = x0 + kRX * tx + rr;
-    const int64_t ii = (iy - g.in_begin) * n + ix;
-    const double delta = a.delta ? a.delta[ii] : a.delta0;
-    const double e = delta * inv_h, e2 = e * e;
-    const int mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
-    const int mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
-    const int64_t ki[2] = {iy, ix};
-    const int Ry = isqrt_floor(mhi);
-    double t0 = 0.0, t1 = 0.0;
-    for (int dy = -Ry; dy <= Ry; ++dy) {
-      const int X = isqrt_floor(mhi - dy * dy);
-      const int m = dy * dy + X * X;
-      if (m < mlo || m == 0) continue;
-      for (int sx = -X; sx <= X; sx += (X > 0 ? 2 * X : 1)) {
-        const int d[2] = {dy, sx};
-        if (!point_in<2>(ki, d, g.h, delta)) continue;
-        const double2 v = tv(dy, rr, sx);
-        const int t = wrow_of(dy) + sx + H;
-        if (KIND == 0) {
-          t0 = fma(wt[t], v.x, t0);
-          if (KW) t1 = fma(wt[t], v.y, t1);
-        } else {
-          t0 = fma(wt[t], v.x, fma(wt[a.wp + t], v.y, t0));
-          t1 = fma(wt[a.wp + t], v.x, fma(wt[2 * a.wp + t], v.y, t1));
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < kRX; ++r) {
-      if (r == rr) {
-        A.a0[r] += t0;
-        A.a1[r] += t1;
       }
     }
   }
   if (!yok) return;
-  const int64_t nout = (g.row_end - g.row_begin) * n;
+  const int64_t plane_out = DIM == 2 ? (g.row_end - g.row_begin) * n : (g.row_end - g.row_begin) * n * n;
 #pragma unroll
   for (int r = 0; r < kRX; ++r) {
     const int64_t ix = x0 + kRX * tx + r;
     if (ix >= n) break;
-    const int64_t ii = (iy - g.in_begin) * n + ix;
-    const int64_t oi = (iy - g.row_begin) * n + ix;
-    const double2 u = tv(0, r, 0);
+    const int64_t ii = in_index(ix);
+    const int64_t oi = ii - (g.row_begin - g.in_begin) * g.stride0;
     if (KIND == 0) {
       const double X = KW ? fma(a.kappa[ii], A.a0[r], A.a1[r]) : A.a0[r];
-      a.out[oi] = a.scale[oi] * (X - u.x * a.diag[oi]);
+      a.out[oi] = a.scale[oi] * (X - a.u[ii] * a.diag[oi]);
     } else {
-      const double dxx = a.diag[oi], dxy = a.diag[nout + oi], dyy = a.diag[2 * nout + oi];
+      const double ux = a.u[ii], uy = a.u[nin_total + ii];
+      const double dxx = a.diag[oi], dxy = a.diag[plane_out + oi], dyy = a.diag[2 * plane_out + oi];
       const double sc = a.scale[oi];
-      a.out[oi] = sc * (A.a0[r] - (dxx * u.x + dxy * u.y));
-      a.out[nout + oi] = sc * (A.a1[r] - (dxy * u.x + dyy * u.y));
+      a.out[oi] = sc * (A.a0[r] - (dxx * ux + dxy * uy));
+      a.out[plane_out + oi] = sc * (A.a1[r] - (dxy * ux + dyy * uy));
     }
   }
 }
@@ -678,61 +782,6 @@ __global__ void __launch_bounds__(k1T) stencil1d_kernel(StArgs a) {
   a.out[oi] = a.scale[oi] * (X - trow[0].x * a.diag[oi]);
 }
 
-// 3-D fractional apply, one thread per target, sources through L1.
-template <bool KW>
-__global__ void __launch_bounds__(128) stencil3d_kernel(StArgs a) {
-  extern __shared__ double wt[];
-  for (int i = threadIdx.x; i < a.tab_len; i += blockDim.x) wt[i] = a.tab[i];
-  __syncthreads();
-  const Geom& g = a.g;
-  const int64_t n = g.n;
-  const int H = a.H, W1 = H + 1, W2 = 2 * H + 1;
-  const int64_t bx = (n + 31) / 32, by = (n + 3) / 4;
-  const int64_t b = blockIdx.x;
-  const int64_t ix = (b % bx) * 32 + (threadIdx.x & 31);
-  const int64_t iy = ((b / bx) % by) * 4 + (threadIdx.x >> 5);
-  const int64_t iz = g.row_begin + b / (bx * by);
-  if (ix >= n || iy >= n || iz >= g.row_end) return;
-  const int64_t plane = n * n;
-  const int64_t ii = (iz - g.in_begin) * plane + iy * n + ix;
-  Ball<3> B;
-  B.init(a.delta ? a.delta[ii] : a.delta0, g.h);
-  B.ki[0] = iz;
-  B.ki[1] = iy;
-  B.ki[2] = ix;
-  const int Rz = isqrt_floor(B.mhi);
-  double acc0 = 0.0, acc1 = 0.0;
-  const double2* pk = a.pk;
-  for (int dz = -Rz; dz <= Rz; ++dz) {
-    const int64_t gz = iz + dz;
-    if (gz < 0 || gz >= n) continue;
-    const int Ry = isqrt_floor(B.mhi - dz * dz);
-    const int az = dz < 0 ? -dz : dz;
-    for (int dy = -Ry; dy <= Ry; ++dy) {
-      const int64_t gy = iy + dy;
-      if (gy < 0 || gy >= n) continue;
-      int d[3] = {dz, dy, 0};
-      int xm, xp;
-      if (!B.span(d, xm, xp)) continue;
-      if (xm > ix) xm = static_cast<int>(ix);                      // clip to the domain (zero field)
-      if (xp > n - 1 - ix) xp = static_cast<int>(n - 1 - ix);
-      const int64_t row = (gz - g.in_begin) * plane + gy * n + ix;
-      const double* wrow = wt + (az * W1 + (dy < 0 ? -dy : dy)) * W2 + H;
-      if (KW) {
-        row_sum<true>(pk + row, wrow, xm, xp, acc0, acc1);
-      } else {
-        double s0 = 0.0;
-        for (int k = -xm; k <= xp; ++k) s0 = fma(wrow[k], __ldg(a.u + row + k), s0);
-        acc0 += s0;
-      }
-    }
-  }
-  const int64_t oi = (iz - g.row_begin) * plane + iy * n + ix;
-  const double ui = KW ? a.pk[ii].x : a.u[ii];
-  const double X = KW ? fma(a.kappa[ii], acc0, acc1) : acc0;
-  a.out[oi] = a.scale[oi] * (X - ui * a.diag[oi]);
-}
-
 __global__ void pack_kernel(const double* u, const double* kappa, int64_t n, double2* pk) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) {
@@ -759,8 +808,9 @@ void launch_t(const StArgs& a, cudaStream_t s, size_t smem) {
 }
 
 size_t tile2d_bytes(const StArgs& a) {
-  return sizeof(double2) * static_cast<size_t>(kBY + 2 * a.H + 1) * tile2d_rs(a.H) + sizeof(double) * a.tab_len +
-         sizeof(int) * isq_len(a.H);
+  const size_t wlen = a.g.dim == 2 ? a.tab_len : static_cast<size_t>(a.H + 1) * a.ws;
+  return sizeof(double2) * static_cast<size_t>(kBY + 2 * a.H + 1) * tile2d_rs(a.H) + sizeof(double) * wlen +
+         sizeof(int) * (isq_len(a.H) + 1);
 }
 
 void launch(const StArgs& a, cudaStream_t s, size_t smem) {
@@ -781,15 +831,17 @@ void launch(const StArgs& a, cudaStream_t s, size_t smem) {
     dim3 grid(static_cast<unsigned>((n + kBX - 1) / kBX),
               static_cast<unsigned>((a.g.row_end - a.g.row_begin + kBY - 1) / kBY));
     const size_t sb = tile2d_bytes(a);
-    if (a.kind == 1) stencil2d_kernel<1, false, kR2Peri><<<grid, dim3(32, 32 / kR2Peri), sb, s>>>(a);
-    else if (a.kw) stencil2d_kernel<0, true, kR2Frac><<<grid, dim3(32, 32 / kR2Frac), sb, s>>>(a);
-    else stencil2d_kernel<0, false, kR2Frac><<<grid, dim3(32, 32 / kR2Frac), sb, s>>>(a);
+    if (a.kind == 1) stencil_rb_kernel<2, 1, false, kR2Peri><<<grid, dim3(32, 32 / kR2Peri), sb, s>>>(a);
+    else if (a.kw) stencil_rb_kernel<2, 0, true, kR2Frac><<<grid, dim3(32, 32 / kR2Frac), sb, s>>>(a);
+    else stencil_rb_kernel<2, 0, false, kR2Frac><<<grid, dim3(32, 32 / kR2Frac), sb, s>>>(a);
     return;
   }
   if (dim == 3 && a.mode == 0) {
-    const int64_t blocks = ((n + 31) / 32) * ((n + 3) / 4) * (a.g.row_end - a.g.row_begin);
-    if (a.kw) stencil3d_kernel<true><<<static_cast<unsigned>(blocks), 128, smem, s>>>(a);
-    else stencil3d_kernel<false><<<static_cast<unsigned>(blocks), 128, smem, s>>>(a);
+    const int64_t ntx = (n + kBX - 1) / kBX;
+    dim3 grid(static_cast<unsigned>(a.g.row_end - a.g.row_begin), static_cast<unsigned>(ntx * ntx));
+    const size_t sb = tile2d_bytes(a);
+    if (a.kw) stencil_rb_kernel<3, 0, true, kR3Frac><<<grid, dim3(32, 32 / kR3Frac), sb, s>>>(a);
+    else stencil_rb_kernel<3, 0, false, kR3Frac><<<grid, dim3(32, 32 / kR3Frac), sb, s>>>(a);
     return;
   }
   if (a.kind == 1) {
@@ -838,13 +890,13 @@ void smem_attr(K k) {
   NLG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 }
 void allow_smem() {
-  smem_attr(stencil2d_kernel<0, true, kR2Frac>);
-  smem_attr(stencil2d_kernel<0, false, kR2Frac>);
-  smem_attr(stencil2d_kernel<1, false, kR2Peri>);
+  smem_attr(stencil_rb_kernel<2, 0, true, kR2Frac>);
+  smem_attr(stencil_rb_kernel<2, 0, false, kR2Frac>);
+  smem_attr(stencil_rb_kernel<2, 1, false, kR2Peri>);
+  smem_attr(stencil_rb_kernel<3, 0, true, kR3Frac>);
+  smem_attr(stencil_rb_kernel<3, 0, false, kR3Frac>);
   smem_attr(stencil1d_kernel<true>);
   smem_attr(stencil1d_kernel<false>);
-  smem_attr(stencil3d_kernel<true>);
-  smem_attr(stencil3d_kernel<false>);
   smem_attr(stencil_kernel<1, 0, 1, true>);
   smem_attr(stencil_kernel<1, 0, 1, false>);
   smem_attr(stencil_kernel<2, 0, 0, true>);
@@ -873,8 +925,8 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   S->dim = g.dim;
   S->kind = peri ? 1 : 0;
   S->H = H;
-  // 2-D rows are read as aligned quads up to index 2H+11
-  S->ws = g.dim == 2 ? ((2 * H + 12 + 3) & ~3) : 2 * H + 1;
+  // 2-D / 3-D rows are read up to index 2H+11 by the register-blocked sweep
+  S->ws = g.dim >= 2 ? ((2 * H + 12 + 3) & ~3) : 2 * H + 1;
   if (frac) {
     // symmetric rows: w[(az * W1 + ay) * W2 + dx + H] = |(az, ay, dx)|^-alpha, w = 0 at the origin
     const int W1 = H + 1, W2 = S->ws;
@@ -915,7 +967,7 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   }
   S->scale = upload_vec(sc);
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * P.n_out * (peri ? 3 : 1)));
-  if (frac && d.kappa && g.dim != 2) NLG_CUDA(cudaMalloc(&S->pack, sizeof(double2) * P.n_in));
+  if (frac && d.kappa && g.dim == 1) NLG_CUDA(cudaMalloc(&S->pack, sizeof(double2) * P.n_in));
   P.st_state = S;
   allow_smem();
   // diag: MODE 1 over the same sets and tables
@@ -928,7 +980,7 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
 
 void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   StencilState* S = P.st_state;
-  if (S->pack && S->dim != 2) {
+  if (S->pack) {
     pack_kernel<<<static_cast<unsigned>((P.n_in + 255) / 256), 256, 0, s>>>(
         u, P.d_kappa, P.n_in, reinterpret_cast<double2*>(S->pack));
   }
