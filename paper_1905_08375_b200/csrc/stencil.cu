@@ -549,6 +549,17 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
       A.a1[r] = fma(mxy, v.x, fma(myy, v.y, A.a1[r]));
     }
   };
+  // one plane's value at (gz, iy + dy, x_r + sx) straight from global memory
+  // (3-D tie points decided differently on the two mirrored planes)
+  auto lone_side = [&](int r, int dy, int sx, int64_t gz) {
+    const int64_t gy = iy + dy, gx = x0 + kRX * tx + r + sx;
+    if (gz < 0 || gz >= n || gz < g.in_begin || gz >= g.in_end || gy < 0 || gy >= n || gx < 0 || gx >= n) return;
+    const int64_t k = ((gz - g.in_begin) * n + gy) * n + gx;
+    const double w = wt[wrow_of(0, dy) + sx + H];
+    const double uu = a.u[k];
+    A.a0[r] = fma(w, uu, A.a0[r]);
+    if (KW) A.a1[r] = fma(w, a.kappa[k] * uu, A.a1[r]);
+  };
   // KIND 0 sweeps rows +ay / -ay together; row 0 pairs with the zero row TH
   auto sweep = [&](int az, int dy, int dm, int XW) {
     const int st = H - XW;                       // start column relative to the lane's first target - H
@@ -595,22 +606,39 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
       }
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    if (KW) {   // (u, kappa) -> (u, kappa u) on the thread's own slots
+    // own slots: (u, kappa) -> (u, kappa u); 3-D az > 0: plus the mirror plane
+    // z - az (the fractional weight and every span are even in dz, so the two
+    // planes are swept as one)
+    const int64_t gzm = 2 * z - gz;
+    const bool mirror = DIM == 3 && KIND == 0 && az > 0;
+    const bool zmin = mirror && gzm >= 0 && gzm < n && gzm >= g.in_begin && gzm < g.in_end;
+    if (KW || mirror) {
       for (int ty = threadIdx.y; ty < TH; ty += kWY) {
+        const int64_t gy = y0 - H + ty;
+        const bool yin = zmin && gy >= 0 && gy < n;
+        const int64_t rowm = ((gzm - g.in_begin) * n + gy) * n;
         double2* trow = tile + static_cast<size_t>(ty) * RS;
         for (int c0 = 0; c0 < TWc; c0 += 32) {
           const int c = c0 + cl;
           if (c >= TWc) continue;
           double2* dst = trow + (c & 3) * Q + (c >> 2);
-          const double2 v = *dst;
-          dst->y = v.y * v.x;
+          double2 v = *dst;
+          if (KW) v.y = v.y * v.x;
+          const int64_t gx = x0 - H + c;
+          if (yin && gx >= 0 && gx < n) {
+            const double um = __ldg(a.u + rowm + gx);
+            v.x = v.x + um;
+            if (KW) v.y = fma(__ldg(a.kappa + rowm + gx), um, v.y);
+          }
+          *dst = v;
         }
       }
     }
     __syncthreads();
   };
-  for (int dz = -Rz; dz <= Rz; ++dz) {
-    const int az = dz < 0 ? -dz : dz, dz2 = dz * dz;
+  // 3-D: planes z +- dz staged pre-added (dz = |dz| = az); 2-D: one pass
+  for (int dz = 0; dz <= Rz; ++dz) {
+    const int az = dz, dz2 = dz * dz;
     if (DIM == 3) __syncthreads();               // the previous plane is consumed
     stage(z + dz, az);
     const int mW = MW - dz2, mN = MN - dz2;
@@ -650,19 +678,31 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
       const int rem0 = m0c - dz2;
       if (m0c >= 0 && rem0 >= 0) {
         const int Ry = isq[rem0];
-        const double ddz = DIM == 3 ? __dsub_rn(coord(z + dz, g.h), coord(z, g.h)) : 0.0;
+        // 3-D: the tile holds planes z+dz and z-dz added; each side has its own
+        // float predicate (coordinates round differently), a lone side adds its
+        // own value from global memory
+        const double ddp = DIM == 3 ? __dsub_rn(coord(z + dz, g.h), coord(z, g.h)) : 0.0;
+        const double ddm = DIM == 3 ? __dsub_rn(coord(z - dz, g.h), coord(z, g.h)) : 0.0;
         for (int dy = -Ry; dy <= Ry; ++dy) {
           const int rem = rem0 - dy * dy, X = isq[rem];
           if (X * X != rem || (dz == 0 && dy == 0 && X == 0)) continue;
           const double ddy = __dsub_rn(coord(iy + dy, g.h), coord(iy, g.h));
-          const double base = DIM == 3 ? __dadd_rn(__dmul_rn(ddz, ddz), __dmul_rn(ddy, ddy)) : __dmul_rn(ddy, ddy);
+          const double yy = __dmul_rn(ddy, ddy);
+          const double bp = DIM == 3 ? __dadd_rn(__dmul_rn(ddp, ddp), yy) : yy;
+          const double bm = DIM == 3 ? __dadd_rn(__dmul_rn(ddm, ddm), yy) : yy;
           for (int sx = -X; sx <= X; sx += (X > 0 ? 2 * X : 1)) {
 #pragma unroll
             for (int r = 0; r < kRX; ++r) {
               const int64_t ix = x0 + kRX * tx + r;
               const double ddx = __dsub_rn(coord(ix + sx, g.h), coord(ix, g.h));
-              const bool in = M[r] >= 0 && __dadd_rn(base, __dmul_rn(ddx, ddx)) < Tc;
-              add(r, az, dy, sx, in ? 1.0 : 0.0);
+              const double xx = __dmul_rn(ddx, ddx);
+              const bool ip = M[r] >= 0 && __dadd_rn(bp, xx) < Tc;
+              const bool im = M[r] >= 0 && __dadd_rn(bm, xx) < Tc;
+              if (DIM == 2 || dz == 0 || ip == im) {
+                add(r, az, dy, sx, ip ? 1.0 : 0.0);
+              } else {
+                lone_side(r, dy, sx, ip ? z + dz : z - dz);
+              }
             }
           }
         }
@@ -689,16 +729,29 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
         const int m = dz2 + dy * dy + X * X;
         if (m < mlo || m == 0) continue;
         for (int sx = -X; sx <= X; sx += (X > 0 ? 2 * X : 1)) {
-          bool in;
+          bool in, im = false;
           if (DIM == 2) {
             const int d[2] = {dy, sx};
             in = point_in<2>(ki, d, g.h, delta);
+            im = in;
           } else {
-            const int d[3] = {dz, dy, sx};
+            const int d[3] = {dz, dy, sx}, dm[3] = {-dz, dy, sx};
             in = point_in<3>(ki, d, g.h, delta);
+            im = dz == 0 ? in : point_in<3>(ki, dm, g.h, delta);
           }
-          if (!in) continue;
-          const double2 v = tv(dy, rr, sx);
+          if (!in && !im) continue;
+          double2 v;
+          if (in == im) {
+            v = tv(dy, rr, sx);                  // both mirrored planes (or the only one)
+          } else {                               // one side: its own value from global memory
+            const int64_t gz = in ? z + dz : z - dz, gy = iy + dy, gx = ix + sx;
+            v = make_double2(0.0, 0.0);
+            if (gz >= 0 && gz < n && gz >= g.in_begin && gz < g.in_end && gy >= 0 && gy < n && gx >= 0 && gx < n) {
+              const int64_t k = ((gz - g.in_begin) * n + gy) * n + gx;
+              v.x = a.u[k];
+              if (KW) v.y = a.kappa[k] * v.x;
+            }
+          }
           const int t = wrow_of(az, dy) + sx + H;
           if (KIND == 0) {
             t0 = fma(wt[t], v.x, t0);
