@@ -16,18 +16,20 @@
 //     G_m(j) = f_j + lambda_m G_m(j+1)  (suffix recurrence; the left side is the
 //     mirrored prefix recurrence).
 //
-// Scan organisation (one pass per direction and term class; the slow class
-// holds the terms whose far-window factor lambda^{D+1} is not negligible):
-//   es_agg   : per 64-node segment, the segment aggregate of every term
-//   es_carry : per term, a block scan of the segment aggregates -> G at every
-//              segment end
-//   es_main  : per segment, the recurrence re-run from its carry
-// A thread owns one (segment, group of 8 terms) pair and walks its 64 nodes
-// sequentially: 8 terms x fields independent FMA chains, no warp scans. The
-// four groups of a segment sit in adjacent lanes and reduce with two shuffles.
-// es_main accumulates c_m lambda^{P+1} G_m(j) into target j - P - 1 (near
-// window) and, for the slow class, c_m lambda^{j-t} G_m(j) into the target t
-// whose horizon ends at j (j = t + D_t + 1, exactly one writer per target).
+// Scan organisation (per direction and per field):
+//   es_walk<agg>  : per kL-node segment, the segment aggregate of every term
+//   es_chunk / es_carry / es_expand : the segment carries G(end of segment) by
+//                   a three-level scan of the aggregates
+//   es_walk<main> : per segment, the recurrences re-run from the carries
+// A CTA owns 32 consecutive segments (one per lane) and one warp per chunk of
+// terms; the field values are staged once in shared memory and every warp
+// walks the 32 segments with its chunk's constants and states in registers
+// (independent FMA chains, no cross-lane traffic). The main walk leaves per
+// node partial sums in shared memory; a last pass over the CTA's nodes (one
+// thread per node, so coalesced) adds sum_m c_m lambda^{P+1} G_m(j) to target
+// j - P - 1 (near window) and subtracts, over the slow terms, c_m
+// lambda^{j-t} G_m(j) from the target t whose horizon ends at j
+// (j = t + D_t + 1, at most two targets per node).
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -38,143 +40,301 @@ namespace nlg {
 
 namespace {
 
-constexpr int kL = 64;               // nodes per segment
-constexpr int kG = 8;                // terms per group (per thread)
-constexpr int kGroups = 4;           // groups per class (adjacent lanes)
-constexpr int kClassMax = kG * kGroups;
+constexpr int kL = 32;               // nodes per segment (one thread each)
+constexpr int kMT = 48;              // terms per pass, padded (lambda = c = 0)
 constexpr int kNear = 32;            // P: offsets 1..P summed directly
-constexpr int kThreads = 128;        // 32 segments x 4 groups per CTA
+constexpr int kThreads = 128;
 
-// Term constants of one class, padded to kClassMax (padding: lam = cn = cw = 0).
-struct ClassTab {
-  const double* lam;
-  const double* cn;      // c_m lambda^{P+1}
-  const double* cw;      // c_m
-  const double* rate;    // t_m
-  const double* linv;    // 1 / lambda_m
-  const double* segpow;  // lambda^{kL}
-  int Mk;                // real terms in the class
-};
+// term constants of a chunk of terms (global, read once into registers):
+// [0][k] lambda, [1][k] c lambda^{P+1}, [2][k] c (slow terms; 0 otherwise),
+// [3][k] 1/lambda, [4][k] rate; row length kMT, padding lambda = c = 0
+constexpr int kTabRows = 5;
 
 struct PassArgs {
-  ClassTab ct;
   const double* u;
-  const double* kappa;   // null: one field
+  const double* kappa;   // field 1: kappa u
   int mirror;            // 0: right (suffix), 1: left (prefix, mirrored indexing)
   int64_t n_in, n_out, o0;
   int64_t q0;            // positions-space index of segment 0 (= o0' + P + 1)
   int64_t nseg;          // segments covering [q0, n_in)
+  int M;                 // real terms
+  int nf;                // fields (1: u, 2: u and kappa u)
   const int* tinfo;      // positions space: (tfirst << 2) | count, -1 none
   const int* dtarget;    // D of each output target in this direction (output order)
-  double* agg;           // [kClassMax * NF][nseg]
-  double* carry;         // [kClassMax * NF][nseg]  G at the end of each segment
-  double* facc;          // [n_out] near-window part of X (+=)
-  double* ffar;          // [n_out] far-window part of X (-=)
+  const double* rate;    // t_m (global; coefficient resets)
+  const double* segpow;  // lambda_m^kL (global; carries)
+  double* agg;           // [nseg][kMT * nf]  (value fastest: the carry scans read it coalesced)
+  double* carry;         // [nseg][kMT * nf]  G at the end of each segment
+  double* facc;          // [nf][n_out] far field of F (near-window part +=, far ends -=)
 };
 
 __device__ __forceinline__ int64_t to_input(const PassArgs& a, int64_t p) {
   return a.mirror ? (a.n_in - 1 - p) : p;
 }
 
-template <int NF>
-__device__ __forceinline__ void load_field(const PassArgs& a, int64_t p, double (&f)[NF]) {
-  f[0] = 0.0;
-  if (NF == 2) f[NF - 1] = 0.0;
-  if (p >= 0 && p < a.n_in) {
-    const int64_t x = to_input(a, p);
-    const double uu = __ldg(a.u + x);
-    f[0] = uu;
-    if (NF == 2) f[NF - 1] = uu * __ldg(a.kappa + x);
-  }
+template <bool KU>
+__device__ __forceinline__ double field_at(const PassArgs& a, int64_t p) {
+  if (p < 0 || p >= a.n_in) return 0.0;
+  const int64_t x = to_input(a, p);
+  const double uu = __ldg(a.u + x);
+  return KU ? uu * __ldg(a.kappa + x) : uu;
 }
 
-// Shared-memory staging: a CTA covers SPC consecutive segments; their field
-// values (and per-node side data) are loaded once, coalesced, into shared
-// memory with a 65-double segment stride (the segments of a warp then hit
-// distinct banks), and the sequential walks read them from there.
-constexpr int kLP = kL + 1;
+constexpr int kLP = kL + 1;                      // padded segment stride in shared memory
+constexpr int kSegs = 32;                        // segments per CTA (one per lane)
+constexpr int kNodes = kSegs * kL;               // nodes per CTA
+constexpr int kNodesP = kSegs * kLP;             // padded
+constexpr int kMaxChunks = 8;                    // warps per CTA (one per term chunk)
+constexpr int kChunkCap = 12;                    // terms per chunk
 
-template <int NF>
-__device__ __forceinline__ void stage_fields(const PassArgs& a, int64_t P0, int npos, double* sf) {
-  for (int i = threadIdx.x; i < npos; i += blockDim.x) {
-    double f[NF];
-    load_field<NF>(a, P0 + i, f);
-    const int si = (i / kL) * kLP + (i % kL);
-#pragma unroll
-    for (int c = 0; c < NF; ++c) sf[c * (npos / kL) * kLP + si] = f[c];
-  }
+struct ChunkPlan {
+  int n;                                         // chunks
+  int mb[kMaxChunks], cnt[kMaxChunks], mt[kMaxChunks], slow[kMaxChunks];
+  int any_slow;
+  const double* tab;                             // [kMaxChunks][kTabRows][kMT]
+};
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool in) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(in ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool in) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(in ? 4 : 0) : "memory");
 }
 
-template <int NF>
-__global__ void __launch_bounds__(kThreads) es_agg(PassArgs a) {
-  constexpr int SPC = kThreads / 4;          // segments per CTA (4 lanes x 8 terms each)
-  __shared__ double sf[NF * SPC * kLP];
-  const int lane = threadIdx.x & 31, grp = lane & 3;
-  const int sl = threadIdx.x >> 2;
-  const int64_t seg0 = static_cast<int64_t>(blockIdx.x) * SPC;
-  const int64_t P0 = a.q0 + seg0 * kL;
-  stage_fields<NF>(a, P0, SPC * kL, sf);
-  __syncthreads();
-  const int64_t seg = seg0 + sl;
-  if (seg >= a.nseg) return;
-  const int mb = grp * kG;
-  double lam[kG], s[kG][NF];
+// walk of one warp: the MT terms of one chunk, both fields, over its lane's
+// segment. (lambda, c lambda^{P+1}) pairs come from shared memory (warp-uniform
+// broadcasts); states and far-window coefficients live in registers; the
+// per-node partial sums are added into shared memory.
+template <int NF, bool MAIN, int MT, bool SLOW>
+__device__ __forceinline__ void es_walk_chunk(const PassArgs& a, const double2* __restrict__ lc,
+                                              const double* __restrict__ tab, int mb, int cnt, const double* sf,
+                                              const int* sti, double* sac, double* sy, int64_t seg, int64_t pseg) {
+  const int lane = threadIdx.x & 31;
+  double g[MT][NF];
 #pragma unroll
-  for (int m = 0; m < kG; ++m) {
-    lam[m] = a.ct.lam[mb + m];
+  for (int m = 0; m < MT; ++m)
 #pragma unroll
-    for (int c = 0; c < NF; ++c) s[m][c] = 0.0;
+    for (int c = 0; c < NF; ++c) g[m][c] = MAIN && m < cnt ? a.carry[seg * (kMT * NF) + (mb + m) * NF + c] : 0.0;
+  const int li = lane * kLP;
+  if (!MAIN) {
+#pragma unroll 2
+    for (int q = kL - 1; q >= 0; --q) {
+      double f[NF];
+#pragma unroll
+      for (int c = 0; c < NF; ++c) f[c] = sf[c * kNodesP + li + q];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const double lam = lc[m].x;
+#pragma unroll
+        for (int c = 0; c < NF; ++c) g[m][c] = fma(lam, g[m][c], f[c]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+      if (m < cnt)                                           // padding terms write nothing
+#pragma unroll
+        for (int c = 0; c < NF; ++c) a.agg[seg * (kMT * NF) + (mb + m) * NF + c] = g[m][c];
+    return;
   }
-  const double* my = sf + sl * kLP;
-#pragma unroll 4
+  double coef[SLOW ? MT : 1];
+#pragma unroll
+  for (int m = 0; m < (SLOW ? MT : 1); ++m) coef[m] = 0.0;
+  int ecur = -1;                              // exponent of coef (p - t), -1: unset
+#pragma unroll 1
   for (int q = kL - 1; q >= 0; --q) {
-    double f[NF];
+    double f[NF], ac[NF][2];
 #pragma unroll
-    for (int c = 0; c < NF; ++c) f[c] = my[c * SPC * kLP + q];
+    for (int c = 0; c < NF; ++c) {
+      f[c] = sf[c * kNodesP + li + q];
+      ac[c][0] = ac[c][1] = 0.0;
+    }
 #pragma unroll
-    for (int m = 0; m < kG; ++m)
+    for (int m = 0; m < MT; ++m) {
+      const double2 k = lc[m];                // (lambda, c lambda^{P+1})
 #pragma unroll
-      for (int c = 0; c < NF; ++c) s[m][c] = fma(lam[m], s[m][c], f[c]);
+      for (int c = 0; c < NF; ++c) {
+        g[m][c] = fma(k.x, g[m][c], f[c]);
+        ac[c][m & 1] = fma(k.y, g[m][c], ac[c][m & 1]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NF; ++c) atomicAdd(sac + c * kNodesP + li + q, ac[c][0] + ac[c][1]);
+    if (SLOW) {
+      const int ti = sti[li + q];
+      const int nt = ti < 0 ? 0 : (ti & 3);
+      if (nt) {
+        const int e = static_cast<int>(pseg + q - (ti >> 2));      // = D_t + 1
+        if (e != ecur) {
+          if (e == ecur + 1) {
+#pragma unroll
+            for (int m = 0; m < MT; ++m) coef[m] *= lc[m].x;
+          } else if (e == ecur - 1) {
+#pragma unroll
+            for (int m = 0; m < MT; ++m) coef[m] *= __ldg(tab + 3 * kMT + m);
+          } else {
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+              const double cw = __ldg(tab + 2 * kMT + m);
+              coef[m] = cw == 0.0 ? 0.0 : cw * exp(-__ldg(tab + 4 * kMT + m) * static_cast<double>(e));
+            }
+          }
+          ecur = e;
+        }
+        double y[NF][2];
+#pragma unroll
+        for (int c = 0; c < NF; ++c) y[c][0] = y[c][1] = 0.0;
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int c = 0; c < NF; ++c) y[c][m & 1] = fma(coef[m], g[m][c], y[c][m & 1]);
+#pragma unroll
+        for (int c = 0; c < NF; ++c) atomicAdd(sy + c * kNodesP + li + q, y[c][0] + y[c][1]);
+        if (nt == 2) {                        // a second target ending here (rare): its own RED
+          const int64_t ob = to_input(a, (ti >> 2) + 1) - a.o0;
+#pragma unroll
+          for (int c = 0; c < NF; ++c) {
+            double z = 0.0;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) z = fma(coef[m] * __ldg(tab + 3 * kMT + m), g[m][c], z);
+            atomicAdd(a.facc + c * a.n_out + ob, -z);
+          }
+        }
+      }
+    }
   }
-  (void)lane;
+}
+
+template <int NF, bool MAIN, bool SLOW>
+__device__ __forceinline__ void es_walk_dispatch(int mt, const PassArgs& a, const double2* lc, const double* tab,
+                                                 int mb, int cnt, const double* sf, const int* sti, double* sac,
+                                                 double* sy, int64_t seg, int64_t pseg) {
+  switch (mt) {
+    case 4: es_walk_chunk<NF, MAIN, 4, SLOW>(a, lc, tab, mb, cnt, sf, sti, sac, sy, seg, pseg); break;
+    case 8: es_walk_chunk<NF, MAIN, 8, SLOW>(a, lc, tab, mb, cnt, sf, sti, sac, sy, seg, pseg); break;
+    default: es_walk_chunk<NF, MAIN, 12, SLOW>(a, lc, tab, mb, cnt, sf, sti, sac, sy, seg, pseg); break;
+  }
+}
+
+// CTA: 32 consecutive segments, one warp per term chunk.
+template <int NF, bool MAIN>
+__global__ void __launch_bounds__(32 * kMaxChunks) es_walk(PassArgs a, ChunkPlan cp) {
+  extern __shared__ double esm[];
+  double* sf = esm;                                        // [NF][kSegs][kLP]  u, kappa u
+  double* sac = sf + NF * kNodesP;                         // [NF][kSegs][kLP]  near-window partials
+  double* sy = sac + (MAIN ? NF * kNodesP : 0);            // [NF][kSegs][kLP]  far-end partials
+  double2* slc = reinterpret_cast<double2*>(sy + (MAIN && cp.any_slow ? NF * kNodesP : 0));   // [chunks][kChunkCap]
+  int* sti = reinterpret_cast<int*>(slc + kMaxChunks * kChunkCap);                          // [kSegs][kLP]
+  int* sdt = sti + kNodesP;                                                                 // [kNodes] D of near targets
+  const int nthr = 32 * cp.n, tid = threadIdx.x;
+  const int64_t seg0 = static_cast<int64_t>(blockIdx.x) * kSegs;
+  const int64_t P0 = a.q0 + seg0 * kL;
+  // staging (cp.async: every load of a thread in flight at once; zero fill past the slab)
+  for (int i = tid; i < kNodes; i += nthr) {
+    const int si = (i / kL) * kLP + (i % kL);
+    const int64_t p = P0 + i;
+    const bool in = p < a.n_in;
+    const int64_t x = in ? to_input(a, p) : 0;
+    cp_async8(sf + si, a.u + x, in);
+    if (NF == 2) cp_async8(sf + kNodesP + si, a.kappa + x, in);
+    if (MAIN) {
+      if (cp.any_slow) cp_async4(sti + si, a.tinfo + (in ? p : 0), in);
+      const int64_t t = p - (kNear + 1);
+      const int64_t oi = to_input(a, t) - a.o0;
+      const bool tin = t >= 0 && oi >= 0 && oi < a.n_out && in;
+      cp_async4(sdt + i, a.dtarget + (tin ? oi : 0), tin);
 #pragma unroll
-  for (int m = 0; m < kG; ++m)
+      for (int c = 0; c < NF; ++c) {
+        sac[c * kNodesP + si] = 0.0;
+        if (cp.any_slow) sy[c * kNodesP + si] = 0.0;
+      }
+    }
+  }
+  for (int i = tid; i < cp.n * kChunkCap; i += nthr) {
+    const int c = i / kChunkCap, m = i % kChunkCap;
+    slc[i] = make_double2(__ldg(cp.tab + c * kTabRows * kMT + m), __ldg(cp.tab + c * kTabRows * kMT + kMT + m));
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  if (NF == 2) {   // kappa -> kappa u on the thread's own slots
+    for (int i = tid; i < kNodes; i += nthr) {
+      const int si = (i / kL) * kLP + (i % kL);
+      sf[kNodesP + si] *= sf[si];
+    }
+  }
+  if (MAIN && !cp.any_slow)
+    for (int i = tid; i < kNodes; i += nthr) sti[(i / kL) * kLP + (i % kL)] = -1;
+  __syncthreads();
+  const int w = tid >> 5, lane = tid & 31;
+  const int64_t seg = seg0 + lane;
+  if (seg < a.nseg) {
+    const double* tab = cp.tab + w * kTabRows * kMT;
+    const double2* lc = slc + w * kChunkCap;
+    const int64_t pseg = P0 + lane * kL;
+    if (cp.slow[w])
+      es_walk_dispatch<NF, MAIN, true>(cp.mt[w], a, lc, tab, cp.mb[w], cp.cnt[w], sf, sti, sac, sy, seg, pseg);
+    else
+      es_walk_dispatch<NF, MAIN, false>(cp.mt[w], a, lc, tab, cp.mb[w], cp.cnt[w], sf, sti, sac, sy, seg, pseg);
+  }
+  if (!MAIN) return;
+  __syncthreads();
+  // one thread per node: partials -> near-window target (t = p - P - 1) and far-end target
+  for (int i = tid; i < kNodes; i += nthr) {
+    const int si = (i / kL) * kLP + (i % kL);
+    const int64_t p = P0 + i;
+    if (p >= a.n_in || seg0 + i / kL >= a.nseg) continue;
+    const int64_t t = p - (kNear + 1);
+    const int64_t oi = to_input(a, t) - a.o0;
+    if (t >= 0 && oi >= 0 && oi < a.n_out && sdt[i] > kNear)
 #pragma unroll
-    for (int c = 0; c < NF; ++c) a.agg[((mb + m) * NF + c) * a.nseg + seg] = s[m][c];
+      for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + oi, sac[c * kNodesP + si]);
+    const int ti = sti[si];
+    if (ti >= 0 && (ti & 3)) {
+      const int64_t oa = to_input(a, ti >> 2) - a.o0;
+#pragma unroll
+      for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + oa, -sy[c * kNodesP + si]);
+    }
+  }
+}
+
+size_t es_walk_smem(const ChunkPlan& cp, int nf, bool main) {
+  size_t d = static_cast<size_t>(nf) * kNodesP;                       // fields
+  if (main) d += static_cast<size_t>(nf) * kNodesP * (cp.any_slow ? 2 : 1);
+  d += 2 * kMaxChunks * kChunkCap;                                    // (lambda, cn) pairs
+  return sizeof(double) * d + sizeof(int) * (kNodesP + kNodes);
 }
 
 // Segment carries by a three-level scan (all fully parallel except a short
 // per-term block scan over chunks of kChunk segments):
-//   es_chunk  : per (term value j, chunk), the chunk aggregate from its segment aggregates
+//   es_chunk  : per (term j, chunk), the chunk aggregate from its segment aggregates
 //   es_carry  : per j, block scan of chunk aggregates -> G at every chunk end
 //   es_expand : per (j, chunk), walk its segments down from the chunk-end G
 // with G(start s) = agg[s] + L G(start s+1), L = lambda^{kL}.
 constexpr int kChunk = 32;                       // segments per chunk
 constexpr int kCarryThreads = 512, kCarryPer = 8;
 
-__global__ void es_chunk(PassArgs a, int NF, int64_t nchunk, double* cagg) {
+__global__ void es_chunk(PassArgs a, int64_t nchunk, double* cagg) {
   const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int V = kClassMax * NF;
+  const int V = kMT * a.nf;
   const int j = static_cast<int>(id % V);
   const int64_t k = id / V;
-  if (k >= nchunk || j / NF >= a.ct.Mk) return;
-  const double L = a.ct.segpow[j / NF];
-  const double* ag = a.agg + static_cast<int64_t>(j) * a.nseg;
+  if (k >= nchunk || j / a.nf >= a.M) return;
+  const double L = a.segpow[j / a.nf];
+  const double* ag = a.agg + j;
   const int64_t s0 = k * kChunk, s1 = min(a.nseg, s0 + kChunk);
   double A = 0.0;
-  for (int64_t s = s1 - 1; s >= s0; --s) A = fma(L, A, __ldg(ag + s));
+  for (int64_t s = s1 - 1; s >= s0; --s) A = fma(L, A, __ldg(ag + s * V));
   cagg[static_cast<int64_t>(j) * nchunk + k] = A;
 }
 
-// One block per value j: gchunk[j][k] = G(end of chunk k); chunk multiplier
+// One block per term j: gchunk[j][k] = G(end of chunk k); chunk multiplier
 // Lc = L^{kChunk} (a short last chunk only matters at the very top, where G = 0).
-__global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int NF, int64_t nchunk, const double* cagg,
+__global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int64_t nchunk, const double* cagg,
                                                           double* gchunk) {
   const int j = blockIdx.x;
-  const int m = j / NF;
-  if (m >= a.ct.Mk) return;
+  if (j / a.nf >= a.M) return;
   double Lc = 1.0;
-  for (int k = 0; k < kChunk; ++k) Lc *= a.ct.segpow[m];
+  for (int k = 0; k < kChunk; ++k) Lc *= a.segpow[j / a.nf];
   const double* ag = cagg + static_cast<int64_t>(j) * nchunk;
   double* gc = gchunk + static_cast<int64_t>(j) * nchunk;
   const int tid = threadIdx.x;
@@ -224,144 +384,21 @@ __global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int NF, in
   }
 }
 
-__global__ void es_expand(PassArgs a, int NF, int64_t nchunk, const double* gchunk) {
+__global__ void es_expand(PassArgs a, int64_t nchunk, const double* gchunk) {
   const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int V = kClassMax * NF;
+  const int V = kMT * a.nf;
   const int j = static_cast<int>(id % V);
   const int64_t k = id / V;
-  if (k >= nchunk || j / NF >= a.ct.Mk) return;
-  const double L = a.ct.segpow[j / NF];
-  const double* ag = a.agg + static_cast<int64_t>(j) * a.nseg;
-  double* cr = a.carry + static_cast<int64_t>(j) * a.nseg;
+  if (k >= nchunk || j / a.nf >= a.M) return;
+  const double L = a.segpow[j / a.nf];
+  const double* ag = a.agg + j;
+  double* cr = a.carry + j;
   const int64_t s0 = k * kChunk, s1 = min(a.nseg, s0 + kChunk);
   double g = gchunk[static_cast<int64_t>(j) * nchunk + k];
   for (int64_t s = s1 - 1; s >= s0; --s) {
-    cr[s] = g;
-    g = fma(L, g, __ldg(ag + s));
+    cr[s * V] = g;
+    g = fma(L, g, __ldg(ag + s * V));
   }
-}
-
-// LANES lanes share a segment, each owning G = kClassMax / LANES terms (the
-// slow class uses 8 lanes x 4 terms to keep its far-scatter state in registers).
-template <int NF, bool SLOW, int LANES>
-__global__ void __launch_bounds__(kThreads) es_main(PassArgs a) {
-  constexpr int G = kClassMax / LANES;
-  constexpr int SPC = kThreads / LANES;       // segments per CTA
-  constexpr int NP = SPC * kL;                // nodes per CTA
-  __shared__ double sf[NF * SPC * kLP];
-  __shared__ int sown[SPC * kLP];             // own near-window target (output index) or -1
-  __shared__ int sti[SLOW ? SPC * kLP : 1];   // far-target info (tfirst << 2 | count) or -1
-  const int lane = threadIdx.x & 31, grp = lane & (LANES - 1);
-  const int sl = threadIdx.x / LANES;
-  const int64_t seg0 = static_cast<int64_t>(blockIdx.x) * SPC;
-  const int64_t P0 = a.q0 + seg0 * kL;
-  stage_fields<NF>(a, P0, NP, sf);
-  for (int i = threadIdx.x; i < NP; i += kThreads) {
-    const int64_t p = P0 + i;
-    const int si = (i / kL) * kLP + (i % kL);
-    const int64_t t = p - (kNear + 1);
-    const int64_t oi = to_input(a, t) - a.o0;
-    sown[si] = (t >= 0 && oi >= 0 && oi < a.n_out && __ldg(a.dtarget + oi) > kNear) ? static_cast<int>(oi) : -1;
-    if (SLOW) sti[si] = p < a.n_in ? __ldg(a.tinfo + p) : -1;
-  }
-  __syncthreads();
-  const int64_t seg = seg0 + sl;
-  const bool live = seg < a.nseg;            // whole lane groups share `live`
-  const int mb = grp * G;
-  double lam[G], cn[G], g[G][NF];
-  double cw[SLOW ? G : 1], li[SLOW ? G : 1], coef[SLOW ? G : 1];
-#pragma unroll
-  for (int m = 0; m < G; ++m) {
-    lam[m] = a.ct.lam[mb + m];
-    cn[m] = a.ct.cn[mb + m];
-#pragma unroll
-    for (int c = 0; c < NF; ++c)
-      g[m][c] = live ? a.carry[((mb + m) * NF + c) * a.nseg + seg] : 0.0;
-    if (SLOW) {
-      cw[m] = a.ct.cw[mb + m];
-      li[m] = a.ct.linv[mb + m];
-      coef[m] = 0.0;
-    }
-  }
-  int ecur = -1;                              // exponent of coef (p - t), -1: unset
-  const double* myf = sf + sl * kLP;
-  const int* myown = sown + sl * kLP;
-  const int* myti = sti + (SLOW ? sl * kLP : 0);
-  const int64_t p0 = P0 + static_cast<int64_t>(sl) * kL;
-#pragma unroll 2
-  for (int q = kL - 1; q >= 0; --q) {
-    double ac[NF];
-#pragma unroll
-    for (int c = 0; c < NF; ++c) ac[c] = 0.0;
-#pragma unroll
-    for (int m = 0; m < G; ++m)
-#pragma unroll
-      for (int c = 0; c < NF; ++c) {
-        g[m][c] = fma(lam[m], g[m][c], myf[c * NP / kL * kLP + q]);
-        ac[c] = fma(cn[m], g[m][c], ac[c]);
-      }
-#pragma unroll
-    for (int c = 0; c < NF; ++c) {
-#pragma unroll
-      for (int o = 1; o < LANES; o <<= 1) ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], o);
-    }
-    const int own = myown[q];
-    if (live && grp == 0 && own >= 0)
-#pragma unroll
-      for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + own, ac[c]);   // RED, no stall
-    if (SLOW) {
-      const int ti = live ? myti[q] : -1;
-      const int cnt = ti < 0 ? 0 : (ti & 3);
-      double y[NF], z[NF];
-#pragma unroll
-      for (int c = 0; c < NF; ++c) y[c] = z[c] = 0.0;
-      if (cnt) {
-        const int e = static_cast<int>(p0 + q - (ti >> 2));      // = D_t + 1
-        if (e != ecur) {
-#pragma unroll
-          for (int m = 0; m < G; ++m) {
-            if (e == ecur + 1) coef[m] *= lam[m];
-            else if (e == ecur - 1) coef[m] *= li[m];
-            else coef[m] = cw[m] * exp(-__ldg(a.ct.rate + mb + m) * static_cast<double>(e));
-          }
-          ecur = e;
-        }
-#pragma unroll
-        for (int m = 0; m < G; ++m)
-#pragma unroll
-          for (int c = 0; c < NF; ++c) y[c] = fma(coef[m], g[m][c], y[c]);
-        if (cnt == 2) {
-#pragma unroll
-          for (int m = 0; m < G; ++m)
-#pragma unroll
-            for (int c = 0; c < NF; ++c) z[c] = fma(coef[m] * li[m], g[m][c], z[c]);
-        }
-      }
-      // the lanes of a segment see the same node, hence the same cnt
-      if (__any_sync(0xffffffffu, cnt != 0)) {
-#pragma unroll
-        for (int c = 0; c < NF; ++c) {
-#pragma unroll
-          for (int o = 1; o < LANES; o <<= 1) {
-            y[c] += __shfl_xor_sync(0xffffffffu, y[c], o);
-            z[c] += __shfl_xor_sync(0xffffffffu, z[c], o);
-          }
-        }
-        if (cnt && grp == 0) {
-          const int tf = ti >> 2;
-          const int64_t oa = to_input(a, tf) - a.o0;
-#pragma unroll
-          for (int c = 0; c < NF; ++c) atomicAdd(a.ffar + c * a.n_out + oa, -y[c]);
-          if (cnt == 2) {
-            const int64_t ob = to_input(a, tf + 1) - a.o0;
-#pragma unroll
-            for (int c = 0; c < NF; ++c) atomicAdd(a.ffar + c * a.n_out + ob, -z[c]);
-          }
-        }
-      }
-    }
-  }
-  (void)lane;
 }
 
 struct CombineArgs {
@@ -374,7 +411,6 @@ struct CombineArgs {
   const double* scale;   // s_i
   const double* diag;
   const double* facc;    // [fields][n_out]
-  const double* ffar;    // [fields][n_out]
   const double* ext;     // mode 1: exact exterior (collar) part of diag, or null
   double* out;           // mode 0: out; mode 1: diag
   int mode;
@@ -458,8 +494,8 @@ __global__ void __launch_bounds__(kCombineThreads) es_near_combine(CombineArgs a
     if (i >= a.n_out) continue;
     // X = kappa_i F[u] + F[kappa u] (or F[u]); the plan-time pass (mode 1)
     // evaluates the same expression with u = 1, so constants cancel exactly.
-    const double fu = nu[j] + a.facc[i] + a.ffar[i];
-    const double X = KW ? fma(a.kappa[a.o0 + i], fu, nk[j] + a.facc[a.n_out + i] + a.ffar[a.n_out + i]) : fu;
+    const double fu = nu[j] + a.facc[i];
+    const double X = KW ? fma(a.kappa[a.o0 + i], fu, nk[j] + a.facc[a.n_out + i]) : fu;
     if (a.mode == 1) {
       a.out[i] = a.ext ? X + a.ext[i] : X;
     } else {
@@ -524,11 +560,16 @@ bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirro
 // Device-side state of the exponential-sum plan (declared in plan.hpp).
 struct ExpSumState {
   int M = 0, Mslow = 0, fields = 1;
-  double* tabs = nullptr;          // [2 classes][6 arrays][kClassMax]
-  int Mk[2] = {0, 0};
+  // term chunks: first global term, real terms, slow flag; constants per chunk
+  int nchunks = 0, cmb[kMaxChunks] = {}, ccnt[kMaxChunks] = {};
+  bool cslow[kMaxChunks] = {};
+  ChunkPlan cp{};
+  double* ctab = nullptr;          // [kMaxChunks][kTabRows][kMT]
+  double* rate = nullptr;          // [kMT] t_m
+  double* segpow = nullptr;        // [kMT] lambda_m^kL
   int *dplus = nullptr, *dminus = nullptr, *tinfoR = nullptr, *tinfoL = nullptr;
   double *wnear = nullptr, *scale = nullptr, *diag = nullptr;
-  double *agg = nullptr, *carry = nullptr, *facc = nullptr, *ffar = nullptr;
+  double *agg = nullptr, *carry = nullptr, *facc = nullptr;
   double *cagg = nullptr, *gchunk = nullptr;
   int64_t nsegR = 0, nsegL = 0, o0R = 0, o0L = 0;
   double* kappa_dev = nullptr;
@@ -563,7 +604,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   int Ms = 0;   // rates ascend: slow terms (far end not negligible) come first
   for (int m = 0; m < M; ++m)
     if (es.rate[m] * static_cast<double>(std::max<int64_t>(dmin, kNear + 1) + 1) <= 40.0) Ms = m + 1;
-  if (Ms > kClassMax || M - Ms > kClassMax) return;
+  if (M > kMT || (Ms + kChunkCap - 1) / kChunkCap + (M - Ms + kChunkCap - 1) / kChunkCap > kMaxChunks) return;
 
   auto* S = new ExpSumState();
   P.es_state = S;
@@ -571,25 +612,53 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   S->M = M;
   S->Mslow = Ms;
   S->fields = d.kappa ? 2 : 1;
-  S->Mk[0] = Ms;          // class 0: slow
-  S->Mk[1] = M - Ms;      // class 1: fast
-  // per-class constant tables, padded with inert terms (lambda = c = 0)
-  std::vector<double> tab(2 * 6 * kClassMax, 0.0);
-  for (int cls = 0; cls < 2; ++cls) {
-    const int mb = cls == 0 ? 0 : Ms;
-    for (int k = 0; k < S->Mk[cls]; ++k) {
-      const int m = mb + k;
+  // term chunks (constants in registers): slow terms in chunks of <= 16 (they
+  // also hold the far-window coefficients), fast terms in chunks of <= 24
+  std::vector<double> rate(kMT, 0.0), segpow(kMT, 0.0);
+  auto add_chunks = [&](int m0, int cnt, int cap, bool slow) {
+    const int parts = (cnt + cap - 1) / cap;
+    for (int k = 0; k < parts; ++k) {
+      const int b = m0 + k * cnt / parts, e = m0 + (k + 1) * cnt / parts;
+      S->cmb[S->nchunks] = b;
+      S->ccnt[S->nchunks] = e - b;
+      S->cslow[S->nchunks] = slow;
+      ++S->nchunks;
+    }
+  };
+  add_chunks(0, Ms, kChunkCap, true);
+  add_chunks(Ms, M - Ms, kChunkCap, false);
+  std::vector<double> ctab(static_cast<size_t>(kMaxChunks) * kTabRows * kMT, 0.0);
+  for (int c = 0; c < S->nchunks; ++c) {
+    double* T = ctab.data() + static_cast<size_t>(c) * kTabRows * kMT;
+    for (int k = 0; k < S->ccnt[c]; ++k) {
+      const int m = S->cmb[c] + k;
       const double t = es.rate[m];
-      double* T = tab.data() + cls * 6 * kClassMax;
-      T[0 * kClassMax + k] = std::exp(-t);
-      T[1 * kClassMax + k] = es.weight[m] * std::exp(-t * (kNear + 1));
-      T[2 * kClassMax + k] = es.weight[m];
-      T[3 * kClassMax + k] = t;
-      T[4 * kClassMax + k] = std::exp(t);
-      T[5 * kClassMax + k] = std::exp(-t * kL);
+      T[0 * kMT + k] = std::exp(-t);
+      T[1 * kMT + k] = es.weight[m] * std::exp(-t * (kNear + 1));
+      T[2 * kMT + k] = S->cslow[c] ? es.weight[m] : 0.0;
+      T[3 * kMT + k] = std::exp(t);
+      T[4 * kMT + k] = t;
     }
   }
-  S->tabs = upload(tab);
+  S->ctab = upload(ctab);
+  for (const void* f : {reinterpret_cast<const void*>(es_walk<1, false>), reinterpret_cast<const void*>(es_walk<2, false>),
+                        reinterpret_cast<const void*>(es_walk<1, true>), reinterpret_cast<const void*>(es_walk<2, true>)})
+    NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  S->cp.n = S->nchunks;
+  S->cp.tab = S->ctab;
+  S->cp.any_slow = Ms > 0;
+  for (int c = 0; c < S->nchunks; ++c) {
+    S->cp.mb[c] = S->cmb[c];
+    S->cp.cnt[c] = S->ccnt[c];
+    S->cp.mt[c] = (S->ccnt[c] + 3) / 4 * 4;
+    S->cp.slow[c] = S->cslow[c];
+  }
+  for (int m = 0; m < M; ++m) {
+    rate[m] = es.rate[m];
+    segpow[m] = std::exp(-es.rate[m] * kL);
+  }
+  S->rate = upload(rate);
+  S->segpow = upload(segpow);
   S->dplus = upload(dplus);
   S->dminus = upload(dminus);
   S->tinfoR = upload(tR);
@@ -620,14 +689,13 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   S->nsegR = nseg_of(S->o0R);
   S->nsegL = nseg_of(S->o0L);
   const int64_t ns = std::max(S->nsegR, S->nsegL);
-  const size_t vals = static_cast<size_t>(kClassMax) * S->fields * ns;
+  const size_t vals = static_cast<size_t>(kMT) * S->fields * ns;
   NLG_CUDA(cudaMalloc(&S->agg, sizeof(double) * vals));
   NLG_CUDA(cudaMalloc(&S->carry, sizeof(double) * vals));
-  const size_t cvals = static_cast<size_t>(kClassMax) * S->fields * ((ns + kChunk - 1) / kChunk);
+  const size_t cvals = static_cast<size_t>(kMT) * S->fields * ((ns + kChunk - 1) / kChunk);
   NLG_CUDA(cudaMalloc(&S->cagg, sizeof(double) * cvals));
   NLG_CUDA(cudaMalloc(&S->gchunk, sizeof(double) * cvals));
   NLG_CUDA(cudaMalloc(&S->facc, sizeof(double) * S->fields * n_out));
-  NLG_CUDA(cudaMalloc(&S->ffar, sizeof(double) * S->fields * n_out));
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * n_out));
   // exterior (zero collar) part of diag, exact: sum_{d > edge distance} w_d,
   // times (kappa_i + kappa_i) when kappa-weighted (kappa_y := kappa_x outside)
@@ -670,7 +738,8 @@ void expsum_setup(Plan& P, const nlg_desc& d) {
 void expsum_free(Plan& P) {
   ExpSumState* S = P.es_state;
   if (!S) return;
-  for (double* p : {S->tabs, S->wnear, S->scale, S->diag, S->agg, S->carry, S->facc, S->ffar, S->cagg, S->gchunk})
+  for (double* p : {S->ctab, S->rate, S->segpow, S->wnear, S->scale, S->diag, S->agg, S->carry, S->facc, S->cagg,
+                    S->gchunk})
     cudaFree(p);
   for (int* p : {S->dplus, S->dminus, S->tinfoR, S->tinfoL}) cudaFree(p);
   delete S;
@@ -682,55 +751,46 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
   const int64_t n_out = P.n_out;
   const int NF = S->fields;
   NLG_CUDA(cudaMemsetAsync(S->facc, 0, sizeof(double) * NF * n_out, s));
-  NLG_CUDA(cudaMemsetAsync(S->ffar, 0, sizeof(double) * NF * n_out, s));
   for (int mirror = 0; mirror < 2; ++mirror) {
-    for (int cls = 0; cls < 2; ++cls) {
-      if (S->Mk[cls] == 0) continue;
-      PassArgs a;
-      const double* T = S->tabs + cls * 6 * kClassMax;
-      a.ct = {T, T + kClassMax, T + 2 * kClassMax, T + 3 * kClassMax, T + 4 * kClassMax, T + 5 * kClassMax,
-              S->Mk[cls]};
-      a.u = u;
-      a.kappa = NF == 2 ? S->kappa_dev : nullptr;
-      a.mirror = mirror;
-      a.n_in = P.n_in;
-      a.n_out = n_out;
-      a.o0 = P.halo_lo;
-      a.q0 = (mirror ? S->o0L : S->o0R) + kNear + 1;
-      a.nseg = mirror ? S->nsegL : S->nsegR;
-      a.tinfo = mirror ? S->tinfoL : S->tinfoR;
-      a.dtarget = mirror ? S->dminus : S->dplus;
-      a.agg = S->agg;
-      a.carry = S->carry;
-      a.facc = S->facc;
-      a.ffar = S->ffar;
-      const unsigned grid = static_cast<unsigned>((a.nseg * 4 + kThreads - 1) / kThreads);
-      cudaEvent_t ev;
-      stage_begin(P, s, kStEsAggregate, &ev);
-      if (NF == 2) es_agg<2><<<grid, kThreads, 0, s>>>(a);
-      else es_agg<1><<<grid, kThreads, 0, s>>>(a);
-      stage_end(P, s, kStEsAggregate, ev, 1);
-      stage_begin(P, s, kStEsCarry, &ev);
-      {
-        const int64_t nchunk = (a.nseg + kChunk - 1) / kChunk;
-        const int64_t work = nchunk * kClassMax * NF;
-        const unsigned gw = static_cast<unsigned>((work + 255) / 256);
-        es_chunk<<<gw, 256, 0, s>>>(a, NF, nchunk, S->cagg);
-        es_carry<<<kClassMax * NF, kCarryThreads, 0, s>>>(a, NF, nchunk, S->cagg, S->gchunk);
-        es_expand<<<gw, 256, 0, s>>>(a, NF, nchunk, S->gchunk);
-      }
-      stage_end(P, s, kStEsCarry, ev, 3);
-      stage_begin(P, s, kStEsMain, &ev);
-      const unsigned grid8 = static_cast<unsigned>((a.nseg * 8 + kThreads - 1) / kThreads);
-      if (NF == 2) {
-        if (cls == 0) es_main<2, true, 8><<<grid8, kThreads, 0, s>>>(a);
-        else es_main<2, false, 4><<<grid, kThreads, 0, s>>>(a);
-      } else {
-        if (cls == 0) es_main<1, true, 8><<<grid8, kThreads, 0, s>>>(a);
-        else es_main<1, false, 4><<<grid, kThreads, 0, s>>>(a);
-      }
-      stage_end(P, s, kStEsMain, ev, 1);
+    PassArgs a;
+    a.u = u;
+    a.kappa = S->kappa_dev;
+    a.mirror = mirror;
+    a.n_in = P.n_in;
+    a.n_out = n_out;
+    a.o0 = P.halo_lo;
+    a.q0 = (mirror ? S->o0L : S->o0R) + kNear + 1;
+    a.nseg = mirror ? S->nsegL : S->nsegR;
+    a.M = S->M;
+    a.nf = NF;
+    a.tinfo = mirror ? S->tinfoL : S->tinfoR;
+    a.dtarget = mirror ? S->dminus : S->dplus;
+    a.rate = S->rate;
+    a.segpow = S->segpow;
+    a.agg = S->agg;
+    a.carry = S->carry;
+    a.facc = S->facc;
+    const unsigned gridw = static_cast<unsigned>((a.nseg + kSegs - 1) / kSegs);
+    const unsigned thr = 32 * S->cp.n;
+    cudaEvent_t ev;
+    stage_begin(P, s, kStEsAggregate, &ev);
+    if (NF == 2) es_walk<2, false><<<gridw, thr, es_walk_smem(S->cp, 2, false), s>>>(a, S->cp);
+    else es_walk<1, false><<<gridw, thr, es_walk_smem(S->cp, 1, false), s>>>(a, S->cp);
+    stage_end(P, s, kStEsAggregate, ev, 1);
+    stage_begin(P, s, kStEsCarry, &ev);
+    {
+      const int64_t nchunk = (a.nseg + kChunk - 1) / kChunk;
+      const int64_t work = nchunk * kMT * NF;
+      const unsigned gw = static_cast<unsigned>((work + 255) / 256);
+      es_chunk<<<gw, 256, 0, s>>>(a, nchunk, S->cagg);
+      es_carry<<<S->M * NF, kCarryThreads, 0, s>>>(a, nchunk, S->cagg, S->gchunk);
+      es_expand<<<gw, 256, 0, s>>>(a, nchunk, S->gchunk);
     }
+    stage_end(P, s, kStEsCarry, ev, 3);
+    stage_begin(P, s, kStEsMain, &ev);
+    if (NF == 2) es_walk<2, true><<<gridw, thr, es_walk_smem(S->cp, 2, true), s>>>(a, S->cp);
+    else es_walk<1, true><<<gridw, thr, es_walk_smem(S->cp, 1, true), s>>>(a, S->cp);
+    stage_end(P, s, kStEsMain, ev, 1);
   }
   CombineArgs c;
   c.u = u;
@@ -744,7 +804,6 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
   c.scale = S->scale;
   c.diag = S->diag;
   c.facc = S->facc;
-  c.ffar = S->ffar;
   c.ext = ext;
   c.out = out;
   c.mode = mode;
