@@ -166,6 +166,37 @@ nlg_status nlg_split(int K, double c, double* poly /* K+1 */, double* tail /* >=
 nlg_status nlg_expsum_fit(double alpha, int near, int64_t dmax, double* rate, double* weight,
                           int* terms, double* rel_err);
 
+/* Matrix view of the direct operators (routes 0-2 and FRACTIONAL; not
+ * PERIDYNAMIC): out = A^T v for the plan's operator A (apply_direct = A u).
+ * The transpose is what CGNR needs for non-symmetric operators (variable
+ * horizons, coefficient_fn); the reference assembles the dense matrix for
+ * this (tools/nonloc_main.cpp:200-219). Host / device pointers as above. */
+nlg_status nlg_apply_transpose(nlg_plan* plan, const double* v, double* out);
+nlg_status nlg_apply_transpose_dev(nlg_plan* plan, const double* v_dev, double* out_dev, void* stream);
+
+/* Dense row-major N x N matrix of an unsharded plan's direct operator
+ * (reference assemble_dense_matrix, operators.cpp:262-303). a: host, N^2. */
+nlg_status nlg_assemble_dense(nlg_plan* plan, double* a_rowmajor);
+
+/* Matrix-free Krylov solve of A u = f with A = -L (the negated operator, the
+ * reference's solve_dirichlet convention, src/solve.cpp:32-108), vectors
+ * resident on the device: CG, or CGNR on the normal equations with the GPU
+ * transpose. L is the plan's fast apply (or its direct apply with
+ * NLG_SOLVE_DIRECT). Unsharded scalar plans only. Non-convergence is reported,
+ * a non-finite operator value is NLG_ERUNTIME (check_finite, solve.cpp:24-28).
+ * f, u: host, N doubles. */
+#define NLG_SOLVE_CG 0
+#define NLG_SOLVE_CGNR 1
+#define NLG_SOLVE_DIRECT 0x10
+typedef struct {
+  int method;              /* NLG_SOLVE_CG or NLG_SOLVE_CGNR                  */
+  int converged;           /* final_residual <= tol                            */
+  int64_t iterations;
+  double final_residual;   /* ||f - A u||_2 / ||f||_2, recomputed at the end   */
+} nlg_solve_report;
+nlg_status nlg_solve_dirichlet(nlg_plan* plan, const double* f, double tol, int64_t max_iter, int method,
+                               double* u, nlg_solve_report* report);
+
 /* Thread-local text of the last error; "" if none. */
 const char* nlg_last_error(void);
 int nlg_abi_version(void);

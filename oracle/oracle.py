@@ -98,6 +98,10 @@ def ref():
         lib.ref_full_dense_general.argtypes = [i, i, _dp, d, _dp, _dp, d, _dp, _dp, _ip]
         lib.ref_full_dense_general_at.argtypes = [i, i, _dp, d, _dp, _dp, d, _dp, _ip, C.c_int64,
                                                   _dp, i, _ip]
+        lib.ref_assemble_dense.argtypes = [i, i, i, i, i, d, d, i, i, i, _dp]
+        lib.ref_solve_truncated.argtypes = [i, i, i, i, d, d, _dp, d, C.c_int64, i, _dp, _ip, _dp,
+                                            C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        lib.ref_dense_direct_solve.argtypes = [C.c_int64, _dp, _dp, _dp]
         _ref = lib
     return _ref
 
@@ -293,3 +297,36 @@ def rel_inf(a, b) -> float:
     den = np.max(np.abs(b)) if b.size else 0.0
     num = np.max(np.abs(a - b)) if b.size else 0.0
     return float(num / den) if den > 0 else float(num)
+
+
+def ref_assemble_dense(dim, n, family, order, horizon_kind, delta0, rule=LEAF, form=MASS, coeff=1.0,
+                       divergence=False):
+    """assemble_dense_matrix (operators.cpp:262-303); family 3 = truncated K=order."""
+    N = n ** dim
+    a = np.empty(N * N)
+    _check_ref(ref().ref_assemble_dense(dim, n, family, order, horizon_kind, delta0, coeff, int(divergence),
+                                        rule, form, _p(a)))
+    return a
+
+
+def ref_solve_truncated(dim, n, K, horizon_kind, delta0, f, tol, max_iter, use_dense=False, coeff=1.0):
+    """The reference's cmd_solve path (tools/nonloc_main.cpp:189-222):
+    returns (u, iterations, final_residual, converged, method)."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    u = np.empty(f.size)
+    it = C.c_int64(0)
+    res = C.c_double(0.0)
+    conv = C.c_int(0)
+    m = C.c_int(0)
+    _check_ref(ref().ref_solve_truncated(dim, n, K, horizon_kind, delta0, coeff, _p(f), tol, max_iter,
+                                         int(use_dense), _p(u), C.byref(it), C.byref(res), C.byref(conv),
+                                         C.byref(m)))
+    return u, it.value, res.value, bool(conv.value), m.value
+
+
+def ref_dense_direct_solve(a, rhs):
+    rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    x = np.empty(rhs.size)
+    _check_ref(ref().ref_dense_direct_solve(rhs.size, _p(a), _p(rhs), _p(x)))
+    return x

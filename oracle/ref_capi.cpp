@@ -9,7 +9,9 @@
 // Every function calls the reference's public API only:
 //   TruncatedOperator (operators.hpp:28-54), apply_truncated_dense (:58-62),
 //   apply_smooth_dense (:66-70), apply_full_dense (:73-75), apply_split (:94-96),
-//   match_polynomial / split (kernel.hpp:63-66), random_vector (bench.hpp:24).
+//   match_polynomial / split (kernel.hpp:63-66), random_vector (bench.hpp:24),
+//   assemble_dense_matrix (operators.hpp:79-81), solve_dirichlet / choose_method /
+//   dense_direct_solve (solve.hpp:27-39).
 // BASELINE-only features (fractional |r|^-alpha kernels, per-node delta(x),
 // C(x) and (kappa(x)+kappa(y))/2 weighting) are expressed through the
 // reference's own coefficient_fn hook (kernel.hpp:101) with an InverseS
@@ -28,6 +30,7 @@
 #include "nonloc/bench.hpp"
 #include "nonloc/kernel.hpp"
 #include "nonloc/operators.hpp"
+#include "nonloc/solve.hpp"
 #include "nonloc/tree.hpp"
 
 using namespace nonloc;
@@ -306,4 +309,87 @@ int ref_full_dense_general_at(int dim, int n, const double* delta, double delta_
   } catch (const std::exception& e) { return fail(e); }
 }
 
+
+// Dense matrix (row-major N x N) of the truncated operator (K, horizon, rule, form)
+// or, for family >= 0 (full-operator profile), of apply_full_dense's operator.
+int ref_assemble_dense(int dim, int n, int family, int order, int horizon_kind, double delta0,
+                       double coeff, int symmetry, int rule, int form, double* a) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    const KernelSpec spec = make_spec(dim, family, order, horizon_kind, delta0, coeff, symmetry);
+    const auto m = assemble_dense_matrix(spec, g, rule == 0 ? InclusionRule::Leaf : InclusionRule::Point,
+                                         form == 0 ? ApplyForm::Mass : ApplyForm::Difference);
+    std::memcpy(a, m.data(), sizeof(double) * m.size());
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// The reference's solve path of tools/nonloc_main.cpp:cmd_solve (lines 189-222):
+// A = -L^P of the truncated K operator; choose_method(spec); CG through the
+// fast TruncatedOperator (use_dense = 0) or the dense Leaf apply (use_dense = 1);
+// CGNR through the assembled dense matrix and its transpose.
+int ref_solve_truncated(int dim, int n, int K, int horizon_kind, double delta0, double coeff,
+                        const double* f, double tol, int64_t max_iter, int use_dense, double* u,
+                        int64_t* iterations, double* final_residual, int* converged, int* method) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    const KernelSpec spec = make_spec(dim, 3, K, horizon_kind, delta0, coeff, 0);
+    const std::span<const double> fs(f, g.total);
+    const SolveMethod m = choose_method(spec);
+    SolveReport rep;
+    if (m == SolveMethod::CG) {
+      if (use_dense) {
+        const auto apply = [&](std::span<const double> x) {
+          auto out = apply_truncated_dense(spec, g, InclusionRule::Leaf, x);
+          for (double& v : out) v = -v;
+          return out;
+        };
+        rep = solve_dirichlet(apply, fs, tol, max_iter, SolveMethod::CG);
+      } else {
+        TruncatedOperator op(spec, g);
+        const auto apply = [&](std::span<const double> x) {
+          auto out = op.apply(x);
+          for (double& v : out) v = -v;
+          return out;
+        };
+        rep = solve_dirichlet(apply, fs, tol, max_iter, SolveMethod::CG);
+      }
+    } else {
+      auto a = assemble_dense_matrix(spec, g, InclusionRule::Leaf, ApplyForm::Mass);
+      for (double& v : a) v = -v;
+      const int64_t N = g.total;
+      const auto apply = [&](std::span<const double> x) {
+        std::vector<double> out(N, 0.0);
+        for (int64_t i = 0; i < N; ++i) {
+          double acc = 0.0;
+          for (int64_t j = 0; j < N; ++j) acc += a[i * N + j] * x[j];
+          out[i] = acc;
+        }
+        return out;
+      };
+      const auto apply_t = [&](std::span<const double> x) {
+        std::vector<double> out(N, 0.0);
+        for (int64_t i = 0; i < N; ++i)
+          for (int64_t j = 0; j < N; ++j) out[j] += a[i * N + j] * x[i];
+        return out;
+      };
+      rep = solve_dirichlet(apply, fs, tol, max_iter, SolveMethod::CGNR, apply_t);
+    }
+    std::memcpy(u, rep.solution.data(), sizeof(double) * g.total);
+    *iterations = rep.iterations;
+    *final_residual = rep.final_residual;
+    *converged = rep.converged ? 1 : 0;
+    *method = m == SolveMethod::CG ? 0 : 1;
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// dense_direct_solve (partial-pivot LU)
+int ref_dense_direct_solve(int64_t n, const double* a, const double* rhs, double* x) {
+  try {
+    const auto r = dense_direct_solve(std::span<const double>(a, n * n), std::span<const double>(rhs, n));
+    std::memcpy(x, r.data(), sizeof(double) * n);
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
 }  // extern "C"

@@ -33,6 +33,14 @@ class Desc(C.Structure):
     ]
 
 
+class SolveReport(C.Structure):
+    _fields_ = [("method", C.c_int), ("converged", C.c_int), ("iterations", C.c_int64),
+                ("final_residual", C.c_double)]
+
+
+SOLVE_CG, SOLVE_CGNR, SOLVE_DIRECT = 0, 1, 0x10
+
+
 class Info(C.Structure):
     _fields_ = [("halo_lo", C.c_int64), ("halo_hi", C.c_int64), ("n_in", C.c_int64),
                 ("n_out", C.c_int64), ("fast_method", C.c_int), ("exp_terms", C.c_int),
@@ -57,6 +65,11 @@ EXPORTS = {
     "nlg_match_polynomial_exact": ([C.c_int, _ip, _ip], C.c_int),
     "nlg_split": ([C.c_int, C.c_double, _dp, _dp, C.POINTER(C.c_int)], C.c_int),
     "nlg_expsum_fit": ([C.c_double, C.c_int, C.c_int64, _dp, _dp, C.POINTER(C.c_int), _dp], C.c_int),
+    "nlg_apply_transpose": ([C.c_void_p, _dp, _dp], C.c_int),
+    "nlg_apply_transpose_dev": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "nlg_assemble_dense": ([C.c_void_p, _dp], C.c_int),
+    "nlg_solve_dirichlet": ([C.c_void_p, _dp, C.c_double, C.c_int64, C.c_int, _dp, C.POINTER(SolveReport)],
+                            C.c_int),
     "nlg_last_error": ([], C.c_char_p),
     "nlg_abi_version": ([], C.c_int),
 }

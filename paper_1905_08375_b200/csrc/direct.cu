@@ -221,7 +221,287 @@ void launch_dim(int kind, const DirectArgs& a, cudaStream_t s) {
   }
 }
 
+// ---- matrix view of the direct operators: transpose apply and dense assembly
+// The operator is out = A u with, for KIND 1-3, A_ik = h^d w_ik (k != i, pair
+// included from row i's side: row i's horizon, coefficient and rule) and
+// A_ii = -h^d sum_k w_ik (exterior collar nodes included); for KIND 0 (the
+// truncated operator) A_ik = h^d front_i p(r/delta_i) on the rule's set S_i
+// (self included) and A_ii = h^d front_i p(0)[i in S_i] - front_i |B| (Mass) or
+// -h^d sum_{k != i} A_ik / h^d (Difference). Rounding follows the products
+// above, not the forward kernel's accumulation order.
+template <int DIM>
+struct RowInfo {
+  int64_t k[3];
+  double x[3];
+  double delta, ci, kap;
+};
+
+template <int DIM>
+__device__ __forceinline__ RowInfo<DIM> row_info(const DirectArgs& a, const int64_t* k) {
+  RowInfo<DIM> R;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    R.k[j] = j < DIM ? k[j] : 0;
+    R.x[j] = j < DIM ? coord(k[j], a.g.h) : 0.0;
+  }
+  const int64_t ii = in_index<DIM>(a.g, k);
+  R.delta = a.delta ? a.delta[ii] : a.delta0;
+  R.ci = a.coeff ? a.coeff[ii] : a.coeff0;
+  R.kap = a.kappa ? a.kappa[ii] : 1.0;
+  return R;
+}
+
+// weight w of the pair (row R, column k) without the h^d factor; false if the
+// pair is not in row R's set. Self pairs: only KIND 0 (its set may hold i).
+template <int DIM, int KIND>
+__device__ __forceinline__ bool pair_weight(const DirectArgs& a, const RowInfo<DIM>& R, const int64_t* k, bool in_dom,
+                                            int64_t kk, double& w) {
+  const double h = a.g.h;
+  bool self = true;
+  double r2 = 0.0;
+  double y[3];
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) {
+    self = self && k[j] == R.k[j];
+    y[j] = coord(k[j], h);
+    const double d = __dsub_rn(y[j], R.x[j]);
+    r2 = __dadd_rn(r2, __dmul_rn(d, d));
+  }
+  const double r = __dsqrt_rn(r2);
+  if (KIND == 0) {
+    bool in;
+    if (a.rule == 1) {
+      in = r < R.delta;
+    } else {
+      double dmin = 0.0;
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) {
+        const double blo = __dmul_rn(static_cast<double>(k[j]), h);
+        const double bhi = __dmul_rn(static_cast<double>(k[j] + 1), h);
+        if (blo > R.x[j]) {
+          const double d = __dsub_rn(blo, R.x[j]);
+          dmin = __dadd_rn(dmin, __dmul_rn(d, d));
+        } else if (bhi < R.x[j]) {
+          const double d = __dsub_rn(bhi, R.x[j]);
+          dmin = __dadd_rn(dmin, __dmul_rn(d, d));
+        }
+      }
+      in = dmin < __dmul_rn(R.delta, R.delta);
+    }
+    if (!in) return false;
+    w = __ddiv_rn(R.ci, delta_power(DIM, R.delta)) * poly_eval(a.p, __ddiv_rn(r, R.delta));
+    return true;
+  }
+  if (self) return false;
+  if (KIND == 1) {
+    if (r >= R.delta) return false;
+    w = R.ci * __ddiv_rn(1.0, delta_power(DIM, R.delta)) * kappa_eval(a.p, __ddiv_rn(r, R.delta));
+    return true;
+  }
+  if (KIND == 2) {
+    double dl = R.delta;
+    if (a.divergence) {
+      const double dk = in_dom ? (a.delta ? a.delta[kk] : a.delta0) : R.delta;
+      dl = __dmul_rn(0.5, __dadd_rn(R.delta, dk));
+    }
+    if (r >= dl) return false;
+    double c = R.ci;
+    if (a.kappa) c = c * (0.5 * (R.kap + (in_dom ? a.kappa[kk] : R.kap)));
+    w = __dmul_rn(__ddiv_rn(c, delta_power(DIM, dl)), profile_eval(a.p, __ddiv_rn(r, dl)));
+    return w != 0.0;
+  }
+  // KIND 3 (BASELINE fractional)
+  if (!(r < R.delta)) return false;
+  double c = R.ci;
+  if (a.kappa) c = c * (0.5 * (R.kap + (in_dom ? a.kappa[kk] : R.kap)));
+  w = c * pow(r, -a.p.alpha);
+  return true;
+}
+
+// window half-width (cells) of row R
+template <int DIM, int KIND>
+__device__ __forceinline__ int64_t row_window(const DirectArgs& a, double delta) {
+  const double radius = (KIND == 2 && a.reach > 0.0) ? a.reach : delta;
+  return static_cast<int64_t>(floor(radius / a.g.h)) + 2;
+}
+
+// diagonal entry A_ii (with h^d) by enumerating row i
+template <int DIM, int KIND>
+__device__ double row_diag(const DirectArgs& a, const RowInfo<DIM>& R) {
+  const Geom& g = a.g;
+  const bool collar = a.exterior == 1 && KIND >= 2;
+  const int64_t W = row_window<DIM, KIND>(a, R.delta);
+  int64_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) {
+    lo[j] = R.k[j] - W;
+    hi[j] = R.k[j] + W;
+    if (!collar) {
+      lo[j] = lo[j] < 0 ? 0 : lo[j];
+      hi[j] = hi[j] > g.n - 1 ? g.n - 1 : hi[j];
+    }
+  }
+  double sum = 0.0, self = 0.0;
+  int64_t k[3] = {0, 0, 0};
+  for (k[0] = lo[0]; k[0] <= hi[0]; ++k[0])
+    for (k[1] = (DIM > 1 ? lo[1] : 0); k[1] <= (DIM > 1 ? hi[1] : 0); ++k[1])
+      for (k[2] = (DIM > 2 ? lo[2] : 0); k[2] <= (DIM > 2 ? hi[2] : 0); ++k[2]) {
+        bool in_dom = true, isself = true;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) {
+          in_dom = in_dom && k[j] >= 0 && k[j] < g.n;
+          isself = isself && k[j] == R.k[j];
+        }
+        const int64_t kk = in_dom ? in_index<DIM>(g, k) : -1;
+        double w;
+        if (!pair_weight<DIM, KIND>(a, R, k, in_dom, kk, w)) continue;
+        if (isself) self = w;
+        else sum += w;
+      }
+  if (KIND == 0) {
+    const double front = __ddiv_rn(R.ci, delta_power(DIM, R.delta));
+    return a.form == 0 ? g.hd * self - front * ball_volume(DIM, R.delta) : -g.hd * sum;
+  }
+  return -g.hd * sum;
+}
+
+// (A^T v)_j, one thread per output column j (this plan's output rows); rows i
+// range over the input slab within the widest horizon
+template <int DIM, int KIND>
+__global__ void __launch_bounds__(128) transpose_kernel(DirectArgs a, double dmax) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= a.ntargets) return;
+  const Geom& g = a.g;
+  int64_t kj[3] = {0, 0, 0};
+  unflatten<DIM>(g, t, kj);
+  const int64_t jj = in_index<DIM>(g, kj);
+  const RowInfo<DIM> Rj = row_info<DIM>(a, kj);
+  double acc = row_diag<DIM, KIND>(a, Rj) * a.u[jj];
+  const int64_t W = row_window<DIM, KIND>(a, dmax);
+  int64_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) {
+    lo[j] = kj[j] - W;
+    hi[j] = kj[j] + W;
+    const int64_t lim_lo = j == 0 ? (g.in_begin > 0 ? g.in_begin : 0) : 0;
+    const int64_t lim_hi = j == 0 ? (g.in_end < g.n ? g.in_end : g.n) - 1 : g.n - 1;
+    lo[j] = lo[j] < lim_lo ? lim_lo : lo[j];
+    hi[j] = hi[j] > lim_hi ? lim_hi : hi[j];
+  }
+  double off = 0.0;
+  int64_t ki[3] = {0, 0, 0};
+  for (ki[0] = lo[0]; ki[0] <= hi[0]; ++ki[0])
+    for (ki[1] = (DIM > 1 ? lo[1] : 0); ki[1] <= (DIM > 1 ? hi[1] : 0); ++ki[1])
+      for (ki[2] = (DIM > 2 ? lo[2] : 0); ki[2] <= (DIM > 2 ? hi[2] : 0); ++ki[2]) {
+        bool isself = true;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) isself = isself && ki[j] == kj[j];
+        if (isself) continue;
+        const RowInfo<DIM> Ri = row_info<DIM>(a, ki);
+        double w;
+        if (!pair_weight<DIM, KIND>(a, Ri, kj, true, jj, w)) continue;
+        off += w * a.u[in_index<DIM>(g, ki)];
+      }
+  a.out[t] = acc + g.hd * off;
+}
+
+// dense row-major matrix of an unsharded plan, one thread per row
+template <int DIM, int KIND>
+__global__ void __launch_bounds__(128) assemble_kernel(DirectArgs a, double* __restrict__ A, int64_t N) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const Geom& g = a.g;
+  int64_t ki[3] = {0, 0, 0};
+  unflatten<DIM>(g, i, ki);
+  const RowInfo<DIM> R = row_info<DIM>(a, ki);
+  const int64_t W = row_window<DIM, KIND>(a, R.delta);
+  int64_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) {
+    lo[j] = ki[j] - W < 0 ? 0 : ki[j] - W;
+    hi[j] = ki[j] + W > g.n - 1 ? g.n - 1 : ki[j] + W;
+  }
+  double* row = A + i * N;
+  int64_t k[3] = {0, 0, 0};
+  for (k[0] = lo[0]; k[0] <= hi[0]; ++k[0])
+    for (k[1] = (DIM > 1 ? lo[1] : 0); k[1] <= (DIM > 1 ? hi[1] : 0); ++k[1])
+      for (k[2] = (DIM > 2 ? lo[2] : 0); k[2] <= (DIM > 2 ? hi[2] : 0); ++k[2]) {
+        bool isself = true;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) isself = isself && k[j] == ki[j];
+        if (isself) continue;
+        const int64_t kk = in_index<DIM>(g, k);
+        double w;
+        if (pair_weight<DIM, KIND>(a, R, k, true, kk, w)) row[kk] = g.hd * w;
+      }
+  row[i] = row_diag<DIM, KIND>(a, R);
+}
+
+template <int DIM>
+void launch_matrix_dim(int kind, bool transpose, const DirectArgs& a, double dmax, double* A, int64_t N,
+                       cudaStream_t s) {
+  const int threads = 128;
+  const int64_t work = transpose ? a.ntargets : N;
+  const unsigned blocks = static_cast<unsigned>((work + threads - 1) / threads);
+  if (blocks == 0) return;
+#define NLG_MAT_CASE(KD)                                                           \
+  case KD:                                                                         \
+    if (transpose) transpose_kernel<DIM, KD><<<blocks, threads, 0, s>>>(a, dmax);  \
+    else assemble_kernel<DIM, KD><<<blocks, threads, 0, s>>>(a, A, N);             \
+    break;
+  switch (kind) {
+    NLG_MAT_CASE(0)
+    NLG_MAT_CASE(1)
+    NLG_MAT_CASE(2)
+    NLG_MAT_CASE(3)
+    default: break;
+  }
+#undef NLG_MAT_CASE
+}
+
+DirectArgs make_direct_args(const Plan& P, const double* u, double* out) {
+  DirectArgs a;
+  a.g = P.geom;
+  a.p = P.prof;
+  a.u = u;
+  a.delta = P.d_delta;
+  a.delta0 = P.delta0;
+  a.coeff = P.d_coeff;
+  a.coeff0 = P.coeff0;
+  a.kappa = P.d_kappa;
+  a.reach = P.reach;
+  a.rule = P.rule;
+  a.form = P.form;
+  a.exterior = P.exterior;
+  a.divergence = P.divergence;
+  a.targets = nullptr;
+  a.ntargets = P.n_out;
+  a.out = out;
+  a.pairs = nullptr;
+  return a;
+}
+
 }  // namespace
+
+void launch_transpose(const Plan& P, const double* v, double* out, cudaStream_t s) {
+  const DirectArgs a = make_direct_args(P, v, out);
+  const int kind = direct_kind(P);
+  switch (P.geom.dim) {
+    case 1: launch_matrix_dim<1>(kind, true, a, P.delta_max, nullptr, 0, s); break;
+    case 2: launch_matrix_dim<2>(kind, true, a, P.delta_max, nullptr, 0, s); break;
+    default: launch_matrix_dim<3>(kind, true, a, P.delta_max, nullptr, 0, s); break;
+  }
+}
+
+void launch_assemble(const Plan& P, double* A, int64_t N, cudaStream_t s) {
+  const DirectArgs a = make_direct_args(P, nullptr, nullptr);
+  const int kind = direct_kind(P);
+  switch (P.geom.dim) {
+    case 1: launch_matrix_dim<1>(kind, false, a, P.delta_max, A, N, s); break;
+    case 2: launch_matrix_dim<2>(kind, false, a, P.delta_max, A, N, s); break;
+    default: launch_matrix_dim<3>(kind, false, a, P.delta_max, A, N, s); break;
+  }
+}
 
 int direct_kind(const Plan& P) {
   if (P.family == 5) return 4;

@@ -491,3 +491,183 @@ nlg_status nlg_expsum_fit(double alpha, int near, int64_t dmax, double* rate, do
 }
 
 }  // extern "C"
+
+// ---- matrix view and Krylov consumer ----------------------------------------
+
+namespace nlg {
+namespace {
+
+void require_matrix_view(const Plan& P) {
+  require(direct_kind(P) <= 3, "matrix view needs a scalar operator (not peridynamic)");
+}
+
+}  // namespace
+}  // namespace nlg
+
+nlg_status nlg_apply_transpose(nlg_plan* plan, const double* v, double* out) {
+  using namespace nlg;
+  return guard([&] {
+    require(plan && v && out, "null argument");
+    Plan& P = plan->p;
+    require_matrix_view(P);
+    NLG_CUDA(cudaSetDevice(P.device));
+    ensure_staging(P);
+    NLG_CUDA(cudaMemcpyAsync(P.d_u, v, sizeof(double) * P.n_in, cudaMemcpyHostToDevice, P.stream));
+    launch_transpose(P, P.d_u, P.d_out, P.stream);
+    NLG_CUDA(cudaGetLastError());
+    ++P.launches;
+    NLG_CUDA(cudaMemcpyAsync(out, P.d_out, sizeof(double) * P.n_out, cudaMemcpyDeviceToHost, P.stream));
+    NLG_CUDA(cudaStreamSynchronize(P.stream));
+  });
+}
+
+nlg_status nlg_apply_transpose_dev(nlg_plan* plan, const double* v_dev, double* out_dev, void* stream) {
+  using namespace nlg;
+  return guard([&] {
+    require(plan && v_dev && out_dev, "null argument");
+    Plan& P = plan->p;
+    require_matrix_view(P);
+    NLG_CUDA(cudaSetDevice(P.device));
+    launch_transpose(P, v_dev, out_dev, static_cast<cudaStream_t>(stream));
+    NLG_CUDA(cudaGetLastError());
+    ++P.launches;
+  });
+}
+
+nlg_status nlg_assemble_dense(nlg_plan* plan, double* a) {
+  using namespace nlg;
+  return guard([&] {
+    require(plan && a, "null argument");
+    Plan& P = plan->p;
+    require_matrix_view(P);
+    require(P.n_in == P.n_out, "dense assembly needs an unsharded plan");
+    const int64_t N = P.n_out;
+    require(N <= 32768, "dense assembly limited to N <= 32768 (N^2 doubles)");
+    NLG_CUDA(cudaSetDevice(P.device));
+    double* d = nullptr;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(N) * static_cast<size_t>(N);
+    NLG_CUDA(cudaMalloc(&d, bytes));
+    cudaError_t e = cudaMemsetAsync(d, 0, bytes, P.stream);
+    if (e == cudaSuccess) {
+      launch_assemble(P, d, N, P.stream);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(a, d, bytes, cudaMemcpyDeviceToHost, P.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(P.stream);
+    cudaFree(d);
+    ++P.launches;
+    NLG_CUDA(e);
+  });
+}
+
+nlg_status nlg_solve_dirichlet(nlg_plan* plan, const double* f, double tol, int64_t max_iter, int method,
+                               double* u_out, nlg_solve_report* rep) {
+  using namespace nlg;
+  std::vector<void*> bufs;
+  nlg_status st = guard([&] {
+    require(plan && f && u_out && rep, "null argument");
+    Plan& P = plan->p;
+    require(components(P) == 1, "the solver needs a scalar operator");
+    require(P.n_in == P.n_out, "the device solver needs an unsharded plan");
+    const int m = method & 0xF;
+    const bool direct = (method & NLG_SOLVE_DIRECT) != 0;
+    require(m == NLG_SOLVE_CG || m == NLG_SOLVE_CGNR, "unknown solve method");
+    if (m == NLG_SOLVE_CGNR) require_matrix_view(P);
+    NLG_CUDA(cudaSetDevice(P.device));
+    const int64_t n = P.n_out;
+    cudaStream_t s = P.stream;
+    auto dalloc = [&](size_t count) {
+      void* q = nullptr;
+      NLG_CUDA(cudaMalloc(&q, count));
+      bufs.push_back(q);
+      return q;
+    };
+    const size_t vb = sizeof(double) * static_cast<size_t>(n);
+    double* df = static_cast<double*>(dalloc(vb));
+    double* du = static_cast<double*>(dalloc(vb));
+    double* dr = static_cast<double*>(dalloc(vb));
+    double* dp = static_cast<double*>(dalloc(vb));
+    double* dap = static_cast<double*>(dalloc(vb));
+    double* dz = m == NLG_SOLVE_CGNR ? static_cast<double*>(dalloc(vb)) : nullptr;
+    double* scratch = static_cast<double*>(dalloc(sizeof(double) * dot_scratch_doubles()));
+    int* bad = static_cast<int*>(dalloc(sizeof(int)));
+    NLG_CUDA(cudaMemcpyAsync(df, f, vb, cudaMemcpyHostToDevice, s));
+    NLG_CUDA(cudaMemsetAsync(du, 0, vb, s));
+    NLG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    // A = -L
+    auto applyA = [&](const double* x, double* y) {
+      if (direct) launch_direct(P, x, y, nullptr, 0, nullptr, s);
+      else fast_dev(P, x, y, s);
+      dev_negate(y, n, s);
+      NLG_CUDA(cudaGetLastError());
+    };
+    auto applyAT = [&](const double* x, double* y) {
+      launch_transpose(P, x, y, s);
+      dev_negate(y, n, s);
+      NLG_CUDA(cudaGetLastError());
+    };
+    auto dot = [&](const double* a, const double* b, const double* chk) {
+      dev_dot(a, b, chk, n, scratch, bad, s);
+      double v = 0.0;
+      int flag = 0;
+      NLG_CUDA(cudaMemcpyAsync(&v, scratch + dot_scratch_doubles() - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+      NLG_CUDA(cudaMemcpyAsync(&flag, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+      NLG_CUDA(cudaStreamSynchronize(s));
+      if (flag) throw Error{NLG_ERUNTIME, "operator produced a non-finite value"};
+      return v;
+    };
+    *rep = nlg_solve_report{m, 0, 0, 0.0};
+    const double fnorm = std::sqrt(dot(df, df, nullptr));
+    if (fnorm == 0.0) {
+      rep->converged = 1;
+      std::memset(u_out, 0, vb);
+      return;
+    }
+    NLG_CUDA(cudaMemcpyAsync(dr, df, vb, cudaMemcpyDeviceToDevice, s));   // r = f - A 0
+    if (m == NLG_SOLVE_CG) {
+      NLG_CUDA(cudaMemcpyAsync(dp, dr, vb, cudaMemcpyDeviceToDevice, s));
+      double rr = dot(dr, dr, nullptr);
+      for (int64_t it = 0; it < max_iter; ++it) {
+        if (std::sqrt(rr) / fnorm <= tol) break;
+        applyA(dp, dap);
+        const double pap = dot(dp, dap, dap);
+        if (pap == 0.0) break;
+        const double alpha = rr / pap;
+        dev_axpy2(du, dr, dp, dap, alpha, n, s);
+        const double rr_next = dot(dr, dr, nullptr);
+        const double beta = rr_next / rr;
+        rr = rr_next;
+        dev_xpby(dp, dr, beta, n, s);
+        rep->iterations = it + 1;
+      }
+    } else {
+      // CG on A^T A u = A^T f; r tracks f - A u
+      applyAT(dr, dz);
+      NLG_CUDA(cudaMemcpyAsync(dp, dz, vb, cudaMemcpyDeviceToDevice, s));
+      double zz = dot(dz, dz, nullptr);
+      for (int64_t it = 0; it < max_iter; ++it) {
+        if (std::sqrt(dot(dr, dr, nullptr)) / fnorm <= tol) break;
+        applyA(dp, dap);
+        const double denom = dot(dap, dap, dap);
+        if (denom == 0.0) break;
+        const double alpha = zz / denom;
+        dev_axpy2(du, dr, dp, dap, alpha, n, s);
+        applyAT(dr, dz);
+        const double zz_next = dot(dz, dz, dz);
+        const double beta = zz_next / zz;
+        zz = zz_next;
+        dev_xpby(dp, dz, beta, n, s);
+        rep->iterations = it + 1;
+      }
+    }
+    // the true residual, not the recurrence
+    applyA(du, dap);
+    dev_diff(dr, df, dap, n, s);
+    rep->final_residual = std::sqrt(dot(dr, dr, nullptr)) / fnorm;
+    rep->converged = rep->final_residual <= tol;
+    NLG_CUDA(cudaMemcpyAsync(u_out, du, vb, cudaMemcpyDeviceToHost, s));
+    NLG_CUDA(cudaStreamSynchronize(s));
+  });
+  for (void* q : bufs) cudaFree(q);
+  return st;
+}

@@ -101,6 +101,8 @@ void stage_end(Plan& P, cudaStream_t s, int stage, cudaEvent_t ev, int nlaunch);
 void launch_direct(const Plan& P, const double* u, double* out, const int64_t* targets,
                    int64_t ntargets, unsigned long long* pairs, cudaStream_t s);
 int direct_kind(const Plan& P);
+void launch_transpose(const Plan& P, const double* v, double* out, cudaStream_t s);
+void launch_assemble(const Plan& P, double* A, int64_t N, cudaStream_t s);
 void spans_setup(Plan& P);
 void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void spans_free(Plan& P);
@@ -110,6 +112,15 @@ void expsum_free(Plan& P);
 void stencil_setup(Plan& P, const nlg_desc& d);
 void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void stencil_free(Plan& P);
+
+// device BLAS-1 (solve.cu)
+size_t dot_scratch_doubles();
+void dev_dot(const double* a, const double* b, const double* chk, int64_t n, double* scratch, int* bad,
+             cudaStream_t s);   // result at scratch[dot_scratch_doubles() - 1]
+void dev_axpy2(double* u, double* r, const double* p, const double* ap, double alpha, int64_t n, cudaStream_t s);
+void dev_xpby(double* p, const double* z, double beta, int64_t n, cudaStream_t s);
+void dev_negate(double* x, int64_t n, cudaStream_t s);
+void dev_diff(double* d, const double* f, const double* x, int64_t n, cudaStream_t s);
 
 // host algebra (algebra.cpp)
 std::vector<double> match_polynomial(int K, double c);

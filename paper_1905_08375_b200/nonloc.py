@@ -272,6 +272,33 @@ class Plan:
         A.check(A.lib().nlg_apply_direct_dev(self._h, C.c_void_p(u_ptr), C.c_void_p(out_ptr),
                                              C.c_void_p(pairs_ptr or None), C.c_void_p(stream)))
 
+    def apply_transpose(self, v) -> np.ndarray:
+        """out = A^T v for the direct operator A (apply_direct)."""
+        v = self._u(v)
+        out = np.empty(self.n_out)
+        A.check(A.lib().nlg_apply_transpose(self._h, A.dptr(v), A.dptr(out)))
+        return out
+
+    def assemble_dense(self) -> np.ndarray:
+        """Dense row-major N x N matrix of the direct operator (unsharded plans)."""
+        a = np.empty(self.n_out * self.n_out)
+        A.check(A.lib().nlg_assemble_dense(self._h, A.dptr(a)))
+        return a
+
+    def solve_dirichlet(self, f, tol: float, max_iter: int, method: int = A.SOLVE_CG,
+                        direct: bool = False) -> "SolveReport":
+        """Device-resident CG / CGNR on A u = f with A = -L (this plan's fast
+        apply, or its direct apply with direct=True)."""
+        f = np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
+        if f.size != self.n_out:
+            raise ValueError("f size does not match grid")
+        u = np.empty(self.n_out)
+        rep = A.SolveReport()
+        A.check(A.lib().nlg_solve_dirichlet(self._h, A.dptr(f), tol, int(max_iter),
+                                            int(method) | (A.SOLVE_DIRECT if direct else 0), A.dptr(u),
+                                            C.byref(rep)))
+        return SolveReport(SolveMethod(rep.method), rep.iterations, rep.final_residual, bool(rep.converged), u)
+
     def set_profiling(self, on: bool = True) -> None:
         A.check(A.lib().nlg_set_profiling(self._h, int(on)))
 
@@ -367,6 +394,14 @@ class TruncatedOperator:
         u = _check_u(self._grid, u)
         self._applies += 1
         return self._plan.apply_fast(u)
+
+    def solve_dirichlet(self, f, tol: float, max_iter: int, method: Optional["SolveMethod"] = None) -> "SolveReport":
+        """solve_dirichlet(-L, f) with the vectors resident on the GPU: CG for a
+        symmetric operator (choose_method), CGNR with the GPU transpose apply
+        otherwise (the reference assembles the dense matrix for this,
+        tools/nonloc_main.cpp:200-219)."""
+        m = choose_method(self._spec) if method is None else method
+        return self._plan.solve_dirichlet(f, tol, max_iter, int(m))
 
     def spec(self):
         return self._spec
@@ -501,3 +536,125 @@ class NonlocalOperator:
 
     def apply_direct_at(self, u, targets):
         return self.plan.apply_direct_at(u, targets)
+
+
+# ---------------------------------------------------------------------------
+# Krylov consumer (reference include/nonloc/solve.hpp, src/solve.cpp)
+# ---------------------------------------------------------------------------
+
+class SolveMethod(IntEnum):
+    CG = 0
+    CGNR = 1
+
+
+@dataclass
+class SolveReport:
+    method: SolveMethod = SolveMethod.CG
+    iterations: int = 0
+    final_residual: float = 0.0        # ||f - A u||_2 / ||f||_2
+    converged: bool = False
+    solution: Optional[np.ndarray] = None
+
+
+def choose_method(spec: KernelSpec) -> SolveMethod:
+    """CG when the configuration yields a symmetric matrix (solve.cpp:110-114)."""
+    symmetric = spec.horizon.kind == HorizonKind.Constant and spec.coefficient_fn is None
+    return SolveMethod.CG if symmetric else SolveMethod.CGNR
+
+
+def solve_dirichlet(apply, f, tol: float, max_iter: int, method: SolveMethod = SolveMethod.CG,
+                    apply_transpose=None) -> SolveReport:
+    """Matrix-free Krylov solve of A u = f for an arbitrary `apply` callable
+    (the reference's ApplyFn, solve.cpp:32-108), same recurrences and stopping
+    rules. For a GPU operator prefer TruncatedOperator.solve_dirichlet /
+    Plan.solve_dirichlet, which keep every vector in HBM."""
+    f = np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
+    n = f.size
+    rep = SolveReport(method=method, solution=np.zeros(n))
+    fnorm = float(np.sqrt(np.dot(f, f)))
+    if fnorm == 0.0:
+        rep.converged = True
+        return rep
+    if method == SolveMethod.CGNR and apply_transpose is None:
+        raise ValueError("CGNR needs the transpose application")
+
+    def checked(v):
+        v = np.asarray(v, dtype=np.float64)
+        if not np.all(np.isfinite(v)):
+            raise A.NonlocError("operator produced a non-finite value")
+        return v
+
+    u = rep.solution
+    r = f.copy()
+    if method == SolveMethod.CG:
+        p = r.copy()
+        rr = float(np.dot(r, r))
+        for it in range(max_iter):
+            if np.sqrt(rr) / fnorm <= tol:
+                break
+            ap = checked(apply(p))
+            pap = float(np.dot(p, ap))
+            if pap == 0.0:
+                break
+            alpha = rr / pap
+            u += alpha * p
+            r -= alpha * ap
+            rr_next = float(np.dot(r, r))
+            beta = rr_next / rr
+            rr = rr_next
+            p = r + beta * p
+            rep.iterations = it + 1
+    else:
+        z = np.asarray(apply_transpose(r), dtype=np.float64)
+        p = z.copy()
+        zz = float(np.dot(z, z))
+        for it in range(max_iter):
+            if np.sqrt(np.dot(r, r)) / fnorm <= tol:
+                break
+            ap = checked(apply(p))
+            denom = float(np.dot(ap, ap))
+            if denom == 0.0:
+                break
+            alpha = zz / denom
+            u += alpha * p
+            r -= alpha * ap
+            z = checked(apply_transpose(r))
+            zz_next = float(np.dot(z, z))
+            beta = zz_next / zz
+            zz = zz_next
+            p = z + beta * p
+            rep.iterations = it + 1
+    au = np.asarray(apply(u), dtype=np.float64)
+    rep.final_residual = float(np.sqrt(np.sum((f - au) ** 2)) / fnorm)
+    rep.converged = rep.final_residual <= tol
+    return rep
+
+
+def dense_direct_solve(a_rowmajor, rhs) -> np.ndarray:
+    """Partial-pivot LU solve of the row-major n x n system (oracle path,
+    solve.cpp:116-127)."""
+    rhs = np.asarray(rhs, dtype=np.float64).reshape(-1)
+    n = rhs.size
+    a = np.asarray(a_rowmajor, dtype=np.float64).reshape(-1)
+    if a.size != n * n:
+        raise ValueError("dense_direct_solve: shape mismatch")
+    return np.linalg.solve(a.reshape(n, n), rhs)
+
+
+def assemble_dense_matrix(spec: KernelSpec, grid: Grid, rule: InclusionRule, form: ApplyForm,
+                          device: int = 0) -> np.ndarray:
+    """Dense row-major matrix of the direct operator (operators.cpp:262-303),
+    assembled on the GPU (one thread per row)."""
+    if form == ApplyForm.Mass:
+        _require_truncated(spec)
+    cn, cv = _coeff(spec)
+    if spec.profile.family == ProfileFamily.PolynomialTruncated:
+        p = Plan(dim=grid.dim, n=grid.n, family=A.TRUNCATED, route=A.ROUTE_TRUNCATED,
+                 poly=spec.profile.poly, rule=int(rule), form=int(form), delta=spec.horizon.nodes(grid),
+                 delta0=spec.horizon.delta0, coeff=cn, coeff0=cv, device=device)
+    else:
+        p = Plan(dim=grid.dim, n=grid.n, route=A.ROUTE_FULL, rule=A.POINT, form=A.DIFFERENCE,
+                 divergence=spec.symmetry == SymmetryClass.Divergence, delta=spec.horizon.nodes(grid),
+                 delta0=spec.horizon.delta0, reach=spec.horizon.max_radius(), coeff=cn, coeff0=cv,
+                 device=device, **_profile_args(spec.profile))
+    return p.assemble_dense()

@@ -108,6 +108,43 @@ def main():
     cases.update(cfg0_u=u, cfg0_out_clip=r, cfg0_pairs=p, cfg0_cdelta=cd)
     save("fractional_general", **cases)
 
+    # Krylov consumer (test_solve.cpp:73-159): manufactured solution
+    # u* = sin(2 pi x) x (1 - x), f = -L u* via the dense Leaf apply
+    sol = {}
+    for tag, n, hk, tol in (("cg_n512", 512, 0, 1e-10), ("cgnr_n256_bump", 256, 1, 1e-10),
+                            ("cg_n128_2it", 128, 0, 1e-14)):
+        x = (np.arange(n) + 0.5) / n
+        ustar = np.sin(2 * np.pi * x) * x * (1 - x)
+        L, _ = O.ref_truncated_dense(1, n, 0, hk, 0.25, ustar, O.LEAF, O.MASS)
+        f = -L
+        max_iter = 2 if tag == "cg_n128_2it" else 10 * n
+        u, it, res, conv, m = O.ref_solve_truncated(1, n, 0, hk, 0.25, f, tol, max_iter)
+        sol.update({f"{tag}_ustar": ustar, f"{tag}_f": f, f"{tag}_u": u, f"{tag}_iters": it,
+                    f"{tag}_residual": res, f"{tag}_converged": conv, f"{tag}_method": m,
+                    f"{tag}_tol": tol, f"{tag}_max_iter": max_iter})
+        if tag != "cg_n128_2it":
+            a = -O.ref_assemble_dense(1, n, 3, 0, hk, 0.25)
+            sol[f"{tag}_direct"] = O.ref_dense_direct_solve(a, f)
+    # dense CG (the "dense matvec" subcase)
+    n = 512
+    u, it, res, conv, m = O.ref_solve_truncated(1, n, 0, 0, 0.25, sol["cg_n512_f"], 1e-10, 10 * n, use_dense=True)
+    sol.update(cg_n512_dense_u=u, cg_n512_dense_iters=it, cg_n512_dense_residual=res)
+    save("solve_dirichlet", src="test_solve.cpp:73-159, nonloc_main.cpp:189-222", **sol)
+
+    # assemble_dense_matrix (operators.cpp:262-303): truncated K=1 constant
+    # (test_solve.cpp:60-71 symmetry case), K=0 bump Leaf/Point x Mass/Difference,
+    # full InverseS bump, 2-D K=0
+    asm = {}
+    for tag, dim, n, fam, K, hk, d0, rule, form, div in (
+            ("k1_const_leaf_mass", 1, 128, 3, 1, 0, 0.25, O.LEAF, O.MASS, 0),
+            ("k0_bump_leaf_mass", 1, 128, 3, 0, 1, 0.25, O.LEAF, O.MASS, 0),
+            ("k0_bump_point_diff", 1, 128, 3, 0, 1, 0.25, O.POINT, O.DIFFERENCE, 0),
+            ("inverse_s_bump", 1, 128, 0, 0, 1, 0.25, O.POINT, O.DIFFERENCE, 0),
+            ("inverse_s_bump_div", 1, 128, 0, 0, 1, 0.25, O.POINT, O.DIFFERENCE, 1),
+            ("k0_2d_leaf_mass", 2, 16, 3, 0, 1, 0.25, O.LEAF, O.MASS, 0)):
+        asm[tag] = O.ref_assemble_dense(dim, n, fam, K, hk, d0, rule, form, divergence=div)
+    save("assemble_dense", src="operators.cpp:262-303", **asm)
+
 
 if __name__ == "__main__":
     main()
