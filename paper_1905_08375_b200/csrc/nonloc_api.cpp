@@ -20,6 +20,7 @@
 #include "nonloc/geometry.hpp"
 #include "nonloc/kernel.hpp"
 #include "nonloc/operators.hpp"
+#include "nonloc/solve.hpp"
 
 namespace nonloc {
 
@@ -436,6 +437,178 @@ std::vector<double> apply_full_dense(const KernelSpec& spec, const Grid& grid, s
   d.form = NLG_DIFFERENCE;
   d.reach = spec.horizon.max_radius();
   return run_direct(d, u, pair_count, grid.total);
+}
+
+std::vector<double> assemble_dense_matrix(const KernelSpec& spec, const Grid& grid, InclusionRule rule,
+                                          ApplyForm form) {
+  if (form == ApplyForm::Mass) require_truncated(spec);
+  NodeArrays na;
+  nlg_desc d = make_desc(spec, grid, na);
+  set_profile(d, spec.profile, na);
+  if (spec.profile.family == ProfileFamily::PolynomialTruncated) {
+    d.route = NLG_ROUTE_TRUNCATED;
+    d.rule = rule == InclusionRule::Leaf ? NLG_LEAF : NLG_POINT;
+    d.form = form == ApplyForm::Mass ? NLG_MASS : NLG_DIFFERENCE;
+    d.divergence = 0;
+  } else {
+    d.route = NLG_ROUTE_FULL;
+    d.rule = NLG_POINT;
+    d.form = NLG_DIFFERENCE;
+    d.reach = spec.horizon.max_radius();
+  }
+  PlanGuard g;
+  check(nlg_plan_create(&d, &g.p));
+  std::vector<double> a(static_cast<std::size_t>(grid.total) * static_cast<std::size_t>(grid.total));
+  check(nlg_assemble_dense(g.p, a.data()));
+  return a;
+}
+
+// ---- Krylov consumer (solve.hpp) -------------------------------------------
+
+namespace {
+
+double norm2(std::span<const double> v) {
+  double s = 0.0;
+  for (double x : v) s += x * x;
+  return std::sqrt(s);
+}
+
+double dot(std::span<const double> a, std::span<const double> b) {
+  double s = 0.0;
+  for (std::size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+
+void check_finite(std::span<const double> v) {
+  for (double x : v)
+    if (!std::isfinite(x)) throw std::runtime_error("operator produced a non-finite value");
+}
+
+}  // namespace
+
+SolveReport solve_dirichlet(const ApplyFn& apply, std::span<const double> f, double tol, std::int64_t max_iter,
+                            SolveMethod method, const ApplyFn& apply_transpose) {
+  const std::size_t n = f.size();
+  SolveReport report;
+  report.method = method;
+  report.solution.assign(n, 0.0);
+  const double fnorm = norm2(f);
+  if (fnorm == 0.0) {
+    report.converged = true;
+    return report;
+  }
+  if (method == SolveMethod::CGNR && !apply_transpose)
+    throw std::invalid_argument("CGNR needs the transpose application");
+  std::vector<double>& u = report.solution;
+  std::vector<double> r(f.begin(), f.end());
+  if (method == SolveMethod::CG) {
+    std::vector<double> p = r;
+    double rr = dot(r, r);
+    for (std::int64_t it = 0; it < max_iter; ++it) {
+      if (std::sqrt(rr) / fnorm <= tol) break;
+      const std::vector<double> ap = apply(p);
+      check_finite(ap);
+      const double pap = dot(p, ap);
+      if (pap == 0.0) break;
+      const double alpha = rr / pap;
+      for (std::size_t i = 0; i < n; ++i) {
+        u[i] += alpha * p[i];
+        r[i] -= alpha * ap[i];
+      }
+      const double rr_next = dot(r, r);
+      const double beta = rr_next / rr;
+      rr = rr_next;
+      for (std::size_t i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
+      report.iterations = it + 1;
+    }
+  } else {
+    std::vector<double> z = apply_transpose(r);
+    std::vector<double> p = z;
+    double zz = dot(z, z);
+    for (std::int64_t it = 0; it < max_iter; ++it) {
+      if (norm2(r) / fnorm <= tol) break;
+      const std::vector<double> ap = apply(p);
+      check_finite(ap);
+      const double denom = dot(ap, ap);
+      if (denom == 0.0) break;
+      const double alpha = zz / denom;
+      for (std::size_t i = 0; i < n; ++i) {
+        u[i] += alpha * p[i];
+        r[i] -= alpha * ap[i];
+      }
+      z = apply_transpose(r);
+      check_finite(z);
+      const double zz_next = dot(z, z);
+      const double beta = zz_next / zz;
+      zz = zz_next;
+      for (std::size_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+      report.iterations = it + 1;
+    }
+  }
+  const std::vector<double> au = apply(u);
+  double rn = 0.0;
+  for (std::size_t i = 0; i < n; ++i) {
+    const double d = f[i] - au[i];
+    rn += d * d;
+  }
+  report.final_residual = std::sqrt(rn) / fnorm;
+  report.converged = report.final_residual <= tol;
+  return report;
+}
+
+SolveReport solve_dirichlet(TruncatedOperator& op, std::span<const double> f, double tol, std::int64_t max_iter,
+                            SolveMethod method) {
+  if (static_cast<std::int64_t>(f.size()) != op.grid().total) throw std::invalid_argument("f size does not match grid");
+  SolveReport report;
+  report.solution.resize(f.size());
+  nlg_solve_report rep{};
+  check(nlg_solve_dirichlet(op.native_plan(), f.data(), tol, max_iter,
+                            method == SolveMethod::CG ? NLG_SOLVE_CG : NLG_SOLVE_CGNR, report.solution.data(), &rep));
+  report.method = method;
+  report.iterations = rep.iterations;
+  report.final_residual = rep.final_residual;
+  report.converged = rep.converged != 0;
+  return report;
+}
+
+SolveReport solve_dirichlet(TruncatedOperator& op, std::span<const double> f, double tol, std::int64_t max_iter) {
+  return solve_dirichlet(op, f, tol, max_iter, choose_method(op.spec()));
+}
+
+SolveMethod choose_method(const KernelSpec& spec) {
+  const bool symmetric = spec.horizon.kind == HorizonKind::Constant && !spec.coefficient_fn;
+  return symmetric ? SolveMethod::CG : SolveMethod::CGNR;
+}
+
+std::vector<double> dense_direct_solve(std::span<const double> a_rowmajor, std::span<const double> rhs) {
+  const std::size_t n = rhs.size();
+  if (a_rowmajor.size() != n * n) throw std::invalid_argument("dense_direct_solve: shape mismatch");
+  std::vector<double> a(a_rowmajor.begin(), a_rowmajor.end()), b(rhs.begin(), rhs.end());
+  std::vector<std::size_t> piv(n);
+  for (std::size_t k = 0; k < n; ++k) {           // partial-pivot LU, in place
+    std::size_t p = k;
+    for (std::size_t i = k + 1; i < n; ++i)
+      if (std::abs(a[i * n + k]) > std::abs(a[p * n + k])) p = i;
+    piv[k] = p;
+    if (p != k) {
+      for (std::size_t j = 0; j < n; ++j) std::swap(a[k * n + j], a[p * n + j]);
+      std::swap(b[k], b[p]);
+    }
+    const double d = a[k * n + k];
+    if (d == 0.0) continue;
+    for (std::size_t i = k + 1; i < n; ++i) {
+      const double l = a[i * n + k] / d;
+      a[i * n + k] = l;
+      for (std::size_t j = k + 1; j < n; ++j) a[i * n + j] -= l * a[k * n + j];
+      b[i] -= l * b[k];
+    }
+  }
+  for (std::size_t k = n; k-- > 0;) {             // back substitution
+    double s = b[k];
+    for (std::size_t j = k + 1; j < n; ++j) s -= a[k * n + j] * b[j];
+    b[k] = s / a[k * n + k];
+  }
+  return b;
 }
 
 std::vector<double> apply_split(const KernelSpec& spec, const Grid& grid, int K, std::span<const double> u,

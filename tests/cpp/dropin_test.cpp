@@ -8,6 +8,7 @@
 
 #include "nonloc/bench.hpp"
 #include "nonloc/operators.hpp"
+#include "nonloc/solve.hpp"
 
 using namespace nonloc;
 
@@ -148,5 +149,97 @@ int main() {
     EXPECT(rec.max_rel_err_vs_dense <= 1e-10 && rec.dense_pairs > 0);
   }
   std::printf("[dropin] failures: %d\n", failures);
+
+  // ---- test_solve.cpp:47-170 through the drop-in solve.hpp ----
+  {
+    const std::vector<double> f0(64, 0.0);
+    const auto rep = solve_dirichlet([](std::span<const double> u) { return std::vector<double>(u.begin(), u.end()); },
+                                     f0, 1e-10, 100);
+    EXPECT(rep.converged && rep.iterations == 0);
+  }
+  {
+    const Grid g = Grid::make(1, 128);
+    const auto a = assemble_dense_matrix(truncated(1, 1, HorizonKind::Constant, 0.25), g, InclusionRule::Leaf,
+                                         ApplyForm::Mass);
+    double num = 0.0, den = 0.0;
+    for (std::int64_t i = 0; i < g.total; ++i)
+      for (std::int64_t j = 0; j < g.total; ++j) {
+        const double d = a[i * g.total + j] - a[j * g.total + i];
+        num += d * d;
+        den += a[i * g.total + j] * a[i * g.total + j];
+      }
+    EXPECT(std::sqrt(num) <= 1e-12 * std::sqrt(den));   // test_solve.cpp:60-71
+  }
+  auto manufactured = [](const Grid& g) {
+    std::vector<double> u(g.total);
+    for (std::int64_t i = 0; i < g.total; ++i) {
+      const double x = (i + 0.5) * g.h;
+      u[i] = std::sin(2.0 * 3.14159265358979323846 * x) * x * (1.0 - x);
+    }
+    return u;
+  };
+  auto negate = [](std::vector<double> v) {
+    for (double& x : v) x = -x;
+    return v;
+  };
+  {
+    const Grid g = Grid::make(1, 512);
+    const KernelSpec spec = truncated(1, 0, HorizonKind::Constant, 0.25);
+    const auto ustar = manufactured(g);
+    const auto f = negate(apply_truncated_dense(spec, g, InclusionRule::Leaf, ustar));
+    const auto apply = [&](std::span<const double> u) {
+      return negate(apply_truncated_dense(spec, g, InclusionRule::Leaf, u));
+    };
+    const auto rep = solve_dirichlet(apply, f, 1e-10, 10 * g.total);   // dense matvec subcase
+    EXPECT(rep.converged && rep.final_residual <= 1e-10);
+    EXPECT(rel(rep.solution, ustar) <= 1e-8);
+    TruncatedOperator op(spec, g);
+    const auto rep2 = solve_dirichlet(op, f, 1e-10, 10 * g.total);    // device-resident, fast apply
+    EXPECT(rep2.method == SolveMethod::CG && rep2.converged);
+    EXPECT(rel(rep2.solution, ustar) <= 1e-8);
+    auto a = assemble_dense_matrix(spec, g, InclusionRule::Leaf, ApplyForm::Mass);
+    for (double& v : a) v = -v;
+    EXPECT(rel(rep2.solution, dense_direct_solve(a, f)) <= 1e-8);
+  }
+  {
+    const Grid g = Grid::make(1, 256);
+    const KernelSpec spec = truncated(1, 0, HorizonKind::GaussianBump, 0.25);
+    EXPECT(choose_method(spec) == SolveMethod::CGNR);
+    const auto ustar = manufactured(g);
+    const auto f = negate(apply_truncated_dense(spec, g, InclusionRule::Leaf, ustar));
+    auto a = assemble_dense_matrix(spec, g, InclusionRule::Leaf, ApplyForm::Mass);
+    for (double& v : a) v = -v;
+    TruncatedOperator op(spec, g);
+    const auto rep = solve_dirichlet(op, f, 1e-10, 10 * g.total);     // CGNR, GPU transpose
+    EXPECT(rep.method == SolveMethod::CGNR && rep.converged);
+    EXPECT(rel(rep.solution, dense_direct_solve(a, f)) <= 1e-6);
+    bool threw = false;
+    try {
+      (void)solve_dirichlet([&](std::span<const double> u) { return std::vector<double>(u.begin(), u.end()); }, f,
+                            1e-10, 10, SolveMethod::CGNR);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    EXPECT(threw);
+  }
+  {
+    const Grid g = Grid::make(1, 128);
+    TruncatedOperator op(truncated(1, 0, HorizonKind::Constant, 0.25), g);
+    const auto f = negate(apply_truncated_dense(op.spec(), g, InclusionRule::Leaf, manufactured(g)));
+    const auto rep = solve_dirichlet(op, f, 1e-14, 2);
+    EXPECT(!rep.converged && rep.iterations == 2);                  // test_solve.cpp:147-158
+    std::vector<double> fn(16, 1.0);
+    bool threw = false;
+    try {
+      (void)solve_dirichlet([](std::span<const double> u) {
+        std::vector<double> out(u.begin(), u.end());
+        out[0] = std::nan("");
+        return out;
+      }, fn, 1e-10, 10);
+    } catch (const std::runtime_error&) {
+      threw = true;
+    }
+    EXPECT(threw);                                                  // test_solve.cpp:160-170
+  }
   return failures;
 }
