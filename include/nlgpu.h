@@ -197,6 +197,17 @@ typedef struct {
 nlg_status nlg_solve_dirichlet(nlg_plan* plan, const double* f, double tol, int64_t max_iter, int method,
                                double* u, nlg_solve_report* report);
 
+/* Step-1 tree instruments of the reference (tree.hpp:31-53), host side: the
+ * panels of decompose_region for one ball (pre-order, up to `cap` written;
+ * npanels = full count), the recursion-call and panel totals over every node
+ * of an n^dim grid with per-node radii (count_recur_calls; the panel total
+ * times the moment count is the reference's step3_ops per apply), and
+ * accumulate_moments (levels 0..L flattened level-major; adds = step2_ops). */
+nlg_status nlg_tree_decompose(int dim, int64_t n, const double* center, double radius, int64_t cap, int* levels,
+                              int64_t* indices, int64_t* npanels, int64_t* recur_calls);
+nlg_status nlg_tree_count(int dim, int64_t n, const double* radii, int64_t* recur_calls, int64_t* panels);
+nlg_status nlg_tree_moments(int dim, int64_t n, int K, const double* u, double* out, int64_t* adds);
+
 /* Thread-local text of the last error; "" if none. */
 const char* nlg_last_error(void);
 int nlg_abi_version(void);

@@ -102,6 +102,9 @@ def ref():
         lib.ref_solve_truncated.argtypes = [i, i, i, i, d, d, _dp, d, C.c_int64, i, _dp, _ip, _dp,
                                             C.POINTER(C.c_int), C.POINTER(C.c_int)]
         lib.ref_dense_direct_solve.argtypes = [C.c_int64, _dp, _dp, _dp]
+        lib.ref_decompose.argtypes = [i, i, _dp, d, C.c_int64, C.POINTER(C.c_int), _ip, _ip, _ip]
+        lib.ref_count_recur_calls.argtypes = [i, i, _dp, _ip]
+        lib.ref_moments.argtypes = [i, i, i, _dp, _dp, _ip]
         _ref = lib
     return _ref
 
@@ -330,3 +333,34 @@ def ref_dense_direct_solve(a, rhs):
     x = np.empty(rhs.size)
     _check_ref(ref().ref_dense_direct_solve(rhs.size, _p(a), _p(rhs), _p(x)))
     return x
+
+
+def ref_decompose(dim, n, center, radius, cap=1 << 20):
+    """decompose_region: (levels, indices, recur_calls)."""
+    c = np.zeros(3)
+    c[:dim] = center
+    lv = np.zeros(cap, dtype=np.int32)
+    ix = np.zeros(cap, dtype=np.int64)
+    npn, rc = C.c_int64(0), C.c_int64(0)
+    _check_ref(ref().ref_decompose(dim, n, _p(c), radius, cap, lv.ctypes.data_as(C.POINTER(C.c_int)),
+                                   ix.ctypes.data_as(_ip), C.byref(npn), C.byref(rc)))
+    k = min(npn.value, cap)
+    return lv[:k].copy(), ix[:k].copy(), rc.value
+
+
+def ref_count_recur_calls(dim, n, radii):
+    radii = np.ascontiguousarray(radii, dtype=np.float64)
+    t = C.c_int64(0)
+    _check_ref(ref().ref_count_recur_calls(dim, n, _p(radii), C.byref(t)))
+    return t.value
+
+
+def ref_moments(dim, n, K, u):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    L = int(round(np.log2(n)))
+    nm = 2 * K + 1 if dim == 1 else 1
+    size = sum((1 << (dim * l)) * nm for l in range(L + 1))
+    out = np.empty(size)
+    adds = C.c_int64(0)
+    _check_ref(ref().ref_moments(dim, n, K, _p(u), _p(out), C.byref(adds)))
+    return out, adds.value

@@ -392,4 +392,43 @@ int ref_dense_direct_solve(int64_t n, const double* a, const double* rhs, double
     return 0;
   } catch (const std::exception& e) { return fail(e); }
 }
+
+// Step-1 tree instruments (tree.hpp:31-53): panels of decompose_region for one
+// ball (levels / indices, up to cap) and the recursion-call count.
+int ref_decompose(int dim, int n, const double* center, double radius, int64_t cap, int* levels,
+                  int64_t* indices, int64_t* npanels, int64_t* recur_calls) {
+  try {
+    const Tree t = build_tree(Grid::make(dim, n));
+    const Point c{center[0], dim > 1 ? center[1] : 0.0, dim > 2 ? center[2] : 0.0};
+    const Decomposition d = decompose_region(t, c, radius);
+    *npanels = static_cast<int64_t>(d.panels.size());
+    *recur_calls = d.recur_calls;
+    for (int64_t k = 0; k < *npanels && k < cap; ++k) {
+      levels[k] = d.panels[k].level;
+      indices[k] = d.panels[k].index;
+    }
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_count_recur_calls(int dim, int n, const double* radii, int64_t* total) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    *total = count_recur_calls(build_tree(g), std::span<const double>(radii, g.total));
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// accumulate_moments (tree.hpp:46-48): all levels flattened level-major.
+int ref_moments(int dim, int n, int K, const double* u, double* out, int64_t* adds) {
+  try {
+    const Grid g = Grid::make(dim, n);
+    const Tree t = build_tree(g);
+    const MomentTable m = accumulate_moments(t, std::span<const double>(u, g.total), K, adds);
+    int64_t o = 0;
+    for (const auto& lv : m.levels)
+      for (double v : lv) out[o++] = v;
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
 }  // extern "C"

@@ -70,6 +70,10 @@ EXPORTS = {
     "nlg_assemble_dense": ([C.c_void_p, _dp], C.c_int),
     "nlg_solve_dirichlet": ([C.c_void_p, _dp, C.c_double, C.c_int64, C.c_int, _dp, C.POINTER(SolveReport)],
                             C.c_int),
+    "nlg_tree_decompose": ([C.c_int, C.c_int64, _dp, C.c_double, C.c_int64, C.POINTER(C.c_int), _ip, _ip, _ip],
+                           C.c_int),
+    "nlg_tree_count": ([C.c_int, C.c_int64, _dp, _ip, _ip], C.c_int),
+    "nlg_tree_moments": ([C.c_int, C.c_int64, C.c_int, _dp, _dp, _ip], C.c_int),
     "nlg_last_error": ([], C.c_char_p),
     "nlg_abi_version": ([], C.c_int),
 }

@@ -38,7 +38,8 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
     objdir = os.path.join(LIB, "obj")
     os.makedirs(objdir, exist_ok=True)
     cu = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
-    cpp = sorted(f for f in os.listdir(CSRC) if f.endswith(".cpp") and f != "nonloc_api.cpp")
+    api_srcs = ["nonloc_api.cpp", "config.cpp"]          # C++ drop-in (libnonloc_b200), g++ -std=c++20
+    cpp = sorted(f for f in os.listdir(CSRC) if f.endswith(".cpp") and f not in api_srcs)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
     headers.append(os.path.join(ROOT, "include", "nlgpu.h"))
     objs = []
@@ -57,20 +58,23 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
         src = os.path.join(CSRC, f)
         obj = os.path.join(objdir, f + ".o")
         if force or _newer(obj, [src] + headers):
-            _run([NVCC, *common, "-x", "cu", *ARCH, "-c", src, "-o", obj])
+            _run([NVCC, *common, "-Xcompiler", "-ffp-contract=off", "-x", "cu", *ARCH, "-c", src, "-o", obj])
         objs.append(obj)
     so = os.path.join(LIB, "libnlgpu.so")
     if force or _newer(so, objs):
         _run([NVCC, *ARCH, "-shared", "-o", so, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
-    # C++ drop-in API over the C-ABI
-    api = os.path.join(CSRC, "nonloc_api.cpp")
-    if os.path.exists(api):
-        so2 = os.path.join(LIB, "libnonloc_b200.so")
-        hdrs = [os.path.join(ROOT, "include", "nonloc", f)
-                for f in os.listdir(os.path.join(ROOT, "include", "nonloc"))]
-        if force or _newer(so2, [api, so] + hdrs):
-            _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
-                  api, "-o", so2, "-L", LIB, "-lnlgpu", "-Wl,-rpath,$ORIGIN"])
+    # C++ drop-in API over the C-ABI, and the drop-in CLI (tools/nonloc_cli.cpp)
+    api = [os.path.join(CSRC, f) for f in api_srcs]
+    hdrs = [os.path.join(ROOT, "include", "nonloc", f) for f in os.listdir(os.path.join(ROOT, "include", "nonloc"))]
+    so2 = os.path.join(LIB, "libnonloc_b200.so")
+    if force or _newer(so2, api + [so] + hdrs):
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-I",
+              os.path.join(ROOT, "include"), *api, "-o", so2, "-L", LIB, "-lnlgpu", "-Wl,-rpath,$ORIGIN"])
+    cli_src = os.path.join(ROOT, "tools", "nonloc_cli.cpp")
+    cli = os.path.join(LIB, "nonloc")
+    if os.path.exists(cli_src) and (force or _newer(cli, [cli_src, so2] + hdrs)):
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I", os.path.join(ROOT, "include"), cli_src,
+              "-o", cli, "-L", LIB, "-lnonloc_b200", "-lnlgpu", "-Wl,-rpath,$ORIGIN"])
     return so
 
 

@@ -21,6 +21,7 @@
 #include "nonloc/kernel.hpp"
 #include "nonloc/operators.hpp"
 #include "nonloc/solve.hpp"
+#include "nonloc/tree.hpp"
 
 namespace nonloc {
 
@@ -382,7 +383,8 @@ TruncatedOperator::TruncatedOperator(const KernelSpec& spec, const Grid& grid) :
 TruncatedOperator::~TruncatedOperator() { nlg_plan_destroy(plan_); }
 
 TruncatedOperator::TruncatedOperator(TruncatedOperator&& o) noexcept
-    : spec_(std::move(o.spec_)), grid_(o.grid_), plan_(o.plan_), applies_(o.applies_) {
+    : spec_(std::move(o.spec_)), grid_(o.grid_), plan_(o.plan_), applies_(o.applies_), tree_(o.tree_),
+      have_totals_(o.have_totals_), recur_(o.recur_), panels_(o.panels_), decomp_(std::move(o.decomp_)) {
   o.plan_ = nullptr;
 }
 
@@ -437,6 +439,152 @@ std::vector<double> apply_full_dense(const KernelSpec& spec, const Grid& grid, s
   d.form = NLG_DIFFERENCE;
   d.reach = spec.horizon.max_radius();
   return run_direct(d, u, pair_count, grid.total);
+}
+
+// ---- Step-1 tree API (tree.hpp) over the host instruments in libnlgpu -------
+
+std::int64_t Tree::panels_at(int level) const { return std::int64_t{1} << (grid.dim * level); }
+
+PanelId Tree::child(const PanelId& id, int which) const {
+  const std::int64_t per = std::int64_t{1} << id.level;
+  std::int64_t k[3] = {0, 0, 0}, rest = id.index;
+  for (int j = grid.dim - 1; j >= 0; --j) {
+    k[j] = rest % per;
+    rest /= per;
+  }
+  std::int64_t f = 0;
+  for (int j = 0; j < grid.dim; ++j) f = f * (2 * per) + (2 * k[j] + ((which >> j) & 1));
+  return {id.level + 1, f};
+}
+
+PanelId Tree::parent(const PanelId& id) const {
+  if (id.level == 0) throw std::invalid_argument("root has no parent");
+  const std::int64_t per = std::int64_t{1} << id.level;
+  std::int64_t k[3] = {0, 0, 0}, rest = id.index;
+  for (int j = grid.dim - 1; j >= 0; --j) {
+    k[j] = rest % per;
+    rest /= per;
+  }
+  std::int64_t f = 0;
+  for (int j = 0; j < grid.dim; ++j) f = f * (per / 2) + k[j] / 2;
+  return {id.level - 1, f};
+}
+
+Tree build_tree(const Grid& grid) {
+  if (!is_power_of_two(grid.n)) throw std::invalid_argument("tree requires n to be a power of two");
+  Tree t;
+  t.grid = grid;
+  t.depth = grid.levels();
+  return t;
+}
+
+Decomposition decompose_region(const Tree& tree, const Point& center, double radius) {
+  Decomposition d;
+  d.center = center;
+  d.radius = radius;
+  std::int64_t cap = 4096;
+  for (;;) {
+    std::vector<int> lv(cap);
+    std::vector<int64_t> ix(cap);
+    int64_t np = 0, rc = 0;
+    check(nlg_tree_decompose(tree.grid.dim, tree.grid.n, center.data(), radius, cap, lv.data(), ix.data(), &np,
+                             &rc));
+    if (np > cap) {
+      cap = np;
+      continue;
+    }
+    d.recur_calls = rc;
+    d.panels.resize(np);
+    for (int64_t k = 0; k < np; ++k) d.panels[k] = {lv[k], ix[k]};
+    return d;
+  }
+}
+
+MomentTable accumulate_moments(const Tree& tree, std::span<const double> u, int K, std::int64_t* add_count) {
+  const Grid& g = tree.grid;
+  if (static_cast<std::int64_t>(u.size()) != g.total) throw std::invalid_argument("u size does not match grid");
+  MomentTable t;
+  t.num_moments = g.dim == 1 ? 2 * K + 1 : 1;
+  if (K < 0 || (g.dim >= 2 && K != 0)) throw std::invalid_argument("moments support K >= 0 in 1d, K = 0 in 2d/3d");
+  std::vector<std::int64_t> sizes;
+  std::int64_t tot = 0;
+  for (int l = 0; l <= tree.depth; ++l) {
+    sizes.push_back(tree.panels_at(l) * t.num_moments);
+    tot += sizes.back();
+  }
+  std::vector<double> flat(tot);
+  int64_t adds = 0;
+  check(nlg_tree_moments(g.dim, g.n, K, u.data(), flat.data(), &adds));
+  if (add_count) *add_count += adds;
+  std::int64_t o = 0;
+  for (std::int64_t sz : sizes) {
+    t.levels.emplace_back(flat.begin() + o, flat.begin() + o + sz);
+    o += sz;
+  }
+  return t;
+}
+
+std::int64_t count_recur_calls(const Tree& tree, std::span<const double> radii) {
+  if (static_cast<std::int64_t>(radii.size()) != tree.grid.total)
+    throw std::invalid_argument("radii size does not match grid");
+  int64_t rc = 0, pc = 0;
+  check(nlg_tree_count(tree.grid.dim, tree.grid.n, radii.data(), &rc, &pc));
+  return rc;
+}
+
+namespace {
+std::vector<double> node_radii(const KernelSpec& spec, const Grid& grid) {
+  std::vector<double> r(grid.total);
+  for (std::int64_t i = 0; i < grid.total; ++i) r[i] = spec.horizon_at(node_position(grid, i));
+  return r;
+}
+}  // namespace
+
+const Tree& TruncatedOperator::tree() const {
+  if (tree_.grid.total != grid_.total || tree_.grid.dim != grid_.dim) tree_ = build_tree(grid_);
+  return tree_;
+}
+
+void TruncatedOperator::tree_totals() const {
+  if (have_totals_) return;
+  const std::vector<double> r = node_radii(spec_, grid_);
+  int64_t rc = 0, pc = 0;
+  check(nlg_tree_count(grid_.dim, grid_.n, r.data(), &rc, &pc));
+  recur_ = rc;
+  panels_ = pc;
+  have_totals_ = true;
+}
+
+const std::vector<Decomposition>& TruncatedOperator::decompositions() const {
+  if (decomp_.empty()) {
+    const Tree& t = tree();
+    decomp_.reserve(grid_.total);
+    for (std::int64_t i = 0; i < grid_.total; ++i) {
+      const Point x = node_position(grid_, i);
+      decomp_.push_back(decompose_region(t, x, spec_.horizon_at(x)));
+    }
+  }
+  return decomp_;
+}
+
+std::int64_t TruncatedOperator::recur_calls() const {
+  tree_totals();
+  return recur_;
+}
+
+std::int64_t TruncatedOperator::step2_ops() const {
+  const int nm = grid_.dim == 1 ? 2 * spec_.profile.order + 1 : 1;
+  std::int64_t per = 0;
+  for (int l = 0; l < grid_.levels(); ++l)
+    per += (std::int64_t{1} << (grid_.dim * l)) * (std::int64_t{1} << grid_.dim) * nm;
+  return applies_ * per;
+}
+
+std::int64_t TruncatedOperator::step3_ops() const {
+  if (applies_ == 0) return 0;
+  tree_totals();
+  const int nm = grid_.dim == 1 ? 2 * spec_.profile.order + 1 : 1;
+  return applies_ * panels_ * nm;
 }
 
 std::vector<double> assemble_dense_matrix(const KernelSpec& spec, const Grid& grid, InclusionRule rule,
@@ -702,6 +850,10 @@ BenchRecord run_apply_case(const KernelSpec& spec, const Grid& grid, std::uint64
     }
     rec.max_rel_err_vs_dense = std::max(rec.max_rel_err_vs_dense, mx > 0.0 ? md / mx : md);
   }
+  // Step-1 instruments, computed on the host by the same Algorithm 1 the
+  // reference runs in its constructor (counters match it exactly)
+  rec.recur_calls = op.recur_calls();
+  rec.step2_ops = op.step2_ops();
   rec.step3_ops = op.step3_ops();
   return rec;
 }

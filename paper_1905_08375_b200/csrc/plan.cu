@@ -671,3 +671,50 @@ nlg_status nlg_solve_dirichlet(nlg_plan* plan, const double* f, double tol, int6
   for (void* q : bufs) cudaFree(q);
   return st;
 }
+
+// ---- Step-1 tree instruments -------------------------------------------------
+
+namespace {
+bool pow2(int64_t n) { return n >= 2 && (n & (n - 1)) == 0; }
+}  // namespace
+
+nlg_status nlg_tree_decompose(int dim, int64_t n, const double* center, double radius, int64_t cap, int* levels,
+                              int64_t* indices, int64_t* npanels, int64_t* recur_calls) {
+  using namespace nlg;
+  return guard([&] {
+    require(center && npanels && recur_calls, "null argument");
+    require(dim >= 1 && dim <= 3, "grid dimension must be 1, 2 or 3");
+    require(pow2(n), "tree requires n to be a power of two");
+    require(radius > 0.0, "radius must be positive");
+    std::vector<int> lv;
+    std::vector<int64_t> ix;
+    tree_decompose(dim, n, center, radius, lv, ix, *recur_calls);
+    *npanels = static_cast<int64_t>(lv.size());
+    for (int64_t k = 0; k < *npanels && k < cap; ++k) {
+      if (levels) levels[k] = lv[k];
+      if (indices) indices[k] = ix[k];
+    }
+  });
+}
+
+nlg_status nlg_tree_count(int dim, int64_t n, const double* radii, int64_t* recur_calls, int64_t* panels) {
+  using namespace nlg;
+  return guard([&] {
+    require(radii && recur_calls && panels, "null argument");
+    require(dim >= 1 && dim <= 3, "grid dimension must be 1, 2 or 3");
+    require(pow2(n), "tree requires n to be a power of two");
+    tree_count(dim, n, radii, *recur_calls, *panels);
+  });
+}
+
+nlg_status nlg_tree_moments(int dim, int64_t n, int K, const double* u, double* out, int64_t* adds) {
+  using namespace nlg;
+  return guard([&] {
+    require(u && out, "null argument");
+    require(dim >= 1 && dim <= 3, "grid dimension must be 1, 2 or 3");
+    require(pow2(n), "tree requires n to be a power of two");
+    require(K >= 0 && (dim == 1 || K == 0), "moments support K >= 0 in 1d, K = 0 in 2d/3d");
+    const int64_t a = tree_moments(dim, n, K, u, out);
+    if (adds) *adds = a;
+  });
+}

@@ -122,6 +122,12 @@ void dev_xpby(double* p, const double* z, double beta, int64_t n, cudaStream_t s
 void dev_negate(double* x, int64_t n, cudaStream_t s);
 void dev_diff(double* d, const double* f, const double* x, int64_t n, cudaStream_t s);
 
+// Step-1 tree instruments (tree.cpp), host side
+void tree_decompose(int dim, int64_t n, const double* center, double radius, std::vector<int>& levels,
+                    std::vector<int64_t>& indices, int64_t& recur_calls);
+void tree_count(int dim, int64_t n, const double* radii, int64_t& recur_calls, int64_t& panels);
+int64_t tree_moments(int dim, int64_t n, int K, const double* u, double* out);
+
 // host algebra (algebra.cpp)
 std::vector<double> match_polynomial(int K, double c);
 void match_polynomial_exact(int K, int64_t* num, int64_t* den);

@@ -395,6 +395,40 @@ class TruncatedOperator:
         self._applies += 1
         return self._plan.apply_fast(u)
 
+    # -- Step-1 instruments (operators.hpp:35-42), computed lazily on the host --
+    def _radii(self) -> np.ndarray:
+        d = self._spec.horizon.nodes(self._grid)
+        return np.full(self._grid.total, self._spec.horizon.delta0) if d is None else d
+
+    def _tree_totals(self):
+        if getattr(self, "_totals", None) is None:
+            self._totals = count_tree(self._grid, self._radii())
+        return self._totals
+
+    def tree(self) -> "Tree":
+        return build_tree(self._grid)
+
+    def decompositions(self) -> list:
+        """Per-node Algorithm-1 panel lists (host; O(N x panels) memory, as the reference)."""
+        t = self.tree()
+        r = self._radii()
+        return [decompose_region(t, node_position(self._grid, i), float(r[i])) for i in range(self._grid.total)]
+
+    def recur_calls(self) -> int:
+        return self._tree_totals()[0]
+
+    def step2_ops(self) -> int:
+        nm = 2 * self._spec.profile.order + 1 if self._grid.dim == 1 else 1
+        d, L = self._grid.dim, self._grid.levels()
+        return self._applies * sum((1 << (d * l)) * (1 << d) * nm for l in range(L))
+
+    def step3_ops(self) -> int:
+        nm = 2 * self._spec.profile.order + 1 if self._grid.dim == 1 else 1
+        return self._applies * self._tree_totals()[1] * nm
+
+    def reset_counters(self) -> None:
+        self._applies = 0
+
     def solve_dirichlet(self, f, tol: float, max_iter: int, method: Optional["SolveMethod"] = None) -> "SolveReport":
         """solve_dirichlet(-L, f) with the vectors resident on the GPU: CG for a
         symmetric operator (choose_method), CGNR with the GPU transpose apply
@@ -658,3 +692,139 @@ def assemble_dense_matrix(spec: KernelSpec, grid: Grid, rule: InclusionRule, for
                  delta0=spec.horizon.delta0, reach=spec.horizon.max_radius(), coeff=cn, coeff0=cv,
                  device=device, **_profile_args(spec.profile))
     return p.assemble_dense()
+
+
+# ---------------------------------------------------------------------------
+# Step-1 tree API (reference include/nonloc/tree.hpp), host side
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class PanelId:
+    level: int
+    index: int
+
+
+@dataclass
+class Tree:
+    grid: Grid
+    depth: int
+
+    def panels_at(self, level: int) -> int:
+        return 1 << (self.grid.dim * level)
+
+    def _k(self, pid: PanelId):
+        per = 1 << pid.level
+        rest, k = pid.index, [0, 0, 0]
+        for j in range(self.grid.dim - 1, -1, -1):
+            k[j] = rest % per
+            rest //= per
+        return k
+
+    def child(self, pid: PanelId, which: int) -> PanelId:
+        per, k = 1 << pid.level, self._k(pid)
+        f = 0
+        for j in range(self.grid.dim):
+            f = f * (2 * per) + (2 * k[j] + ((which >> j) & 1))
+        return PanelId(pid.level + 1, f)
+
+    def parent(self, pid: PanelId) -> PanelId:
+        if pid.level == 0:
+            raise ValueError("root has no parent")
+        per, k = 1 << pid.level, self._k(pid)
+        f = 0
+        for j in range(self.grid.dim):
+            f = f * (per // 2) + k[j] // 2
+        return PanelId(pid.level - 1, f)
+
+    def bounds(self, pid: PanelId):
+        w = 1.0 / (1 << pid.level)
+        k = self._k(pid)
+        return ([k[j] * w for j in range(self.grid.dim)], [(k[j] + 1) * w for j in range(self.grid.dim)])
+
+    def is_leaf(self, pid: PanelId) -> bool:
+        return pid.level == self.depth
+
+
+def build_tree(grid: Grid) -> Tree:
+    if not _is_pow2(grid.n):
+        raise ValueError("tree requires n to be a power of two")
+    return Tree(grid, grid.levels())
+
+
+def node_position(grid: Grid, i: int) -> np.ndarray:
+    k, rest = [0, 0, 0], int(i)
+    for j in range(grid.dim - 1, -1, -1):
+        k[j] = rest % grid.n
+        rest //= grid.n
+    return np.array([(k[j] + 0.5) * grid.h for j in range(grid.dim)])
+
+
+@dataclass
+class Decomposition:
+    center: np.ndarray
+    radius: float
+    panels: list
+    recur_calls: int
+
+
+def decompose_region(tree: Tree, center, radius: float) -> Decomposition:
+    """Algorithm 1 panels (pre-order) covering B_r(center) at leaf resolution."""
+    if radius <= 0.0:
+        raise ValueError("radius must be positive")
+    c = np.zeros(3)
+    c[:tree.grid.dim] = np.asarray(center, dtype=np.float64).reshape(-1)[:tree.grid.dim]
+    cap = 1 << 16
+    while True:
+        lv = np.zeros(cap, dtype=np.int32)
+        ix = np.zeros(cap, dtype=np.int64)
+        npn, rc = C.c_int64(0), C.c_int64(0)
+        A.check(A.lib().nlg_tree_decompose(tree.grid.dim, tree.grid.n, A.dptr(c), radius, cap,
+                                           lv.ctypes.data_as(C.POINTER(C.c_int)), ix.ctypes.data_as(A._ip),
+                                           C.byref(npn), C.byref(rc)))
+        if npn.value <= cap:
+            break
+        cap = npn.value
+    panels = [PanelId(int(lv[k]), int(ix[k])) for k in range(npn.value)]
+    return Decomposition(c[:tree.grid.dim].copy(), radius, panels, rc.value)
+
+
+def count_tree(grid: Grid, radii) -> tuple:
+    """(recur calls, panels) summed over every node's ball (host threads)."""
+    r = np.ascontiguousarray(radii, dtype=np.float64)
+    if r.size != grid.total:
+        raise ValueError("radii size does not match grid")
+    rc, pc = C.c_int64(0), C.c_int64(0)
+    A.check(A.lib().nlg_tree_count(grid.dim, grid.n, A.dptr(r), C.byref(rc), C.byref(pc)))
+    return rc.value, pc.value
+
+
+def count_recur_calls(tree: Tree, radii) -> int:
+    return count_tree(tree.grid, radii)[0]
+
+
+@dataclass
+class MomentTable:
+    num_moments: int
+    levels: list
+
+    def moment(self, pid: PanelId, m: int) -> float:
+        return float(self.levels[pid.level][pid.index * self.num_moments + m])
+
+
+def accumulate_moments(tree: Tree, u, K: int, add_count: Optional[list] = None) -> MomentTable:
+    g = tree.grid
+    u = _check_u(g, u)
+    if K < 0 or (g.dim >= 2 and K != 0):
+        raise ValueError("moments support K >= 0 in 1d, K = 0 in 2d/3d")
+    nm = 2 * K + 1 if g.dim == 1 else 1
+    sizes = [tree.panels_at(l) * nm for l in range(tree.depth + 1)]
+    out = np.empty(sum(sizes))
+    adds = C.c_int64(0)
+    A.check(A.lib().nlg_tree_moments(g.dim, g.n, K, A.dptr(u), A.dptr(out), C.byref(adds)))
+    if add_count is not None:
+        add_count.append(adds.value)
+    levels, o = [], 0
+    for sz in sizes:
+        levels.append(out[o:o + sz])
+        o += sz
+    return MomentTable(nm, levels)

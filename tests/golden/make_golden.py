@@ -145,6 +145,32 @@ def main():
         asm[tag] = O.ref_assemble_dense(dim, n, fam, K, hk, d0, rule, form, divergence=div)
     save("assemble_dense", src="operators.cpp:262-303", **asm)
 
+    # Step-1 tree API (tree.hpp:31-53; test_tree.cpp:83-133, 214-249):
+    # decompose_region panel lists, count_recur_calls, accumulate_moments
+    rng = np.random.default_rng(77)
+    tr = {}
+    k = 0
+    for dim, n in ((1, 64), (1, 1024), (2, 32), (3, 8)):
+        for _ in range(6):
+            c = rng.random(dim)
+            r = 0.02 + 0.5 * rng.random()
+            lv, ix, rc = O.ref_decompose(dim, n, c, r)
+            tr.update({f"d{k}_dim": dim, f"d{k}_n": n, f"d{k}_c": c, f"d{k}_r": r, f"d{k}_levels": lv,
+                       f"d{k}_indices": ix, f"d{k}_recur": rc})
+            k += 1
+    tr["ndecomp"] = k
+    for dim, n in ((1, 256), (2, 32), (3, 8)):
+        radii = 0.05 + 0.3 * rng.random(n ** dim)
+        tr[f"radii{dim}"] = radii
+        tr[f"recur{dim}"] = O.ref_count_recur_calls(dim, n, radii)
+    for dim, n, K in ((1, 16, 0), (1, 16, 3), (2, 8, 0), (3, 4, 0)):
+        u = O.ref_random_vector(n ** dim, 9)
+        m, adds = O.ref_moments(dim, n, K, u)
+        tr[f"mom{dim}_{K}_u"] = u
+        tr[f"mom{dim}_{K}"] = m
+        tr[f"mom{dim}_{K}_adds"] = adds
+    save("tree_api", src="tree.hpp:31-53, tree.cpp", **tr)
+
 
 if __name__ == "__main__":
     main()

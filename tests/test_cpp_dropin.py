@@ -29,6 +29,10 @@ def test_dropin_reference_cases_on_gpu():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    exe = EXE if os.path.exists(EXE) else build_test()
+    hdr = os.path.join(ROOT, "include", "nonloc")
+    deps = [os.path.join(LIB, "libnonloc_b200.so"), os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp")] + \
+        [os.path.join(hdr, f) for f in os.listdir(hdr)]
+    fresh = os.path.exists(EXE) and all(os.path.getmtime(EXE) >= os.path.getmtime(d) for d in deps)
+    exe = EXE if fresh else build_test()
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
