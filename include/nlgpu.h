@@ -197,6 +197,11 @@ typedef struct {
 nlg_status nlg_solve_dirichlet(nlg_plan* plan, const double* f, double tol, int64_t max_iter, int method,
                                double* u, nlg_solve_report* report);
 
+/* Short exponential sum for |d|^-alpha on the narrow window [lo, hi]
+ * (far-end tails of the 1-D fractional fast path); arrays of max_terms. */
+nlg_status nlg_expsum_fit_narrow(double alpha, int64_t lo, int64_t hi, double tol, int max_terms, double* rate,
+                                 double* weight, int* terms, double* rel_err);
+
 /* Step-1 tree instruments of the reference (tree.hpp:31-53), host side: the
  * panels of decompose_region for one ball (pre-order, up to `cap` written;
  * npanels = full count), the recursion-call and panel totals over every node

@@ -70,6 +70,8 @@ EXPORTS = {
     "nlg_assemble_dense": ([C.c_void_p, _dp], C.c_int),
     "nlg_solve_dirichlet": ([C.c_void_p, _dp, C.c_double, C.c_int64, C.c_int, _dp, C.POINTER(SolveReport)],
                             C.c_int),
+    "nlg_expsum_fit_narrow": ([C.c_double, C.c_int64, C.c_int64, C.c_double, C.c_int, _dp, _dp,
+                               C.POINTER(C.c_int), _dp], C.c_int),
     "nlg_tree_decompose": ([C.c_int, C.c_int64, _dp, C.c_double, C.c_int64, C.POINTER(C.c_int), _ip, _ip, _ip],
                            C.c_int),
     "nlg_tree_count": ([C.c_int, C.c_int64, _dp, _ip, _ip], C.c_int),
@@ -120,4 +122,5 @@ def dptr(a):
     return a.ctypes.data_as(_dp)
 
 
-STAGES = ["direct", "span_scan", "span_eval", "es_aggregate", "es_carry", "es_main", "es_combine", "stencil"]
+STAGES = ["direct", "span_scan", "span_eval", "es_aggregate", "es_carry", "es_main", "es_combine", "stencil",
+          "es_fft"]

@@ -62,7 +62,8 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
         objs.append(obj)
     so = os.path.join(LIB, "libnlgpu.so")
     if force or _newer(so, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", so, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
+        _run([NVCC, *ARCH, "-shared", "-o", so, *objs, "-lcudart_static", "-L/usr/local/cuda/lib64", "-lcufft",
+              "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-lrt", "-ldl", "-lpthread"])
     # C++ drop-in API over the C-ABI, and the drop-in CLI (tools/nonloc_cli.cpp)
     api = [os.path.join(CSRC, f) for f in api_srcs]
     hdrs = [os.path.join(ROOT, "include", "nonloc", f) for f in os.listdir(os.path.join(ROOT, "include", "nonloc"))]

@@ -175,6 +175,127 @@ std::vector<double> lstsq(std::vector<double> A, std::vector<double> b, int m, i
 
 }  // namespace
 
+
+// Short exponential sum for d^-alpha on a NARROW window [lo, hi] (ratio a few):
+// the far-end tails of the 1-D fractional operator. Candidate rates on a log
+// grid, columns scaled to relative error; column-pivoted Householder QR (long
+// double) orders them by independence; the first M are refit by long-double
+// least squares, M growing until the worst relative error over every integer
+// of the window is <= tol (or max_terms is reached: rel_err tells).
+ExpSum fit_exponential_sum_narrow(double alpha, int64_t lo, int64_t hi, double tol, int max_terms) {
+  using ld = long double;
+  ExpSum es;
+  es.near = static_cast<int>(lo - 1);
+  es.dmax = hi;
+  if (hi < lo || lo < 1) return es;
+  const ld a = static_cast<ld>(lo), r = static_cast<ld>(hi) / a;
+  const int nc = 150, ns = 402;
+  std::vector<ld> tau(nc), xs(ns);
+  for (int k = 0; k < nc; ++k) tau[k] = std::exp(std::log(1e-3L / r) + (std::log(60.0L) - std::log(1e-3L / r)) * k / (nc - 1));
+  xs[0] = 1.0L;
+  xs[ns - 1] = r;
+  const ld pi = 3.141592653589793238462643383279502884L;
+  for (int i = 1; i < ns - 1; ++i) xs[i] = 1.0L + (r - 1.0L) * (1.0L - std::cos(pi * (i - 0.5L) / (ns - 2))) / 2.0L;
+  // E[i][k] = exp(-tau_k x_i) x_i^alpha  (so the target is 1: relative error)
+  std::vector<ld> E(static_cast<size_t>(ns) * nc);
+  for (int i = 0; i < ns; ++i)
+    for (int k = 0; k < nc; ++k) E[i * nc + k] = std::exp(-tau[k] * xs[i]) * std::pow(xs[i], static_cast<ld>(alpha));
+  // column-pivoted Householder QR on a copy: pivot order
+  std::vector<ld> W = E;
+  std::vector<int> piv(nc);
+  for (int k = 0; k < nc; ++k) piv[k] = k;
+  const int kmax = std::min(max_terms, nc);
+  for (int k = 0; k < kmax; ++k) {
+    int best = k;
+    ld bn = -1;
+    for (int j = k; j < nc; ++j) {
+      ld s = 0;
+      for (int i = k; i < ns; ++i) s += W[i * nc + j] * W[i * nc + j];
+      if (s > bn) { bn = s; best = j; }
+    }
+    if (best != k) {
+      for (int i = 0; i < ns; ++i) std::swap(W[i * nc + k], W[i * nc + best]);
+      std::swap(piv[k], piv[best]);
+    }
+    const ld nrm = std::sqrt(bn);
+    if (nrm == 0) break;
+    const ld al = W[k * nc + k] > 0 ? -nrm : nrm;
+    std::vector<ld> v(ns - k);
+    for (int i = k; i < ns; ++i) v[i - k] = W[i * nc + k];
+    v[0] -= al;
+    ld vn = 0;
+    for (ld x : v) vn += x * x;
+    if (vn == 0) continue;
+    for (int j = k; j < nc; ++j) {
+      ld sdot = 0;
+      for (int i = k; i < ns; ++i) sdot += v[i - k] * W[i * nc + j];
+      sdot = 2 * sdot / vn;
+      for (int i = k; i < ns; ++i) W[i * nc + j] -= sdot * v[i - k];
+    }
+  }
+  for (int M = 2; M <= kmax; ++M) {
+    // long-double least squares on the first M pivot columns
+    std::vector<ld> A(static_cast<size_t>(ns) * M), b(ns, 1.0L);
+    for (int i = 0; i < ns; ++i)
+      for (int j = 0; j < M; ++j) A[i * M + j] = E[i * nc + piv[j]];
+    for (int k = 0; k < M; ++k) {
+      ld nrm = 0;
+      for (int i = k; i < ns; ++i) nrm += A[i * M + k] * A[i * M + k];
+      nrm = std::sqrt(nrm);
+      if (nrm == 0) continue;
+      const ld al = A[k * M + k] > 0 ? -nrm : nrm;
+      std::vector<ld> v(ns - k);
+      for (int i = k; i < ns; ++i) v[i - k] = A[i * M + k];
+      v[0] -= al;
+      ld vn = 0;
+      for (ld x : v) vn += x * x;
+      if (vn == 0) continue;
+      for (int j = k; j < M; ++j) {
+        ld sdot = 0;
+        for (int i = k; i < ns; ++i) sdot += v[i - k] * A[i * M + j];
+        sdot = 2 * sdot / vn;
+        for (int i = k; i < ns; ++i) A[i * M + j] -= sdot * v[i - k];
+      }
+      ld sb = 0;
+      for (int i = k; i < ns; ++i) sb += v[i - k] * b[i];
+      sb = 2 * sb / vn;
+      for (int i = k; i < ns; ++i) b[i] -= sb * v[i - k];
+    }
+    std::vector<ld> c(M, 0);
+    for (int k = M - 1; k >= 0; --k) {
+      ld sm = b[k];
+      for (int j = k + 1; j < M; ++j) sm -= A[k * M + j] * c[j];
+      c[k] = A[k * M + k] != 0 ? sm / A[k * M + k] : 0;
+    }
+    std::vector<double> rate(M), weight(M);
+    for (int j = 0; j < M; ++j) {
+      rate[j] = static_cast<double>(tau[piv[j]] / a);
+      weight[j] = static_cast<double>(c[j] * std::pow(a, static_cast<ld>(-alpha)));
+    }
+    double worst = 0.0;
+    for (int64_t d = lo; d <= hi; ++d) {
+      const double x = static_cast<double>(d);
+      double sm = 0.0;
+      for (int j = 0; j < M; ++j) sm += weight[j] * std::exp(-rate[j] * x);
+      worst = std::max(worst, std::fabs(sm * std::pow(x, alpha) - 1.0));
+      if (worst > tol && M < kmax) break;   // early out: try more terms
+    }
+    if (worst <= tol || M == kmax) {
+      std::vector<int> idx(M);
+      for (int j = 0; j < M; ++j) idx[j] = j;
+      std::sort(idx.begin(), idx.end(), [&](int x, int y) { return rate[x] < rate[y]; });
+      for (int j : idx) {
+        es.rate.push_back(rate[j]);
+        es.weight.push_back(weight[j]);
+      }
+      es.terms = M;
+      es.rel_err = worst;
+      return es;
+    }
+  }
+  return es;
+}
+
 ExpSum fit_exponential_sum(double alpha, int near, int64_t dmax, double tol) {
   ExpSum es;
   es.near = near;

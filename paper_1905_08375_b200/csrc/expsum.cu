@@ -34,6 +34,8 @@
 #include <cmath>
 #include <vector>
 
+#include <cufft.h>
+
 #include "plan.hpp"
 
 namespace nlg {
@@ -58,13 +60,15 @@ struct PassArgs {
   int64_t q0;            // positions-space index of segment 0 (= o0' + P + 1)
   int64_t nseg;          // segments covering [q0, n_in)
   int M;                 // real terms
+  int64_t off;           // fixed-offset target distance (near window P+1, or Dmax+1 in FFT mode)
+  int dth;               // fixed-offset targets need D > dth (P; -1 in FFT mode: every target)
   int nf;                // fields (1: u, 2: u and kappa u)
   const int* tinfo;      // positions space: (tfirst << 2) | count, -1 none
   const int* dtarget;    // D of each output target in this direction (output order)
   const double* rate;    // t_m (global; coefficient resets)
   const double* segpow;  // lambda_m^kL (global; carries)
-  double* agg;           // [nseg][kMT * nf]  (value fastest: the carry scans read it coalesced)
-  double* carry;         // [nseg][kMT * nf]  G at the end of each segment
+  double* agg;           // [nseg][M * nf]  (value fastest: the carry scans read it coalesced)
+  double* carry;         // [nseg][M * nf]  G at the end of each segment
   double* facc;          // [nf][n_out] far field of F (near-window part +=, far ends -=)
 };
 
@@ -85,7 +89,7 @@ constexpr int kSegs = 32;                        // segments per CTA (one per la
 constexpr int kNodes = kSegs * kL;               // nodes per CTA
 constexpr int kNodesP = kSegs * kLP;             // padded
 constexpr int kMaxChunks = 8;                    // warps per CTA (one per term chunk)
-constexpr int kChunkCap = 12;                    // terms per chunk
+constexpr int kChunkCap = 16;                    // terms per chunk (at most)
 
 struct ChunkPlan {
   int n;                                         // chunks
@@ -103,6 +107,15 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool in) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(in ? 4 : 0) : "memory");
 }
 
+// warp-uniform shared-memory broadcast the compiler may not hoist into
+// registers (the walks keep their register file for the recurrence states)
+__device__ __forceinline__ double2 ld_shared2_any(const double2* p) {
+  double2 v;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+
 // walk of one warp: the MT terms of one chunk, both fields, over its lane's
 // segment. (lambda, c lambda^{P+1}) pairs come from shared memory (warp-uniform
 // broadcasts); states and far-window coefficients live in registers; the
@@ -116,7 +129,7 @@ __device__ __forceinline__ void es_walk_chunk(const PassArgs& a, const double2* 
 #pragma unroll
   for (int m = 0; m < MT; ++m)
 #pragma unroll
-    for (int c = 0; c < NF; ++c) g[m][c] = MAIN && m < cnt ? a.carry[seg * (kMT * NF) + (mb + m) * NF + c] : 0.0;
+    for (int c = 0; c < NF; ++c) g[m][c] = MAIN && m < cnt ? a.carry[seg * (a.M * NF) + (mb + m) * NF + c] : 0.0;
   const int li = lane * kLP;
   if (!MAIN) {
 #pragma unroll 2
@@ -135,7 +148,7 @@ __device__ __forceinline__ void es_walk_chunk(const PassArgs& a, const double2* 
     for (int m = 0; m < MT; ++m)
       if (m < cnt)                                           // padding terms write nothing
 #pragma unroll
-        for (int c = 0; c < NF; ++c) a.agg[seg * (kMT * NF) + (mb + m) * NF + c] = g[m][c];
+        for (int c = 0; c < NF; ++c) a.agg[seg * (a.M * NF) + (mb + m) * NF + c] = g[m][c];
     return;
   }
   double coef[SLOW ? MT : 1];
@@ -213,7 +226,8 @@ __device__ __forceinline__ void es_walk_dispatch(int mt, const PassArgs& a, cons
   switch (mt) {
     case 4: es_walk_chunk<NF, MAIN, 4, SLOW>(a, lc, tab, mb, cnt, sf, sti, sac, sy, seg, pseg); break;
     case 8: es_walk_chunk<NF, MAIN, 8, SLOW>(a, lc, tab, mb, cnt, sf, sti, sac, sy, seg, pseg); break;
-    default: es_walk_chunk<NF, MAIN, 12, SLOW>(a, lc, tab, mb, cnt, sf, sti, sac, sy, seg, pseg); break;
+    case 12: es_walk_chunk<NF, MAIN, 12, SLOW>(a, lc, tab, mb, cnt, sf, sti, sac, sy, seg, pseg); break;
+    default: es_walk_chunk<NF, MAIN, 16, SLOW>(a, lc, tab, mb, cnt, sf, sti, sac, sy, seg, pseg); break;
   }
 }
 
@@ -240,7 +254,7 @@ __global__ void __launch_bounds__(32 * kMaxChunks) es_walk(PassArgs a, ChunkPlan
     if (NF == 2) cp_async8(sf + kNodesP + si, a.kappa + x, in);
     if (MAIN) {
       if (cp.any_slow) cp_async4(sti + si, a.tinfo + (in ? p : 0), in);
-      const int64_t t = p - (kNear + 1);
+      const int64_t t = p - a.off;
       const int64_t oi = to_input(a, t) - a.o0;
       const bool tin = t >= 0 && oi >= 0 && oi < a.n_out && in;
       cp_async4(sdt + i, a.dtarget + (tin ? oi : 0), tin);
@@ -278,14 +292,14 @@ __global__ void __launch_bounds__(32 * kMaxChunks) es_walk(PassArgs a, ChunkPlan
   }
   if (!MAIN) return;
   __syncthreads();
-  // one thread per node: partials -> near-window target (t = p - P - 1) and far-end target
+  // one thread per node: partials -> fixed-offset target (t = p - off) and far-end target
   for (int i = tid; i < kNodes; i += nthr) {
     const int si = (i / kL) * kLP + (i % kL);
     const int64_t p = P0 + i;
     if (p >= a.n_in || seg0 + i / kL >= a.nseg) continue;
-    const int64_t t = p - (kNear + 1);
+    const int64_t t = p - a.off;
     const int64_t oi = to_input(a, t) - a.o0;
-    if (t >= 0 && oi >= 0 && oi < a.n_out && sdt[i] > kNear)
+    if (t >= 0 && oi >= 0 && oi < a.n_out && sdt[i] > a.dth)
 #pragma unroll
       for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + oi, sac[c * kNodesP + si]);
     const int ti = sti[si];
@@ -304,6 +318,184 @@ size_t es_walk_smem(const ChunkPlan& cp, int nf, bool main) {
   return sizeof(double) * d + sizeof(int) * (kNodesP + kNodes);
 }
 
+// FFT-mode tail walk: few terms (<= 16, all with far ends), so one warp owns
+// 32 segments (a lane each) and every term; no shared-memory staging of the
+// fields (each lane streams its own segment from L1) and no cross-warp
+// reduction. Per node a lane forms the fixed-end sum (target p - off) and the
+// variable-end sum (its tinfo target); every kTB nodes the warp transposes the
+// partials through a small shared buffer so that each RED of the warp covers
+// kTB consecutive nodes of 32 / kTB segments. CTA = kTailWarps independent warps.
+constexpr int kTB = 4, kTailWarps = 4;
+
+template <int NF, bool MAIN, int MT>
+__global__ void __launch_bounds__(32 * kTailWarps, 3) es_tail_walk(PassArgs a, const double* __restrict__ tab) {
+  __shared__ double2 slc[MT];                                // (lambda, c lambda^off)
+  __shared__ double sbuf[kTailWarps][kTB][4][33];            // [warp][node][value][lane]
+  __shared__ double sfld[kTailWarps][2][kTB][NF][33];        // staged fields: [warp][buf][node][field][lane]
+  __shared__ int stin[kTailWarps][2][kTB][33];               // staged tinfo
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  for (int m = tid; m < MT; m += 32 * kTailWarps) slc[m] = make_double2(__ldg(tab + m), __ldg(tab + kMT + m));
+  __syncthreads();
+  const int64_t seg0 = (static_cast<int64_t>(blockIdx.x) * kTailWarps + w) * 32;
+  const int64_t seg = seg0 + lane;
+  const bool live = seg < a.nseg;
+  const int64_t pseg = a.q0 + seg * kL;
+  const int V = a.M * NF;
+  double g[MT][NF];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int c = 0; c < NF; ++c) g[m][c] = MAIN && live && m < a.M ? a.carry[seg * V + m * NF + c] : 0.0;
+  // stage nodes qb..qb+kTB-1 of the warp's 32 segments: lane j of a round
+  // takes segment (round*32 + j) / kTB, node (round*32 + j) % kTB, so each
+  // warp instruction reads kTB consecutive nodes of 32/kTB segments
+  auto stage = [&](int qb, int buf) {
+#pragma unroll
+    for (int rr = 0; rr < kTB; ++rr) {
+      const int j = rr * 32 + lane;
+      const int sl = j / kTB, r = j % kTB;
+      const int64_t p = a.q0 + (seg0 + sl) * kL + qb + r;
+      const bool in = seg0 + sl < a.nseg && p < a.n_in;
+      const int64_t x = in ? to_input(a, p) : 0;
+      cp_async8(&sfld[w][buf][r][0][sl], a.u + x, in);
+      if (NF == 2) cp_async8(&sfld[w][buf][r][NF - 1][sl], a.kappa + x, in);
+      if (MAIN) cp_async4(&stin[w][buf][r][sl], a.tinfo + (in ? p : 0), in);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  auto get_f = [&](int buf, int r, double* f) {
+    f[0] = sfld[w][buf][r][0][lane];
+    if (NF == 2) f[1] = sfld[w][buf][r][1][lane] * f[0];
+  };
+  stage(kL - kTB, 0);
+  if (!MAIN) {
+    int buf = 0;
+    for (int qb = kL - kTB; qb >= 0; qb -= kTB, buf ^= 1) {
+      if (qb - kTB >= 0) {
+        stage(qb - kTB, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = kTB - 1; r >= 0; --r) {
+        double f[NF];
+        get_f(buf, r, f);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          const double lam = ld_shared2_any(slc + m).x;
+#pragma unroll
+          for (int c = 0; c < NF; ++c) g[m][c] = fma(lam, g[m][c], f[c]);
+        }
+      }
+      __syncwarp();
+    }
+    if (live)
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+        if (m < a.M)
+#pragma unroll
+          for (int c = 0; c < NF; ++c) a.agg[seg * V + m * NF + c] = g[m][c];
+    return;
+  }
+  double coef[MT];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) coef[m] = 0.0;
+  int ecur = -1;
+  int buf = 0;
+  for (int qb = kL - kTB; qb >= 0; qb -= kTB, buf ^= 1) {
+    if (qb - kTB >= 0) {
+      stage(qb - kTB, buf ^ 1);                                // next block in flight
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int r = kTB - 1; r >= 0; --r) {
+      const int64_t p = pseg + qb + r;
+      double f[NF];
+      get_f(buf, r, f);
+      double ac[NF][2];
+#pragma unroll
+      for (int c = 0; c < NF; ++c) ac[c][0] = ac[c][1] = 0.0;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const double2 k = ld_shared2_any(slc + m);
+#pragma unroll
+        for (int c = 0; c < NF; ++c) {
+          g[m][c] = fma(k.x, g[m][c], f[c]);
+          ac[c][m & 1] = fma(k.y, g[m][c], ac[c][m & 1]);
+        }
+      }
+      const int ti = live ? stin[w][buf][r][lane] : -1;
+      const int nt = ti < 0 ? 0 : (ti & 3);
+      double y[NF];
+#pragma unroll
+      for (int c = 0; c < NF; ++c) y[c] = 0.0;
+      if (nt) {
+        const int e = static_cast<int>(p - (ti >> 2));       // = D_t + 1
+        if (e != ecur) {
+          if (e == ecur + 1) {
+#pragma unroll
+            for (int m = 0; m < MT; ++m) coef[m] *= ld_shared2_any(slc + m).x;
+          } else if (e == ecur - 1) {
+#pragma unroll
+            for (int m = 0; m < MT; ++m) coef[m] *= __ldg(tab + 3 * kMT + m);
+          } else {
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+              const double cw = __ldg(tab + 2 * kMT + m);
+              coef[m] = cw == 0.0 ? 0.0 : cw * exp(-__ldg(tab + 4 * kMT + m) * static_cast<double>(e));
+            }
+          }
+          ecur = e;
+        }
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int c = 0; c < NF; ++c) y[c] = fma(coef[m], g[m][c], y[c]);
+        if (nt == 2) {                        // a second target ending here (rare): its own RED
+          const int64_t ob = to_input(a, (ti >> 2) + 1) - a.o0;
+#pragma unroll
+          for (int c = 0; c < NF; ++c) {
+            double z = 0.0;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) z = fma(coef[m] * __ldg(tab + 3 * kMT + m), g[m][c], z);
+            atomicAdd(a.facc + c * a.n_out + ob, -z);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NF; ++c) {
+        sbuf[w][r][c][lane] = ac[c][0] + ac[c][1];
+        sbuf[w][r][2 + c][lane] = y[c];
+      }
+    }
+    __syncwarp();
+    // transposed write-out: kTB consecutive nodes of a segment per lane group
+#pragma unroll
+    for (int rr = 0; rr < kTB; ++rr) {
+      const int j = rr * 32 + lane;
+      const int sl = j / kTB, r = j % kTB;
+      const int64_t sg = seg0 + sl;
+      const int64_t p = a.q0 + sg * kL + qb + r;
+      if (sg >= a.nseg || p >= a.n_in) continue;
+      const int64_t t = p - a.off;
+      const int64_t oi = to_input(a, t) - a.o0;
+      if (t >= 0 && oi >= 0 && oi < a.n_out)
+#pragma unroll
+        for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + oi, sbuf[w][r][c][sl]);
+      const int ti = stin[w][buf][r][sl];
+      if (ti >= 0 && (ti & 3))
+#pragma unroll
+        for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + (to_input(a, ti >> 2) - a.o0), -sbuf[w][r][2 + c][sl]);
+    }
+    __syncwarp();
+  }
+}
+
 // Segment carries by a three-level scan (all fully parallel except a short
 // per-term block scan over chunks of kChunk segments):
 //   es_chunk  : per (term j, chunk), the chunk aggregate from its segment aggregates
@@ -315,7 +507,7 @@ constexpr int kCarryThreads = 512, kCarryPer = 8;
 
 __global__ void es_chunk(PassArgs a, int64_t nchunk, double* cagg) {
   const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int V = kMT * a.nf;
+  const int V = a.M * a.nf;
   const int j = static_cast<int>(id % V);
   const int64_t k = id / V;
   if (k >= nchunk || j / a.nf >= a.M) return;
@@ -386,7 +578,7 @@ __global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int64_t nc
 
 __global__ void es_expand(PassArgs a, int64_t nchunk, const double* gchunk) {
   const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int V = kMT * a.nf;
+  const int V = a.M * a.nf;
   const int j = static_cast<int>(id % V);
   const int64_t k = id / V;
   if (k >= nchunk || j / a.nf >= a.M) return;
@@ -509,6 +701,7 @@ T* upload(const std::vector<T>& v) {
   T* d = nullptr;
   NLG_CUDA(cudaMalloc(&d, sizeof(T) * std::max<size_t>(v.size(), 1)));
   if (!v.empty()) NLG_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
   return d;
 }
 
@@ -529,13 +722,13 @@ int64_t extent(int64_t g, int dir, double delta, double h, int64_t cap) {
 
 // positions -> targets map for one direction; false if a node would end more
 // than two horizons or the map is not monotone (the scan path then declines).
-bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirror, std::vector<int>& tinfo) {
+bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirror, int dth, std::vector<int>& tinfo) {
   tinfo.assign(static_cast<size_t>(n_in), -1);
   const int64_t n_out = static_cast<int64_t>(D.size());
   int64_t last_p = -1;
   for (int64_t k = 0; k < n_out; ++k) {
     const int64_t oi = mirror ? (n_out - 1 - k) : k;
-    if (D[oi] <= kNear) continue;
+    if (D[oi] <= dth) continue;
     const int64_t tin = o0 + oi;
     const int64_t t = mirror ? (n_in - 1 - tin) : tin;
     const int64_t p = t + D[oi] + 1;
@@ -555,16 +748,100 @@ bool build_tinfo(const std::vector<int>& D, int64_t n_in, int64_t o0, bool mirro
   return true;
 }
 
+// ---- FFT mode: fixed-window far field by convolution -------------------------
+
+__global__ void fft_pack(const double* __restrict__ u, const double* __restrict__ kappa, int64_t n_in, int64_t L,
+                         cufftDoubleComplex* __restrict__ z) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= L) return;
+  double a = 0.0, b = 0.0;
+  if (i < n_in) {
+    a = u[i];
+    if (kappa) b = kappa[i] * a;
+  }
+  z[i] = make_cuDoubleComplex(a, b);
+}
+
+__global__ void fft_scale(cufftDoubleComplex* __restrict__ z, const double* __restrict__ kr, int64_t L) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= L) return;
+  const double k = kr[i];
+  z[i] = make_cuDoubleComplex(z[i].x * k, z[i].y * k);
+}
+
+__global__ void fft_real_part(const cufftDoubleComplex* __restrict__ z, double* __restrict__ kr, int64_t L) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < L) kr[i] = z[i].x;
+}
+
+struct FftCombineArgs {
+  const double* u;
+  const double* kappa;
+  const cufftDoubleComplex* z;
+  double inv_l;
+  int64_t n_out, o0;
+  const double* scale;
+  const double* diag;
+  const double* facc;   // [fields][n_out] tails (fixed end - variable end)
+  const double* ext;
+  double* out;
+  int mode;
+};
+
+// X = kappa_i F[u] + F[kappa u] with F = conv/L + tails; out = s (X - u_i diag)
+template <bool KW>
+__global__ void es_fft_combine(FftCombineArgs a) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= a.n_out) return;
+  const int64_t x = a.o0 + i;
+  const cufftDoubleComplex c = a.z[x];
+  const double fu = fma(c.x, a.inv_l, a.facc[i]);
+  const double X = KW ? fma(a.kappa[x], fu, fma(c.y, a.inv_l, a.facc[a.n_out + i])) : fu;
+  if (a.mode == 1) a.out[i] = a.ext ? X + a.ext[i] : X;
+  else a.out[i] = a.scale[i] * (X - a.u[x] * a.diag[i]);
+}
+
+// FFT length >= m: 2^a 3^b with 3^b <= 9 (cuFFT runs these in the fewest
+// passes; measured on B200: 2^19*9 and 2^22 beat 7-smooth sizes near 4.3M by ~25%)
+int64_t smooth_size(int64_t m) {
+  int64_t best = 0;
+  for (int64_t t : {1, 3, 9}) {
+    int64_t L = t;
+    while (L < m) L *= 2;
+    if (best == 0 || L < best) best = L;
+  }
+  return best;
+}
+
+#define NLG_CUFFT(call)                                                                  \
+  do {                                                                                   \
+    const cufftResult r_ = (call);                                                       \
+    if (r_ != CUFFT_SUCCESS) throw ::nlg::Error{NLG_ECUDA, std::string(#call) + " failed: cufft " + std::to_string(r_)}; \
+  } while (0)
+
 }  // namespace
 
 // Device-side state of the exponential-sum plan (declared in plan.hpp).
 struct ExpSumState {
   int M = 0, Mslow = 0, fields = 1;
+  // FFT mode: the fixed-window part of the far field (all offsets 1..Dmax) by
+  // one complex FFT convolution of (u, kappa u); the per-target tails
+  // sum_{D_i < d <= Dmax} by a short exponential sum fitted on [Dmin+1, Dmax]
+  bool fft = false;
+  int64_t L = 0, off = 0, q_off = 0;   // FFT length; fixed-offset distance; first scan position offset
+  int dth = 0;
+  cufftHandle fplan = 0;
+  cudaStream_t fstream = nullptr;      // the FFT chain overlaps the tail scans
+  cudaEvent_t fork = nullptr, join = nullptr;
+  cufftDoubleComplex* z = nullptr;     // [L] (u, kappa u) -> transform -> convolution
+  double* kr = nullptr;                // [L] real transform of the symmetric far kernel
   // term chunks: first global term, real terms, slow flag; constants per chunk
   int nchunks = 0, cmb[kMaxChunks] = {}, ccnt[kMaxChunks] = {};
   bool cslow[kMaxChunks] = {};
   ChunkPlan cp{};
+  ChunkPlan cp_agg{};                  // aggregate walk: chunks of <= 8 terms (independent warps)
   double* ctab = nullptr;          // [kMaxChunks][kTabRows][kMT]
+  double* ctab_agg = nullptr;      // the aggregate walk's chunk tables
   double* rate = nullptr;          // [kMT] t_m
   double* segpow = nullptr;        // [kMT] lambda_m^kL
   int *dplus = nullptr, *dminus = nullptr, *tinfoR = nullptr, *tinfoL = nullptr;
@@ -594,21 +871,34 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   }
   // the scan path pays off only for wide horizons
   if (dmax < 4 * kNear) return;
-  ExpSum es = fit_exponential_sum(d.alpha, kNear, dmax, 1e-11);
-  if (es.terms == 0 || es.rel_err > 1e-11) return;
-  std::vector<int> tR, tL;
-  if (!build_tinfo(dplus, n_in, o0, false, tR) || !build_tinfo(dminus, n_in, o0, true, tL)) return;
-  const int M = es.terms;
   int64_t dmin = dmax;
   for (int64_t i = 0; i < n_out; ++i) dmin = std::min<int64_t>(dmin, std::min(dplus[i], dminus[i]));
+  // FFT mode when the horizons span a narrow range (a short tail fit exists);
+  // otherwise near window P + exponential sum over the whole far range
+  ExpSum es = dmin >= 1 ? fit_exponential_sum_narrow(d.alpha, dmin + 1, dmax, 5e-10, kChunkCap) : ExpSum{};
+  const bool fft = dmin >= 1 && es.terms > 0 && es.rel_err <= 5e-10;
+  if (!fft) {
+    es = fit_exponential_sum(d.alpha, kNear, dmax, 1e-11);
+    if (es.terms == 0 || es.rel_err > 1e-11) return;
+  }
+  const int dth = fft ? -1 : kNear;
+  std::vector<int> tR, tL;
+  if (!build_tinfo(dplus, n_in, o0, false, dth, tR) || !build_tinfo(dminus, n_in, o0, true, dth, tL)) return;
+  const int M = es.terms;
   int Ms = 0;   // rates ascend: slow terms (far end not negligible) come first
   for (int m = 0; m < M; ++m)
-    if (es.rate[m] * static_cast<double>(std::max<int64_t>(dmin, kNear + 1) + 1) <= 40.0) Ms = m + 1;
-  if (M > kMT || (Ms + kChunkCap - 1) / kChunkCap + (M - Ms + kChunkCap - 1) / kChunkCap > kMaxChunks) return;
+    if (fft || es.rate[m] * static_cast<double>(std::max<int64_t>(dmin, kNear + 1) + 1) <= 40.0) Ms = m + 1;
+  const int cap = fft ? kChunkCap : 12;
+  if (M > kMT || (Ms + cap - 1) / cap + (M - Ms + cap - 1) / cap > kMaxChunks) return;
+  const int64_t off = fft ? dmax + 1 : kNear + 1;
 
   auto* S = new ExpSumState();
   P.es_state = S;
   P.es = es;
+  S->fft = fft;
+  S->off = off;
+  S->dth = dth;
+  S->q_off = fft ? dmin + 1 : kNear + 1;
   S->M = M;
   S->Mslow = Ms;
   S->fields = d.kappa ? 2 : 1;
@@ -625,8 +915,8 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
       ++S->nchunks;
     }
   };
-  add_chunks(0, Ms, kChunkCap, true);
-  add_chunks(Ms, M - Ms, kChunkCap, false);
+  add_chunks(0, Ms, cap, true);
+  add_chunks(Ms, M - Ms, cap, false);
   std::vector<double> ctab(static_cast<size_t>(kMaxChunks) * kTabRows * kMT, 0.0);
   for (int c = 0; c < S->nchunks; ++c) {
     double* T = ctab.data() + static_cast<size_t>(c) * kTabRows * kMT;
@@ -634,7 +924,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
       const int m = S->cmb[c] + k;
       const double t = es.rate[m];
       T[0 * kMT + k] = std::exp(-t);
-      T[1 * kMT + k] = es.weight[m] * std::exp(-t * (kNear + 1));
+      T[1 * kMT + k] = es.weight[m] * std::exp(-t * static_cast<double>(off));
       T[2 * kMT + k] = S->cslow[c] ? es.weight[m] : 0.0;
       T[3 * kMT + k] = std::exp(t);
       T[4 * kMT + k] = t;
@@ -644,6 +934,24 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   for (const void* f : {reinterpret_cast<const void*>(es_walk<1, false>), reinterpret_cast<const void*>(es_walk<2, false>),
                         reinterpret_cast<const void*>(es_walk<1, true>), reinterpret_cast<const void*>(es_walk<2, true>)})
     NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  // aggregate walk plan: chunks of <= 8 terms (lambda only), one warp each
+  {
+    ChunkPlan& ca = S->cp_agg;
+    const int parts = std::min(kMaxChunks, (M + 7) / 8);
+    std::vector<double> ta(static_cast<size_t>(kMaxChunks) * kTabRows * kMT, 0.0);
+    ca.n = parts;
+    ca.any_slow = 0;
+    for (int c = 0; c < parts; ++c) {
+      const int b = c * M / parts, e = (c + 1) * M / parts;
+      ca.mb[c] = b;
+      ca.cnt[c] = e - b;
+      ca.mt[c] = (e - b + 3) / 4 * 4;
+      ca.slow[c] = 0;
+      for (int k = 0; k < e - b; ++k) ta[static_cast<size_t>(c) * kTabRows * kMT + k] = std::exp(-es.rate[b + k]);
+    }
+    S->ctab_agg = upload(ta);
+    ca.tab = S->ctab_agg;
+  }
   S->cp.n = S->nchunks;
   S->cp.tab = S->ctab;
   S->cp.any_slow = Ms > 0;
@@ -677,13 +985,38 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
     sc[i] = (d.kappa ? 0.5 : 1.0) * hs * c;
   }
   S->scale = upload(sc);
+  if (fft) {
+    // circular convolution of length L >= n_in + Dmax: outputs in the slab see
+    // no wrap-around (u is zero-padded); kernel w_d at +-d, 1 <= d <= Dmax
+    S->L = smooth_size(std::max<int64_t>(n_in + dmax + 1, 2 * dmax + 2));
+    const int64_t L = S->L;
+    NLG_CUFFT(cufftPlan1d(&S->fplan, static_cast<int>(L), CUFFT_Z2Z, 1));
+    NLG_CUDA(cudaStreamCreateWithFlags(&S->fstream, cudaStreamNonBlocking));
+    NLG_CUDA(cudaEventCreateWithFlags(&S->fork, cudaEventDisableTiming));
+    NLG_CUDA(cudaEventCreateWithFlags(&S->join, cudaEventDisableTiming));
+    NLG_CUDA(cudaMalloc(&S->z, sizeof(cufftDoubleComplex) * L));
+    NLG_CUDA(cudaMalloc(&S->kr, sizeof(double) * L));
+    std::vector<cufftDoubleComplex> kh(static_cast<size_t>(L), make_cuDoubleComplex(0.0, 0.0));
+    for (int64_t k = 1; k <= dmax; ++k) {
+      const double w = std::pow(static_cast<double>(k), -d.alpha);
+      kh[k].x = w;
+      kh[L - k].x = w;
+    }
+    NLG_CUDA(cudaMemcpy(S->z, kh.data(), sizeof(cufftDoubleComplex) * L, cudaMemcpyHostToDevice));
+    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
+    NLG_CUFFT(cufftSetStream(S->fplan, P.stream));
+    NLG_CUFFT(cufftExecZ2Z(S->fplan, S->z, S->z, CUFFT_FORWARD));
+    fft_real_part<<<static_cast<unsigned>((L + 255) / 256), 256, 0, P.stream>>>(S->z, S->kr, L);   // symmetric: real
+    NLG_CUDA(cudaGetLastError());
+    NLG_CUDA(cudaStreamSynchronize(P.stream));
+  }
   S->kappa_dev = P.d_kappa;
   // scan geometry per direction (positions space); the last segments may own
   // no near-window target but still end far windows and feed the carries
   S->o0R = o0;
   S->o0L = n_in - o0 - n_out;
   auto nseg_of = [&](int64_t oo) {
-    const int64_t q0 = oo + kNear + 1;
+    const int64_t q0 = oo + S->q_off;
     return std::max<int64_t>((std::max<int64_t>(n_in - q0, 0) + kL - 1) / kL, 1);
   };
   S->nsegR = nseg_of(S->o0R);
@@ -722,6 +1055,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   {
     std::vector<double> o(static_cast<size_t>(n_in), 1.0);
     NLG_CUDA(cudaMemcpy(ones, o.data(), sizeof(double) * n_in, cudaMemcpyHostToDevice));
+    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
   }
   P.fast_method = 2;
   expsum_run(P, ones, S->diag, P.stream, 1, ext_dev);
@@ -738,19 +1072,59 @@ void expsum_setup(Plan& P, const nlg_desc& d) {
 void expsum_free(Plan& P) {
   ExpSumState* S = P.es_state;
   if (!S) return;
-  for (double* p : {S->ctab, S->rate, S->segpow, S->wnear, S->scale, S->diag, S->agg, S->carry, S->facc, S->cagg,
+  for (double* p : {S->ctab, S->ctab_agg, S->rate, S->segpow, S->wnear, S->scale, S->diag, S->agg, S->carry, S->facc, S->cagg,
                     S->gchunk})
     cudaFree(p);
   for (int* p : {S->dplus, S->dminus, S->tinfoR, S->tinfoL}) cudaFree(p);
+  if (S->fplan) cufftDestroy(S->fplan);
+  if (S->fstream) cudaStreamDestroy(S->fstream);
+  if (S->fork) cudaEventDestroy(S->fork);
+  if (S->join) cudaEventDestroy(S->join);
+  cudaFree(S->z);
+  cudaFree(S->kr);
   delete S;
   P.es_state = nullptr;
 }
+
+namespace {
+template <int NF, bool MAIN>
+void launch_tail_t(int M, const PassArgs& a, const double* tab, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>((a.nseg + 32 * kTailWarps - 1) / (32 * kTailWarps));
+  if (M <= 8) es_tail_walk<NF, MAIN, 8><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
+  else if (M <= 12) es_tail_walk<NF, MAIN, 12><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
+  else es_tail_walk<NF, MAIN, 16><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
+}
+void launch_tail(int nf, bool main, int M, const PassArgs& a, const double* tab, cudaStream_t s) {
+  if (nf == 2) {
+    if (main) launch_tail_t<2, true>(M, a, tab, s);
+    else launch_tail_t<2, false>(M, a, tab, s);
+  } else {
+    if (main) launch_tail_t<1, true>(M, a, tab, s);
+    else launch_tail_t<1, false>(M, a, tab, s);
+  }
+}
+}  // namespace
 
 void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode, const double* ext) {
   ExpSumState* S = P.es_state;
   const int64_t n_out = P.n_out;
   const int NF = S->fields;
   NLG_CUDA(cudaMemsetAsync(S->facc, 0, sizeof(double) * NF * n_out, s));
+  if (S->fft) {   // fixed-window far field z = FFT^-1( K^ . FFT(u + i kappa u) ), on a side stream
+    NLG_CUDA(cudaEventRecord(S->fork, s));
+    NLG_CUDA(cudaStreamWaitEvent(S->fstream, S->fork, 0));
+    cudaStream_t fs = S->fstream;
+    cudaEvent_t ev;
+    stage_begin(P, fs, kStEsFft, &ev);
+    const unsigned gl = static_cast<unsigned>((S->L + 255) / 256);
+    fft_pack<<<gl, 256, 0, fs>>>(u, NF == 2 ? S->kappa_dev : nullptr, P.n_in, S->L, S->z);
+    NLG_CUFFT(cufftSetStream(S->fplan, fs));
+    NLG_CUFFT(cufftExecZ2Z(S->fplan, S->z, S->z, CUFFT_FORWARD));
+    fft_scale<<<gl, 256, 0, fs>>>(S->z, S->kr, S->L);
+    NLG_CUFFT(cufftExecZ2Z(S->fplan, S->z, S->z, CUFFT_INVERSE));
+    stage_end(P, fs, kStEsFft, ev, 4);
+    NLG_CUDA(cudaEventRecord(S->join, fs));
+  }
   for (int mirror = 0; mirror < 2; ++mirror) {
     PassArgs a;
     a.u = u;
@@ -759,7 +1133,9 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     a.n_in = P.n_in;
     a.n_out = n_out;
     a.o0 = P.halo_lo;
-    a.q0 = (mirror ? S->o0L : S->o0R) + kNear + 1;
+    a.q0 = (mirror ? S->o0L : S->o0R) + S->q_off;
+    a.off = S->off;
+    a.dth = S->dth;
     a.nseg = mirror ? S->nsegL : S->nsegR;
     a.M = S->M;
     a.nf = NF;
@@ -774,13 +1150,14 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     const unsigned thr = 32 * S->cp.n;
     cudaEvent_t ev;
     stage_begin(P, s, kStEsAggregate, &ev);
-    if (NF == 2) es_walk<2, false><<<gridw, thr, es_walk_smem(S->cp, 2, false), s>>>(a, S->cp);
-    else es_walk<1, false><<<gridw, thr, es_walk_smem(S->cp, 1, false), s>>>(a, S->cp);
+    const unsigned thra = 32 * S->cp_agg.n;
+    if (NF == 2) es_walk<2, false><<<gridw, thra, es_walk_smem(S->cp_agg, 2, false), s>>>(a, S->cp_agg);
+    else es_walk<1, false><<<gridw, thra, es_walk_smem(S->cp_agg, 1, false), s>>>(a, S->cp_agg);
     stage_end(P, s, kStEsAggregate, ev, 1);
     stage_begin(P, s, kStEsCarry, &ev);
     {
       const int64_t nchunk = (a.nseg + kChunk - 1) / kChunk;
-      const int64_t work = nchunk * kMT * NF;
+      const int64_t work = nchunk * S->M * NF;
       const unsigned gw = static_cast<unsigned>((work + 255) / 256);
       es_chunk<<<gw, 256, 0, s>>>(a, nchunk, S->cagg);
       es_carry<<<S->M * NF, kCarryThreads, 0, s>>>(a, nchunk, S->cagg, S->gchunk);
@@ -788,9 +1165,33 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     }
     stage_end(P, s, kStEsCarry, ev, 3);
     stage_begin(P, s, kStEsMain, &ev);
-    if (NF == 2) es_walk<2, true><<<gridw, thr, es_walk_smem(S->cp, 2, true), s>>>(a, S->cp);
+    if (S->fft) launch_tail(NF, true, S->M, a, S->ctab, s);
+    else if (NF == 2) es_walk<2, true><<<gridw, thr, es_walk_smem(S->cp, 2, true), s>>>(a, S->cp);
     else es_walk<1, true><<<gridw, thr, es_walk_smem(S->cp, 1, true), s>>>(a, S->cp);
     stage_end(P, s, kStEsMain, ev, 1);
+  }
+  if (S->fft) {
+    NLG_CUDA(cudaStreamWaitEvent(s, S->join, 0));
+    FftCombineArgs f;
+    f.u = u;
+    f.kappa = S->kappa_dev;
+    f.z = S->z;
+    f.inv_l = 1.0 / static_cast<double>(S->L);
+    f.n_out = n_out;
+    f.o0 = P.halo_lo;
+    f.scale = S->scale;
+    f.diag = S->diag;
+    f.facc = S->facc;
+    f.ext = ext;
+    f.out = out;
+    f.mode = mode;
+    cudaEvent_t ev;
+    stage_begin(P, s, kStEsCombine, &ev);
+    const unsigned g = static_cast<unsigned>((n_out + 255) / 256);
+    if (NF == 2) es_fft_combine<true><<<g, 256, 0, s>>>(f);
+    else es_fft_combine<false><<<g, 256, 0, s>>>(f);
+    stage_end(P, s, kStEsCombine, ev, 1);
+    return;
   }
   CombineArgs c;
   c.u = u;

@@ -206,14 +206,17 @@ nlg_status nlg_plan_create(const nlg_desc* desc, nlg_plan** out) {
     if (d.delta) {
       NLG_CUDA(cudaMalloc(&P.d_delta, bytes_in));
       NLG_CUDA(cudaMemcpy(P.d_delta, d.delta, bytes_in, cudaMemcpyHostToDevice));
+    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
     }
     if (d.coeff) {
       NLG_CUDA(cudaMalloc(&P.d_coeff, bytes_in));
       NLG_CUDA(cudaMemcpy(P.d_coeff, d.coeff, bytes_in, cudaMemcpyHostToDevice));
+    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
     }
     if (d.kappa) {
       NLG_CUDA(cudaMalloc(&P.d_kappa, bytes_in));
       NLG_CUDA(cudaMemcpy(P.d_kappa, d.kappa, bytes_in, cudaMemcpyHostToDevice));
+    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
     }
     NLG_CUDA(cudaMalloc(&P.d_pairs, sizeof(unsigned long long)));
 
@@ -716,5 +719,21 @@ nlg_status nlg_tree_moments(int dim, int64_t n, int K, const double* u, double* 
     require(K >= 0 && (dim == 1 || K == 0), "moments support K >= 0 in 1d, K = 0 in 2d/3d");
     const int64_t a = tree_moments(dim, n, K, u, out);
     if (adds) *adds = a;
+  });
+}
+
+nlg_status nlg_expsum_fit_narrow(double alpha, int64_t lo, int64_t hi, double tol, int max_terms, double* rate,
+                                 double* weight, int* terms, double* rel_err) {
+  using namespace nlg;
+  return guard([&] {
+    require(rate && weight && terms && rel_err, "null argument");
+    require(lo >= 1 && hi >= lo && max_terms >= 2, "invalid window");
+    const ExpSum es = fit_exponential_sum_narrow(alpha, lo, hi, tol, max_terms);
+    *terms = es.terms;
+    *rel_err = es.rel_err;
+    for (int k = 0; k < es.terms; ++k) {
+      rate[k] = es.rate[k];
+      weight[k] = es.weight[k];
+    }
   });
 }

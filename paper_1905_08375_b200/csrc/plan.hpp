@@ -40,7 +40,7 @@ struct StencilState;
 
 // Optional per-stage CUDA-event timing (nlg_set_profiling / nlg_stage_times).
 enum Stage { kStDirect = 0, kStSpanScan, kStSpanEval, kStEsAggregate, kStEsCarry, kStEsMain,
-             kStEsCombine, kStStencil, kNumStages };
+             kStEsCombine, kStStencil, kStEsFft, kNumStages };
 struct StageProf {
   bool on = false;
   struct Rec { int stage; cudaEvent_t a, b; };
@@ -133,5 +133,6 @@ std::vector<double> match_polynomial(int K, double c);
 void match_polynomial_exact(int K, int64_t* num, int64_t* den);
 void split_kernel(int K, double c, std::vector<double>& poly, std::vector<double>& tail);
 ExpSum fit_exponential_sum(double alpha, int near, int64_t dmax, double tol);
+ExpSum fit_exponential_sum_narrow(double alpha, int64_t lo, int64_t hi, double tol, int max_terms);
 
 }  // namespace nlg

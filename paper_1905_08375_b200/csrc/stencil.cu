@@ -848,6 +848,7 @@ T* upload_vec(const std::vector<T>& v) {
   T* d = nullptr;
   NLG_CUDA(cudaMalloc(&d, sizeof(T) * std::max<size_t>(v.size(), 1)));
   if (!v.empty()) NLG_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
   return d;
 }
 

