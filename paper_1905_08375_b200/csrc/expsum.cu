@@ -70,6 +70,10 @@ struct PassArgs {
   double* agg;           // [nseg][M * nf]  (value fastest: the carry scans read it coalesced)
   double* carry;         // [nseg][M * nf]  G at the end of each segment
   double* facc;          // [nf][n_out] far field of F (near-window part +=, far ends -=)
+  // warp-fused carries (tail walks): a warp's 32 segments are one chunk
+  double* cagg;          // [M * nf][nchunk] chunk aggregates
+  const double* gchunk;  // [M * nf][nchunk] G at the end of each chunk
+  int64_t nchunk;
 };
 
 __device__ __forceinline__ int64_t to_input(const PassArgs& a, int64_t p) {
@@ -345,7 +349,35 @@ __global__ void __launch_bounds__(32 * kTailWarps, 3) es_tail_walk(PassArgs a, c
 #pragma unroll
   for (int m = 0; m < MT; ++m)
 #pragma unroll
-    for (int c = 0; c < NF; ++c) g[m][c] = MAIN && live && m < a.M ? a.carry[seg * V + m * NF + c] : 0.0;
+    for (int c = 0; c < NF; ++c) g[m][c] = 0.0;
+  if (MAIN) {
+    // carry of segment seg0 + l: exclusive suffix scan of the chunk's segment
+    // aggregates (multiplier L = lambda^kL) plus L^{31-l} G(chunk end)
+    const int64_t k = seg0 / 32;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      if (m >= a.M) break;
+      const double L = __ldg(a.segpow + m);
+      double Le = 1.0, b = L;                     // L^{31 - lane}
+#pragma unroll
+      for (int bit = 0; bit < 5; ++bit) {
+        if (((31 - lane) >> bit) & 1) Le *= b;
+        b *= b;
+      }
+#pragma unroll
+      for (int c = 0; c < NF; ++c) {
+        double x = live ? a.agg[seg * V + m * NF + c] : 0.0, Lk = L;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const double y = __shfl_down_sync(0xffffffffu, x, d);
+          if (lane + d < 32) x = fma(Lk, y, x);
+          Lk *= Lk;
+        }
+        const double ex = __shfl_down_sync(0xffffffffu, x, 1);
+        g[m][c] = fma(Le, __ldg(a.gchunk + static_cast<int64_t>(m * NF + c) * a.nchunk + k), lane < 31 ? ex : 0.0);
+      }
+    }
+  }
   // stage nodes qb..qb+kTB-1 of the warp's 32 segments: lane j of a round
   // takes segment (round*32 + j) / kTB, node (round*32 + j) % kTB, so each
   // warp instruction reads kTB consecutive nodes of 32/kTB segments
@@ -397,6 +429,24 @@ __global__ void __launch_bounds__(32 * kTailWarps, 3) es_tail_walk(PassArgs a, c
         if (m < a.M)
 #pragma unroll
           for (int c = 0; c < NF; ++c) a.agg[seg * V + m * NF + c] = g[m][c];
+    // chunk aggregate sum_l L^l agg[seg0 + l] by a shuffle tree into lane 0
+    // (lanes past the last segment hold 0)
+    const int64_t k = seg0 / 32;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      if (m >= a.M) break;
+      const double L = __ldg(a.segpow + m);
+#pragma unroll
+      for (int c = 0; c < NF; ++c) {
+        double v = g[m][c], Lk = L;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          v = fma(Lk, __shfl_down_sync(0xffffffffu, v, d), v);
+          Lk *= Lk;
+        }
+        if (lane == 0) a.cagg[static_cast<int64_t>(m * NF + c) * a.nchunk + k] = v;
+      }
+    }
     return;
   }
   double coef[MT];
@@ -502,7 +552,8 @@ __global__ void __launch_bounds__(32 * kTailWarps, 3) es_tail_walk(PassArgs a, c
 //   es_carry  : per j, block scan of chunk aggregates -> G at every chunk end
 //   es_expand : per (j, chunk), walk its segments down from the chunk-end G
 // with G(start s) = agg[s] + L G(start s+1), L = lambda^{kL}.
-constexpr int kChunk = 32;                       // segments per chunk
+constexpr int kChunk = 32;                       // segments per chunk (= one tail-walk warp)
+static_assert(kChunk == 32, "tail walks fuse one chunk per warp");
 constexpr int kCarryThreads = 512, kCarryPer = 8;
 
 __global__ void es_chunk(PassArgs a, int64_t nchunk, double* cagg) {
@@ -1091,7 +1142,9 @@ template <int NF, bool MAIN>
 void launch_tail_t(int M, const PassArgs& a, const double* tab, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>((a.nseg + 32 * kTailWarps - 1) / (32 * kTailWarps));
   if (M <= 8) es_tail_walk<NF, MAIN, 8><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
+  else if (M <= 10) es_tail_walk<NF, MAIN, 10><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
   else if (M <= 12) es_tail_walk<NF, MAIN, 12><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
+  else if (M <= 14) es_tail_walk<NF, MAIN, 14><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
   else es_tail_walk<NF, MAIN, 16><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
 }
 void launch_tail(int nf, bool main, int M, const PassArgs& a, const double* tab, cudaStream_t s) {
@@ -1149,6 +1202,21 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     const unsigned gridw = static_cast<unsigned>((a.nseg + kSegs - 1) / kSegs);
     const unsigned thr = 32 * S->cp.n;
     cudaEvent_t ev;
+    if (S->fft) {   // tail walks: aggregate (+ chunk aggregates), chunk scan, main (+ segment carries)
+      a.nchunk = (a.nseg + kChunk - 1) / kChunk;
+      a.cagg = S->cagg;
+      a.gchunk = S->gchunk;
+      stage_begin(P, s, kStEsAggregate, &ev);
+      launch_tail(NF, false, S->M, a, S->ctab, s);
+      stage_end(P, s, kStEsAggregate, ev, 1);
+      stage_begin(P, s, kStEsCarry, &ev);
+      es_carry<<<S->M * NF, kCarryThreads, 0, s>>>(a, a.nchunk, S->cagg, S->gchunk);
+      stage_end(P, s, kStEsCarry, ev, 1);
+      stage_begin(P, s, kStEsMain, &ev);
+      launch_tail(NF, true, S->M, a, S->ctab, s);
+      stage_end(P, s, kStEsMain, ev, 1);
+      continue;
+    }
     stage_begin(P, s, kStEsAggregate, &ev);
     const unsigned thra = 32 * S->cp_agg.n;
     if (NF == 2) es_walk<2, false><<<gridw, thra, es_walk_smem(S->cp_agg, 2, false), s>>>(a, S->cp_agg);
@@ -1165,8 +1233,7 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     }
     stage_end(P, s, kStEsCarry, ev, 3);
     stage_begin(P, s, kStEsMain, &ev);
-    if (S->fft) launch_tail(NF, true, S->M, a, S->ctab, s);
-    else if (NF == 2) es_walk<2, true><<<gridw, thr, es_walk_smem(S->cp, 2, true), s>>>(a, S->cp);
+    if (NF == 2) es_walk<2, true><<<gridw, thr, es_walk_smem(S->cp, 2, true), s>>>(a, S->cp);
     else es_walk<1, true><<<gridw, thr, es_walk_smem(S->cp, 1, true), s>>>(a, S->cp);
     stage_end(P, s, kStEsMain, ev, 1);
   }
