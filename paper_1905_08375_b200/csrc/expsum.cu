@@ -67,6 +67,7 @@ struct PassArgs {
   const int* dtarget;    // D of each output target in this direction (output order)
   const double* rate;    // t_m (global; coefficient resets)
   const double* segpow;  // lambda_m^kL (global; carries)
+  const double* segpw;   // [kMT][32] (lambda_m^kL)^(31 - lane)   (tail walks)
   double* agg;           // [nseg][M * nf]  (value fastest: the carry scans read it coalesced)
   double* carry;         // [nseg][M * nf]  G at the end of each segment
   double* facc;          // [nf][n_out] far field of F (near-window part +=, far ends -=)
@@ -322,139 +323,99 @@ size_t es_walk_smem(const ChunkPlan& cp, int nf, bool main) {
   return sizeof(double) * d + sizeof(int) * (kNodesP + kNodes);
 }
 
-// FFT-mode tail walk: few terms (<= 16, all with far ends), so one warp owns
-// 32 segments (a lane each) and every term; no shared-memory staging of the
-// fields (each lane streams its own segment from L1) and no cross-warp
-// reduction. Per node a lane forms the fixed-end sum (target p - off) and the
-// variable-end sum (its tinfo target); every kTB nodes the warp transposes the
-// partials through a small shared buffer so that each RED of the warp covers
-// kTB consecutive nodes of 32 / kTB segments. CTA = kTailWarps independent warps.
+// FFT-mode tail walks: few terms (<= 16, all with far ends). A warp owns 32
+// consecutive segments (a lane each, = one carry chunk) and one field (u or
+// kappa u), with every term of that field in registers. Fields are staged per
+// warp through a double-buffered cp.async ring of kTB-node blocks (each load
+// instruction covers kTB consecutive nodes of 32 / kTB segments). CTA =
+// kTailWarps independent warps: with two fields, warp pairs share segments.
+//
+// Aggregate walk (MAIN = false): after the walk lane l holds agg_l (the
+// segment's sum_q lambda^q f), and the warp turns its chunk into
+//   E_l = sum_{s > l} L^{s-l-1} agg_s  (L = lambda^kL), chunk aggregate E_{-1},
+// by one sequential pass per term through shared memory; E goes to global as
+// [chunk][value][lane] (coalesced both ways), the chunk aggregate to cagg.
+// Main walk (MAIN = true): the carry of lane l is E_l + L^{31-l} G(chunk end);
+// per node the lane forms the fixed-end sum (target p - off) and the
+// variable-end sum (its tinfo target); every kTB nodes the warp transposes
+// the partials so each RED instruction covers kTB consecutive nodes.
 constexpr int kTB = 4, kTailWarps = 4;
+#ifndef NLG_TAIL_MAIN_CTAS
+#define NLG_TAIL_MAIN_CTAS 3
+#endif
+constexpr int kTailMainCtas = NLG_TAIL_MAIN_CTAS;
 
 template <int NF, bool MAIN, int MT>
-__global__ void __launch_bounds__(32 * kTailWarps, 3) es_tail_walk(PassArgs a, const double* __restrict__ tab) {
+__global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_tail_walk(PassArgs a, const double* __restrict__ tab) {
+  constexpr int FW = MAIN ? NF : 1;                          // fields per warp
+  constexpr int kG = kTailWarps * FW / NF;                   // chunks per CTA
+  constexpr int kSK = (32 / kTB) * kL;                       // node stride between staging rounds
   __shared__ double2 slc[MT];                                // (lambda, c lambda^off)
-  __shared__ double sbuf[kTailWarps][kTB][4][33];            // [warp][node][value][lane]
-  __shared__ double sfld[kTailWarps][2][kTB][NF][33];        // staged fields: [warp][buf][node][field][lane]
-  __shared__ int stin[kTailWarps][2][kTB][33];               // staged tinfo
+  __shared__ double sbuf[kTailWarps][kTB][2 * FW][33];       // [warp][node][ac.., y..][lane]
+  __shared__ double sfld[kTailWarps][2][kTB][2][33];         // staged u, kappa: [warp][buf][node][u|k][lane]
+  __shared__ int stin[kTailWarps][MAIN ? 2 : 1][kTB][33];    // staged tinfo
+  __shared__ double sagg[MAIN ? 1 : kTailWarps][32][MT + 1]; // aggregate walk: chunk transposition
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   for (int m = tid; m < MT; m += 32 * kTailWarps) slc[m] = make_double2(__ldg(tab + m), __ldg(tab + kMT + m));
-  __syncthreads();
-  const int64_t seg0 = (static_cast<int64_t>(blockIdx.x) * kTailWarps + w) * 32;
+  const int c0 = FW == NF ? 0 : (w & 1);                     // my first field
+  const bool kap = NF == 2 && (FW == 2 || c0 == 1);          // kappa needed
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * kG + (FW == NF ? w : (w >> 1));   // my chunk
+  const int64_t seg0 = k * 32;
   const int64_t seg = seg0 + lane;
   const bool live = seg < a.nseg;
-  const int64_t pseg = a.q0 + seg * kL;
   const int V = a.M * NF;
-  double g[MT][NF];
-#pragma unroll
-  for (int m = 0; m < MT; ++m)
-#pragma unroll
-    for (int c = 0; c < NF; ++c) g[m][c] = 0.0;
-  if (MAIN) {
-    // carry of segment seg0 + l: exclusive suffix scan of the chunk's segment
-    // aggregates (multiplier L = lambda^kL) plus L^{31-l} G(chunk end)
-    const int64_t k = seg0 / 32;
-#pragma unroll
-    for (int m = 0; m < MT; ++m) {
-      if (m >= a.M) break;
-      const double L = __ldg(a.segpow + m);
-      double Le = 1.0, b = L;                     // L^{31 - lane}
-#pragma unroll
-      for (int bit = 0; bit < 5; ++bit) {
-        if (((31 - lane) >> bit) & 1) Le *= b;
-        b *= b;
-      }
-#pragma unroll
-      for (int c = 0; c < NF; ++c) {
-        double x = live ? a.agg[seg * V + m * NF + c] : 0.0, Lk = L;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const double y = __shfl_down_sync(0xffffffffu, x, d);
-          if (lane + d < 32) x = fma(Lk, y, x);
-          Lk *= Lk;
-        }
-        const double ex = __shfl_down_sync(0xffffffffu, x, 1);
-        g[m][c] = fma(Le, __ldg(a.gchunk + static_cast<int64_t>(m * NF + c) * a.nchunk + k), lane < 31 ? ex : 0.0);
-      }
-    }
-  }
-  // stage nodes qb..qb+kTB-1 of the warp's 32 segments: lane j of a round
-  // takes segment (round*32 + j) / kTB, node (round*32 + j) % kTB, so each
-  // warp instruction reads kTB consecutive nodes of 32/kTB segments
+  // staging / write-out geometry: round rr of block qb covers node r0 of
+  // segment seg0 + rr * 32/kTB + sl0, i.e. position pb + rr * kSK + qb
+  const int sl0 = lane / kTB, r0 = lane % kTB;
+  const int64_t pb = a.q0 + (seg0 + sl0) * kL + r0;
+  const int dir = a.mirror ? -1 : 1;
+  const int64_t xb = a.mirror ? a.n_in - 1 - pb : pb;       // input index of pb
+  const int64_t ob = a.mirror ? a.n_in - 1 - pb + a.off - a.o0 : pb - a.off - a.o0;   // output of p - off
+  const int64_t tb = a.mirror ? a.n_in - 1 - a.o0 : -a.o0;   // output of position t: tb + dir t
+  const int64_t nv = a.nseg - seg0 - sl0;                    // rounds rr with rr * 32/kTB < nv are live
+  const int64_t pend = a.n_in - pb;                          // live while rr * kSK + qb < pend
   auto stage = [&](int qb, int buf) {
 #pragma unroll
     for (int rr = 0; rr < kTB; ++rr) {
-      const int j = rr * 32 + lane;
-      const int sl = j / kTB, r = j % kTB;
-      const int64_t p = a.q0 + (seg0 + sl) * kL + qb + r;
-      const bool in = seg0 + sl < a.nseg && p < a.n_in;
-      const int64_t x = in ? to_input(a, p) : 0;
-      cp_async8(&sfld[w][buf][r][0][sl], a.u + x, in);
-      if (NF == 2) cp_async8(&sfld[w][buf][r][NF - 1][sl], a.kappa + x, in);
-      if (MAIN) cp_async4(&stin[w][buf][r][sl], a.tinfo + (in ? p : 0), in);
+      const int sl = rr * (32 / kTB) + sl0;
+      const int d = rr * kSK + qb;
+      const bool in = rr * (32 / kTB) < nv && d < pend;
+      const int64_t x = in ? xb + dir * d : 0;
+      cp_async8(&sfld[w][buf][r0][0][sl], a.u + x, in);
+      if (kap) cp_async8(&sfld[w][buf][r0][1][sl], a.kappa + x, in);
+      if (MAIN) cp_async4(&stin[w][buf][r0][sl], a.tinfo + (in ? pb + d : 0), in);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  auto get_f = [&](int buf, int r, double* f) {
-    f[0] = sfld[w][buf][r][0][lane];
-    if (NF == 2) f[1] = sfld[w][buf][r][1][lane] * f[0];
-  };
   stage(kL - kTB, 0);
-  if (!MAIN) {
-    int buf = 0;
-    for (int qb = kL - kTB; qb >= 0; qb -= kTB, buf ^= 1) {
-      if (qb - kTB >= 0) {
-        stage(qb - kTB, buf ^ 1);
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      } else {
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      }
-      __syncwarp();
+  double g[MT][FW];
 #pragma unroll
-      for (int r = kTB - 1; r >= 0; --r) {
-        double f[NF];
-        get_f(buf, r, f);
+  for (int m = 0; m < MT; ++m)
 #pragma unroll
-        for (int m = 0; m < MT; ++m) {
-          const double lam = ld_shared2_any(slc + m).x;
-#pragma unroll
-          for (int c = 0; c < NF; ++c) g[m][c] = fma(lam, g[m][c], f[c]);
-        }
-      }
-      __syncwarp();
-    }
-    if (live)
-#pragma unroll
-      for (int m = 0; m < MT; ++m)
-        if (m < a.M)
-#pragma unroll
-          for (int c = 0; c < NF; ++c) a.agg[seg * V + m * NF + c] = g[m][c];
-    // chunk aggregate sum_l L^l agg[seg0 + l] by a shuffle tree into lane 0
-    // (lanes past the last segment hold 0)
-    const int64_t k = seg0 / 32;
+    for (int c = 0; c < FW; ++c) g[m][c] = 0.0;
+  if (MAIN) {
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
       if (m >= a.M) break;
-      const double L = __ldg(a.segpow + m);
+      const double pw = __ldg(a.segpw + m * 32 + lane);
 #pragma unroll
-      for (int c = 0; c < NF; ++c) {
-        double v = g[m][c], Lk = L;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          v = fma(Lk, __shfl_down_sync(0xffffffffu, v, d), v);
-          Lk *= Lk;
-        }
-        if (lane == 0) a.cagg[static_cast<int64_t>(m * NF + c) * a.nchunk + k] = v;
+      for (int c = 0; c < FW; ++c) {
+        const int j = m * NF + c;
+        g[m][c] = fma(pw, __ldg(a.gchunk + j * a.nchunk + k), __ldg(a.agg + (k * V + j) * 32 + lane));
       }
     }
-    return;
   }
-  double coef[MT];
-#pragma unroll
-  for (int m = 0; m < MT; ++m) coef[m] = 0.0;
-  int ecur = -1;
-  int buf = 0;
-  for (int qb = kL - kTB; qb >= 0; qb -= kTB, buf ^= 1) {
+  __syncthreads();
+  auto get_f = [&](int buf, int r, double* f) {
+    const double uu = sfld[w][buf][r][0][lane];
+    if (FW == 2) {
+      f[0] = uu;
+      f[FW - 1] = uu * sfld[w][buf][r][1][lane];
+    } else {
+      f[0] = kap ? uu * sfld[w][buf][r][1][lane] : uu;
+    }
+  };
+  auto advance = [&](int qb, int buf) {
     if (qb - kTB >= 0) {
       stage(qb - kTB, buf ^ 1);                                // next block in flight
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
@@ -462,30 +423,72 @@ __global__ void __launch_bounds__(32 * kTailWarps, 3) es_tail_walk(PassArgs a, c
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncwarp();
+  };
+  if (!MAIN) {
+    int buf = 0;
+    for (int qb = kL - kTB; qb >= 0; qb -= kTB, buf ^= 1) {
+      advance(qb, buf);
+#pragma unroll
+      for (int r = kTB - 1; r >= 0; --r) {
+        double f[FW];
+        get_f(buf, r, f);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) g[m][0] = fma(ld_shared2_any(slc + m).x, g[m][0], f[0]);
+      }
+      __syncwarp();
+    }
+    double (*sa)[MT + 1] = sagg[MAIN ? 0 : w];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) sa[lane][m] = g[m][0];
+    __syncwarp();
+    if (lane < a.M) {                                          // lane = term: walk the chunk down
+      const double L = __ldg(a.segpow + lane);
+      double acc = 0.0;
+#pragma unroll 8
+      for (int sl = 31; sl >= 0; --sl) {
+        const double v = sa[sl][lane];
+        sa[sl][lane] = acc;
+        acc = fma(L, acc, v);
+      }
+      a.cagg[static_cast<int64_t>(lane * NF + c0) * a.nchunk + k] = acc;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+      if (m < a.M) a.agg[(k * V + m * NF + c0) * 32 + lane] = sa[lane][m];
+    return;
+  }
+  double coef[MT];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) coef[m] = 0.0;
+  int ecur = -1;
+  int buf = 0;
+  const int64_t pseg = a.q0 + seg * kL;
+  for (int qb = kL - kTB; qb >= 0; qb -= kTB, buf ^= 1) {
+    advance(qb, buf);
 #pragma unroll 1
     for (int r = kTB - 1; r >= 0; --r) {
-      const int64_t p = pseg + qb + r;
-      double f[NF];
+      double f[FW];
       get_f(buf, r, f);
-      double ac[NF][2];
+      double ac[FW][2];
 #pragma unroll
-      for (int c = 0; c < NF; ++c) ac[c][0] = ac[c][1] = 0.0;
+      for (int c = 0; c < FW; ++c) ac[c][0] = ac[c][1] = 0.0;
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
-        const double2 k = ld_shared2_any(slc + m);
+        const double2 kk = ld_shared2_any(slc + m);
 #pragma unroll
-        for (int c = 0; c < NF; ++c) {
-          g[m][c] = fma(k.x, g[m][c], f[c]);
-          ac[c][m & 1] = fma(k.y, g[m][c], ac[c][m & 1]);
+        for (int c = 0; c < FW; ++c) {
+          g[m][c] = fma(kk.x, g[m][c], f[c]);
+          ac[c][m & 1] = fma(kk.y, g[m][c], ac[c][m & 1]);
         }
       }
       const int ti = live ? stin[w][buf][r][lane] : -1;
       const int nt = ti < 0 ? 0 : (ti & 3);
-      double y[NF];
+      double y[FW][2];
 #pragma unroll
-      for (int c = 0; c < NF; ++c) y[c] = 0.0;
+      for (int c = 0; c < FW; ++c) y[c][0] = y[c][1] = 0.0;
       if (nt) {
-        const int e = static_cast<int>(p - (ti >> 2));       // = D_t + 1
+        const int e = static_cast<int>(pseg + qb + r - (ti >> 2));   // = D_t + 1
         if (e != ecur) {
           if (e == ecur + 1) {
 #pragma unroll
@@ -505,45 +508,55 @@ __global__ void __launch_bounds__(32 * kTailWarps, 3) es_tail_walk(PassArgs a, c
 #pragma unroll
         for (int m = 0; m < MT; ++m)
 #pragma unroll
-          for (int c = 0; c < NF; ++c) y[c] = fma(coef[m], g[m][c], y[c]);
+          for (int c = 0; c < FW; ++c) y[c][m & 1] = fma(coef[m], g[m][c], y[c][m & 1]);
         if (nt == 2) {                        // a second target ending here (rare): its own RED
-          const int64_t ob = to_input(a, (ti >> 2) + 1) - a.o0;
+          const int64_t o2 = tb + dir * ((ti >> 2) + 1);
 #pragma unroll
-          for (int c = 0; c < NF; ++c) {
+          for (int c = 0; c < FW; ++c) {
             double z = 0.0;
 #pragma unroll
             for (int m = 0; m < MT; ++m) z = fma(coef[m] * __ldg(tab + 3 * kMT + m), g[m][c], z);
-            atomicAdd(a.facc + c * a.n_out + ob, -z);
+            atomicAdd(a.facc + c * a.n_out + o2, -z);
           }
         }
       }
 #pragma unroll
-      for (int c = 0; c < NF; ++c) {
+      for (int c = 0; c < FW; ++c) {
         sbuf[w][r][c][lane] = ac[c][0] + ac[c][1];
-        sbuf[w][r][2 + c][lane] = y[c];
+        sbuf[w][r][FW + c][lane] = y[c][0] + y[c][1];
       }
     }
     __syncwarp();
     // transposed write-out: kTB consecutive nodes of a segment per lane group
 #pragma unroll
     for (int rr = 0; rr < kTB; ++rr) {
-      const int j = rr * 32 + lane;
-      const int sl = j / kTB, r = j % kTB;
-      const int64_t sg = seg0 + sl;
-      const int64_t p = a.q0 + sg * kL + qb + r;
-      if (sg >= a.nseg || p >= a.n_in) continue;
-      const int64_t t = p - a.off;
-      const int64_t oi = to_input(a, t) - a.o0;
-      if (t >= 0 && oi >= 0 && oi < a.n_out)
+      const int sl = rr * (32 / kTB) + sl0;
+      const int d = rr * kSK + qb;
+      if (rr * (32 / kTB) >= nv || d >= pend) continue;
+      const int64_t oi = ob + dir * d;
+      if (pb + d >= a.off && oi >= 0 && oi < a.n_out)
 #pragma unroll
-        for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + oi, sbuf[w][r][c][sl]);
-      const int ti = stin[w][buf][r][sl];
-      if (ti >= 0 && (ti & 3))
+        for (int c = 0; c < FW; ++c) atomicAdd(a.facc + c * a.n_out + oi, sbuf[w][r0][c][sl]);
+      const int ti = stin[w][buf][r0][sl];
+      if (ti >= 0 && (ti & 3)) {
+        const int64_t ot = tb + dir * (ti >> 2);
 #pragma unroll
-        for (int c = 0; c < NF; ++c) atomicAdd(a.facc + c * a.n_out + (to_input(a, ti >> 2) - a.o0), -sbuf[w][r][2 + c][sl]);
+        for (int c = 0; c < FW; ++c) atomicAdd(a.facc + c * a.n_out + ot, -sbuf[w][r0][FW + c][sl]);
+      }
     }
     __syncwarp();
   }
+}
+
+template <int NF, bool MAIN>
+void launch_tail_t(int M, const PassArgs& a, const double* tab, cudaStream_t s) {
+  constexpr int kG = kTailWarps * (MAIN ? NF : 1) / NF;
+  const unsigned grid = static_cast<unsigned>((a.nchunk + kG - 1) / kG);
+  if (M <= 8) es_tail_walk<NF, MAIN, 8><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
+  else if (M <= 10) es_tail_walk<NF, MAIN, 10><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
+  else if (M <= 12) es_tail_walk<NF, MAIN, 12><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
+  else if (M <= 14) es_tail_walk<NF, MAIN, 14><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
+  else es_tail_walk<NF, MAIN, 16><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
 }
 
 // Segment carries by a three-level scan (all fully parallel except a short
@@ -895,6 +908,7 @@ struct ExpSumState {
   double* ctab_agg = nullptr;      // the aggregate walk's chunk tables
   double* rate = nullptr;          // [kMT] t_m
   double* segpow = nullptr;        // [kMT] lambda_m^kL
+  double* segpw = nullptr;         // [kMT][32] (lambda_m^kL)^(31 - l)
   int *dplus = nullptr, *dminus = nullptr, *tinfoR = nullptr, *tinfoL = nullptr;
   double *wnear = nullptr, *scale = nullptr, *diag = nullptr;
   double *agg = nullptr, *carry = nullptr, *facc = nullptr;
@@ -1018,6 +1032,10 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   }
   S->rate = upload(rate);
   S->segpow = upload(segpow);
+  std::vector<double> segpw(static_cast<size_t>(kMT) * 32, 0.0);
+  for (int m = 0; m < M; ++m)
+    for (int l = 0; l < 32; ++l) segpw[m * 32 + l] = std::exp(-es.rate[m] * kL * (31 - l));
+  S->segpw = upload(segpw);
   S->dplus = upload(dplus);
   S->dminus = upload(dminus);
   S->tinfoR = upload(tR);
@@ -1073,7 +1091,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   S->nsegR = nseg_of(S->o0R);
   S->nsegL = nseg_of(S->o0L);
   const int64_t ns = std::max(S->nsegR, S->nsegL);
-  const size_t vals = static_cast<size_t>(kMT) * S->fields * ns;
+  const size_t vals = static_cast<size_t>(kMT) * S->fields * ((ns + kChunk - 1) / kChunk * kChunk);
   NLG_CUDA(cudaMalloc(&S->agg, sizeof(double) * vals));
   NLG_CUDA(cudaMalloc(&S->carry, sizeof(double) * vals));
   const size_t cvals = static_cast<size_t>(kMT) * S->fields * ((ns + kChunk - 1) / kChunk);
@@ -1123,7 +1141,7 @@ void expsum_setup(Plan& P, const nlg_desc& d) {
 void expsum_free(Plan& P) {
   ExpSumState* S = P.es_state;
   if (!S) return;
-  for (double* p : {S->ctab, S->ctab_agg, S->rate, S->segpow, S->wnear, S->scale, S->diag, S->agg, S->carry, S->facc, S->cagg,
+  for (double* p : {S->ctab, S->ctab_agg, S->rate, S->segpow, S->segpw, S->wnear, S->scale, S->diag, S->agg, S->carry, S->facc, S->cagg,
                     S->gchunk})
     cudaFree(p);
   for (int* p : {S->dplus, S->dminus, S->tinfoR, S->tinfoL}) cudaFree(p);
@@ -1138,15 +1156,6 @@ void expsum_free(Plan& P) {
 }
 
 namespace {
-template <int NF, bool MAIN>
-void launch_tail_t(int M, const PassArgs& a, const double* tab, cudaStream_t s) {
-  const unsigned grid = static_cast<unsigned>((a.nseg + 32 * kTailWarps - 1) / (32 * kTailWarps));
-  if (M <= 8) es_tail_walk<NF, MAIN, 8><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
-  else if (M <= 10) es_tail_walk<NF, MAIN, 10><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
-  else if (M <= 12) es_tail_walk<NF, MAIN, 12><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
-  else if (M <= 14) es_tail_walk<NF, MAIN, 14><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
-  else es_tail_walk<NF, MAIN, 16><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
-}
 void launch_tail(int nf, bool main, int M, const PassArgs& a, const double* tab, cudaStream_t s) {
   if (nf == 2) {
     if (main) launch_tail_t<2, true>(M, a, tab, s);
@@ -1196,6 +1205,7 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     a.dtarget = mirror ? S->dminus : S->dplus;
     a.rate = S->rate;
     a.segpow = S->segpow;
+    a.segpw = S->segpw;
     a.agg = S->agg;
     a.carry = S->carry;
     a.facc = S->facc;
