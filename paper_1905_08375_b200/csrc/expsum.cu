@@ -345,8 +345,18 @@ constexpr int kTB = 4, kTailWarps = 4;
 #endif
 constexpr int kTailMainCtas = NLG_TAIL_MAIN_CTAS;
 
+// both scan directions in one launch: blocks [0, split) run d[0], the rest d[1]
+struct PassPair {
+  PassArgs d[2];
+  int64_t split;
+};
+
 template <int NF, bool MAIN, int MT>
-__global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_tail_walk(PassArgs a, const double* __restrict__ tab) {
+__global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_tail_walk(const __grid_constant__ PassPair pp,
+                                                                                        const double* __restrict__ tab) {
+  const bool second = blockIdx.x >= pp.split;
+  const PassArgs& a = pp.d[second ? 1 : 0];
+  const int64_t bid = static_cast<int64_t>(blockIdx.x) - (second ? pp.split : 0);
   constexpr int FW = MAIN ? NF : 1;                          // fields per warp
   constexpr int kG = kTailWarps * FW / NF;                   // chunks per CTA
   constexpr int kSK = (32 / kTB) * kL;                       // node stride between staging rounds
@@ -359,7 +369,7 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
   for (int m = tid; m < MT; m += 32 * kTailWarps) slc[m] = make_double2(__ldg(tab + m), __ldg(tab + kMT + m));
   const int c0 = FW == NF ? 0 : (w & 1);                     // my first field
   const bool kap = NF == 2 && (FW == 2 || c0 == 1);          // kappa needed
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * kG + (FW == NF ? w : (w >> 1));   // my chunk
+  const int64_t k = bid * kG + (FW == NF ? w : (w >> 1));   // my chunk
   const int64_t seg0 = k * 32;
   const int64_t seg = seg0 + lane;
   const bool live = seg < a.nseg;
@@ -549,14 +559,15 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
 }
 
 template <int NF, bool MAIN>
-void launch_tail_t(int M, const PassArgs& a, const double* tab, cudaStream_t s) {
+void launch_tail_t(int M, PassPair pp, const double* tab, cudaStream_t s) {
   constexpr int kG = kTailWarps * (MAIN ? NF : 1) / NF;
-  const unsigned grid = static_cast<unsigned>((a.nchunk + kG - 1) / kG);
-  if (M <= 8) es_tail_walk<NF, MAIN, 8><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
-  else if (M <= 10) es_tail_walk<NF, MAIN, 10><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
-  else if (M <= 12) es_tail_walk<NF, MAIN, 12><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
-  else if (M <= 14) es_tail_walk<NF, MAIN, 14><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
-  else es_tail_walk<NF, MAIN, 16><<<grid, 32 * kTailWarps, 0, s>>>(a, tab);
+  pp.split = (pp.d[0].nchunk + kG - 1) / kG;
+  const unsigned grid = static_cast<unsigned>(pp.split + (pp.d[1].nchunk + kG - 1) / kG);
+  if (M <= 8) es_tail_walk<NF, MAIN, 8><<<grid, 32 * kTailWarps, 0, s>>>(pp, tab);
+  else if (M <= 10) es_tail_walk<NF, MAIN, 10><<<grid, 32 * kTailWarps, 0, s>>>(pp, tab);
+  else if (M <= 12) es_tail_walk<NF, MAIN, 12><<<grid, 32 * kTailWarps, 0, s>>>(pp, tab);
+  else if (M <= 14) es_tail_walk<NF, MAIN, 14><<<grid, 32 * kTailWarps, 0, s>>>(pp, tab);
+  else es_tail_walk<NF, MAIN, 16><<<grid, 32 * kTailWarps, 0, s>>>(pp, tab);
 }
 
 // Segment carries by a three-level scan (all fully parallel except a short
@@ -586,7 +597,12 @@ __global__ void es_chunk(PassArgs a, int64_t nchunk, double* cagg) {
 // One block per term j: gchunk[j][k] = G(end of chunk k); chunk multiplier
 // Lc = L^{kChunk} (a short last chunk only matters at the very top, where G = 0).
 __global__ void __launch_bounds__(kCarryThreads) es_carry(PassArgs a, int64_t nchunk, const double* cagg,
-                                                          double* gchunk) {
+                                                          double* gchunk, int64_t nchunk1, int64_t cstride) {
+  if (blockIdx.y == 1) {   // second scan direction (tail walks launch both at once)
+    nchunk = nchunk1;
+    cagg += cstride;
+    gchunk += cstride;
+  }
   const int j = blockIdx.x;
   if (j / a.nf >= a.M) return;
   double Lc = 1.0;
@@ -913,6 +929,7 @@ struct ExpSumState {
   double *wnear = nullptr, *scale = nullptr, *diag = nullptr;
   double *agg = nullptr, *carry = nullptr, *facc = nullptr;
   double *cagg = nullptr, *gchunk = nullptr;
+  size_t astride = 0, cstride = 0;   // per-direction regions (FFT mode)
   int64_t nsegR = 0, nsegL = 0, o0R = 0, o0L = 0;
   double* kappa_dev = nullptr;
 };
@@ -1092,11 +1109,13 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   S->nsegL = nseg_of(S->o0L);
   const int64_t ns = std::max(S->nsegR, S->nsegL);
   const size_t vals = static_cast<size_t>(kMT) * S->fields * ((ns + kChunk - 1) / kChunk * kChunk);
-  NLG_CUDA(cudaMalloc(&S->agg, sizeof(double) * vals));
-  NLG_CUDA(cudaMalloc(&S->carry, sizeof(double) * vals));
+  S->astride = S->fft ? vals : 0;            // tail walks: one region per direction
+  NLG_CUDA(cudaMalloc(&S->agg, sizeof(double) * vals * (S->fft ? 2 : 1)));
+  if (!S->fft) NLG_CUDA(cudaMalloc(&S->carry, sizeof(double) * vals));   // tail walks fuse the carries
   const size_t cvals = static_cast<size_t>(kMT) * S->fields * ((ns + kChunk - 1) / kChunk);
-  NLG_CUDA(cudaMalloc(&S->cagg, sizeof(double) * cvals));
-  NLG_CUDA(cudaMalloc(&S->gchunk, sizeof(double) * cvals));
+  S->cstride = S->fft ? cvals : 0;
+  NLG_CUDA(cudaMalloc(&S->cagg, sizeof(double) * cvals * (S->fft ? 2 : 1)));
+  NLG_CUDA(cudaMalloc(&S->gchunk, sizeof(double) * cvals * (S->fft ? 2 : 1)));
   NLG_CUDA(cudaMalloc(&S->facc, sizeof(double) * S->fields * n_out));
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * n_out));
   // exterior (zero collar) part of diag, exact: sum_{d > edge distance} w_d,
@@ -1156,13 +1175,13 @@ void expsum_free(Plan& P) {
 }
 
 namespace {
-void launch_tail(int nf, bool main, int M, const PassArgs& a, const double* tab, cudaStream_t s) {
+void launch_tail(int nf, bool main, int M, const PassPair& pp, const double* tab, cudaStream_t s) {
   if (nf == 2) {
-    if (main) launch_tail_t<2, true>(M, a, tab, s);
-    else launch_tail_t<2, false>(M, a, tab, s);
+    if (main) launch_tail_t<2, true>(M, pp, tab, s);
+    else launch_tail_t<2, false>(M, pp, tab, s);
   } else {
-    if (main) launch_tail_t<1, true>(M, a, tab, s);
-    else launch_tail_t<1, false>(M, a, tab, s);
+    if (main) launch_tail_t<1, true>(M, pp, tab, s);
+    else launch_tail_t<1, false>(M, pp, tab, s);
   }
 }
 }  // namespace
@@ -1187,6 +1206,7 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     stage_end(P, fs, kStEsFft, ev, 4);
     NLG_CUDA(cudaEventRecord(S->join, fs));
   }
+  PassPair pp;
   for (int mirror = 0; mirror < 2; ++mirror) {
     PassArgs a;
     a.u = u;
@@ -1212,19 +1232,12 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     const unsigned gridw = static_cast<unsigned>((a.nseg + kSegs - 1) / kSegs);
     const unsigned thr = 32 * S->cp.n;
     cudaEvent_t ev;
-    if (S->fft) {   // tail walks: aggregate (+ chunk aggregates), chunk scan, main (+ segment carries)
+    if (S->fft) {   // tail walks: both directions per launch (stitched below)
       a.nchunk = (a.nseg + kChunk - 1) / kChunk;
-      a.cagg = S->cagg;
-      a.gchunk = S->gchunk;
-      stage_begin(P, s, kStEsAggregate, &ev);
-      launch_tail(NF, false, S->M, a, S->ctab, s);
-      stage_end(P, s, kStEsAggregate, ev, 1);
-      stage_begin(P, s, kStEsCarry, &ev);
-      es_carry<<<S->M * NF, kCarryThreads, 0, s>>>(a, a.nchunk, S->cagg, S->gchunk);
-      stage_end(P, s, kStEsCarry, ev, 1);
-      stage_begin(P, s, kStEsMain, &ev);
-      launch_tail(NF, true, S->M, a, S->ctab, s);
-      stage_end(P, s, kStEsMain, ev, 1);
+      a.cagg = S->cagg + mirror * S->cstride;
+      a.gchunk = S->gchunk + mirror * S->cstride;
+      a.agg = S->agg + mirror * S->astride;
+      pp.d[mirror] = a;
       continue;
     }
     stage_begin(P, s, kStEsAggregate, &ev);
@@ -1238,7 +1251,7 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
       const int64_t work = nchunk * S->M * NF;
       const unsigned gw = static_cast<unsigned>((work + 255) / 256);
       es_chunk<<<gw, 256, 0, s>>>(a, nchunk, S->cagg);
-      es_carry<<<S->M * NF, kCarryThreads, 0, s>>>(a, nchunk, S->cagg, S->gchunk);
+      es_carry<<<S->M * NF, kCarryThreads, 0, s>>>(a, nchunk, S->cagg, S->gchunk, 0, 0);
       es_expand<<<gw, 256, 0, s>>>(a, nchunk, S->gchunk);
     }
     stage_end(P, s, kStEsCarry, ev, 3);
@@ -1248,6 +1261,18 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     stage_end(P, s, kStEsMain, ev, 1);
   }
   if (S->fft) {
+    // tail walks: aggregate (+ chunk suffixes), chunk scan, main (+ segment carries)
+    cudaEvent_t ev;
+    stage_begin(P, s, kStEsAggregate, &ev);
+    launch_tail(NF, false, S->M, pp, S->ctab, s);
+    stage_end(P, s, kStEsAggregate, ev, 1);
+    stage_begin(P, s, kStEsCarry, &ev);
+    es_carry<<<dim3(S->M * NF, 2), kCarryThreads, 0, s>>>(pp.d[0], pp.d[0].nchunk, S->cagg, S->gchunk, pp.d[1].nchunk,
+                                                         S->cstride);
+    stage_end(P, s, kStEsCarry, ev, 1);
+    stage_begin(P, s, kStEsMain, &ev);
+    launch_tail(NF, true, S->M, pp, S->ctab, s);
+    stage_end(P, s, kStEsMain, ev, 1);
     NLG_CUDA(cudaStreamWaitEvent(s, S->join, 0));
     FftCombineArgs f;
     f.u = u;
@@ -1262,7 +1287,6 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     f.ext = ext;
     f.out = out;
     f.mode = mode;
-    cudaEvent_t ev;
     stage_begin(P, s, kStEsCombine, &ev);
     const unsigned g = static_cast<unsigned>((n_out + 255) / 256);
     if (NF == 2) es_fft_combine<true><<<g, 256, 0, s>>>(f);
