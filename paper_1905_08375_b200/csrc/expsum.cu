@@ -346,27 +346,35 @@ constexpr int kTB = 4, kTailWarps = 4;
 constexpr int kTailMainCtas = NLG_TAIL_MAIN_CTAS;
 
 // both scan directions in one launch: blocks [0, split) run d[0], the rest d[1]
+// term constants of the tail walks (<= 16 terms), passed by value so that the
+// walks read them as constant-bank operands (no load instruction per use)
+constexpr int kTailMT = 16;
+struct TailTab {
+  double lam[kTailMT];    // lambda_m
+  double cn[kTailMT];     // c_m lambda_m^off (fixed end)
+  double cw[kTailMT];     // c_m
+  double ilam[kTailMT];   // 1 / lambda_m
+  double rate[kTailMT];   // t_m
+};
 struct PassPair {
   PassArgs d[2];
   int64_t split;
+  TailTab t;
 };
 
 template <int NF, bool MAIN, int MT>
-__global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_tail_walk(const __grid_constant__ PassPair pp,
-                                                                                        const double* __restrict__ tab) {
+__global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_tail_walk(const __grid_constant__ PassPair pp) {
   const bool second = blockIdx.x >= pp.split;
   const PassArgs& a = pp.d[second ? 1 : 0];
   const int64_t bid = static_cast<int64_t>(blockIdx.x) - (second ? pp.split : 0);
   constexpr int FW = MAIN ? NF : 1;                          // fields per warp
   constexpr int kG = kTailWarps * FW / NF;                   // chunks per CTA
   constexpr int kSK = (32 / kTB) * kL;                       // node stride between staging rounds
-  __shared__ double2 slc[MT];                                // (lambda, c lambda^off)
   __shared__ double sbuf[kTailWarps][kTB][2 * FW][33];       // [warp][node][ac.., y..][lane]
   __shared__ double sfld[kTailWarps][2][kTB][2][33];         // staged u, kappa: [warp][buf][node][u|k][lane]
   __shared__ int stin[kTailWarps][MAIN ? 2 : 1][kTB][33];    // staged tinfo
   __shared__ double sagg[MAIN ? 1 : kTailWarps][32][MT + 1]; // aggregate walk: chunk transposition
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  for (int m = tid; m < MT; m += 32 * kTailWarps) slc[m] = make_double2(__ldg(tab + m), __ldg(tab + kMT + m));
   const int c0 = FW == NF ? 0 : (w & 1);                     // my first field
   const bool kap = NF == 2 && (FW == 2 || c0 == 1);          // kappa needed
   const int64_t k = bid * kG + (FW == NF ? w : (w >> 1));   // my chunk
@@ -415,7 +423,6 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
       }
     }
   }
-  __syncthreads();
   auto get_f = [&](int buf, int r, double* f) {
     const double uu = sfld[w][buf][r][0][lane];
     if (FW == 2) {
@@ -443,7 +450,7 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
         double f[FW];
         get_f(buf, r, f);
 #pragma unroll
-        for (int m = 0; m < MT; ++m) g[m][0] = fma(ld_shared2_any(slc + m).x, g[m][0], f[0]);
+        for (int m = 0; m < MT; ++m) g[m][0] = fma(pp.t.lam[m], g[m][0], f[0]);
       }
       __syncwarp();
     }
@@ -485,11 +492,10 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
       for (int c = 0; c < FW; ++c) ac[c][0] = ac[c][1] = 0.0;
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
-        const double2 kk = ld_shared2_any(slc + m);
 #pragma unroll
         for (int c = 0; c < FW; ++c) {
-          g[m][c] = fma(kk.x, g[m][c], f[c]);
-          ac[c][m & 1] = fma(kk.y, g[m][c], ac[c][m & 1]);
+          g[m][c] = fma(pp.t.lam[m], g[m][c], f[c]);
+          ac[c][m & 1] = fma(pp.t.cn[m], g[m][c], ac[c][m & 1]);
         }
       }
       const int ti = live ? stin[w][buf][r][lane] : -1;
@@ -502,15 +508,15 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
         if (e != ecur) {
           if (e == ecur + 1) {
 #pragma unroll
-            for (int m = 0; m < MT; ++m) coef[m] *= ld_shared2_any(slc + m).x;
+            for (int m = 0; m < MT; ++m) coef[m] *= pp.t.lam[m];
           } else if (e == ecur - 1) {
 #pragma unroll
-            for (int m = 0; m < MT; ++m) coef[m] *= __ldg(tab + 3 * kMT + m);
+            for (int m = 0; m < MT; ++m) coef[m] *= pp.t.ilam[m];
           } else {
 #pragma unroll
             for (int m = 0; m < MT; ++m) {
-              const double cw = __ldg(tab + 2 * kMT + m);
-              coef[m] = cw == 0.0 ? 0.0 : cw * exp(-__ldg(tab + 4 * kMT + m) * static_cast<double>(e));
+              const double cw = pp.t.cw[m];
+              coef[m] = cw == 0.0 ? 0.0 : cw * exp(-pp.t.rate[m] * static_cast<double>(e));
             }
           }
           ecur = e;
@@ -525,7 +531,7 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
           for (int c = 0; c < FW; ++c) {
             double z = 0.0;
 #pragma unroll
-            for (int m = 0; m < MT; ++m) z = fma(coef[m] * __ldg(tab + 3 * kMT + m), g[m][c], z);
+            for (int m = 0; m < MT; ++m) z = fma(coef[m] * pp.t.ilam[m], g[m][c], z);
             atomicAdd(a.facc + c * a.n_out + o2, -z);
           }
         }
@@ -559,15 +565,15 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
 }
 
 template <int NF, bool MAIN>
-void launch_tail_t(int M, PassPair pp, const double* tab, cudaStream_t s) {
+void launch_tail_t(int M, PassPair pp, cudaStream_t s) {
   constexpr int kG = kTailWarps * (MAIN ? NF : 1) / NF;
   pp.split = (pp.d[0].nchunk + kG - 1) / kG;
   const unsigned grid = static_cast<unsigned>(pp.split + (pp.d[1].nchunk + kG - 1) / kG);
-  if (M <= 8) es_tail_walk<NF, MAIN, 8><<<grid, 32 * kTailWarps, 0, s>>>(pp, tab);
-  else if (M <= 10) es_tail_walk<NF, MAIN, 10><<<grid, 32 * kTailWarps, 0, s>>>(pp, tab);
-  else if (M <= 12) es_tail_walk<NF, MAIN, 12><<<grid, 32 * kTailWarps, 0, s>>>(pp, tab);
-  else if (M <= 14) es_tail_walk<NF, MAIN, 14><<<grid, 32 * kTailWarps, 0, s>>>(pp, tab);
-  else es_tail_walk<NF, MAIN, 16><<<grid, 32 * kTailWarps, 0, s>>>(pp, tab);
+  if (M <= 8) es_tail_walk<NF, MAIN, 8><<<grid, 32 * kTailWarps, 0, s>>>(pp);
+  else if (M <= 10) es_tail_walk<NF, MAIN, 10><<<grid, 32 * kTailWarps, 0, s>>>(pp);
+  else if (M <= 12) es_tail_walk<NF, MAIN, 12><<<grid, 32 * kTailWarps, 0, s>>>(pp);
+  else if (M <= 14) es_tail_walk<NF, MAIN, 14><<<grid, 32 * kTailWarps, 0, s>>>(pp);
+  else es_tail_walk<NF, MAIN, 16><<<grid, 32 * kTailWarps, 0, s>>>(pp);
 }
 
 // Segment carries by a three-level scan (all fully parallel except a short
@@ -930,6 +936,7 @@ struct ExpSumState {
   double *agg = nullptr, *carry = nullptr, *facc = nullptr;
   double *cagg = nullptr, *gchunk = nullptr;
   size_t astride = 0, cstride = 0;   // per-direction regions (FFT mode)
+  TailTab tt{};                      // tail-walk term constants (FFT mode)
   int64_t nsegR = 0, nsegL = 0, o0R = 0, o0L = 0;
   double* kappa_dev = nullptr;
 };
@@ -1013,6 +1020,16 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
     }
   }
   S->ctab = upload(ctab);
+  if (fft) {   // tail walks: all terms in chunk 0
+    if (S->nchunks != 1 || M > kTailMT) throw Error{NLG_ERUNTIME, "expsum: tail walk needs <= 16 terms in one chunk"};
+    for (int k = 0; k < kTailMT; ++k) {
+      S->tt.lam[k] = ctab[0 * kMT + k];
+      S->tt.cn[k] = ctab[1 * kMT + k];
+      S->tt.cw[k] = ctab[2 * kMT + k];
+      S->tt.ilam[k] = ctab[3 * kMT + k];
+      S->tt.rate[k] = ctab[4 * kMT + k];
+    }
+  }
   for (const void* f : {reinterpret_cast<const void*>(es_walk<1, false>), reinterpret_cast<const void*>(es_walk<2, false>),
                         reinterpret_cast<const void*>(es_walk<1, true>), reinterpret_cast<const void*>(es_walk<2, true>)})
     NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -1175,13 +1192,13 @@ void expsum_free(Plan& P) {
 }
 
 namespace {
-void launch_tail(int nf, bool main, int M, const PassPair& pp, const double* tab, cudaStream_t s) {
+void launch_tail(int nf, bool main, int M, const PassPair& pp, cudaStream_t s) {
   if (nf == 2) {
-    if (main) launch_tail_t<2, true>(M, pp, tab, s);
-    else launch_tail_t<2, false>(M, pp, tab, s);
+    if (main) launch_tail_t<2, true>(M, pp, s);
+    else launch_tail_t<2, false>(M, pp, s);
   } else {
-    if (main) launch_tail_t<1, true>(M, pp, tab, s);
-    else launch_tail_t<1, false>(M, pp, tab, s);
+    if (main) launch_tail_t<1, true>(M, pp, s);
+    else launch_tail_t<1, false>(M, pp, s);
   }
 }
 }  // namespace
@@ -1207,6 +1224,7 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     NLG_CUDA(cudaEventRecord(S->join, fs));
   }
   PassPair pp;
+  pp.t = S->tt;
   for (int mirror = 0; mirror < 2; ++mirror) {
     PassArgs a;
     a.u = u;
@@ -1264,14 +1282,14 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     // tail walks: aggregate (+ chunk suffixes), chunk scan, main (+ segment carries)
     cudaEvent_t ev;
     stage_begin(P, s, kStEsAggregate, &ev);
-    launch_tail(NF, false, S->M, pp, S->ctab, s);
+    launch_tail(NF, false, S->M, pp, s);
     stage_end(P, s, kStEsAggregate, ev, 1);
     stage_begin(P, s, kStEsCarry, &ev);
     es_carry<<<dim3(S->M * NF, 2), kCarryThreads, 0, s>>>(pp.d[0], pp.d[0].nchunk, S->cagg, S->gchunk, pp.d[1].nchunk,
                                                          S->cstride);
     stage_end(P, s, kStEsCarry, ev, 1);
     stage_begin(P, s, kStEsMain, &ev);
-    launch_tail(NF, true, S->M, pp, S->ctab, s);
+    launch_tail(NF, true, S->M, pp, s);
     stage_end(P, s, kStEsMain, ev, 1);
     NLG_CUDA(cudaStreamWaitEvent(s, S->join, 0));
     FftCombineArgs f;
