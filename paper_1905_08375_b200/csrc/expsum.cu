@@ -412,16 +412,23 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
 #pragma unroll
     for (int c = 0; c < FW; ++c) g[m][c] = 0.0;
   if (MAIN) {
+    // clamped term index, no branches: every load of the warp is in flight at once
+    double pw[MT], gc[MT][FW];
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
-      if (m >= a.M) break;
-      const double pw = __ldg(a.segpw + m * 32 + lane);
+      const int mm = min(m, a.M - 1);
+      pw[m] = __ldg(a.segpw + mm * 32 + lane);
 #pragma unroll
       for (int c = 0; c < FW; ++c) {
-        const int j = m * NF + c;
-        g[m][c] = fma(pw, __ldg(a.gchunk + j * a.nchunk + k), __ldg(a.agg + (k * V + j) * 32 + lane));
+        const int j = mm * NF + c;
+        gc[m][c] = __ldg(a.gchunk + j * a.nchunk + k);
+        g[m][c] = __ldg(a.agg + (k * V + j) * 32 + lane);
       }
     }
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int c = 0; c < FW; ++c) g[m][c] = m < a.M ? fma(pw[m], gc[m][c], g[m][c]) : 0.0;
   }
   auto get_f = [&](int buf, int r, double* f) {
     const double uu = sfld[w][buf][r][0][lane];
