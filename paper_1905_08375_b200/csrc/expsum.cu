@@ -345,6 +345,10 @@ constexpr int kTB = 4, kTailWarps = 4;
 #endif
 constexpr int kTailMainCtas = NLG_TAIL_MAIN_CTAS;
 
+__device__ __forceinline__ int clamp_int(int64_t v, int lo, int hi) {
+  return static_cast<int>(v < lo ? lo : (v > hi ? hi : v));
+}
+
 // both scan directions in one launch: blocks [0, split) run d[0], the rest d[1]
 // term constants of the tail walks (<= 16 terms), passed by value so that the
 // walks read them as constant-bank operands (no load instruction per use)
@@ -487,7 +491,19 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
   for (int m = 0; m < MT; ++m) coef[m] = 0.0;
   int ecur = -1;
   int buf = 0;
-  const int64_t pseg = a.q0 + seg * kL;
+  const int pseg = static_cast<int>(a.q0 + seg * kL);       // positions fit in int (tinfo is int)
+  // write-out bases: the fixed-end target of position pb + d is output ob + dir d,
+  // valid for d in [dlo, dhi); the far-end target of position t is tb + dir t
+  int lmask = 0;                                             // rounds whose segment is live
+#pragma unroll
+  for (int rr = 0; rr < kTB; ++rr) lmask |= (rr * (32 / kTB) < nv) << rr;
+  const int pend32 = clamp_int(pend, 0, kTB * kSK);
+  double* const fa = a.facc + ob;
+  double* const fy = a.facc + tb;
+  const int64_t no = a.n_out;
+  const int64_t lo = a.off - pb, lo2 = dir > 0 ? -ob : ob - no + 1;
+  const int dlo = clamp_int(lo > lo2 ? lo : lo2, 0, kTB * kSK);
+  const int dhi = clamp_int(dir > 0 ? no - ob : ob + 1, 0, pend32);
   for (int qb = kL - kTB; qb >= 0; qb -= kTB, buf ^= 1) {
     advance(qb, buf);
 #pragma unroll 1
@@ -511,7 +527,7 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
 #pragma unroll
       for (int c = 0; c < FW; ++c) y[c][0] = y[c][1] = 0.0;
       if (nt) {
-        const int e = static_cast<int>(pseg + qb + r - (ti >> 2));   // = D_t + 1
+        const int e = pseg + qb + r - (ti >> 2);                     // = D_t + 1
         if (e != ecur) {
           if (e == ecur + 1) {
 #pragma unroll
@@ -533,20 +549,20 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
 #pragma unroll
           for (int c = 0; c < FW; ++c) y[c][m & 1] = fma(coef[m], g[m][c], y[c][m & 1]);
         if (nt == 2) {                        // a second target ending here (rare): its own RED
-          const int64_t o2 = tb + dir * ((ti >> 2) + 1);
+          double* const o2 = fy + dir * ((ti >> 2) + 1);
 #pragma unroll
           for (int c = 0; c < FW; ++c) {
             double z = 0.0;
 #pragma unroll
             for (int m = 0; m < MT; ++m) z = fma(coef[m] * pp.t.ilam[m], g[m][c], z);
-            atomicAdd(a.facc + c * a.n_out + o2, -z);
+            atomicAdd(o2 + c * no, -z);
           }
         }
       }
 #pragma unroll
       for (int c = 0; c < FW; ++c) {
         sbuf[w][r][c][lane] = ac[c][0] + ac[c][1];
-        sbuf[w][r][FW + c][lane] = y[c][0] + y[c][1];
+        sbuf[w][r][FW + c][lane] = -(y[c][0] + y[c][1]);
       }
     }
     __syncwarp();
@@ -555,16 +571,17 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
     for (int rr = 0; rr < kTB; ++rr) {
       const int sl = rr * (32 / kTB) + sl0;
       const int d = rr * kSK + qb;
-      if (rr * (32 / kTB) >= nv || d >= pend) continue;
-      const int64_t oi = ob + dir * d;
-      if (pb + d >= a.off && oi >= 0 && oi < a.n_out)
+      if (!((lmask >> rr) & 1) || d >= pend32) continue;
+      if (d >= dlo && d < dhi) {
+        double* const o = fa + dir * d;
 #pragma unroll
-        for (int c = 0; c < FW; ++c) atomicAdd(a.facc + c * a.n_out + oi, sbuf[w][r0][c][sl]);
+        for (int c = 0; c < FW; ++c) atomicAdd(o + c * no, sbuf[w][r0][c][sl]);
+      }
       const int ti = stin[w][buf][r0][sl];
       if (ti >= 0 && (ti & 3)) {
-        const int64_t ot = tb + dir * (ti >> 2);
+        double* const o = fy + dir * (ti >> 2);
 #pragma unroll
-        for (int c = 0; c < FW; ++c) atomicAdd(a.facc + c * a.n_out + ot, -sbuf[w][r0][FW + c][sl]);
+        for (int c = 0; c < FW; ++c) atomicAdd(o + c * no, sbuf[w][r0][FW + c][sl]);
       }
     }
     __syncwarp();
