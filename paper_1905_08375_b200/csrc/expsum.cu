@@ -36,6 +36,7 @@
 
 #include <cufft.h>
 
+#include "fft.cuh"
 #include "plan.hpp"
 
 namespace nlg {
@@ -945,6 +946,8 @@ struct ExpSumState {
   cudaEvent_t fork = nullptr, join = nullptr;
   cufftDoubleComplex* z = nullptr;     // [L] (u, kappa u) -> transform -> convolution
   double* kr = nullptr;                // [L] real transform of the symmetric far kernel
+  bool four = false;                   // four-step FFT (fft.cu) instead of the cuFFT chain
+  FourStep fs{};
   // term chunks: first global term, real terms, slow flag; constants per chunk
   int nchunks = 0, cmb[kMaxChunks] = {}, ccnt[kMaxChunks] = {};
   bool cslow[kMaxChunks] = {};
@@ -1135,6 +1138,15 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
     NLG_CUFFT(cufftExecZ2Z(S->fplan, S->z, S->z, CUFFT_FORWARD));
     fft_real_part<<<static_cast<unsigned>((L + 255) / 256), 256, 0, P.stream>>>(S->z, S->kr, L);   // symmetric: real
     NLG_CUDA(cudaGetLastError());
+    S->four = fourstep_plan(L, S->fs);
+    if (S->four) {   // fused four-step passes; the cuFFT plan was only needed for the kernel spectrum
+      fourstep_setup(S->fs, S->kr, P.stream);
+      NLG_CUDA(cudaStreamSynchronize(P.stream));
+      cufftDestroy(S->fplan);
+      S->fplan = 0;
+      NLG_CUDA(cudaFree(S->kr));
+      S->kr = nullptr;
+    }
     NLG_CUDA(cudaStreamSynchronize(P.stream));
   }
   S->kappa_dev = P.d_kappa;
@@ -1211,6 +1223,7 @@ void expsum_free(Plan& P) {
   if (S->join) cudaEventDestroy(S->join);
   cudaFree(S->z);
   cudaFree(S->kr);
+  fourstep_free(S->fs);
   delete S;
   P.es_state = nullptr;
 }
@@ -1235,6 +1248,16 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
   if (S->fft) {   // fixed-window far field z = FFT^-1( K^ . FFT(u + i kappa u) ), on a side stream
     NLG_CUDA(cudaEventRecord(S->fork, s));
     NLG_CUDA(cudaStreamWaitEvent(S->fstream, S->fork, 0));
+    if (S->four) {
+      cudaStream_t fs = S->fstream;
+      cudaEvent_t ev;
+      stage_begin(P, fs, kStEsFft, &ev);
+      fourstep_forward_product(S->fs, u, NF == 2 ? S->kappa_dev : nullptr, P.n_in, reinterpret_cast<double2*>(S->z), fs);
+      stage_end(P, fs, kStEsFft, ev, 2);
+      NLG_CUDA(cudaEventRecord(S->join, fs));
+    }
+  }
+  if (S->fft && !S->four) {
     cudaStream_t fs = S->fstream;
     cudaEvent_t ev;
     stage_begin(P, fs, kStEsFft, &ev);
@@ -1316,6 +1339,24 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     launch_tail(NF, true, S->M, pp, s);
     stage_end(P, s, kStEsMain, ev, 1);
     NLG_CUDA(cudaStreamWaitEvent(s, S->join, 0));
+    if (S->four) {
+      FsCombine c;
+      c.u = u;
+      c.kappa = NF == 2 ? S->kappa_dev : nullptr;
+      c.n_in = P.n_in;
+      c.n_out = n_out;
+      c.o0 = P.halo_lo;
+      c.scale = S->scale;
+      c.diag = S->diag;
+      c.facc = S->facc;
+      c.ext = ext;
+      c.out = out;
+      c.mode = mode;
+      stage_begin(P, s, kStEsCombine, &ev);
+      fourstep_inverse_combine(S->fs, reinterpret_cast<const double2*>(S->z), c, s);
+      stage_end(P, s, kStEsCombine, ev, 1);
+      return;
+    }
     FftCombineArgs f;
     f.u = u;
     f.kappa = S->kappa_dev;

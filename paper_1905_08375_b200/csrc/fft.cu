@@ -1,0 +1,468 @@
+// paper_1905_08375_b200/csrc/fft.cu — four-step fp64 FFT convolution (expsum
+// FFT mode).
+//
+// The fixed-window far field is conv(f, K) for f = u + i kappa u (two real
+// fields in one complex signal) and the real symmetric window kernel K. With
+// L = N1 N2, x = N2 n1 + n2 and k = k1 + N1 k2 the transform splits into
+// column FFTs (length N1), a twiddle W_L^{n2 k1} and row FFTs (length N2). The
+// whole convolution runs in three HBM passes:
+//   P1 fs_cols_fwd : load u, kappa (the packing), column FFTs, twiddle -> z
+//   P2 fs_rows     : row FFT, x K^/L, conj, row FFT (the inverse row step by
+//                    the conjugate identity), one CTA per row in shared memory
+//   P3 fs_cols_inv : twiddle, column FFTs, conj -> conv, fused with the
+//                    expsum combine (tails, kappa weighting, scale and diagonal)
+// Every FFT is a self-sorting mixed-radix Stockham transform in shared memory
+// (radix 2/3/4/8 butterflies held in registers between two barriers).
+// Against the cuFFT chain (pack, 3 + 3 passes, spectrum product, combine) this
+// moves ~0.64 GB instead of ~1.5 GB per apply at N = 2^22.
+#include "fft.cuh"
+
+#include <cmath>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace nlg {
+namespace {
+
+constexpr int kFsC = 8;          // columns per column-pass CTA (8 x 16 B = 128 B rows)
+constexpr int kFsEl = 8;         // elements per thread per stage (register budget)
+constexpr int kFsTwB = 4096;     // four-step twiddle split: W^P = A[P / 4096] B[P % 4096]
+
+struct FsDev {
+  int n1, n2;
+  const double2* tw1;
+  const double2* tw2;
+  const double2* twa;
+  const double2* twb;
+  const double* krp;
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }   // a (-i)
+
+// forward DFTs of size R (exp(-2 pi i j k / R)), in place, natural order
+template <int R>
+struct Dft;
+template <>
+struct Dft<2> {
+  __device__ __forceinline__ static void run(double2* v) {
+    const double2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  }
+};
+template <>
+struct Dft<3> {
+  __device__ __forceinline__ static void run(double2* v) {
+    constexpr double kS3 = 0.86602540378443864676;   // sin(2 pi / 3)
+    const double2 s = cadd(v[1], v[2]), d = csub(v[1], v[2]);
+    const double2 m = make_double2(fma(-0.5, s.x, v[0].x), fma(-0.5, s.y, v[0].y));
+    const double2 t = make_double2(kS3 * d.y, -kS3 * d.x);   // -i sin(2pi/3) d
+    v[0] = cadd(v[0], s);
+    v[1] = cadd(m, t);
+    v[2] = csub(m, t);
+  }
+};
+template <>
+struct Dft<4> {
+  __device__ __forceinline__ static void run(double2* v) {
+    const double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    const double2 t2 = cadd(v[1], v[3]), t3 = mul_mi(csub(v[1], v[3]));
+    v[0] = cadd(t0, t2);
+    v[2] = csub(t0, t2);
+    v[1] = cadd(t1, t3);
+    v[3] = csub(t1, t3);
+  }
+};
+template <>
+struct Dft<8> {
+  __device__ __forceinline__ static void run(double2* v) {
+    constexpr double kC = 0.70710678118654752440;    // cos(pi / 4)
+    double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+    Dft<4>::run(e);
+    Dft<4>::run(o);
+    const double2 w[4] = {o[0], make_double2(kC * (o[1].x + o[1].y), kC * (o[1].y - o[1].x)), mul_mi(o[2]),
+                          make_double2(kC * (o[3].y - o[3].x), -kC * (o[3].x + o[3].y))};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = cadd(e[k], w[k]);
+      v[k + 4] = csub(e[k], w[k]);
+    }
+  }
+};
+template <>
+struct Dft<9> {   // 3 x 3 with W9 twiddles
+  __device__ __forceinline__ static void run(double2* v) {
+    // W9^k = (cos(2 pi k / 9), -sin(2 pi k / 9)), k = 1, 2, 4
+    constexpr double c1 = 0.76604444311897803520, s1 = 0.64278760968653932632;
+    constexpr double c2 = 0.17364817766693034885, s2 = 0.98480775301220805936;
+    constexpr double c4 = -0.93969262078590838405, s4 = 0.34202014332566873304;
+    double2 a[3][3];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {   // a[m] = DFT3(v[m], v[m + 3], v[m + 6])
+      a[m][0] = v[m];
+      a[m][1] = v[m + 3];
+      a[m][2] = v[m + 6];
+      Dft<3>::run(a[m]);
+    }
+    a[1][1] = cmul(a[1][1], make_double2(c1, -s1));   // W9^{m k}
+    a[1][2] = cmul(a[1][2], make_double2(c2, -s2));
+    a[2][1] = cmul(a[2][1], make_double2(c2, -s2));
+    a[2][2] = cmul(a[2][2], make_double2(c4, -s4));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {   // X[k + 3 q] = DFT3_m(a[m][k])[q]
+      double2 b[3] = {a[0][k], a[1][k], a[2][k]};
+      Dft<3>::run(b);
+      v[k] = b[0];
+      v[k + 3] = b[1];
+      v[k + 6] = b[2];
+    }
+  }
+};
+template <>
+struct Dft<16> {
+  __device__ __forceinline__ static void run(double2* v) {
+    // W16^k = (cos(pi k / 8), -sin(pi k / 8)), k = 1..7
+    constexpr double kc[8] = {1.0, 0.92387953251128675613, 0.70710678118654752440, 0.38268343236508977173,
+                              0.0, -0.38268343236508977173, -0.70710678118654752440, -0.92387953251128675613};
+    constexpr double ks[8] = {0.0, 0.38268343236508977173, 0.70710678118654752440, 0.92387953251128675613,
+                              1.0, 0.92387953251128675613, 0.70710678118654752440, 0.38268343236508977173};
+    double2 e[8], o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      e[k] = v[2 * k];
+      o[k] = v[2 * k + 1];
+    }
+    Dft<8>::run(e);
+    Dft<8>::run(o);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double2 w = k == 0 ? o[0] : (k == 4 ? mul_mi(o[4]) : cmul(o[k], make_double2(kc[k], -ks[k])));
+      v[k] = cadd(e[k], w);
+      v[k + 8] = csub(e[k], w);
+    }
+  }
+};
+
+// element q of the shared buffer (rows pad one slot per 8: the radix-8
+// stores at Ns = 1 of a quarter warp hit 8 distinct 16-byte bank groups)
+template <bool PAD>
+__device__ __forceinline__ int sidx(int q) { return PAD ? q + (q >> 3) : q; }
+
+// Radix plans (compile time). Columns: a 9 (or 3) first, then 8s, then the
+// 4 / 2 remainder. Rows: 16s with the remainder second, so that the first and
+// last radix agree and the last forward stage fuses with the first inverse one.
+template <int N, int Ns>
+__host__ __device__ constexpr int fs_radix_cols() {
+  return (N / Ns) % 9 == 0 ? 9 : ((N / Ns) % 3 == 0 ? 3 : ((N / Ns) % 8 == 0 ? 8 : ((N / Ns) % 4 == 0 ? 4 : 2)));
+}
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+template <int N, int Ns>
+__host__ __device__ constexpr int fs_radix_rows() {
+  return (Ns == 16 && (1 << (ilog2(N) % 4)) > 1) ? (1 << (ilog2(N) % 4)) : 16;
+}
+template <bool ROWS, int N, int Ns>
+__host__ __device__ constexpr int fs_radix() { return ROWS ? fs_radix_rows<N, Ns>() : fs_radix_cols<N, Ns>(); }
+
+// One Stockham stage over C interleaved transforms of length N (element e of
+// transform c at e * C + c). Inputs come from shared memory or, for the first
+// stage, from ld(e, c); outputs go to shared memory or, for the last stage, to
+// st(e, c, v). Every butterfly of the thread sits in registers between the
+// reads and the writes, so a shared-to-shared stage is in place.
+template <bool ROWS, int N, int Ns, int C, int T, bool PAD, class LD, class ST>
+__device__ __forceinline__ void fs_stage(double2* s, const double2* __restrict__ tw, int tid, const LD& ld, const ST& st) {
+  constexpr int R = fs_radix<ROWS, N, Ns>();
+  constexpr bool kFirst = Ns == 1, kLast = Ns * R == N;
+  constexpr int nq = N / R, nb = nq * C;
+  constexpr int J = (nb + T - 1) / T;
+  double2 v[J][R];
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    const int b = tid + jj * T;
+    if (nb % T == 0 || b < nb) {
+      const int c = b % C, j = b / C;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[jj][r] = kFirst ? ld(j + r * nq, c) : s[sidx<PAD>((j + r * nq) * C + c)];
+    }
+  }
+  if (!kFirst && !kLast) __syncthreads();
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    const int b = tid + jj * T;
+    if (nb % T == 0 || b < nb) {
+      const int c = b % C, j = b / C;
+      const int k = j % Ns;
+      if (!kFirst && k > 0) {   // twiddles w^r, w = exp(-2 pi i k / (Ns R))
+        const double2 w = __ldg(tw + k * (N / (Ns * R)));
+        double2 wr = w;
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          v[jj][r] = cmul(v[jj][r], wr);
+          if (r + 1 < R) wr = cmul(wr, w);
+        }
+      }
+      Dft<R>::run(v[jj]);
+      const int base = (j - k) * R + k;   // (j / Ns) Ns R + j % Ns
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (kLast) st(base + r * Ns, c, v[jj][r]);
+        else s[sidx<PAD>((base + r * Ns) * C + c)] = v[jj][r];
+      }
+    }
+  }
+  if (!kLast) __syncthreads();
+}
+
+// forward FFT stages from sub-size Ns up to (not including) STOP; the first
+// stage of the transform reads ld, the last writes st
+template <bool ROWS, int N, int Ns, int STOP, int C, int T, bool PAD, class LD, class ST>
+__device__ __forceinline__ void fs_fft(double2* s, const double2* tw, int tid, const LD& ld, const ST& st) {
+  if constexpr (Ns < STOP) {
+    fs_stage<ROWS, N, Ns, C, T, PAD>(s, tw, tid, ld, st);
+    fs_fft<ROWS, N, Ns * fs_radix<ROWS, N, Ns>(), STOP, C, T, PAD>(s, tw, tid, ld, st);
+  }
+}
+
+__device__ __forceinline__ double2 four_tw(const FsDev& d, int p) {   // W_L^p, 0 <= p < L
+  return cmul(__ldg(d.twa + (p >> 12)), __ldg(d.twb + (p & (kFsTwB - 1))));
+}
+
+// column passes: T threads cover the N1 * kFsC elements of a CTA, kFsEl each
+template <int N1>
+__host__ __device__ constexpr int cols_threads() { return (N1 * kFsC + kFsEl - 1) / kFsEl; }
+constexpr int kFsRowEl = 16;   // row passes: elements per thread
+
+// P1: columns c0..c0+7, x = N2 n1 + n2 -> z[k1][n2] = W^{n2 k1} FFT_N1(f)[k1]
+template <int N1, bool KW>
+__global__ void __launch_bounds__(cols_threads<N1>(), 2) fs_cols_fwd(const __grid_constant__ FsDev d,
+                                                                    const double* __restrict__ u,
+                                                                    const double* __restrict__ kappa, int64_t n_in,
+                                                                    double2* __restrict__ z) {
+  constexpr int T = cols_threads<N1>();
+  extern __shared__ double2 fsm[];
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * kFsC;
+  auto ld = [&](int n1, int c) {
+    const int64_t x = static_cast<int64_t>(n1) * d.n2 + c0 + c;
+    if (x >= n_in) return make_double2(0.0, 0.0);
+    const double a = __ldg(u + x);
+    return make_double2(a, KW ? a * __ldg(kappa + x) : 0.0);
+  };
+  auto st = [&](int k1, int c, double2 v) {
+    const int n2 = c0 + c;
+    z[static_cast<int64_t>(k1) * d.n2 + n2] = cmul(v, four_tw(d, n2 * k1));
+  };
+  fs_fft<false, N1, 1, N1, kFsC, T, false>(fsm, d.tw1, tid, ld, st);
+}
+
+// P2: one row k1: forward FFT, x K^[k1 + N1 k2] / L, conjugate, forward FFT.
+// The last forward stage (thread j holds X[j + r N/R]) and the first stage of
+// the second transform (reads j + r N/R) share their elements: the spectrum
+// product happens in registers between the two butterflies.
+template <int N2>
+__global__ void __launch_bounds__(N2 / kFsRowEl) fs_rows(const __grid_constant__ FsDev d, double2* __restrict__ z) {
+  constexpr int T = N2 / kFsRowEl;
+  constexpr int R = 16;                 // first = last radix of the row plan
+  constexpr int nq = N2 / R;
+  static_assert(nq == T, "one butterfly per thread in the fused stage");
+  extern __shared__ double2 fsm[];
+  const int tid = threadIdx.x;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * N2;
+  auto ld = [&](int e, int) { return z[row + e]; };
+  auto none = [&](int, int, double2) {};
+  // forward transform up to (not including) its last stage
+  fs_fft<true, N2, 1, N2 / R, 1, T, true>(fsm, d.tw2, tid, ld, none);
+  {
+    // fused: last forward stage (Ns = N2 / R), product, first stage of the second transform
+    constexpr int Ns = N2 / R;
+    const int j = tid, k = j;           // j < Ns
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = fsm[sidx<true>(j + r * nq)];
+    __syncthreads();
+    if (k > 0) {
+      const double2 w = __ldg(d.tw2 + k * (N2 / (Ns * R)));
+      double2 wr = w;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        v[r] = cmul(v[r], wr);
+        if (r + 1 < R) wr = cmul(wr, w);
+      }
+    }
+    Dft<R>::run(v);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {       // X[j + r Ns]: x K^ / L, conjugate
+      const double kk = __ldg(d.krp + row + j + r * Ns);
+      v[r] = make_double2(v[r].x * kk, -v[r].y * kk);
+    }
+    Dft<R>::run(v);                     // first stage of the second transform (Ns = 1)
+#pragma unroll
+    for (int r = 0; r < R; ++r) fsm[sidx<true>(j * R + r)] = v[r];
+    __syncthreads();
+  }
+  auto st = [&](int e, int, double2 v) { z[row + e] = v; };
+  fs_fft<true, N2, R, N2, 1, T, true>(fsm, d.tw2, tid, ld, st);
+}
+
+// P3: columns: conv(x) = conj(FFT_N1(W^{n2 k1} z[k1][n2]))[n1], then the combine
+template <int N1, bool KW>
+__global__ void __launch_bounds__(cols_threads<N1>(), 2) fs_cols_inv(const __grid_constant__ FsDev d,
+                                                                    const double2* __restrict__ z,
+                                                                    const __grid_constant__ FsCombine cb) {
+  constexpr int T = cols_threads<N1>();
+  extern __shared__ double2 fsm[];
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * kFsC;
+  auto ld = [&](int k1, int c) {
+    const int n2 = c0 + c;
+    return cmul(z[static_cast<int64_t>(k1) * d.n2 + n2], four_tw(d, n2 * k1));
+  };
+  auto st = [&](int n1, int c, double2 r) {   // conv = (r.x, -r.y)
+    const int64_t x = static_cast<int64_t>(n1) * d.n2 + c0 + c;
+    const int64_t i = x - cb.o0;
+    if (i < 0 || i >= cb.n_out) return;
+    const double fu = r.x + cb.facc[i];
+    const double X = KW ? fma(cb.kappa[x], fu, cb.facc[cb.n_out + i] - r.y) : fu;
+    if (cb.mode == 1) cb.out[i] = cb.ext ? X + cb.ext[i] : X;
+    else cb.out[i] = cb.scale[i] * (X - cb.u[x] * cb.diag[i]);
+  };
+  fs_fft<false, N1, 1, N1, kFsC, T, false>(fsm, d.tw1, tid, ld, st);
+}
+
+__global__ void fs_permute(const double* __restrict__ kr, double* __restrict__ krp, int n1, int n2, double inv_l) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;   // k1 * N2 + k2
+  if (q >= static_cast<int64_t>(n1) * n2) return;
+  const int64_t k1 = q / n2, k2 = q % n2;
+  krp[q] = kr[k1 + n1 * k2] * inv_l;
+}
+
+FsDev dev_of(const FourStep& F) {
+  FsDev d;
+  d.n1 = F.n1;
+  d.n2 = F.n2;
+  d.tw1 = F.tw1;
+  d.tw2 = F.tw2;
+  d.twa = F.twa;
+  d.twb = F.twb;
+  d.krp = F.krp;
+  return d;
+}
+
+// supported column lengths 2^a {1, 3, 9} in [64, 768] (one thread per column element)
+#define NLG_FS_N1(X) X(64) X(72) X(96) X(128) X(144) X(192) X(256) X(288) X(384) X(512) X(576) X(768)
+
+size_t cols_smem(int n1) { return sizeof(double2) * n1 * kFsC; }
+size_t rows_smem(int n2) { return sizeof(double2) * (n2 + n2 / 8); }
+
+template <int N1>
+void cols_attr() {
+  for (const void* f : {reinterpret_cast<const void*>(fs_cols_fwd<N1, true>), reinterpret_cast<const void*>(fs_cols_fwd<N1, false>),
+                        reinterpret_cast<const void*>(fs_cols_inv<N1, true>), reinterpret_cast<const void*>(fs_cols_inv<N1, false>)})
+    NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cols_smem(N1))));
+}
+
+template <int N1>
+void cols_fwd(const FsDev& d, const double* u, const double* kappa, int64_t n_in, double2* z, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>(d.n2 / kFsC);
+  if (kappa) fs_cols_fwd<N1, true><<<g, cols_threads<N1>(), cols_smem(N1), s>>>(d, u, kappa, n_in, z);
+  else fs_cols_fwd<N1, false><<<g, cols_threads<N1>(), cols_smem(N1), s>>>(d, u, kappa, n_in, z);
+}
+
+template <int N1>
+void cols_inv(const FsDev& d, const double2* z, const FsCombine& c, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>(d.n2 / kFsC);
+  if (c.kappa) fs_cols_inv<N1, true><<<g, cols_threads<N1>(), cols_smem(N1), s>>>(d, z, c);
+  else fs_cols_inv<N1, false><<<g, cols_threads<N1>(), cols_smem(N1), s>>>(d, z, c);
+}
+
+bool n1_supported(int64_t n1) {
+#define NLG_FS_CASE(N) if (n1 == N) return true;
+  NLG_FS_N1(NLG_FS_CASE)
+#undef NLG_FS_CASE
+  return false;
+}
+
+std::vector<double2> twiddles(int64_t n, int64_t count, int64_t step) {   // exp(-2 pi i step t / n)
+  std::vector<double2> t(static_cast<size_t>(count));
+  const long double pi2 = 2.0L * std::acos(-1.0L);
+  for (int64_t i = 0; i < count; ++i) {
+    const long double a = pi2 * static_cast<long double>((step * i) % n) / static_cast<long double>(n);
+    t[i] = make_double2(static_cast<double>(std::cos(a)), static_cast<double>(-std::sin(a)));
+  }
+  return t;
+}
+
+double2* upload2(const std::vector<double2>& v) {
+  double2* p = nullptr;
+  NLG_CUDA(cudaMalloc(&p, sizeof(double2) * v.size()));
+  NLG_CUDA(cudaMemcpy(p, v.data(), sizeof(double2) * v.size(), cudaMemcpyHostToDevice));
+  return p;
+}
+
+}  // namespace
+
+bool fourstep_plan(int64_t L, FourStep& F) {
+  for (int n2 : {8192, 4096, 2048}) {
+    if (L % n2 || !n1_supported(L / n2)) continue;
+    F.L = L;
+    F.n1 = static_cast<int>(L / n2);
+    F.n2 = n2;
+    return true;
+  }
+  return false;
+}
+
+void fourstep_setup(FourStep& F, const double* kr, cudaStream_t s) {
+  F.tw1 = upload2(twiddles(F.n1, F.n1, 1));
+  F.tw2 = upload2(twiddles(F.n2, F.n2, 1));
+  F.twa = upload2(twiddles(F.L, F.L / kFsTwB + 1, kFsTwB));
+  F.twb = upload2(twiddles(F.L, kFsTwB, 1));
+  NLG_CUDA(cudaDeviceSynchronize());   // pageable uploads complete before any stream work
+  NLG_CUDA(cudaMalloc(&F.krp, sizeof(double) * F.L));
+  fs_permute<<<static_cast<unsigned>((F.L + 255) / 256), 256, 0, s>>>(kr, F.krp, F.n1, F.n2,
+                                                                      1.0 / static_cast<double>(F.L));
+  NLG_CUDA(cudaGetLastError());
+#define NLG_FS_CASE(N) \
+  if (F.n1 == N) cols_attr<N>();
+  NLG_FS_N1(NLG_FS_CASE)
+#undef NLG_FS_CASE
+  for (const void* f : {reinterpret_cast<const void*>(fs_rows<2048>), reinterpret_cast<const void*>(fs_rows<4096>),
+                        reinterpret_cast<const void*>(fs_rows<8192>)})
+    NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rows_smem(8192))));
+}
+
+void fourstep_free(FourStep& F) {
+  for (double2* p : {F.tw1, F.tw2, F.twa, F.twb}) cudaFree(p);
+  cudaFree(F.krp);
+  F = FourStep{};
+}
+
+void fourstep_forward_product(const FourStep& F, const double* u, const double* kappa, int64_t n_in, double2* z,
+                              cudaStream_t s) {
+  const FsDev d = dev_of(F);
+#define NLG_FS_CASE(N) \
+  if (F.n1 == N) cols_fwd<N>(d, u, kappa, n_in, z, s);
+  NLG_FS_N1(NLG_FS_CASE)
+#undef NLG_FS_CASE
+  const size_t rs = rows_smem(F.n2);
+  if (F.n2 == 8192) fs_rows<8192><<<F.n1, 8192 / kFsRowEl, rs, s>>>(d, z);
+  else if (F.n2 == 4096) fs_rows<4096><<<F.n1, 4096 / kFsRowEl, rs, s>>>(d, z);
+  else fs_rows<2048><<<F.n1, 2048 / kFsRowEl, rs, s>>>(d, z);
+}
+
+void fourstep_inverse_combine(const FourStep& F, const double2* z, const FsCombine& c, cudaStream_t s) {
+  const FsDev d = dev_of(F);
+#define NLG_FS_CASE(N) \
+  if (F.n1 == N) cols_inv<N>(d, z, c, s);
+  NLG_FS_N1(NLG_FS_CASE)
+#undef NLG_FS_CASE
+}
+
+int fourstep_launches() { return 3; }
+
+}  // namespace nlg

@@ -1,0 +1,51 @@
+// paper_1905_08375_b200/csrc/fft.cuh — four-step fp64 FFT convolution for the
+// 1-D fixed-window far field (expsum FFT mode), with the field packing, the
+// spectrum product and the final combine fused into its three HBM passes.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nlg {
+
+// L = N1 * N2 (N2 = 2^b rows, N1 = 2^a {1,3,9} columns); element x of the
+// signal is (n1, n2) = (x / N2, x % N2), frequency k = k1 + N1 k2.
+struct FourStep {
+  int64_t L = 0;
+  int n1 = 0, n2 = 0;
+  double2* tw1 = nullptr;    // [N1] exp(-2 pi i t / N1)
+  double2* tw2 = nullptr;    // [N2] exp(-2 pi i t / N2)
+  double2* twa = nullptr;    // [L / 4096 + 1] exp(-2 pi i 4096 a / L)
+  double2* twb = nullptr;    // [4096] exp(-2 pi i b / L)
+  double* krp = nullptr;     // [N1][N2] kernel spectrum / L at k1 + N1 k2
+};
+
+// inputs of the combine fused into the last pass:
+//   X = kappa_x (conv_u + facc0) + conv_ku + facc1  (kappa) or conv_u + facc0
+//   mode 0: out = scale (X - u_x diag);  mode 1: out = X (+ ext)
+struct FsCombine {
+  const double* u;
+  const double* kappa;       // null: no kappa weighting
+  int64_t n_in, n_out, o0;
+  const double* scale;
+  const double* diag;
+  const double* facc;        // [fields][n_out]
+  const double* ext;
+  double* out;
+  int mode;
+};
+
+// Plan for length L, or false when L has no supported split (the caller then
+// runs the cuFFT path).
+bool fourstep_plan(int64_t L, FourStep& F);
+// Device tables; kr = real kernel spectrum in natural order (length L).
+void fourstep_setup(FourStep& F, const double* kr, cudaStream_t s);
+void fourstep_free(FourStep& F);
+// z <- row spectra product, from u (+ kappa u) (passes 1 and 2)
+void fourstep_forward_product(const FourStep& F, const double* u, const double* kappa, int64_t n_in, double2* z,
+                              cudaStream_t s);
+// inverse column pass with the combine (pass 3)
+void fourstep_inverse_combine(const FourStep& F, const double2* z, const FsCombine& c, cudaStream_t s);
+int fourstep_launches();
+
+}  // namespace nlg
