@@ -115,6 +115,10 @@ typedef struct nlg_info {
   int exp_terms;             /* far-field terms of the 1-D exponential sum     */
   int near_cells;            /* near-field radius (cells) of the 1-D scan path */
   double far_rel_err;        /* fitted kernel error of the exponential sum     */
+  int64_t fft_len;           /* 1-D far window by FFT convolution: length L,
+                                0 when the scan path runs without it           */
+  int fft_rows;              /* four-step split L = N1 x fft_rows (fft.cu);
+                                0: the cuFFT path for lengths it does not cover */
 } nlg_info;
 
 /* Halo rows a slab [row_begin,row_end) needs for this operator, before the

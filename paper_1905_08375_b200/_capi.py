@@ -44,7 +44,8 @@ SOLVE_CG, SOLVE_CGNR, SOLVE_DIRECT = 0, 1, 0x10
 class Info(C.Structure):
     _fields_ = [("halo_lo", C.c_int64), ("halo_hi", C.c_int64), ("n_in", C.c_int64),
                 ("n_out", C.c_int64), ("fast_method", C.c_int), ("exp_terms", C.c_int),
-                ("near_cells", C.c_int), ("far_rel_err", C.c_double)]
+                ("near_cells", C.c_int), ("far_rel_err", C.c_double), ("fft_len", C.c_int64),
+                ("fft_rows", C.c_int)]
 
 
 EXPORTS = {

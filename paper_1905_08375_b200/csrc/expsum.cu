@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
   const int c0 = FW == NF ? 0 : (w & 1);                     // my first field
   const bool kap = NF == 2 && (FW == 2 || c0 == 1);          // kappa needed
   const int64_t k = bid * kG + (FW == NF ? w : (w >> 1));   // my chunk
+  if (k >= a.nchunk) return;                                 // grid padding (warp-uniform; no CTA barriers below)
   const int64_t seg0 = k * 32;
   const int64_t seg = seg0 + lane;
   const bool live = seg < a.nseg;
@@ -1399,6 +1400,12 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
   if (c.kappa) es_near_combine<true><<<gc, kCombineThreads, cbytes, s>>>(c);
   else es_near_combine<false><<<gc, kCombineThreads, cbytes, s>>>(c);
   stage_end(P, s, kStEsCombine, ev, 1);
+}
+
+void expsum_fft_info(const Plan& P, int64_t& len, int& rows) {
+  const ExpSumState* S = P.es_state;
+  len = S && S->fft ? S->L : 0;
+  rows = S && S->four ? S->fs.n2 : 0;
 }
 
 void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s) {

@@ -208,10 +208,11 @@ __device__ __forceinline__ void fs_stage(double2* s, const double2* __restrict__
       }
       Dft<R>::run(v[jj]);
       const int base = (j - k) * R + k;   // (j / Ns) Ns R + j % Ns
+      if constexpr (kLast) {
+        st(base, Ns, c, v[jj]);   // outputs e = base + r Ns, r < R
+      } else {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (kLast) st(base + r * Ns, c, v[jj][r]);
-        else s[sidx<PAD>((base + r * Ns) * C + c)] = v[jj][r];
+        for (int r = 0; r < R; ++r) s[sidx<PAD>((base + r * Ns) * C + c)] = v[jj][r];
       }
     }
   }
@@ -253,9 +254,14 @@ __global__ void __launch_bounds__(cols_threads<N1>(), 2) fs_cols_fwd(const __gri
     const double a = __ldg(u + x);
     return make_double2(a, KW ? a * __ldg(kappa + x) : 0.0);
   };
-  auto st = [&](int k1, int c, double2 v) {
+  auto st = [&](int base, int stride, int c, auto& v) {   // k1 = base + r stride
+    constexpr int R = sizeof(v) / sizeof(v[0]);
     const int n2 = c0 + c;
-    z[static_cast<int64_t>(k1) * d.n2 + n2] = cmul(v, four_tw(d, n2 * k1));
+    double2 w[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) w[r] = four_tw(d, n2 * (base + r * stride));
+#pragma unroll
+    for (int r = 0; r < R; ++r) z[static_cast<int64_t>(base + r * stride) * d.n2 + n2] = cmul(v[r], w[r]);
   };
   fs_fft<false, N1, 1, N1, kFsC, T, false>(fsm, d.tw1, tid, ld, st);
 }
@@ -271,16 +277,25 @@ __global__ void __launch_bounds__(N2 / kFsRowEl) fs_rows(const __grid_constant__
   constexpr int nq = N2 / R;
   static_assert(nq == T, "one butterfly per thread in the fused stage");
   extern __shared__ double2 fsm[];
+  double* skr = reinterpret_cast<double*>(fsm + N2 + N2 / 8);   // the row of K^ / L, prefetched
   const int tid = threadIdx.x;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * N2;
+#pragma unroll
+  for (int it = 0; it < N2 / T; ++it) {
+    const int q = tid + it * T;
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(skr + q));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(d.krp + row + q) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
   auto ld = [&](int e, int) { return z[row + e]; };
-  auto none = [&](int, int, double2) {};
+  auto none = [&](int, int, int, auto&) {};
   // forward transform up to (not including) its last stage
   fs_fft<true, N2, 1, N2 / R, 1, T, true>(fsm, d.tw2, tid, ld, none);
   {
     // fused: last forward stage (Ns = N2 / R), product, first stage of the second transform
     constexpr int Ns = N2 / R;
     const int j = tid, k = j;           // j < Ns
+    asm volatile("cp.async.wait_all;\n" ::: "memory");   // own K^ loads; the barrier below publishes all
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = fsm[sidx<true>(j + r * nq)];
@@ -297,7 +312,7 @@ __global__ void __launch_bounds__(N2 / kFsRowEl) fs_rows(const __grid_constant__
     Dft<R>::run(v);
 #pragma unroll
     for (int r = 0; r < R; ++r) {       // X[j + r Ns]: x K^ / L, conjugate
-      const double kk = __ldg(d.krp + row + j + r * Ns);
+      const double kk = skr[j + r * Ns];
       v[r] = make_double2(v[r].x * kk, -v[r].y * kk);
     }
     Dft<R>::run(v);                     // first stage of the second transform (Ns = 1)
@@ -305,7 +320,11 @@ __global__ void __launch_bounds__(N2 / kFsRowEl) fs_rows(const __grid_constant__
     for (int r = 0; r < R; ++r) fsm[sidx<true>(j * R + r)] = v[r];
     __syncthreads();
   }
-  auto st = [&](int e, int, double2 v) { z[row + e] = v; };
+  auto st = [&](int base, int stride, int, auto& v) {
+    constexpr int RR = sizeof(v) / sizeof(v[0]);
+#pragma unroll
+    for (int r = 0; r < RR; ++r) z[row + base + r * stride] = v[r];
+  };
   fs_fft<true, N2, R, N2, 1, T, true>(fsm, d.tw2, tid, ld, st);
 }
 
@@ -322,14 +341,20 @@ __global__ void __launch_bounds__(cols_threads<N1>(), 2) fs_cols_inv(const __gri
     const int n2 = c0 + c;
     return cmul(z[static_cast<int64_t>(k1) * d.n2 + n2], four_tw(d, n2 * k1));
   };
-  auto st = [&](int n1, int c, double2 r) {   // conv = (r.x, -r.y)
-    const int64_t x = static_cast<int64_t>(n1) * d.n2 + c0 + c;
-    const int64_t i = x - cb.o0;
-    if (i < 0 || i >= cb.n_out) return;
-    const double fu = r.x + cb.facc[i];
-    const double X = KW ? fma(cb.kappa[x], fu, cb.facc[cb.n_out + i] - r.y) : fu;
-    if (cb.mode == 1) cb.out[i] = cb.ext ? X + cb.ext[i] : X;
-    else cb.out[i] = cb.scale[i] * (X - cb.u[x] * cb.diag[i]);
+  auto st = [&](int base, int stride, int c, auto& v) {   // n1 = base + r stride; conv = (v.x, -v.y)
+    constexpr int R = sizeof(v) / sizeof(v[0]);
+    const int64_t x0 = static_cast<int64_t>(base) * d.n2 + c0 + c - cb.o0;   // output index of r = 0
+    const int64_t xs = static_cast<int64_t>(stride) * d.n2;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t i = x0 + r * xs;
+      if (i < 0 || i >= cb.n_out) continue;
+      const int64_t x = i + cb.o0;
+      const double fu = v[r].x + __ldg(cb.facc + i);
+      const double X = KW ? fma(__ldg(cb.kappa + x), fu, __ldg(cb.facc + cb.n_out + i) - v[r].y) : fu;
+      if (cb.mode == 1) cb.out[i] = cb.ext ? X + __ldg(cb.ext + i) : X;
+      else cb.out[i] = __ldg(cb.scale + i) * (X - __ldg(cb.u + x) * __ldg(cb.diag + i));
+    }
   };
   fs_fft<false, N1, 1, N1, kFsC, T, false>(fsm, d.tw1, tid, ld, st);
 }
@@ -357,7 +382,7 @@ FsDev dev_of(const FourStep& F) {
 #define NLG_FS_N1(X) X(64) X(72) X(96) X(128) X(144) X(192) X(256) X(288) X(384) X(512) X(576) X(768)
 
 size_t cols_smem(int n1) { return sizeof(double2) * n1 * kFsC; }
-size_t rows_smem(int n2) { return sizeof(double2) * (n2 + n2 / 8); }
+size_t rows_smem(int n2) { return sizeof(double2) * (n2 + n2 / 8) + sizeof(double) * n2; }
 
 template <int N1>
 void cols_attr() {
@@ -433,7 +458,7 @@ void fourstep_setup(FourStep& F, const double* kr, cudaStream_t s) {
 #undef NLG_FS_CASE
   for (const void* f : {reinterpret_cast<const void*>(fs_rows<2048>), reinterpret_cast<const void*>(fs_rows<4096>),
                         reinterpret_cast<const void*>(fs_rows<8192>)})
-    NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rows_smem(8192))));
+    NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rows_smem(8192))));   // 208 KB
 }
 
 void fourstep_free(FourStep& F) {

@@ -274,6 +274,9 @@ nlg_status nlg_plan_info(const nlg_plan* plan, nlg_info* info) {
     info->exp_terms = P.es.terms;
     info->near_cells = P.es.near;
     info->far_rel_err = P.es.rel_err;
+    info->fft_len = 0;
+    info->fft_rows = 0;
+    if (P.es_state) expsum_fft_info(P, info->fft_len, info->fft_rows);
   });
 }
 

@@ -109,6 +109,7 @@ void spans_free(Plan& P);
 void expsum_setup(Plan& P, const nlg_desc& d);
 void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void expsum_free(Plan& P);
+void expsum_fft_info(const Plan& P, int64_t& len, int& rows);
 void stencil_setup(Plan& P, const nlg_desc& d);
 void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void stencil_free(Plan& P);
