@@ -44,7 +44,14 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
     headers.append(os.path.join(ROOT, "include", "nlgpu.h"))
     objs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
-    common += os.environ.get("NLG_NVCC_EXTRA", "").split()   # experiment builds (e.g. -DNLG_R2FRAC=4)
+    extra = os.environ.get("NLG_NVCC_EXTRA", "").split()   # experiment builds (e.g. -DNLG_R2FRAC=4)
+    common += extra
+    stamp = os.path.join(objdir, "flags.txt")               # rebuild everything when the extra flags change
+    prev = open(stamp).read() if os.path.exists(stamp) else None
+    if prev != " ".join(extra):
+        force = True
+        with open(stamp, "w") as f:
+            f.write(" ".join(extra))
     for f in cu:
         src = os.path.join(CSRC, f)
         obj = os.path.join(objdir, f + ".o")

@@ -27,6 +27,9 @@ namespace {
 
 constexpr int kFsC = 8;          // columns per column-pass CTA (8 x 16 B = 128 B rows)
 constexpr int kFsEl = 8;         // elements per thread per stage (register budget)
+#ifndef NLG_FS_KRP_PREFETCH
+#define NLG_FS_KRP_PREFETCH 0     // K^ row staged by cp.async (208 KB CTAs: no co-residence with the scans)
+#endif
 constexpr int kFsTwB = 4096;     // four-step twiddle split: W^P = A[P / 4096] B[P % 4096]
 
 struct FsDev {
@@ -280,6 +283,7 @@ __global__ void __launch_bounds__(N2 / kFsRowEl) fs_rows(const __grid_constant__
   double* skr = reinterpret_cast<double*>(fsm + N2 + N2 / 8);   // the row of K^ / L, prefetched
   const int tid = threadIdx.x;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * N2;
+#if NLG_FS_KRP_PREFETCH
 #pragma unroll
   for (int it = 0; it < N2 / T; ++it) {
     const int q = tid + it * T;
@@ -287,6 +291,7 @@ __global__ void __launch_bounds__(N2 / kFsRowEl) fs_rows(const __grid_constant__
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(d.krp + row + q) : "memory");
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
+#endif
   auto ld = [&](int e, int) { return z[row + e]; };
   auto none = [&](int, int, int, auto&) {};
   // forward transform up to (not including) its last stage
@@ -295,7 +300,9 @@ __global__ void __launch_bounds__(N2 / kFsRowEl) fs_rows(const __grid_constant__
     // fused: last forward stage (Ns = N2 / R), product, first stage of the second transform
     constexpr int Ns = N2 / R;
     const int j = tid, k = j;           // j < Ns
+#if NLG_FS_KRP_PREFETCH
     asm volatile("cp.async.wait_all;\n" ::: "memory");   // own K^ loads; the barrier below publishes all
+#endif
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = fsm[sidx<true>(j + r * nq)];
@@ -312,7 +319,11 @@ __global__ void __launch_bounds__(N2 / kFsRowEl) fs_rows(const __grid_constant__
     Dft<R>::run(v);
 #pragma unroll
     for (int r = 0; r < R; ++r) {       // X[j + r Ns]: x K^ / L, conjugate
+#if NLG_FS_KRP_PREFETCH
       const double kk = skr[j + r * Ns];
+#else
+      const double kk = __ldg(d.krp + row + j + r * Ns);
+#endif
       v[r] = make_double2(v[r].x * kk, -v[r].y * kk);
     }
     Dft<R>::run(v);                     // first stage of the second transform (Ns = 1)
@@ -382,7 +393,7 @@ FsDev dev_of(const FourStep& F) {
 #define NLG_FS_N1(X) X(64) X(72) X(96) X(128) X(144) X(192) X(256) X(288) X(384) X(512) X(576) X(768)
 
 size_t cols_smem(int n1) { return sizeof(double2) * n1 * kFsC; }
-size_t rows_smem(int n2) { return sizeof(double2) * (n2 + n2 / 8) + sizeof(double) * n2; }
+size_t rows_smem(int n2) { return sizeof(double2) * (n2 + n2 / 8) + (NLG_FS_KRP_PREFETCH ? sizeof(double) * n2 : 0); }
 
 template <int N1>
 void cols_attr() {
