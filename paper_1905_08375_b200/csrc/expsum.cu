@@ -39,6 +39,14 @@
 #include "fft.cuh"
 #include "plan.hpp"
 
+#ifndef NLG_TAIL_TOL
+#define NLG_TAIL_TOL 5e-10     // narrow-window tail fit: max relative kernel error
+#endif
+#ifndef NLG_FFT_SERIAL
+#define NLG_FFT_SERIAL 0
+#endif
+
+
 namespace nlg {
 
 namespace {
@@ -992,8 +1000,8 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   for (int64_t i = 0; i < n_out; ++i) dmin = std::min<int64_t>(dmin, std::min(dplus[i], dminus[i]));
   // FFT mode when the horizons span a narrow range (a short tail fit exists);
   // otherwise near window P + exponential sum over the whole far range
-  ExpSum es = dmin >= 1 ? fit_exponential_sum_narrow(d.alpha, dmin + 1, dmax, 5e-10, kChunkCap) : ExpSum{};
-  const bool fft = dmin >= 1 && es.terms > 0 && es.rel_err <= 5e-10;
+  ExpSum es = dmin >= 1 ? fit_exponential_sum_narrow(d.alpha, dmin + 1, dmax, NLG_TAIL_TOL, kChunkCap) : ExpSum{};
+  const bool fft = dmin >= 1 && es.terms > 0 && es.rel_err <= NLG_TAIL_TOL;
   if (!fft) {
     es = fit_exponential_sum(d.alpha, kNear, dmax, 1e-11);
     if (es.terms == 0 || es.rel_err > 1e-11) return;
@@ -1250,11 +1258,15 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     NLG_CUDA(cudaEventRecord(S->fork, s));
     NLG_CUDA(cudaStreamWaitEvent(S->fstream, S->fork, 0));
     if (S->four) {
-      cudaStream_t fs = S->fstream;
+      cudaStream_t fs = NLG_FFT_SERIAL ? s : S->fstream;   // experiment knob: no side-stream overlap
       cudaEvent_t ev;
       stage_begin(P, fs, kStEsFft, &ev);
+      // all three passes on the side stream (they do not depend on the scans);
+      // the combine runs after the join (measured: fusing it into the last pass
+      // keeps that pass off the side stream and costs more than the extra z pass)
       fourstep_forward_product(S->fs, u, NF == 2 ? S->kappa_dev : nullptr, P.n_in, reinterpret_cast<double2*>(S->z), fs);
-      stage_end(P, fs, kStEsFft, ev, 2);
+      fourstep_inverse(S->fs, reinterpret_cast<double2*>(S->z), fs);
+      stage_end(P, fs, kStEsFft, ev, 3);
       NLG_CUDA(cudaEventRecord(S->join, fs));
     }
   }
@@ -1340,29 +1352,11 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     launch_tail(NF, true, S->M, pp, s);
     stage_end(P, s, kStEsMain, ev, 1);
     NLG_CUDA(cudaStreamWaitEvent(s, S->join, 0));
-    if (S->four) {
-      FsCombine c;
-      c.u = u;
-      c.kappa = NF == 2 ? S->kappa_dev : nullptr;
-      c.n_in = P.n_in;
-      c.n_out = n_out;
-      c.o0 = P.halo_lo;
-      c.scale = S->scale;
-      c.diag = S->diag;
-      c.facc = S->facc;
-      c.ext = ext;
-      c.out = out;
-      c.mode = mode;
-      stage_begin(P, s, kStEsCombine, &ev);
-      fourstep_inverse_combine(S->fs, reinterpret_cast<const double2*>(S->z), c, s);
-      stage_end(P, s, kStEsCombine, ev, 1);
-      return;
-    }
     FftCombineArgs f;
     f.u = u;
     f.kappa = S->kappa_dev;
     f.z = S->z;
-    f.inv_l = 1.0 / static_cast<double>(S->L);
+    f.inv_l = S->four ? 1.0 : 1.0 / static_cast<double>(S->L);   // four-step: K^ / L folded in
     f.n_out = n_out;
     f.o0 = P.halo_lo;
     f.scale = S->scale;

@@ -9,12 +9,12 @@
 //   P1 fs_cols_fwd : load u, kappa (the packing), column FFTs, twiddle -> z
 //   P2 fs_rows     : row FFT, x K^/L, conj, row FFT (the inverse row step by
 //                    the conjugate identity), one CTA per row in shared memory
-//   P3 fs_cols_inv : twiddle, column FFTs, conj -> conv, fused with the
-//                    expsum combine (tails, kappa weighting, scale and diagonal)
+//   P3 fs_cols_inv : twiddle, column FFTs, conj -> conv (in z, signal order)
 // Every FFT is a self-sorting mixed-radix Stockham transform in shared memory
 // (radix 2/3/4/8 butterflies held in registers between two barriers).
-// Against the cuFFT chain (pack, 3 + 3 passes, spectrum product, combine) this
-// moves ~0.64 GB instead of ~1.5 GB per apply at N = 2^22.
+// Against the cuFFT chain (pack, 3 + 3 passes, spectrum product) this moves
+// ~0.55 GB instead of ~1.2 GB per apply at N = 2^22; all three passes run on
+// the side stream, overlapping the exponential-sum scans.
 #include "fft.cuh"
 
 #include <cmath>
@@ -25,7 +25,6 @@
 namespace nlg {
 namespace {
 
-constexpr int kFsC = 8;          // columns per column-pass CTA (8 x 16 B = 128 B rows)
 constexpr int kFsEl = 8;         // elements per thread per stage (register budget)
 #ifndef NLG_FS_KRP_PREFETCH
 #define NLG_FS_KRP_PREFETCH 0     // K^ row staged by cp.async (208 KB CTAs: no co-residence with the scans)
@@ -165,12 +164,17 @@ __host__ __device__ constexpr int fs_radix_cols() {
   return (N / Ns) % 9 == 0 ? 9 : ((N / Ns) % 3 == 0 ? 3 : ((N / Ns) % 8 == 0 ? 8 : ((N / Ns) % 4 == 0 ? 4 : 2)));
 }
 __host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
-template <int N, int Ns>
+// rows: radix EL (elements per thread), the remainder second
+template <int N, int Ns, int EL>
 __host__ __device__ constexpr int fs_radix_rows() {
-  return (Ns == 16 && (1 << (ilog2(N) % 4)) > 1) ? (1 << (ilog2(N) % 4)) : 16;
+  return (Ns == EL && (1 << (ilog2(N) % ilog2(EL))) > 1) ? (1 << (ilog2(N) % ilog2(EL))) : EL;
 }
+template <int N2>
+__host__ __device__ constexpr int rows_el() { return N2 >= 8192 ? 16 : 8; }
 template <bool ROWS, int N, int Ns>
-__host__ __device__ constexpr int fs_radix() { return ROWS ? fs_radix_rows<N, Ns>() : fs_radix_cols<N, Ns>(); }
+__host__ __device__ constexpr int fs_radix() {
+  return ROWS ? fs_radix_rows<N, Ns, rows_el<N>()>() : fs_radix_cols<N, Ns>();
+}
 
 // One Stockham stage over C interleaved transforms of length N (element e of
 // transform c at e * C + c). Inputs come from shared memory or, for the first
@@ -236,10 +240,12 @@ __device__ __forceinline__ double2 four_tw(const FsDev& d, int p) {   // W_L^p, 
   return cmul(__ldg(d.twa + (p >> 12)), __ldg(d.twb + (p & (kFsTwB - 1))));
 }
 
-// column passes: T threads cover the N1 * kFsC elements of a CTA, kFsEl each
+// column passes: C columns per CTA (8: 128-byte row pieces; 4 beyond N1 = 768
+// to stay within 576 threads), T threads cover the N1 * C elements, kFsEl each
 template <int N1>
-__host__ __device__ constexpr int cols_threads() { return (N1 * kFsC + kFsEl - 1) / kFsEl; }
-constexpr int kFsRowEl = 16;   // row passes: elements per thread
+__host__ __device__ constexpr int cols_c() { return N1 <= 768 ? 8 : 4; }
+template <int N1>
+__host__ __device__ constexpr int cols_threads() { return (N1 * cols_c<N1>() + kFsEl - 1) / kFsEl; }
 
 // P1: columns c0..c0+7, x = N2 n1 + n2 -> z[k1][n2] = W^{n2 k1} FFT_N1(f)[k1]
 template <int N1, bool KW>
@@ -247,10 +253,10 @@ __global__ void __launch_bounds__(cols_threads<N1>(), 2) fs_cols_fwd(const __gri
                                                                     const double* __restrict__ u,
                                                                     const double* __restrict__ kappa, int64_t n_in,
                                                                     double2* __restrict__ z) {
-  constexpr int T = cols_threads<N1>();
+  constexpr int T = cols_threads<N1>(), C = cols_c<N1>();
   extern __shared__ double2 fsm[];
   const int tid = threadIdx.x;
-  const int c0 = blockIdx.x * kFsC;
+  const int c0 = blockIdx.x * C;
   auto ld = [&](int n1, int c) {
     const int64_t x = static_cast<int64_t>(n1) * d.n2 + c0 + c;
     if (x >= n_in) return make_double2(0.0, 0.0);
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(cols_threads<N1>(), 2) fs_cols_fwd(const __gri
 #pragma unroll
     for (int r = 0; r < R; ++r) z[static_cast<int64_t>(base + r * stride) * d.n2 + n2] = cmul(v[r], w[r]);
   };
-  fs_fft<false, N1, 1, N1, kFsC, T, false>(fsm, d.tw1, tid, ld, st);
+  fs_fft<false, N1, 1, N1, C, T, false>(fsm, d.tw1, tid, ld, st);
 }
 
 // P2: one row k1: forward FFT, x K^[k1 + N1 k2] / L, conjugate, forward FFT.
@@ -274,9 +280,10 @@ __global__ void __launch_bounds__(cols_threads<N1>(), 2) fs_cols_fwd(const __gri
 // the second transform (reads j + r N/R) share their elements: the spectrum
 // product happens in registers between the two butterflies.
 template <int N2>
-__global__ void __launch_bounds__(N2 / kFsRowEl) fs_rows(const __grid_constant__ FsDev d, double2* __restrict__ z) {
-  constexpr int T = N2 / kFsRowEl;
-  constexpr int R = 16;                 // first = last radix of the row plan
+__global__ void __launch_bounds__(N2 / rows_el<N2>(), (N2 / rows_el<N2>() <= 512 && N2 < 8192) ? 2 : 1)
+    fs_rows(const __grid_constant__ FsDev d, double2* __restrict__ z) {
+  constexpr int T = N2 / rows_el<N2>();
+  constexpr int R = rows_el<N2>();      // first = last radix of the row plan
   constexpr int nq = N2 / R;
   static_assert(nq == T, "one butterfly per thread in the fused stage");
   extern __shared__ double2 fsm[];
@@ -339,35 +346,26 @@ __global__ void __launch_bounds__(N2 / kFsRowEl) fs_rows(const __grid_constant__
   fs_fft<true, N2, R, N2, 1, T, true>(fsm, d.tw2, tid, ld, st);
 }
 
-// P3: columns: conv(x) = conj(FFT_N1(W^{n2 k1} z[k1][n2]))[n1], then the combine
-template <int N1, bool KW>
+// P3: columns: conv(x) = conj(FFT_N1(W^{n2 k1} z[k1][n2]))[n1] -> z[x] = (conv u, conv kappa u),
+// in place (a CTA reads and writes only its own columns)
+template <int N1>
 __global__ void __launch_bounds__(cols_threads<N1>(), 2) fs_cols_inv(const __grid_constant__ FsDev d,
-                                                                    const double2* __restrict__ z,
-                                                                    const __grid_constant__ FsCombine cb) {
-  constexpr int T = cols_threads<N1>();
+                                                                          double2* z) {
+  constexpr int T = cols_threads<N1>(), C = cols_c<N1>();
   extern __shared__ double2 fsm[];
   const int tid = threadIdx.x;
-  const int c0 = blockIdx.x * kFsC;
+  const int c0 = blockIdx.x * C;
   auto ld = [&](int k1, int c) {
     const int n2 = c0 + c;
     return cmul(z[static_cast<int64_t>(k1) * d.n2 + n2], four_tw(d, n2 * k1));
   };
-  auto st = [&](int base, int stride, int c, auto& v) {   // n1 = base + r stride; conv = (v.x, -v.y)
+  auto st = [&](int base, int stride, int c, auto& v) {
     constexpr int R = sizeof(v) / sizeof(v[0]);
-    const int64_t x0 = static_cast<int64_t>(base) * d.n2 + c0 + c - cb.o0;   // output index of r = 0
-    const int64_t xs = static_cast<int64_t>(stride) * d.n2;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int64_t i = x0 + r * xs;
-      if (i < 0 || i >= cb.n_out) continue;
-      const int64_t x = i + cb.o0;
-      const double fu = v[r].x + __ldg(cb.facc + i);
-      const double X = KW ? fma(__ldg(cb.kappa + x), fu, __ldg(cb.facc + cb.n_out + i) - v[r].y) : fu;
-      if (cb.mode == 1) cb.out[i] = cb.ext ? X + __ldg(cb.ext + i) : X;
-      else cb.out[i] = __ldg(cb.scale + i) * (X - __ldg(cb.u + x) * __ldg(cb.diag + i));
-    }
+    for (int r = 0; r < R; ++r)
+      z[static_cast<int64_t>(base + r * stride) * d.n2 + c0 + c] = make_double2(v[r].x, -v[r].y);
   };
-  fs_fft<false, N1, 1, N1, kFsC, T, false>(fsm, d.tw1, tid, ld, st);
+  fs_fft<false, N1, 1, N1, C, T, false>(fsm, d.tw1, tid, ld, st);
 }
 
 __global__ void fs_permute(const double* __restrict__ kr, double* __restrict__ krp, int n1, int n2, double inv_l) {
@@ -389,32 +387,33 @@ FsDev dev_of(const FourStep& F) {
   return d;
 }
 
-// supported column lengths 2^a {1, 3, 9} in [64, 768] (one thread per column element)
-#define NLG_FS_N1(X) X(64) X(72) X(96) X(128) X(144) X(192) X(256) X(288) X(384) X(512) X(576) X(768)
+// supported column lengths 2^a {1, 3, 9} in [64, 1536]
+#define NLG_FS_N1(X) X(64) X(72) X(96) X(128) X(144) X(192) X(256) X(288) X(384) X(512) X(576) X(768) X(1152) X(1536)
 
-size_t cols_smem(int n1) { return sizeof(double2) * n1 * kFsC; }
+template <int N1>
+size_t cols_smem() { return sizeof(double2) * N1 * cols_c<N1>(); }
 size_t rows_smem(int n2) { return sizeof(double2) * (n2 + n2 / 8) + (NLG_FS_KRP_PREFETCH ? sizeof(double) * n2 : 0); }
 
 template <int N1>
 void cols_attr() {
   for (const void* f : {reinterpret_cast<const void*>(fs_cols_fwd<N1, true>), reinterpret_cast<const void*>(fs_cols_fwd<N1, false>),
-                        reinterpret_cast<const void*>(fs_cols_inv<N1, true>), reinterpret_cast<const void*>(fs_cols_inv<N1, false>)})
-    NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cols_smem(N1))));
+                        reinterpret_cast<const void*>(fs_cols_inv<N1>)})
+    NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cols_smem<N1>())));
 }
 
 template <int N1>
 void cols_fwd(const FsDev& d, const double* u, const double* kappa, int64_t n_in, double2* z, cudaStream_t s) {
-  const unsigned g = static_cast<unsigned>(d.n2 / kFsC);
-  if (kappa) fs_cols_fwd<N1, true><<<g, cols_threads<N1>(), cols_smem(N1), s>>>(d, u, kappa, n_in, z);
-  else fs_cols_fwd<N1, false><<<g, cols_threads<N1>(), cols_smem(N1), s>>>(d, u, kappa, n_in, z);
+  const unsigned g = static_cast<unsigned>(d.n2 / cols_c<N1>());
+  if (kappa) fs_cols_fwd<N1, true><<<g, cols_threads<N1>(), cols_smem<N1>(), s>>>(d, u, kappa, n_in, z);
+  else fs_cols_fwd<N1, false><<<g, cols_threads<N1>(), cols_smem<N1>(), s>>>(d, u, kappa, n_in, z);
 }
 
 template <int N1>
-void cols_inv(const FsDev& d, const double2* z, const FsCombine& c, cudaStream_t s) {
-  const unsigned g = static_cast<unsigned>(d.n2 / kFsC);
-  if (c.kappa) fs_cols_inv<N1, true><<<g, cols_threads<N1>(), cols_smem(N1), s>>>(d, z, c);
-  else fs_cols_inv<N1, false><<<g, cols_threads<N1>(), cols_smem(N1), s>>>(d, z, c);
+void cols_inv(const FsDev& d, double2* z, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>(d.n2 / cols_c<N1>());
+  fs_cols_inv<N1><<<g, cols_threads<N1>(), cols_smem<N1>(), s>>>(d, z);
 }
+
 
 bool n1_supported(int64_t n1) {
 #define NLG_FS_CASE(N) if (n1 == N) return true;
@@ -442,8 +441,13 @@ double2* upload2(const std::vector<double2>& v) {
 
 }  // namespace
 
+#ifndef NLG_FS_ROWS_FIRST
+#define NLG_FS_ROWS_FIRST 8192   // preferred row length when several splits exist
+#endif
+
 bool fourstep_plan(int64_t L, FourStep& F) {
-  for (int n2 : {8192, 4096, 2048}) {
+  const int order[3] = {NLG_FS_ROWS_FIRST, NLG_FS_ROWS_FIRST == 8192 ? 4096 : 8192, 2048};
+  for (int n2 : order) {
     if (L % n2 || !n1_supported(L / n2)) continue;
     F.L = L;
     F.n1 = static_cast<int>(L / n2);
@@ -486,19 +490,18 @@ void fourstep_forward_product(const FourStep& F, const double* u, const double* 
   NLG_FS_N1(NLG_FS_CASE)
 #undef NLG_FS_CASE
   const size_t rs = rows_smem(F.n2);
-  if (F.n2 == 8192) fs_rows<8192><<<F.n1, 8192 / kFsRowEl, rs, s>>>(d, z);
-  else if (F.n2 == 4096) fs_rows<4096><<<F.n1, 4096 / kFsRowEl, rs, s>>>(d, z);
-  else fs_rows<2048><<<F.n1, 2048 / kFsRowEl, rs, s>>>(d, z);
+  if (F.n2 == 8192) fs_rows<8192><<<F.n1, 8192 / rows_el<8192>(), rs, s>>>(d, z);
+  else if (F.n2 == 4096) fs_rows<4096><<<F.n1, 4096 / rows_el<4096>(), rs, s>>>(d, z);
+  else fs_rows<2048><<<F.n1, 2048 / rows_el<2048>(), rs, s>>>(d, z);
 }
 
-void fourstep_inverse_combine(const FourStep& F, const double2* z, const FsCombine& c, cudaStream_t s) {
+void fourstep_inverse(const FourStep& F, double2* z, cudaStream_t s) {
   const FsDev d = dev_of(F);
 #define NLG_FS_CASE(N) \
-  if (F.n1 == N) cols_inv<N>(d, z, c, s);
+  if (F.n1 == N) cols_inv<N>(d, z, s);
   NLG_FS_N1(NLG_FS_CASE)
 #undef NLG_FS_CASE
 }
 
-int fourstep_launches() { return 3; }
 
 }  // namespace nlg

@@ -1,6 +1,6 @@
 // paper_1905_08375_b200/csrc/fft.cuh — four-step fp64 FFT convolution for the
 // 1-D fixed-window far field (expsum FFT mode), with the field packing, the
-// spectrum product and the final combine fused into its three HBM passes.
+// spectrum product fused into its three HBM passes.
 #pragma once
 
 #include <cstdint>
@@ -20,21 +20,6 @@ struct FourStep {
   double* krp = nullptr;     // [N1][N2] kernel spectrum / L at k1 + N1 k2
 };
 
-// inputs of the combine fused into the last pass:
-//   X = kappa_x (conv_u + facc0) + conv_ku + facc1  (kappa) or conv_u + facc0
-//   mode 0: out = scale (X - u_x diag);  mode 1: out = X (+ ext)
-struct FsCombine {
-  const double* u;
-  const double* kappa;       // null: no kappa weighting
-  int64_t n_in, n_out, o0;
-  const double* scale;
-  const double* diag;
-  const double* facc;        // [fields][n_out]
-  const double* ext;
-  double* out;
-  int mode;
-};
-
 // Plan for length L, or false when L has no supported split (the caller then
 // runs the cuFFT path).
 bool fourstep_plan(int64_t L, FourStep& F);
@@ -44,8 +29,7 @@ void fourstep_free(FourStep& F);
 // z <- row spectra product, from u (+ kappa u) (passes 1 and 2)
 void fourstep_forward_product(const FourStep& F, const double* u, const double* kappa, int64_t n_in, double2* z,
                               cudaStream_t s);
-// inverse column pass with the combine (pass 3)
-void fourstep_inverse_combine(const FourStep& F, const double2* z, const FsCombine& c, cudaStream_t s);
-int fourstep_launches();
+// inverse column pass alone: z <- (conv u, conv kappa u) in signal order
+void fourstep_inverse(const FourStep& F, double2* z, cudaStream_t s);
 
 }  // namespace nlg
