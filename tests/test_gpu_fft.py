@@ -11,7 +11,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 FAST_TOL = 1e-10
 REPEAT_TOL = 1e-12
-N1_SUPPORTED = {64, 72, 96, 128, 144, 192, 256, 288, 384, 512, 576, 768, 1152, 1536}
+N1_SUPPORTED = {64, 72, 96, 128, 144, 192, 256, 288, 384, 512, 576, 768, 1024, 1152, 1536}
 
 
 @pytest.fixture(scope="module")
@@ -23,9 +23,12 @@ def N():
     return nonloc
 
 
-def expected_split(L):
+def expected_split(L, first=4096):
     """Mirror of fourstep_plan (fft.cu): first row length whose column length is supported."""
-    for n2 in (8192, 4096, 2048):
+    if first == 0:
+        return 0
+    order = (first, 8192 if first == 4096 else 4096, 8192 if first == 2048 else 2048)
+    for n2 in order:
         if L % n2 == 0 and L // n2 in N1_SUPPORTED:
             return n2
     return 0
@@ -65,9 +68,21 @@ def test_fft_split_fast_vs_direct(sweep, n):
 
 def test_fft_splits_covered(sweep):
     rows = {info.fft_rows for info, _ in sweep.values()}
-    assert {0, 2048, 4096, 8192} <= rows, rows          # 0: the cuFFT path
+    assert {0, 2048, 4096} <= rows, rows                # 0: the cuFFT path; 8192 forced below
     n1 = [info.fft_len // info.fft_rows for info, _ in sweep.values() if info.fft_rows]
     assert any(v % 9 == 0 for v in n1) and any(v % 3 == 0 and v % 9 for v in n1) and any(v % 3 for v in n1), n1
+
+
+@pytest.mark.parametrize("rows", [8192, 2048, 0])
+@pytest.mark.parametrize("n", [1 << 19, 1 << 20])
+def test_fft_forced_row_length(N, n, rows, monkeypatch):
+    """Row kernels the default preference does not reach at test sizes
+    (8192), the 2048 rows and the cuFFT path (0), forced at plan time."""
+    from paper_1905_08375_b200 import configs
+    monkeypatch.setenv("NLG_FS_ROWS", str(rows))
+    info, err = sampled_check(N, configs.cfg1(n), n)
+    assert info.fft_rows == expected_split(info.fft_len, rows)
+    assert err <= FAST_TOL, (n, rows, info.fft_len, info.fft_rows, err)
 
 
 @pytest.mark.parametrize("n", [1 << 19, 1 << 16])
@@ -92,7 +107,7 @@ def test_fft_repeat_and_second_plan(N):
     w = configs.cfg1(n)
     a = N.NonlocalOperator(w.dim, w.n, **w.op_kwargs())
     b = N.NonlocalOperator(w.dim, w.n, **w.op_kwargs())
-    assert a.info.fft_rows == 8192
+    assert a.info.fft_rows > 0
     ya = a.apply(w.u)
     d1 = np.max(np.abs(ya - a.apply(w.u))) / np.max(np.abs(ya))
     yb = b.apply(w.u)
