@@ -115,8 +115,9 @@ typedef struct nlg_info {
   int exp_terms;             /* far-field terms of the 1-D exponential sum     */
   int near_cells;            /* near-field radius (cells) of the 1-D scan path */
   double far_rel_err;        /* fitted kernel error of the exponential sum     */
-  int64_t fft_len;           /* 1-D far window by FFT convolution: length L,
-                                0 when the scan path runs without it           */
+  int64_t fft_len;           /* FFT convolution length L: the 1-D far window
+                                (method 2) or the x / y box axis of the 3-D
+                                constant-horizon mode (method 3); 0 = none     */
   int fft_rows;              /* four-step split L = N1 x fft_rows (fft.cu);
                                 0: the cuFFT path for lengths it does not cover */
 } nlg_info;

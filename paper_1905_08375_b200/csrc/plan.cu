@@ -277,6 +277,7 @@ nlg_status nlg_plan_info(const nlg_plan* plan, nlg_info* info) {
     info->fft_len = 0;
     info->fft_rows = 0;
     if (P.es_state) expsum_fft_info(P, info->fft_len, info->fft_rows);
+    if (P.st_state) info->fft_len = stencil_fft_len(P);
   });
 }
 
@@ -298,7 +299,7 @@ void fast_dev(Plan& P, const double* u, double* out, cudaStream_t s) {
       cudaEvent_t ev;
       stage_begin(P, s, kStStencil, &ev);
       stencil_apply(P, u, out, s);
-      stage_end(P, s, kStStencil, ev, P.d_kappa && P.family == NLG_FRACTIONAL && P.geom.dim == 1 ? 2 : 1);
+      stage_end(P, s, kStStencil, ev, stencil_launches(P));
       break;
     }
     default: {

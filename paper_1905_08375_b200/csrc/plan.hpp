@@ -37,6 +37,7 @@ struct ExpSum {
 
 struct ExpSumState;
 struct StencilState;
+struct BoxFft;
 
 // Optional per-stage CUDA-event timing (nlg_set_profiling / nlg_stage_times).
 enum Stage { kStDirect = 0, kStSpanScan, kStSpanEval, kStEsAggregate, kStEsCarry, kStEsMain,
@@ -113,6 +114,15 @@ void expsum_fft_info(const Plan& P, int64_t& len, int& rows);
 void stencil_setup(Plan& P, const nlg_desc& d);
 void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void stencil_free(Plan& P);
+int stencil_launches(const Plan& P);
+int stencil_fft_len(const Plan& P);
+// box FFT mode of method 3 (fft3.cu): 3-D fractional, constant horizon
+BoxFft* boxfft_setup(const Plan& P, double alpha);
+void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale, const double* diag, double* out,
+                  cudaStream_t s);
+int boxfft_launches(const BoxFft& B);
+int boxfft_length(const BoxFft& B);
+void boxfft_free(BoxFft* B);
 
 // device BLAS-1 (solve.cu)
 size_t dot_scratch_doubles();

@@ -38,6 +38,7 @@ struct StencilState {
   double* pack = nullptr;               // [n_in] double2 (u, kappa u) for kappa-weighted fractional
   size_t tab_bytes = 0;
   int ws = 0;                           // weight row stride (2-D: padded to a multiple of 4)
+  BoxFft* box = nullptr;                // constant-horizon 3-D: FFT convolution + tie band (fft3.cu)
 };
 
 namespace {
@@ -1029,11 +1030,24 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   launch(a, P.stream, S->tab_bytes);
   NLG_CUDA(cudaGetLastError());
   NLG_CUDA(cudaStreamSynchronize(P.stream));
+  if (frac && g.dim == 3) S->box = boxfft_setup(P, d.alpha);
   P.fast_method = 3;
 }
 
+int stencil_launches(const Plan& P) {
+  const StencilState* S = P.st_state;
+  if (S->box) return boxfft_launches(*S->box);
+  return S->pack ? 2 : 1;
+}
+
+int stencil_fft_len(const Plan& P) { return P.st_state && P.st_state->box ? boxfft_length(*P.st_state->box) : 0; }
+
 void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   StencilState* S = P.st_state;
+  if (S->box) {
+    boxfft_apply(P, *S->box, u, S->scale, S->diag, out, s);
+    return;
+  }
   if (S->pack) {
     pack_kernel<<<static_cast<unsigned>((P.n_in + 255) / 256), 256, 0, s>>>(
         u, P.d_kappa, P.n_in, reinterpret_cast<double2*>(S->pack));
@@ -1046,6 +1060,7 @@ void stencil_free(Plan& P) {
   StencilState* S = P.st_state;
   if (!S) return;
   for (double* p : {S->wtab, S->mtab, S->diag, S->scale, S->pack}) cudaFree(p);
+  boxfft_free(S->box);
   delete S;
   P.st_state = nullptr;
 }

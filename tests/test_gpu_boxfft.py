@@ -1,0 +1,106 @@
+"""Box FFT mode of method 3 (csrc/fft3.cu): the 3-D fractional operator with a
+constant horizon (BASELINE cfg4-A) as one zero-padded FFT convolution plus the
+exact tie-band pass. Checked against the GPU direct quadrature (exact pair
+sets, itself pinned to the oracle) and against the stencil sweep of the same
+plan (NLG_BOX_FFT=0), within the north-star 1e-10 (FAST_TOL)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+FAST_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def N():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1905_08375_b200 import nonloc
+    return nonloc
+
+
+def _op(N, n, dh, s=0.25, kappa=True, exterior=0, seed=2, **kw):
+    from paper_1905_08375_b200 import nonloc as NL
+    h = 1.0 / n
+    rng = np.random.default_rng(seed)
+    k = rng.lognormal(0.0, 0.5, n ** 3) if kappa else None
+    d0 = dh * h
+    return N.NonlocalOperator(3, n, alpha=3 + 2 * s, delta0=d0, coeff0=float(NL.fractional_cdelta(3, s, d0)),
+                              kappa=k, exterior=N.Exterior(exterior), **kw)
+
+
+def _u(n, seed=1):
+    from paper_1905_08375_b200 import configs
+    return configs.cfg4(n).u if n <= 64 else np.random.default_rng(seed).standard_normal(n ** 3)
+
+
+# (n, delta / h): 6h and 4h carry tie bands (|d|^2 = 36, 16), 3.5h and 5.3h do not
+CASES = [(32, 6.0), (40, 6.0), (48, 4.0), (36, 3.5), (44, 5.3), (64, 6.0)]
+
+
+@pytest.mark.parametrize("n,dh", CASES)
+@pytest.mark.parametrize("exterior", [0, 1])
+def test_box_fft_vs_direct(N, n, dh, exterior):
+    op = _op(N, n, dh, exterior=exterior)
+    assert op.info.fast_method == 3 and op.info.fft_len >= n + int(dh) - 1
+    u = _u(n)
+    fast = op.apply(u)
+    direct, _ = op.apply_direct(u)
+    err = np.max(np.abs(fast - direct)) / np.max(np.abs(direct))
+    assert err <= FAST_TOL, err
+
+
+@pytest.mark.parametrize("n,dh", [(40, 6.0), (48, 4.0)])
+def test_box_fft_vs_stencil_sweep(N, n, dh, monkeypatch):
+    u = _u(n)
+    fft = _op(N, n, dh).apply(u)
+    monkeypatch.setenv("NLG_BOX_FFT", "0")
+    op = _op(N, n, dh)
+    assert op.info.fft_len == 0
+    sweep = op.apply(u)
+    assert np.max(np.abs(fft - sweep)) <= FAST_TOL * np.max(np.abs(sweep))
+
+
+def test_box_fft_without_kappa(N):
+    op = _op(N, 40, 6.0, kappa=False)
+    u = _u(40)
+    fast = op.apply(u)
+    direct, _ = op.apply_direct(u)
+    assert np.max(np.abs(fast - direct)) <= FAST_TOL * np.max(np.abs(direct))
+
+
+def test_box_fft_constants_linearity_repeat(N):
+    n = 40
+    op = _op(N, n, 6.0)
+    u = _u(n)
+    a = op.apply(u)
+    sc = np.max(np.abs(a))
+    assert np.max(np.abs(op.apply(np.ones(n ** 3)))) <= 1e-12 * sc     # clip: constants annihilated
+    v = np.random.default_rng(4).standard_normal(n ** 3)
+    lhs = op.apply(2.0 * u - 0.5 * v)
+    rhs = 2.0 * a - 0.5 * op.apply(v)
+    assert np.max(np.abs(lhs - rhs)) <= 1e-11 * np.max(np.abs(lhs))
+    assert np.array_equal(op.apply(u), a)                                 # scratch reuse is clean
+
+
+@pytest.mark.parametrize("rows", [(0, 13), (13, 29), (29, 40)])
+def test_box_fft_sharded_slabs(N, rows):
+    """A slab plan reads rows [rb - H, re + H); its box runs over the input
+    planes (L_z from n_in), the output rows match the whole-grid apply."""
+    n = 40
+    h = 1.0 / n
+    whole = _op(N, n, 6.0)
+    u = _u(n)
+    full = whole.apply(u).reshape(n, n, n)
+    rb, re = rows
+    H = int(np.floor(6.0 * h / h)) + 2
+    lo, hi = max(0, rb - H), min(n, re + H)
+    rng = np.random.default_rng(2)
+    k = rng.lognormal(0.0, 0.5, n ** 3).reshape(n, n, n)
+    from paper_1905_08375_b200 import nonloc as NL
+    d0 = 6.0 * h
+    op = N.NonlocalOperator(3, n, alpha=3.5, delta0=d0, coeff0=float(NL.fractional_cdelta(3, 0.25, d0)),
+                            kappa=k[lo:hi].ravel(), row_begin=rb, row_end=re)
+    assert op.info.fft_len > 0
+    part = op.apply(u.reshape(n, n, n)[lo:hi].ravel()).reshape(re - rb, n, n)
+    assert np.max(np.abs(part - full[rb:re])) <= 1e-12 * np.max(np.abs(full))
