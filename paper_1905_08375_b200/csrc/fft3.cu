@@ -8,7 +8,7 @@
 //   A_i = sum_{d in N} w(d) u_{i+d},   B_i = sum_{d in N} w(d) (kappa u)_{i+d}
 // is a convolution of f = u + i kappa u (two real fields in one complex
 // signal) with the real, even kernel w(d) = |d|^-alpha. On a zero-padded box
-// L_z x L_y x L_x (L_j >= extent + r_f, 2^a 3^b) it runs in five HBM passes,
+// L_z x L_y x L_x (L_j >= extent + r_f, 2^a 3^b 5^c) it runs in five HBM passes,
 // each a Stockham transform in shared memory (stockham.cuh):
 //   PA  f3_rows<fwd>  : rows (z, y): load u, kappa (the packing), FFT_x -> Z
 //   PB  f3_cols       : columns along y (8 kx per CTA): FFT_y
@@ -37,8 +37,19 @@
 
 namespace nlg {
 
+constexpr int kTieTX = 32, kTieTY = 8, kTieZC = 64, kMaxTie = 64, kMaxTieR = 16;
+
+struct TieGroups {
+  int R, q, ngroup, ntie;   // q: gcd of the t0's (planes z + t0 share z's class mod q)
+  int t0[2 * kMaxTieR + 1];
+  int beg[2 * kMaxTieR + 2];
+  int t1[kMaxTie], t2[kMaxTie];   // ties in t0 order; bit k = k-th tie
+  int off[kMaxTie];               // t1 W + t2: offset in the staged window (f3_ties)
+};
+
 struct BoxFft {
   int lx = 0, ly = 0, lz = 0, rf = 0;
+  int cols = 4;                                     // columns per CTA of the strided passes (NLG_F3_COLS)
   int64_t n = 0, n_in = 0, o0 = 0, rows_out = 0;   // z: input planes, first output plane, output planes
   double2* z = nullptr;                             // [n_in][ly][lx]
   double2* twx = nullptr;                           // [lx] exp(-2 pi i t / lx)
@@ -46,23 +57,27 @@ struct BoxFft {
   double2* twz = nullptr;
   double* cz = nullptr;                             // [lz] cos(2 pi t / lz)
   double* g = nullptr;                              // [ly][lx][rf + 1] partial spectra / (lx ly lz)
-  int ntie = 0;
-  int4* tie = nullptr;                              // (t0, t1, t2, 0) tie-band offsets
-  double* tiew = nullptr;                           // w(t)
-  double thr = 0.0;                                 // r2 < thr  <=>  sqrt_rn(r2) < delta
+  int ntie = 0;                                     // tie-band offsets (all |t|^2 = m)
+  TieGroups tg{};                                   // ties grouped by t0 (f3_ties)
+  int tie_m = 0;                                    // |t|^2 of the band
+  double tie_w = 0.0;                               // w_m
+  double tie_thr = 0.0;                             // r2 < thr  <=>  sqrt_rn(r2) < delta
+  void* tie_mask = nullptr;                         // [n_out] per-target inclusion bits (uint32 / uint64)
 };
 
 namespace {
 
 using namespace stockham;
 
-constexpr int kF3Cols = 8;   // columns per CTA in the strided passes (128-byte row pieces)
+// Strided passes: C = 4 columns per CTA (64-byte row pieces, two CTAs per SM: 3.6 ms per y pass at
+// 768^3 against 5.2 ms for C = 8 with one CTA per SM); NLG_F3_COLS=8 (plan time) selects 8.
+constexpr int kF3Cols = 8;
 constexpr int kF3El = 8;     // elements per thread per stage
 
 template <int L>
 __host__ __device__ constexpr int rows_threads() { return L / kF3El < 32 ? 32 : (L / kF3El > 128 ? 128 : L / kF3El); }
-template <int L>
-__host__ __device__ constexpr int cols_threads3() { return L * kF3Cols / kF3El; }
+template <int L, int C>
+__host__ __device__ constexpr int cols_threads3() { return L * C / kF3El; }
 
 struct F3Args {
   int64_t n, n_in, o0, rows_out;
@@ -75,7 +90,8 @@ struct F3Args {
   double2* z;
   const double* u;       // [n_in rows]
   const double* kappa;   // or null
-  const double* scale;   // [n_out]
+  const double* scale;   // [n_out], or null: scale0 everywhere (constant coefficient)
+  double scale0;
   const double* diag;    // [n_out]
   double* out;           // [n_out]
 };
@@ -117,7 +133,8 @@ __global__ void __launch_bounds__(rows_threads<L>()) f3_rows(const __grid_consta
         if (x < a.n) {
           const double A = v[q].x, B = -v[q].y;      // conjugate: (conv u, conv kappa u)
           const double X = KW ? fma(__ldg(a.kappa + ii + x), A, B) : A;
-          a.out[oi + x] = __ldg(a.scale + oi + x) * (X - __ldg(a.u + ii + x) * __ldg(a.diag + oi + x));
+          const double sc = a.scale ? __ldg(a.scale + oi + x) : a.scale0;
+          a.out[oi + x] = sc * (X - __ldg(a.u + ii + x) * __ldg(a.diag + oi + x));
         }
       }
     };
@@ -127,9 +144,9 @@ __global__ void __launch_bounds__(rows_threads<L>()) f3_rows(const __grid_consta
 
 // PB / PD: kF3Cols adjacent kx columns along y in one plane. PB reads y < n
 // (zero padding above) and writes every ky; PD reads every ky and writes y < n.
-template <int L, bool PD>
-__global__ void __launch_bounds__(cols_threads3<L>(), 1) f3_cols(const __grid_constant__ F3Args a) {
-  constexpr int T = cols_threads3<L>(), C = kF3Cols;
+template <int L, bool PD, int C>
+__global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_cols(const __grid_constant__ F3Args a) {
+  constexpr int T = cols_threads3<L, C>();
   extern __shared__ double2 fsm3[];
   const int tid = threadIdx.x;
   const int kx0 = blockIdx.x * C;
@@ -152,9 +169,9 @@ __global__ void __launch_bounds__(cols_threads3<L>(), 1) f3_cols(const __grid_co
 
 // PC: kF3Cols adjacent kx columns along z at one ky: forward FFT, x K^,
 // conjugate, forward FFT; planes [o0, o0 + rows_out) stored.
-template <int L>
-__global__ void __launch_bounds__(cols_threads3<L>(), 1) f3_zconv(const __grid_constant__ F3Args a) {
-  constexpr int T = cols_threads3<L>(), C = kF3Cols;
+template <int L, int C>
+__global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_zconv(const __grid_constant__ F3Args a) {
+  constexpr int T = cols_threads3<L, C>();
   extern __shared__ double2 fsm3[];
   double* gs = reinterpret_cast<double*>(fsm3 + L * C);   // [C][rf + 1]
   double* cs = gs + C * (a.rf + 1);                       // [L] cos table
@@ -224,52 +241,223 @@ __global__ void f3_spectrum(const double* __restrict__ w, int rf, int lx, int ly
   }
 }
 
-// Tie band: out_i += s_i (kappa_i At_i + Bt_i) over the tie offsets t that
-// the reference's predicate admits at target i (sources inside the domain).
+// Tie band. Every offset t of the band has the same |t|^2 = m, so one weight
+// w_m. Whether t belongs to N_i is the reference's float predicate (exactly as
+// stencil.cu point_in), decided once at plan time into a per-target bit mask
+// (f3_tie_mask, bit k = tie k, sources outside the domain never set).
+// f3_ties then adds  out_i += s_i w_m (kappa_i At_i + Bt_i),  At / Bt the sums
+// of u / kappa u over the set bits, sliding along z: a CTA owns a 32 x 8
+// column of targets over a chunk of planes of one residue class mod q (q =
+// gcd of the tie t0's, 2 at delta = 6h: the sources of plane z are the planes
+// z + t0 of the same class). The source planes z - R .. z + R of the class sit
+// in a shared-memory ring of NS = 2R/q + 1 staged windows (with an R-cell
+// halo, as (u, kappa u) pairs; slot HH W of each reads as zero); each step
+// stages ONE new plane, so the L2 traffic per target is ~ (8 + 2R)(32 + 2R) /
+// 256 staged pairs instead of one per (target, tie). An excluded tie reads the
+// zero slot: no select on the sums.
 struct TieArgs {
   Geom g;
-  int ntie;
-  const int4* tie;
-  const double* tiew;
-  double thr;
+  TieGroups tg;
+  double w;              // w_m
+  double thr;            // r2 < thr  <=>  sqrt_rn(r2) < delta
+  const void* mask;      // [n_out] uint32 / uint64
   const double* u;
   const double* kappa;
-  const double* scale;
+  const double* scale;   // or null: scale0
+  double scale0;
   double* out;
 };
 
-template <bool KW>
-__global__ void __launch_bounds__(256) f3_ties(const __grid_constant__ TieArgs a) {
+template <typename MT>
+__global__ void f3_tie_mask(const __grid_constant__ TieArgs a, MT* __restrict__ mask) {
   const Geom& g = a.g;
   const int64_t n = g.n;
   const int64_t x = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
   const int64_t y = static_cast<int64_t>(blockIdx.y) * 8 + threadIdx.y;
-  const int64_t z = g.row_begin + blockIdx.z;        // global plane
+  const int64_t z = g.row_begin + blockIdx.z;
   if (x >= n || y >= n) return;
   const double h = g.h;
   const double cz = coord(z, h), cy = coord(y, h), cx = coord(x, h);
-  const int64_t ii = ((z - g.in_begin) * n + y) * n + x;
-  double At = 0.0, Bt = 0.0;
-  for (int t = 0; t < a.ntie; ++t) {
-    const int4 d = __ldg(a.tie + t);
-    const int64_t sz = z + d.x, sy = y + d.y, sx = x + d.z;
-    if (sz < 0 || sz >= n || sy < 0 || sy >= n || sx < 0 || sx >= n) continue;
-    const double d0 = __dsub_rn(coord(sz, h), cz), d1 = __dsub_rn(coord(sy, h), cy), d2 = __dsub_rn(coord(sx, h), cx);
-    const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
-    if (!(r2 < a.thr)) continue;
-    const int64_t si = ii + (static_cast<int64_t>(d.x) * n + d.y) * n + d.z;
-    const double w = __ldg(a.tiew + t), us = __ldg(a.u + si);
-    At = fma(w, us, At);
-    if (KW) Bt = fma(w, us * __ldg(a.kappa + si), Bt);
+  MT m = 0;
+  for (int gi = 0; gi < a.tg.ngroup; ++gi) {
+    const int64_t sz = z + a.tg.t0[gi];
+    if (sz < 0 || sz >= n) continue;
+    const double d0 = __dsub_rn(coord(sz, h), cz);
+    for (int k = a.tg.beg[gi]; k < a.tg.beg[gi + 1]; ++k) {
+      const int64_t sy = y + a.tg.t1[k], sx = x + a.tg.t2[k];
+      if (sy < 0 || sy >= n || sx < 0 || sx >= n) continue;
+      const double d1 = __dsub_rn(coord(sy, h), cy), d2 = __dsub_rn(coord(sx, h), cx);
+      const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+      if (r2 < a.thr) m |= static_cast<MT>(1) << k;
+    }
   }
-  const int64_t oi = ii - (g.row_begin - g.in_begin) * n * n;
-  const double X = KW ? fma(__ldg(a.kappa + ii), At, Bt) : At;
-  if (X != 0.0) a.out[oi] = fma(__ldg(a.scale + oi), X, a.out[oi]);
+  mask[((z - g.row_begin) * n + y) * n + x] = m;
 }
 
-// supported axis lengths 2^a 3^b (multiples of kF3Cols, <= 1024 threads per column CTA)
+constexpr int kTieStage = 4;   // staged (u, kappa) pairs per thread per plane: (8 + 2R)(32 + 2R) <= 1024
+
+// Compile-time tie set of |t|^2 = M, in the host's order (dz, dy, dx ascending).
+struct TieSet {
+  int n = 0, R = 0, q = 0;
+  int t0[kMaxTie] = {}, t1[kMaxTie] = {}, t2[kMaxTie] = {};
+};
+__host__ __device__ constexpr TieSet make_ties(int M) {
+  TieSet s{};
+  while ((s.R + 1) * (s.R + 1) <= M) ++s.R;
+  for (int dz = -s.R; dz <= s.R; ++dz)
+    for (int dy = -s.R; dy <= s.R; ++dy)
+      for (int dx = -s.R; dx <= s.R; ++dx)
+        if (dz * dz + dy * dy + dx * dx == M && s.n < kMaxTie) {
+          s.t0[s.n] = dz;
+          s.t1[s.n] = dy;
+          s.t2[s.n] = dx;
+          ++s.n;
+        }
+  for (int k = 0; k < s.n; ++k) {   // gcd of the t0's
+    int a = s.t0[k] < 0 ? -s.t0[k] : s.t0[k], b = s.q;
+    while (b) { const int t = a % b; a = b; b = t; }
+    s.q = a;
+  }
+  if (s.q == 0) s.q = 1;
+  return s;
+}
+constexpr int kTieFixedM = 36;   // the BASELINE cfg4-A band (delta = 6h): specialised, fully unrolled
+
+// @p A += v  (a predicated DADD: no select on the sum)
+__device__ __forceinline__ void padd(double& acc, double v, unsigned bit) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q add.rn.f64 %0, %0, %1;\n\t}" : "+d"(acc) : "d"(v), "r"(bit));
+}
+
+// M > 0: the tie set of |t|^2 = M at compile time (offsets, slots and mask
+// bits are immediates); M = 0: the runtime set in a.tg.
+template <int M, bool KW, typename MT>
+__global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant__ TieArgs a) {
+  extern __shared__ __align__(16) double2 tsm[];
+  const Geom& g = a.g;
+  const int n = static_cast<int>(g.n);
+  const int64_t nn = g.n * g.n;
+  constexpr TieSet TS = make_ties(M);
+  const int R = M ? TS.R : a.tg.R, q = M ? TS.q : a.tg.q, NS = 2 * R / q + 1;
+  const int W = kTieTX + 2 * R, SB = (kTieTY + 2 * R) * W, SL = SB + 1;   // slot stride; [SB] = 0
+  constexpr int NT = kTieTX * kTieTY;
+  const int tid = threadIdx.y * kTieTX + threadIdx.x;
+  const int x0 = blockIdx.x * kTieTX, y0 = blockIdx.y * kTieTY;
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  const bool live = x < n && y < n;
+  const int cls = blockIdx.z % q;
+  (void)cls;
+  const int zb = static_cast<int>(g.row_begin) + static_cast<int>(blockIdx.z / q) * kTieZC;
+  const int ze = min(static_cast<int>(g.row_end), zb + kTieZC);
+  int zf = zb + ((cls - zb) % q + q) % q;                 // first target plane of the class
+  if (zf >= ze) return;
+  const MT* mask = static_cast<const MT*>(a.mask);
+  const int tgt = y * n + x;
+  const int sbase = (threadIdx.y + R) * W + threadIdx.x + R;
+  for (int sl = tid; sl < NS; sl += NT) tsm[sl * SL + SB] = make_double2(0.0, 0.0);
+  int soff[kTieStage];
+  bool sok[kTieStage];
+#pragma unroll
+  for (int k = 0; k < kTieStage; ++k) {
+    const int e = tid + k * NT;
+    const int r = e / W, c = e - r * W;
+    const int gy = y0 - R + r, gx = x0 - R + c;
+    sok[k] = e < SB && gy >= 0 && gy < n && gx >= 0 && gx < n;
+    soff[k] = sok[k] ? gy * n + gx : 0;
+  }
+  double su[kTieStage], sk[kTieStage];
+  auto prefetch = [&](int p) {
+    const bool pin = p >= 0 && p < n;
+    const double* up = a.u + (static_cast<int64_t>(p) - g.in_begin) * nn;
+    const double* kp = KW ? a.kappa + (static_cast<int64_t>(p) - g.in_begin) * nn : nullptr;
+#pragma unroll
+    for (int k = 0; k < kTieStage; ++k) {
+      su[k] = 0.0;
+      sk[k] = 0.0;
+      if (pin && sok[k]) {
+        su[k] = __ldg(up + soff[k]);
+        if (KW) sk[k] = __ldg(kp + soff[k]);
+      }
+    }
+  };
+  auto put = [&](int slot) {
+    double2* st = tsm + slot * SL;
+#pragma unroll
+    for (int k = 0; k < kTieStage; ++k) {
+      const int e = tid + k * NT;
+      if (e < SB) st[e] = make_double2(su[k], KW ? su[k] * sk[k] : 0.0);
+    }
+  };
+  // ring: plane zf - R + i q lives in slot i mod NS; fill i = 0 .. NS - 2
+  for (int i = 0; i + 1 < NS; ++i) {
+    prefetch(zf - R + i * q);
+    put(i);
+  }
+  prefetch(zf + R);
+  int head = 0;                                           // slot of plane zt - R
+  for (int zt = zf; zt < ze; zt += q) {
+    const int snew = head == 0 ? NS - 1 : head - 1;       // slot of plane zt + R (held plane zt - R - q)
+    __syncthreads();                                      // previous step's reads of that slot are done
+    put(snew);
+    const int64_t ii = (static_cast<int64_t>(zt) - g.in_begin) * nn + tgt;
+    const int64_t oi = (static_cast<int64_t>(zt) - g.row_begin) * nn + tgt;
+    MT m = 0;
+    double ek = 0.0, es = 0.0, eo = 0.0;
+    if (live) {
+      m = __ldg(mask + oi);
+      if (KW) ek = __ldg(a.kappa + ii);
+      es = a.scale ? __ldg(a.scale + oi) : a.scale0;
+      eo = a.out[oi];
+    }
+    __syncthreads();
+    if (zt + q < ze) prefetch(zt + q + R);                // next plane in flight during the sums
+    double A = 0.0, B = 0.0;
+    if (m) {
+      if constexpr (M > 0) {
+        constexpr int kNS = 2 * TS.R / TS.q + 1;
+        const double2* slot[kNS];
+#pragma unroll
+        for (int r = 0; r < kNS; ++r) slot[r] = tsm + (head + r < kNS ? head + r : head + r - kNS) * SL + sbase;
+        const double2* zero = tsm + SB;                 // slot 0's zero element
+        double A1 = 0.0, B1 = 0.0;                      // two chains per field
+#pragma unroll
+        for (int k = 0; k < TS.n; ++k) {                // an excluded tie reads the zero element
+          const double2* src = slot[(TS.t0[k] + TS.R) / TS.q] + TS.t1[k] * (kTieTX + 2 * TS.R) + TS.t2[k];
+          const double2 v = *((m & (1u << k)) ? src : zero);
+          if (k & 1) {
+            A1 += v.x;
+            if (KW) B1 += v.y;
+          } else {
+            A += v.x;
+            if (KW) B += v.y;
+          }
+        }
+        A += A1;
+        B += B1;
+      } else {
+        for (int gi = 0; gi < a.tg.ngroup; ++gi) {
+          int sl = head + (a.tg.t0[gi] + R) / q;
+          sl = sl >= NS ? sl - NS : sl;
+          const double2* st = tsm + sl * SL;
+          const int kb = a.tg.beg[gi], kend = a.tg.beg[gi + 1];
+#pragma unroll 4
+          for (int k = kb; k < kend; ++k) {             // an excluded tie reads the zero slot
+            const double2 v = st[(m >> k) & 1 ? sbase + a.tg.off[k] : SB];
+            A += v.x;
+            B += v.y;
+          }
+        }
+      }
+      const double X = KW ? fma(ek, A, B) : A;
+      a.out[oi] = fma(es * a.w, X, eo);
+    }
+    head = head + 1 == NS ? 0 : head + 1;
+  }
+}
+
+// supported axis lengths 2^a 3^b 5^c (multiples of kF3Cols, <= 1024 threads per column CTA)
 #define NLG_F3_L(X) \
-  X(48) X(64) X(72) X(96) X(128) X(144) X(192) X(256) X(288) X(384) X(512) X(576) X(768) X(864) X(1024)
+  X(48) X(64) X(72) X(80) X(96) X(128) X(144) X(160) X(192) X(256) X(288) X(384) X(400) X(512) X(576) X(768) \
+  X(800) X(864) X(1024)
 
 bool f3_supported(int L) {
 #define NLG_F3_CASE(N) if (L == N) return true;
@@ -279,23 +467,28 @@ bool f3_supported(int L) {
 }
 
 int f3_length(int64_t need) {
-  const int c[] = {48, 64, 72, 96, 128, 144, 192, 256, 288, 384, 512, 576, 768, 864, 1024};
+  const int c[] = {48, 64, 72, 80, 96, 128, 144, 160, 192, 256, 288, 384, 400, 512, 576, 768, 800, 864, 1024};
   for (int L : c)
     if (L >= need) return L;
   return 0;
 }
 
-template <int L>
-size_t cols_smem3() { return sizeof(double2) * L * kF3Cols; }
+template <int L, int C>
+size_t cols_smem3() { return sizeof(double2) * L * C; }
 
+template <int L, int C>
+void f3_attr_c(int rf) {
+  NLG_CUDA(cudaFuncSetAttribute(f3_cols<L, false, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(cols_smem3<L, C>())));
+  NLG_CUDA(cudaFuncSetAttribute(f3_cols<L, true, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(cols_smem3<L, C>())));
+  NLG_CUDA(cudaFuncSetAttribute(f3_zconv<L, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(cols_smem3<L, C>() + sizeof(double) * (C * (rf + 1) + L))));
+}
 template <int L>
 void f3_attr(int rf) {
-  NLG_CUDA(cudaFuncSetAttribute(f3_cols<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(cols_smem3<L>())));
-  NLG_CUDA(cudaFuncSetAttribute(f3_cols<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(cols_smem3<L>())));
-  NLG_CUDA(cudaFuncSetAttribute(f3_zconv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(cols_smem3<L>() + sizeof(double) * (kF3Cols * (rf + 1) + L))));
+  f3_attr_c<L, 8>(rf);
+  f3_attr_c<L, 4>(rf);
 }
 
 template <int L>
@@ -311,18 +504,28 @@ void launch_rows(const F3Args& a, bool inv, int64_t rows, cudaStream_t s) {
   }
 }
 
+template <int L, int C>
+void launch_cols_c(const F3Args& a, bool pd, int64_t planes, cudaStream_t s) {
+  const dim3 grid(static_cast<unsigned>(a.lx / C), static_cast<unsigned>(planes));
+  if (pd) f3_cols<L, true, C><<<grid, cols_threads3<L, C>(), cols_smem3<L, C>(), s>>>(a);
+  else f3_cols<L, false, C><<<grid, cols_threads3<L, C>(), cols_smem3<L, C>(), s>>>(a);
+}
 template <int L>
-void launch_cols(const F3Args& a, bool pd, int64_t planes, cudaStream_t s) {
-  const dim3 grid(static_cast<unsigned>(a.lx / kF3Cols), static_cast<unsigned>(planes));
-  if (pd) f3_cols<L, true><<<grid, cols_threads3<L>(), cols_smem3<L>(), s>>>(a);
-  else f3_cols<L, false><<<grid, cols_threads3<L>(), cols_smem3<L>(), s>>>(a);
+void launch_cols(const F3Args& a, int cols, bool pd, int64_t planes, cudaStream_t s) {
+  if (cols == 4) launch_cols_c<L, 4>(a, pd, planes, s);
+  else launch_cols_c<L, 8>(a, pd, planes, s);
 }
 
+template <int L, int C>
+void launch_zconv_c(const F3Args& a, cudaStream_t s) {
+  const dim3 grid(static_cast<unsigned>(a.lx / C), static_cast<unsigned>(a.ly));
+  const size_t sb = cols_smem3<L, C>() + sizeof(double) * (C * (a.rf + 1) + L);
+  f3_zconv<L, C><<<grid, cols_threads3<L, C>(), sb, s>>>(a);
+}
 template <int L>
-void launch_zconv(const F3Args& a, cudaStream_t s) {
-  const dim3 grid(static_cast<unsigned>(a.lx / kF3Cols), static_cast<unsigned>(a.ly));
-  const size_t sb = cols_smem3<L>() + sizeof(double) * (kF3Cols * (a.rf + 1) + L);
-  f3_zconv<L><<<grid, cols_threads3<L>(), sb, s>>>(a);
+void launch_zconv(const F3Args& a, int cols, cudaStream_t s) {
+  if (cols == 4) launch_zconv_c<L, 4>(a, s);
+  else launch_zconv_c<L, 8>(a, s);
 }
 
 std::vector<double2> twiddles3(int n) {
@@ -367,6 +570,7 @@ F3Args args_of(const Plan& P, const BoxFft& B) {
   a.u = nullptr;
   a.kappa = P.d_kappa;
   a.scale = nullptr;
+  a.scale0 = 0.0;
   a.diag = nullptr;
   a.out = nullptr;
   return a;
@@ -377,6 +581,21 @@ double sqrt_threshold_host(double delta) {
   double t = delta * delta;
   while (t > 0.0 && std::sqrt(t) >= delta) t = std::nextafter(t, 0.0);
   while (std::sqrt(t) < delta) t = std::nextafter(t, 1e300);
+  return t;
+}
+
+TieArgs tie_args(const Plan& P, const BoxFft& B) {
+  TieArgs t;
+  t.g = P.geom;
+  t.tg = B.tg;
+  t.w = B.tie_w;
+  t.thr = B.tie_thr;
+  t.mask = B.tie_mask;
+  t.u = nullptr;
+  t.kappa = P.d_kappa;
+  t.scale = nullptr;
+  t.scale0 = 0.0;
+  t.out = nullptr;
   return t;
 }
 
@@ -404,6 +623,7 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   B->lx = B->ly = lx;
   B->lz = lz;
   B->rf = rf;
+  if (const char* ce = std::getenv("NLG_F3_COLS")) B->cols = std::atoi(ce) == 8 ? 8 : 4;
   B->n = n;
   B->n_in = n_in;
   B->o0 = P.halo_lo;
@@ -416,23 +636,56 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
         const int m = dz * dz + dy * dy + dx * dx;
         if (m > 0 && m < mlo) w[(dz * G + dy) * G + dx] = std::pow(static_cast<double>(m), -0.5 * alpha);
       }
-  std::vector<int4> ties;
-  std::vector<double> tw;
+  // tie band: one |t|^2 = m (the band is narrower than 1), grouped by t0
   if (mlo <= mhi) {
-    const int R = static_cast<int>(std::floor(std::sqrt(static_cast<double>(mhi)))) + 1;
+    TieGroups& tg = B->tg;
+    const int m = mlo;
+    const int R = static_cast<int>(std::floor(std::sqrt(static_cast<double>(m)) + 1e-9));
+    std::vector<int> t0s, t1s, t2s;
     for (int dz = -R; dz <= R; ++dz)
       for (int dy = -R; dy <= R; ++dy)
-        for (int dx = -R; dx <= R; ++dx) {
-          const int m = dz * dz + dy * dy + dx * dx;
-          if (m < mlo || m > mhi) continue;
-          ties.push_back(make_int4(dz, dy, dx, 0));
-          tw.push_back(std::pow(static_cast<double>(m), -0.5 * alpha));
-        }
+        for (int dx = -R; dx <= R; ++dx)
+          if (dz * dz + dy * dy + dx * dx == m) {
+            t0s.push_back(dz);
+            t1s.push_back(dy);
+            t2s.push_back(dx);
+          }
+    const int nt = static_cast<int>(t0s.size());
+    if (nt > kMaxTie || R > kMaxTieR || (kTieTY + 2 * R) * (kTieTX + 2 * R) > kTieStage * kTieTX * kTieTY) {   // outside the mask / ring capacity: keep the stencil sweep
+      delete B;
+      return nullptr;
+    }
+    tg.R = R;
+    tg.ntie = nt;
+    tg.ngroup = 0;
+    for (int k = 0; k < nt; ++k) {   // t0s is sorted (dz outermost)
+      if (tg.ngroup == 0 || tg.t0[tg.ngroup - 1] != t0s[k]) {
+        tg.t0[tg.ngroup] = t0s[k];
+        tg.beg[tg.ngroup] = k;
+        ++tg.ngroup;
+      }
+      tg.t1[k] = t1s[k];
+      tg.t2[k] = t2s[k];
+      tg.off[k] = t1s[k] * (kTieTX + 2 * R) + t2s[k];
+    }
+    tg.beg[tg.ngroup] = nt;
+    int q = 0;
+    for (int gi = 0; gi < tg.ngroup; ++gi) {
+      int a = std::abs(tg.t0[gi]), b = q;
+      while (b) { const int t = a % b; a = b; b = t; }
+      q = a;
+    }
+    tg.q = q == 0 ? 1 : q;
+    const size_t ring = sizeof(double2) * (2 * R / tg.q + 1) * ((kTieTY + 2 * R) * (kTieTX + 2 * R) + 1);
+    if (ring > 227 * 1024) {   // the plane ring does not fit in shared memory: keep the stencil sweep
+      delete B;
+      return nullptr;
+    }
+    B->ntie = nt;
+    B->tie_m = m;
+    B->tie_w = std::pow(static_cast<double>(m), -0.5 * alpha);
+    B->tie_thr = sqrt_threshold_host(P.delta0);
   }
-  B->ntie = static_cast<int>(ties.size());
-  B->thr = sqrt_threshold_host(P.delta0);
-  B->tie = upload3(ties);
-  B->tiew = upload3(tw);
   B->twx = upload3(twiddles3(lx));
   B->twy = B->twx;
   B->twz = lz == lx ? B->twx : upload3(twiddles3(lz));
@@ -449,6 +702,23 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   NLG_CUDA(cudaStreamSynchronize(P.stream));
   cudaFree(dw);
   cudaFree(cx);
+  if (B->ntie > 0) {
+    const bool wide = B->ntie > 32;
+    const size_t nmask = static_cast<size_t>(B->rows_out) * n * n;
+    NLG_CUDA(cudaMalloc(&B->tie_mask, nmask * (wide ? 8 : 4)));
+    TieArgs t = tie_args(P, *B);
+    const dim3 grid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((n + 7) / 8),
+                    static_cast<unsigned>(B->rows_out));
+    if (wide) f3_tie_mask<uint64_t><<<grid, dim3(32, 8), 0, P.stream>>>(t, static_cast<uint64_t*>(B->tie_mask));
+    else f3_tie_mask<uint32_t><<<grid, dim3(32, 8), 0, P.stream>>>(t, static_cast<uint32_t*>(B->tie_mask));
+    NLG_CUDA(cudaGetLastError());
+    NLG_CUDA(cudaStreamSynchronize(P.stream));
+    for (const void* f : {reinterpret_cast<const void*>(f3_ties<0, true, uint32_t>), reinterpret_cast<const void*>(f3_ties<0, false, uint32_t>),
+                          reinterpret_cast<const void*>(f3_ties<0, true, uint64_t>), reinterpret_cast<const void*>(f3_ties<0, false, uint64_t>),
+                          reinterpret_cast<const void*>(f3_ties<kTieFixedM, true, uint32_t>),
+                          reinterpret_cast<const void*>(f3_ties<kTieFixedM, false, uint32_t>)})
+      NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  }
 #define NLG_F3_CASE(N) \
   if (lx == N) f3_attr<N>(rf); \
   if (lz == N && lz != lx) f3_attr<N>(rf);
@@ -457,11 +727,12 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   return B;
 }
 
-void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale, const double* diag, double* out,
-                  cudaStream_t s) {
+void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
+                  double* out, cudaStream_t s) {
   F3Args a = args_of(P, B);
   a.u = u;
   a.scale = scale;
+  a.scale0 = scale0;
   a.diag = diag;
   a.out = out;
   const int lx = B.lx, lz = B.lz;
@@ -470,15 +741,15 @@ void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
 #define NLG_F3_CASE(N) \
-  if (lx == N) launch_cols<N>(a, false, B.n_in, s);
+  if (lx == N) launch_cols<N>(a, B.cols, false, B.n_in, s);
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
 #define NLG_F3_CASE(N) \
-  if (lz == N) launch_zconv<N>(a, s);
+  if (lz == N) launch_zconv<N>(a, B.cols, s);
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
 #define NLG_F3_CASE(N) \
-  if (lx == N) launch_cols<N>(a, true, B.rows_out, s);
+  if (lx == N) launch_cols<N>(a, B.cols, true, B.rows_out, s);
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
 #define NLG_F3_CASE(N) \
@@ -486,20 +757,28 @@ void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
   if (B.ntie > 0) {
-    TieArgs t;
-    t.g = P.geom;
-    t.ntie = B.ntie;
-    t.tie = B.tie;
-    t.tiew = B.tiew;
-    t.thr = B.thr;
+    TieArgs t = tie_args(P, B);
     t.u = u;
-    t.kappa = P.d_kappa;
     t.scale = scale;
+    t.scale0 = scale0;
     t.out = out;
-    const dim3 grid(static_cast<unsigned>((B.n + 31) / 32), static_cast<unsigned>((B.n + 7) / 8),
-                    static_cast<unsigned>(B.rows_out));
-    if (P.d_kappa) f3_ties<true><<<grid, dim3(32, 8), 0, s>>>(t);
-    else f3_ties<false><<<grid, dim3(32, 8), 0, s>>>(t);
+    const int R = B.tg.R, NS = 2 * R / B.tg.q + 1;
+    const bool wide = B.ntie > 32;
+    const size_t sb = sizeof(double2) * NS * ((kTieTY + 2 * R) * (kTieTX + 2 * R) + 1);
+    const dim3 grid(static_cast<unsigned>((B.n + kTieTX - 1) / kTieTX), static_cast<unsigned>((B.n + kTieTY - 1) / kTieTY),
+                    static_cast<unsigned>((B.rows_out + kTieZC - 1) / kTieZC * B.tg.q));
+    const dim3 blk(kTieTX, kTieTY);
+    const bool fixed = B.tie_m == kTieFixedM;
+    if (wide) {
+      if (P.d_kappa) f3_ties<0, true, uint64_t><<<grid, blk, sb, s>>>(t);
+      else f3_ties<0, false, uint64_t><<<grid, blk, sb, s>>>(t);
+    } else if (fixed) {
+      if (P.d_kappa) f3_ties<kTieFixedM, true, uint32_t><<<grid, blk, sb, s>>>(t);
+      else f3_ties<kTieFixedM, false, uint32_t><<<grid, blk, sb, s>>>(t);
+    } else {
+      if (P.d_kappa) f3_ties<0, true, uint32_t><<<grid, blk, sb, s>>>(t);
+      else f3_ties<0, false, uint32_t><<<grid, blk, sb, s>>>(t);
+    }
   }
 }
 
@@ -510,7 +789,7 @@ void boxfft_free(BoxFft* B) {
   if (!B) return;
   if (B->twz != B->twx) cudaFree(B->twz);
   for (void* p : {static_cast<void*>(B->twx), static_cast<void*>(B->cz), static_cast<void*>(B->g),
-                  static_cast<void*>(B->z), static_cast<void*>(B->tie), static_cast<void*>(B->tiew)})
+                  static_cast<void*>(B->z), B->tie_mask})
     cudaFree(p);
   delete B;
 }

@@ -118,8 +118,8 @@ int stencil_launches(const Plan& P);
 int stencil_fft_len(const Plan& P);
 // box FFT mode of method 3 (fft3.cu): 3-D fractional, constant horizon
 BoxFft* boxfft_setup(const Plan& P, double alpha);
-void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale, const double* diag, double* out,
-                  cudaStream_t s);
+void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
+                  double* out, cudaStream_t s);
 int boxfft_launches(const BoxFft& B);
 int boxfft_length(const BoxFft& B);
 void boxfft_free(BoxFft* B);

@@ -39,6 +39,8 @@ struct StencilState {
   size_t tab_bytes = 0;
   int ws = 0;                           // weight row stride (2-D: padded to a multiple of 4)
   BoxFft* box = nullptr;                // constant-horizon 3-D: FFT convolution + tie band (fft3.cu)
+  bool scale_const = false;             // no per-node coefficient: scale[i] == scale0
+  double scale0 = 0.0;
 };
 
 namespace {
@@ -1021,6 +1023,8 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
     sc[i] = frac ? (d.kappa ? 0.5 : 1.0) * hd * std::pow(g.h, -d.alpha) * c : -hd / g.h * c;
   }
   S->scale = upload_vec(sc);
+  S->scale_const = d.coeff == nullptr;
+  S->scale0 = sc.empty() ? 0.0 : sc[0];
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * P.n_out * (peri ? 3 : 1)));
   if (frac && d.kappa && g.dim == 1) NLG_CUDA(cudaMalloc(&S->pack, sizeof(double2) * P.n_in));
   P.st_state = S;
@@ -1045,7 +1049,7 @@ int stencil_fft_len(const Plan& P) { return P.st_state && P.st_state->box ? boxf
 void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   StencilState* S = P.st_state;
   if (S->box) {
-    boxfft_apply(P, *S->box, u, S->scale, S->diag, out, s);
+    boxfft_apply(P, *S->box, u, S->scale_const ? nullptr : S->scale, S->scale0, S->diag, out, s);
     return;
   }
   if (S->pack) {

@@ -51,6 +51,23 @@ struct Dft<4> {
   }
 };
 template <>
+struct Dft<5> {
+  __device__ __forceinline__ static void run(double2* v) {
+    constexpr double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;   // cos(2 pi / 5), cos(4 pi / 5)
+    constexpr double s1 = 0.95105651629515357212, s2 = 0.58778525229247312917;    // sin(2 pi / 5), sin(4 pi / 5)
+    const double2 t1 = cadd(v[1], v[4]), t2 = cadd(v[2], v[3]), t3 = csub(v[1], v[4]), t4 = csub(v[2], v[3]);
+    const double2 a1 = make_double2(fma(c2, t2.x, fma(c1, t1.x, v[0].x)), fma(c2, t2.y, fma(c1, t1.y, v[0].y)));
+    const double2 a2 = make_double2(fma(c1, t2.x, fma(c2, t1.x, v[0].x)), fma(c1, t2.y, fma(c2, t1.y, v[0].y)));
+    const double2 b1 = make_double2(fma(s2, t4.x, s1 * t3.x), fma(s2, t4.y, s1 * t3.y));
+    const double2 b2 = make_double2(fma(-s1, t4.x, s2 * t3.x), fma(-s1, t4.y, s2 * t3.y));
+    v[0] = cadd(v[0], cadd(t1, t2));
+    v[1] = cadd(a1, mul_mi(b1));   // a - i b
+    v[4] = csub(a1, mul_mi(b1));
+    v[2] = cadd(a2, mul_mi(b2));
+    v[3] = csub(a2, mul_mi(b2));
+  }
+};
+template <>
 struct Dft<8> {
   __device__ __forceinline__ static void run(double2* v) {
     constexpr double kC = 0.70710678118654752440;    // cos(pi / 4)
@@ -125,12 +142,13 @@ struct Dft<16> {
 template <bool PAD>
 __device__ __forceinline__ int sidx(int q) { return PAD ? q + (q >> 3) : q; }
 
-// Radix plans (compile time). Columns: a 9 (or 3) first, then 8s, then the
+// Radix plans (compile time). Columns: 9s (or a 3) first, then 5s, then 8s, then the
 // 4 / 2 remainder. Rows: 16s with the remainder second, so that the first and
 // last radix agree and the last forward stage fuses with the first inverse one.
 template <int N, int Ns>
 __host__ __device__ constexpr int fs_radix_cols() {
-  return (N / Ns) % 9 == 0 ? 9 : ((N / Ns) % 3 == 0 ? 3 : ((N / Ns) % 8 == 0 ? 8 : ((N / Ns) % 4 == 0 ? 4 : 2)));
+  return (N / Ns) % 9 == 0 ? 9
+         : ((N / Ns) % 3 == 0 ? 3 : ((N / Ns) % 5 == 0 ? 5 : ((N / Ns) % 8 == 0 ? 8 : ((N / Ns) % 4 == 0 ? 4 : 2))));
 }
 __host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 // rows: radix EL (elements per thread), the remainder second

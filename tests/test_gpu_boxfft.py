@@ -34,8 +34,10 @@ def _u(n, seed=1):
     return configs.cfg4(n).u if n <= 64 else np.random.default_rng(seed).standard_normal(n ** 3)
 
 
-# (n, delta / h): 6h and 4h carry tie bands (|d|^2 = 36, 16), 3.5h and 5.3h do not
-CASES = [(32, 6.0), (40, 6.0), (48, 4.0), (36, 3.5), (44, 5.3), (64, 6.0)]
+# (n, delta / h): 6h, 5h, 4h carry tie bands (|d|^2 = 36, 25, 16: plane classes q = 2, 1, 4),
+# 3.5h and 5.3h do not
+CASES = [(32, 6.0), (40, 6.0), (48, 4.0), (40, 5.0), (36, 3.5), (44, 5.3), (64, 6.0),
+         (72, 6.0)]   # 72 + 5 -> L = 80: radix-5 stages
 
 
 @pytest.mark.parametrize("n,dh", CASES)
@@ -59,6 +61,16 @@ def test_box_fft_vs_stencil_sweep(N, n, dh, monkeypatch):
     assert op.info.fft_len == 0
     sweep = op.apply(u)
     assert np.max(np.abs(fft - sweep)) <= FAST_TOL * np.max(np.abs(sweep))
+
+
+@pytest.mark.parametrize("n", [40, 72])
+def test_box_fft_eight_columns(N, n, monkeypatch):
+    """NLG_F3_COLS=8: the strided passes with 8 columns per CTA (one CTA per SM)."""
+    u = _u(n)
+    ref = _op(N, n, 6.0).apply(u)
+    monkeypatch.setenv("NLG_F3_COLS", "8")
+    got = _op(N, n, 6.0).apply(u)
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
 
 
 def test_box_fft_without_kappa(N):
