@@ -73,6 +73,7 @@ using namespace stockham;
 // 768^3 against 5.2 ms for C = 8 with one CTA per SM); NLG_F3_COLS=8 (plan time) selects 8.
 constexpr int kF3Cols = 8;
 constexpr int kF3El = 8;     // elements per thread per stage
+constexpr int kF3MaxG = 7;   // kernel support radius r_f <= 6 (partial spectra per column in registers)
 
 template <int L>
 __host__ __device__ constexpr int rows_threads() { return L / kF3El < 32 ? 32 : (L / kF3El > 128 ? 128 : L / kF3El); }
@@ -173,34 +174,43 @@ template <int L, int C>
 __global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_zconv(const __grid_constant__ F3Args a) {
   constexpr int T = cols_threads3<L, C>();
   extern __shared__ double2 fsm3[];
-  double* gs = reinterpret_cast<double*>(fsm3 + L * C);   // [C][rf + 1]
-  double* cs = gs + C * (a.rf + 1);                       // [L] cos table
+  double* cs = reinterpret_cast<double*>(fsm3 + L * C);   // [L] cos(2 pi t / L)
   const int tid = threadIdx.x;
   const int kx0 = blockIdx.x * C;
   const int64_t ky = blockIdx.y;
   const int64_t plane = static_cast<int64_t>(a.ly) * a.lx;
   double2* col = a.z + ky * a.lx + kx0;
   const int G = a.rf + 1;
-  for (int i = tid; i < C * G; i += T) gs[i] = __ldg(a.g + (ky * a.lx + kx0) * G + i);
+  // T is a multiple of C, so every butterfly of this thread is in column tid % C:
+  // its partial spectra G[0..rf] sit in registers
+  static_assert(T % C == 0, "one column per thread");
+  double gr[kF3MaxG];
+  {
+    const double* gp = a.g + (ky * a.lx + kx0 + tid % C) * G;
+#pragma unroll
+    for (int d = 0; d < kF3MaxG; ++d) gr[d] = d < G ? __ldg(gp + d) : 0.0;
+  }
   for (int i = tid; i < L; i += T) cs[i] = __ldg(a.cz + i);
   __syncthreads();
   auto ld = [&](int e, int c) {
     if (e >= a.n_in) return make_double2(0.0, 0.0);
     return col[e * plane + c];
   };
-  auto mul = [&](int base, int stride, int c, auto& v) {   // K^(kz) = sum_dz G(dz) cos(2 pi kz dz / L)
+  // K^(kz) = sum_dz G(dz) T_dz(cos(2 pi kz / L)) by Clenshaw's recurrence
+  auto mul = [&](int base, int stride, int c, auto& v) {
     constexpr int R = sizeof(v) / sizeof(v[0]);
-    const double* gc = gs + c * G;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int kz = base + q * stride;
-      double k = gc[0];
-      int p = 0;
-      for (int dz = 1; dz < G; ++dz) {
-        p += kz;
-        if (p >= L) p -= L;
-        k = fma(gc[dz], cs[p], k);
+      const double x = cs[kz], x2 = 2.0 * x;
+      double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+      for (int d = kF3MaxG - 1; d >= 1; --d) {
+        const double b0 = fma(x2, b1, gr[d] - b2);
+        b2 = b1;
+        b1 = b0;
       }
+      const double k = fma(x, b1, gr[0] - b2);
       fsm3[kz * C + c] = make_double2(v[q].x * k, -v[q].y * k);
     }
   };
@@ -330,6 +340,11 @@ __device__ __forceinline__ void padd(double& acc, double v, unsigned bit) {
 
 // M > 0: the tie set of |t|^2 = M at compile time (offsets, slots and mask
 // bits are immediates); M = 0: the runtime set in a.tg.
+__device__ __forceinline__ void cp_async8z(void* dst, const void* src, bool in) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(in ? 8 : 0) : "memory");
+}
+
 template <int M, bool KW, typename MT>
 __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant__ TieArgs a) {
   extern __shared__ __align__(16) double2 tsm[];
@@ -337,23 +352,22 @@ __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant
   const int n = static_cast<int>(g.n);
   const int64_t nn = g.n * g.n;
   constexpr TieSet TS = make_ties(M);
-  const int R = M ? TS.R : a.tg.R, q = M ? TS.q : a.tg.q, NS = 2 * R / q + 1;
+  const int R = M ? TS.R : a.tg.R, q = M ? TS.q : a.tg.q, NS = 2 * R / q + 1, NR = NS + 1;
   const int W = kTieTX + 2 * R, SB = (kTieTY + 2 * R) * W, SL = SB + 1;   // slot stride; [SB] = 0
   constexpr int NT = kTieTX * kTieTY;
   const int tid = threadIdx.y * kTieTX + threadIdx.x;
   const int x0 = blockIdx.x * kTieTX, y0 = blockIdx.y * kTieTY;
   const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
   const bool live = x < n && y < n;
-  const int cls = blockIdx.z % q;
-  (void)cls;
+  const int cls = static_cast<int>(blockIdx.z) % q;
   const int zb = static_cast<int>(g.row_begin) + static_cast<int>(blockIdx.z / q) * kTieZC;
   const int ze = min(static_cast<int>(g.row_end), zb + kTieZC);
-  int zf = zb + ((cls - zb) % q + q) % q;                 // first target plane of the class
+  const int zf = zb + ((cls - zb) % q + q) % q;           // first target plane of the class
   if (zf >= ze) return;
   const MT* mask = static_cast<const MT*>(a.mask);
   const int tgt = y * n + x;
   const int sbase = (threadIdx.y + R) * W + threadIdx.x + R;
-  for (int sl = tid; sl < NS; sl += NT) tsm[sl * SL + SB] = make_double2(0.0, 0.0);
+  for (int sl = tid; sl < NR; sl += NT) tsm[sl * SL + SB] = make_double2(0.0, 0.0);
   int soff[kTieStage];
   bool sok[kTieStage];
 #pragma unroll
@@ -364,93 +378,95 @@ __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant
     sok[k] = e < SB && gy >= 0 && gy < n && gx >= 0 && gx < n;
     soff[k] = sok[k] ? gy * n + gx : 0;
   }
-  double su[kTieStage], sk[kTieStage];
-  auto prefetch = [&](int p) {
+  // plane p -> slot: (u, kappa) pairs by cp.async, zero outside the domain
+  auto stage = [&](int p, int slot) {
     const bool pin = p >= 0 && p < n;
-    const double* up = a.u + (static_cast<int64_t>(p) - g.in_begin) * nn;
-    const double* kp = KW ? a.kappa + (static_cast<int64_t>(p) - g.in_begin) * nn : nullptr;
-#pragma unroll
-    for (int k = 0; k < kTieStage; ++k) {
-      su[k] = 0.0;
-      sk[k] = 0.0;
-      if (pin && sok[k]) {
-        su[k] = __ldg(up + soff[k]);
-        if (KW) sk[k] = __ldg(kp + soff[k]);
-      }
-    }
-  };
-  auto put = [&](int slot) {
-    double2* st = tsm + slot * SL;
+    const int64_t pb = (static_cast<int64_t>(pin ? p : 0) - g.in_begin) * nn;
+    double* st = reinterpret_cast<double*>(tsm + slot * SL);
 #pragma unroll
     for (int k = 0; k < kTieStage; ++k) {
       const int e = tid + k * NT;
-      if (e < SB) st[e] = make_double2(su[k], KW ? su[k] * sk[k] : 0.0);
+      if (e < SB) {
+        const bool in = pin && sok[k];
+        cp_async8z(st + 2 * e, a.u + pb + soff[k], in);
+        if (KW) cp_async8z(st + 2 * e + 1, a.kappa + pb + soff[k], in);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  // ring of NR = NS + 1 slots: plane zf - R + i q in slot i mod NR
+  for (int i = 0; i < NS; ++i) stage(zf - R + i * q, i);
+  // per-target operands of plane z, fetched one step ahead
+  MT m = 0, mn = 0;
+  double ek = 0.0, es = 0.0, eo = 0.0, ekn = 0.0, esn = 0.0, eon = 0.0;
+  auto fetch = [&](int z) {
+    mn = 0;
+    ekn = esn = eon = 0.0;
+    if (live && z < ze) {
+      const int64_t ii = (static_cast<int64_t>(z) - g.in_begin) * nn + tgt;
+      const int64_t oi = (static_cast<int64_t>(z) - g.row_begin) * nn + tgt;
+      mn = __ldg(mask + oi);
+      if (KW) ekn = __ldg(a.kappa + ii);
+      esn = a.scale ? __ldg(a.scale + oi) : a.scale0;
+      eon = a.out[oi];
     }
   };
-  // ring: plane zf - R + i q lives in slot i mod NS; fill i = 0 .. NS - 2
-  for (int i = 0; i + 1 < NS; ++i) {
-    prefetch(zf - R + i * q);
-    put(i);
-  }
-  prefetch(zf + R);
+  fetch(zf);
   int head = 0;                                           // slot of plane zt - R
   for (int zt = zf; zt < ze; zt += q) {
-    const int snew = head == 0 ? NS - 1 : head - 1;       // slot of plane zt + R (held plane zt - R - q)
-    __syncthreads();                                      // previous step's reads of that slot are done
-    put(snew);
-    const int64_t ii = (static_cast<int64_t>(zt) - g.in_begin) * nn + tgt;
+    m = mn;
+    ek = ekn;
+    es = esn;
+    eo = eon;
     const int64_t oi = (static_cast<int64_t>(zt) - g.row_begin) * nn + tgt;
-    MT m = 0;
-    double ek = 0.0, es = 0.0, eo = 0.0;
-    if (live) {
-      m = __ldg(mask + oi);
-      if (KW) ek = __ldg(a.kappa + ii);
-      es = a.scale ? __ldg(a.scale + oi) : a.scale0;
-      eo = a.out[oi];
-    }
-    __syncthreads();
-    if (zt + q < ze) prefetch(zt + q + R);                // next plane in flight during the sums
+    asm volatile("cp.async.wait_all;\n" ::: "memory");   // planes zt - R .. zt + R (own copies)
+    __syncthreads();                                      // everyone's copies; last step's reads done
+    const int sn = head == 0 ? NR - 1 : head - 1;          // slot of plane zt - R - q: free now
+    if (zt + q < ze) stage(zt + q + R, sn);               // next step's plane in flight during the sums
+    fetch(zt + q);
     double A = 0.0, B = 0.0;
-    if (m) {
-      if constexpr (M > 0) {
-        constexpr int kNS = 2 * TS.R / TS.q + 1;
-        const double2* slot[kNS];
+    if constexpr (M > 0) {
+      constexpr int kNS = 2 * TS.R / TS.q + 1;
+      const double2* slot[kNS];
 #pragma unroll
-        for (int r = 0; r < kNS; ++r) slot[r] = tsm + (head + r < kNS ? head + r : head + r - kNS) * SL + sbase;
-        const double2* zero = tsm + SB;                 // slot 0's zero element
-        double A1 = 0.0, B1 = 0.0;                      // two chains per field
+      for (int r = 0; r < kNS; ++r) slot[r] = tsm + (head + r < NR ? head + r : head + r - NR) * SL + sbase;
+      const double2* zero = tsm + SB;                     // slot 0's zero element
+      double A1 = 0.0, B1 = 0.0;                          // two chains per field
 #pragma unroll
-        for (int k = 0; k < TS.n; ++k) {                // an excluded tie reads the zero element
-          const double2* src = slot[(TS.t0[k] + TS.R) / TS.q] + TS.t1[k] * (kTieTX + 2 * TS.R) + TS.t2[k];
-          const double2 v = *((m & (1u << k)) ? src : zero);
-          if (k & 1) {
-            A1 += v.x;
-            if (KW) B1 += v.y;
-          } else {
-            A += v.x;
-            if (KW) B += v.y;
-          }
+      for (int k = 0; k < TS.n; ++k) {                    // an excluded tie reads the zero element
+        const double2* src = slot[(TS.t0[k] + TS.R) / TS.q] + TS.t1[k] * (kTieTX + 2 * TS.R) + TS.t2[k];
+        const double2 v = *((m & (1u << k)) ? src : zero);
+        if (k & 1) {
+          A1 += v.x;
+          if (KW) B1 = fma(v.x, v.y, B1);
+        } else {
+          A += v.x;
+          if (KW) B = fma(v.x, v.y, B);
         }
-        A += A1;
-        B += B1;
-      } else {
+      }
+      A += A1;
+      B += B1;
+    } else {
+      if (m) {
         for (int gi = 0; gi < a.tg.ngroup; ++gi) {
           int sl = head + (a.tg.t0[gi] + R) / q;
-          sl = sl >= NS ? sl - NS : sl;
+          sl = sl >= NR ? sl - NR : sl;
           const double2* st = tsm + sl * SL;
           const int kb = a.tg.beg[gi], kend = a.tg.beg[gi + 1];
 #pragma unroll 4
           for (int k = kb; k < kend; ++k) {             // an excluded tie reads the zero slot
             const double2 v = st[(m >> k) & 1 ? sbase + a.tg.off[k] : SB];
             A += v.x;
-            B += v.y;
+            if (KW) B = fma(v.x, v.y, B);
           }
         }
       }
+    }
+    if (m) {
       const double X = KW ? fma(ek, A, B) : A;
       a.out[oi] = fma(es * a.w, X, eo);
     }
-    head = head + 1 == NS ? 0 : head + 1;
+    head = head + 1 == NR ? 0 : head + 1;
   }
 }
 
@@ -483,7 +499,7 @@ void f3_attr_c(int rf) {
   NLG_CUDA(cudaFuncSetAttribute(f3_cols<L, true, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(cols_smem3<L, C>())));
   NLG_CUDA(cudaFuncSetAttribute(f3_zconv<L, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(cols_smem3<L, C>() + sizeof(double) * (C * (rf + 1) + L))));
+                                static_cast<int>(cols_smem3<L, C>() + sizeof(double) * L)));
 }
 template <int L>
 void f3_attr(int rf) {
@@ -519,7 +535,7 @@ void launch_cols(const F3Args& a, int cols, bool pd, int64_t planes, cudaStream_
 template <int L, int C>
 void launch_zconv_c(const F3Args& a, cudaStream_t s) {
   const dim3 grid(static_cast<unsigned>(a.lx / C), static_cast<unsigned>(a.ly));
-  const size_t sb = cols_smem3<L, C>() + sizeof(double) * (C * (a.rf + 1) + L);
+  const size_t sb = cols_smem3<L, C>() + sizeof(double) * L;
   f3_zconv<L, C><<<grid, cols_threads3<L, C>(), sb, s>>>(a);
 }
 template <int L>
@@ -615,7 +631,7 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   const int mhi = static_cast<int>(std::floor(e2 * (1.0 + 1e-12)));
   int rf = 0;
   while ((rf + 1) * (rf + 1) < mlo) ++rf;         // largest component inside the strict ball
-  if (rf < 1) return nullptr;
+  if (rf < 1 || rf + 1 > kF3MaxG) return nullptr;
   const int64_t n = g.n, n_in = g.in_end - g.in_begin;
   const int lx = f3_length(n + rf), lz = f3_length(n_in + rf);
   if (!lx || !lz || !f3_supported(lx) || !f3_supported(lz)) return nullptr;
@@ -676,7 +692,7 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
       q = a;
     }
     tg.q = q == 0 ? 1 : q;
-    const size_t ring = sizeof(double2) * (2 * R / tg.q + 1) * ((kTieTY + 2 * R) * (kTieTX + 2 * R) + 1);
+    const size_t ring = sizeof(double2) * (2 * R / tg.q + 2) * ((kTieTY + 2 * R) * (kTieTX + 2 * R) + 1);
     if (ring > 227 * 1024) {   // the plane ring does not fit in shared memory: keep the stencil sweep
       delete B;
       return nullptr;
@@ -764,11 +780,11 @@ void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale
     t.out = out;
     const int R = B.tg.R, NS = 2 * R / B.tg.q + 1;
     const bool wide = B.ntie > 32;
-    const size_t sb = sizeof(double2) * NS * ((kTieTY + 2 * R) * (kTieTX + 2 * R) + 1);
+    const bool fixed = B.tie_m == kTieFixedM && !wide;
+    const size_t sb = sizeof(double2) * (NS + 1) * ((kTieTY + 2 * R) * (kTieTX + 2 * R) + 1);
     const dim3 grid(static_cast<unsigned>((B.n + kTieTX - 1) / kTieTX), static_cast<unsigned>((B.n + kTieTY - 1) / kTieTY),
                     static_cast<unsigned>((B.rows_out + kTieZC - 1) / kTieZC * B.tg.q));
     const dim3 blk(kTieTX, kTieTY);
-    const bool fixed = B.tie_m == kTieFixedM;
     if (wide) {
       if (P.d_kappa) f3_ties<0, true, uint64_t><<<grid, blk, sb, s>>>(t);
       else f3_ties<0, false, uint64_t><<<grid, blk, sb, s>>>(t);
