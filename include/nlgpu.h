@@ -151,8 +151,11 @@ nlg_status nlg_counters(const nlg_plan* plan, int64_t* pairs, int64_t* fast_appl
 
 /* Per-stage CUDA-event timing of this plan's kernels (off by default).
  * Stages: 0 direct, 1 span scan, 2 span eval, 3 exp-sum aggregate, 4 exp-sum
- * carry, 5 exp-sum main, 6 near+combine, 7 stencil. nlg_stage_times returns (and resets)
- * the accumulated milliseconds and launch counts per stage (8 slots). */
+ * carry, 5 exp-sum main, 6 near+combine, 7 stencil, 8 exp-sum FFT, 9 box FFT
+ * passes, 10 box tie band. nlg_stage_times returns (and resets) the
+ * accumulated milliseconds and launch counts per stage: the caller's arrays
+ * hold NLG_NUM_STAGES slots. */
+#define NLG_NUM_STAGES 11
 nlg_status nlg_set_profiling(nlg_plan* plan, int on);
 nlg_status nlg_stage_times(nlg_plan* plan, double* ms, int64_t* launches, int* nstages);
 /* Total kernels this plan has launched. */

@@ -124,4 +124,4 @@ def dptr(a):
 
 
 STAGES = ["direct", "span_scan", "span_eval", "es_aggregate", "es_carry", "es_main", "es_combine", "stencil",
-          "es_fft"]
+          "es_fft", "box_fft", "box_ties"]   # plan.hpp enum Stage (kNumStages slots)

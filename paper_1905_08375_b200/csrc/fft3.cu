@@ -743,7 +743,7 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   return B;
 }
 
-void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
+void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
                   double* out, cudaStream_t s) {
   F3Args a = args_of(P, B);
   a.u = u;
@@ -752,6 +752,8 @@ void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale
   a.diag = diag;
   a.out = out;
   const int lx = B.lx, lz = B.lz;
+  cudaEvent_t ev;
+  stage_begin(P, s, kStBoxFft, &ev);
 #define NLG_F3_CASE(N) \
   if (lx == N) launch_rows<N>(a, false, B.n_in * B.n, s);
   NLG_F3_L(NLG_F3_CASE)
@@ -772,7 +774,9 @@ void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale
   if (lx == N) launch_rows<N>(a, true, B.rows_out * B.n, s);
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
+  stage_end(P, s, kStBoxFft, ev, 5);
   if (B.ntie > 0) {
+    stage_begin(P, s, kStBoxTie, &ev);
     TieArgs t = tie_args(P, B);
     t.u = u;
     t.scale = scale;
@@ -795,6 +799,7 @@ void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale
       if (P.d_kappa) f3_ties<0, true, uint32_t><<<grid, blk, sb, s>>>(t);
       else f3_ties<0, false, uint32_t><<<grid, blk, sb, s>>>(t);
     }
+    stage_end(P, s, kStBoxTie, ev, 1);
   }
 }
 

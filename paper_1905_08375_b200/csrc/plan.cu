@@ -296,6 +296,10 @@ void fast_dev(Plan& P, const double* u, double* out, cudaStream_t s) {
     case 1: spans_apply(P, u, out, s); break;
     case 2: expsum_apply(P, u, out, s); break;
     case 3: {
+      if (stencil_box(P)) {   // box FFT mode: its passes and tie pass are stages of their own
+        stencil_apply(P, u, out, s);
+        break;
+      }
       cudaEvent_t ev;
       stage_begin(P, s, kStStencil, &ev);
       stencil_apply(P, u, out, s);
@@ -422,6 +426,8 @@ nlg_status nlg_set_profiling(nlg_plan* plan, int on) {
     plan->p.sprof.on = on != 0;
   });
 }
+
+static_assert(nlg::kNumStages == NLG_NUM_STAGES, "stage slots of the C-ABI");
 
 nlg_status nlg_stage_times(nlg_plan* plan, double* ms, int64_t* launches, int* nstages) {
   return guard([&] {

@@ -41,7 +41,7 @@ struct BoxFft;
 
 // Optional per-stage CUDA-event timing (nlg_set_profiling / nlg_stage_times).
 enum Stage { kStDirect = 0, kStSpanScan, kStSpanEval, kStEsAggregate, kStEsCarry, kStEsMain,
-             kStEsCombine, kStStencil, kStEsFft, kNumStages };
+             kStEsCombine, kStStencil, kStEsFft, kStBoxFft, kStBoxTie, kNumStages };
 struct StageProf {
   bool on = false;
   struct Rec { int stage; cudaEvent_t a, b; };
@@ -116,9 +116,10 @@ void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void stencil_free(Plan& P);
 int stencil_launches(const Plan& P);
 int stencil_fft_len(const Plan& P);
+bool stencil_box(const Plan& P);   // method 3 runs the box FFT mode (brackets its own stages)
 // box FFT mode of method 3 (fft3.cu): 3-D fractional, constant horizon
 BoxFft* boxfft_setup(const Plan& P, double alpha);
-void boxfft_apply(const Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
+void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
                   double* out, cudaStream_t s);
 int boxfft_launches(const BoxFft& B);
 int boxfft_length(const BoxFft& B);

@@ -1044,6 +1044,8 @@ int stencil_launches(const Plan& P) {
   return S->pack ? 2 : 1;
 }
 
+bool stencil_box(const Plan& P) { return P.st_state && P.st_state->box; }
+
 int stencil_fft_len(const Plan& P) { return P.st_state && P.st_state->box ? boxfft_length(*P.st_state->box) : 0; }
 
 void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s) {

@@ -66,3 +66,12 @@ def test_halo_rows(capi):
     # window of floor(delta/h)+2 cells, a superset of window_around (operators.cpp:31-42)
     assert N.halo_rows(dim=2, n=4096, family=capi.FRACTIONAL, delta_max=12 / 4096) == 14
     assert N.halo_rows(dim=1, n=1 << 22, family=capi.FRACTIONAL, delta_max=0.015) == 62916
+
+
+def test_stage_slots_match_header():
+    """nlg_stage_times fills NLG_NUM_STAGES slots; the Python stage names cover them."""
+    import re
+    from paper_1905_08375_b200 import _capi
+    src = open(os.path.join(ROOT, "include", "nlgpu.h")).read()
+    n = int(re.search(r"#define NLG_NUM_STAGES (\d+)", src).group(1))
+    assert len(_capi.STAGES) == n
