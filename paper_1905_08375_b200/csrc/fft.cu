@@ -154,6 +154,81 @@ __global__ void __launch_bounds__(N2 / rows_el<N2>(), (N2 / rows_el<N2>() <= 512
   fs_fft<true, N2, R, N2, 1, T, true>(fsm, d.tw2, tid, ld, st);
 }
 
+// P2, persistent: CTAs loop over rows (grid = resident CTAs) and prefetch the
+// next row's first-stage inputs and K^ values into registers while the
+// current row is in its later stages, so HBM stays busy while a CTA computes
+// (the one-row kernel above loads, computes and stores in series).
+template <int N2>
+__global__ void __launch_bounds__(N2 / rows_el<N2>(), 1)
+    fs_rows_pp(const __grid_constant__ FsDev d, double2* __restrict__ z, int nrows) {
+  constexpr int T = N2 / rows_el<N2>();
+  constexpr int R = rows_el<N2>();
+  constexpr int nq = N2 / R;
+  static_assert(nq == T, "one butterfly per thread in the first and fused stages");
+  extern __shared__ double2 fsm[];
+  const int tid = threadIdx.x;
+  double2 pre[R];
+  double kpre[R];
+  auto fetch_z = [&](int rw) {
+    if (rw < nrows) {
+      const double2* src = z + static_cast<int64_t>(rw) * N2 + tid;
+#pragma unroll
+      for (int r = 0; r < R; ++r) pre[r] = src[r * nq];
+    }
+  };
+  auto fetch_k = [&](int rw) {
+    if (rw < nrows) {
+      const double* src = d.krp + static_cast<int64_t>(rw) * N2 + tid;
+#pragma unroll
+      for (int r = 0; r < R; ++r) kpre[r] = __ldg(src + r * nq);
+    }
+  };
+  int rw = blockIdx.x;
+  fetch_z(rw);
+  fetch_k(rw);
+  for (; rw < nrows; rw += gridDim.x) {
+    const int64_t row = static_cast<int64_t>(rw) * N2;
+    // first stage from the prefetched registers: element e = tid + r nq is pre[r]
+    auto ld = [&](int e, int) { return pre[(e - tid) / nq]; };
+    auto none = [&](int, int, int, auto&) {};
+    fs_fft<true, N2, 1, R, 1, T, true>(fsm, d.tw2, tid, ld, none);
+    fetch_z(rw + gridDim.x);                                   // next row in flight
+    fs_fft<true, N2, R, N2 / R, 1, T, true>(fsm, d.tw2, tid, ld, none);
+    {
+      constexpr int Ns = N2 / R;
+      const int j = tid, k = j;
+      double2 v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = fsm[sidx<true>(j + r * nq)];
+      __syncthreads();
+      if (k > 0) {
+        const double2 w = __ldg(d.tw2 + k * (N2 / (Ns * R)));
+        double2 wr = w;
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          v[r] = cmul(v[r], wr);
+          if (r + 1 < R) wr = cmul(wr, w);
+        }
+      }
+      Dft<R>::run(v);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = make_double2(v[r].x * kpre[r], -v[r].y * kpre[r]);   // K^[j + r Ns]
+      fetch_k(rw + gridDim.x);
+      Dft<R>::run(v);
+#pragma unroll
+      for (int r = 0; r < R; ++r) fsm[sidx<true>(j * R + r)] = v[r];
+      __syncthreads();
+    }
+    auto st = [&](int base, int stride, int, auto& v) {
+      constexpr int RR = sizeof(v) / sizeof(v[0]);
+#pragma unroll
+      for (int r = 0; r < RR; ++r) z[row + base + r * stride] = v[r];
+    };
+    fs_fft<true, N2, R, N2, 1, T, true>(fsm, d.tw2, tid, ld, st);
+    __syncthreads();                                           // last stage's shared reads before the next row
+  }
+}
+
 // P3: columns: conv(x) = conj(FFT_N1(W^{n2 k1} z[k1][n2]))[n1] -> z[x] = (conv u, conv kappa u),
 // in place (a CTA reads and writes only its own columns)
 template <int N1>
@@ -288,6 +363,26 @@ void fourstep_setup(FourStep& F, const double* kr, cudaStream_t s) {
   for (const void* f : {reinterpret_cast<const void*>(fs_rows<2048>), reinterpret_cast<const void*>(fs_rows<4096>),
                         reinterpret_cast<const void*>(fs_rows<8192>)})
     NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rows_smem(8192))));   // 208 KB
+  for (const void* f : {reinterpret_cast<const void*>(fs_rows_pp<2048>), reinterpret_cast<const void*>(fs_rows_pp<4096>),
+                        reinterpret_cast<const void*>(fs_rows_pp<8192>)})
+    NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rows_smem(8192))));
+  // persistent rows: one resident CTA wave looping over the rows, selected by
+  // NLG_FS_PERSIST=1 at plan time (cfg1: 71 vs 75 us isolated, no change
+  // inside the overlapped apply: 0.438 vs 0.437 ms; default one CTA per row)
+  const char* pe = std::getenv("NLG_FS_PERSIST");
+  F.rows_grid = 0;
+  if (pe && std::atoi(pe) == 1) {
+    int dev = 0, sms = 0, per = 0;
+    NLG_CUDA(cudaGetDevice(&dev));
+    NLG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t rp = sizeof(double2) * (F.n2 + F.n2 / 8);
+    const void* f = F.n2 == 8192 ? reinterpret_cast<const void*>(fs_rows_pp<8192>)
+                    : (F.n2 == 4096 ? reinterpret_cast<const void*>(fs_rows_pp<4096>)
+                                    : reinterpret_cast<const void*>(fs_rows_pp<2048>));
+    const int thr = F.n2 == 8192 ? 8192 / rows_el<8192>() : (F.n2 == 4096 ? 4096 / rows_el<4096>() : 2048 / rows_el<2048>());
+    NLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, thr, rp));
+    F.rows_grid = std::min<int64_t>(F.n1, static_cast<int64_t>(std::max(per, 1)) * sms);
+  }
 }
 
 void fourstep_free(FourStep& F) {
@@ -304,6 +399,14 @@ void fourstep_forward_product(const FourStep& F, const double* u, const double* 
   NLG_FS_N1(NLG_FS_CASE)
 #undef NLG_FS_CASE
   const size_t rs = rows_smem(F.n2);
+  if (F.rows_grid > 0) {   // persistent rows (register prefetch of the next row)
+    const unsigned g = static_cast<unsigned>(F.rows_grid);
+    const size_t rp = sizeof(double2) * (F.n2 + F.n2 / 8);
+    if (F.n2 == 8192) fs_rows_pp<8192><<<g, 8192 / rows_el<8192>(), rp, s>>>(d, z, F.n1);
+    else if (F.n2 == 4096) fs_rows_pp<4096><<<g, 4096 / rows_el<4096>(), rp, s>>>(d, z, F.n1);
+    else fs_rows_pp<2048><<<g, 2048 / rows_el<2048>(), rp, s>>>(d, z, F.n1);
+    return;
+  }
   if (F.n2 == 8192) fs_rows<8192><<<F.n1, 8192 / rows_el<8192>(), rs, s>>>(d, z);
   else if (F.n2 == 4096) fs_rows<4096><<<F.n1, 4096 / rows_el<4096>(), rs, s>>>(d, z);
   else fs_rows<2048><<<F.n1, 2048 / rows_el<2048>(), rs, s>>>(d, z);

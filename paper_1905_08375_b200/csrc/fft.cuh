@@ -18,6 +18,7 @@ struct FourStep {
   double2* twa = nullptr;    // [L / 4096 + 1] exp(-2 pi i 4096 a / L)
   double2* twb = nullptr;    // [4096] exp(-2 pi i b / L)
   double* krp = nullptr;     // [N1][N2] kernel spectrum / L at k1 + N1 k2
+  int64_t rows_grid = 0;     // P2 persistent grid (0: one CTA per row)
 };
 
 // Plan for length L, or false when L has no supported split (the caller then
