@@ -795,21 +795,25 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
   }
 }
 
-// 1-D fractional apply (horizons below the scan threshold, e.g. cfg0): one
-// thread per target over a shared-memory tile of the CTA's neighbourhood.
+// 1-D fractional apply (horizons below the scan threshold, e.g. cfg0): S
+// lanes per target over a shared-memory tile of the CTA's neighbourhood, lane
+// s summing the offsets k = s mod S of the target's span, then a shuffle
+// reduction. S = 8 when one target per thread would leave most SMs idle
+// (cfg0: 4096 targets = 16 CTAs of 256; with S = 8, 128 CTAs of 32 targets).
 constexpr int k1T = 256;
 
-template <bool KW>
+template <bool KW, int S>
 __global__ void __launch_bounds__(k1T) stencil1d_kernel(StArgs a) {
   extern __shared__ double sm[];
+  constexpr int TPC = k1T / S;                         // targets per CTA
   const int H = a.H;
-  const int TW = k1T + 2 * H;
+  const int TW = TPC + 2 * H;
   double2* tile = reinterpret_cast<double2*>(sm);
   double* wt = sm + 2 * static_cast<size_t>(TW);
   for (int i = threadIdx.x; i < a.tab_len; i += k1T) wt[i] = a.tab[i];
   const Geom& g = a.g;
   const int64_t n = g.n;
-  const int64_t x0 = g.row_begin + static_cast<int64_t>(blockIdx.x) * k1T;
+  const int64_t x0 = g.row_begin + static_cast<int64_t>(blockIdx.x) * TPC;
   for (int i = threadIdx.x; i < TW; i += k1T) {
     const int64_t gx = x0 - H + i;
     const bool in = gx >= 0 && gx < n && gx >= g.in_begin && gx < g.in_end;
@@ -822,17 +826,39 @@ __global__ void __launch_bounds__(k1T) stencil1d_kernel(StArgs a) {
     tile[i] = v;
   }
   __syncthreads();
-  const int64_t ix = x0 + threadIdx.x;
-  if (ix >= g.row_end) return;
+  const int t = threadIdx.x / S, ls = threadIdx.x % S;  // target within the CTA, lane within its group
+  const int64_t ix = x0 + t;
+  const bool live = ix < g.row_end;
   const int64_t ii = ix - g.in_begin;
-  Ball<1> B;
-  B.init(a.delta ? a.delta[ii] : a.delta0, g.h);
-  B.ki[0] = ix;
-  int d[1] = {0};
-  int xm, xp;
   double acc0 = 0.0, acc1 = 0.0;
-  const double2* trow = tile + threadIdx.x + H;
-  if (B.span(d, xm, xp)) row_sum<KW>(trow, wt + H, xm, xp, acc0, acc1);
+  const double2* trow = tile + t + H;
+  if (live) {
+    Ball<1> B;
+    B.init(a.delta ? a.delta[ii] : a.delta0, g.h);
+    B.ki[0] = ix;
+    int d[1] = {0};
+    int xm, xp;
+    if (B.span(d, xm, xp)) {
+      if (S == 1) {
+        row_sum<KW>(trow, wt + H, xm, xp, acc0, acc1);
+      } else {
+        const double* w = wt + H;
+        for (int k = -xm + ls; k <= xp; k += S) {
+          const double2 v = trow[k];
+          acc0 = fma(w[k], v.x, acc0);
+          if (KW) acc1 = fma(w[k], v.y, acc1);
+        }
+      }
+    }
+  }
+  if (S > 1) {   // groups of S consecutive lanes (S divides 32)
+#pragma unroll
+    for (int o = S / 2; o > 0; o >>= 1) {
+      acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
+      if (KW) acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
+    }
+  }
+  if (!live || ls != 0) return;
   const int64_t oi = ix - g.row_begin;
   const double X = KW ? fma(a.kappa[ii], acc0, acc1) : acc0;
   a.out[oi] = a.scale[oi] * (X - trow[0].x * a.diag[oi]);
@@ -875,10 +901,18 @@ void launch(const StArgs& a, cudaStream_t s, size_t smem) {
   const int64_t n = a.g.n;
   if (dim == 1) {
     if (a.mode == 0) {
-      const unsigned grid = static_cast<unsigned>((a.g.row_end - a.g.row_begin + k1T - 1) / k1T);
-      const size_t sb = sizeof(double) * (2 * static_cast<size_t>(k1T + 2 * a.H) + a.tab_len);
-      if (a.kw) stencil1d_kernel<true><<<grid, k1T, sb, s>>>(a);
-      else stencil1d_kernel<false><<<grid, k1T, sb, s>>>(a);
+      const int64_t nt = a.g.row_end - a.g.row_begin;
+      const bool split = (nt + k1T - 1) / k1T < 2 * 148;   // too few CTAs for one target per thread
+      const int tpc = split ? k1T / 8 : k1T;
+      const unsigned grid = static_cast<unsigned>((nt + tpc - 1) / tpc);
+      const size_t sb = sizeof(double) * (2 * static_cast<size_t>(tpc + 2 * a.H) + a.tab_len);
+      if (split) {
+        if (a.kw) stencil1d_kernel<true, 8><<<grid, k1T, sb, s>>>(a);
+        else stencil1d_kernel<false, 8><<<grid, k1T, sb, s>>>(a);
+      } else {
+        if (a.kw) stencil1d_kernel<true, 1><<<grid, k1T, sb, s>>>(a);
+        else stencil1d_kernel<false, 1><<<grid, k1T, sb, s>>>(a);
+      }
     } else {
       if (a.kw) launch_t<1, 0, 1, true>(a, s, smem); else launch_t<1, 0, 1, false>(a, s, smem);
     }
@@ -952,8 +986,10 @@ void allow_smem() {
   smem_attr(stencil_rb_kernel<2, 1, false, kR2Peri>);
   smem_attr(stencil_rb_kernel<3, 0, true, kR3Frac>);
   smem_attr(stencil_rb_kernel<3, 0, false, kR3Frac>);
-  smem_attr(stencil1d_kernel<true>);
-  smem_attr(stencil1d_kernel<false>);
+  smem_attr(stencil1d_kernel<true, 1>);
+  smem_attr(stencil1d_kernel<false, 1>);
+  smem_attr(stencil1d_kernel<true, 8>);
+  smem_attr(stencil1d_kernel<false, 8>);
   smem_attr(stencil_kernel<1, 0, 1, true>);
   smem_attr(stencil_kernel<1, 0, 1, false>);
   smem_attr(stencil_kernel<2, 0, 0, true>);
