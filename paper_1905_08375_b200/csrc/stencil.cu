@@ -581,8 +581,8 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
   // 4 (i & 7) + (i >> 3), so each quarter warp fills consecutive slots of one plane
   const int cl = 4 * (threadIdx.x & 7) + (threadIdx.x >> 3);
   auto stage = [&](int64_t gz, int az) {
-    if (DIM == 3)
-      for (int i = tid; i < wlen; i += 32 * kWY) wt[i] = a.tab[static_cast<size_t>(az) * wlen + i];
+    if (DIM == 3)   // this |dz|'s weight rows, in flight with the plane
+      for (int i = tid; i < wlen; i += 32 * kWY) cp_async8(wt + i, a.tab + static_cast<size_t>(az) * wlen + i, true);
     const bool zin = DIM == 2 || (gz >= 0 && gz < n && gz >= g.in_begin && gz < g.in_end);
     for (int ty = threadIdx.y; ty < TH; ty += kWY) {
       const int64_t gy = y0 - H + ty;
