@@ -30,6 +30,10 @@ namespace {
 using namespace stockham;
 
 constexpr int kFsEl = 8;         // elements per thread per stage (register budget)
+#ifndef NLG_FS_WIDE
+#define NLG_FS_WIDE 0             // experiment: 8 columns per CTA beyond N1 = 768 (16 elements per thread, one CTA per
+                                  // SM): 64-byte u pieces, but 70 vs 60 us per column pass at cfg1 (0.448 vs 0.426 ms)
+#endif
 #ifndef NLG_FS_KRP_PREFETCH
 #define NLG_FS_KRP_PREFETCH 0     // K^ row staged by cp.async (208 KB CTAs: no co-residence with the scans)
 #endif
@@ -51,13 +55,17 @@ __device__ __forceinline__ double2 four_tw(const FsDev& d, int p) {   // W_L^p, 
 // column passes: C columns per CTA (8: 128-byte row pieces; 4 beyond N1 = 768
 // to stay within 576 threads), T threads cover the N1 * C elements, kFsEl each
 template <int N1>
-__host__ __device__ constexpr int cols_c() { return N1 <= 768 ? 8 : 4; }
+__host__ __device__ constexpr int cols_c() { return N1 <= 768 || NLG_FS_WIDE ? 8 : 4; }
 template <int N1>
-__host__ __device__ constexpr int cols_threads() { return (N1 * cols_c<N1>() + kFsEl - 1) / kFsEl; }
+__host__ __device__ constexpr int cols_el() { return N1 * cols_c<N1>() > 1024 * kFsEl ? 2 * kFsEl : kFsEl; }
+template <int N1>
+__host__ __device__ constexpr int cols_threads() { return (N1 * cols_c<N1>() + cols_el<N1>() - 1) / cols_el<N1>(); }
+template <int N1>
+__host__ __device__ constexpr int cols_ctas() { return cols_el<N1>() > kFsEl ? 1 : 2; }
 
 // P1: columns c0..c0+7, x = N2 n1 + n2 -> z[k1][n2] = W^{n2 k1} FFT_N1(f)[k1]
 template <int N1, bool KW>
-__global__ void __launch_bounds__(cols_threads<N1>(), 2) fs_cols_fwd(const __grid_constant__ FsDev d,
+__global__ void __launch_bounds__(cols_threads<N1>(), cols_ctas<N1>()) fs_cols_fwd(const __grid_constant__ FsDev d,
                                                                     const double* __restrict__ u,
                                                                     const double* __restrict__ kappa, int64_t n_in,
                                                                     double2* __restrict__ z) {
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(N2 / rows_el<N2>(), 1)
 // P3: columns: conv(x) = conj(FFT_N1(W^{n2 k1} z[k1][n2]))[n1] -> z[x] = (conv u, conv kappa u),
 // in place (a CTA reads and writes only its own columns)
 template <int N1>
-__global__ void __launch_bounds__(cols_threads<N1>(), 2) fs_cols_inv(const __grid_constant__ FsDev d,
+__global__ void __launch_bounds__(cols_threads<N1>(), cols_ctas<N1>()) fs_cols_inv(const __grid_constant__ FsDev d,
                                                                           double2* z) {
   constexpr int T = cols_threads<N1>(), C = cols_c<N1>();
   extern __shared__ double2 fsm[];
