@@ -75,8 +75,15 @@ constexpr int kF3Cols = 8;
 constexpr int kF3El = 8;     // elements per thread per stage
 constexpr int kF3MaxG = 7;   // kernel support radius r_f <= 6 (partial spectra per column in registers)
 
-template <int L>
-__host__ __device__ constexpr int rows_threads() { return L / kF3El < 32 ? 32 : (L / kF3El > 128 ? 128 : L / kF3El); }
+// Row passes: L / 8 threads, except the forward pass of lengths with radix-5
+// stages, L / 5 (one radix-5 butterfly per thread: 800-point PA 3.63 ms against
+// 4.47 ms; the inverse pass, which also runs the combine, is faster at L / 8).
+template <int L, bool INV>
+__host__ __device__ constexpr int rows_el() { return !INV && L % 5 == 0 ? 5 : kF3El; }
+template <int L, bool INV>
+__host__ __device__ constexpr int rows_threads() {
+  return L / rows_el<L, INV>() < 32 ? 32 : (L / rows_el<L, INV>() > 256 ? 256 : L / rows_el<L, INV>());
+}
 template <int L, int C>
 __host__ __device__ constexpr int cols_threads3() { return L * C / kF3El; }
 
@@ -100,8 +107,8 @@ struct F3Args {
 // PA / PE: one row (plane z, row y) per CTA along the contiguous x axis.
 // PA: z in [0, n_in); PE: z in output planes, combine into out.
 template <int L, bool INV, bool KW>
-__global__ void __launch_bounds__(rows_threads<L>()) f3_rows(const __grid_constant__ F3Args a) {
-  constexpr int T = rows_threads<L>();
+__global__ void __launch_bounds__(rows_threads<L, INV>()) f3_rows(const __grid_constant__ F3Args a) {
+  constexpr int T = rows_threads<L, INV>();
   __shared__ double2 sm[L + L / 8];
   const int64_t r = blockIdx.x;                      // row within the pass
   const int64_t zr = r / a.n, y = r % a.n;
@@ -510,13 +517,13 @@ void f3_attr(int rf) {
 template <int L>
 void launch_rows(const F3Args& a, bool inv, int64_t rows, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>(rows);
-  constexpr int T = rows_threads<L>();
+  constexpr int TF = rows_threads<L, false>(), TI = rows_threads<L, true>();
   if (!inv) {
-    if (a.kappa) f3_rows<L, false, true><<<grid, T, 0, s>>>(a);
-    else f3_rows<L, false, false><<<grid, T, 0, s>>>(a);
+    if (a.kappa) f3_rows<L, false, true><<<grid, TF, 0, s>>>(a);
+    else f3_rows<L, false, false><<<grid, TF, 0, s>>>(a);
   } else {
-    if (a.kappa) f3_rows<L, true, true><<<grid, T, 0, s>>>(a);
-    else f3_rows<L, true, false><<<grid, T, 0, s>>>(a);
+    if (a.kappa) f3_rows<L, true, true><<<grid, TI, 0, s>>>(a);
+    else f3_rows<L, true, false><<<grid, TI, 0, s>>>(a);
   }
 }
 
