@@ -481,6 +481,26 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
   auto in_index = [&](int64_t ix) {
     return DIM == 2 ? (iy - g.in_begin) * n + ix : ((z - g.in_begin) * n + iy) * n + ix;
   };
+  // 3-D: the epilogue's per-target operands (u, kappa, scale, diag) are
+  // independent of the sweep: prefetched into L2 now, they are hits when the
+  // sums are done (cfg4-B 137 -> 135 ms; in 2-D it costs more than it saves)
+  if (DIM == 3 && yok && x0 + kRX * tx < n) {
+    const int64_t i0 = in_index(x0 + kRX * tx), o0 = i0 - (g.row_begin - g.in_begin) * g.stride0;
+    const int64_t last = min(static_cast<int64_t>(kRX - 1), n - 1 - (x0 + kRX * tx));
+    const int64_t pout = (g.row_end - g.row_begin) * g.stride0;
+    auto pf = [](const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); };
+    for (int64_t e : {int64_t(0), last}) {
+      pf(a.u + i0 + e);
+      pf(a.scale + o0 + e);
+      pf(a.diag + o0 + e);
+      if (KW) pf(a.kappa + i0 + e);
+      if (KIND == 1) {
+        pf(a.u + nin_total + i0 + e);
+        pf(a.diag + pout + o0 + e);
+        pf(a.diag + 2 * pout + o0 + e);
+      }
+    }
+  }
   // targets of this lane: M = largest |d|^2 surely inside (below the tie band)
   int M[kRX];
   unsigned tiem = 0;
