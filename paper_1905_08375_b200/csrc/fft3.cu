@@ -317,25 +317,64 @@ constexpr int kTieStage = 4;   // staged (u, kappa) pairs per thread per plane: 
 struct TieSet {
   int n = 0, R = 0, q = 0;
   int t0[kMaxTie] = {}, t1[kMaxTie] = {}, t2[kMaxTie] = {};
+  int bit[kMaxTie] = {};   // mask bit: position in the full band's enumeration
 };
-__host__ __device__ constexpr TieSet make_ties(int M) {
+// DENSE: only the ties without a component of size floor(sqrt(M)) (at M = 36
+// the 24 of the (4,4,2) family: R = 4; the 6 axis ties (6,0,0) enter ~2% of
+// the targets and are read from global memory in the same pass)
+__host__ __device__ constexpr TieSet make_ties(int M, bool dense = false) {
   TieSet s{};
-  while ((s.R + 1) * (s.R + 1) <= M) ++s.R;
-  for (int dz = -s.R; dz <= s.R; ++dz)
-    for (int dy = -s.R; dy <= s.R; ++dy)
-      for (int dx = -s.R; dx <= s.R; ++dx)
-        if (dz * dz + dy * dy + dx * dx == M && s.n < kMaxTie) {
-          s.t0[s.n] = dz;
-          s.t1[s.n] = dy;
-          s.t2[s.n] = dx;
-          ++s.n;
+  int Rf = 0;
+  while ((Rf + 1) * (Rf + 1) <= M) ++Rf;
+  int k = 0;
+  for (int dz = -Rf; dz <= Rf; ++dz)
+    for (int dy = -Rf; dy <= Rf; ++dy)
+      for (int dx = -Rf; dx <= Rf; ++dx)
+        if (dz * dz + dy * dy + dx * dx == M) {
+          const int az = dz < 0 ? -dz : dz, ay = dy < 0 ? -dy : dy, ax = dx < 0 ? -dx : dx;
+          const int mc = az > ay ? (az > ax ? az : ax) : (ay > ax ? ay : ax);
+          if ((!dense || mc < Rf) && s.n < kMaxTie) {
+            s.t0[s.n] = dz;
+            s.t1[s.n] = dy;
+            s.t2[s.n] = dx;
+            s.bit[s.n] = k;
+            s.R = mc > s.R ? mc : s.R;
+            ++s.n;
+          }
+          ++k;
         }
-  for (int k = 0; k < s.n; ++k) {   // gcd of the t0's
-    int a = s.t0[k] < 0 ? -s.t0[k] : s.t0[k], b = s.q;
+  for (int j = 0; j < s.n; ++j) {   // gcd of the t0's
+    int a = s.t0[j] < 0 ? -s.t0[j] : s.t0[j], b = s.q;
     while (b) { const int t = a % b; a = b; b = t; }
     s.q = a;
   }
   if (s.q == 0) s.q = 1;
+  return s;
+}
+// the complement: the axis ties (+-R, 0, 0) and permutations of a band with
+// M = R^2 (each enters ~2% of the targets at delta = 6h, 768^3)
+__host__ __device__ constexpr TieSet make_axis_ties(int M) {
+  TieSet s{};
+  int Rf = 0;
+  while ((Rf + 1) * (Rf + 1) <= M) ++Rf;
+  int k = 0;
+  for (int dz = -Rf; dz <= Rf; ++dz)
+    for (int dy = -Rf; dy <= Rf; ++dy)
+      for (int dx = -Rf; dx <= Rf; ++dx)
+        if (dz * dz + dy * dy + dx * dx == M) {
+          const int az = dz < 0 ? -dz : dz, ay = dy < 0 ? -dy : dy, ax = dx < 0 ? -dx : dx;
+          const int mc = az > ay ? (az > ax ? az : ax) : (ay > ax ? ay : ax);
+          if (mc == Rf && s.n < kMaxTie) {
+            s.t0[s.n] = dz;
+            s.t1[s.n] = dy;
+            s.t2[s.n] = dx;
+            s.bit[s.n] = k;
+            s.R = Rf;
+            ++s.n;
+          }
+          ++k;
+        }
+  s.q = 1;
   return s;
 }
 constexpr int kTieFixedM = 36;   // the BASELINE cfg4-A band (delta = 6h): specialised, fully unrolled
@@ -358,7 +397,7 @@ __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant
   const Geom& g = a.g;
   const int n = static_cast<int>(g.n);
   const int64_t nn = g.n * g.n;
-  constexpr TieSet TS = make_ties(M);
+  constexpr TieSet TS = make_ties(M, true);           // fixed M: the dense part of the band
   const int R = M ? TS.R : a.tg.R, q = M ? TS.q : a.tg.q, NS = 2 * R / q + 1, NR = NS + 1;
   const int W = kTieTX + 2 * R, SB = (kTieTY + 2 * R) * W, SL = SB + 1;   // slot stride; [SB] = 0
   constexpr int NT = kTieTX * kTieTY;
@@ -433,6 +472,20 @@ __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant
     fetch(zt + q);
     double A = 0.0, B = 0.0;
     if constexpr (M > 0) {
+      // axis ties (outside the staged window): the few included sources straight
+      // from global memory, loads issued before the window sums (predicated per lane)
+      constexpr TieSet AX = make_axis_ties(M);
+      double xu[AX.n > 0 ? AX.n : 1], xk[AX.n > 0 ? AX.n : 1];
+      {
+        const int64_t ii = (static_cast<int64_t>(zt) - g.in_begin) * nn + tgt;
+#pragma unroll
+        for (int k = 0; k < AX.n; ++k) {
+          const bool on = (m >> AX.bit[k]) & 1u;
+          const int64_t s = ii + (static_cast<int64_t>(AX.t0[k]) * n + AX.t1[k]) * n + AX.t2[k];
+          xu[k] = on ? __ldg(a.u + s) : 0.0;
+          xk[k] = on && KW ? __ldg(a.kappa + s) : 0.0;
+        }
+      }
       constexpr int kNS = 2 * TS.R / TS.q + 1;
       const double2* slot[kNS];
 #pragma unroll
@@ -442,7 +495,7 @@ __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant
 #pragma unroll
       for (int k = 0; k < TS.n; ++k) {                    // an excluded tie reads the zero element
         const double2* src = slot[(TS.t0[k] + TS.R) / TS.q] + TS.t1[k] * (kTieTX + 2 * TS.R) + TS.t2[k];
-        const double2 v = *((m & (1u << k)) ? src : zero);
+        const double2 v = *((m & (1u << TS.bit[k])) ? src : zero);
         if (k & 1) {
           A1 += v.x;
           if (KW) B1 = fma(v.x, v.y, B1);
@@ -453,6 +506,11 @@ __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant
       }
       A += A1;
       B += B1;
+#pragma unroll
+      for (int k = 0; k < AX.n; ++k) {
+        A += xu[k];
+        if (KW) B = fma(xu[k], xk[k], B);
+      }
     } else {
       if (m) {
         for (int gi = 0; gi < a.tg.ngroup; ++gi) {
@@ -789,12 +847,13 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
     t.scale = scale;
     t.scale0 = scale0;
     t.out = out;
-    const int R = B.tg.R, NS = 2 * R / B.tg.q + 1;
     const bool wide = B.ntie > 32;
     const bool fixed = B.tie_m == kTieFixedM && !wide;
+    constexpr TieSet kDense = make_ties(kTieFixedM, true);
+    const int R = fixed ? kDense.R : B.tg.R, q = fixed ? kDense.q : B.tg.q, NS = 2 * R / q + 1;
     const size_t sb = sizeof(double2) * (NS + 1) * ((kTieTY + 2 * R) * (kTieTX + 2 * R) + 1);
     const dim3 grid(static_cast<unsigned>((B.n + kTieTX - 1) / kTieTX), static_cast<unsigned>((B.n + kTieTY - 1) / kTieTY),
-                    static_cast<unsigned>((B.rows_out + kTieZC - 1) / kTieZC * B.tg.q));
+                    static_cast<unsigned>((B.rows_out + kTieZC - 1) / kTieZC * q));
     const dim3 blk(kTieTX, kTieTY);
     if (wide) {
       if (P.d_kappa) f3_ties<0, true, uint64_t><<<grid, blk, sb, s>>>(t);
