@@ -379,11 +379,6 @@ __host__ __device__ constexpr TieSet make_axis_ties(int M) {
 }
 constexpr int kTieFixedM = 36;   // the BASELINE cfg4-A band (delta = 6h): specialised, fully unrolled
 
-// @p A += v  (a predicated DADD: no select on the sum)
-__device__ __forceinline__ void padd(double& acc, double v, unsigned bit) {
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q add.rn.f64 %0, %0, %1;\n\t}" : "+d"(acc) : "d"(v), "r"(bit));
-}
-
 // M > 0: the tie set of |t|^2 = M at compile time (offsets, slots and mask
 // bits are immediates); M = 0: the runtime set in a.tg.
 __device__ __forceinline__ void cp_async8z(void* dst, const void* src, bool in) {
