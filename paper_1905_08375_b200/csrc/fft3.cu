@@ -71,7 +71,6 @@ using namespace stockham;
 
 // Strided passes: C = 4 columns per CTA (64-byte row pieces, two CTAs per SM: 3.6 ms per y pass at
 // 768^3 against 5.2 ms for C = 8 with one CTA per SM); NLG_F3_COLS=8 (plan time) selects 8.
-constexpr int kF3Cols = 8;
 constexpr int kF3El = 8;     // elements per thread per stage
 constexpr int kF3MaxG = 7;   // kernel support radius r_f <= 6 (partial spectra per column in registers)
 
@@ -102,10 +101,12 @@ struct F3Args {
   double scale0;
   const double* diag;    // [n_out]
   double* out;           // [n_out]
+  int ab;                // PE: store (A, B) into the Z row (the tie pass combines)
 };
 
 // PA / PE: one row (plane z, row y) per CTA along the contiguous x axis.
-// PA: z in [0, n_in); PE: z in output planes, combine into out.
+// PA: z in [0, n_in); PE: z in output planes, combine into out (or, with a tie
+// band, (A, B) back into the row for the tie pass's combine).
 template <int L, bool INV, bool KW>
 __global__ void __launch_bounds__(rows_threads<L, INV>()) f3_rows(const __grid_constant__ F3Args a) {
   constexpr int T = rows_threads<L, INV>();
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(rows_threads<L, INV>()) f3_rows(const __grid_c
     fs_fft<false, L, 1, L, 1, T, true>(sm, a.twx, tid, ld, st);
   } else {
     const int64_t zi = a.o0 + zr;                    // input plane of this output plane
-    const double2* zrow = a.z + (zi * a.ly + y) * a.lx;
+    double2* zrow = a.z + (zi * a.ly + y) * a.lx;
     const int64_t ii = (zi * a.n + y) * a.n;         // input index of x = 0
     const int64_t oi = (zr * a.n + y) * a.n;         // output index of x = 0
     auto ld = [&](int e, int) { return zrow[e]; };
@@ -140,6 +141,10 @@ __global__ void __launch_bounds__(rows_threads<L, INV>()) f3_rows(const __grid_c
         const int x = base + q * stride;
         if (x < a.n) {
           const double A = v[q].x, B = -v[q].y;      // conjugate: (conv u, conv kappa u)
+          if (a.ab) {                                // the row's own elements: read before (first stage)
+            zrow[x] = make_double2(A, B);
+            continue;
+          }
           const double X = KW ? fma(__ldg(a.kappa + ii + x), A, B) : A;
           const double sc = a.scale ? __ldg(a.scale + oi + x) : a.scale0;
           a.out[oi + x] = sc * (X - __ldg(a.u + ii + x) * __ldg(a.diag + oi + x));
@@ -150,7 +155,7 @@ __global__ void __launch_bounds__(rows_threads<L, INV>()) f3_rows(const __grid_c
   }
 }
 
-// PB / PD: kF3Cols adjacent kx columns along y in one plane. PB reads y < n
+// PB / PD: C adjacent kx columns along y in one plane. PB reads y < n
 // (zero padding above) and writes every ky; PD reads every ky and writes y < n.
 template <int L, bool PD, int C>
 __global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_cols(const __grid_constant__ F3Args a) {
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_cols(const __
   fs_fft<false, L, 1, L, C, T, false>(fsm3, a.twy, tid, ld, st);
 }
 
-// PC: kF3Cols adjacent kx columns along z at one ky: forward FFT, x K^,
+// PC: C adjacent kx columns along z at one ky: forward FFT, x K^,
 // conjugate, forward FFT; planes [o0, o0 + rows_out) stored.
 template <int L, int C>
 __global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_zconv(const __grid_constant__ F3Args a) {
@@ -283,6 +288,9 @@ struct TieArgs {
   const double* scale;   // or null: scale0
   double scale0;
   double* out;
+  const double2* zab;    // (A, B) of the FFT convolution in the Z rows: [in plane][y][x], strides below
+  int64_t zly, zlx;
+  const double* diag;    // [n_out]
 };
 
 template <typename MT>
@@ -437,28 +445,31 @@ __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant
   };
   // ring of NR = NS + 1 slots: plane zf - R + i q in slot i mod NR
   for (int i = 0; i < NS; ++i) stage(zf - R + i * q, i);
-  // per-target operands of plane z, fetched one step ahead
+  // per-target operands of plane z, fetched one step ahead: the mask, the
+  // FFT's (A, B), diag, scale (the target's own u, kappa are in the ring)
   MT m = 0, mn = 0;
-  double ek = 0.0, es = 0.0, eo = 0.0, ekn = 0.0, esn = 0.0, eon = 0.0;
+  double2 ab = make_double2(0.0, 0.0), abn = ab;
+  double ed = 0.0, es = 0.0, edn = 0.0, esn = 0.0;
   auto fetch = [&](int z) {
     mn = 0;
-    ekn = esn = eon = 0.0;
+    abn = make_double2(0.0, 0.0);
+    edn = esn = 0.0;
     if (live && z < ze) {
-      const int64_t ii = (static_cast<int64_t>(z) - g.in_begin) * nn + tgt;
       const int64_t oi = (static_cast<int64_t>(z) - g.row_begin) * nn + tgt;
+      const int64_t zi = static_cast<int64_t>(z) - g.in_begin;
       mn = __ldg(mask + oi);
-      if (KW) ekn = __ldg(a.kappa + ii);
+      abn = a.zab[(zi * a.zly + y) * a.zlx + x];
+      edn = __ldg(a.diag + oi);
       esn = a.scale ? __ldg(a.scale + oi) : a.scale0;
-      eon = a.out[oi];
     }
   };
   fetch(zf);
   int head = 0;                                           // slot of plane zt - R
   for (int zt = zf; zt < ze; zt += q) {
     m = mn;
-    ek = ekn;
+    ab = abn;
+    ed = edn;
     es = esn;
-    eo = eon;
     const int64_t oi = (static_cast<int64_t>(zt) - g.row_begin) * nn + tgt;
     asm volatile("cp.async.wait_all;\n" ::: "memory");   // planes zt - R .. zt + R (own copies)
     __syncthreads();                                      // everyone's copies; last step's reads done
@@ -522,15 +533,17 @@ __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant
         }
       }
     }
-    if (m) {
-      const double X = KW ? fma(ek, A, B) : A;
-      a.out[oi] = fma(es * a.w, X, eo);
+    if (live) {   // the combine of stencil.cu: out = s (kappa (A + w At) + B + w Bt - u diag)
+      const double2 own = tsm[(head + R / q < NR ? head + R / q : head + R / q - NR) * SL + sbase];
+      const double uA = fma(a.w, A, ab.x);
+      const double X = KW ? fma(own.y, uA, fma(a.w, B, ab.y)) : uA;
+      a.out[oi] = es * (X - own.x * ed);
     }
     head = head + 1 == NR ? 0 : head + 1;
   }
 }
 
-// supported axis lengths 2^a 3^b 5^c (multiples of kF3Cols, <= 1024 threads per column CTA)
+// supported axis lengths 2^a 3^b 5^c (multiples of 8 columns, <= 1024 threads per column CTA)
 #define NLG_F3_L(X) \
   X(48) X(64) X(72) X(80) X(96) X(128) X(144) X(160) X(192) X(256) X(288) X(384) X(400) X(512) X(576) X(768) \
   X(800) X(864) X(1024)
@@ -649,6 +662,7 @@ F3Args args_of(const Plan& P, const BoxFft& B) {
   a.scale0 = 0.0;
   a.diag = nullptr;
   a.out = nullptr;
+  a.ab = 0;
   return a;
 }
 
@@ -672,6 +686,10 @@ TieArgs tie_args(const Plan& P, const BoxFft& B) {
   t.scale = nullptr;
   t.scale0 = 0.0;
   t.out = nullptr;
+  t.zab = B.z;
+  t.zly = B.ly;
+  t.zlx = B.lx;
+  t.diag = nullptr;
   return t;
 }
 
@@ -811,6 +829,7 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
   a.scale0 = scale0;
   a.diag = diag;
   a.out = out;
+  a.ab = B.ntie > 0;   // with a tie band the tie pass writes out
   const int lx = B.lx, lz = B.lz;
   cudaEvent_t ev;
   stage_begin(P, s, kStBoxFft, &ev);
@@ -842,6 +861,7 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
     t.scale = scale;
     t.scale0 = scale0;
     t.out = out;
+    t.diag = diag;
     const bool wide = B.ntie > 32;
     const bool fixed = B.tie_m == kTieFixedM && !wide;
     constexpr TieSet kDense = make_ties(kTieFixedM, true);
