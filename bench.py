@@ -102,7 +102,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.02)
+            self._stop.wait(0.002)   # several samples even in a ~10 ms timed region
 
     def stop(self):
         self._stop.set()
