@@ -1073,10 +1073,11 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   // s_i: fractional h^{d-alpha} C_i (x 1/2 with kappa); peridynamic -h^{d-1} c_i
   std::vector<double> sc(P.n_out);
   const double hd = g.hd;
+  // the node-independent factor once (same operation order as factor * c per node)
+  const double f = frac ? (d.kappa ? 0.5 : 1.0) * hd * std::pow(g.h, -d.alpha) : -hd / g.h;
   for (int64_t i = 0; i < P.n_out; ++i) {
     const int64_t x = P.halo_lo * g.stride0 + i;
-    const double c = d.coeff ? d.coeff[x] : d.coeff0;
-    sc[i] = frac ? (d.kappa ? 0.5 : 1.0) * hd * std::pow(g.h, -d.alpha) * c : -hd / g.h * c;
+    sc[i] = f * (d.coeff ? d.coeff[x] : d.coeff0);
   }
   S->scale = upload_vec(sc);
   S->scale_const = d.coeff == nullptr;
