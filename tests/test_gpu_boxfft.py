@@ -116,3 +116,16 @@ def test_box_fft_sharded_slabs(N, rows):
     assert op.info.fft_len > 0
     part = op.apply(u.reshape(n, n, n)[lo:hi].ravel()).reshape(re - rb, n, n)
     assert np.max(np.abs(part - full[rb:re])) <= 1e-12 * np.max(np.abs(full))
+
+
+@pytest.mark.parametrize("s", [0.1, 0.75, 0.95])
+def test_box_fft_singularity_orders(N, s):
+    """Stronger singularities raise |w|_1 against |Lu| (more cancellation in
+    kappa A + B - u diag): the FFT route must still meet 1e-10."""
+    n = 48
+    op = _op(N, n, 6.0, s=s)
+    assert op.info.fft_len > 0
+    u = _u(n)
+    fast = op.apply(u)
+    direct, _ = op.apply_direct(u)
+    assert np.max(np.abs(fast - direct)) <= FAST_TOL * np.max(np.abs(direct))
