@@ -7,19 +7,21 @@
 // (delta/h)^2 (1 -+ 1e-12), stencil.cu Ball::init), and
 //   A_i = sum_{d in N} w(d) u_{i+d},   B_i = sum_{d in N} w(d) (kappa u)_{i+d}
 // is a convolution of f = u + i kappa u (two real fields in one complex
-// signal) with the real, even kernel w(d) = |d|^-alpha. On a zero-padded box
-// L_z x L_y x L_x (L_j >= extent + r_f, 2^a 3^b 5^c) it runs in five HBM passes,
-// each a Stockham transform in shared memory (stockham.cuh):
+// signal) with the real, even kernel w(d) = |d|^-alpha. On a box zero-padded
+// in x and y (L >= n + r_f, 2^a 3^b 5^c) it runs in five HBM passes; the x / y
+// transforms are Stockham FFTs in shared memory (stockham.cuh), the z
+// direction a short direct convolution on the partial spectra:
 //   PA  f3_rows<fwd>  : rows (z, y): load u, kappa (the packing), FFT_x -> Z
-//   PB  f3_cols       : columns along y (8 kx per CTA): FFT_y
-//   PC  f3_zconv      : columns along z: FFT_z, x K^ (built per column from
-//                       the plan-time partial spectra G[ky][kx][|dz|] and a
-//                       cos table), conjugate, FFT_z -- only output planes stored
+//   PB  f3_cols       : columns along y (4 kx per CTA): FFT_y
+//   PC  f3_zstencil   : per (ky, kx) column the (2 r_f + 1)-tap convolution along
+//                       z with G(|dz|; ky, kx) (plan-time partial spectra),
+//                       conjugated, in place
 //   PD  f3_cols       : FFT_y, only y < n stored
 //   PE  f3_rows<inv>  : FFT_x, conjugate: (A, B) of the row, then the combine
 //                       out = s (kappa A + B - u diag) of stencil.cu with the
-//                       plan's diag / scale (MODE 1 of the stencil: exact sets)
-// conj(F(conj(X))) = L IFFT(X), so the 1 / (L_x L_y L_z) scale is folded into G.
+//                       plan's diag / scale (MODE 1 of the stencil: exact sets),
+//                       or (A, B) back into the row when the tie pass combines
+// conj(F(conj(X))) = L IFFT(X), so the 1 / (L_x L_y) scale is folded into G.
 // Offsets in the tie band (|d|^2 in [m_lo, m_hi], e.g. the 30 offsets of
 // |d|^2 = 36 at delta = 6h) belong to N_i only where the reference's float
 // predicate sqrt(sum (y_j - x_j)^2) < delta on the node coordinates holds
@@ -48,15 +50,13 @@ struct TieGroups {
 };
 
 struct BoxFft {
-  int lx = 0, ly = 0, lz = 0, rf = 0;
+  int lx = 0, ly = 0, rf = 0;
   int cols = 4;                                     // columns per CTA of the strided passes (NLG_F3_COLS)
   int64_t n = 0, n_in = 0, o0 = 0, rows_out = 0;   // z: input planes, first output plane, output planes
   double2* z = nullptr;                             // [n_in][ly][lx]
   double2* twx = nullptr;                           // [lx] exp(-2 pi i t / lx)
   double2* twy = nullptr;
-  double2* twz = nullptr;
-  double* cz = nullptr;                             // [lz] cos(2 pi t / lz)
-  double* g = nullptr;                              // [ly][lx][rf + 1] partial spectra / (lx ly lz)
+  double* g = nullptr;                              // [ly][lx][rf + 1] partial spectra / (lx ly)
   int ntie = 0;                                     // tie-band offsets (all |t|^2 = m)
   TieGroups tg{};                                   // ties grouped by t0 (f3_ties)
   int tie_m = 0;                                    // |t|^2 of the band
@@ -88,11 +88,9 @@ __host__ __device__ constexpr int cols_threads3() { return L * C / kF3El; }
 
 struct F3Args {
   int64_t n, n_in, o0, rows_out;
-  int lx, ly, lz, rf;
+  int lx, ly, rf;
   const double2* twx;
   const double2* twy;
-  const double2* twz;
-  const double* cz;
   const double* g;
   double2* z;
   const double* u;       // [n_in rows]
@@ -180,67 +178,54 @@ __global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_cols(const __
   fs_fft<false, L, 1, L, C, T, false>(fsm3, a.twy, tid, ld, st);
 }
 
-// PC: C adjacent kx columns along z at one ky: forward FFT, x K^,
-// conjugate, forward FFT; planes [o0, o0 + rows_out) stored.
-template <int L, int C>
-__global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_zconv(const __grid_constant__ F3Args a) {
-  constexpr int T = cols_threads3<L, C>();
-  extern __shared__ double2 fsm3[];
-  double* cs = reinterpret_cast<double*>(fsm3 + L * C);   // [L] cos(2 pi t / L)
-  const int tid = threadIdx.x;
-  const int kx0 = blockIdx.x * C;
-  const int64_t ky = blockIdx.y;
+// PC: the z direction is not transformed. After FFT_x FFT_y the operator is,
+// per column (ky, kx), a (2 r_f + 1)-tap convolution along z with the partial
+// spectra G(|dz|; ky, kx) = sum_{dy,dx} w(dz,dy,dx) cos(2 pi ky dy/L_y)
+// cos(2 pi kx dx/L_x) / (L_x L_y): one thread per column walks the planes with
+// a register window (in place: the window holds the planes the writes
+// overwrite), output planes stored conjugated for the forward-transform
+// inverses. No z padding, 2 r_f + 1 FMA pairs per element instead of two
+// 800-point transforms.
+constexpr int kZW = 2 * (kF3MaxG - 1) + 1;   // window: r_f <= kF3MaxG - 1
+
+__global__ void __launch_bounds__(256) f3_zstencil(const __grid_constant__ F3Args a) {
   const int64_t plane = static_cast<int64_t>(a.ly) * a.lx;
-  double2* col = a.z + ky * a.lx + kx0;
-  const int G = a.rf + 1;
-  // T is a multiple of C, so every butterfly of this thread is in column tid % C:
-  // its partial spectra G[0..rf] sit in registers
-  static_assert(T % C == 0, "one column per thread");
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (col >= plane) return;
+  constexpr int RW = kF3MaxG - 1;                // window half width
   double gr[kF3MaxG];
   {
-    const double* gp = a.g + (ky * a.lx + kx0 + tid % C) * G;
+    const int G = a.rf + 1;
+    const double* gp = a.g + col * G;
 #pragma unroll
     for (int d = 0; d < kF3MaxG; ++d) gr[d] = d < G ? __ldg(gp + d) : 0.0;
   }
-  for (int i = tid; i < L; i += T) cs[i] = __ldg(a.cz + i);
-  __syncthreads();
-  auto ld = [&](int e, int c) {
-    if (e >= a.n_in) return make_double2(0.0, 0.0);
-    return col[e * plane + c];
-  };
-  // K^(kz) = sum_dz G(dz) T_dz(cos(2 pi kz / L)) by Clenshaw's recurrence
-  auto mul = [&](int base, int stride, int c, auto& v) {
-    constexpr int R = sizeof(v) / sizeof(v[0]);
+  double2* zc = a.z + col;
+  const int64_t nz = a.n_in, zo0 = a.o0, zo1 = a.o0 + a.rows_out;
+  auto ldz = [&](int64_t zz) { return zz >= 0 && zz < nz ? zc[zz * plane] : make_double2(0.0, 0.0); };
+  double2 win[kZW];                              // win[(z + RW) % kZW] = plane z, planes z - RW .. z + RW
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int kz = base + q * stride;
-      const double x = cs[kz], x2 = 2.0 * x;
-      double b1 = 0.0, b2 = 0.0;
+  for (int j = 0; j < kZW - 1; ++j) win[j] = ldz(zo0 - RW + j);
+  for (int64_t zb = zo0; zb < zo1; zb += kZW) {
 #pragma unroll
-      for (int d = kF3MaxG - 1; d >= 1; --d) {
-        const double b0 = fma(x2, b1, gr[d] - b2);
-        b2 = b1;
-        b1 = b0;
+    for (int c = 0; c < kZW; ++c) {              // output plane z = zb + c; window slot of plane z + k: (c + RW + k) % kZW
+      const int64_t z = zb + c;
+      win[(c + kZW - 1) % kZW] = ldz(z + RW);
+      if (z < zo1) {
+        double2 acc = make_double2(gr[0] * win[(c + RW) % kZW].x, gr[0] * win[(c + RW) % kZW].y);
+#pragma unroll
+        for (int k = 1; k <= RW; ++k) {
+          const double2 p = win[(c + RW + k) % kZW], m = win[(c + RW - k + kZW) % kZW];
+          acc.x = fma(gr[k], p.x + m.x, acc.x);
+          acc.y = fma(gr[k], p.y + m.y, acc.y);
+        }
+        zc[z * plane] = make_double2(acc.x, -acc.y);   // conjugate
       }
-      const double k = fma(x, b1, gr[0] - b2);
-      fsm3[kz * C + c] = make_double2(v[q].x * k, -v[q].y * k);
     }
-  };
-  fs_fft<false, L, 1, L, C, T, false, true>(fsm3, a.twz, tid, ld, mul);
-  __syncthreads();
-  auto ld2 = [&](int e, int c) { return fsm3[e * C + c]; };
-  auto st = [&](int base, int stride, int c, auto& v) {
-    constexpr int R = sizeof(v) / sizeof(v[0]);
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int64_t e = base + q * stride;
-      if (e >= a.o0 && e < a.o0 + a.rows_out) col[e * plane + c] = v[q];
-    }
-  };
-  fs_fft<false, L, 1, L, C, T, false, true>(fsm3, a.twz, tid, ld2, st);
+  }
 }
 
-// Plan-time partial spectra: G[ky][kx][dz] = m(dz) / (lx ly lz)
+// Plan-time partial spectra: G[ky][kx][dz] = 1 / (lx ly)
 //   sum_{dy, dx >= 0} m(dy) m(dx) w(dz, dy, dx) cos(2 pi ky dy / ly) cos(2 pi kx dx / lx),
 // m(0) = 1, m(>0) = 2 (the kernel is even in every component).
 __global__ void f3_spectrum(const double* __restrict__ w, int rf, int lx, int ly, const double* __restrict__ cx,
@@ -259,7 +244,7 @@ __global__ void f3_spectrum(const double* __restrict__ w, int rf, int lx, int ly
       }
       acc = fma((dy ? 2.0 : 1.0) * row, cy[(static_cast<int64_t>(ky) * dy) % ly], acc);
     }
-    g[q * G + dz] = (dz ? 2.0 : 1.0) * scale * acc;
+    g[q * G + dz] = scale * acc;
   }
 }
 
@@ -571,8 +556,6 @@ void f3_attr_c(int rf) {
                                 static_cast<int>(cols_smem3<L, C>())));
   NLG_CUDA(cudaFuncSetAttribute(f3_cols<L, true, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(cols_smem3<L, C>())));
-  NLG_CUDA(cudaFuncSetAttribute(f3_zconv<L, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(cols_smem3<L, C>() + sizeof(double) * L)));
 }
 template <int L>
 void f3_attr(int rf) {
@@ -603,18 +586,6 @@ template <int L>
 void launch_cols(const F3Args& a, int cols, bool pd, int64_t planes, cudaStream_t s) {
   if (cols == 4) launch_cols_c<L, 4>(a, pd, planes, s);
   else launch_cols_c<L, 8>(a, pd, planes, s);
-}
-
-template <int L, int C>
-void launch_zconv_c(const F3Args& a, cudaStream_t s) {
-  const dim3 grid(static_cast<unsigned>(a.lx / C), static_cast<unsigned>(a.ly));
-  const size_t sb = cols_smem3<L, C>() + sizeof(double) * L;
-  f3_zconv<L, C><<<grid, cols_threads3<L, C>(), sb, s>>>(a);
-}
-template <int L>
-void launch_zconv(const F3Args& a, int cols, cudaStream_t s) {
-  if (cols == 4) launch_zconv_c<L, 4>(a, s);
-  else launch_zconv_c<L, 8>(a, s);
 }
 
 std::vector<double2> twiddles3(int n) {
@@ -648,12 +619,9 @@ F3Args args_of(const Plan& P, const BoxFft& B) {
   a.rows_out = B.rows_out;
   a.lx = B.lx;
   a.ly = B.ly;
-  a.lz = B.lz;
   a.rf = B.rf;
   a.twx = B.twx;
   a.twy = B.twy;
-  a.twz = B.twz;
-  a.cz = B.cz;
   a.g = B.g;
   a.z = B.z;
   a.u = nullptr;
@@ -711,11 +679,10 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   while ((rf + 1) * (rf + 1) < mlo) ++rf;         // largest component inside the strict ball
   if (rf < 1 || rf + 1 > kF3MaxG) return nullptr;
   const int64_t n = g.n, n_in = g.in_end - g.in_begin;
-  const int lx = f3_length(n + rf), lz = f3_length(n_in + rf);
-  if (!lx || !lz || !f3_supported(lx) || !f3_supported(lz)) return nullptr;
+  const int lx = f3_length(n + rf);
+  if (!lx || !f3_supported(lx)) return nullptr;
   auto* B = new BoxFft();
   B->lx = B->ly = lx;
-  B->lz = lz;
   B->rf = rf;
   if (const char* ce = std::getenv("NLG_F3_COLS")) B->cols = std::atoi(ce) == 8 ? 8 : 4;
   B->n = n;
@@ -782,14 +749,12 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   }
   B->twx = upload3(twiddles3(lx));
   B->twy = B->twx;
-  B->twz = lz == lx ? B->twx : upload3(twiddles3(lz));
-  B->cz = upload3(costab(lz));
   double* dw = upload3(w);
   double* cx = upload3(costab(lx));
   NLG_CUDA(cudaMalloc(&B->g, sizeof(double) * static_cast<size_t>(lx) * lx * G));
   NLG_CUDA(cudaMalloc(&B->z, sizeof(double2) * static_cast<size_t>(n_in) * lx * lx));
   NLG_CUDA(cudaDeviceSynchronize());
-  const double scale = 1.0 / (static_cast<double>(lx) * lx * lz);
+  const double scale = 1.0 / (static_cast<double>(lx) * lx);
   f3_spectrum<<<static_cast<unsigned>((static_cast<int64_t>(lx) * lx + 255) / 256), 256, 0, P.stream>>>(
       dw, rf, lx, lx, cx, cx, scale, B->g);
   NLG_CUDA(cudaGetLastError());
@@ -814,8 +779,7 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
       NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   }
 #define NLG_F3_CASE(N) \
-  if (lx == N) f3_attr<N>(rf); \
-  if (lz == N && lz != lx) f3_attr<N>(rf);
+  if (lx == N) f3_attr<N>(rf);
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
   return B;
@@ -830,7 +794,7 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
   a.diag = diag;
   a.out = out;
   a.ab = B.ntie > 0;   // with a tie band the tie pass writes out
-  const int lx = B.lx, lz = B.lz;
+  const int lx = B.lx;
   cudaEvent_t ev;
   stage_begin(P, s, kStBoxFft, &ev);
 #define NLG_F3_CASE(N) \
@@ -841,10 +805,7 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
   if (lx == N) launch_cols<N>(a, B.cols, false, B.n_in, s);
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
-#define NLG_F3_CASE(N) \
-  if (lz == N) launch_zconv<N>(a, B.cols, s);
-  NLG_F3_L(NLG_F3_CASE)
-#undef NLG_F3_CASE
+  f3_zstencil<<<static_cast<unsigned>((static_cast<int64_t>(B.ly) * B.lx + 255) / 256), 256, 0, s>>>(a);
 #define NLG_F3_CASE(N) \
   if (lx == N) launch_cols<N>(a, B.cols, true, B.rows_out, s);
   NLG_F3_L(NLG_F3_CASE)
@@ -889,8 +850,7 @@ int boxfft_length(const BoxFft& B) { return B.lx; }
 
 void boxfft_free(BoxFft* B) {
   if (!B) return;
-  if (B->twz != B->twx) cudaFree(B->twz);
-  for (void* p : {static_cast<void*>(B->twx), static_cast<void*>(B->cz), static_cast<void*>(B->g),
+  for (void* p : {static_cast<void*>(B->twx), static_cast<void*>(B->g),
                   static_cast<void*>(B->z), B->tie_mask})
     cudaFree(p);
   delete B;
