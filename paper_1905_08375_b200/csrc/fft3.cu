@@ -186,29 +186,28 @@ __global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_cols(const __
 // overwrite), output planes stored conjugated for the forward-transform
 // inverses. No z padding, 2 r_f + 1 FMA pairs per element instead of two
 // 800-point transforms.
-constexpr int kZW = 2 * (kF3MaxG - 1) + 1;   // window: r_f <= kF3MaxG - 1
-
-__global__ void __launch_bounds__(256) f3_zstencil(const __grid_constant__ F3Args a) {
+// RW = r_f (template: the window and the taps in registers)
+template <int RW>
+__global__ void __launch_bounds__(256, 3) f3_zstencil(const __grid_constant__ F3Args a) {
+  constexpr int kZW = 2 * RW + 1;
   const int64_t plane = static_cast<int64_t>(a.ly) * a.lx;
   const int64_t col = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (col >= plane) return;
-  constexpr int RW = kF3MaxG - 1;                // window half width
-  double gr[kF3MaxG];
+  double gr[RW + 1];
   {
-    const int G = a.rf + 1;
-    const double* gp = a.g + col * G;
+    const double* gp = a.g + col * (RW + 1);
 #pragma unroll
-    for (int d = 0; d < kF3MaxG; ++d) gr[d] = d < G ? __ldg(gp + d) : 0.0;
+    for (int d = 0; d <= RW; ++d) gr[d] = __ldg(gp + d);
   }
   double2* zc = a.z + col;
   const int64_t nz = a.n_in, zo0 = a.o0, zo1 = a.o0 + a.rows_out;
   auto ldz = [&](int64_t zz) { return zz >= 0 && zz < nz ? zc[zz * plane] : make_double2(0.0, 0.0); };
-  double2 win[kZW];                              // win[(z + RW) % kZW] = plane z, planes z - RW .. z + RW
+  double2 win[kZW];                              // slot (p - zo0 + RW) % kZW holds plane p
 #pragma unroll
   for (int j = 0; j < kZW - 1; ++j) win[j] = ldz(zo0 - RW + j);
   for (int64_t zb = zo0; zb < zo1; zb += kZW) {
 #pragma unroll
-    for (int c = 0; c < kZW; ++c) {              // output plane z = zb + c; window slot of plane z + k: (c + RW + k) % kZW
+    for (int c = 0; c < kZW; ++c) {              // output plane z = zb + c; plane z + k in slot (c + RW + k) % kZW
       const int64_t z = zb + c;
       win[(c + kZW - 1) % kZW] = ldz(z + RW);
       if (z < zo1) {
@@ -222,6 +221,18 @@ __global__ void __launch_bounds__(256) f3_zstencil(const __grid_constant__ F3Arg
         zc[z * plane] = make_double2(acc.x, -acc.y);   // conjugate
       }
     }
+  }
+}
+
+void launch_zstencil(const F3Args& a, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>((static_cast<int64_t>(a.ly) * a.lx + 255) / 256);
+  switch (a.rf) {
+    case 1: f3_zstencil<1><<<g, 256, 0, s>>>(a); break;
+    case 2: f3_zstencil<2><<<g, 256, 0, s>>>(a); break;
+    case 3: f3_zstencil<3><<<g, 256, 0, s>>>(a); break;
+    case 4: f3_zstencil<4><<<g, 256, 0, s>>>(a); break;
+    case 5: f3_zstencil<5><<<g, 256, 0, s>>>(a); break;
+    default: f3_zstencil<6><<<g, 256, 0, s>>>(a); break;
   }
 }
 
@@ -805,7 +816,7 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
   if (lx == N) launch_cols<N>(a, B.cols, false, B.n_in, s);
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
-  f3_zstencil<<<static_cast<unsigned>((static_cast<int64_t>(B.ly) * B.lx + 255) / 256), 256, 0, s>>>(a);
+  launch_zstencil(a, s);
 #define NLG_F3_CASE(N) \
   if (lx == N) launch_cols<N>(a, B.cols, true, B.rows_out, s);
   NLG_F3_L(NLG_F3_CASE)
