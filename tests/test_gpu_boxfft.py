@@ -37,7 +37,8 @@ def _u(n, seed=1):
 # (n, delta / h): 6h, 5h, 4h carry tie bands (|d|^2 = 36, 25, 16: plane classes q = 2, 1, 4),
 # 3.5h and 5.3h do not
 CASES = [(32, 6.0), (40, 6.0), (48, 4.0), (40, 5.0), (36, 3.5), (44, 5.3), (64, 6.0),
-         (72, 6.0)]   # 72 + 5 -> L = 80: radix-5 stages
+         (72, 6.0),   # 72 + 5 -> L = 80: radix-5 stages
+         (20, 6.0), (12, 6.0)]   # the ball wider than the domain
 
 
 @pytest.mark.parametrize("n,dh", CASES)
