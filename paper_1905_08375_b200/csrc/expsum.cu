@@ -374,6 +374,7 @@ struct PassPair {
   PassArgs d[2];
   int64_t split;
   TailTab t;
+  int zero_facc;   // the aggregate walk clears facc (FFT mode)
 };
 
 template <int NF, bool MAIN, int MT>
@@ -389,6 +390,12 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
   __shared__ int stin[kTailWarps][MAIN ? 2 : 1][kTB][33];    // staged tinfo
   __shared__ double sagg[MAIN ? 1 : kTailWarps][32][MT + 1]; // aggregate walk: chunk transposition
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  if (!MAIN && pp.zero_facc) {   // the tail accumulator of the main walk, cleared here (no memset launch)
+    const int64_t tot = static_cast<int64_t>(pp.d[0].nf) * pp.d[0].n_out;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid; i < tot;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      pp.d[0].facc[i] = 0.0;
+  }
   const int c0 = FW == NF ? 0 : (w & 1);                     // my first field
   const bool kap = NF == 2 && (FW == 2 || c0 == 1);          // kappa needed
   const int64_t k = bid * kG + (FW == NF ? w : (w >> 1));   // my chunk
@@ -1261,7 +1268,7 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
   ExpSumState* S = P.es_state;
   const int64_t n_out = P.n_out;
   const int NF = S->fields;
-  NLG_CUDA(cudaMemsetAsync(S->facc, 0, sizeof(double) * NF * n_out, s));
+  if (!(S->fft && S->four)) NLG_CUDA(cudaMemsetAsync(S->facc, 0, sizeof(double) * NF * n_out, s));
   if (S->fft) {   // fixed-window far field z = FFT^-1( K^ . FFT(u + i kappa u) ), on a side stream
     NLG_CUDA(cudaEventRecord(S->fork, s));
     NLG_CUDA(cudaStreamWaitEvent(S->fstream, S->fork, 0));
@@ -1293,6 +1300,7 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
   }
   PassPair pp;
   pp.t = S->tt;
+  pp.zero_facc = S->fft && S->four;
   for (int mirror = 0; mirror < 2; ++mirror) {
     PassArgs a;
     a.u = u;
