@@ -310,6 +310,19 @@ def run_ours(args):
         dfma = _dfma_peak()
         if dfma:
             roof["fp64_peak_tflops_measured"] = dfma
+            info = plan.info
+            if int(info.fast_method) == 2 and int(info.fft_len) > 0:
+                # the 1-D path's algorithmic fp64 work: the four-step
+                # convolution, 2 x 5 L log2 L, and the tail walks, 4 DFMA (aggregate 1 +
+                # main 3) per term, field, node and direction
+                import math
+                L = int(info.fft_len)
+                nf = 2 if w.kappa is not None else 1
+                flops = 2 * 5 * L * math.log2(L) + 2 * 4 * int(info.exp_terms) * nf * 2 * plan.n_in
+                tf = flops / (ms_step * 1e-3) / 1e12
+                roof["fp64"] = {"achieved_tflops": tf, "peak_tflops": dfma, "frac": tf / dfma,
+                                "flop_per_apply": flops,
+                                "scope": "FFT 10 L log2 L + tail walks 8 M nf N (2 directions)"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
