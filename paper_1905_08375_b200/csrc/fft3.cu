@@ -34,6 +34,9 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "plan.hpp"
 #include "stockham.cuh"
 
@@ -52,6 +55,9 @@ struct TieGroups {
 struct BoxFft {
   int lx = 0, ly = 0, rf = 0;
   int cols = 4;                                     // columns per CTA of the strided passes (NLG_F3_COLS)
+  bool tma = false;                                 // PB / PD through bulk tensor copies (NLG_F3_TMA)
+  int tma_br = 0;                                   // rows per tensor box
+  CUtensorMap pb_in{}, pb_out{}, pd_in{}, pd_out{};
   int64_t n = 0, n_in = 0, o0 = 0, rows_out = 0;   // z: input planes, first output plane, output planes
   double2* z = nullptr;                             // [n_in][ly][lx]
   double2* twx = nullptr;                           // [lx] exp(-2 pi i t / lx)
@@ -176,6 +182,62 @@ __global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_cols(const __
     }
   };
   fs_fft<false, L, 1, L, C, T, false>(fsm3, a.twy, tid, ld, st);
+}
+
+// PB / PD with TMA: the CTA's 4-column tile (L rows x 64 bytes, row pitch
+// L_x x 16 B) arrives by cp.async.bulk.tensor in boxes of br rows (the tensor
+// map's row extent clips: rows beyond it are zero-filled on the load and
+// dropped on the store), is transformed in place in shared memory, and leaves
+// by bulk tensor stores. No per-thread address arithmetic or 16-byte loads.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+template <int L>
+__global__ void __launch_bounds__(cols_threads3<L, 4>(), 2)
+    f3_cols_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+                const __grid_constant__ F3Args a, int br) {
+  constexpr int C = 4, T = cols_threads3<L, C>();
+  extern __shared__ __align__(128) double2 fsm3[];
+  __shared__ __align__(8) unsigned long long mbar;
+  const int tid = threadIdx.x;
+  const int cx = blockIdx.x * 2 * C;             // first double of the tile in the row
+  const int pz = blockIdx.y;                     // plane of the view
+  const unsigned mb = smem_u32(&mbar);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                 "r"(static_cast<unsigned>(L * C * sizeof(double2)))
+                 : "memory");
+    for (int r0 = 0; r0 < L; r0 += br)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+              smem_u32(fsm3 + r0 * C)),
+          "l"(&tin), "r"(cx), "r"(r0), "r"(pz), "r"(mb)
+          : "memory");
+  }
+  __syncthreads();
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra WAIT_%=;\n\t}" ::"r"(mb)
+      : "memory");
+  auto ld = [&](int e, int c) { return fsm3[e * C + c]; };
+  auto st = [&](int base, int stride, int c, auto& v) {
+    constexpr int R = sizeof(v) / sizeof(v[0]);
+#pragma unroll
+    for (int q = 0; q < R; ++q) fsm3[(base + q * stride) * C + c] = v[q];
+  };
+  fs_fft<false, L, 1, L, C, T, false, true>(fsm3, a.twy, tid, ld, st);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy writes -> the bulk store
+  __syncthreads();
+  if (tid == 0) {
+    for (int r0 = 0; r0 < L; r0 += br)
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(&tout),
+                   "r"(cx), "r"(r0), "r"(pz), "r"(smem_u32(fsm3 + r0 * C))
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
 }
 
 // PC: the z direction is not transformed. After FFT_x FFT_y the operator is,
@@ -572,6 +634,8 @@ template <int L>
 void f3_attr(int rf) {
   f3_attr_c<L, 8>(rf);
   f3_attr_c<L, 4>(rf);
+  NLG_CUDA(cudaFuncSetAttribute(f3_cols_tma<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(double2) * L * 4)));
 }
 
 template <int L>
@@ -593,6 +657,14 @@ void launch_cols_c(const F3Args& a, bool pd, int64_t planes, cudaStream_t s) {
   if (pd) f3_cols<L, true, C><<<grid, cols_threads3<L, C>(), cols_smem3<L, C>(), s>>>(a);
   else f3_cols<L, false, C><<<grid, cols_threads3<L, C>(), cols_smem3<L, C>(), s>>>(a);
 }
+template <int L>
+void launch_cols_tma(const BoxFft& B, const F3Args& a, bool pd, int64_t planes, cudaStream_t s) {
+  const dim3 grid(static_cast<unsigned>(a.lx / 4), static_cast<unsigned>(planes));
+  const size_t sb = sizeof(double2) * L * 4;
+  if (pd) f3_cols_tma<L><<<grid, cols_threads3<L, 4>(), sb, s>>>(B.pd_in, B.pd_out, a, B.tma_br);
+  else f3_cols_tma<L><<<grid, cols_threads3<L, 4>(), sb, s>>>(B.pb_in, B.pb_out, a, B.tma_br);
+}
+
 template <int L>
 void launch_cols(const F3Args& a, int cols, bool pd, int64_t planes, cudaStream_t s) {
   if (cols == 4) launch_cols_c<L, 4>(a, pd, planes, s);
@@ -670,6 +742,28 @@ TieArgs tie_args(const Plan& P, const BoxFft& B) {
   t.zlx = B.lx;
   t.diag = nullptr;
   return t;
+}
+
+
+// 3-D tensor map over Z viewed as doubles: (2 L_x, rows, planes), row pitch
+// L_x complex, plane pitch L_y L_x complex; boxes of (8 doubles, br rows, 1).
+bool encode_cols_map(CUtensorMap* m, void* base, int lx, int ly, int64_t rows, int64_t planes, int br) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return false;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * lx), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(planes)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(lx) * 16, static_cast<cuuint64_t>(ly) * lx * 16};
+  const cuuint32_t box[3] = {8, static_cast<cuuint32_t>(br), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -764,6 +858,20 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   double* cx = upload3(costab(lx));
   NLG_CUDA(cudaMalloc(&B->g, sizeof(double) * static_cast<size_t>(lx) * lx * G));
   NLG_CUDA(cudaMalloc(&B->z, sizeof(double2) * static_cast<size_t>(n_in) * lx * lx));
+  {
+    const char* te = std::getenv("NLG_F3_TMA");
+    if (te && std::atoi(te) == 1) {
+      int br = 1;
+      for (int d = 1; d <= 256 && d <= lx; ++d)
+        if (lx % d == 0) br = d;
+      B->tma_br = br;
+      double2* zo = B->z + static_cast<size_t>(B->o0) * lx * lx;
+      B->tma = encode_cols_map(&B->pb_in, B->z, lx, lx, n, n_in, br) &&
+               encode_cols_map(&B->pb_out, B->z, lx, lx, lx, n_in, br) &&
+               encode_cols_map(&B->pd_in, zo, lx, lx, lx, B->rows_out, br) &&
+               encode_cols_map(&B->pd_out, zo, lx, lx, n, B->rows_out, br);
+    }
+  }
   NLG_CUDA(cudaDeviceSynchronize());
   const double scale = 1.0 / (static_cast<double>(lx) * lx);
   f3_spectrum<<<static_cast<unsigned>((static_cast<int64_t>(lx) * lx + 255) / 256), 256, 0, P.stream>>>(
@@ -813,12 +921,12 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
 #define NLG_F3_CASE(N) \
-  if (lx == N) launch_cols<N>(a, B.cols, false, B.n_in, s);
+  if (lx == N) { if (B.tma) launch_cols_tma<N>(B, a, false, B.n_in, s); else launch_cols<N>(a, B.cols, false, B.n_in, s); }
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
   launch_zstencil(a, s);
 #define NLG_F3_CASE(N) \
-  if (lx == N) launch_cols<N>(a, B.cols, true, B.rows_out, s);
+  if (lx == N) { if (B.tma) launch_cols_tma<N>(B, a, true, B.rows_out, s); else launch_cols<N>(a, B.cols, true, B.rows_out, s); }
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
 #define NLG_F3_CASE(N) \

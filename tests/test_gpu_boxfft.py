@@ -74,6 +74,19 @@ def test_box_fft_eight_columns(N, n, monkeypatch):
     assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
 
 
+@pytest.mark.parametrize("n,dh", [(40, 6.0), (72, 6.0), (48, 4.0), (12, 6.0)])
+def test_box_fft_tma_columns(N, n, dh, monkeypatch):
+    """NLG_F3_TMA=1: the strided y passes through bulk tensor copies (tensor-map
+    row clipping for the zero padding and the y < n store) agree with the
+    per-thread path."""
+    u = _u(n)
+    monkeypatch.setenv("NLG_F3_TMA", "0")
+    ref = _op(N, n, dh).apply(u)
+    monkeypatch.setenv("NLG_F3_TMA", "1")
+    got = _op(N, n, dh).apply(u)
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
 def test_box_fft_without_kappa(N):
     op = _op(N, 40, 6.0, kappa=False)
     u = _u(40)
