@@ -42,7 +42,7 @@
 
 namespace nlg {
 
-constexpr int kTieTX = 32, kTieTY = 8, kTieZC = 64, kMaxTie = 64, kMaxTieR = 16;
+constexpr int kTieTX = 32, kTieTY = 8, kTieZC = 128, kMaxTie = 64, kMaxTieR = 16;
 
 struct TieGroups {
   int R, q, ngroup, ntie;   // q: gcd of the t0's (planes z + t0 share z's class mod q)
