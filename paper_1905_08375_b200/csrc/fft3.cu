@@ -80,14 +80,15 @@ using namespace stockham;
 constexpr int kF3El = 8;     // elements per thread per stage
 constexpr int kF3MaxG = 7;   // kernel support radius r_f <= 6 (partial spectra per column in registers)
 
-// Row passes: L / 8 threads, except the forward pass of lengths with radix-5
-// stages, L / 5 (one radix-5 butterfly per thread: 800-point PA 3.63 ms against
-// 4.47 ms; the inverse pass, which also runs the combine, is faster at L / 8).
-template <int L, bool INV>
-__host__ __device__ constexpr int rows_el() { return !INV && L % 5 == 0 ? 5 : kF3El; }
-template <int L, bool INV>
+// Row passes: L / 5 threads for lengths with radix-5 stages (one radix-5
+// butterfly per thread: 800-point PA 3.63 ms against 4.47 ms at L / 8, PE in
+// (A, B) mode 2.97 against 3.22 ms), except the inverse pass that applies the
+// combine, which is faster at L / 8.
+template <int L, bool CMB>
+__host__ __device__ constexpr int rows_el() { return !CMB && L % 5 == 0 ? 5 : kF3El; }
+template <int L, bool CMB>
 __host__ __device__ constexpr int rows_threads() {
-  return L / rows_el<L, INV>() < 32 ? 32 : (L / rows_el<L, INV>() > 256 ? 256 : L / rows_el<L, INV>());
+  return L / rows_el<L, CMB>() < 32 ? 32 : (L / rows_el<L, CMB>() > 256 ? 256 : L / rows_el<L, CMB>());
 }
 template <int L, int C>
 __host__ __device__ constexpr int cols_threads3() { return L * C / kF3El; }
@@ -111,9 +112,11 @@ struct F3Args {
 // PA / PE: one row (plane z, row y) per CTA along the contiguous x axis.
 // PA: z in [0, n_in); PE: z in output planes, combine into out (or, with a tie
 // band, (A, B) back into the row for the tie pass's combine).
-template <int L, bool INV, bool KW>
-__global__ void __launch_bounds__(rows_threads<L, INV>()) f3_rows(const __grid_constant__ F3Args a) {
-  constexpr int T = rows_threads<L, INV>();
+// AB (inverse only): store (A, B) into the row (the tie pass combines);
+// otherwise the inverse pass applies the combine (and then runs faster at L / 8).
+template <int L, bool INV, bool KW, bool AB = false>
+__global__ void __launch_bounds__(rows_threads<L, INV && !AB>()) f3_rows(const __grid_constant__ F3Args a) {
+  constexpr int T = rows_threads<L, INV && !AB>();
   __shared__ double2 sm[L + L / 8];
   const int64_t r = blockIdx.x;                      // row within the pass
   const int64_t zr = r / a.n, y = r % a.n;
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(rows_threads<L, INV>()) f3_rows(const __grid_c
         const int x = base + q * stride;
         if (x < a.n) {
           const double A = v[q].x, B = -v[q].y;      // conjugate: (conv u, conv kappa u)
-          if (a.ab) {                                // the row's own elements: read before (first stage)
+          if (AB) {                                  // the row's own elements: read before (first stage)
             zrow[x] = make_double2(A, B);
             continue;
           }
@@ -645,6 +648,8 @@ void launch_rows(const F3Args& a, bool inv, int64_t rows, cudaStream_t s) {
   if (!inv) {
     if (a.kappa) f3_rows<L, false, true><<<grid, TF, 0, s>>>(a);
     else f3_rows<L, false, false><<<grid, TF, 0, s>>>(a);
+  } else if (a.ab) {
+    f3_rows<L, true, false, true><<<grid, TF, 0, s>>>(a);
   } else {
     if (a.kappa) f3_rows<L, true, true><<<grid, TI, 0, s>>>(a);
     else f3_rows<L, true, false><<<grid, TI, 0, s>>>(a);
