@@ -132,3 +132,32 @@ def test_sharded_plans_match_unsharded(case, orc):
     # each shard fits its own far-tail exponential sum from its own horizons
     # (1-D FFT mode), so the 1-D case agrees to the fit level, not bit-near
     assert orc.rel_inf(got, ref) <= (1e-11 if case == "cfg1_small" else 1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_cfg1_full_size_slabs_as_in_bench(world, orc):
+    """The exact slab plans bench.py --gpus N builds for the headline cfg1
+    (2^22 nodes, 62916-cell halos), applied one after the other on this GPU,
+    reassemble to the single-plan output; each slab's FFT length comes from its
+    own input rows."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1905_08375_b200 import nonloc as N, configs
+    from paper_1905_08375_b200.slabs import Slab
+    w = configs.cfg1()
+    ref = N.NonlocalOperator(w.dim, w.n, **w.op_kwargs()).apply(w.u)
+    dmax = float(w.delta.max())
+    halo = N.halo_rows(dim=1, n=w.n, family=4, delta_max=dmax)
+    parts = []
+    for r in range(world):
+        sl = Slab(w.n, 1, halo, r, world)
+        kw = w.op_kwargs()
+        for key in ("delta", "coeff", "kappa"):
+            kw[key] = sl.input_slice(kw[key])
+        op = N.NonlocalOperator(1, w.n, row_begin=sl.row_begin, row_end=sl.row_end, reach=dmax, **kw)
+        assert op.info.fast_method == 2 and op.info.fft_len > 0
+        parts.append(op.apply(sl.input_slice(w.u)))
+    got = np.concatenate(parts)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
