@@ -1135,7 +1135,12 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   if (fft) {
     // circular convolution of length L >= n_in + Dmax: outputs in the slab see
     // no wrap-around (u is zero-padded); kernel w_d at +-d, 1 <= d <= Dmax
-    S->L = smooth_size(std::max<int64_t>(n_in + dmax + 1, 2 * dmax + 2));
+    {
+      const int64_t m = std::max<int64_t>(n_in + dmax + 1, 2 * dmax + 2);
+      const int64_t l4 = fourstep_length(m);   // a split with radix-5 columns can be tighter (cfg1: 4423680 vs 4718592)
+      S->L = smooth_size(m);
+      if (l4 > 0 && l4 < S->L) S->L = l4;
+    }
     const int64_t L = S->L;
     NLG_CUFFT(cufftPlan1d(&S->fplan, static_cast<int>(L), CUFFT_Z2Z, 1));
     // default priority: giving the FFT stream the highest one finishes the FFT

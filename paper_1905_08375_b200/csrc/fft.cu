@@ -278,9 +278,11 @@ FsDev dev_of(const FourStep& F) {
   return d;
 }
 
-// supported column lengths 2^a {1, 3, 9} in [64, 1536]
+// supported column lengths 2^a {1, 3, 9} in [64, 1536], plus 180, 320, 1080 (radix-5 stages:
+// tighter lengths for cfg1 and its 4- and 8-way slabs)
 #define NLG_FS_N1(X) \
-  X(64) X(72) X(96) X(128) X(144) X(192) X(256) X(288) X(384) X(512) X(576) X(768) X(1024) X(1152) X(1536)
+  X(64) X(72) X(96) X(128) X(144) X(180) X(192) X(256) X(288) X(320) X(384) X(512) X(576) X(768) X(1024) \
+  X(1080) X(1152) X(1536)
 
 template <int N1>
 size_t cols_smem() { return sizeof(double2) * N1 * cols_c<N1>(); }
@@ -337,6 +339,21 @@ double2* upload2(const std::vector<double2>& v) {
 #define NLG_FS_ROWS_FIRST 4096   // preferred row length when several splits exist (measured, cfg1:
                                  // 4096 x 1152 beats 8192 x 576 by 3%: two row CTAs per SM)
 #endif
+
+// Only the preferred 4096-row split with columns of at least 256 (measured:
+// 1080 x 4096 for cfg1 and 320 x 4096 for its 4-way slabs beat the next
+// 2^a {1,3,9} length; a 2048-row or a 180-column split does not).
+int64_t fourstep_length(int64_t m) {
+  const char* env = std::getenv("NLG_FS_ROWS");
+  if (env && std::atoi(env) != NLG_FS_ROWS_FIRST) return 0;   // forced splits / cuFFT: the 2^a {1,3,9} lengths
+  const int64_t n2 = NLG_FS_ROWS_FIRST;
+  int64_t best = 0;
+#define NLG_FS_CASE(N) \
+  if (N >= 256 && N * n2 >= m && (best == 0 || N * n2 < best)) best = N * n2;
+  NLG_FS_N1(NLG_FS_CASE)
+#undef NLG_FS_CASE
+  return best;
+}
 
 bool fourstep_plan(int64_t L, FourStep& F) {
   // NLG_FS_ROWS (environment, read at plan time): preferred row length, for tests

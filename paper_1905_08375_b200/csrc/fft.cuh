@@ -24,6 +24,9 @@ struct FourStep {
 // Plan for length L, or false when L has no supported split (the caller then
 // runs the cuFFT path).
 bool fourstep_plan(int64_t L, FourStep& F);
+// Smallest L >= m with the preferred 4096-row split and >= 256 columns (0 when
+// another split or the cuFFT path is forced through NLG_FS_ROWS).
+int64_t fourstep_length(int64_t m);
 // Device tables; kr = real kernel spectrum in natural order (length L).
 void fourstep_setup(FourStep& F, const double* kr, cudaStream_t s);
 void fourstep_free(FourStep& F);
