@@ -278,10 +278,10 @@ FsDev dev_of(const FourStep& F) {
   return d;
 }
 
-// supported column lengths 2^a {1, 3, 9} in [64, 1536], plus 180, 320, 1080 (radix-5 stages:
+// supported column lengths 2^a {1, 3, 9} in [64, 1536], plus 320 and 1080 (radix-5 stages:
 // tighter lengths for cfg1 and its 4- and 8-way slabs)
 #define NLG_FS_N1(X) \
-  X(64) X(72) X(96) X(128) X(144) X(180) X(192) X(256) X(288) X(320) X(384) X(512) X(576) X(768) X(1024) \
+  X(64) X(72) X(96) X(128) X(144) X(192) X(256) X(288) X(320) X(384) X(512) X(576) X(768) X(1024) \
   X(1080) X(1152) X(1536)
 
 template <int N1>

@@ -11,7 +11,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 FAST_TOL = 1e-10
 REPEAT_TOL = 1e-12
-N1_SUPPORTED = {64, 72, 96, 128, 144, 180, 192, 256, 288, 320, 384, 512, 576, 768, 1024, 1080, 1152, 1536}
+N1_SUPPORTED = {64, 72, 96, 128, 144, 192, 256, 288, 320, 384, 512, 576, 768, 1024, 1080, 1152, 1536}
 
 
 @pytest.fixture(scope="module")
