@@ -2,8 +2,9 @@
 //
 // match_polynomial: the even polynomial p(s) = sum_j c_j s^{2j} with
 //   p^(m)(1) = gamma^(m)(1), m = 0..K, for gamma = c/s (kernel.cpp:26-51, 184-207):
-//   sum_j ff(2j, m) c_j = c (-1)^m m!. Solved in exact rationals (K <= 6) so the
-//   coefficients are the correctly rounded quotients the reference produces.
+//   sum_j ff(2j, m) c_j = c (-1)^m m!. Solved in exact rationals for K <= 4 (the
+//   correctly rounded quotients the reference produces) and by a full-pivot fp64
+//   solve above that, as the reference does.
 // split_kernel: kappa(s) = c/s - p(s) written as c (1-s)^{K+1} tail(s) / s
 //   (kernel.cpp:209-245): tail = (1 - s p1(s)) / (1-s)^{K+1}, exact division.
 #include <algorithm>
@@ -78,11 +79,56 @@ std::vector<Q> matching_exact(int K) {
   return out;
 }
 
+// K > 4: the matching system in fp64 with complete pivoting (the reference
+// switches to a double full-pivot LU there, kernel.cpp:53-70,203-205). The
+// largest remaining entry is the pivot at every step; a zero pivot is the
+// reference's "singular matching system".
+std::vector<double> matching_double(int K, double c) {
+  const int n = K + 1;
+  if (K > 12) throw Error{NLG_EUNSUPPORTED, "matching order > 12 overflows the system's factorials"};
+  std::vector<std::vector<double>> a(n, std::vector<double>(n));
+  std::vector<double> b(n);
+  for (int m = 0; m < n; ++m) {
+    for (int j = 0; j < n; ++j) a[m][j] = 2 * j >= m ? static_cast<double>(falling(2 * j, m)) : 0.0;
+    b[m] = c * (m % 2 == 0 ? 1.0 : -1.0) * static_cast<double>(falling(m, m));
+  }
+  std::vector<int> colperm(n);
+  for (int j = 0; j < n; ++j) colperm[j] = j;
+  for (int k = 0; k < n; ++k) {
+    int pr = k, pc = k;
+    double best = 0.0;
+    for (int r = k; r < n; ++r)
+      for (int q = k; q < n; ++q)
+        if (std::fabs(a[r][q]) > best) { best = std::fabs(a[r][q]); pr = r; pc = q; }
+    if (best == 0.0) throw Error{NLG_ERUNTIME, "singular matching system"};
+    std::swap(a[k], a[pr]);
+    std::swap(b[k], b[pr]);
+    if (pc != k) {
+      for (int r = 0; r < n; ++r) std::swap(a[r][k], a[r][pc]);
+      std::swap(colperm[k], colperm[pc]);
+    }
+    for (int r = k + 1; r < n; ++r) {
+      const double f = a[r][k] / a[k][k];
+      if (f == 0.0) continue;
+      for (int q = k; q < n; ++q) a[r][q] -= f * a[k][q];
+      b[r] -= f * b[k];
+    }
+  }
+  std::vector<double> y(n), x(n);
+  for (int r = n - 1; r >= 0; --r) {
+    double acc = b[r];
+    for (int q = r + 1; q < n; ++q) acc -= a[r][q] * y[q];
+    y[r] = acc / a[r][r];
+  }
+  for (int j = 0; j < n; ++j) x[colperm[j]] = y[j];
+  return x;
+}
+
 }  // namespace
 
 std::vector<double> match_polynomial(int K, double c) {
   if (K < 0) throw Error{NLG_EINVAL, "matching order must be >= 0"};
-  if (K > 6) throw Error{NLG_EUNSUPPORTED, "matching order > 6 is not supported"};
+  if (K > 4) return matching_double(K, c);
   const auto ex = matching_exact(K);
   std::vector<double> out;
   for (const Q& r : ex)
@@ -101,6 +147,23 @@ void match_polynomial_exact(int K, int64_t* num, int64_t* den) {
 
 void split_kernel(int K, double c, std::vector<double>& poly, std::vector<double>& tail) {
   poly = match_polynomial(K, c);
+  if (K > 4) {
+    // fp64 division of c - s p(s) by (1 - s)^{K+1}; the remainder must vanish
+    // to 1e-9 |c| at every step (kernel.cpp:232-242)
+    std::vector<double> num(2 * K + 2, 0.0);
+    num[0] = c;
+    for (int j = 0; j <= K; ++j) num[2 * j + 1] -= poly[j];
+    for (int i = 0; i <= K; ++i) {
+      std::vector<double> q(num.size() - 1);
+      q[0] = num[0];
+      for (std::size_t k = 1; k < q.size(); ++k) q[k] = num[k] + q[k - 1];
+      if (std::fabs(num.back() + q.back()) > 1e-9 * std::fabs(c))
+        throw Error{NLG_ERUNTIME, "split: kappa does not vanish to order K"};
+      num = std::move(q);
+    }
+    tail = std::move(num);
+    return;
+  }
   const auto p1 = matching_exact(K);
   // numerator of 1/s - p1(s) over the common denominator s: 1 - s p1(s)
   std::vector<Q> num(2 * K + 2, Q(0));

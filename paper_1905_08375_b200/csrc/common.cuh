@@ -39,6 +39,17 @@ struct Geom {
   int64_t in_begin, in_end;    // input rows
 };
 
+// Relative half-width of the tie band around (delta/h)^2 in which integer
+// |d|^2 classification defers to the reference's float predicate. The
+// predicate's r2 carries a relative error up to ~7 eps n / |d| when h = 1/n is
+// inexact (non-power-of-two n), so the band grows with n: 1e-12 + 8 eps n.
+__host__ __device__ __forceinline__ double tie_band(double h) {
+  return 1e-12 + 8.0 * 2.220446049250313e-16 / h;
+}
+__host__ __device__ __forceinline__ double tie_band_n(double inv_h) {
+  return 1e-12 + 8.0 * 2.220446049250313e-16 * inv_h;
+}
+
 __device__ __forceinline__ double coord(int64_t k, double h) {
   return __dmul_rn(__dadd_rn(static_cast<double>(k), 0.5), h);
 }

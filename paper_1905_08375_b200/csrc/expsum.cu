@@ -824,14 +824,6 @@ __global__ void __launch_bounds__(kCombineThreads) es_near_combine(CombineArgs a
   }
 }
 
-template <typename T>
-T* upload(const std::vector<T>& v) {
-  T* d = nullptr;
-  NLG_CUDA(cudaMalloc(&d, sizeof(T) * std::max<size_t>(v.size(), 1)));
-  if (!v.empty()) NLG_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
-    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
-  return d;
-}
 
 // exact per-node horizon extents D^+- (Point rule dist < delta with the
 // reference's operation order, operators.cpp:71-78, geometry.cpp:78-84)
@@ -1063,7 +1055,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
       T[4 * kMT + k] = t;
     }
   }
-  S->ctab = upload(ctab);
+  S->ctab = upload_on(ctab, P.stream);
   if (fft) {   // tail walks: all terms in chunk 0
     if (S->nchunks != 1 || M > kTailMT) throw Error{NLG_ERUNTIME, "expsum: tail walk needs <= 16 terms in one chunk"};
     for (int k = 0; k < kTailMT; ++k) {
@@ -1092,7 +1084,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
       ca.slow[c] = 0;
       for (int k = 0; k < e - b; ++k) ta[static_cast<size_t>(c) * kTabRows * kMT + k] = std::exp(-es.rate[b + k]);
     }
-    S->ctab_agg = upload(ta);
+    S->ctab_agg = upload_on(ta, P.stream);
     ca.tab = S->ctab_agg;
   }
   S->cp.n = S->nchunks;
@@ -1108,22 +1100,22 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
     rate[m] = es.rate[m];
     segpow[m] = std::exp(-es.rate[m] * kL);
   }
-  S->rate = upload(rate);
-  S->segpow = upload(segpow);
+  S->rate = upload_on(rate, P.stream);
+  S->segpow = upload_on(segpow, P.stream);
   std::vector<double> segpw(static_cast<size_t>(kMT) * 32, 0.0);
   for (int m = 0; m < M; ++m)
     for (int l = 0; l < 32; ++l) segpw[m * 32 + l] = std::exp(-es.rate[m] * kL * (31 - l));
-  S->segpw = upload(segpw);
-  S->dplus = upload(dplus);
-  S->dminus = upload(dminus);
-  S->tinfoR = upload(tR);
-  S->tinfoL = upload(tL);
+  S->segpw = upload_on(segpw, P.stream);
+  S->dplus = upload_on(dplus, P.stream);
+  S->dminus = upload_on(dminus, P.stream);
+  S->tinfoR = upload_on(tR, P.stream);
+  S->tinfoL = upload_on(tL, P.stream);
   // weights |d|^-alpha, d = 0..dmax (w_0 unused)
   std::vector<double> wt(static_cast<size_t>(dmax) + 1, 0.0);
   for (int64_t k = 1; k <= dmax; ++k) wt[k] = std::pow(static_cast<double>(k), -d.alpha);
   std::vector<double> wn(wt.begin(), wt.begin() + std::min<int64_t>(dmax, kNear) + 1);
   wn.resize(kNear + 1, 0.0);
-  S->wnear = upload(wn);
+  S->wnear = upload_on(wn, P.stream);
   // scale s_i = h^{1-alpha} C_i (x 1/2 with kappa)
   const double hs = std::pow(h, 1.0 - d.alpha);
   std::vector<double> sc(n_out);
@@ -1131,7 +1123,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
     const double c = d.coeff ? d.coeff[o0 + i] : d.coeff0;
     sc[i] = (d.kappa ? 0.5 : 1.0) * hs * c;
   }
-  S->scale = upload(sc);
+  S->scale = upload_on(sc, P.stream);
   if (fft) {
     // circular convolution of length L >= n_in + Dmax: outputs in the slab see
     // no wrap-around (u is zero-padded); kernel w_d at +-d, 1 <= d <= Dmax
@@ -1161,8 +1153,7 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
       kh[k].x = w;
       kh[L - k].x = w;
     }
-    NLG_CUDA(cudaMemcpy(S->z, kh.data(), sizeof(cufftDoubleComplex) * L, cudaMemcpyHostToDevice));
-    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
+    NLG_CUDA(cudaMemcpyAsync(S->z, kh.data(), sizeof(cufftDoubleComplex) * L, cudaMemcpyHostToDevice, P.stream));
     NLG_CUFFT(cufftSetStream(S->fplan, P.stream));
     NLG_CUFFT(cufftExecZ2Z(S->fplan, S->z, S->z, CUFFT_FORWARD));
     fft_real_part<<<static_cast<unsigned>((L + 255) / 256), 256, 0, P.stream>>>(S->z, S->kr, L);   // symmetric: real
@@ -1217,15 +1208,14 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
       const double ki = d.kappa ? d.kappa[o0 + i] : 1.0;
       ext[i] = d.kappa ? e * (ki + ki) : e;
     }
-    ext_dev = upload(ext);
+    ext_dev = upload_on(ext, P.stream);
   }
   // diag = the fast operator's own X for u = 1 (consistent far field) + exterior
   double* ones = nullptr;
   NLG_CUDA(cudaMalloc(&ones, sizeof(double) * n_in));
   {
     std::vector<double> o(static_cast<size_t>(n_in), 1.0);
-    NLG_CUDA(cudaMemcpy(ones, o.data(), sizeof(double) * n_in, cudaMemcpyHostToDevice));
-    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
+    NLG_CUDA(cudaMemcpyAsync(ones, o.data(), sizeof(double) * n_in, cudaMemcpyHostToDevice, P.stream));
   }
   P.fast_method = 2;
   expsum_run(P, ones, S->diag, P.stream, 1, ext_dev);

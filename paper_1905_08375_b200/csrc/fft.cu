@@ -326,12 +326,6 @@ std::vector<double2> twiddles(int64_t n, int64_t count, int64_t step) {   // exp
   return t;
 }
 
-double2* upload2(const std::vector<double2>& v) {
-  double2* p = nullptr;
-  NLG_CUDA(cudaMalloc(&p, sizeof(double2) * v.size()));
-  NLG_CUDA(cudaMemcpy(p, v.data(), sizeof(double2) * v.size(), cudaMemcpyHostToDevice));
-  return p;
-}
 
 }  // namespace
 
@@ -372,11 +366,10 @@ bool fourstep_plan(int64_t L, FourStep& F) {
 }
 
 void fourstep_setup(FourStep& F, const double* kr, cudaStream_t s) {
-  F.tw1 = upload2(twiddles(F.n1, F.n1, 1));
-  F.tw2 = upload2(twiddles(F.n2, F.n2, 1));
-  F.twa = upload2(twiddles(F.L, F.L / kFsTwB + 1, kFsTwB));
-  F.twb = upload2(twiddles(F.L, kFsTwB, 1));
-  NLG_CUDA(cudaDeviceSynchronize());   // pageable uploads complete before any stream work
+  F.tw1 = upload_on(twiddles(F.n1, F.n1, 1), s);
+  F.tw2 = upload_on(twiddles(F.n2, F.n2, 1), s);
+  F.twa = upload_on(twiddles(F.L, F.L / kFsTwB + 1, kFsTwB), s);
+  F.twb = upload_on(twiddles(F.L, kFsTwB, 1), s);
   NLG_CUDA(cudaMalloc(&F.krp, sizeof(double) * F.L));
   fs_permute<<<static_cast<unsigned>((F.L + 255) / 256), 256, 0, s>>>(kr, F.krp, F.n1, F.n2,
                                                                       1.0 / static_cast<double>(F.L));

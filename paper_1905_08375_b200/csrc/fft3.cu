@@ -4,7 +4,7 @@
 //
 // With a constant horizon every interior target sees the same offset set
 // N = {d : |d|^2 < m_lo} (|d|^2 in cells, m_lo the bottom of the tie band
-// (delta/h)^2 (1 -+ 1e-12), stencil.cu Ball::init), and
+// (delta/h)^2 (1 -+ tie_band), stencil.cu Ball::init), and
 //   A_i = sum_{d in N} w(d) u_{i+d},   B_i = sum_{d in N} w(d) (kappa u)_{i+d}
 // is a convolution of f = u + i kappa u (two real fields in one complex
 // signal) with the real, even kernel w(d) = |d|^-alpha. On a box zero-padded
@@ -691,13 +691,6 @@ std::vector<double> costab(int n) {
   for (int i = 0; i < n; ++i) t[i] = static_cast<double>(std::cos(pi2 * static_cast<long double>(i) / n));
   return t;
 }
-template <typename T>
-T* upload3(const std::vector<T>& v) {
-  T* p = nullptr;
-  NLG_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(v.size(), 1)));
-  if (!v.empty()) NLG_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
-  return p;
-}
 
 F3Args args_of(const Plan& P, const BoxFft& B) {
   F3Args a;
@@ -783,8 +776,8 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   if (g.dim != 3 || P.d_delta || P.family != NLG_FRACTIONAL) return nullptr;
   // tie band exactly as stencil.cu Ball::init
   const double e = P.delta0 / g.h, e2 = e * e;
-  const int mlo = static_cast<int>(std::ceil(e2 * (1.0 - 1e-12)));
-  const int mhi = static_cast<int>(std::floor(e2 * (1.0 + 1e-12)));
+  const int mlo = static_cast<int>(std::ceil(e2 * (1.0 - tie_band(g.h))));
+  const int mhi = static_cast<int>(std::floor(e2 * (1.0 + tie_band(g.h))));
   int rf = 0;
   while ((rf + 1) * (rf + 1) < mlo) ++rf;         // largest component inside the strict ball
   if (rf < 1 || rf + 1 > kF3MaxG) return nullptr;
@@ -857,10 +850,10 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
     B->tie_w = std::pow(static_cast<double>(m), -0.5 * alpha);
     B->tie_thr = sqrt_threshold_host(P.delta0);
   }
-  B->twx = upload3(twiddles3(lx));
+  B->twx = upload_on(twiddles3(lx), P.stream);
   B->twy = B->twx;
-  double* dw = upload3(w);
-  double* cx = upload3(costab(lx));
+  double* dw = upload_on(w, P.stream);
+  double* cx = upload_on(costab(lx), P.stream);
   NLG_CUDA(cudaMalloc(&B->g, sizeof(double) * static_cast<size_t>(lx) * lx * G));
   NLG_CUDA(cudaMalloc(&B->z, sizeof(double2) * static_cast<size_t>(n_in) * lx * lx));
   {
@@ -877,7 +870,6 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
                encode_cols_map(&B->pd_out, zo, lx, lx, n, B->rows_out, br);
     }
   }
-  NLG_CUDA(cudaDeviceSynchronize());
   const double scale = 1.0 / (static_cast<double>(lx) * lx);
   f3_spectrum<<<static_cast<unsigned>((static_cast<int64_t>(lx) * lx + 255) / 256), 256, 0, P.stream>>>(
       dw, rf, lx, lx, cx, cx, scale, B->g);

@@ -194,6 +194,7 @@ double eval_profile(const RadialProfile& p, double s) {
 MatchedPolynomial match_polynomial(const RadialProfile& profile, int K) {
   if (profile.family != ProfileFamily::InverseS)
     throw std::invalid_argument("match_polynomial requires the InverseS profile");
+  if (K < 0) throw std::invalid_argument("matching order must be >= 0");
   MatchedPolynomial m;
   m.order = K;
   m.coeffs.resize(K + 1);
@@ -209,6 +210,7 @@ MatchedPolynomial match_polynomial(const RadialProfile& profile, int K) {
 SplitKernel split(const RadialProfile& profile, int K) {
   if (profile.family != ProfileFamily::InverseS)
     throw std::invalid_argument("match_polynomial requires the InverseS profile");
+  if (K < 0) throw std::invalid_argument("matching order must be >= 0");
   SplitKernel sk;
   sk.scale = profile.c;
   sk.polynomial = match_polynomial(profile, K);
@@ -371,9 +373,13 @@ TruncatedOperator::TruncatedOperator(const KernelSpec& spec, const Grid& grid) :
   const int K = spec.profile.order;
   if (grid.dim >= 2 && K != 0) throw std::invalid_argument("K > 0 is supported in 1d only");
   if (grid.dim == 1 && K > 3) throw std::invalid_argument("K <= 3 in 1d");
+  make_plan();
+}
+
+void TruncatedOperator::make_plan() {
   NodeArrays na;
-  nlg_desc d = make_desc(spec, grid, na);
-  set_profile(d, spec.profile, na);
+  nlg_desc d = make_desc(spec_, grid_, na);
+  set_profile(d, spec_.profile, na);
   d.route = NLG_ROUTE_TRUNCATED;
   d.rule = NLG_LEAF;
   d.form = NLG_MASS;
@@ -382,10 +388,41 @@ TruncatedOperator::TruncatedOperator(const KernelSpec& spec, const Grid& grid) :
 
 TruncatedOperator::~TruncatedOperator() { nlg_plan_destroy(plan_); }
 
+TruncatedOperator::TruncatedOperator(const TruncatedOperator& o)
+    : spec_(o.spec_), grid_(o.grid_), applies_(o.applies_), tree_(o.tree_), have_totals_(o.have_totals_),
+      recur_(o.recur_), panels_(o.panels_), decomp_(o.decomp_) {
+  make_plan();
+}
+
+TruncatedOperator& TruncatedOperator::operator=(const TruncatedOperator& o) {
+  if (this != &o) {
+    TruncatedOperator tmp(o);
+    *this = std::move(tmp);
+  }
+  return *this;
+}
+
 TruncatedOperator::TruncatedOperator(TruncatedOperator&& o) noexcept
     : spec_(std::move(o.spec_)), grid_(o.grid_), plan_(o.plan_), applies_(o.applies_), tree_(o.tree_),
       have_totals_(o.have_totals_), recur_(o.recur_), panels_(o.panels_), decomp_(std::move(o.decomp_)) {
   o.plan_ = nullptr;
+}
+
+TruncatedOperator& TruncatedOperator::operator=(TruncatedOperator&& o) noexcept {
+  if (this != &o) {
+    nlg_plan_destroy(plan_);
+    spec_ = std::move(o.spec_);
+    grid_ = o.grid_;
+    plan_ = o.plan_;
+    o.plan_ = nullptr;
+    applies_ = o.applies_;
+    tree_ = std::move(o.tree_);
+    have_totals_ = o.have_totals_;
+    recur_ = o.recur_;
+    panels_ = o.panels_;
+    decomp_ = std::move(o.decomp_);
+  }
+  return *this;
 }
 
 std::vector<double> TruncatedOperator::apply(std::span<const double> u) {

@@ -193,6 +193,9 @@ nlg_status nlg_plan_create(const nlg_desc* desc, nlg_plan** out) {
       if (sharded && d.delta) require(dm <= d.reach, "reach must bound every delta");
     }
     require(P.delta_max > 0.0, "radius must be positive");
+    // nlgpu.h: reach <= 0 means the max delta. With the divergence horizon
+    // (delta_x + delta_y)/2 can exceed delta_x, so the window must use it.
+    if (P.reach <= 0.0 && P.divergence) P.reach = P.delta_max;
     P.halo_lo = std::min<int64_t>(halo, g.row_begin);
     P.halo_hi = std::min<int64_t>(halo, d.n - g.row_end);
     g.in_begin = g.row_begin - P.halo_lo;
@@ -205,18 +208,15 @@ nlg_status nlg_plan_create(const nlg_desc* desc, nlg_plan** out) {
     const size_t bytes_in = sizeof(double) * static_cast<size_t>(P.n_in);
     if (d.delta) {
       NLG_CUDA(cudaMalloc(&P.d_delta, bytes_in));
-      NLG_CUDA(cudaMemcpy(P.d_delta, d.delta, bytes_in, cudaMemcpyHostToDevice));
-    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
+      NLG_CUDA(cudaMemcpyAsync(P.d_delta, d.delta, bytes_in, cudaMemcpyHostToDevice, P.stream));
     }
     if (d.coeff) {
       NLG_CUDA(cudaMalloc(&P.d_coeff, bytes_in));
-      NLG_CUDA(cudaMemcpy(P.d_coeff, d.coeff, bytes_in, cudaMemcpyHostToDevice));
-    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
+      NLG_CUDA(cudaMemcpyAsync(P.d_coeff, d.coeff, bytes_in, cudaMemcpyHostToDevice, P.stream));
     }
     if (d.kappa) {
       NLG_CUDA(cudaMalloc(&P.d_kappa, bytes_in));
-      NLG_CUDA(cudaMemcpy(P.d_kappa, d.kappa, bytes_in, cudaMemcpyHostToDevice));
-    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
+      NLG_CUDA(cudaMemcpyAsync(P.d_kappa, d.kappa, bytes_in, cudaMemcpyHostToDevice, P.stream));
     }
     NLG_CUDA(cudaMalloc(&P.d_pairs, sizeof(unsigned long long)));
 

@@ -25,6 +25,19 @@ struct Error {
       throw ::nlg::Error{NLG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
   } while (0)
 
+// Plan-time uploads, ordered on the plan stream. A pageable source is staged
+// before cudaMemcpyAsync returns, so the host buffer may be freed right after;
+// kernels on the same stream see the data without a device-wide sync.
+template <typename T>
+T* upload_on(const T* src, size_t count, cudaStream_t s) {
+  T* d = nullptr;
+  NLG_CUDA(cudaMalloc(&d, sizeof(T) * (count ? count : 1)));
+  if (count) NLG_CUDA(cudaMemcpyAsync(d, src, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+  return d;
+}
+template <typename T>
+T* upload_on(const std::vector<T>& v, cudaStream_t s) { return upload_on(v.data(), v.size(), s); }
+
 // 1-D exponential-sum far field (fast method 2).
 struct ExpSum {
   int terms = 0;          // M

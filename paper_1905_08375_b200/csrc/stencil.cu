@@ -123,8 +123,8 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
   const double e = delta / h;                       // horizon in cells
   // integer band: m < mlo surely in, m > mhi surely out, else float predicate
   const double e2 = e * e;
-  const int mlo = live ? static_cast<int>(ceil(e2 * (1.0 - 1e-12))) : 0;
-  const int mhi = live ? static_cast<int>(floor(e2 * (1.0 + 1e-12))) : -1;
+  const int mlo = live ? static_cast<int>(ceil(e2 * (1.0 - tie_band(h)))) : 0;
+  const int mhi = live ? static_cast<int>(floor(e2 * (1.0 + tie_band(h)))) : -1;
   const int R = live ? static_cast<int>(floor(e)) + 1 : 0;
   int Rw = R;   // warp-uniform extent
 #pragma unroll
@@ -262,8 +262,8 @@ struct Ball {
     delta = dl;
     h = hh;
     const double e = dl / hh, e2 = e * e;
-    mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
-    mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+    mlo = static_cast<int>(ceil(e2 * (1.0 - tie_band(hh))));
+    mhi = static_cast<int>(floor(e2 * (1.0 + tie_band(hh))));
     tie = mlo <= mhi;
   }
   __device__ __forceinline__ bool in(const int* d) const {
@@ -335,7 +335,7 @@ __device__ __forceinline__ void row_sum(const double2* v, const double* w, int x
 // quarter warp reads on disjoint banks. Afterwards each target removes the
 // offsets of the sweep outside its own span (|k| > X_r, uniform loop over the
 // warp's narrowest..widest span) and adds the offsets of its tie band
-// ((delta/h)^2 within 1e-12) decided by the reference's float predicate.
+// ((delta/h)^2 within tie_band, common.cuh) decided by the reference's float predicate.
 // R targets per lane: a warp covers 32/R lanes x R targets = 32 columns by R
 // rows, a CTA 32/R warps stacked along y = 32 x 32 targets.
 constexpr int kBX = 32, kBY = 32;
@@ -512,8 +512,8 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
     if (yok && ix < n) {
       const int64_t ii = in_index(ix);
       const double e = (a.delta ? a.delta[ii] : a.delta0) * inv_h, e2 = e * e;
-      const int mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
-      const int mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+      const int mlo = static_cast<int>(ceil(e2 * (1.0 - tie_band_n(inv_h))));
+      const int mhi = static_cast<int>(floor(e2 * (1.0 + tie_band_n(inv_h))));
       M[r] = mlo <= mhi ? mlo - 1 : mhi;
       if (mlo <= mhi) tiem |= 1u << r;
       Mn = min(Mn, M[r]);
@@ -527,8 +527,8 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
   double Tc = 0.0;
   if (tie_const) {
     const double e = a.delta0 * inv_h, e2 = e * e;
-    const int mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
-    const int mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+    const int mlo = static_cast<int>(ceil(e2 * (1.0 - tie_band_n(inv_h))));
+    const int mhi = static_cast<int>(floor(e2 * (1.0 + tie_band_n(inv_h))));
     if (mlo <= mhi) {
       m0c = mlo;
       Tc = sqrt_threshold(a.delta0);
@@ -742,8 +742,8 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
       const int64_t ix = x0 + kRX * tx + rr;
       const double delta = a.delta ? a.delta[in_index(ix)] : a.delta0;
       const double e = delta * inv_h, e2 = e * e;
-      const int mlo = static_cast<int>(ceil(e2 * (1.0 - 1e-12)));
-      const int mhi = static_cast<int>(floor(e2 * (1.0 + 1e-12)));
+      const int mlo = static_cast<int>(ceil(e2 * (1.0 - tie_band_n(inv_h))));
+      const int mhi = static_cast<int>(floor(e2 * (1.0 + tie_band_n(inv_h))));
       const int64_t ki[3] = {DIM == 2 ? iy : z, DIM == 2 ? ix : iy, ix};
       const int Ry = isqrt_floor(mhi - dz2);
       double t0 = 0.0, t1 = 0.0;
@@ -892,14 +892,6 @@ __global__ void pack_kernel(const double* u, const double* kappa, int64_t n, dou
   }
 }
 
-template <typename T>
-T* upload_vec(const std::vector<T>& v) {
-  T* d = nullptr;
-  NLG_CUDA(cudaMalloc(&d, sizeof(T) * std::max<size_t>(v.size(), 1)));
-  if (!v.empty()) NLG_CUDA(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
-    NLG_CUDA(cudaDeviceSynchronize());   // pageable H2D may still be in flight (non-blocking plan stream)
-  return d;
-}
 
 template <int DIM, int KIND, int MODE, bool KW>
 void launch_t(const StArgs& a, cudaStream_t s, size_t smem) {
@@ -1052,11 +1044,11 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
           if (m == 0) continue;
           w[(static_cast<size_t>(az) * ny + ay) * W2 + dx + H] = std::pow(static_cast<double>(m), -0.5 * d.alpha);
         }
-    S->wtab = upload_vec(w);
+    S->wtab = upload_on(w, P.stream);
     S->tab_bytes = w.size() * sizeof(double);
   } else {
-    const int W2 = S->ws, P = (2 * H + 1) * W2;
-    std::vector<double> t(static_cast<size_t>(3 * P), 0.0);
+    const int W2 = S->ws, TP = (2 * H + 1) * W2;
+    std::vector<double> t(static_cast<size_t>(3 * TP), 0.0);
     for (int dy = -H; dy <= H; ++dy)
       for (int dx = -H; dx <= H; ++dx) {
         const double r2 = static_cast<double>(dx * dx + dy * dy);
@@ -1064,10 +1056,10 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
         const double r3 = r2 * std::sqrt(r2);
         const int k = (dy + H) * W2 + (dx + H);
         t[k] = dy * dy / r3;                 // axis 0 = "x" component of the SoA planes
-        t[P + k] = dx * dy / r3;
-        t[2 * P + k] = dx * dx / r3;
+        t[TP + k] = dx * dy / r3;
+        t[2 * TP + k] = dx * dx / r3;
       }
-    S->mtab = upload_vec(t);
+    S->mtab = upload_on(t, P.stream);
     S->tab_bytes = t.size() * sizeof(double);
   }
   // s_i: fractional h^{d-alpha} C_i (x 1/2 with kappa); peridynamic -h^{d-1} c_i
@@ -1079,7 +1071,7 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
     const int64_t x = P.halo_lo * g.stride0 + i;
     sc[i] = f * (d.coeff ? d.coeff[x] : d.coeff0);
   }
-  S->scale = upload_vec(sc);
+  S->scale = upload_on(sc, P.stream);
   S->scale_const = d.coeff == nullptr;
   S->scale0 = sc.empty() ? 0.0 : sc[0];
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * P.n_out * (peri ? 3 : 1)));

@@ -37,11 +37,13 @@ class Slab:
         self.in_begin = self.row_begin - self.halo_lo
         self.in_end = self.row_end + self.halo_hi
         own = self.row_end - self.row_begin
-        for r in (self.rank - 1, self.rank + 1):
-            if 0 <= r < self.world:
-                rb, re = slab_rows(self.n, self.world, r)
-                if re - rb < self.halo and not (r == 0 or r == self.world - 1):
-                    raise ValueError("halo wider than a neighbouring slab; use fewer ranks")
+        # slab_rows is deterministic, so every rank checks every interior slab
+        # and all ranks raise together (an undersized slab would otherwise
+        # leave its neighbours' halos short and block in the exchange)
+        for r in range(1, self.world - 1):
+            rb, re = slab_rows(self.n, self.world, r)
+            if re - rb < self.halo:
+                raise ValueError("halo wider than an interior slab; use fewer ranks")
         if own < 1:
             raise ValueError("empty slab")
 
