@@ -141,9 +141,11 @@ nlg_status nlg_apply_direct_dev(nlg_plan* plan, const double* u_dev, double* out
                                 int64_t* pair_count_dev, void* stream);
 
 /* Direct apply at a subset of output nodes (flat indices into the output
- * slab); used for sampled parity at BASELINE sizes. Host pointers, blocking. */
+ * slab); used for sampled parity at BASELINE sizes. Host pointers, blocking.
+ * pair_count (optional) receives the pairs summed over those targets, counted
+ * as the reference's pair_count (operators.cpp:193,225,253). */
 nlg_status nlg_apply_direct_at(nlg_plan* plan, const double* u, const int64_t* targets,
-                               int64_t ntargets, double* out);
+                               int64_t ntargets, double* out, int64_t* pair_count);
 
 /* Counters in the reference's semantics: pairs summed by the last direct apply
  * (operators.cpp:193,225,253); number of fast applies issued. */

@@ -57,7 +57,7 @@ EXPORTS = {
     "nlg_apply_direct": ([C.c_void_p, _dp, _dp, _ip], C.c_int),
     "nlg_apply_fast_dev": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "nlg_apply_direct_dev": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
-    "nlg_apply_direct_at": ([C.c_void_p, _dp, _ip, C.c_int64, _dp], C.c_int),
+    "nlg_apply_direct_at": ([C.c_void_p, _dp, _ip, C.c_int64, _dp, _ip], C.c_int),
     "nlg_counters": ([C.c_void_p, _ip, _ip], C.c_int),
     "nlg_set_profiling": ([C.c_void_p, C.c_int], C.c_int),
     "nlg_stage_times": ([C.c_void_p, _dp, _ip, C.POINTER(C.c_int)], C.c_int),

@@ -383,7 +383,7 @@ nlg_status nlg_apply_direct_dev(nlg_plan* plan, const double* u_dev, double* out
 }
 
 nlg_status nlg_apply_direct_at(nlg_plan* plan, const double* u, const int64_t* targets,
-                               int64_t ntargets, double* out) {
+                               int64_t ntargets, double* out, int64_t* pair_count) {
   return guard([&] {
     require(plan && u && targets && out && ntargets >= 0, "null argument");
     Plan& P = plan->p;
@@ -402,13 +402,17 @@ nlg_status nlg_apply_direct_at(nlg_plan* plan, const double* u, const int64_t* t
     NLG_CUDA(cudaMalloc(&d_o, sizeof(double) * nc * std::max<int64_t>(ntargets, 1)));
     NLG_CUDA(cudaMemcpyAsync(P.d_u, u, sizeof(double) * nc * P.n_in, cudaMemcpyHostToDevice, P.stream));
     NLG_CUDA(cudaMemcpyAsync(P.d_targets, targets, sizeof(int64_t) * ntargets, cudaMemcpyHostToDevice, P.stream));
-    launch_direct(P, P.d_u, d_o, P.d_targets, ntargets, nullptr, P.stream);
+    NLG_CUDA(cudaMemsetAsync(P.d_pairs, 0, sizeof(unsigned long long), P.stream));
+    launch_direct(P, P.d_u, d_o, P.d_targets, ntargets, P.d_pairs, P.stream);
+    unsigned long long pairs = 0;
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(out, d_o, sizeof(double) * nc * ntargets, cudaMemcpyDeviceToHost, P.stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&pairs, P.d_pairs, sizeof(pairs), cudaMemcpyDeviceToHost, P.stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(P.stream);
     cudaFree(d_o);
     if (e != cudaSuccess) throw Error{NLG_ECUDA, cudaGetErrorString(e)};
+    if (pair_count) *pair_count = static_cast<int64_t>(pairs);
   });
 }
 

@@ -256,13 +256,16 @@ class Plan:
         A.check(A.lib().nlg_apply_direct(self._h, A.dptr(u), A.dptr(out), C.byref(pairs)))
         return out, pairs.value
 
-    def apply_direct_at(self, u, targets) -> np.ndarray:
+    def apply_direct_at(self, u, targets, return_pairs: bool = False):
+        """Direct sum at the given output nodes; with return_pairs, also the
+        number of pairs summed (the reference's pair_count semantics)."""
         u = self._u(u)
         t = np.ascontiguousarray(targets, dtype=np.int64)
         out = np.empty(self.components * len(t))
+        pairs = C.c_int64(0)
         A.check(A.lib().nlg_apply_direct_at(self._h, A.dptr(u), t.ctypes.data_as(A._ip), len(t),
-                                            A.dptr(out)))
-        return out
+                                            A.dptr(out), C.byref(pairs)))
+        return (out, pairs.value) if return_pairs else out
 
     def apply_fast_dev(self, u_ptr: int, out_ptr: int, stream: int = 0) -> None:
         A.check(A.lib().nlg_apply_fast_dev(self._h, C.c_void_p(u_ptr), C.c_void_p(out_ptr),
@@ -568,8 +571,8 @@ class NonlocalOperator:
     def apply_direct(self, u):
         return self.plan.apply_direct(u)
 
-    def apply_direct_at(self, u, targets):
-        return self.plan.apply_direct_at(u, targets)
+    def apply_direct_at(self, u, targets, return_pairs: bool = False):
+        return self.plan.apply_direct_at(u, targets, return_pairs)
 
 
 # ---------------------------------------------------------------------------

@@ -143,3 +143,32 @@ def test_box_fft_singularity_orders(N, s):
     fast = op.apply(u)
     direct, _ = op.apply_direct(u)
     assert np.max(np.abs(fast - direct)) <= FAST_TOL * np.max(np.abs(direct))
+
+
+@pytest.mark.parametrize("n,dh", [(32, 6.0), (48, 4.0), (40, 5.0), (72, 6.0), (12, 6.0)])
+@pytest.mark.parametrize("exterior", [0, 1])
+def test_box_fft_vs_oracle(N, orc, n, dh, exterior):
+    """Oracle leg: the box FFT route against the restated CPU direct sum
+    (oracle/nonloc_oracle.c, pinned to the compiled reference's
+    apply_full_dense + eval_omega, operators.cpp:236-260, kernel.cpp:275-287)
+    on every face layer and random interior nodes; the GPU direct sum on the
+    same nodes must carry the same pair count."""
+    from paper_1905_08375_b200 import nonloc as NL
+    h = 1.0 / n
+    rng = np.random.default_rng(2)
+    k = rng.lognormal(0.0, 0.5, n ** 3)
+    d0 = dh * h
+    cd = float(NL.fractional_cdelta(3, 0.25, d0))
+    op = N.NonlocalOperator(3, n, alpha=3.5, delta0=d0, coeff0=cd, kappa=k, exterior=N.Exterior(exterior))
+    assert op.info.fft_len > 0
+    u = _u(n)
+    fast = op.apply(u)
+    idx = np.stack(np.unravel_index(np.arange(n ** 3), (n, n, n)))
+    face = np.any((idx < 3) | (idx >= n - 3), axis=0)
+    tg = np.unique(np.concatenate([np.nonzero(face)[0][::7], rng.integers(0, n ** 3, 1500)]))
+    ref, pairs = orc.apply(3, n, u, targets=tg, family=orc.FRACTIONAL, alpha=3.5, delta0=d0, coeff0=cd,
+                           kappa=k, exterior=exterior)
+    gd, gpairs = op.apply_direct_at(u, tg, return_pairs=True)
+    assert gpairs == pairs
+    assert orc.rel_inf(gd, ref) <= 1e-12
+    assert np.max(np.abs(fast[tg] - ref)) <= FAST_TOL * np.max(np.abs(fast))
