@@ -111,7 +111,9 @@ typedef struct nlg_info {
   int fast_method;           /* 0 direct quadrature, 1 span prefix sums
                                 (polynomial kernels), 2 exponential-sum scans
                                 (1-D fractional), 3 offset-table stencil
-                                (2-D/3-D fractional, 2-D peridynamics)         */
+                                (2-D/3-D fractional, 2-D peridynamics),
+                                4 centred moment scans (1-D polynomial K = 1..3,
+                                Mass form: the reference's Steps 2 + 3)        */
   int exp_terms;             /* far-field terms of the 1-D exponential sum     */
   int near_cells;            /* near-field radius (cells) of the 1-D scan path */
   double far_rel_err;        /* fitted kernel error of the exponential sum     */
@@ -131,7 +133,11 @@ void nlg_plan_destroy(nlg_plan* plan);
 nlg_status nlg_plan_info(const nlg_plan* plan, nlg_info* info);
 
 /* Host pointers, blocking. u covers the input rows (components planes
- * [dim][n_in] for PERIDYNAMIC); out covers the output rows. */
+ * [dim][n_in] for PERIDYNAMIC); out covers the output rows. For 2-D / 3-D
+ * scalar stencil and box-FFT plans of >= 4 Mi nodes nlg_apply_fast is a
+ * chunked pipeline (H2D of input rows, the apply of every output row range
+ * whose window is resident, D2H of finished rows, on three streams); pinned
+ * host buffers let the copies overlap. NLG_NO_PIPELINE=1 disables it. */
 nlg_status nlg_apply_fast(nlg_plan* plan, const double* u, double* out);
 nlg_status nlg_apply_direct(nlg_plan* plan, const double* u, double* out, int64_t* pair_count);
 
@@ -139,6 +145,15 @@ nlg_status nlg_apply_direct(nlg_plan* plan, const double* u, double* out, int64_
 nlg_status nlg_apply_fast_dev(nlg_plan* plan, const double* u_dev, double* out_dev, void* stream);
 nlg_status nlg_apply_direct_dev(nlg_plan* plan, const double* u_dev, double* out_dev,
                                 int64_t* pair_count_dev, void* stream);
+
+/* Split-phase device apply for sharded plans (multi-GPU halo overlap):
+ * _begin enqueues the part of the fast apply that does not read u's halo rows
+ * (box FFT mode: the x / y transforms of the owned planes), _end the rest once
+ * the halo rows of u_dev hold the neighbours' values. begin + end ==
+ * nlg_apply_fast_dev; for methods without a halo-independent part _begin does
+ * nothing. Same stream for both calls. */
+nlg_status nlg_apply_fast_dev_begin(nlg_plan* plan, const double* u_dev, double* out_dev, void* stream);
+nlg_status nlg_apply_fast_dev_end(nlg_plan* plan, const double* u_dev, double* out_dev, void* stream);
 
 /* Direct apply at a subset of output nodes (flat indices into the output
  * slab); used for sampled parity at BASELINE sizes. Host pointers, blocking.
@@ -153,11 +168,14 @@ nlg_status nlg_counters(const nlg_plan* plan, int64_t* pairs, int64_t* fast_appl
 
 /* Per-stage CUDA-event timing of this plan's kernels (off by default).
  * Stages: 0 direct, 1 span scan, 2 span eval, 3 exp-sum aggregate, 4 exp-sum
- * carry, 5 exp-sum main, 6 near+combine, 7 stencil, 8 exp-sum FFT, 9 box FFT
- * passes, 10 box tie band. nlg_stage_times returns (and resets) the
+ * carry, 5 exp-sum main, 6 near+combine, 7 stencil, 8 exp-sum FFT (cuFFT
+ * chain), 9 box FFT (unused), 10 box tie band, 11-15 box FFT passes PA..PE,
+ * 16-18 four-step FFT passes P1..P3. With profiling on, side streams are
+ * folded into the apply's stream so stage times never overlap (one kernel per
+ * stage except 4, 7 and 8). nlg_stage_times returns (and resets) the
  * accumulated milliseconds and launch counts per stage: the caller's arrays
  * hold NLG_NUM_STAGES slots. */
-#define NLG_NUM_STAGES 11
+#define NLG_NUM_STAGES 19
 nlg_status nlg_set_profiling(nlg_plan* plan, int on);
 nlg_status nlg_stage_times(nlg_plan* plan, double* ms, int64_t* launches, int* nstages);
 /* Total kernels this plan has launched. */
@@ -222,6 +240,34 @@ nlg_status nlg_tree_decompose(int dim, int64_t n, const double* center, double r
                               int64_t* indices, int64_t* npanels, int64_t* recur_calls);
 nlg_status nlg_tree_count(int dim, int64_t n, const double* radii, int64_t* recur_calls, int64_t* panels);
 nlg_status nlg_tree_moments(int dim, int64_t n, int K, const double* u, double* out, int64_t* adds);
+
+/* Multi-GPU plans: one process, ndev devices. The grid's
+ * axis-0 rows are split into ndev slabs (even split), one sharded plan per
+ * device; u's halo rows (the reference's window, operators.cpp:31-42) move
+ * between neighbouring devices by NCCL point-to-point (ncclCommInitAll over
+ * the device list; NCCL loaded at run time, errors and
+ * ncclCommGetAsyncError -> NLG_ENCCL), overlapped with the halo-independent
+ * part of each slab's apply. A device ordinal repeated in the list (several
+ * slabs on one GPU: tests) uses peer copies instead of NCCL.
+ * desc covers the WHOLE grid (row_begin = row_end = 0; per-node arrays of
+ * n^dim entries); desc->device is ignored. */
+typedef struct nlg_group nlg_group;
+nlg_status nlg_group_create(const nlg_desc* desc, int ndev, const int* devices, nlg_group** out);
+void nlg_group_destroy(nlg_group* group);
+/* ndev, whether NCCL carries the halos, and per device: owned rows
+ * [row_begin, row_end) and input nodes n_in (arrays of ndev, may be NULL). */
+nlg_status nlg_group_info(const nlg_group* group, int* ndev, int* nccl, int64_t* row_begin, int64_t* row_end,
+                          int64_t* n_in);
+/* Host pointers over the whole grid (components planes [dim][N] for
+ * PERIDYNAMIC): owned rows H2D per device, halo exchange device to device,
+ * apply, owned output rows D2H. Blocking. */
+nlg_status nlg_group_apply_fast(nlg_group* group, const double* u, double* out);
+/* Device pointers: u_dev[k] holds device k's input rows (n_in nodes per
+ * component; only the owned rows need to be filled, the halos are exchanged
+ * inside), out_dev[k] its output rows. Blocking. */
+nlg_status nlg_group_apply_fast_dev(nlg_group* group, double* const* u_dev, double* const* out_dev);
+/* Text of the last group error on this thread. */
+const char* nlg_group_last_error(void);
 
 /* Thread-local text of the last error; "" if none. */
 const char* nlg_last_error(void);

@@ -60,7 +60,15 @@ EXPORTS = {
     "nlg_apply_direct_at": ([C.c_void_p, _dp, _ip, C.c_int64, _dp, _ip], C.c_int),
     "nlg_counters": ([C.c_void_p, _ip, _ip], C.c_int),
     "nlg_set_profiling": ([C.c_void_p, C.c_int], C.c_int),
+    "nlg_apply_fast_dev_begin": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "nlg_apply_fast_dev_end": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "nlg_stage_times": ([C.c_void_p, _dp, _ip, C.POINTER(C.c_int)], C.c_int),
+    "nlg_group_create": ([C.POINTER(Desc), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)], C.c_int),
+    "nlg_group_destroy": ([C.c_void_p], None),
+    "nlg_group_info": ([C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), _ip, _ip, _ip], C.c_int),
+    "nlg_group_apply_fast": ([C.c_void_p, _dp, _dp], C.c_int),
+    "nlg_group_apply_fast_dev": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)], C.c_int),
+    "nlg_group_last_error": ([], C.c_char_p),
     "nlg_launch_count": ([C.c_void_p, _ip], C.c_int),
     "nlg_match_polynomial": ([C.c_int, C.c_double, _dp], C.c_int),
     "nlg_match_polynomial_exact": ([C.c_int, _ip, _ip], C.c_int),
@@ -104,10 +112,10 @@ class NonlocError(RuntimeError):
     pass
 
 
-def check(status: int) -> None:
+def check(status: int, group: bool = False) -> None:
     if status == NLG_OK:
         return
-    msg = lib().nlg_last_error().decode()
+    msg = (lib().nlg_group_last_error() if group else lib().nlg_last_error()).decode()
     if status in (NLG_EINVAL, NLG_EUNSUPPORTED):
         raise ValueError(msg)            # std::invalid_argument
     if status == NLG_EDOMAIN:
@@ -124,4 +132,6 @@ def dptr(a):
 
 
 STAGES = ["direct", "span_scan", "span_eval", "es_aggregate", "es_carry", "es_main", "es_combine", "stencil",
-          "es_fft", "box_fft", "box_ties"]   # plan.hpp enum Stage (kNumStages slots)
+          "es_fft", "box_fft", "box_ties", "box_pa_rows_fwd", "box_pb_cols_fwd", "box_pc_zstencil",
+          "box_pd_cols_inv", "box_pe_rows_inv", "es_fft_p1_cols_fwd", "es_fft_p2_rows",
+          "es_fft_p3_cols_inv"]   # plan.hpp enum Stage (kNumStages slots)

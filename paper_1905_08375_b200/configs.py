@@ -36,6 +36,10 @@ class Workload:
     exterior: int = 0               # 0 clip, 1 zero collar
     seeds: dict = field(default_factory=dict)
     algo_bytes: int = 16            # algorithmic HBM bytes per point
+    # kernel == "truncated": the reference's own fast route, TruncatedOperator
+    # (operators.cpp:102-167), polynomial profile of order K, Leaf rule, Mass form
+    K: int = 0
+    horizon_kind: int = 0           # 0 Constant, 1 GaussianBump (kernel.hpp:80-89)
 
     @property
     def N(self) -> int:
@@ -230,5 +234,25 @@ def cfg4(n: int = 768, variable: bool = False) -> Workload:
                     algo_bytes=32 if variable else 24)
 
 
+def trunc1d(n: int = 1 << 22) -> Workload:
+    """The reference's own fast route on the cfg1 grid:
+    TruncatedOperator, 1-D N=2^22, Gaussian-bump horizon delta0=0.005
+    (delta in [0.005, 0.01]), K=0, C=1, Leaf rule, Mass form; u = 16 modes +
+    noise (as cfg0/cfg1). The reference arm times TruncatedOperator::apply
+    (Steps 2+3, bench.cpp:47-49) on the same grid."""
+    u = _u_1d(n, np.random.default_rng(1))
+    return Workload("trunc1d_K0_bump_n4194304", 1, n, "truncated", 0.0, 0.0, u, delta0=0.005,
+                    coeff0=1.0, seeds={"u": 1}, algo_bytes=16, K=0, horizon_kind=1)
+
+
+def trunc2d(n: int = 1024) -> Workload:
+    """TruncatedOperator in 2-D, 1024^2, constant delta = 8h, K=0."""
+    ru = np.random.default_rng(1)
+    ks, amp, ph = _modes(ru, 64, 8, 2)
+    u = _field(n, 2, ks, amp, ph) + _noise(n * n, ru)
+    return Workload("trunc2d_K0_delta8h_n1024", 2, n, "truncated", 0.0, 0.0, u, delta0=8.0 / n,
+                    coeff0=1.0, seeds={"u": 1}, algo_bytes=16, K=0, horizon_kind=0)
+
+
 WORKLOADS = {"cfg0": cfg0, "cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4,
-             "cfg4b": lambda n=768: cfg4(n, variable=True)}
+             "cfg4b": lambda n=768: cfg4(n, variable=True), "trunc1d": trunc1d, "trunc2d": trunc2d}

@@ -1268,20 +1268,27 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
     NLG_CUDA(cudaEventRecord(S->fork, s));
     NLG_CUDA(cudaStreamWaitEvent(S->fstream, S->fork, 0));
     if (S->four) {
-      cudaStream_t fs = NLG_FFT_SERIAL ? s : S->fstream;   // experiment knob: no side-stream overlap
+      // experiment knob / per-kernel timing: no side-stream overlap
+      cudaStream_t fs = NLG_FFT_SERIAL || P.sprof.on ? s : S->fstream;
       cudaEvent_t ev;
-      stage_begin(P, fs, kStEsFft, &ev);
       // all three passes on the side stream (they do not depend on the scans);
       // the combine runs after the join (measured: fusing it into the last pass
       // keeps that pass off the side stream and costs more than the extra z pass)
-      fourstep_forward_product(S->fs, u, NF == 2 ? S->kappa_dev : nullptr, P.n_in, reinterpret_cast<double2*>(S->z), fs);
-      fourstep_inverse(S->fs, reinterpret_cast<double2*>(S->z), fs);
-      stage_end(P, fs, kStEsFft, ev, 3);
+      double2* z = reinterpret_cast<double2*>(S->z);
+      stage_begin(P, fs, kStEsFftP1, &ev);
+      fourstep_cols_forward(S->fs, u, NF == 2 ? S->kappa_dev : nullptr, P.n_in, z, fs);
+      stage_end(P, fs, kStEsFftP1, ev, 1);
+      stage_begin(P, fs, kStEsFftP2, &ev);
+      fourstep_rows_product(S->fs, z, fs);
+      stage_end(P, fs, kStEsFftP2, ev, 1);
+      stage_begin(P, fs, kStEsFftP3, &ev);
+      fourstep_inverse(S->fs, z, fs);
+      stage_end(P, fs, kStEsFftP3, ev, 1);
       NLG_CUDA(cudaEventRecord(S->join, fs));
     }
   }
   if (S->fft && !S->four) {
-    cudaStream_t fs = S->fstream;
+    cudaStream_t fs = P.sprof.on ? s : S->fstream;
     cudaEvent_t ev;
     stage_begin(P, fs, kStEsFft, &ev);
     const unsigned gl = static_cast<unsigned>((S->L + 255) / 256);

@@ -409,13 +409,17 @@ void fourstep_free(FourStep& F) {
   F = FourStep{};
 }
 
-void fourstep_forward_product(const FourStep& F, const double* u, const double* kappa, int64_t n_in, double2* z,
-                              cudaStream_t s) {
+void fourstep_cols_forward(const FourStep& F, const double* u, const double* kappa, int64_t n_in, double2* z,
+                           cudaStream_t s) {
   const FsDev d = dev_of(F);
 #define NLG_FS_CASE(N) \
   if (F.n1 == N) cols_fwd<N>(d, u, kappa, n_in, z, s);
   NLG_FS_N1(NLG_FS_CASE)
 #undef NLG_FS_CASE
+}
+
+void fourstep_rows_product(const FourStep& F, double2* z, cudaStream_t s) {
+  const FsDev d = dev_of(F);
   const size_t rs = rows_smem(F.n2);
   if (F.rows_grid > 0) {   // persistent rows (register prefetch of the next row)
     const unsigned g = static_cast<unsigned>(F.rows_grid);
@@ -428,6 +432,12 @@ void fourstep_forward_product(const FourStep& F, const double* u, const double* 
   if (F.n2 == 8192) fs_rows<8192><<<F.n1, 8192 / rows_el<8192>(), rs, s>>>(d, z);
   else if (F.n2 == 4096) fs_rows<4096><<<F.n1, 4096 / rows_el<4096>(), rs, s>>>(d, z);
   else fs_rows<2048><<<F.n1, 2048 / rows_el<2048>(), rs, s>>>(d, z);
+}
+
+void fourstep_forward_product(const FourStep& F, const double* u, const double* kappa, int64_t n_in, double2* z,
+                              cudaStream_t s) {
+  fourstep_cols_forward(F, u, kappa, n_in, z, s);
+  fourstep_rows_product(F, z, s);
 }
 
 void fourstep_inverse(const FourStep& F, double2* z, cudaStream_t s) {

@@ -35,5 +35,9 @@ void fourstep_forward_product(const FourStep& F, const double* u, const double* 
                               cudaStream_t s);
 // inverse column pass alone: z <- (conv u, conv kappa u) in signal order
 void fourstep_inverse(const FourStep& F, double2* z, cudaStream_t s);
+// the two halves of fourstep_forward_product (per-kernel timing)
+void fourstep_cols_forward(const FourStep& F, const double* u, const double* kappa, int64_t n_in, double2* z,
+                           cudaStream_t s);
+void fourstep_rows_product(const FourStep& F, double2* z, cudaStream_t s);
 
 }  // namespace nlg

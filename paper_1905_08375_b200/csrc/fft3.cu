@@ -59,7 +59,8 @@ struct BoxFft {
   int tma_br = 0;                                   // rows per tensor box
   CUtensorMap pb_in{}, pb_out{}, pd_in{}, pd_out{};
   int64_t n = 0, n_in = 0, o0 = 0, rows_out = 0;   // z: input planes, first output plane, output planes
-  double2* z = nullptr;                             // [n_in][ly][lx]
+  double2* z = nullptr;                             // [n_in][ly][lx]: PA / PB output, PC input
+  double2* z2 = nullptr;                            // [n_in][ly][lx]: PC output (output planes), PD / PE / ties
   double2* twx = nullptr;                           // [lx] exp(-2 pi i t / lx)
   double2* twy = nullptr;
   double* g = nullptr;                              // [ly][lx][rf + 1] partial spectra / (lx ly)
@@ -100,6 +101,8 @@ struct F3Args {
   const double2* twy;
   const double* g;
   double2* z;
+  double2* z2;           // PC writes here (out of place), PD / PE work in it
+  int64_t p0, p1;        // plane range of this launch: input planes (PA, PB), output planes (PC, PD, PE)
   const double* u;       // [n_in rows]
   const double* kappa;   // or null
   const double* scale;   // [n_out], or null: scale0 everywhere (constant coefficient)
@@ -118,8 +121,8 @@ template <int L, bool INV, bool KW, bool AB = false>
 __global__ void __launch_bounds__(rows_threads<L, INV && !AB>()) f3_rows(const __grid_constant__ F3Args a) {
   constexpr int T = rows_threads<L, INV && !AB>();
   __shared__ double2 sm[L + L / 8];
-  const int64_t r = blockIdx.x;                      // row within the pass
-  const int64_t zr = r / a.n, y = r % a.n;
+  const int64_t r = blockIdx.x;                      // row within the launch
+  const int64_t zr = a.p0 + r / a.n, y = r % a.n;
   const int tid = threadIdx.x;
   if (!INV) {
     const int64_t src = (zr * a.n + y) * a.n;        // u row
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(rows_threads<L, INV && !AB>()) f3_rows(const _
     fs_fft<false, L, 1, L, 1, T, true>(sm, a.twx, tid, ld, st);
   } else {
     const int64_t zi = a.o0 + zr;                    // input plane of this output plane
-    double2* zrow = a.z + (zi * a.ly + y) * a.lx;
+    double2* zrow = a.z2 + (zi * a.ly + y) * a.lx;
     const int64_t ii = (zi * a.n + y) * a.n;         // input index of x = 0
     const int64_t oi = (zr * a.n + y) * a.n;         // output index of x = 0
     auto ld = [&](int e, int) { return zrow[e]; };
@@ -170,8 +173,8 @@ __global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_cols(const __
   extern __shared__ double2 fsm3[];
   const int tid = threadIdx.x;
   const int kx0 = blockIdx.x * C;
-  const int64_t zi = PD ? a.o0 + blockIdx.y : blockIdx.y;
-  double2* col = a.z + zi * a.ly * a.lx + kx0;
+  const int64_t zi = PD ? a.o0 + a.p0 + blockIdx.y : a.p0 + blockIdx.y;
+  double2* col = (PD ? a.z2 : a.z) + zi * a.ly * a.lx + kx0;
   auto ld = [&](int e, int c) {
     if (!PD && e >= a.n) return make_double2(0.0, 0.0);
     return col[static_cast<int64_t>(e) * a.lx + c];
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(cols_threads3<L, 4>(), 2)
   __shared__ __align__(8) unsigned long long mbar;
   const int tid = threadIdx.x;
   const int cx = blockIdx.x * 2 * C;             // first double of the tile in the row
-  const int pz = blockIdx.y;                     // plane of the view
+  const int pz = static_cast<int>(a.p0) + blockIdx.y;   // plane of the view
   const unsigned mb = smem_u32(&mbar);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
@@ -246,58 +249,79 @@ __global__ void __launch_bounds__(cols_threads3<L, 4>(), 2)
 // PC: the z direction is not transformed. After FFT_x FFT_y the operator is,
 // per column (ky, kx), a (2 r_f + 1)-tap convolution along z with the partial
 // spectra G(|dz|; ky, kx) = sum_{dy,dx} w(dz,dy,dx) cos(2 pi ky dy/L_y)
-// cos(2 pi kx dx/L_x) / (L_x L_y): one thread per column walks the planes with
-// a register window (in place: the window holds the planes the writes
-// overwrite), output planes stored conjugated for the forward-transform
-// inverses. No z padding, 2 r_f + 1 FMA pairs per element instead of two
-// 800-point transforms.
-// RW = r_f (template: the window and the taps in registers)
+// cos(2 pi kx dx/L_x) / (L_x L_y): 2 r_f + 1 FMA pairs per element instead of
+// two padded z transforms. Out of place (Z -> Z2) and cut into z chunks: a
+// thread owns one column over zc consecutive output planes, so the grid has
+// (columns x chunks) threads and every block of 2 r_f + 1 planes issues all its
+// loads before the first FMA (the in-place single-walk version kept one load
+// in flight per thread: 34 long-scoreboard stalls per issue, 3.7 TB/s). The
+// output planes are stored conjugated for the forward-transform inverses.
 template <int RW>
-__global__ void __launch_bounds__(256, 3) f3_zstencil(const __grid_constant__ F3Args a) {
+__global__ void __launch_bounds__(256, 2) f3_zstencil(const __grid_constant__ F3Args a, int zc) {
   constexpr int kZW = 2 * RW + 1;
+  // one thread per (column, component): the real and imaginary parts of a
+  // column are adjacent doubles, so a warp still reads 256 contiguous bytes per
+  // plane, and the window + the block's prefetch fit in ~60 registers
   const int64_t plane = static_cast<int64_t>(a.ly) * a.lx;
-  const int64_t col = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (col >= plane) return;
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= 2 * plane) return;
+  const int64_t col = e >> 1;
+  const double sgn = (e & 1) ? -1.0 : 1.0;       // conjugate on the store
+  // output planes [z0, z1) of this thread, input-plane coordinates
+  const int64_t z0 = a.o0 + a.p0 + static_cast<int64_t>(blockIdx.y) * zc;
+  const int64_t z1 = min(z0 + zc, a.o0 + a.p1);
+  if (z0 >= z1) return;
   double gr[RW + 1];
   {
     const double* gp = a.g + col * (RW + 1);
 #pragma unroll
     for (int d = 0; d <= RW; ++d) gr[d] = __ldg(gp + d);
   }
-  double2* zc = a.z + col;
-  const int64_t nz = a.n_in, zo0 = a.o0, zo1 = a.o0 + a.rows_out;
-  auto ldz = [&](int64_t zz) { return zz >= 0 && zz < nz ? zc[zz * plane] : make_double2(0.0, 0.0); };
-  double2 win[kZW];                              // slot (p - zo0 + RW) % kZW holds plane p
+  const double* __restrict__ src = reinterpret_cast<const double*>(a.z) + e;
+  double* __restrict__ dst = reinterpret_cast<double*>(a.z2) + e;
+  const int64_t nz = a.n_in, pl2 = 2 * plane;
+  auto ldz = [&](int64_t zz) { return zz >= 0 && zz < nz ? src[zz * pl2] : 0.0; };
+  double win[kZW];                               // slot (p - z0 + RW) % kZW holds plane p
 #pragma unroll
-  for (int j = 0; j < kZW - 1; ++j) win[j] = ldz(zo0 - RW + j);
-  for (int64_t zb = zo0; zb < zo1; zb += kZW) {
+  for (int j = 0; j < kZW - 1; ++j) win[j] = ldz(z0 - RW + j);
+  for (int64_t zb = z0; zb < z1; zb += kZW) {
+    double nx[kZW];                              // the block's new planes, all loads in flight at once
+    if (zb + kZW <= z1 && zb + kZW - 1 + RW < nz) {   // interior block: one pointer bumped per load
+      const double* p = src + (zb + RW) * pl2;
+#pragma unroll
+      for (int c = 0; c < kZW; ++c, p += pl2) nx[c] = *p;
+    } else {
+#pragma unroll
+      for (int c = 0; c < kZW; ++c) nx[c] = zb + c < z1 ? ldz(zb + c + RW) : 0.0;
+    }
 #pragma unroll
     for (int c = 0; c < kZW; ++c) {              // output plane z = zb + c; plane z + k in slot (c + RW + k) % kZW
       const int64_t z = zb + c;
-      win[(c + kZW - 1) % kZW] = ldz(z + RW);
-      if (z < zo1) {
-        double2 acc = make_double2(gr[0] * win[(c + RW) % kZW].x, gr[0] * win[(c + RW) % kZW].y);
+      win[(c + kZW - 1) % kZW] = nx[c];
+      if (z < z1) {
+        double acc = gr[0] * win[(c + RW) % kZW];
 #pragma unroll
-        for (int k = 1; k <= RW; ++k) {
-          const double2 p = win[(c + RW + k) % kZW], m = win[(c + RW - k + kZW) % kZW];
-          acc.x = fma(gr[k], p.x + m.x, acc.x);
-          acc.y = fma(gr[k], p.y + m.y, acc.y);
-        }
-        zc[z * plane] = make_double2(acc.x, -acc.y);   // conjugate
+        for (int k = 1; k <= RW; ++k) acc = fma(gr[k], win[(c + RW + k) % kZW] + win[(c + RW - k + kZW) % kZW], acc);
+        dst[z * pl2] = sgn * acc;
       }
     }
   }
 }
 
+// output planes [a.p0, a.p1) in z chunks of about 128 planes
 void launch_zstencil(const F3Args& a, cudaStream_t s) {
-  const unsigned g = static_cast<unsigned>((static_cast<int64_t>(a.ly) * a.lx + 255) / 256);
+  const int64_t planes = a.p1 - a.p0;
+  if (planes <= 0) return;
+  const int64_t nch = std::max<int64_t>(1, (planes + 127) / 128);
+  const int zc = static_cast<int>((planes + nch - 1) / nch);
+  const dim3 g(static_cast<unsigned>((2 * static_cast<int64_t>(a.ly) * a.lx + 255) / 256), static_cast<unsigned>(nch));
   switch (a.rf) {
-    case 1: f3_zstencil<1><<<g, 256, 0, s>>>(a); break;
-    case 2: f3_zstencil<2><<<g, 256, 0, s>>>(a); break;
-    case 3: f3_zstencil<3><<<g, 256, 0, s>>>(a); break;
-    case 4: f3_zstencil<4><<<g, 256, 0, s>>>(a); break;
-    case 5: f3_zstencil<5><<<g, 256, 0, s>>>(a); break;
-    default: f3_zstencil<6><<<g, 256, 0, s>>>(a); break;
+    case 1: f3_zstencil<1><<<g, 256, 0, s>>>(a, zc); break;
+    case 2: f3_zstencil<2><<<g, 256, 0, s>>>(a, zc); break;
+    case 3: f3_zstencil<3><<<g, 256, 0, s>>>(a, zc); break;
+    case 4: f3_zstencil<4><<<g, 256, 0, s>>>(a, zc); break;
+    case 5: f3_zstencil<5><<<g, 256, 0, s>>>(a, zc); break;
+    default: f3_zstencil<6><<<g, 256, 0, s>>>(a, zc); break;
   }
 }
 
@@ -352,6 +376,7 @@ struct TieArgs {
   const double2* zab;    // (A, B) of the FFT convolution in the Z rows: [in plane][y][x], strides below
   int64_t zly, zlx;
   const double* diag;    // [n_out]
+  int64_t zlo, zhi;      // target planes [zlo, zhi) of this launch (absolute rows)
 };
 
 template <typename MT>
@@ -450,13 +475,22 @@ constexpr int kTieFixedM = 36;   // the BASELINE cfg4-A band (delta = 6h): speci
 
 // M > 0: the tie set of |t|^2 = M at compile time (offsets, slots and mask
 // bits are immediates); M = 0: the runtime set in a.tg.
-__device__ __forceinline__ void cp_async8z(void* dst, const void* src, bool in) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(in ? 8 : 0) : "memory");
-}
+
+// build-time experiment knobs (tools/macro_ab.sh): minimum resident CTAs for
+// the register budget, the warp-level skip of ties no lane includes, and a
+// timing-only variant without the tie sums (wrong results: floor measurement)
+#ifndef NLG_TIES_MINB
+#define NLG_TIES_MINB 1
+#endif
+#ifndef NLG_TIES_SKIP
+#define NLG_TIES_SKIP 1
+#endif
+#ifndef NLG_TIES_NOSUM
+#define NLG_TIES_NOSUM 0
+#endif
 
 template <int M, bool KW, typename MT>
-__global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant__ TieArgs a) {
+__global__ void __launch_bounds__(kTieTX * kTieTY, NLG_TIES_MINB) f3_ties(const __grid_constant__ TieArgs a) {
   extern __shared__ __align__(16) double2 tsm[];
   const Geom& g = a.g;
   const int n = static_cast<int>(g.n);
@@ -470,36 +504,48 @@ __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant
   const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
   const bool live = x < n && y < n;
   const int cls = static_cast<int>(blockIdx.z) % q;
-  const int zb = static_cast<int>(g.row_begin) + static_cast<int>(blockIdx.z / q) * kTieZC;
-  const int ze = min(static_cast<int>(g.row_end), zb + kTieZC);
+  const int zb = static_cast<int>(a.zlo) + static_cast<int>(blockIdx.z / q) * kTieZC;
+  const int ze = min(static_cast<int>(a.zhi), zb + kTieZC);
   const int zf = zb + ((cls - zb) % q + q) % q;           // first target plane of the class
   if (zf >= ze) return;
   const MT* mask = static_cast<const MT*>(a.mask);
   const int tgt = y * n + x;
   const int sbase = (threadIdx.y + R) * W + threadIdx.x + R;
   for (int sl = tid; sl < NR; sl += NT) tsm[sl * SL + SB] = make_double2(0.0, 0.0);
+  if (M > 0)   // the zero block behind the ring (fixed-M excluded ties read it)
+    for (int e = tid; e < 2 * (R * W + R) + 8; e += NT) tsm[((NR * SL + 7) & ~7) + e] = make_double2(0.0, 0.0);
+  // this thread's staged elements: e = tid + k NT < SB; source offset within a
+  // plane (0 outside the domain: the copy then zero-fills)
   int soff[kTieStage];
-  bool sok[kTieStage];
+  unsigned sact = 0, sin_ = 0;
 #pragma unroll
   for (int k = 0; k < kTieStage; ++k) {
     const int e = tid + k * NT;
     const int r = e / W, c = e - r * W;
     const int gy = y0 - R + r, gx = x0 - R + c;
-    sok[k] = e < SB && gy >= 0 && gy < n && gx >= 0 && gx < n;
-    soff[k] = sok[k] ? gy * n + gx : 0;
+    const bool ok = e < SB && gy >= 0 && gy < n && gx >= 0 && gx < n;
+    if (e < SB) sact |= 1u << k;
+    if (ok) sin_ |= 1u << k;
+    soff[k] = ok ? gy * n + gx : 0;
   }
-  // plane p -> slot: (u, kappa) pairs by cp.async, zero outside the domain
+  const unsigned smem0 = static_cast<unsigned>(__cvta_generic_to_shared(tsm)) + 16u * tid;
+  // plane p -> slot: (u, kappa) pairs by cp.async, zero outside the domain;
+  // the plane base pointers once per plane, per element one add and the copy
   auto stage = [&](int p, int slot) {
     const bool pin = p >= 0 && p < n;
-    const int64_t pb = (static_cast<int64_t>(pin ? p : 0) - g.in_begin) * nn;
-    double* st = reinterpret_cast<double*>(tsm + slot * SL);
+    const int64_t pb = (static_cast<int64_t>(pin ? p : g.in_begin) - g.in_begin) * nn;
+    const double* ub = a.u + pb;
+    const double* kb = KW ? a.kappa + pb : nullptr;
+    const unsigned d0 = smem0 + 16u * static_cast<unsigned>(slot * SL);
 #pragma unroll
     for (int k = 0; k < kTieStage; ++k) {
-      const int e = tid + k * NT;
-      if (e < SB) {
-        const bool in = pin && sok[k];
-        cp_async8z(st + 2 * e, a.u + pb + soff[k], in);
-        if (KW) cp_async8z(st + 2 * e + 1, a.kappa + pb + soff[k], in);
+      if (sact & (1u << k)) {
+        const unsigned sz = pin && (sin_ & (1u << k)) ? 8u : 0u;
+        const unsigned d = d0 + 16u * k * NT;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(ub + soff[k]), "r"(sz) : "memory");
+        if (KW)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d + 8u), "l"(kb + soff[k]), "r"(sz)
+                       : "memory");
       }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -557,12 +603,28 @@ __global__ void __launch_bounds__(kTieTX * kTieTY) f3_ties(const __grid_constant
       const double2* slot[kNS];
 #pragma unroll
       for (int r = 0; r < kNS; ++r) slot[r] = tsm + (head + r < NR ? head + r : head + r - NR) * SL + sbase;
-      const double2* zero = tsm + SB;                     // slot 0's zero element
+      constexpr int kZH = TS.R * (kTieTX + 2 * TS.R) + TS.R;   // largest |tie offset| in a window
+      // Excluded ties read a zero block through the same immediate offset (one
+      // SEL of the base per tie, no select on the sums). The zero base of slot
+      // r is congruent to the slot's own base mod 8 elements (128 B), so a
+      // warp mixing real and zero reads still hits each bank once per quarter.
+      const int zb0 = (NR * SL + 7) & ~7;                  // 8-aligned zero block, 2 kZH + 8 elements
+      const double2* zc[kNS];
+#pragma unroll
+      for (int r = 0; r < kNS; ++r) {
+        const int sr = static_cast<int>(slot[r] - tsm);
+        zc[r] = tsm + zb0 + kZH + (((sr - (zb0 + kZH)) % 8) + 8) % 8;
+      }
+      // ties no lane of the warp includes are skipped (the inclusion pattern is
+      // smooth along x: ~15 of the 24 are needed per warp at 768^3)
+      const unsigned wm = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(m));
       double A1 = 0.0, B1 = 0.0;                          // two chains per field
 #pragma unroll
-      for (int k = 0; k < TS.n; ++k) {                    // an excluded tie reads the zero element
-        const double2* src = slot[(TS.t0[k] + TS.R) / TS.q] + TS.t1[k] * (kTieTX + 2 * TS.R) + TS.t2[k];
-        const double2 v = *((m & (1u << TS.bit[k])) ? src : zero);
+      for (int k = 0; k < (NLG_TIES_NOSUM ? 0 : TS.n); ++k) {
+        if (NLG_TIES_SKIP && !(wm & (1u << TS.bit[k]))) continue;
+        const int r = (TS.t0[k] + TS.R) / TS.q;
+        const double2* base = (m & (1u << TS.bit[k])) ? slot[r] : zc[r];
+        const double2 v = base[TS.t1[k] * (kTieTX + 2 * TS.R) + TS.t2[k]];
         if (k & 1) {
           A1 += v.x;
           if (KW) B1 = fma(v.x, v.y, B1);
@@ -705,6 +767,9 @@ F3Args args_of(const Plan& P, const BoxFft& B) {
   a.twy = B.twy;
   a.g = B.g;
   a.z = B.z;
+  a.z2 = B.z2;
+  a.p0 = 0;
+  a.p1 = 0;
   a.u = nullptr;
   a.kappa = P.d_kappa;
   a.scale = nullptr;
@@ -735,10 +800,12 @@ TieArgs tie_args(const Plan& P, const BoxFft& B) {
   t.scale = nullptr;
   t.scale0 = 0.0;
   t.out = nullptr;
-  t.zab = B.z;
+  t.zab = B.z2;
   t.zly = B.ly;
   t.zlx = B.lx;
   t.diag = nullptr;
+  t.zlo = P.geom.row_begin;
+  t.zhi = P.geom.row_end;
   return t;
 }
 
@@ -856,6 +923,7 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   double* cx = upload_on(costab(lx), P.stream);
   NLG_CUDA(cudaMalloc(&B->g, sizeof(double) * static_cast<size_t>(lx) * lx * G));
   NLG_CUDA(cudaMalloc(&B->z, sizeof(double2) * static_cast<size_t>(n_in) * lx * lx));
+  NLG_CUDA(cudaMalloc(&B->z2, sizeof(double2) * static_cast<size_t>(n_in) * lx * lx));
   {
     const char* te = std::getenv("NLG_F3_TMA");
     if (te && std::atoi(te) == 1) {
@@ -863,7 +931,7 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
       for (int d = 1; d <= 256 && d <= lx; ++d)
         if (lx % d == 0) br = d;
       B->tma_br = br;
-      double2* zo = B->z + static_cast<size_t>(B->o0) * lx * lx;
+      double2* zo = B->z2 + static_cast<size_t>(B->o0) * lx * lx;
       B->tma = encode_cols_map(&B->pb_in, B->z, lx, lx, n, n_in, br) &&
                encode_cols_map(&B->pb_out, B->z, lx, lx, lx, n_in, br) &&
                encode_cols_map(&B->pd_in, zo, lx, lx, lx, B->rows_out, br) &&
@@ -901,8 +969,10 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   return B;
 }
 
-void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
-                  double* out, cudaStream_t s) {
+namespace {
+
+F3Args apply_args(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
+                  double* out) {
   F3Args a = args_of(P, B);
   a.u = u;
   a.scale = scale;
@@ -910,27 +980,58 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
   a.diag = diag;
   a.out = out;
   a.ab = B.ntie > 0;   // with a tie band the tie pass writes out
+  return a;
+}
+
+}  // namespace
+
+// PA + PB on input planes [p0, p1)
+void boxfft_in(Plan& P, BoxFft& B, const double* u, int64_t p0, int64_t p1, cudaStream_t s) {
+  if (p1 <= p0) return;
+  F3Args a = apply_args(P, B, u, nullptr, 0.0, nullptr, nullptr);
+  a.p0 = p0;
+  a.p1 = p1;
   const int lx = B.lx;
   cudaEvent_t ev;
-  stage_begin(P, s, kStBoxFft, &ev);
+  stage_begin(P, s, kStBoxPA, &ev);
 #define NLG_F3_CASE(N) \
-  if (lx == N) launch_rows<N>(a, false, B.n_in * B.n, s);
+  if (lx == N) launch_rows<N>(a, false, (p1 - p0) * B.n, s);
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
+  stage_end(P, s, kStBoxPA, ev, 1);
+  stage_begin(P, s, kStBoxPB, &ev);
 #define NLG_F3_CASE(N) \
-  if (lx == N) { if (B.tma) launch_cols_tma<N>(B, a, false, B.n_in, s); else launch_cols<N>(a, B.cols, false, B.n_in, s); }
+  if (lx == N) { if (B.tma) launch_cols_tma<N>(B, a, false, p1 - p0, s); else launch_cols<N>(a, B.cols, false, p1 - p0, s); }
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
+  stage_end(P, s, kStBoxPB, ev, 1);
+}
+
+// PC, PD, PE and the tie pass on output planes [q0, q1) (needs PB done on the
+// input planes up to q1 + r_f)
+void boxfft_out(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
+                double* out, int64_t q0, int64_t q1, cudaStream_t s) {
+  if (q1 <= q0) return;
+  F3Args a = apply_args(P, B, u, scale, scale0, diag, out);
+  a.p0 = q0;
+  a.p1 = q1;
+  const int lx = B.lx;
+  cudaEvent_t ev;
+  stage_begin(P, s, kStBoxPC, &ev);
   launch_zstencil(a, s);
+  stage_end(P, s, kStBoxPC, ev, 1);
+  stage_begin(P, s, kStBoxPD, &ev);
 #define NLG_F3_CASE(N) \
-  if (lx == N) { if (B.tma) launch_cols_tma<N>(B, a, true, B.rows_out, s); else launch_cols<N>(a, B.cols, true, B.rows_out, s); }
+  if (lx == N) { if (B.tma) launch_cols_tma<N>(B, a, true, q1 - q0, s); else launch_cols<N>(a, B.cols, true, q1 - q0, s); }
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
+  stage_end(P, s, kStBoxPD, ev, 1);
+  stage_begin(P, s, kStBoxPE, &ev);
 #define NLG_F3_CASE(N) \
-  if (lx == N) launch_rows<N>(a, true, B.rows_out * B.n, s);
+  if (lx == N) launch_rows<N>(a, true, (q1 - q0) * B.n, s);
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
-  stage_end(P, s, kStBoxFft, ev, 5);
+  stage_end(P, s, kStBoxPE, ev, 1);
   if (B.ntie > 0) {
     stage_begin(P, s, kStBoxTie, &ev);
     TieArgs t = tie_args(P, B);
@@ -939,13 +1040,16 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
     t.scale0 = scale0;
     t.out = out;
     t.diag = diag;
+    t.zlo = P.geom.row_begin + q0;
+    t.zhi = P.geom.row_begin + q1;
     const bool wide = B.ntie > 32;
     const bool fixed = B.tie_m == kTieFixedM && !wide;
     constexpr TieSet kDense = make_ties(kTieFixedM, true);
     const int R = fixed ? kDense.R : B.tg.R, q = fixed ? kDense.q : B.tg.q, NS = 2 * R / q + 1;
-    const size_t sb = sizeof(double2) * (NS + 1) * ((kTieTY + 2 * R) * (kTieTX + 2 * R) + 1);
+    const size_t sb = sizeof(double2) * ((NS + 1) * ((kTieTY + 2 * R) * (kTieTX + 2 * R) + 1) +
+                                         (fixed ? 2 * (R * (kTieTX + 2 * R) + R) + 16 : 0));
     const dim3 grid(static_cast<unsigned>((B.n + kTieTX - 1) / kTieTX), static_cast<unsigned>((B.n + kTieTY - 1) / kTieTY),
-                    static_cast<unsigned>((B.rows_out + kTieZC - 1) / kTieZC * q));
+                    static_cast<unsigned>((q1 - q0 + kTieZC - 1) / kTieZC * q));
     const dim3 blk(kTieTX, kTieTY);
     if (wide) {
       if (P.d_kappa) f3_ties<0, true, uint64_t><<<grid, blk, sb, s>>>(t);
@@ -961,13 +1065,19 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
   }
 }
 
+void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
+                  double* out, cudaStream_t s) {
+  boxfft_in(P, B, u, 0, B.n_in, s);
+  boxfft_out(P, B, u, scale, scale0, diag, out, 0, B.rows_out, s);
+}
+
 int boxfft_launches(const BoxFft& B) { return 5 + (B.ntie > 0 ? 1 : 0); }
 int boxfft_length(const BoxFft& B) { return B.lx; }
 
 void boxfft_free(BoxFft* B) {
   if (!B) return;
   for (void* p : {static_cast<void*>(B->twx), static_cast<void*>(B->g),
-                  static_cast<void*>(B->z), B->tie_mask})
+                  static_cast<void*>(B->z), static_cast<void*>(B->z2), B->tie_mask})
     cudaFree(p);
   delete B;
 }

@@ -5,7 +5,9 @@
 // C / kappa arrays the reference caches (delta_, coeff_, operators.cpp:119-120)
 // and prepares the fast method. There is no panel list: the GPU replaces
 // Algorithm 1 by spans / scans computed on the fly.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -224,6 +226,9 @@ nlg_status nlg_plan_create(const nlg_desc* desc, nlg_plan** out) {
     if (P.family == NLG_TRUNCATED && P.route == NLG_ROUTE_TRUNCATED && pr.npoly == 1) {
       P.fast_method = 1;
       spans_setup(P);
+    } else if (P.family == NLG_TRUNCATED && P.route == NLG_ROUTE_TRUNCATED && g.dim == 1 && pr.npoly <= 4 &&
+               P.form == NLG_MASS && !P.divergence) {
+      moments_setup(P, pr.npoly - 1);            // 1-D K = 1..3: centred moment scans
     } else if (P.family == NLG_FRACTIONAL && g.dim == 1) {
       expsum_setup(P, d);                       // wide horizons: exponential-sum scans
       if (P.fast_method == 0) stencil_setup(P, d);   // narrow ones: 1-D stencil
@@ -259,6 +264,9 @@ void nlg_plan_destroy(nlg_plan* plan) {
   cudaFree(P.d_pairs);
   cudaFree(P.d_targets);
   if (P.stream) cudaStreamDestroy(P.stream);
+  if (P.h2d_stream) cudaStreamDestroy(P.h2d_stream);
+  if (P.d2h_stream) cudaStreamDestroy(P.d2h_stream);
+  for (auto e : P.pipe_ev) cudaEventDestroy(e);
   delete plan;
 }
 
@@ -294,6 +302,7 @@ void ensure_staging(Plan& P) {
 void fast_dev(Plan& P, const double* u, double* out, cudaStream_t s) {
   switch (P.fast_method) {
     case 1: spans_apply(P, u, out, s); break;
+    case 4: moments_apply(P, u, out, s); break;
     case 2: expsum_apply(P, u, out, s); break;
     case 3: {
       if (stencil_box(P)) {   // box FFT mode: its passes and tie pass are stages of their own
@@ -318,6 +327,66 @@ void fast_dev(Plan& P, const double* u, double* out, cudaStream_t s) {
   ++P.fast_applies;
 }
 
+// The chunked host pipeline of nlg_apply_fast: 2-D / 3-D scalar stencil and
+// box-FFT plans of at least 4 Mi nodes. Input rows travel H2D in chunks on one
+// copy stream; each output row range is computed as soon as every input row
+// it reads (H rows either side) is resident, and travels D2H on a second copy
+// stream while the next chunks copy in and compute: PCIe in, PCIe out and the
+// apply overlap instead of running back to back.
+bool pipelinable(const Plan& P) {
+  return P.fast_method == 3 && P.geom.dim >= 2 && components(P) == 1 && P.n_out >= (int64_t{1} << 22) &&
+         stencil_reach_rows(P) > 0;
+}
+
+void apply_fast_pipelined(Plan& P, const double* u, double* out) {
+  const Geom& g = P.geom;
+  const int64_t st = g.stride0, rows_in = g.in_end - g.in_begin, rows_out = g.row_end - g.row_begin;
+  const int64_t H = stencil_reach_rows(P);
+  const bool box = stencil_box(P);
+  const int nch = static_cast<int>(std::min<int64_t>(box ? 12 : 8, rows_in));
+  if (!P.h2d_stream) {
+    NLG_CUDA(cudaStreamCreateWithFlags(&P.h2d_stream, cudaStreamNonBlocking));
+    NLG_CUDA(cudaStreamCreateWithFlags(&P.d2h_stream, cudaStreamNonBlocking));
+  }
+  while (static_cast<int>(P.pipe_ev.size()) < 2 * nch) {
+    cudaEvent_t e;
+    NLG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    P.pipe_ev.push_back(e);
+  }
+  int64_t q_done = 0;
+  for (int k = 0; k < nch; ++k) {
+    const int64_t i0 = rows_in * k / nch, i1 = rows_in * (k + 1) / nch;
+    NLG_CUDA(cudaMemcpyAsync(P.d_u + i0 * st, u + i0 * st, sizeof(double) * (i1 - i0) * st, cudaMemcpyHostToDevice,
+                             P.h2d_stream));
+    NLG_CUDA(cudaEventRecord(P.pipe_ev[k], P.h2d_stream));
+    NLG_CUDA(cudaStreamWaitEvent(P.stream, P.pipe_ev[k], 0));
+    if (box) stencil_box_in(P, P.d_u, i0, i1, P.stream);
+    // output rows whose whole window [r - H, r + H] is resident
+    const int64_t tile = box ? 1 : stencil_row_tile(P);
+    const int64_t q_ready =
+        k == nch - 1 ? rows_out
+                     : std::clamp<int64_t>(g.in_begin + i1 - H - g.row_begin, 0, rows_out) / tile * tile;
+    if (q_ready <= q_done) continue;
+    if (box) {
+      stencil_box_out(P, P.d_u, P.d_out, q_done, q_ready, P.stream);
+    } else {
+      cudaEvent_t ev;
+      stage_begin(P, P.stream, kStStencil, &ev);
+      stencil_apply_rows(P, P.d_u, P.d_out, q_done, q_ready, P.stream);
+      stage_end(P, P.stream, kStStencil, ev, 1);
+    }
+    NLG_CUDA(cudaGetLastError());
+    NLG_CUDA(cudaEventRecord(P.pipe_ev[nch + k], P.stream));
+    NLG_CUDA(cudaStreamWaitEvent(P.d2h_stream, P.pipe_ev[nch + k], 0));
+    NLG_CUDA(cudaMemcpyAsync(out + q_done * st, P.d_out + q_done * st, sizeof(double) * (q_ready - q_done) * st,
+                             cudaMemcpyDeviceToHost, P.d2h_stream));
+    q_done = q_ready;
+  }
+  NLG_CUDA(cudaStreamSynchronize(P.d2h_stream));
+  NLG_CUDA(cudaStreamSynchronize(P.stream));
+  ++P.fast_applies;
+}
+
 }  // namespace
 
 nlg_status nlg_apply_fast(nlg_plan* plan, const double* u, double* out) {
@@ -326,11 +395,54 @@ nlg_status nlg_apply_fast(nlg_plan* plan, const double* u, double* out) {
     Plan& P = plan->p;
     NLG_CUDA(cudaSetDevice(P.device));
     ensure_staging(P);
+    if (pipelinable(P) && !std::getenv("NLG_NO_PIPELINE")) {
+      apply_fast_pipelined(P, u, out);
+      return;
+    }
     const int nc = components(P);
     NLG_CUDA(cudaMemcpyAsync(P.d_u, u, sizeof(double) * nc * P.n_in, cudaMemcpyHostToDevice, P.stream));
     fast_dev(P, P.d_u, P.d_out, P.stream);
     NLG_CUDA(cudaMemcpyAsync(out, P.d_out, sizeof(double) * nc * P.n_out, cudaMemcpyDeviceToHost, P.stream));
     NLG_CUDA(cudaStreamSynchronize(P.stream));
+  });
+}
+
+// Split-phase device apply for sharded plans: _begin enqueues the work that
+// does not read u's halo rows (box FFT: the x / y transforms of the owned
+// planes), so a caller can exchange the halos meanwhile; _end the rest. For
+// every other method _begin does nothing and _end is nlg_apply_fast_dev.
+nlg_status nlg_apply_fast_dev_begin(nlg_plan* plan, const double* u_dev, double* out_dev, void* stream) {
+  return guard([&] {
+    require(plan && u_dev && out_dev, "null argument");
+    Plan& P = plan->p;
+    NLG_CUDA(cudaSetDevice(P.device));
+    P.split_begun = false;
+    if (P.fast_method == 3 && stencil_box(P)) {
+      const int64_t rows_in = P.geom.in_end - P.geom.in_begin;
+      stencil_box_in(P, u_dev, P.halo_lo, rows_in - P.halo_hi, static_cast<cudaStream_t>(stream));
+      NLG_CUDA(cudaGetLastError());
+      P.split_begun = true;
+    }
+  });
+}
+
+nlg_status nlg_apply_fast_dev_end(nlg_plan* plan, const double* u_dev, double* out_dev, void* stream) {
+  return guard([&] {
+    require(plan && u_dev && out_dev, "null argument");
+    Plan& P = plan->p;
+    NLG_CUDA(cudaSetDevice(P.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (P.split_begun) {
+      const int64_t rows_in = P.geom.in_end - P.geom.in_begin;
+      stencil_box_in(P, u_dev, 0, P.halo_lo, s);
+      stencil_box_in(P, u_dev, rows_in - P.halo_hi, rows_in, s);
+      stencil_box_out(P, u_dev, out_dev, 0, P.geom.row_end - P.geom.row_begin, s);
+      NLG_CUDA(cudaGetLastError());
+      ++P.fast_applies;
+      P.split_begun = false;
+      return;
+    }
+    fast_dev(P, u_dev, out_dev, s);
   });
 }
 

@@ -49,12 +49,18 @@ struct ExpSum {
 };
 
 struct ExpSumState;
+struct ScanBuffers;
 struct StencilState;
 struct BoxFft;
 
 // Optional per-stage CUDA-event timing (nlg_set_profiling / nlg_stage_times).
+// With profiling on, every stage is timed on the apply's own stream (side
+// streams are folded into it), so the stage times do not overlap and their
+// shares add up to the serialized apply.
 enum Stage { kStDirect = 0, kStSpanScan, kStSpanEval, kStEsAggregate, kStEsCarry, kStEsMain,
-             kStEsCombine, kStStencil, kStEsFft, kStBoxFft, kStBoxTie, kNumStages };
+             kStEsCombine, kStStencil, kStEsFft, kStBoxFft, kStBoxTie,
+             kStBoxPA, kStBoxPB, kStBoxPC, kStBoxPD, kStBoxPE, kStEsFftP1, kStEsFftP2, kStEsFftP3,
+             kNumStages };
 struct StageProf {
   bool on = false;
   struct Rec { int stage; cudaEvent_t a, b; };
@@ -90,8 +96,9 @@ struct Plan {
   // fast method 1 (span prefix sums)
   double* d_pref_hi = nullptr;   // local exclusive prefix, [rows][len]
   double* d_pref_lo = nullptr;
-  double* d_seg_hi = nullptr;    // segment totals -> exclusive offsets
+  double* d_seg_hi = nullptr;    // row totals (the prefix at p = len)
   double* d_seg_lo = nullptr;
+  ScanBuffers* scan_buf = nullptr;   // look-back state; method 4 moment tables
   int64_t scan_rows = 0, scan_len = 0, scan_nseg = 0;
 
   // fast method 2 (1-D exponential-sum scans)
@@ -100,6 +107,11 @@ struct Plan {
 
   // fast method 3 (2-D/3-D offset-table stencil)
   StencilState* st_state = nullptr;
+
+  // host pipeline of nlg_apply_fast (row chunks: H2D / apply / D2H overlapped)
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;
+  bool split_begun = false;   // nlg_apply_fast_dev_begin enqueued the halo-independent part
 
   int64_t last_pairs = 0;
   int64_t fast_applies = 0;
@@ -120,6 +132,9 @@ void launch_assemble(const Plan& P, double* A, int64_t N, cudaStream_t s);
 void spans_setup(Plan& P);
 void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void spans_free(Plan& P);
+void moments_setup(Plan& P, int K);   // fast method 4: 1-D K >= 1 centred moment scans
+void moments_apply(Plan& P, const double* u, double* out, cudaStream_t s);
+int64_t moments_segment(const Plan& P);
 void expsum_setup(Plan& P, const nlg_desc& d);
 void expsum_apply(Plan& P, const double* u, double* out, cudaStream_t s);
 void expsum_free(Plan& P);
@@ -130,10 +145,19 @@ void stencil_free(Plan& P);
 int stencil_launches(const Plan& P);
 int stencil_fft_len(const Plan& P);
 bool stencil_box(const Plan& P);   // method 3 runs the box FFT mode (brackets its own stages)
+void stencil_apply_rows(Plan& P, const double* u, double* out, int64_t a, int64_t b, cudaStream_t s);
+void stencil_box_in(Plan& P, const double* u, int64_t p0, int64_t p1, cudaStream_t s);
+void stencil_box_out(Plan& P, const double* u, double* out, int64_t q0, int64_t q1, cudaStream_t s);
+int stencil_components(const Plan& P);
+int stencil_reach_rows(const Plan& P);   // axis-0 rows an output row reads on either side
+int stencil_row_tile(const Plan& P);     // row-range cuts at multiples of it keep results bit-identical
 // box FFT mode of method 3 (fft3.cu): 3-D fractional, constant horizon
 BoxFft* boxfft_setup(const Plan& P, double alpha);
 void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
                   double* out, cudaStream_t s);
+void boxfft_in(Plan& P, BoxFft& B, const double* u, int64_t p0, int64_t p1, cudaStream_t s);
+void boxfft_out(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
+                double* out, int64_t q0, int64_t q1, cudaStream_t s);
 int boxfft_launches(const BoxFft& B);
 int boxfft_length(const BoxFft& B);
 void boxfft_free(BoxFft* B);

@@ -12,6 +12,9 @@
 // (SURVEY §7 hard part 2).
 //   out_i = C_i/delta_i^{d+2} (h^d c_0 S_i - |B_delta| u_i)        (Mass)
 //   out_i = C_i/delta_i^{d+2}  h^d c_0 (S_i - count_i u_i)         (Difference)
+#include <algorithm>
+#include <vector>
+
 #include "plan.hpp"
 
 namespace nlg {
@@ -27,29 +30,52 @@ struct RowGeom {
   int64_t rows, len, nseg;
 };
 
-// Block-wide exclusive scan of (hi, lo) pairs, kScanThreads threads, each
-// owning kSeg / kScanThreads consecutive elements.
-__global__ void __launch_bounds__(kScanThreads) scan_segments(const double* __restrict__ u, RowGeom rg,
+// Single-pass row prefix sums with decoupled look-back (one launch, no
+// serial offset pass). Tiles of kSeg nodes; a CTA takes the next tile ticket
+// (tiles are handed out in row-major order, so every predecessor of a tile is
+// already running or done: forward progress without co-residency
+// assumptions), scans its tile in double-double, publishes the tile aggregate,
+// walks back over its row's predecessors (adding aggregates until it meets an
+// inclusive prefix), publishes its own inclusive prefix and writes GLOBAL
+// exclusive prefixes P(p) = sum_{q < p} u_q. Flags carry the apply's epoch, so
+// nothing is reset between applies.
+struct ScanState {
+  unsigned long long* ticket;   // tickets handed out (monotone across applies)
+  unsigned* flag;               // [tiles] epoch << 2 | {1 aggregate, 2 inclusive}
+  double2* agg;                 // [tiles] (hi, lo)
+  double2* inc;                 // [tiles] (hi, lo)
+};
+
+__device__ __forceinline__ void publish(unsigned* f, unsigned v) {
+  __threadfence();
+  atomicExch(f, v);
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_lookback(const double* __restrict__ u, RowGeom rg,
+                                                             ScanState st, unsigned epoch, unsigned long long base,
                                                              double* __restrict__ pref_hi,
                                                              double* __restrict__ pref_lo,
-                                                             double* __restrict__ seg_hi,
-                                                             double* __restrict__ seg_lo) {
+                                                             double* __restrict__ tot_hi,
+                                                             double* __restrict__ tot_lo) {
   constexpr int PER = kSeg / kScanThreads;
-  const int64_t row = blockIdx.x / rg.nseg;
-  const int64_t seg = blockIdx.x % rg.nseg;
-  const int64_t base = row * rg.len + seg * kSeg;
-  const int64_t lim = min(static_cast<int64_t>(kSeg), rg.len - seg * kSeg);
+  __shared__ unsigned long long s_tile;
+  __shared__ double sh[kScanThreads], sl[kScanThreads];
+  __shared__ dd s_off;
   const int tid = threadIdx.x;
+  if (tid == 0) s_tile = atomicAdd(st.ticket, 1ull) - base;
+  __syncthreads();
+  const int64_t tile = static_cast<int64_t>(s_tile);
+  const int64_t row = tile / rg.nseg, seg = tile % rg.nseg;
+  const int64_t b0 = row * rg.len + seg * kSeg;
+  const int64_t lim = min(static_cast<int64_t>(kSeg), rg.len - seg * kSeg);
   double v[PER];
   dd run{0.0, 0.0};
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int64_t p = static_cast<int64_t>(tid) * PER + j;
-    v[j] = p < lim ? u[base + p] : 0.0;
+    v[j] = p < lim ? u[b0 + p] : 0.0;
     run = dd_add(run, {v[j], 0.0});
   }
-  // block scan of per-thread totals (double-double) through shared memory
-  __shared__ double sh[kScanThreads], sl[kScanThreads];
   sh[tid] = run.hi;
   sl[tid] = run.lo;
   __syncthreads();
@@ -58,43 +84,57 @@ __global__ void __launch_bounds__(kScanThreads) scan_segments(const double* __re
     if (tid >= off) add = {sh[tid - off], sl[tid - off]};
     __syncthreads();
     if (tid >= off) {
-      dd cur = dd_add({sh[tid], sl[tid]}, add);
+      const dd cur = dd_add({sh[tid], sl[tid]}, add);
       sh[tid] = cur.hi;
       sl[tid] = cur.lo;
     }
     __syncthreads();
   }
-  dd excl = tid ? dd{sh[tid - 1], sl[tid - 1]} : dd{0.0, 0.0};
+  if (tid == 0) {
+    const dd agg{sh[kScanThreads - 1], sl[kScanThreads - 1]};
+    dd off{0.0, 0.0};
+    if (seg == 0) {
+      st.inc[tile] = make_double2(agg.hi, agg.lo);
+      publish(st.flag + tile, epoch << 2 | 2u);
+    } else {
+      st.agg[tile] = make_double2(agg.hi, agg.lo);
+      publish(st.flag + tile, epoch << 2 | 1u);
+      for (int64_t p = tile - 1;; --p) {   // look back within the row
+        unsigned f;
+        do {
+          f = *reinterpret_cast<volatile unsigned*>(st.flag + p);
+        } while ((f >> 2) != epoch);
+        __threadfence();
+        if ((f & 3u) == 2u) {
+          const double2 w = __ldcg(st.inc + p);   // L2 (coherent), not a stale L1 line
+          off = dd_add(off, {w.x, w.y});
+          break;
+        }
+        const double2 w = __ldcg(st.agg + p);
+        off = dd_add(off, {w.x, w.y});
+      }
+      const dd inc = dd_add(off, agg);
+      st.inc[tile] = make_double2(inc.hi, inc.lo);
+      publish(st.flag + tile, epoch << 2 | 2u);
+    }
+    if (seg == rg.nseg - 1) {
+      const dd tot = dd_add(off, agg);
+      tot_hi[row] = tot.hi;
+      tot_lo[row] = tot.lo;
+    }
+    s_off = off;
+  }
+  __syncthreads();
+  dd excl = dd_add(s_off, tid ? dd{sh[tid - 1], sl[tid - 1]} : dd{0.0, 0.0});
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int64_t p = static_cast<int64_t>(tid) * PER + j;
     if (p < lim) {
-      pref_hi[base + p] = excl.hi;
-      pref_lo[base + p] = excl.lo;
+      pref_hi[b0 + p] = excl.hi;
+      pref_lo[b0 + p] = excl.lo;
     }
     excl = dd_add(excl, {v[j], 0.0});
   }
-  if (tid == kScanThreads - 1) {
-    seg_hi[row * (rg.nseg + 1) + seg] = sh[tid];
-    seg_lo[row * (rg.nseg + 1) + seg] = sl[tid];
-  }
-}
-
-// Per row: exclusive scan of the segment totals; entry nseg = row total.
-__global__ void scan_offsets(RowGeom rg, double* __restrict__ seg_hi, double* __restrict__ seg_lo) {
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (row >= rg.rows) return;
-  double* sh = seg_hi + row * (rg.nseg + 1);
-  double* sl = seg_lo + row * (rg.nseg + 1);
-  dd run{0.0, 0.0};
-  for (int64_t s = 0; s < rg.nseg; ++s) {
-    const dd t{sh[s], sl[s]};
-    sh[s] = run.hi;
-    sl[s] = run.lo;
-    run = dd_add(run, t);
-  }
-  sh[rg.nseg] = run.hi;
-  sl[rg.nseg] = run.lo;
 }
 
 struct SpanArgs {
@@ -107,18 +147,14 @@ struct SpanArgs {
   double coeff0;
   double c0;
   int rule, form;
-  const double *pref_hi, *pref_lo, *seg_hi, *seg_lo;
+  const double *pref_hi, *pref_lo, *tot_hi, *tot_lo;
   double* out;
 };
 
-// prefix P(row, p) for p in [0, len]
+// global exclusive prefix P(row, p) for p in [0, len] (P(len) = row total)
 __device__ __forceinline__ dd prefix_at(const SpanArgs& a, int64_t row, int64_t p) {
-  const int64_t segs = a.rg.nseg + 1;
-  if (p >= a.rg.len) return {a.seg_hi[row * segs + a.rg.nseg], a.seg_lo[row * segs + a.rg.nseg]};
-  const int64_t s = p / kSeg;
-  const dd off{a.seg_hi[row * segs + s], a.seg_lo[row * segs + s]};
-  const dd loc{a.pref_hi[row * a.rg.len + p], a.pref_lo[row * a.rg.len + p]};
-  return dd_add(off, loc);
+  if (p >= a.rg.len) return {a.tot_hi[row], a.tot_lo[row]};
+  return {a.pref_hi[row * a.rg.len + p], a.pref_lo[row * a.rg.len + p]};
 }
 
 // Exact membership of source multi-index k for target x (Leaf: cube_intersects_ball
@@ -264,7 +300,153 @@ RowGeom row_geom(const Plan& P) {
   return rg;
 }
 
+// ---------------------------------------------------------------------------
+// 1-D, K >= 1: centred moment scans (the reference's Steps 2 + 3,
+// tree.cpp:115-161 and operators.cpp:126-167, re-based). The reference sums
+// raw global monomials x^m u and expands (y - x)^{2j} binomially around the
+// origin, which loses all digits at small delta (ledger L4).
+// Here the moments are centred on short segments: segment s of Ls nodes
+// (Ls a power of two <= the smallest horizon in cells) has centre c_s, node k
+// the exact half-integer offset t_k = k - c_s, and the scan stores
+//   I_m(p) = sum_{k in seg(p), k <= p} t_k^m u_k,   m = 0 .. 2K
+// (double-double, inclusive within the segment; no carry between segments:
+// the origins differ, and a global carry would bring the conditioning back).
+// A target's exact Leaf span [a, b] is cut at segment boundaries; each piece
+// contributes its moment differences shifted from c_s to the target by the
+// binomial identity (t - d)^{2j} = sum_m C(2j, m) t^m (-d)^{2j-m}, |d| <=
+// delta/h + Ls, so the expansion never cancels more than ~4^{2j} ulps:
+//   S_i = sum_j c_j (h / delta)^{2j} sum_pieces sum_m C(2j,m) (-d)^{2j-m} dM_m
+//   out_i = C_i / delta^3 (h S_i - |B_delta| u_i)                  (Mass form)
+
+constexpr int kMaxMom = 7;   // 2K + 1 for K <= 3
+
+struct MomArgs {
+  Geom g;
+  int64_t n_in, ls, lshift;   // segment length Ls = 1 << lshift
+  int nm, K;
+  const double* u;
+  const double* delta;
+  double delta0;
+  const double* coeff;
+  double coeff0;
+  double c[4];                // p(s) = sum_j c_j s^{2j}
+  int rule;
+  double* mhi;                // [nm][n_in]
+  double* mlo;
+  double* out;
+};
+
+// one warp per segment, 32-node strides, warp-shuffle inclusive scans in dd
+__global__ void __launch_bounds__(256) moment_scan(const __grid_constant__ MomArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t s0 = seg << a.lshift;
+  if (s0 >= a.n_in) return;
+  const double cs = static_cast<double>(a.ls - 1) * 0.5;   // centre (segment-local index)
+  dd carry[kMaxMom];
+#pragma unroll
+  for (int m = 0; m < kMaxMom; ++m) carry[m] = {0.0, 0.0};
+  for (int64_t q = 0; q < a.ls; q += 32) {
+    const int64_t k = s0 + q + lane;
+    const bool in = q + lane < a.ls && k < a.n_in;
+    const double uk = in ? a.u[k] : 0.0;
+    const double t = static_cast<double>(q + lane) - cs;
+    double tm = 1.0;
+#pragma unroll
+    for (int m = 0; m < kMaxMom; ++m) {
+      if (m < a.nm) {
+        dd v{tm * uk, fma(tm, uk, -(tm * uk))};        // t^m u as an exact dd product of the double t^m
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double hh = __shfl_up_sync(0xffffffffu, v.hi, o);
+          const double ll = __shfl_up_sync(0xffffffffu, v.lo, o);
+          if (lane >= o) v = dd_add(v, {hh, ll});
+        }
+        v = dd_add(v, carry[m]);
+        if (in) {
+          a.mhi[m * a.n_in + k] = v.hi;
+          a.mlo[m * a.n_in + k] = v.lo;
+        }
+        carry[m] = {__shfl_sync(0xffffffffu, v.hi, 31), __shfl_sync(0xffffffffu, v.lo, 31)};
+        tm *= t;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ dd mom_at(const MomArgs& a, int m, int64_t k, int64_t s0) {
+  // inclusive in-segment prefix at k, 0 before the segment start
+  if (k < s0) return {0.0, 0.0};
+  return {a.mhi[m * a.n_in + k], a.mlo[m * a.n_in + k]};
+}
+
+__global__ void __launch_bounds__(256) moment_eval(const __grid_constant__ MomArgs a) {
+  const Geom& g = a.g;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nout = g.row_end - g.row_begin;
+  if (t >= nout) return;
+  const int64_t kx = g.row_begin + t;
+  const int64_t ii = kx - g.in_begin;
+  const double h = g.h;
+  double x[1] = {coord(kx, h)};
+  const double delta = a.delta ? a.delta[ii] : a.delta0;
+  const double ci = a.coeff ? a.coeff[ii] : a.coeff0;
+  const double r2max = __dmul_rn(delta, delta);
+  const double rc = delta / h;
+  int64_t k[1] = {kx};
+  double out = 0.0;
+  if (member<1>(a.rule, k, x, h, delta, r2max)) {
+    const int64_t est = static_cast<int64_t>(rc);
+    const int64_t er = span_extent<1>(a.rule, k, kx, +1, x, h, delta, r2max, est);
+    const int64_t el = span_extent<1>(a.rule, k, kx, -1, x, h, delta, r2max, est);
+    const int64_t lo = max(kx - el, int64_t(0)) - g.in_begin, hi = min(kx + er, g.n - 1) - g.in_begin;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};   // sum (t - d)^{2j} u over the span, j = 0..K
+    for (int64_t s0 = (lo >> a.lshift) << a.lshift; s0 <= hi; s0 += a.ls) {
+      const int64_t pa = max(lo, s0), pb = min(hi, s0 + a.ls - 1);
+      const double d = static_cast<double>(ii - s0) - static_cast<double>(a.ls - 1) * 0.5;   // target - centre
+      double dm[kMaxMom];
+#pragma unroll
+      for (int m = 0; m < kMaxMom; ++m)
+        dm[m] = m < a.nm ? dd_val(dd_sub(mom_at(a, m, pb, s0), mom_at(a, m, pa - 1, s0))) : 0.0;
+      // (t - d)^{2j} = sum_m C(2j, m) t^m (-d)^{2j - m}
+      double np[kMaxMom];   // (-d)^e
+      np[0] = 1.0;
+#pragma unroll
+      for (int e = 1; e < kMaxMom; ++e) np[e] = np[e - 1] * (-d);
+      acc[0] += dm[0];
+      if (a.K >= 1) acc[1] += np[2] * dm[0] + 2.0 * np[1] * dm[1] + dm[2];
+      if (a.K >= 2) acc[2] += np[4] * dm[0] + 4.0 * np[3] * dm[1] + 6.0 * np[2] * dm[2] + 4.0 * np[1] * dm[3] + dm[4];
+      if (a.K >= 3)
+        acc[3] += np[6] * dm[0] + 6.0 * np[5] * dm[1] + 15.0 * np[4] * dm[2] + 20.0 * np[3] * dm[3] +
+                  15.0 * np[2] * dm[4] + 6.0 * np[1] * dm[5] + dm[6];
+    }
+    const double q = (h / delta) * (h / delta);   // (h / delta)^2: t is in cells
+    double S = 0.0, qj = 1.0;
+    for (int j = 0; j <= a.K; ++j) {
+      S = fma(a.c[j] * qj, acc[j], S);
+      qj *= q;
+    }
+    const double front = __ddiv_rn(ci, delta_power(1, delta));
+    out = front * (g.hd * S - ball_volume(1, delta) * a.u[ii]);
+  } else {
+    const double front = __ddiv_rn(ci, delta_power(1, delta));
+    out = front * (0.0 - ball_volume(1, delta) * a.u[ii]);
+  }
+  a.out[t] = out;
+}
+
 }  // namespace
+
+struct ScanBuffers {
+  ScanState st{};
+  unsigned epoch = 0;
+  unsigned long long tickets = 0;   // handed out so far (host mirror)
+  // method 4 (1-D centred moments)
+  double* mhi = nullptr;
+  double* mlo = nullptr;
+  int64_t ls = 0;
+  int lshift = 0, K = 0;
+};
 
 void spans_setup(Plan& P) {
   const RowGeom rg = row_geom(P);
@@ -272,12 +454,45 @@ void spans_setup(Plan& P) {
   P.scan_len = rg.len;
   P.scan_nseg = rg.nseg;
   const size_t n = static_cast<size_t>(rg.rows * rg.len);
-  const size_t ns = static_cast<size_t>(rg.rows * (rg.nseg + 1));
+  const size_t tiles = static_cast<size_t>(rg.rows * rg.nseg);
+  auto* B = new ScanBuffers();
+  P.scan_buf = B;
   NLG_CUDA(cudaMalloc(&P.d_pref_hi, sizeof(double) * n));
   NLG_CUDA(cudaMalloc(&P.d_pref_lo, sizeof(double) * n));
-  NLG_CUDA(cudaMalloc(&P.d_seg_hi, sizeof(double) * ns));
-  NLG_CUDA(cudaMalloc(&P.d_seg_lo, sizeof(double) * ns));
+  NLG_CUDA(cudaMalloc(&P.d_seg_hi, sizeof(double) * rg.rows));   // row totals
+  NLG_CUDA(cudaMalloc(&P.d_seg_lo, sizeof(double) * rg.rows));
+  NLG_CUDA(cudaMalloc(&B->st.ticket, sizeof(unsigned long long)));
+  NLG_CUDA(cudaMalloc(&B->st.flag, sizeof(unsigned) * tiles));
+  NLG_CUDA(cudaMalloc(&B->st.agg, sizeof(double2) * tiles));
+  NLG_CUDA(cudaMalloc(&B->st.inc, sizeof(double2) * tiles));
+  NLG_CUDA(cudaMemsetAsync(B->st.ticket, 0, sizeof(unsigned long long), P.stream));
+  NLG_CUDA(cudaMemsetAsync(B->st.flag, 0, sizeof(unsigned) * tiles, P.stream));
 }
+
+// K >= 1, 1-D: the centred moment scans (fast method 4)
+void moments_setup(Plan& P, int K) {
+  auto* B = new ScanBuffers();
+  P.scan_buf = B;
+  B->K = K;
+  // segment length: the largest power of two <= the smallest horizon in cells (16 .. 1024)
+  double dmin = P.delta0;
+  if (P.d_delta) {
+    std::vector<double> d(P.n_in);
+    NLG_CUDA(cudaMemcpyAsync(d.data(), P.d_delta, sizeof(double) * P.n_in, cudaMemcpyDeviceToHost, P.stream));
+    NLG_CUDA(cudaStreamSynchronize(P.stream));
+    dmin = *std::min_element(d.begin(), d.end());
+  }
+  int lsh = 4;
+  while (lsh < 10 && static_cast<double>(int64_t{1} << (lsh + 1)) <= dmin / P.geom.h) ++lsh;
+  B->lshift = lsh;
+  B->ls = int64_t{1} << lsh;
+  const size_t nm = static_cast<size_t>(2 * K + 1);
+  NLG_CUDA(cudaMalloc(&B->mhi, sizeof(double) * nm * P.n_in));
+  NLG_CUDA(cudaMalloc(&B->mlo, sizeof(double) * nm * P.n_in));
+  P.fast_method = 4;
+}
+
+int64_t moments_segment(const Plan& P) { return P.scan_buf ? P.scan_buf->ls : 0; }
 
 void spans_free(Plan& P) {
   cudaFree(P.d_pref_hi);
@@ -285,16 +500,30 @@ void spans_free(Plan& P) {
   cudaFree(P.d_seg_hi);
   cudaFree(P.d_seg_lo);
   P.d_pref_hi = P.d_pref_lo = P.d_seg_hi = P.d_seg_lo = nullptr;
+  if (ScanBuffers* B = P.scan_buf) {
+    for (void* p : {static_cast<void*>(B->st.ticket), static_cast<void*>(B->st.flag), static_cast<void*>(B->st.agg),
+                    static_cast<void*>(B->st.inc), static_cast<void*>(B->mhi), static_cast<void*>(B->mlo)})
+      cudaFree(p);
+    delete B;
+    P.scan_buf = nullptr;
+  }
 }
 
 void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   const RowGeom rg = row_geom(P);
-  const unsigned nblk = static_cast<unsigned>(rg.rows * rg.nseg);
+  ScanBuffers& B = *P.scan_buf;
+  const unsigned long long tiles = static_cast<unsigned long long>(rg.rows * rg.nseg);
+  ++B.epoch;
+  if (B.epoch >= (1u << 30)) {   // flag epochs wrap: reset once in a long while
+    NLG_CUDA(cudaMemsetAsync(B.st.flag, 0, sizeof(unsigned) * tiles, s));
+    B.epoch = 1;
+  }
   cudaEvent_t ev;
   stage_begin(P, s, kStSpanScan, &ev);
-  scan_segments<<<nblk, kScanThreads, 0, s>>>(u, rg, P.d_pref_hi, P.d_pref_lo, P.d_seg_hi, P.d_seg_lo);
-  scan_offsets<<<static_cast<unsigned>((rg.rows + 127) / 128), 128, 0, s>>>(rg, P.d_seg_hi, P.d_seg_lo);
-  stage_end(P, s, kStSpanScan, ev, 2);
+  scan_lookback<<<static_cast<unsigned>(tiles), kScanThreads, 0, s>>>(u, rg, B.st, B.epoch, B.tickets, P.d_pref_hi,
+                                                                        P.d_pref_lo, P.d_seg_hi, P.d_seg_lo);
+  B.tickets += tiles;
+  stage_end(P, s, kStSpanScan, ev, 1);
   stage_begin(P, s, kStSpanEval, &ev);
   SpanArgs a;
   a.g = P.geom;
@@ -309,8 +538,8 @@ void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   a.form = P.form;
   a.pref_hi = P.d_pref_hi;
   a.pref_lo = P.d_pref_lo;
-  a.seg_hi = P.d_seg_hi;
-  a.seg_lo = P.d_seg_lo;
+  a.tot_hi = P.d_seg_hi;
+  a.tot_lo = P.d_seg_lo;
   a.out = out;
   const unsigned blocks = static_cast<unsigned>((P.n_out + 255) / 256);
   switch (P.geom.dim) {
@@ -318,6 +547,35 @@ void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
     case 2: span_eval<2><<<blocks, 256, 0, s>>>(a); break;
     default: span_eval<3><<<blocks, 256, 0, s>>>(a); break;
   }
+  stage_end(P, s, kStSpanEval, ev, 1);
+}
+
+void moments_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
+  ScanBuffers& B = *P.scan_buf;
+  MomArgs a;
+  a.g = P.geom;
+  a.n_in = P.n_in;
+  a.ls = B.ls;
+  a.lshift = B.lshift;
+  a.K = B.K;
+  a.nm = 2 * B.K + 1;
+  a.u = u;
+  a.delta = P.d_delta;
+  a.delta0 = P.delta0;
+  a.coeff = P.d_coeff;
+  a.coeff0 = P.coeff0;
+  for (int j = 0; j < 4; ++j) a.c[j] = j < P.prof.npoly ? P.prof.poly[j] : 0.0;
+  a.rule = P.rule;
+  a.mhi = B.mhi;
+  a.mlo = B.mlo;
+  a.out = out;
+  cudaEvent_t ev;
+  stage_begin(P, s, kStSpanScan, &ev);
+  const int64_t nseg = (P.n_in + B.ls - 1) / B.ls;
+  moment_scan<<<static_cast<unsigned>((nseg * 32 + 255) / 256), 256, 0, s>>>(a);
+  stage_end(P, s, kStSpanScan, ev, 1);
+  stage_begin(P, s, kStSpanEval, &ev);
+  moment_eval<<<static_cast<unsigned>((P.n_out + 255) / 256), 256, 0, s>>>(a);
   stage_end(P, s, kStSpanEval, ev, 1);
 }
 

@@ -1111,6 +1111,34 @@ void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   launch(a, s, S->tab_bytes);
 }
 
+// Row-range pieces of the apply (the chunked host pipeline of nlg_apply_fast).
+// Output rows [a, b) relative to row_begin; u covers the plan's input rows.
+// Scalar operators only (the peridynamic planes are strided by n_out).
+void stencil_apply_rows(Plan& P, const double* u, double* out, int64_t a, int64_t b, cudaStream_t s) {
+  StencilState* S = P.st_state;
+  if (b <= a) return;
+  const int64_t off = a * P.geom.stride0;
+  StArgs A = make_args(P, *S, 0, u, out + off);
+  A.g.row_begin = P.geom.row_begin + a;
+  A.g.row_end = P.geom.row_begin + b;
+  A.diag = S->diag + off;
+  A.scale = S->scale ? S->scale + off : nullptr;
+  launch(A, s, S->tab_bytes);
+}
+void stencil_box_in(Plan& P, const double* u, int64_t p0, int64_t p1, cudaStream_t s) {
+  boxfft_in(P, *P.st_state->box, u, p0, p1, s);
+}
+void stencil_box_out(Plan& P, const double* u, double* out, int64_t q0, int64_t q1, cudaStream_t s) {
+  StencilState* S = P.st_state;
+  boxfft_out(P, *S->box, u, S->scale_const ? nullptr : S->scale, S->scale0, S->diag, out, q0, q1, s);
+}
+int stencil_reach_rows(const Plan& P) { return P.st_state ? P.st_state->H : 0; }
+// output rows per CTA row of the sweep: row ranges cut at multiples of it keep
+// the CTA tiling (and so every warp's sweep range and summation order) of the
+// one-call apply, so a chunked apply is bit-identical to it
+int stencil_row_tile(const Plan& P) { return P.geom.dim == 2 ? kBY : 1; }
+int stencil_components(const Plan& P) { return P.st_state ? (P.st_state->kind == 1 ? P.geom.dim : 1) : 1; }
+
 void stencil_free(Plan& P) {
   StencilState* S = P.st_state;
   if (!S) return;

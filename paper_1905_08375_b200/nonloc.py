@@ -271,6 +271,20 @@ class Plan:
         A.check(A.lib().nlg_apply_fast_dev(self._h, C.c_void_p(u_ptr), C.c_void_p(out_ptr),
                                            C.c_void_p(stream)))
 
+    def apply_fast_dev_begin(self, u_ptr: int, out_ptr: int, stream: int = 0) -> None:
+        """The halo-independent part of a sharded fast apply (nlg_apply_fast_dev_begin)."""
+        A.check(A.lib().nlg_apply_fast_dev_begin(self._h, C.c_void_p(u_ptr), C.c_void_p(out_ptr),
+                                                 C.c_void_p(stream)))
+
+    def apply_fast_dev_end(self, u_ptr: int, out_ptr: int, stream: int = 0) -> None:
+        A.check(A.lib().nlg_apply_fast_dev_end(self._h, C.c_void_p(u_ptr), C.c_void_p(out_ptr),
+                                               C.c_void_p(stream)))
+
+    def apply_fast_host_ptr(self, u_ptr: int, out_ptr: int) -> None:
+        """nlg_apply_fast on raw host pointers (pinned buffers: the chunked
+        H2D / apply / D2H pipeline overlaps its copies)."""
+        A.check(A.lib().nlg_apply_fast(self._h, C.cast(u_ptr, A._dp), C.cast(out_ptr, A._dp)))
+
     def apply_direct_dev(self, u_ptr: int, out_ptr: int, pairs_ptr: int = 0, stream: int = 0) -> None:
         A.check(A.lib().nlg_apply_direct_dev(self._h, C.c_void_p(u_ptr), C.c_void_p(out_ptr),
                                              C.c_void_p(pairs_ptr or None), C.c_void_p(stream)))
@@ -573,6 +587,68 @@ class NonlocalOperator:
 
     def apply_direct_at(self, u, targets, return_pairs: bool = False):
         return self.plan.apply_direct_at(u, targets, return_pairs)
+
+
+class Group:
+    """Multi-GPU operator (nlg_group_*, csrc/group.cu): the grid split into
+    axis-0 slabs over `devices`, one sharded plan per device, u's halo rows
+    exchanged device to device by NCCL (a repeated device ordinal: peer
+    copies), overlapped with the halo-independent part of each apply.
+    Arguments as Plan, over the whole grid."""
+
+    def __init__(self, devices, *, dim, n, family, route=A.ROUTE_FULL, poly=None, alpha=1.0, rule=A.POINT,
+                 form=A.DIFFERENCE, exterior=A.CLIP, delta=None, delta0=0.0, coeff=None, coeff0=1.0, kappa=None):
+        keep = []
+
+        def arr(a):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            keep.append(a)
+            return a
+
+        poly, delta, coeff, kappa = map(arr, (poly, delta, coeff, kappa))
+        self.dim, self.n = dim, n
+        self.components = dim if family == A.PERIDYNAMIC else 1
+        desc = A.Desc(dim, n, family, route, A.dptr(poly), 0 if poly is None else len(poly), None, 0, 0, 1.0,
+                      alpha, rule, form, int(exterior), 0, A.dptr(delta), delta0, 0.0, A.dptr(coeff), coeff0,
+                      A.dptr(kappa), 0, 0, 0)
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        A.check(A.lib().nlg_group_create(C.byref(desc), len(devices), devs, C.byref(h)), group=True)
+        self._h = h
+        nd, nc = C.c_int(0), C.c_int(0)
+        rb = np.zeros(len(devices), dtype=np.int64)
+        re = np.zeros(len(devices), dtype=np.int64)
+        nin = np.zeros(len(devices), dtype=np.int64)
+        A.check(A.lib().nlg_group_info(self._h, C.byref(nd), C.byref(nc), rb.ctypes.data_as(A._ip),
+                                       re.ctypes.data_as(A._ip), nin.ctypes.data_as(A._ip)), group=True)
+        self.ndev, self.nccl = nd.value, bool(nc.value)
+        self.row_begin, self.row_end, self.n_in = rb, re, nin
+
+    def apply(self, u) -> np.ndarray:
+        u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
+        if u.size != self.components * self.n ** self.dim:
+            raise ValueError("u size does not match grid")
+        out = np.empty_like(u)
+        A.check(A.lib().nlg_group_apply_fast(self._h, A.dptr(u), A.dptr(out)), group=True)
+        return out
+
+    def apply_dev(self, u_ptrs, out_ptrs) -> None:
+        up = (C.c_void_p * self.ndev)(*u_ptrs)
+        op = (C.c_void_p * self.ndev)(*out_ptrs)
+        A.check(A.lib().nlg_group_apply_fast_dev(self._h, up, op), group=True)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            A.lib().nlg_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------------------

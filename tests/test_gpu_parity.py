@@ -51,7 +51,9 @@ def test_truncated_operator_matches_reference(N, name):
     if K <= 1 or name == "trunc_1d_n2048_k3_bump":
         assert rel(out, g["fast"]) <= (1e-12 if K == 0 else 1e-10)
     if K == 0:
-        assert op.fast_method() == 1   # span prefix sums, not the direct quadrature
+        assert op.fast_method() == 1   # span prefix sums (look-back scan), not the direct quadrature
+    elif int(g["dim"]) == 1:
+        assert op.fast_method() == 4   # centred moment scans, not the direct quadrature
 
 
 @pytest.mark.parametrize("name", TRUNC)
