@@ -70,16 +70,19 @@ def _dfma_peak():
         return None
 
 
-def _traffic(workload, kernel):
-    """ncu dram bytes (read + write) per launch of `kernel` for `workload`, from a
-    committed `ncu --set full` capture (profiles/ncu_traffic.json), or None."""
+def _traffic(keys, kernel):
+    """ncu dram bytes (read + write) per launch of the stage `kernel` for the
+    workload (any of `keys`), from a committed `ncu --set full` capture
+    (profiles/ncu_traffic.json, written by tools/ncu_summary.py --r02), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            t = json.load(f).get(workload)
+            t = json.load(f)
     except Exception:
         return None
-    if isinstance(t, dict):
-        return t.get(kernel, {}).get("bytes") if isinstance(t.get(kernel), dict) else t.get(kernel)
+    for k in keys:
+        e = t.get(k)
+        if isinstance(e, dict) and isinstance(e.get(kernel), dict):
+            return e[kernel].get("bytes")
     return None
 
 
@@ -338,7 +341,7 @@ def measure(name, args, world, rank, local, dev, full=True):
     import torch
     import torch.distributed as dist
     from paper_1905_08375_b200 import nonloc as NL
-    from paper_1905_08375_b200.slabs import Slab
+    from paper_1905_08375_b200.slabs import Slab, slab_apply
 
     w = _workload(name)
     stride = w.n ** (w.dim - 1)
@@ -362,9 +365,7 @@ def measure(name, args, world, rank, local, dev, full=True):
     def step():
         if world > 1:
             # halo-independent part first, u's halos in flight meanwhile
-            plan.apply_fast_dev_begin(u_in.data_ptr(), out.data_ptr(), stream.cuda_stream)
-            sl.exchange(u_in)
-            plan.apply_fast_dev_end(u_in.data_ptr(), out.data_ptr(), stream.cuda_stream)
+            slab_apply(sl, plan, u_in, out, stream.cuda_stream)
         else:
             plan.apply_fast_dev(u_in.data_ptr(), out.data_ptr(), stream.cuda_stream)
 
@@ -433,7 +434,7 @@ def measure(name, args, world, rank, local, dev, full=True):
            "path": "nlg_apply_fast (host pointers; plane-chunked H2D / apply / D2H pipeline where the "
                    "method supports it)"}
 
-    res = {"w": w, "plan": plan, "value": value, "ms_per_step": ms_step, "e2e": e2e, "stages": stages,
+    res = {"key": name, "w": w, "plan": plan, "value": value, "ms_per_step": ms_step, "e2e": e2e, "stages": stages,
            "launches": launches, "clocks": clk, "plan_seconds": t_plan, "n_out": plan.n_out}
     del u_in, out, flush
     return res
@@ -456,7 +457,7 @@ def _roofline(res, world):
         # kernel's average launch duration (CUDA events, serialized pass)
         dom_ms = per_launch[dom]
         ach = bpp * units / (dom_ms * 1e-3) / 1e9
-        roof.update({"achieved": ach, "frac": ach / peak, "traffic": _traffic(w.name, dom),
+        roof.update({"achieved": ach, "frac": ach / peak, "traffic": _traffic((res["key"], w.name), dom),
                      "dominant_kernel": dom, "dominant_ms_per_launch": dom_ms,
                      "dominant_share": share[dom],
                      "scope": f"dominant kernel: algorithmic {bpp} B/pt x {units} pts per launch / its mean "

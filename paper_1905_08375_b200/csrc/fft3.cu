@@ -70,6 +70,9 @@ struct BoxFft {
   double tie_w = 0.0;                               // w_m
   double tie_thr = 0.0;                             // r2 < thr  <=>  sqrt_rn(r2) < delta
   void* tie_mask = nullptr;                         // [n_out] per-target inclusion bits (uint32 / uint64)
+  bool tie_tma = false;                             // fixed-band tie pass with the TMA plane ring (f3_ties_tma)
+  CUtensorMap tmu{}, tmk{};                         // u, kappa over the input planes: boxes of one window
+  const double* tmu_base = nullptr;                 // the u the map tmu was encoded for
 };
 
 namespace {
@@ -666,6 +669,163 @@ __global__ void __launch_bounds__(kTieTX * kTieTY, NLG_TIES_MINB) f3_ties(const 
   }
 }
 
+// Tie pass, fixed band (|t|^2 = kTieFixedM), fed by TMA. Same sums and
+// combine as f3_ties; the source planes of the residue class arrive in a ring
+// of NR = NS + 2 slots by cp.async.bulk.tensor (one elected thread, boxes of
+// the (8 + 2R) x (32 + 2R) window of u and of kappa, zero fill outside the
+// domain by the tensor map's bounds), each slot completing on its own
+// mbarrier, two planes ahead of the step that first reads them: the threads
+// issue no staging instructions and the plane latency is hidden by two steps
+// of sums. Measured on the cp.async version: without its tie sums the pass
+// still took 7.1 of 9.9 ms (staging / operand latency, one step ahead).
+__device__ __forceinline__ void mbar_wait(unsigned mb, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n\t}" ::"r"(mb),
+      "r"(parity)
+      : "memory");
+}
+
+template <bool KW>
+__global__ void __launch_bounds__(kTieTX * kTieTY, 3)
+    f3_ties_tma(const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmk,
+                const __grid_constant__ TieArgs a) {
+  constexpr TieSet TS = make_ties(kTieFixedM, true);
+  constexpr TieSet AX = make_axis_ties(kTieFixedM);
+  constexpr int R = TS.R, q = TS.q, NS = 2 * R / q + 1, NR = NS + 2;
+  constexpr int W = kTieTX + 2 * R, SB = (kTieTY + 2 * R) * W;      // window elements
+  constexpr int SLOT = (KW ? 2 : 1) * SB;                             // doubles per ring slot
+  constexpr unsigned BYTES = sizeof(double) * SLOT;
+  extern __shared__ __align__(128) double rsm[];
+  __shared__ __align__(8) unsigned long long mbar[NR];
+  const Geom& g = a.g;
+  const int n = static_cast<int>(g.n);
+  const int64_t nn = g.n * g.n;
+  const int tid = threadIdx.y * kTieTX + threadIdx.x;
+  const int x0 = blockIdx.x * kTieTX, y0 = blockIdx.y * kTieTY;
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  const bool live = x < n && y < n;
+  const int cls = static_cast<int>(blockIdx.z) % q;
+  const int zb = static_cast<int>(a.zlo) + static_cast<int>(blockIdx.z / q) * kTieZC;
+  const int ze = min(static_cast<int>(a.zhi), zb + kTieZC);
+  const int zf = zb + ((cls - zb) % q + q) % q;                      // first target plane of the class
+  if (zf >= ze) return;
+  const int J = (ze - zf + q - 1) / q;                                // target planes of this CTA
+  const int NP = J + NS - 1;                                          // source planes: zf - R + i q, i < NP
+  const unsigned mb0 = static_cast<unsigned>(__cvta_generic_to_shared(mbar));
+  const unsigned sm0 = static_cast<unsigned>(__cvta_generic_to_shared(rsm));
+  auto issue = [&](int i) {                                           // plane i -> slot i % NR (thread 0)
+    const int sl = i % NR;
+    const unsigned mb = mb0 + 8u * sl, dst = sm0 + static_cast<unsigned>(sizeof(double)) * SLOT * sl;
+    const int pz = zf - R + i * q - static_cast<int>(g.in_begin);      // input plane (out of range: zero fill)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(BYTES) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(&tmu), "r"(x0 - R), "r"(y0 - R), "r"(pz), "r"(mb)
+        : "memory");
+    if (KW)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+              dst + static_cast<unsigned>(sizeof(double)) * SB),
+          "l"(&tmk), "r"(x0 - R), "r"(y0 - R), "r"(pz), "r"(mb)
+          : "memory");
+  };
+  if (tid == 0) {
+    for (int i = 0; i < NR; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u * i) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int i = 0; i < min(NS + 1, NP); ++i) issue(i);
+  }
+  __syncthreads();
+  auto wait_plane = [&](int i) { mbar_wait(mb0 + 8u * (i % NR), static_cast<unsigned>((i / NR) & 1)); };
+  for (int i = 0; i < NS - 1; ++i) wait_plane(i);
+  const uint32_t* mask = static_cast<const uint32_t*>(a.mask);
+  const int tgt = y * n + x;
+  const int sbase = (threadIdx.y + R) * W + threadIdx.x + R;
+  uint32_t mn = 0;
+  double2 abn = make_double2(0.0, 0.0);
+  double edn = 0.0, esn = 0.0;
+  auto fetch = [&](int z) {
+    mn = 0;
+    abn = make_double2(0.0, 0.0);
+    edn = esn = 0.0;
+    if (live && z < ze) {
+      const int64_t oi = (static_cast<int64_t>(z) - g.row_begin) * nn + tgt;
+      const int64_t zi = static_cast<int64_t>(z) - g.in_begin;
+      mn = __ldg(mask + oi);
+      abn = a.zab[(zi * a.zly + y) * a.zlx + x];
+      edn = __ldg(a.diag + oi);
+      esn = a.scale ? __ldg(a.scale + oi) : a.scale0;
+    }
+  };
+  auto prefetch = [&](int z) {   // the operands of a later step into L2
+    if (live && z < ze) {
+      const int64_t oi = (static_cast<int64_t>(z) - g.row_begin) * nn + tgt;
+      const int64_t zi = static_cast<int64_t>(z) - g.in_begin;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.zab + (zi * a.zly + y) * a.zlx + x));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.diag + oi));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(mask + oi));
+    }
+  };
+  fetch(zf);
+  prefetch(zf + q);
+  for (int j = 0; j < J; ++j) {
+    const int zt = zf + j * q;
+    const uint32_t m = mn;
+    const double2 ab = abn;
+    const double ed = edn, es = esn;
+    __syncthreads();                                                  // step j - 1's reads done: slot of plane j - 1 free
+    if (tid == 0 && j + NS + 1 < NP) issue(j + NS + 1);               // two planes ahead
+    wait_plane(j + NS - 1);                                           // the newest plane this step reads
+    fetch(zt + q);
+    prefetch(zt + 2 * q);
+    const int64_t oi = (static_cast<int64_t>(zt) - g.row_begin) * nn + tgt;
+    // axis ties (outside the window): the few included sources from global memory
+    double xu[AX.n > 0 ? AX.n : 1], xk[AX.n > 0 ? AX.n : 1];
+    {
+      const int64_t ii = (static_cast<int64_t>(zt) - g.in_begin) * nn + tgt;
+#pragma unroll
+      for (int k = 0; k < AX.n; ++k) {
+        const bool on = (m >> AX.bit[k]) & 1u;
+        const int64_t sidx = ii + (static_cast<int64_t>(AX.t0[k]) * n + AX.t1[k]) * n + AX.t2[k];
+        xu[k] = on ? __ldg(a.u + sidx) : 0.0;
+        xk[k] = on && KW ? __ldg(a.kappa + sidx) : 0.0;
+      }
+    }
+    const double* slot[NS];
+#pragma unroll
+    for (int r = 0; r < NS; ++r) slot[r] = rsm + ((j + r) % NR) * SLOT + sbase;
+    // ties no lane of the warp includes are skipped (~15 of 24 needed per warp)
+    const unsigned wm = __reduce_or_sync(0xffffffffu, m);
+    double A = 0.0, B = 0.0, A1 = 0.0, B1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < TS.n; ++k) {
+      if (!(wm & (1u << TS.bit[k]))) continue;
+      const double* sp = slot[(TS.t0[k] + R) / q] + TS.t1[k] * W + TS.t2[k];
+      const double uu = (m & (1u << TS.bit[k])) ? sp[0] : 0.0;
+      if (k & 1) {
+        A1 += uu;
+        if (KW) B1 = fma(uu, sp[SB], B1);
+      } else {
+        A += uu;
+        if (KW) B = fma(uu, sp[SB], B);
+      }
+    }
+    A += A1;
+    B += B1;
+#pragma unroll
+    for (int k = 0; k < AX.n; ++k) {
+      A += xu[k];
+      if (KW) B = fma(xu[k], xk[k], B);
+    }
+    if (live) {   // out = s (kappa (A + w At) + B + w Bt - u diag); own u, kappa from the ring
+      const double* own = slot[R / q];
+      const double uA = fma(a.w, A, ab.x);
+      const double X = KW ? fma(own[SB], uA, fma(a.w, B, ab.y)) : uA;
+      a.out[oi] = es * (X - own[0] * ed);
+    }
+  }
+}
+
 // supported axis lengths 2^a 3^b 5^c (multiples of 8 columns, <= 1024 threads per column CTA)
 #define NLG_F3_L(X) \
   X(48) X(64) X(72) X(80) X(96) X(128) X(144) X(160) X(192) X(256) X(288) X(384) X(400) X(512) X(576) X(768) \
@@ -831,6 +991,28 @@ bool encode_cols_map(CUtensorMap* m, void* base, int lx, int ly, int64_t rows, i
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D tensor map over an input field (x: n, y: n, z: input planes) with
+// boxes of one tie window ((32 + 2R) x (8 + 2R) x 1); out-of-bounds boxes
+// are zero filled (the domain / slab edges).
+bool encode_window_map(CUtensorMap* m, const double* base, int64_t n, int64_t planes, int R) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess || !fn)
+      return false;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if ((n * 8) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(planes)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(n) * 8, static_cast<cuuint64_t>(n) * n * 8};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(kTieTX + 2 * R), static_cast<cuuint32_t>(kTieTY + 2 * R), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 // Box FFT mode applies to the 3-D fractional operator with a constant horizon
@@ -956,6 +1138,14 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
     else f3_tie_mask<uint32_t><<<grid, dim3(32, 8), 0, P.stream>>>(t, static_cast<uint32_t*>(B->tie_mask));
     NLG_CUDA(cudaGetLastError());
     NLG_CUDA(cudaStreamSynchronize(P.stream));
+    {
+      constexpr TieSet kD = make_ties(kTieFixedM, true);
+      const char* te = std::getenv("NLG_TIES_TMA");
+      B->tie_tma = !(te && std::atoi(te) == 0) && B->tie_m == kTieFixedM && B->ntie <= 32 && n % 2 == 0;
+      if (B->tie_tma && P.d_kappa) B->tie_tma = encode_window_map(&B->tmk, P.d_kappa, n, n_in, kD.R);
+      for (const void* f : {reinterpret_cast<const void*>(f3_ties_tma<true>), reinterpret_cast<const void*>(f3_ties_tma<false>)})
+        NLG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));   // + static mbarriers
+    }
     for (const void* f : {reinterpret_cast<const void*>(f3_ties<0, true, uint32_t>), reinterpret_cast<const void*>(f3_ties<0, false, uint32_t>),
                           reinterpret_cast<const void*>(f3_ties<0, true, uint64_t>), reinterpret_cast<const void*>(f3_ties<0, false, uint64_t>),
                           reinterpret_cast<const void*>(f3_ties<kTieFixedM, true, uint32_t>),
@@ -1051,7 +1241,13 @@ void boxfft_out(Plan& P, BoxFft& B, const double* u, const double* scale, double
     const dim3 grid(static_cast<unsigned>((B.n + kTieTX - 1) / kTieTX), static_cast<unsigned>((B.n + kTieTY - 1) / kTieTY),
                     static_cast<unsigned>((q1 - q0 + kTieZC - 1) / kTieZC * q));
     const dim3 blk(kTieTX, kTieTY);
-    if (wide) {
+    if (fixed && B.tie_tma && (B.tmu_base == u || encode_window_map(&B.tmu, u, B.n, B.n_in, kDense.R))) {
+      B.tmu_base = u;
+      constexpr int NR = 2 * kDense.R / kDense.q + 3;
+      const size_t sbt = sizeof(double) * NR * (P.d_kappa ? 2 : 1) * (kTieTY + 2 * kDense.R) * (kTieTX + 2 * kDense.R);
+      if (P.d_kappa) f3_ties_tma<true><<<grid, blk, sbt, s>>>(B.tmu, B.tmk, t);
+      else f3_ties_tma<false><<<grid, blk, sbt, s>>>(B.tmu, B.tmk, t);
+    } else if (wide) {
       if (P.d_kappa) f3_ties<0, true, uint64_t><<<grid, blk, sb, s>>>(t);
       else f3_ties<0, false, uint64_t><<<grid, blk, sb, s>>>(t);
     } else if (fixed) {

@@ -92,3 +92,15 @@ class Slab:
         if ops:
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
+
+
+def slab_apply(sl: Slab, plan, u_in, out, stream: int = 0) -> None:
+    """One sharded fast apply, the sequence bench.py times at N > 1: the part
+    of the apply that does not read u's halo rows (plan.apply_fast_dev_begin),
+    the halo exchange with the neighbours (NCCL point-to-point; it overlaps
+    the begin part on the device), then the rest (plan.apply_fast_dev_end).
+    u_in covers the slab's input rows; only its owned rows need to be valid on
+    entry."""
+    plan.apply_fast_dev_begin(u_in.data_ptr(), out.data_ptr(), stream)
+    sl.exchange(u_in)
+    plan.apply_fast_dev_end(u_in.data_ptr(), out.data_ptr(), stream)

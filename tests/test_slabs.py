@@ -61,6 +61,82 @@ def test_gloo_halo_exchange_world2(dim, n, delta):
         assert err == 0.0, f"rank {rank}: rel {err}"
 
 
+class _OraclePlan:
+    """Stands in for a sharded plan in bench.py's N > 1 step: begin() sees u_in
+    before the exchange (records that its halo rows are still unset), end()
+    evaluates the slab's output rows with the oracle from u_in alone."""
+
+    def __init__(self, O, sl, dim, n, delta, u_in):
+        self.O, self.sl, self.dim, self.n, self.delta, self.u_in = O, sl, dim, n, delta, u_in
+        self.begin_saw = None
+
+    def apply_fast_dev_begin(self, u_ptr, out_ptr, stream):
+        self.begin_saw = self.u_in.clone()
+
+    def apply_fast_dev_end(self, u_ptr, out_ptr, stream):
+        sl, N = self.sl, self.n ** self.dim
+        v = np.zeros(N)
+        v[sl.in_begin * sl.stride: sl.in_end * sl.stride] = self.u_in.numpy()
+        own = sl.output_slice()
+        self.out, _ = self.O.apply(self.dim, self.n, v, targets=np.arange(own.start, own.stop),
+                                   family=self.O.FRACTIONAL, alpha=1.5, delta0=self.delta)
+
+
+def _bench_seq_worker(rank, world, port, dim, n, delta, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    import oracle as O
+    from paper_1905_08375_b200.slabs import Slab, slab_apply
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    N, stride = n ** dim, n ** (dim - 1)
+    u = O.random_vector(N, 6)
+    sl = Slab(n, stride, int(np.floor(delta * n)) + 2, rank, world)
+    u_in = torch.full((sl.n_in,), float("nan"), dtype=torch.float64)   # halos unset until the exchange
+    u_in[sl.halo_lo * stride: sl.halo_lo * stride + sl.n_out] = torch.from_numpy(u[sl.output_slice()])
+    plan = _OraclePlan(O, sl, dim, n, delta, u_in)
+    slab_apply(sl, plan, u_in, u_in, 0)
+    own = sl.output_slice()
+    ref, _ = O.apply(dim, n, u, targets=np.arange(own.start, own.stop), family=O.FRACTIONAL, alpha=1.5,
+                     delta0=delta)
+    halos_unset_at_begin = bool(torch.isnan(plan.begin_saw).any()) if sl.n_in > sl.n_out else True
+    q.put((rank, O.rel_inf(plan.out, ref), halos_unset_at_begin))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dim,n,delta", [(1, 512, 0.05), (3, 16, 0.25)])
+def test_gloo_bench_slab_sequence_world2(dim, n, delta):
+    """bench.py's N > 1 step (slabs.slab_apply: begin -> exchange -> end) with
+    the oracle standing in for the plan reproduces the whole-grid oracle."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29650 + dim * 11 + n % 89
+    procs = [ctx.Process(target=_bench_seq_worker, args=(r, 2, port, dim, n, delta, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, err, unset in res:
+        assert err == 0.0, f"rank {rank}: rel {err}"
+        assert unset, f"rank {rank}: begin() already saw halo values"
+
+
+def test_bench_multi_gpu_fails_loudly_without_gpus():
+    """--gpus 2 on a box without two GPUs must not silently run one rank."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "--gpus 2" in (r.stderr + r.stdout)
+
+
 def test_slab_rows_partition():
     from paper_1905_08375_b200.slabs import slab_rows
     for n in (7, 64, 4096, 768):

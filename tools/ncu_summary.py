@@ -69,7 +69,26 @@ def to_bytes(s):
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
+# kernel name -> bench.py stage (nlg stage names, _capi.STAGES)
+def stage_of(name):
+    import re
+    n = name.replace("void ", "").replace("nlg::<unnamed>::", "").replace("<unnamed>::", "")
+    rules = [(r"f3_ties", "box_ties"), (r"f3_rows<\d+, 0", "box_pa_rows_fwd"), (r"f3_rows<\d+, 1", "box_pe_rows_inv"),
+             (r"f3_cols(_tma)?<\d+, 0", "box_pb_cols_fwd"), (r"f3_cols(_tma)?<\d+, 1", "box_pd_cols_inv"),
+             (r"f3_zstencil", "box_pc_zstencil"), (r"es_tail_walk<\d+, 1", "es_main"),
+             (r"es_tail_walk<\d+, 0", "es_aggregate"), (r"es_carry", "es_carry"), (r"cols_fwd", "es_fft_p1_cols_fwd"),
+             (r"fs_rows", "es_fft_p2_rows"), (r"cols_inv", "es_fft_p3_cols_inv"), (r"es_fft_combine", "es_combine"),
+             (r"stencil", "stencil"), (r"direct", "direct"), (r"scan_lookback|moment_scan", "span_scan"),
+             (r"span_eval|moment_eval", "span_eval")]
+    for pat, st in rules:
+        if re.search(pat, n):
+            return st
+    return n
+
+
 def main():
+    if sys.argv[1] == "--r02":
+        return main_r02(sys.argv[2:])
     lpath, fpath, workload, tag = sys.argv[1:5]
     os.makedirs(PROF, exist_ok=True)
     L = launches(lpath)
@@ -86,6 +105,33 @@ def main():
                              "source": f"profiles/{tag}_ncu_full.json"}
         json.dump(traffic, open(tp, "w"), indent=1)
     print(json.dumps({"launches": L, "traffic": traffic.get(workload)}, indent=1))
+
+
+def main_r02(argv):
+    """ncu_summary.py --r02 <launches.csv|-> <full.ncu-rep> <workload key> <tag>: every
+    captured kernel keyed by its bench stage; ncu_traffic.json[workload][stage] =
+    dram read+write bytes per launch."""
+    lpath, fpath, workload, tag = argv[:4]
+    os.makedirs(PROF, exist_ok=True)
+    res = {"workload": workload}
+    if lpath != "-":
+        L = launches(lpath)
+        res["launches"] = L
+        json.dump(L, open(os.path.join(PROF, f"{tag}_launches.json"), "w"), indent=1)
+    F = full(fpath)
+    for d in F:
+        d["stage"] = stage_of(d["Kernel Name"])
+    json.dump(F, open(os.path.join(PROF, f"{tag}_ncu_full.json"), "w"), indent=1)
+    tp = os.path.join(PROF, "ncu_traffic.json")
+    traffic = json.load(open(tp)) if os.path.exists(tp) else {}
+    ent = traffic.get(workload) if isinstance(traffic.get(workload), dict) and "kernel" not in traffic.get(workload, {}) else {}
+    for d in F:
+        if "dram__bytes_read.sum" in d:
+            ent[d["stage"]] = {"bytes": to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"]),
+                               "kernel": d["Kernel Name"], "source": f"profiles/{tag}_ncu_full.json"}
+    traffic[workload] = ent
+    json.dump(traffic, open(tp, "w"), indent=1)
+    print(json.dumps({k: v["bytes"] for k, v in ent.items()}, indent=1))
 
 
 if __name__ == "__main__":
