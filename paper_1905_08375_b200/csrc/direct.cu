@@ -11,6 +11,9 @@
 //   KIND 4  BASELINE peridynamics  -h^d sum C(x)/|r| (e.(u_y-u_x)) e, Point rule
 // Exterior: clip (reference) or zero collar (u = 0 outside, kappa_y := kappa_x,
 // delta_y := delta_x outside).
+#include <cmath>
+#include <vector>
+
 #include "plan.hpp"
 
 namespace nlg {
@@ -32,6 +35,8 @@ struct DirectArgs {
   int64_t ntargets;
   double* out;
   unsigned long long* pairs;
+  const double2* wfrac;   // KIND 3 weight table: (|d h|^-alpha, 1 / (d h)^2) by |d| (1-D) or |d|^2
+  int64_t wfrac_len;
 };
 
 template <int DIM>
@@ -207,6 +212,118 @@ __global__ void __launch_bounds__(256) direct_kernel(DirectArgs a) {
   }
 }
 
+// KIND 3 (the BASELINE fractional operator) with the per-pair work cut to
+// the algorithmic minimum. Same inclusion set and pair count as direct_kernel:
+// integer |d|^2 decides every candidate outside the tie band (m_lo, m_hi
+// around (delta/h)^2, common.cuh tie_band), the reference's float predicate
+// sqrt(r2) < delta (operators.cpp:71-78) the ones inside it; each row of the
+// window is cut to |d_last|^2 <= m_hi - (the other components), so no
+// candidate outside the ball is visited. The weight |r|^-alpha comes from a
+// plan table at the exact lattice distance, w(m) = |d h|^-alpha, corrected to
+// the float r2 of the node coordinates to first order,
+//   |r|^-alpha = w(m) (1 - alpha/2 (r2 / r2(m) - 1)),
+// (exact when the coordinates are exact, e.g. n = 2^L; the neglected term is
+// ~ (alpha r2 rel err)^2 ~ 1e-26 otherwise) instead of a pow() per pair
+// (profiles/r02_direct_cfg2_ncu_full.json: 52 DFMA per pair before).
+template <int DIM>
+__global__ void __launch_bounds__(256) direct_frac_kernel(const __grid_constant__ DirectArgs a) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long my_pairs = 0;
+  if (t < a.ntargets) {
+    const Geom& g = a.g;
+    const int64_t tt = a.targets ? a.targets[t] : t;
+    int64_t ki[3] = {0, 0, 0};
+    unflatten<DIM>(g, tt, ki);
+    const int64_t ii = in_index<DIM>(g, ki);
+    const double h = g.h, inv_h = 1.0 / h;
+    double x[3];
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) x[j] = coord(ki[j], h);
+    const double delta = a.delta ? a.delta[ii] : a.delta0;
+    const double ci = a.coeff ? a.coeff[ii] : a.coeff0;
+    const double kap_i = a.kappa ? a.kappa[ii] : 1.0;
+    const bool collar = a.exterior == 1;
+    const double e = delta * inv_h, e2 = e * e;
+    const int64_t mlo = static_cast<int64_t>(ceil(e2 * (1.0 - tie_band_n(inv_h))));
+    const int64_t mhi = static_cast<int64_t>(floor(e2 * (1.0 + tie_band_n(inv_h))));
+    const double ui = a.u[ii];
+    const double ca = 0.5 * a.p.alpha;
+    // sum w (u_y - u_i), w = ci (kappa_i + kappa_y)/2 |r|^-alpha:  A = sum w0 (u_y - u_i),
+    // B = sum w0 kappa_y (u_y - u_i)  (w0 = |r|^-alpha), out = h^d ci (kappa_i A + B) / 2
+    double A = 0.0, Bk = 0.0;
+    auto isq = [](int64_t m) {
+      int64_t r = static_cast<int64_t>(sqrt(static_cast<double>(m)));
+      while (r * r > m) --r;
+      while ((r + 1) * (r + 1) <= m) ++r;
+      return r;
+    };
+    auto visit = [&](const int64_t* k, int64_t m) {
+      bool in_dom = true;
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) in_dom = in_dom && k[j] >= 0 && k[j] < g.n;
+      double r2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) {
+        const double d = __dsub_rn(coord(k[j], h), x[j]);
+        r2 = __dadd_rn(r2, __dmul_rn(d, d));
+      }
+      if (m >= mlo && !(__dsqrt_rn(r2) < delta)) return;   // tie band: the reference's predicate
+      const int64_t ti = DIM == 1 ? (k[0] > ki[0] ? k[0] - ki[0] : ki[0] - k[0]) : m;
+      const double2 wt = __ldg(a.wfrac + ti);
+      const double w0 = fma(-ca * fma(r2, wt.y, -1.0), wt.x, wt.x);
+      ++my_pairs;
+      const int64_t kk = in_dom ? in_index<DIM>(g, k) : 0;
+      const double du = (in_dom ? a.u[kk] : 0.0) - ui;   // difference form, as the reference
+      A = fma(w0, du, A);
+      if (a.kappa) Bk = fma(w0 * (in_dom ? a.kappa[kk] : kap_i), du, Bk);
+    };
+    const int64_t W = isq(mhi);
+    int64_t k[3] = {0, 0, 0};
+    auto lo_of = [&](int j, int64_t r) { const int64_t v = ki[j] - r; return collar ? v : (v < 0 ? 0 : v); };
+    auto hi_of = [&](int j, int64_t r) { const int64_t v = ki[j] + r; return collar ? v : (v > g.n - 1 ? g.n - 1 : v); };
+    if (DIM == 1) {
+      for (k[0] = lo_of(0, W); k[0] <= hi_of(0, W); ++k[0]) {
+        const int64_t d0 = k[0] - ki[0];
+        if (d0 == 0) continue;
+        visit(k, d0 * d0);
+      }
+    } else if (DIM == 2) {
+      for (k[0] = lo_of(0, W); k[0] <= hi_of(0, W); ++k[0]) {
+        const int64_t d0 = k[0] - ki[0], b = mhi - d0 * d0;
+        if (b < 0) continue;
+        const int64_t X = isq(b);
+        for (k[1] = lo_of(1, X); k[1] <= hi_of(1, X); ++k[1]) {
+          const int64_t d1 = k[1] - ki[1], m = d0 * d0 + d1 * d1;
+          if (m == 0) continue;
+          visit(k, m);
+        }
+      }
+    } else {
+      for (k[0] = lo_of(0, W); k[0] <= hi_of(0, W); ++k[0]) {
+        const int64_t d0 = k[0] - ki[0], b0 = mhi - d0 * d0;
+        if (b0 < 0) continue;
+        const int64_t Y = isq(b0);
+        for (k[1] = lo_of(1, Y); k[1] <= hi_of(1, Y); ++k[1]) {
+          const int64_t d1 = k[1] - ki[1], b1 = b0 - d1 * d1;
+          if (b1 < 0) continue;
+          const int64_t X = isq(b1);
+          for (k[2] = lo_of(2, X); k[2] <= hi_of(2, X); ++k[2]) {
+            const int64_t d2 = k[2] - ki[2], m = d0 * d0 + d1 * d1 + d2 * d2;
+            if (m == 0) continue;
+            visit(k, m);
+          }
+        }
+      }
+    }
+    const double acc = a.kappa ? 0.5 * ci * fma(kap_i, A, Bk) : ci * A;
+    a.out[t] = g.hd * acc;
+  }
+  if (a.pairs) {
+    my_pairs = warp_sum(my_pairs);
+    if ((threadIdx.x & 31) == 0 && my_pairs) atomicAdd(a.pairs, my_pairs);
+  }
+}
+
 template <int DIM>
 void launch_dim(int kind, const DirectArgs& a, cudaStream_t s) {
   const int threads = 256;
@@ -216,7 +333,10 @@ void launch_dim(int kind, const DirectArgs& a, cudaStream_t s) {
     case 0: direct_kernel<DIM, 0><<<blocks, threads, 0, s>>>(a); break;
     case 1: direct_kernel<DIM, 1><<<blocks, threads, 0, s>>>(a); break;
     case 2: direct_kernel<DIM, 2><<<blocks, threads, 0, s>>>(a); break;
-    case 3: direct_kernel<DIM, 3><<<blocks, threads, 0, s>>>(a); break;
+    case 3:
+      if (a.wfrac) direct_frac_kernel<DIM><<<blocks, threads, 0, s>>>(a);
+      else direct_kernel<DIM, 3><<<blocks, threads, 0, s>>>(a);
+      break;
     default: direct_kernel<DIM, 4><<<blocks, threads, 0, s>>>(a); break;
   }
 }
@@ -503,6 +623,29 @@ void launch_assemble(const Plan& P, double* A, int64_t N, cudaStream_t s) {
   }
 }
 
+// KIND 3 weight table (direct_frac_kernel): entry i = (|r_i|^-alpha, 1 / r_i^2)
+// at the lattice distance r_i = |d| h (1-D: i = |d|) or sqrt(i) h (2-D / 3-D:
+// i = |d|^2), r_i^2 in the reference's rounding of h^2 d^2. Plan-time, host.
+void direct_frac_setup(Plan& P) {
+  if (P.family != NLG_FRACTIONAL) return;
+  const int dim = P.geom.dim;
+  const double h = P.geom.h;
+  const double e = P.delta_max / h, e2 = e * e * (1.0 + tie_band(h));
+  const int64_t W = static_cast<int64_t>(std::floor(std::sqrt(e2))) + 2;
+  const int64_t len = dim == 1 ? W + 1 : static_cast<int64_t>(e2) + 2;
+  if (len > (int64_t{1} << 24)) return;   // keep the pow() kernel
+  std::vector<double2> tab(static_cast<size_t>(len));
+  tab[0] = make_double2(0.0, 0.0);
+  for (int64_t i = 1; i < len; ++i) {
+    const double d2 = dim == 1 ? static_cast<double>(i) * static_cast<double>(i) : static_cast<double>(i);
+    const double r2 = d2 * (h * h);
+    const long double r = std::sqrt(static_cast<long double>(d2)) * static_cast<long double>(h);
+    tab[i] = make_double2(static_cast<double>(std::pow(r, -static_cast<long double>(P.prof.alpha))), 1.0 / r2);
+  }
+  P.d_wfrac = upload_on(tab, P.stream);
+  P.wfrac_len = len;
+}
+
 int direct_kind(const Plan& P) {
   if (P.family == 5) return 4;
   if (P.family == 4) return 3;
@@ -529,6 +672,8 @@ void launch_direct(const Plan& P, const double* u, double* out, const int64_t* t
   a.ntargets = targets ? ntargets : P.n_out;
   a.out = out;
   a.pairs = pairs;
+  a.wfrac = P.d_wfrac;
+  a.wfrac_len = P.wfrac_len;
   const int kind = direct_kind(P);
   switch (P.geom.dim) {
     case 1: launch_dim<1>(kind, a, s); break;

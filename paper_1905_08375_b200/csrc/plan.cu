@@ -221,6 +221,7 @@ nlg_status nlg_plan_create(const nlg_desc* desc, nlg_plan** out) {
       NLG_CUDA(cudaMemcpyAsync(P.d_kappa, d.kappa, bytes_in, cudaMemcpyHostToDevice, P.stream));
     }
     NLG_CUDA(cudaMalloc(&P.d_pairs, sizeof(unsigned long long)));
+    direct_frac_setup(P);
 
     // fast method selection
     if (P.family == NLG_TRUNCATED && P.route == NLG_ROUTE_TRUNCATED && pr.npoly == 1) {
@@ -263,6 +264,7 @@ void nlg_plan_destroy(nlg_plan* plan) {
   cudaFree(P.d_out);
   cudaFree(P.d_pairs);
   cudaFree(P.d_targets);
+  cudaFree(P.d_wfrac);
   if (P.stream) cudaStreamDestroy(P.stream);
   if (P.h2d_stream) cudaStreamDestroy(P.h2d_stream);
   if (P.d2h_stream) cudaStreamDestroy(P.d2h_stream);

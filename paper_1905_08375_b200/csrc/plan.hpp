@@ -86,6 +86,10 @@ struct Plan {
   double* d_coeff = nullptr;
   double* d_kappa = nullptr;
 
+  // KIND 3 direct-sum weight table (direct.cu direct_frac_setup)
+  double2* d_wfrac = nullptr;
+  int64_t wfrac_len = 0;
+
   // staging for the host entry points
   double* d_u = nullptr;
   double* d_out = nullptr;
@@ -127,6 +131,7 @@ void stage_end(Plan& P, cudaStream_t s, int stage, cudaEvent_t ev, int nlaunch);
 void launch_direct(const Plan& P, const double* u, double* out, const int64_t* targets,
                    int64_t ntargets, unsigned long long* pairs, cudaStream_t s);
 int direct_kind(const Plan& P);
+void direct_frac_setup(Plan& P);
 void launch_transpose(const Plan& P, const double* v, double* out, cudaStream_t s);
 void launch_assemble(const Plan& P, double* A, int64_t N, cudaStream_t s);
 void spans_setup(Plan& P);
