@@ -251,67 +251,69 @@ __global__ void __launch_bounds__(256) direct_frac_kernel(const __grid_constant_
     // sum w (u_y - u_i), w = ci (kappa_i + kappa_y)/2 |r|^-alpha:  A = sum w0 (u_y - u_i),
     // B = sum w0 kappa_y (u_y - u_i)  (w0 = |r|^-alpha), out = h^d ci (kappa_i A + B) / 2
     double A = 0.0, Bk = 0.0;
+    // one row of the window along the last axis: k_last in [c0, c1], the other
+    // components fixed (their squared float distance r2o summed first, in the
+    // reference's dimension order, and their squared lattice distance mo)
+    auto row = [&](const int64_t* ko, double r2o, int64_t mo, bool dom_o, int64_t c0, int64_t c1) {
+      constexpr int L = DIM - 1;
+      int64_t base = 0;   // input index of k_last = 0 on this row
+      if (DIM > 1) {
+        int64_t rest = 0;
+#pragma unroll
+        for (int j = 1; j < L; ++j) rest = rest * g.n + ko[j];
+        base = DIM == 2 ? (ko[0] - g.in_begin) * g.stride0 : (ko[0] - g.in_begin) * g.stride0 + rest * g.n;
+      } else {
+        base = -g.in_begin;
+      }
+      for (int64_t kl = c0; kl <= c1; ++kl) {
+        const int64_t dl = kl - ki[L], m = mo + dl * dl;
+        if (m == 0) continue;
+        const double d = __dsub_rn(coord(kl, h), x[L]);
+        const double r2 = __dadd_rn(r2o, __dmul_rn(d, d));
+        if (m >= mlo && !(__dsqrt_rn(r2) < delta)) continue;   // tie band: the reference's predicate
+        const double2 wt = __ldg(a.wfrac + (DIM == 1 ? (dl < 0 ? -dl : dl) : m));
+        const double w0 = fma(-ca * fma(r2, wt.y, -1.0), wt.x, wt.x);
+        ++my_pairs;
+        const bool in_dom = dom_o && kl >= 0 && kl < g.n;
+        const double du = (in_dom ? a.u[base + kl] : 0.0) - ui;   // difference form, as the reference
+        A = fma(w0, du, A);
+        if (a.kappa) Bk = fma(w0 * (in_dom ? a.kappa[base + kl] : kap_i), du, Bk);
+      }
+    };
     auto isq = [](int64_t m) {
       int64_t r = static_cast<int64_t>(sqrt(static_cast<double>(m)));
       while (r * r > m) --r;
       while ((r + 1) * (r + 1) <= m) ++r;
       return r;
     };
-    auto visit = [&](const int64_t* k, int64_t m) {
-      bool in_dom = true;
-#pragma unroll
-      for (int j = 0; j < DIM; ++j) in_dom = in_dom && k[j] >= 0 && k[j] < g.n;
-      double r2 = 0.0;
-#pragma unroll
-      for (int j = 0; j < DIM; ++j) {
-        const double d = __dsub_rn(coord(k[j], h), x[j]);
-        r2 = __dadd_rn(r2, __dmul_rn(d, d));
-      }
-      if (m >= mlo && !(__dsqrt_rn(r2) < delta)) return;   // tie band: the reference's predicate
-      const int64_t ti = DIM == 1 ? (k[0] > ki[0] ? k[0] - ki[0] : ki[0] - k[0]) : m;
-      const double2 wt = __ldg(a.wfrac + ti);
-      const double w0 = fma(-ca * fma(r2, wt.y, -1.0), wt.x, wt.x);
-      ++my_pairs;
-      const int64_t kk = in_dom ? in_index<DIM>(g, k) : 0;
-      const double du = (in_dom ? a.u[kk] : 0.0) - ui;   // difference form, as the reference
-      A = fma(w0, du, A);
-      if (a.kappa) Bk = fma(w0 * (in_dom ? a.kappa[kk] : kap_i), du, Bk);
-    };
     const int64_t W = isq(mhi);
     int64_t k[3] = {0, 0, 0};
     auto lo_of = [&](int j, int64_t r) { const int64_t v = ki[j] - r; return collar ? v : (v < 0 ? 0 : v); };
     auto hi_of = [&](int j, int64_t r) { const int64_t v = ki[j] + r; return collar ? v : (v > g.n - 1 ? g.n - 1 : v); };
     if (DIM == 1) {
-      for (k[0] = lo_of(0, W); k[0] <= hi_of(0, W); ++k[0]) {
-        const int64_t d0 = k[0] - ki[0];
-        if (d0 == 0) continue;
-        visit(k, d0 * d0);
-      }
+      row(k, 0.0, 0, true, lo_of(0, W), hi_of(0, W));
     } else if (DIM == 2) {
       for (k[0] = lo_of(0, W); k[0] <= hi_of(0, W); ++k[0]) {
         const int64_t d0 = k[0] - ki[0], b = mhi - d0 * d0;
         if (b < 0) continue;
         const int64_t X = isq(b);
-        for (k[1] = lo_of(1, X); k[1] <= hi_of(1, X); ++k[1]) {
-          const int64_t d1 = k[1] - ki[1], m = d0 * d0 + d1 * d1;
-          if (m == 0) continue;
-          visit(k, m);
-        }
+        const double e0 = __dsub_rn(coord(k[0], h), x[0]);
+        row(k, __dmul_rn(e0, e0), d0 * d0, k[0] >= 0 && k[0] < g.n, lo_of(1, X), hi_of(1, X));
       }
     } else {
       for (k[0] = lo_of(0, W); k[0] <= hi_of(0, W); ++k[0]) {
         const int64_t d0 = k[0] - ki[0], b0 = mhi - d0 * d0;
         if (b0 < 0) continue;
         const int64_t Y = isq(b0);
+        const double e0 = __dsub_rn(coord(k[0], h), x[0]);
+        const double s0 = __dmul_rn(e0, e0);
         for (k[1] = lo_of(1, Y); k[1] <= hi_of(1, Y); ++k[1]) {
           const int64_t d1 = k[1] - ki[1], b1 = b0 - d1 * d1;
           if (b1 < 0) continue;
           const int64_t X = isq(b1);
-          for (k[2] = lo_of(2, X); k[2] <= hi_of(2, X); ++k[2]) {
-            const int64_t d2 = k[2] - ki[2], m = d0 * d0 + d1 * d1 + d2 * d2;
-            if (m == 0) continue;
-            visit(k, m);
-          }
+          const double e1 = __dsub_rn(coord(k[1], h), x[1]);
+          row(k, __dadd_rn(s0, __dmul_rn(e1, e1)), d0 * d0 + d1 * d1,
+              k[0] >= 0 && k[0] < g.n && k[1] >= 0 && k[1] < g.n, lo_of(2, X), hi_of(2, X));
         }
       }
     }
