@@ -57,6 +57,8 @@ struct BoxFft {
   int cols = 4;                                     // columns per CTA of the strided passes (NLG_F3_COLS)
   bool tma = false;                                 // PB / PD through bulk tensor copies (NLG_F3_TMA)
   int tma_br = 0;                                   // rows per tensor box
+  bool pers = false;                                // PB / PD persistent double-buffered TMA passes (NLG_F3_PERS)
+  int pers_ctas = 2;                                // CTAs per SM of the persistent passes
   CUtensorMap pb_in{}, pb_out{}, pd_in{}, pd_out{};
   int64_t n = 0, n_in = 0, o0 = 0, rows_out = 0;   // z: input planes, first output plane, output planes
   double2* z = nullptr;                             // [n_in][ly][lx]: PA / PB output, PC input
@@ -247,6 +249,79 @@ __global__ void __launch_bounds__(cols_threads3<L, 4>(), 2)
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
+}
+
+// PB / PD, persistent and double buffered: a CTA loops over (column group,
+// plane) tiles; the NEXT tile's bulk tensor loads are in flight in the second
+// shared-memory buffer while the current tile is transformed, and finished
+// tiles leave by bulk tensor stores (the buffer is reloaded only after the
+// store has read it: cp.async.bulk.wait_group.read). One elected thread issues
+// all copies; the transform is the same in-place Stockham FFT as f3_cols_tma.
+template <int L>
+__global__ void __launch_bounds__(cols_threads3<L, 4>(), 2)
+    f3_cols_pers(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+                 const __grid_constant__ F3Args a, int br, int planes) {
+  constexpr int C = 4, T = cols_threads3<L, C>();
+  constexpr unsigned kTile = static_cast<unsigned>(L * C * sizeof(double2));
+  extern __shared__ __align__(128) double2 fsm3[];           // [2][L * C]
+  __shared__ __align__(8) unsigned long long mbar[2];
+  const int tid = threadIdx.x;
+  const int ngx = a.lx / C;
+  const int ntile = ngx * planes;
+  const unsigned mb0 = smem_u32(mbar), s0 = smem_u32(fsm3);
+  auto issue_load = [&](int t, int buf) {
+    const int cx = (t % ngx) * 2 * C, pz = static_cast<int>(a.p0) + t / ngx;
+    const unsigned mb = mb0 + 8u * buf, dst = s0 + kTile * buf;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(kTile) : "memory");
+    for (int r0 = 0; r0 < L; r0 += br)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+              dst + static_cast<unsigned>(r0 * C * sizeof(double2))),
+          "l"(&tin), "r"(cx), "r"(r0), "r"(pz), "r"(mb)
+          : "memory");
+  };
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (static_cast<int>(blockIdx.x) < ntile) issue_load(blockIdx.x, 0);
+  }
+  __syncthreads();
+  int it = 0;
+  for (int t = blockIdx.x; t < ntile; t += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int tn = t + gridDim.x;
+    if (tid == 0 && tn < ntile) {
+      // the other buffer's store (tile it - 1) must have been read out first
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      issue_load(tn, buf ^ 1);
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n\t}" ::"r"(
+            mb0 + 8u * buf),
+        "r"(static_cast<unsigned>((it >> 1) & 1))
+        : "memory");
+    double2* tile = fsm3 + buf * L * C;
+    auto ld = [&](int e, int c) { return tile[e * C + c]; };
+    auto st = [&](int base, int stride, int c, auto& v) {
+      constexpr int R = sizeof(v) / sizeof(v[0]);
+#pragma unroll
+      for (int q = 0; q < R; ++q) tile[(base + q * stride) * C + c] = v[q];
+    };
+    stockham::fs_fft<false, L, 1, L, C, T, false, true>(tile, a.twy, tid, ld, st);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy writes -> the bulk store
+    __syncthreads();
+    if (tid == 0) {
+      const int cx = (t % ngx) * 2 * C, pz = static_cast<int>(a.p0) + t / ngx;
+      for (int r0 = 0; r0 < L; r0 += br)
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(&tout),
+                     "r"(cx), "r"(r0), "r"(pz), "r"(s0 + kTile * buf + static_cast<unsigned>(r0 * C * sizeof(double2)))
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // PC: the z direction is not transformed. After FFT_x FFT_y the operator is,
@@ -859,6 +934,8 @@ template <int L>
 void f3_attr(int rf) {
   f3_attr_c<L, 8>(rf);
   f3_attr_c<L, 4>(rf);
+  NLG_CUDA(cudaFuncSetAttribute(f3_cols_pers<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(2 * sizeof(double2) * L * 4)));
   NLG_CUDA(cudaFuncSetAttribute(f3_cols_tma<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sizeof(double2) * L * 4)));
 }
@@ -883,6 +960,16 @@ void launch_cols_c(const F3Args& a, bool pd, int64_t planes, cudaStream_t s) {
   const dim3 grid(static_cast<unsigned>(a.lx / C), static_cast<unsigned>(planes));
   if (pd) f3_cols<L, true, C><<<grid, cols_threads3<L, C>(), cols_smem3<L, C>(), s>>>(a);
   else f3_cols<L, false, C><<<grid, cols_threads3<L, C>(), cols_smem3<L, C>(), s>>>(a);
+}
+template <int L>
+void launch_cols_pers(const BoxFft& B, const F3Args& a, bool pd, int64_t planes, cudaStream_t s) {
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t ntile = static_cast<int64_t>(a.lx / 4) * planes;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ntile, static_cast<int64_t>(B.pers_ctas) * nsm));
+  const size_t sb = 2 * sizeof(double2) * L * 4;
+  if (pd) f3_cols_pers<L><<<grid, cols_threads3<L, 4>(), sb, s>>>(B.pd_in, B.pd_out, a, B.tma_br, static_cast<int>(planes));
+  else f3_cols_pers<L><<<grid, cols_threads3<L, 4>(), sb, s>>>(B.pb_in, B.pb_out, a, B.tma_br, static_cast<int>(planes));
 }
 template <int L>
 void launch_cols_tma(const BoxFft& B, const F3Args& a, bool pd, int64_t planes, cudaStream_t s) {
@@ -1108,7 +1195,10 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   NLG_CUDA(cudaMalloc(&B->z2, sizeof(double2) * static_cast<size_t>(n_in) * lx * lx));
   {
     const char* te = std::getenv("NLG_F3_TMA");
-    if (te && std::atoi(te) == 1) {
+    const char* pe = std::getenv("NLG_F3_PERS");
+    const bool want_pers = pe && std::atoi(pe) >= 1;
+    if (const char* pc = std::getenv("NLG_F3_PERS_CTAS")) B->pers_ctas = std::max(1, std::atoi(pc));
+    if ((te && std::atoi(te) == 1) || want_pers) {
       int br = 1;
       for (int d = 1; d <= 256 && d <= lx; ++d)
         if (lx % d == 0) br = d;
@@ -1118,6 +1208,8 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
                encode_cols_map(&B->pb_out, B->z, lx, lx, lx, n_in, br) &&
                encode_cols_map(&B->pd_in, zo, lx, lx, lx, B->rows_out, br) &&
                encode_cols_map(&B->pd_out, zo, lx, lx, n, B->rows_out, br);
+      B->pers = B->tma && want_pers;
+      B->tma = B->tma && te && std::atoi(te) == 1;
     }
   }
   const double scale = 1.0 / (static_cast<double>(lx) * lx);
@@ -1191,7 +1283,7 @@ void boxfft_in(Plan& P, BoxFft& B, const double* u, int64_t p0, int64_t p1, cuda
   stage_end(P, s, kStBoxPA, ev, 1);
   stage_begin(P, s, kStBoxPB, &ev);
 #define NLG_F3_CASE(N) \
-  if (lx == N) { if (B.tma) launch_cols_tma<N>(B, a, false, p1 - p0, s); else launch_cols<N>(a, B.cols, false, p1 - p0, s); }
+  if (lx == N) { if (B.pers) launch_cols_pers<N>(B, a, false, p1 - p0, s); else if (B.tma) launch_cols_tma<N>(B, a, false, p1 - p0, s); else launch_cols<N>(a, B.cols, false, p1 - p0, s); }
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
   stage_end(P, s, kStBoxPB, ev, 1);
@@ -1212,7 +1304,7 @@ void boxfft_out(Plan& P, BoxFft& B, const double* u, const double* scale, double
   stage_end(P, s, kStBoxPC, ev, 1);
   stage_begin(P, s, kStBoxPD, &ev);
 #define NLG_F3_CASE(N) \
-  if (lx == N) { if (B.tma) launch_cols_tma<N>(B, a, true, q1 - q0, s); else launch_cols<N>(a, B.cols, true, q1 - q0, s); }
+  if (lx == N) { if (B.pers) launch_cols_pers<N>(B, a, true, q1 - q0, s); else if (B.tma) launch_cols_tma<N>(B, a, true, q1 - q0, s); else launch_cols<N>(a, B.cols, true, q1 - q0, s); }
   NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
   stage_end(P, s, kStBoxPD, ev, 1);

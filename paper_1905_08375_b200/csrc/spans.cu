@@ -90,39 +90,61 @@ __global__ void __launch_bounds__(kScanThreads) scan_lookback(const double* __re
     }
     __syncthreads();
   }
-  if (tid == 0) {
+  if (tid < 32) {   // warp 0: publish, then look back 32 predecessors at a time
+    const int lane = tid;
     const dd agg{sh[kScanThreads - 1], sl[kScanThreads - 1]};
     dd off{0.0, 0.0};
     if (seg == 0) {
-      st.inc[tile] = make_double2(agg.hi, agg.lo);
-      publish(st.flag + tile, epoch << 2 | 2u);
-    } else {
-      st.agg[tile] = make_double2(agg.hi, agg.lo);
-      publish(st.flag + tile, epoch << 2 | 1u);
-      for (int64_t p = tile - 1;; --p) {   // look back within the row
-        unsigned f;
-        do {
-          f = *reinterpret_cast<volatile unsigned*>(st.flag + p);
-        } while ((f >> 2) != epoch);
-        __threadfence();
-        if ((f & 3u) == 2u) {
-          const double2 w = __ldcg(st.inc + p);   // L2 (coherent), not a stale L1 line
-          off = dd_add(off, {w.x, w.y});
-          break;
-        }
-        const double2 w = __ldcg(st.agg + p);
-        off = dd_add(off, {w.x, w.y});
+      if (lane == 0) {
+        st.inc[tile] = make_double2(agg.hi, agg.lo);
+        publish(st.flag + tile, epoch << 2 | 2u);
       }
-      const dd inc = dd_add(off, agg);
-      st.inc[tile] = make_double2(inc.hi, inc.lo);
-      publish(st.flag + tile, epoch << 2 | 2u);
+    } else {
+      if (lane == 0) {
+        st.agg[tile] = make_double2(agg.hi, agg.lo);
+        publish(st.flag + tile, epoch << 2 | 1u);
+      }
+      const int64_t first = tile - seg;                      // first tile of this row
+      for (int64_t top = tile - 1;; top -= 32) {
+        const int64_t p = top - lane;                        // lane l inspects tile top - l
+        const bool valid = p >= first;
+        unsigned f = 0;
+        if (valid) {
+          do {
+            f = *reinterpret_cast<volatile unsigned*>(st.flag + p);
+          } while ((f >> 2) != epoch);
+        }
+        __threadfence();
+        const unsigned incl = __ballot_sync(0xffffffffu, valid && (f & 3u) == 2u);
+        const int stop = incl ? __ffs(incl) - 1 : 32;        // nearest predecessor with an inclusive prefix
+        dd v{0.0, 0.0};
+        if (valid && lane <= stop) {
+          const double2 w = lane == stop ? __ldcg(st.inc + p) : __ldcg(st.agg + p);
+          v = {w.x, w.y};
+        }
+        // warp sum in double-double (fixed tree: deterministic)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const dd u2{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
+          v = dd_add(v, u2);
+        }
+        off = dd_add(off, v);
+        if (incl || top - 32 < first) break;
+      }
+      if (lane == 0) {
+        const dd inc = dd_add(off, agg);
+        st.inc[tile] = make_double2(inc.hi, inc.lo);
+        publish(st.flag + tile, epoch << 2 | 2u);
+      }
     }
-    if (seg == rg.nseg - 1) {
-      const dd tot = dd_add(off, agg);
-      tot_hi[row] = tot.hi;
-      tot_lo[row] = tot.lo;
+    if (lane == 0) {
+      if (seg == rg.nseg - 1) {
+        const dd tot = dd_add(off, agg);
+        tot_hi[row] = tot.hi;
+        tot_lo[row] = tot.lo;
+      }
+      s_off = off;
     }
-    s_off = off;
   }
   __syncthreads();
   dd excl = dd_add(s_off, tid ? dd{sh[tid - 1], sl[tid - 1]} : dd{0.0, 0.0});
