@@ -170,6 +170,80 @@ __global__ void __launch_bounds__(rows_threads<L, INV && !AB>()) f3_rows(const _
   }
 }
 
+// PA with several rows per CTA (RPC): the u and kappa rows of row r + 1
+// arrive by 1-D bulk copies (cp.async.bulk, one elected thread, mbarrier
+// completion) into a second staging buffer while row r is transformed, so the
+// global-load latency that stalled the one-row CTAs (ncu: long-scoreboard
+// stalls on the u * kappa products, 63% of the samples,
+// profiles/r02_cfg4_ncu_full.json) overlaps the shared-memory stages. Same
+// arithmetic as f3_rows. Rows are n contiguous doubles (n * 8 a multiple of 16).
+#ifndef NLG_PA_RPC
+#define NLG_PA_RPC 4
+#endif
+template <int L, bool KW>
+__global__ void __launch_bounds__(rows_threads<L, false>(), 5) f3_rows_fwd_multi(const __grid_constant__ F3Args a,
+                                                                              int64_t rows) {
+  constexpr int T = rows_threads<L, false>();
+  __shared__ double2 sm[L + L / 8];
+  extern __shared__ __align__(128) double stg[];               // [2][KW ? 2 : 1][n]
+  __shared__ __align__(8) unsigned long long mbar[2];
+  const int tid = threadIdx.x;
+  const int n = static_cast<int>(a.n);
+  const int F = KW ? 2 : 1;
+  const unsigned rb = static_cast<unsigned>(n * sizeof(double));
+  const unsigned mb0 = static_cast<unsigned>(__cvta_generic_to_shared(mbar));
+  const unsigned s0 = static_cast<unsigned>(__cvta_generic_to_shared(stg));
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * NLG_PA_RPC;
+  const int64_t r1 = min(r0 + NLG_PA_RPC, rows);
+  auto issue = [&](int64_t r, int buf) {
+    const int64_t zr = a.p0 + r / a.n, y = r % a.n;
+    const int64_t src = (zr * a.n + y) * a.n;
+    const unsigned mb = mb0 + 8u * buf, dst = s0 + static_cast<unsigned>(buf * F) * rb;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(rb * F) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(a.u + src), "r"(rb), "r"(mb)
+                 : "memory");
+    if (KW)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       dst + rb),
+                   "l"(a.kappa + src), "r"(rb), "r"(mb)
+                   : "memory");
+  };
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (r0 < r1) issue(r0, 0);
+  }
+  __syncthreads();
+  int it = 0;
+  for (int64_t r = r0; r < r1; ++r, ++it) {
+    const int buf = it & 1;
+    if (tid == 0 && r + 1 < r1) issue(r + 1, buf ^ 1);          // its buffer was last read by row r - 1 (barrier below)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n\t}" ::"r"(
+            mb0 + 8u * buf),
+        "r"(static_cast<unsigned>((it >> 1) & 1))
+        : "memory");
+    const double* su = stg + static_cast<size_t>(buf * F) * n;
+    const int64_t zr = a.p0 + r / a.n, y = r % a.n;
+    double2* zrow = a.z + (zr * a.ly + y) * a.lx;
+    auto ld = [&](int e, int) {
+      if (e >= n) return make_double2(0.0, 0.0);
+      const double v = su[e];
+      return make_double2(v, KW ? v * su[n + e] : 0.0);
+    };
+    auto st = [&](int base, int stride, int, auto& v) {
+      constexpr int R = sizeof(v) / sizeof(v[0]);
+#pragma unroll
+      for (int q = 0; q < R; ++q) zrow[base + q * stride] = v[q];
+    };
+    fs_fft<false, L, 1, L, 1, T, true>(sm, a.twx, tid, ld, st);
+    __syncthreads();   // this row's staging and FFT buffers are free for the next issue / row
+  }
+}
+
 // PB / PD: C adjacent kx columns along y in one plane. PB reads y < n
 // (zero padding above) and writes every ky; PD reads every ky and writes y < n.
 template <int L, bool PD, int C>
@@ -813,36 +887,33 @@ __global__ void __launch_bounds__(kTieTX * kTieTY, 3)
   __syncthreads();
   auto wait_plane = [&](int i) { mbar_wait(mb0 + 8u * (i % NR), static_cast<unsigned>((i / NR) & 1)); };
   for (int i = 0; i < NS - 1; ++i) wait_plane(i);
-  const uint32_t* mask = static_cast<const uint32_t*>(a.mask);
   const int tgt = y * n + x;
   const int sbase = (threadIdx.y + R) * W + threadIdx.x + R;
+  // running pointers to the target plane zt's operands (advanced by q planes a
+  // step: no per-step 64-bit index arithmetic); dead lanes point at target 0
+  const int64_t step_n = static_cast<int64_t>(q) * nn, step_z = static_cast<int64_t>(q) * a.zly * a.zlx;
+  const int64_t t0i = live ? tgt : 0;
+  const int64_t oi0 = (static_cast<int64_t>(zf) - g.row_begin) * nn + t0i;
+  const int64_t ii0 = (static_cast<int64_t>(zf) - g.in_begin) * nn + t0i;
+  const uint32_t* pm = static_cast<const uint32_t*>(a.mask) + oi0;
+  const double2* pab = a.zab + ((static_cast<int64_t>(zf) - g.in_begin) * a.zly + (live ? y : 0)) * a.zlx + (live ? x : 0);
+  const double* pd = a.diag + oi0;
+  const double* ps = a.scale ? a.scale + oi0 : nullptr;
+  double* po = a.out + oi0;
+  const double* pu = a.u + ii0;
+  const double* pkp = KW ? a.kappa + ii0 : nullptr;
+  int64_t axoff[AX.n > 0 ? AX.n : 1];
+#pragma unroll
+  for (int k = 0; k < AX.n; ++k) axoff[k] = (static_cast<int64_t>(AX.t0[k]) * n + AX.t1[k]) * n + AX.t2[k];
   uint32_t mn = 0;
   double2 abn = make_double2(0.0, 0.0);
   double edn = 0.0, esn = 0.0;
-  auto fetch = [&](int z) {
-    mn = 0;
-    abn = make_double2(0.0, 0.0);
-    edn = esn = 0.0;
-    if (live && z < ze) {
-      const int64_t oi = (static_cast<int64_t>(z) - g.row_begin) * nn + tgt;
-      const int64_t zi = static_cast<int64_t>(z) - g.in_begin;
-      mn = __ldg(mask + oi);
-      abn = a.zab[(zi * a.zly + y) * a.zlx + x];
-      edn = __ldg(a.diag + oi);
-      esn = a.scale ? __ldg(a.scale + oi) : a.scale0;
-    }
-  };
-  auto prefetch = [&](int z) {   // the operands of a later step into L2
-    if (live && z < ze) {
-      const int64_t oi = (static_cast<int64_t>(z) - g.row_begin) * nn + tgt;
-      const int64_t zi = static_cast<int64_t>(z) - g.in_begin;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.zab + (zi * a.zly + y) * a.zlx + x));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.diag + oi));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(mask + oi));
-    }
-  };
-  fetch(zf);
-  prefetch(zf + q);
+  if (live) {   // plane zf
+    mn = __ldg(pm);
+    abn = pab[0];
+    edn = __ldg(pd);
+    esn = ps ? __ldg(ps) : a.scale0;
+  }
   for (int j = 0; j < J; ++j) {
     const int zt = zf + j * q;
     const uint32_t m = mn;
@@ -851,26 +922,33 @@ __global__ void __launch_bounds__(kTieTX * kTieTY, 3)
     __syncthreads();                                                  // step j - 1's reads done: slot of plane j - 1 free
     if (tid == 0 && j + NS + 1 < NP) issue(j + NS + 1);               // two planes ahead
     wait_plane(j + NS - 1);                                           // the newest plane this step reads
-    fetch(zt + q);
-    prefetch(zt + 2 * q);
-    const int64_t oi = (static_cast<int64_t>(zt) - g.row_begin) * nn + tgt;
+    const bool more = live && zt + q < ze;
+    mn = more ? __ldg(pm + step_n) : 0u;                              // the next step's operands, one step ahead
+    abn = more ? pab[step_z] : make_double2(0.0, 0.0);
+    edn = more ? __ldg(pd + step_n) : 0.0;
+    esn = more ? (ps ? __ldg(ps + step_n) : a.scale0) : 0.0;
+    if (live && zt + 2 * q < ze) {                                    // and the one after that into L2
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pab + 2 * step_z));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pd + 2 * step_n));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pm + 2 * step_n));
+    }
+    // ties no lane of the warp includes are skipped (~15 of 24 ring ties needed
+    // per warp at 768^3; the axis ties enter ~2% of the targets)
+    const unsigned wm = __reduce_or_sync(0xffffffffu, m);
     // axis ties (outside the window): the few included sources from global memory
     double xu[AX.n > 0 ? AX.n : 1], xk[AX.n > 0 ? AX.n : 1];
-    {
-      const int64_t ii = (static_cast<int64_t>(zt) - g.in_begin) * nn + tgt;
 #pragma unroll
-      for (int k = 0; k < AX.n; ++k) {
+    for (int k = 0; k < AX.n; ++k) {
+      xu[k] = xk[k] = 0.0;
+      if (wm & (1u << AX.bit[k])) {
         const bool on = (m >> AX.bit[k]) & 1u;
-        const int64_t sidx = ii + (static_cast<int64_t>(AX.t0[k]) * n + AX.t1[k]) * n + AX.t2[k];
-        xu[k] = on ? __ldg(a.u + sidx) : 0.0;
-        xk[k] = on && KW ? __ldg(a.kappa + sidx) : 0.0;
+        xu[k] = on ? __ldg(pu + axoff[k]) : 0.0;
+        xk[k] = on && KW ? __ldg(pkp + axoff[k]) : 0.0;
       }
     }
     const double* slot[NS];
 #pragma unroll
     for (int r = 0; r < NS; ++r) slot[r] = rsm + ((j + r) % NR) * SLOT + sbase;
-    // ties no lane of the warp includes are skipped (~15 of 24 needed per warp)
-    const unsigned wm = __reduce_or_sync(0xffffffffu, m);
     double A = 0.0, B = 0.0, A1 = 0.0, B1 = 0.0;
 #pragma unroll
     for (int k = 0; k < TS.n; ++k) {
@@ -896,8 +974,15 @@ __global__ void __launch_bounds__(kTieTX * kTieTY, 3)
       const double* own = slot[R / q];
       const double uA = fma(a.w, A, ab.x);
       const double X = KW ? fma(own[SB], uA, fma(a.w, B, ab.y)) : uA;
-      a.out[oi] = es * (X - own[0] * ed);
+      *po = es * (X - own[0] * ed);
     }
+    pm += step_n;
+    pab += step_z;
+    pd += step_n;
+    if (ps) ps += step_n;
+    po += step_n;
+    pu += step_n;
+    if (KW) pkp += step_n;
   }
 }
 
@@ -945,8 +1030,18 @@ void launch_rows(const F3Args& a, bool inv, int64_t rows, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>(rows);
   constexpr int TF = rows_threads<L, false>(), TI = rows_threads<L, true>();
   if (!inv) {
-    if (a.kappa) f3_rows<L, false, true><<<grid, TF, 0, s>>>(a);
-    else f3_rows<L, false, false><<<grid, TF, 0, s>>>(a);
+    // NLG_PA_MULTI=1: bulk-copy-fed multi-row PA (measured 4.5 vs 3.7 ms at 768^3: off)
+    static const bool multi = [] { const char* e = std::getenv("NLG_PA_MULTI"); return e && std::atoi(e) == 1; }();
+    if (NLG_PA_RPC > 1 && multi && (a.n * 8) % 16 == 0) {
+      const unsigned g2 = static_cast<unsigned>((rows + NLG_PA_RPC - 1) / NLG_PA_RPC);
+      const size_t sb = sizeof(double) * 2 * (a.kappa ? 2 : 1) * a.n;
+      if (a.kappa) f3_rows_fwd_multi<L, true><<<g2, TF, sb, s>>>(a, rows);
+      else f3_rows_fwd_multi<L, false><<<g2, TF, sb, s>>>(a, rows);
+    } else if (a.kappa) {
+      f3_rows<L, false, true><<<grid, TF, 0, s>>>(a);
+    } else {
+      f3_rows<L, false, false><<<grid, TF, 0, s>>>(a);
+    }
   } else if (a.ab) {
     f3_rows<L, true, false, true><<<grid, TF, 0, s>>>(a);
   } else {
