@@ -636,43 +636,24 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
     const bool mirror = DIM == 3 && KIND == 0 && az > 0;
     const bool zmin = mirror && gzm >= 0 && gzm < n && gzm >= g.in_begin && gzm < g.in_end;
     if (KW || mirror) {
-      // the thread's (row, column) slots in batches: all mirror-plane loads of a
-      // batch are issued before any shared-memory update (one global latency per
-      // batch instead of one per slot: the loads could not move past the
-      // generic-pointer smem stores)
-      constexpr int kB = 8;
-      const int ncw = (TWc + 31) / 32;
-      const int nrow = (TH - static_cast<int>(threadIdx.y) + kWY - 1) / kWY;
-      const int nitem = nrow * ncw;
-      for (int i0 = 0; i0 < nitem; i0 += kB) {
-        double um[kB], km[kB];
-#pragma unroll
-        for (int b = 0; b < kB; ++b) {
-          um[b] = 0.0;
-          km[b] = 0.0;
-          const int it = i0 + b;
-          const int ty = threadIdx.y + (it / ncw) * kWY, c = (it % ncw) * 32 + cl;
-          const int64_t gy = y0 - H + ty, gx = x0 - H + c;
-          if (it < nitem && c < TWc && zmin && gy >= 0 && gy < n && gx >= 0 && gx < n) {
-            const int64_t k = ((gzm - g.in_begin) * n + gy) * n + gx;
-            um[b] = __ldg(a.u + k);
-            if (KW) km[b] = __ldg(a.kappa + k);
+      for (int ty = threadIdx.y; ty < TH; ty += kWY) {
+        const int64_t gy = y0 - H + ty;
+        const bool yin = zmin && gy >= 0 && gy < n;
+        const int64_t rowm = ((gzm - g.in_begin) * n + gy) * n;
+        double2* trow = tile + static_cast<size_t>(ty) * RS;
+        for (int c0 = 0; c0 < TWc; c0 += 32) {
+          const int c = c0 + cl;
+          if (c >= TWc) continue;
+          double2* dst = trow + (c & 3) * Q + (c >> 2);
+          double2 v = *dst;
+          if (KW) v.y = v.y * v.x;
+          const int64_t gx = x0 - H + c;
+          if (yin && gx >= 0 && gx < n) {
+            const double um = __ldg(a.u + rowm + gx);
+            v.x = v.x + um;
+            if (KW) v.y = fma(__ldg(a.kappa + rowm + gx), um, v.y);
           }
-        }
-#pragma unroll
-        for (int b = 0; b < kB; ++b) {
-          const int it = i0 + b;
-          const int ty = threadIdx.y + (it / ncw) * kWY, c = (it % ncw) * 32 + cl;
-          if (it < nitem && c < TWc) {
-            double2* dst = tile + static_cast<size_t>(ty) * RS + (c & 3) * Q + (c >> 2);
-            double2 v = *dst;
-            if (KW) v.y = v.y * v.x;
-            if (mirror) {
-              v.x = v.x + um[b];
-              if (KW) v.y = fma(km[b], um[b], v.y);
-            }
-            *dst = v;
-          }
+          *dst = v;
         }
       }
     }
