@@ -75,3 +75,15 @@ def test_stage_slots_match_header():
     src = open(os.path.join(ROOT, "include", "nlgpu.h")).read()
     n = int(re.search(r"#define NLG_NUM_STAGES (\d+)", src).group(1))
     assert len(_capi.STAGES) == n
+
+
+def test_group_argument_errors(capi):
+    """nlg_group_create validates its arguments before touching a device
+    (std::invalid_argument semantics): no devices, a sharded descriptor, and
+    slabs thinner than the halo (which would leave neighbours' halos short)."""
+    from paper_1905_08375_b200 import nonloc as N
+    A = N.A
+    with pytest.raises(ValueError):
+        N.Group([], dim=3, n=32, family=A.FRACTIONAL, alpha=3.5, delta0=6 / 32)
+    with pytest.raises(ValueError, match="slab thinner than the halo"):
+        N.Group([0] * 8, dim=3, n=32, family=A.FRACTIONAL, alpha=3.5, delta0=6 / 32)
