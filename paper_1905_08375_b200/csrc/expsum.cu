@@ -606,16 +606,50 @@ __global__ void __launch_bounds__(32 * kTailWarps, MAIN ? kTailMainCtas : 5) es_
   }
 }
 
+// L2 residency of the main walk's RED target (facc: fields x n_out doubles,
+// 64 MB at cfg1): the walk's REDs arrive from both scan directions, two ends
+// each, while u / kappa / tinfo / the chunk carries stream through L2; with a
+// persisting access-policy window on facc the REDs stop re-reading evicted
+// lines from DRAM. Plan-time knob NLG_L2_PERSIST (bytes of the device-wide
+// persisting set-aside; 0 = off).
+struct L2Window {
+  void* base = nullptr;
+  size_t bytes = 0;
+};
+
+template <typename K>
+void launch_with_window(K kernel, unsigned grid, unsigned block, cudaStream_t s, const L2Window& w, const PassPair& pp) {
+  if (!w.base || !w.bytes) {
+    kernel<<<grid, block, 0, s>>>(pp);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[0].val.accessPolicyWindow.base_ptr = w.base;
+  at[0].val.accessPolicyWindow.num_bytes = w.bytes;
+  at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+  at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  NLG_CUDA(cudaLaunchKernelEx(&cfg, kernel, pp));
+}
+
 template <int NF, bool MAIN>
-void launch_tail_t(int M, PassPair pp, cudaStream_t s) {
+void launch_tail_t(int M, PassPair pp, cudaStream_t s, const L2Window& w) {
   constexpr int kG = kTailWarps * (MAIN ? NF : 1) / NF;
   pp.split = (pp.d[0].nchunk + kG - 1) / kG;
   const unsigned grid = static_cast<unsigned>(pp.split + (pp.d[1].nchunk + kG - 1) / kG);
-  if (M <= 8) es_tail_walk<NF, MAIN, 8><<<grid, 32 * kTailWarps, 0, s>>>(pp);
-  else if (M <= 10) es_tail_walk<NF, MAIN, 10><<<grid, 32 * kTailWarps, 0, s>>>(pp);
-  else if (M <= 12) es_tail_walk<NF, MAIN, 12><<<grid, 32 * kTailWarps, 0, s>>>(pp);
-  else if (M <= 14) es_tail_walk<NF, MAIN, 14><<<grid, 32 * kTailWarps, 0, s>>>(pp);
-  else es_tail_walk<NF, MAIN, 16><<<grid, 32 * kTailWarps, 0, s>>>(pp);
+  const unsigned blk = 32 * kTailWarps;
+  if (M <= 8) launch_with_window(es_tail_walk<NF, MAIN, 8>, grid, blk, s, w, pp);
+  else if (M <= 10) launch_with_window(es_tail_walk<NF, MAIN, 10>, grid, blk, s, w, pp);
+  else if (M <= 12) launch_with_window(es_tail_walk<NF, MAIN, 12>, grid, blk, s, w, pp);
+  else if (M <= 14) launch_with_window(es_tail_walk<NF, MAIN, 14>, grid, blk, s, w, pp);
+  else launch_with_window(es_tail_walk<NF, MAIN, 16>, grid, blk, s, w, pp);
 }
 
 // Segment carries by a three-level scan (all fully parallel except a short
@@ -973,6 +1007,7 @@ struct ExpSumState {
   double *cagg = nullptr, *gchunk = nullptr;
   size_t astride = 0, cstride = 0;   // per-direction regions (FFT mode)
   TailTab tt{};                      // tail-walk term constants (FFT mode)
+  L2Window l2w{};                    // persisting L2 window on facc for the main walk (NLG_L2_PERSIST)
   int64_t nsegR = 0, nsegL = 0, o0R = 0, o0L = 0;
   double* kappa_dev = nullptr;
 };
@@ -1190,6 +1225,19 @@ void expsum_setup_impl(Plan& P, const nlg_desc& d) {
   NLG_CUDA(cudaMalloc(&S->cagg, sizeof(double) * cvals * (S->fft ? 2 : 1)));
   NLG_CUDA(cudaMalloc(&S->gchunk, sizeof(double) * cvals * (S->fft ? 2 : 1)));
   NLG_CUDA(cudaMalloc(&S->facc, sizeof(double) * S->fields * n_out));
+  if (const char* pe = std::getenv("NLG_L2_PERSIST")) {
+    // device-wide persisting set-aside (bytes), then the main walk's window on facc
+    const size_t want = static_cast<size_t>(std::atoll(pe));
+    int maxp = 0, maxw = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, P.device);
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, P.device);
+    const size_t setaside = std::min(want, static_cast<size_t>(maxp));
+    if (setaside > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside) == cudaSuccess) {
+      S->l2w.base = S->facc;
+      S->l2w.bytes = std::min({sizeof(double) * S->fields * n_out, static_cast<size_t>(maxw), setaside});
+    }
+    cudaGetLastError();
+  }
   NLG_CUDA(cudaMalloc(&S->diag, sizeof(double) * n_out));
   // exterior (zero collar) part of diag, exact: sum_{d > edge distance} w_d,
   // times (kappa_i + kappa_i) when kappa-weighted (kappa_y := kappa_x outside)
@@ -1248,13 +1296,13 @@ void expsum_free(Plan& P) {
 }
 
 namespace {
-void launch_tail(int nf, bool main, int M, const PassPair& pp, cudaStream_t s) {
+void launch_tail(int nf, bool main, int M, const PassPair& pp, cudaStream_t s, const L2Window& w = L2Window{}) {
   if (nf == 2) {
-    if (main) launch_tail_t<2, true>(M, pp, s);
-    else launch_tail_t<2, false>(M, pp, s);
+    if (main) launch_tail_t<2, true>(M, pp, s, w);
+    else launch_tail_t<2, false>(M, pp, s, L2Window{});
   } else {
-    if (main) launch_tail_t<1, true>(M, pp, s);
-    else launch_tail_t<1, false>(M, pp, s);
+    if (main) launch_tail_t<1, true>(M, pp, s, w);
+    else launch_tail_t<1, false>(M, pp, s, L2Window{});
   }
 }
 }  // namespace
@@ -1367,7 +1415,7 @@ void expsum_run(Plan& P, const double* u, double* out, cudaStream_t s, int mode,
                                                          S->cstride);
     stage_end(P, s, kStEsCarry, ev, 1);
     stage_begin(P, s, kStEsMain, &ev);
-    launch_tail(NF, true, S->M, pp, s);
+    launch_tail(NF, true, S->M, pp, s, S->l2w);
     stage_end(P, s, kStEsMain, ev, 1);
     NLG_CUDA(cudaStreamWaitEvent(s, S->join, 0));
     FftCombineArgs f;

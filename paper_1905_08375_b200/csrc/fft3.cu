@@ -1019,6 +1019,7 @@ template <int L>
 void f3_attr(int rf) {
   f3_attr_c<L, 8>(rf);
   f3_attr_c<L, 4>(rf);
+  f3_attr_c<L, 2>(rf);
   NLG_CUDA(cudaFuncSetAttribute(f3_cols_pers<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(2 * sizeof(double2) * L * 4)));
   NLG_CUDA(cudaFuncSetAttribute(f3_cols_tma<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1077,6 +1078,7 @@ void launch_cols_tma(const BoxFft& B, const F3Args& a, bool pd, int64_t planes, 
 template <int L>
 void launch_cols(const F3Args& a, int cols, bool pd, int64_t planes, cudaStream_t s) {
   if (cols == 4) launch_cols_c<L, 4>(a, pd, planes, s);
+  else if (cols == 2) launch_cols_c<L, 2>(a, pd, planes, s);
   else launch_cols_c<L, 8>(a, pd, planes, s);
 }
 
@@ -1218,7 +1220,7 @@ BoxFft* boxfft_setup(const Plan& P, double alpha) {
   auto* B = new BoxFft();
   B->lx = B->ly = lx;
   B->rf = rf;
-  if (const char* ce = std::getenv("NLG_F3_COLS")) B->cols = std::atoi(ce) == 8 ? 8 : 4;
+  if (const char* ce = std::getenv("NLG_F3_COLS")) B->cols = std::atoi(ce) == 8 ? 8 : (std::atoi(ce) == 2 ? 2 : 4);
   B->n = n;
   B->n_in = n_in;
   B->o0 = P.halo_lo;
