@@ -345,7 +345,8 @@ void apply_fast_pipelined(Plan& P, const double* u, double* out) {
   const int64_t st = g.stride0, rows_in = g.in_end - g.in_begin, rows_out = g.row_end - g.row_begin;
   const int64_t H = stencil_reach_rows(P);
   const bool box = stencil_box(P);
-  const int nch = static_cast<int>(std::min<int64_t>(box ? 12 : 8, rows_in));
+  static const int env_chunks = [] { const char* e = std::getenv("NLG_PIPE_CHUNKS"); return e ? std::atoi(e) : 0; }();
+  const int nch = static_cast<int>(std::min<int64_t>(env_chunks > 0 ? env_chunks : (box ? 24 : 16), rows_in));
   if (!P.h2d_stream) {
     NLG_CUDA(cudaStreamCreateWithFlags(&P.h2d_stream, cudaStreamNonBlocking));
     NLG_CUDA(cudaStreamCreateWithFlags(&P.d2h_stream, cudaStreamNonBlocking));

@@ -171,6 +171,7 @@ struct SpanArgs {
   int rule, form;
   const double *pref_hi, *pref_lo, *tot_hi, *tot_lo;
   double* out;
+  int sym;   // n a power of two: exact coordinates, mirror-symmetric spans
 };
 
 // global exclusive prefix P(row, p) for p in [0, len] (P(len) = row total)
@@ -278,7 +279,10 @@ __global__ void __launch_bounds__(256) span_eval(SpanArgs a) {
       if (DIM > 2) { const double d = fabs(static_cast<double>(a1 - ki[1])); q += d * d; }
       const int64_t est = static_cast<int64_t>(sqrt(fmax(rc * rc - q, 0.0)));
       const int64_t er = span_extent<DIM>(a.rule, k, kc, +1, x, h, delta, r2max, est);
-      const int64_t el = span_extent<DIM>(a.rule, k, kc, -1, x, h, delta, r2max, est);
+      // n = 2^L: node coordinates and cell faces are exact dyadics, so the
+      // predicate is mirror-symmetric about the target's cell and the left
+      // extent equals the right one (half the probes)
+      const int64_t el = a.sym ? er : span_extent<DIM>(a.rule, k, kc, -1, x, h, delta, r2max, est);
       int64_t lo = kc - el, hi = kc + er;
       lo = max(lo, int64_t(0));
       hi = min(hi, g.n - 1);
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(256) moment_eval(const __grid_constant__ MomAr
   if (member<1>(a.rule, k, x, h, delta, r2max)) {
     const int64_t est = static_cast<int64_t>(rc);
     const int64_t er = span_extent<1>(a.rule, k, kx, +1, x, h, delta, r2max, est);
-    const int64_t el = span_extent<1>(a.rule, k, kx, -1, x, h, delta, r2max, est);
+    const int64_t el = (g.n & (g.n - 1)) == 0 ? er : span_extent<1>(a.rule, k, kx, -1, x, h, delta, r2max, est);
     const int64_t lo = max(kx - el, int64_t(0)) - g.in_begin, hi = min(kx + er, g.n - 1) - g.in_begin;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};   // sum (t - d)^{2j} u over the span, j = 0..K
     for (int64_t s0 = (lo >> a.lshift) << a.lshift; s0 <= hi; s0 += a.ls) {
@@ -563,6 +567,7 @@ void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   a.tot_hi = P.d_seg_hi;
   a.tot_lo = P.d_seg_lo;
   a.out = out;
+  a.sym = (P.geom.n & (P.geom.n - 1)) == 0;
   const unsigned blocks = static_cast<unsigned>((P.n_out + 255) / 256);
   switch (P.geom.dim) {
     case 1: span_eval<1><<<blocks, 256, 0, s>>>(a); break;
