@@ -148,7 +148,9 @@ nlg_status nlg_apply_direct_dev(nlg_plan* plan, const double* u_dev, double* out
 
 /* Split-phase device apply for sharded plans (multi-GPU halo overlap):
  * _begin enqueues the part of the fast apply that does not read u's halo rows
- * (box FFT mode: the x / y transforms of the owned planes), _end the rest once
+ * (box FFT mode: the x / y transforms of the owned planes; 2-D / 3-D scalar
+ * stencil slabs: the output rows whose window lies in the owned input rows),
+ * _end the rest once
  * the halo rows of u_dev hold the neighbours' values. begin + end ==
  * nlg_apply_fast_dev; for methods without a halo-independent part _begin does
  * nothing. Same stream for both calls. */

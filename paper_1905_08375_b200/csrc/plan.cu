@@ -420,11 +420,30 @@ nlg_status nlg_apply_fast_dev_begin(nlg_plan* plan, const double* u_dev, double*
     Plan& P = plan->p;
     NLG_CUDA(cudaSetDevice(P.device));
     P.split_begun = false;
+    P.split_lo = P.split_hi = 0;
     if (P.fast_method == 3 && stencil_box(P)) {
       const int64_t rows_in = P.geom.in_end - P.geom.in_begin;
       stencil_box_in(P, u_dev, P.halo_lo, rows_in - P.halo_hi, static_cast<cudaStream_t>(stream));
       NLG_CUDA(cudaGetLastError());
       P.split_begun = true;
+    } else if (P.fast_method == 3 && P.geom.dim >= 2 && components(P) == 1 && (P.halo_lo > 0 || P.halo_hi > 0)) {
+      // stencil slab: the output rows whose whole window lies in the owned
+      // input rows (r >= H past a lower halo, r < rows_out - H before an upper
+      // one), cut at CTA-row multiples so the result is bit-identical
+      const int64_t rows_out = P.geom.row_end - P.geom.row_begin, H = stencil_reach_rows(P);
+      const int64_t tile = stencil_row_tile(P);
+      const int64_t lo = P.halo_lo > 0 ? (H + tile - 1) / tile * tile : 0;
+      const int64_t hi = P.halo_hi > 0 ? (rows_out - H) / tile * tile : rows_out;
+      if (hi > lo) {
+        cudaEvent_t ev;
+        stage_begin(P, static_cast<cudaStream_t>(stream), kStStencil, &ev);
+        stencil_apply_rows(P, u_dev, out_dev, lo, hi, static_cast<cudaStream_t>(stream));
+        stage_end(P, static_cast<cudaStream_t>(stream), kStStencil, ev, 1);
+        NLG_CUDA(cudaGetLastError());
+        P.split_lo = lo;
+        P.split_hi = hi;
+        P.split_begun = true;
+      }
     }
   });
 }
@@ -435,11 +454,23 @@ nlg_status nlg_apply_fast_dev_end(nlg_plan* plan, const double* u_dev, double* o
     Plan& P = plan->p;
     NLG_CUDA(cudaSetDevice(P.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (P.split_begun) {
+    if (P.split_begun && stencil_box(P)) {
       const int64_t rows_in = P.geom.in_end - P.geom.in_begin;
       stencil_box_in(P, u_dev, 0, P.halo_lo, s);
       stencil_box_in(P, u_dev, rows_in - P.halo_hi, rows_in, s);
       stencil_box_out(P, u_dev, out_dev, 0, P.geom.row_end - P.geom.row_begin, s);
+      NLG_CUDA(cudaGetLastError());
+      ++P.fast_applies;
+      P.split_begun = false;
+      return;
+    }
+    if (P.split_begun) {   // stencil slab: the edge rows that read the halos
+      const int64_t rows_out = P.geom.row_end - P.geom.row_begin;
+      cudaEvent_t ev;
+      stage_begin(P, s, kStStencil, &ev);
+      stencil_apply_rows(P, u_dev, out_dev, 0, P.split_lo, s);
+      stencil_apply_rows(P, u_dev, out_dev, P.split_hi, rows_out, s);
+      stage_end(P, s, kStStencil, ev, (P.split_lo > 0) + (P.split_hi < rows_out));
       NLG_CUDA(cudaGetLastError());
       ++P.fast_applies;
       P.split_begun = false;

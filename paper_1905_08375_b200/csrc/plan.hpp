@@ -116,6 +116,7 @@ struct Plan {
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   std::vector<cudaEvent_t> pipe_ev;
   bool split_begun = false;   // nlg_apply_fast_dev_begin enqueued the halo-independent part
+  int64_t split_lo = 0, split_hi = 0;   // stencil slabs: the output rows begin computed
 
   int64_t last_pairs = 0;
   int64_t fast_applies = 0;

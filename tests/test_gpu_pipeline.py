@@ -108,3 +108,26 @@ def test_split_phase_box_slab(N, rows):
     a = _dev_apply(op, u)
     b = _dev_apply(op, u, split=True)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dim,n,rows", [(2, 512, (128, 320)), (2, 512, (0, 200)), (3, 96, (30, 70)), (3, 96, (60, 96))])
+def test_split_phase_stencil_slab(N, dim, n, rows):
+    """begin (interior output rows) + end (edge rows) on a sharded stencil slab
+    (variable horizon: cfg2 / cfg4-B families) equals the one-call device apply."""
+    from paper_1905_08375_b200 import configs, nonloc as NL
+    w = configs.cfg2(n) if dim == 2 else configs.cfg4(n, variable=True)
+    dmax = float(w.delta.max())
+    halo = NL.halo_rows(dim=dim, n=n, family=4, delta_max=dmax)
+    rb, re = rows
+    st = n ** (dim - 1)
+    ib, ie = max(0, rb - halo), min(n, re + halo)
+    sl = slice(ib * st, ie * st)
+    kw = w.op_kwargs()
+    for key in ("delta", "coeff", "kappa"):
+        kw[key] = kw[key][sl] if kw[key] is not None else None
+    op = N.NonlocalOperator(dim, n, row_begin=rb, row_end=re, reach=dmax, **kw)
+    assert op.info.fast_method == 3 and op.info.fft_len == 0
+    u = w.u[sl].copy()
+    a = _dev_apply(op, u)
+    b = _dev_apply(op, u, split=True)
+    assert np.array_equal(a, b)
