@@ -131,3 +131,26 @@ def test_split_phase_stencil_slab(N, dim, n, rows):
     a = _dev_apply(op, u)
     b = _dev_apply(op, u, split=True)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("case", ["box", "stencil3d"])
+def test_pipeline_sharded_slab_bitwise(N, case):
+    """The host pipeline on a sharded slab plan (input rows = owned rows +
+    halos, the per-rank e2e path of bench.py --gpus N) equals its device apply."""
+    from paper_1905_08375_b200 import configs, nonloc as NL
+    n = 192
+    w = configs.cfg4(n) if case == "box" else configs.cfg4(n, variable=True)
+    dmax = float(w.delta.max()) if w.delta is not None else w.delta0
+    halo = NL.halo_rows(dim=3, n=n, family=4, delta_max=dmax)
+    rb, re = 70, 190
+    st = n * n
+    ib, ie = rb - halo, min(n, re + halo)
+    sl = slice(ib * st, ie * st)
+    kw = w.op_kwargs()
+    for key in ("delta", "coeff", "kappa"):
+        kw[key] = kw[key][sl] if kw[key] is not None else None
+    op = N.NonlocalOperator(3, n, row_begin=rb, row_end=re, reach=dmax, **kw)
+    assert (op.info.fft_len > 0) == (case == "box")
+    assert op.plan.n_out >= 1 << 22   # the pipelined host path
+    u = w.u[sl].copy()
+    assert np.array_equal(op.apply(u), _dev_apply(op, u))
