@@ -254,6 +254,18 @@ __global__ void __launch_bounds__(256) direct_frac_kernel(const __grid_constant_
     // one row of the window along the last axis: k_last in [c0, c1], the other
     // components fixed (their squared float distance r2o summed first, in the
     // reference's dimension order, and their squared lattice distance mo)
+    // the reference's predicate sqrt_rn(r2) < delta as r2 < thr (sqrt_rn is
+    // monotone; thr = the smallest double whose rounded root reaches delta)
+    double thr = __dmul_rn(delta, delta);
+    while (thr > 0.0 && __dsqrt_rn(thr) >= delta) thr = __longlong_as_double(__double_as_longlong(thr) - 1);
+    while (__dsqrt_rn(thr) < delta) thr = __longlong_as_double(__double_as_longlong(thr) + 1);
+    const double xl = x[DIM - 1];
+    const int kil = static_cast<int>(ki[DIM - 1]);
+    const int nl = static_cast<int>(g.n);
+    const int mlo32 = static_cast<int>(mlo);
+    // one row of the window along the last axis: k_last in [c0, c1], the other
+    // components fixed (their squared float distance r2o summed first, in the
+    // reference's dimension order, and their squared lattice distance mo)
     auto row = [&](const int64_t* ko, double r2o, int64_t mo, bool dom_o, int64_t c0, int64_t c1) {
       constexpr int L = DIM - 1;
       int64_t base = 0;   // input index of k_last = 0 on this row
@@ -265,19 +277,22 @@ __global__ void __launch_bounds__(256) direct_frac_kernel(const __grid_constant_
       } else {
         base = -g.in_begin;
       }
-      for (int64_t kl = c0; kl <= c1; ++kl) {
-        const int64_t dl = kl - ki[L], m = mo + dl * dl;
+      const double* __restrict__ ur = a.u + base;
+      const double* __restrict__ kr = a.kappa ? a.kappa + base : nullptr;
+      const int mo32 = static_cast<int>(mo);
+      for (int kl = static_cast<int>(c0); kl <= static_cast<int>(c1); ++kl) {
+        const int dl = kl - kil, m = mo32 + dl * dl;
         if (m == 0) continue;
-        const double d = __dsub_rn(coord(kl, h), x[L]);
+        const double d = __dsub_rn(__dmul_rn(__dadd_rn(static_cast<double>(kl), 0.5), h), xl);
         const double r2 = __dadd_rn(r2o, __dmul_rn(d, d));
-        if (m >= mlo && !(__dsqrt_rn(r2) < delta)) continue;   // tie band: the reference's predicate
+        if (m >= mlo32 && !(r2 < thr)) continue;                    // tie band: the reference's predicate
         const double2 wt = __ldg(a.wfrac + (DIM == 1 ? (dl < 0 ? -dl : dl) : m));
         const double w0 = fma(-ca * fma(r2, wt.y, -1.0), wt.x, wt.x);
         ++my_pairs;
-        const bool in_dom = dom_o && kl >= 0 && kl < g.n;
-        const double du = (in_dom ? a.u[base + kl] : 0.0) - ui;   // difference form, as the reference
+        const bool in_dom = dom_o && kl >= 0 && kl < nl;
+        const double du = (in_dom ? ur[kl] : 0.0) - ui;              // difference form, as the reference
         A = fma(w0, du, A);
-        if (a.kappa) Bk = fma(w0 * (in_dom ? a.kappa[base + kl] : kap_i), du, Bk);
+        if (kr) Bk = fma(w0 * (in_dom ? kr[kl] : kap_i), du, Bk);
       }
     };
     auto isq = [](int64_t m) {
