@@ -350,8 +350,21 @@ constexpr int kBX = 32, kBY = 32;
 #endif
 constexpr int kR2Frac = NLG_R2FRAC, kR2Peri = NLG_R2PERI, kR3Frac = NLG_R3FRAC;   // targets per lane
 
-__host__ __device__ inline int tile2d_q(int H) { return kBX / 4 + 2 + H / 2; }   // slots per plane
-__host__ __device__ inline int tile2d_rs(int H) { return 4 * tile2d_q(H) + 1; }  // row stride in slots (odd)
+// 2-D fractional tiles may be NLG_BX2 columns wide (64: two CTAs of 8 warps per
+// SM instead of three of 4, a smaller halo share); every other variant 32
+#ifndef NLG_BX2
+#define NLG_BX2 32
+#endif
+#ifndef NLG_BX3
+#define NLG_BX3 32
+#endif
+template <int DIM, int KIND>
+__host__ __device__ constexpr int tile_bx() { return KIND != 0 ? kBX : (DIM == 2 ? NLG_BX2 : (DIM == 3 ? NLG_BX3 : kBX)); }
+__host__ __device__ inline int tile_bx_rt(int dim, int kind) {
+  return kind != 0 ? kBX : (dim == 2 ? NLG_BX2 : (dim == 3 ? NLG_BX3 : kBX));
+}
+__host__ __device__ inline int tile2d_q(int H, int bx = kBX) { return bx / 4 + 2 + H / 2; }   // slots per plane
+__host__ __device__ inline int tile2d_rs(int H, int bx = kBX) { return 4 * tile2d_q(H, bx) + 1; }  // row stride in slots (odd)
 __host__ __device__ inline int isq_len(int H) { return (H + 1) * (H + 1) + 1; }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool in) {
@@ -437,10 +450,12 @@ __device__ __forceinline__ void sweep_row(Acc2<KIND, KW, kRX>& A, const double2*
 // the grid runs z fastest so the blocks in flight share their source planes
 // in L2.
 template <int DIM, int KIND, bool KW, int kRX>
-__global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kernel(StArgs a) {
-  constexpr int kLX = 32 / kRX, kLY = kRX, kWY = 32 / kRX;
+__global__ void __launch_bounds__(tile_bx<DIM, KIND>() * kBY / kRX, (kRX == 8 ? 4 : 3) * kBX / tile_bx<DIM, KIND>())
+    stencil_rb_kernel(StArgs a) {
+  constexpr int kBXt = tile_bx<DIM, KIND>();
+  constexpr int kLX = kBXt / kRX, kLY = 32 / kLX, kWY = kBY / kLY;
   extern __shared__ __align__(16) double sm[];
-  const int H = a.H, Q = tile2d_q(H), RS = tile2d_rs(H), TH = kBY + 2 * H, TWc = 4 * Q;
+  const int H = a.H, Q = tile2d_q(H, kBXt), RS = tile2d_rs(H, kBXt), TH = kBY + 2 * H, TWc = 4 * Q;
   double2* tile = reinterpret_cast<double2*>(sm);          // [TH][RS slots: 4 planes x Q, +1 pad]
   double* wt = sm + 2 * static_cast<size_t>(TH + 1) * RS;  // row TH: zeros (partner of row 0)
   // weights in shared memory: the whole table (2-D) or the rows of the current |dz| (3-D)
@@ -463,13 +478,13 @@ __global__ void __launch_bounds__(1024 / kRX, kRX == 8 ? 4 : 3) stencil_rb_kerne
   // tile origin: 2-D (x0, y0) from the grid; 3-D z fastest, then the x-y tile
   int64_t x0, y0, z = 0;
   if (DIM == 2) {
-    x0 = static_cast<int64_t>(blockIdx.x) * kBX;
+    x0 = static_cast<int64_t>(blockIdx.x) * kBXt;
     y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * kBY;
   } else {
-    const int64_t ntx = (n + kBX - 1) / kBX;
+    const int64_t ntx = (n + kBXt - 1) / kBXt;
     z = g.row_begin + blockIdx.x;
-    x0 = (blockIdx.y % ntx) * kBX;
-    y0 = (blockIdx.y / ntx) * kBY;
+    x0 = (blockIdx.y % ntx) * kBXt;
+    y0 = (blockIdx.y / ntx) * kBY;   // grid.y = ntx * ceil(n / kBY)
   }
   const int64_t ystop = DIM == 2 ? g.row_end : n;
   const int64_t nin_total = (g.in_end - g.in_begin) * g.stride0;
@@ -904,7 +919,8 @@ void launch_t(const StArgs& a, cudaStream_t s, size_t smem) {
 
 size_t tile2d_bytes(const StArgs& a) {
   const size_t wlen = a.g.dim == 2 ? a.tab_len : static_cast<size_t>(a.H + 1) * a.ws;
-  return sizeof(double2) * static_cast<size_t>(kBY + 2 * a.H + 1) * tile2d_rs(a.H) + sizeof(double) * wlen +
+  return sizeof(double2) * static_cast<size_t>(kBY + 2 * a.H + 1) * tile2d_rs(a.H, tile_bx_rt(a.g.dim, a.kind)) +
+         sizeof(double) * wlen +
          sizeof(int) * (isq_len(a.H) + 1);
 }
 
@@ -931,20 +947,23 @@ void launch(const StArgs& a, cudaStream_t s, size_t smem) {
     return;
   }
   if (dim == 2 && a.mode == 0) {
-    dim3 grid(static_cast<unsigned>((n + kBX - 1) / kBX),
+    const int bx = tile_bx_rt(2, a.kind);
+    dim3 grid(static_cast<unsigned>((n + bx - 1) / bx),
               static_cast<unsigned>((a.g.row_end - a.g.row_begin + kBY - 1) / kBY));
     const size_t sb = tile2d_bytes(a);
-    if (a.kind == 1) stencil_rb_kernel<2, 1, false, kR2Peri><<<grid, dim3(32, 32 / kR2Peri), sb, s>>>(a);
-    else if (a.kw) stencil_rb_kernel<2, 0, true, kR2Frac><<<grid, dim3(32, 32 / kR2Frac), sb, s>>>(a);
-    else stencil_rb_kernel<2, 0, false, kR2Frac><<<grid, dim3(32, 32 / kR2Frac), sb, s>>>(a);
+    constexpr int kWF = tile_bx<2, 0>() / kR2Frac, kWP = tile_bx<2, 1>() / kR2Peri;   // warps per CTA
+    if (a.kind == 1) stencil_rb_kernel<2, 1, false, kR2Peri><<<grid, dim3(32, kWP), sb, s>>>(a);
+    else if (a.kw) stencil_rb_kernel<2, 0, true, kR2Frac><<<grid, dim3(32, kWF), sb, s>>>(a);
+    else stencil_rb_kernel<2, 0, false, kR2Frac><<<grid, dim3(32, kWF), sb, s>>>(a);
     return;
   }
   if (dim == 3 && a.mode == 0) {
-    const int64_t ntx = (n + kBX - 1) / kBX;
-    dim3 grid(static_cast<unsigned>(a.g.row_end - a.g.row_begin), static_cast<unsigned>(ntx * ntx));
+    constexpr int bx = tile_bx<3, 0>(), kW3 = bx / kR3Frac;
+    const int64_t ntx = (n + bx - 1) / bx, nty = (n + kBY - 1) / kBY;
+    dim3 grid(static_cast<unsigned>(a.g.row_end - a.g.row_begin), static_cast<unsigned>(ntx * nty));
     const size_t sb = tile2d_bytes(a);
-    if (a.kw) stencil_rb_kernel<3, 0, true, kR3Frac><<<grid, dim3(32, 32 / kR3Frac), sb, s>>>(a);
-    else stencil_rb_kernel<3, 0, false, kR3Frac><<<grid, dim3(32, 32 / kR3Frac), sb, s>>>(a);
+    if (a.kw) stencil_rb_kernel<3, 0, true, kR3Frac><<<grid, dim3(32, kW3), sb, s>>>(a);
+    else stencil_rb_kernel<3, 0, false, kR3Frac><<<grid, dim3(32, kW3), sb, s>>>(a);
     return;
   }
   if (a.kind == 1) {
