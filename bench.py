@@ -48,9 +48,10 @@ UNIT = "grid points/s"
 TARGET_SEED = 20261020          # the fixed CPU-baseline target set
 
 # Fixed CPU-baseline samples (output nodes): one-core leg, all-cores leg.
-# Sized for ~1-3 s of wall time each on the GPU box's host.
-CPU_SAMPLE = {"cfg0": (4096, 4096), "cfg1": (64, 1024), "cfg2": (8192, 131072), "cfg3": (8192, 65536),
-              "cfg4": (1024, 16384), "cfg4b": (512, 8192)}
+# Sized for ~1-3 s of wall time each on the GPU box's host (16 threads);
+# large enough that thread start-up and scheduling noise stay small.
+CPU_SAMPLE = {"cfg0": (4096, 4096), "cfg1": (128, 2048), "cfg2": (16384, 262144), "cfg3": (16384, 131072),
+              "cfg4": (4096, 65536), "cfg4b": (2048, 32768)}
 
 
 def _peaks():
