@@ -1389,29 +1389,35 @@ void boxfft_in(Plan& P, BoxFft& B, const double* u, int64_t p0, int64_t p1, cuda
 // PC, PD, PE and the tie pass on output planes [q0, q1) (needs PB done on the
 // input planes up to q1 + r_f)
 void boxfft_out(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
-                double* out, int64_t q0, int64_t q1, cudaStream_t s) {
+                double* out, int64_t q0, int64_t q1, cudaStream_t s, int parts) {
   if (q1 <= q0) return;
   F3Args a = apply_args(P, B, u, scale, scale0, diag, out);
   a.p0 = q0;
   a.p1 = q1;
   const int lx = B.lx;
   cudaEvent_t ev;
-  stage_begin(P, s, kStBoxPC, &ev);
-  launch_zstencil(a, s);
-  stage_end(P, s, kStBoxPC, ev, 1);
-  stage_begin(P, s, kStBoxPD, &ev);
+  if (parts & 1) {
+    stage_begin(P, s, kStBoxPC, &ev);
+    launch_zstencil(a, s);
+    stage_end(P, s, kStBoxPC, ev, 1);
+  }
+  if (parts & 2) {
+    stage_begin(P, s, kStBoxPD, &ev);
 #define NLG_F3_CASE(N) \
   if (lx == N) { if (B.pers) launch_cols_pers<N>(B, a, true, q1 - q0, s); else if (B.tma) launch_cols_tma<N>(B, a, true, q1 - q0, s); else launch_cols<N>(a, B.cols, true, q1 - q0, s); }
-  NLG_F3_L(NLG_F3_CASE)
+    NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
-  stage_end(P, s, kStBoxPD, ev, 1);
-  stage_begin(P, s, kStBoxPE, &ev);
+    stage_end(P, s, kStBoxPD, ev, 1);
+  }
+  if (parts & 4) {
+    stage_begin(P, s, kStBoxPE, &ev);
 #define NLG_F3_CASE(N) \
   if (lx == N) launch_rows<N>(a, true, (q1 - q0) * B.n, s);
-  NLG_F3_L(NLG_F3_CASE)
+    NLG_F3_L(NLG_F3_CASE)
 #undef NLG_F3_CASE
-  stage_end(P, s, kStBoxPE, ev, 1);
-  if (B.ntie > 0) {
+    stage_end(P, s, kStBoxPE, ev, 1);
+  }
+  if (B.ntie > 0 && (parts & 8)) {
     stage_begin(P, s, kStBoxTie, &ev);
     TieArgs t = tie_args(P, B);
     t.u = u;
@@ -1452,8 +1458,19 @@ void boxfft_out(Plan& P, BoxFft& B, const double* u, const double* scale, double
 
 void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
                   double* out, cudaStream_t s) {
-  boxfft_in(P, B, u, 0, B.n_in, s);
-  boxfft_out(P, B, u, scale, scale0, diag, out, 0, B.rows_out, s);
+  // NLG_F3_CHUNK=k (planes, read once): PA -> PB and PD -> PE run chunk by chunk so the
+  // second pass of each pair finds its input in L2 (a plane of Z is ~10 MB at L = 800)
+  static const int chunk = [] { const char* e = std::getenv("NLG_F3_CHUNK"); return e ? std::atoi(e) : 0; }();
+  if (chunk <= 0) {
+    boxfft_in(P, B, u, 0, B.n_in, s);
+    boxfft_out(P, B, u, scale, scale0, diag, out, 0, B.rows_out, s);
+    return;
+  }
+  for (int64_t p0 = 0; p0 < B.n_in; p0 += chunk) boxfft_in(P, B, u, p0, std::min<int64_t>(p0 + chunk, B.n_in), s);
+  boxfft_out(P, B, u, scale, scale0, diag, out, 0, B.rows_out, s, 1);
+  for (int64_t q0 = 0; q0 < B.rows_out; q0 += chunk)
+    boxfft_out(P, B, u, scale, scale0, diag, out, q0, std::min<int64_t>(q0 + chunk, B.rows_out), s, 2 | 4);
+  boxfft_out(P, B, u, scale, scale0, diag, out, 0, B.rows_out, s, 8);
 }
 
 int boxfft_launches(const BoxFft& B) { return 5 + (B.ntie > 0 ? 1 : 0); }

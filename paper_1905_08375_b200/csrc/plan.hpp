@@ -163,7 +163,7 @@ void boxfft_apply(Plan& P, BoxFft& B, const double* u, const double* scale, doub
                   double* out, cudaStream_t s);
 void boxfft_in(Plan& P, BoxFft& B, const double* u, int64_t p0, int64_t p1, cudaStream_t s);
 void boxfft_out(Plan& P, BoxFft& B, const double* u, const double* scale, double scale0, const double* diag,
-                double* out, int64_t q0, int64_t q1, cudaStream_t s);
+                double* out, int64_t q0, int64_t q1, cudaStream_t s, int parts = 15);
 int boxfft_launches(const BoxFft& B);
 int boxfft_length(const BoxFft& B);
 void boxfft_free(BoxFft* B);

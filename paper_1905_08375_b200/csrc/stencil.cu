@@ -22,8 +22,12 @@
 // are shared-memory broadcasts.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "plan.hpp"
 
@@ -41,6 +45,11 @@ struct StencilState {
   BoxFft* box = nullptr;                // constant-horizon 3-D: FFT convolution + tie band (fft3.cu)
   bool scale_const = false;             // no per-node coefficient: scale[i] == scale0
   double scale0 = 0.0;
+  // column-lane apply (stencil_cy_kernel): per-node horizons, sources by TMA
+  bool cy = false;
+  int hs = 0;                           // largest offset component any target includes
+  CUtensorMap tmu, tmk;                 // boxes of the input planes of u (re-encoded when u moves) and kappa
+  const double* tmu_base = nullptr;
 };
 
 namespace {
@@ -50,6 +59,7 @@ constexpr int kTX = 32, kTY = 4;        // 128 threads, lanes along the fastest 
 struct StArgs {
   Geom g;
   int kind, kw, collar, mode, H;
+  int hs;                 // column-lane apply: box halo
   const double* u;        // [comps][n_in]
   const double2* pk;      // (u, kappa u) when kw
   const double* delta;
@@ -830,6 +840,384 @@ __global__ void __launch_bounds__(tile_bx<DIM, KIND>() * kBY / kRX, (kRX == 8 ? 
   }
 }
 
+
+// ---- column-lane apply (fractional, per-node horizons): stencil_cy_kernel -----
+// The variable-horizon 2-D / 3-D apply (cfg2, cfg4-B). Lanes run along x (the
+// contiguous axis), a lane owns kCyR consecutive targets of one column, and the
+// window slides along y: for a column offset dx the lane walks dy = -YW..YW,
+// one new source (rows are dense, any row pitch is conflict-free) and one
+// weight (broadcast) per step feeding 2 kCyR FMAs (A and B sums). The weight is
+// even in dx, so columns +dx / -dx are added while loading; in 3-D the source
+// planes z +- dz are added once in shared memory (the combine pass), which
+// also forms kappa u. Sources arrive as dense boxes by cp.async.bulk.tensor
+// (one elected thread; zero fill outside the domain / slab from the tensor
+// map's bounds = the clip exterior); the mirror planes of the next |dz| are in
+// flight during the sweep of the current one. Per-target horizons: the sweep
+// range is the warp's widest (M_W); steps every target of the warp includes
+// (|d|^2 <= M_N) run unmasked, the others predicate each FMA pair on
+// |d|^2 <= M_r (integer, exact). Tie-band targets (rare with a variable
+// horizon) add their band afterwards from global memory with the reference's
+// float predicate.
+#ifndef NLG_CY_R
+#define NLG_CY_R 16
+#endif
+constexpr int kCyR = NLG_CY_R;          // targets per lane: 16 (5 ring phases) or 8 (3)
+#ifndef NLG_CY_RING
+#define NLG_CY_RING 0
+#endif
+#ifndef NLG_CY_MINB
+#define NLG_CY_MINB 1
+#endif
+#ifndef NLG_CY_W2
+#define NLG_CY_W2 4
+#endif
+#ifndef NLG_CY_W3
+#define NLG_CY_W3 2
+#endif
+template <int DIM>
+__host__ __device__ constexpr int cy_warps() { return DIM == 2 ? NLG_CY_W2 : NLG_CY_W3; }
+__host__ __device__ inline int cy_bw(int hs) { return 32 + 2 * hs; }
+__host__ __device__ inline int cy_bhl(int hs, int warps) { return warps * kCyR + 2 * hs; }
+__host__ __device__ inline int cy_box(int hs, int warps) {     // doubles per box, 128-byte multiple
+  return (cy_bw(hs) * (cy_bhl(hs, warps) + 3) + 15) & ~15;
+}
+
+__device__ __forceinline__ void cy_mbar_wait(unsigned mb, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n\t}" ::"r"(mb),
+      "r"(parity)
+      : "memory");
+}
+
+// one column pair (+dx / -dx; dx = 0 passes the same column twice with halved
+// weights): steps dy = -YW .. YW (+ up to 3 masked overshoot steps). The
+// window of kCyR + 4 sources per field lives in registers as a ring: chunk
+// number PH (mod 5) finds logical element i at (i + 4 PH) mod (kCyR + 4), so
+// sliding by four costs no register moves.
+template <bool KW, int PH>
+__device__ __forceinline__ void cy_chunk(double (&a0)[kCyR], double (&a1)[kCyR], const int (&M)[kCyR],
+                                         double (&Wu)[kCyR + 4], double (&Wk)[kCyR + 4], const double*& up,
+                                         const double*& um, const double*& kp, const double*& km, int BW,
+                                         const double*& wk, int dy0, int YW, int YN, int c0) {
+  constexpr int NW = kCyR + 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    Wu[(kCyR + j + 4 * PH) % NW] = up[j * BW] + um[j * BW];
+    if (KW) Wk[(kCyR + j + 4 * PH) % NW] = kp[j * BW] + km[j * BW];
+  }
+  if (dy0 >= -YN && min(dy0 + 3, YW) <= YN) {   // every step of the chunk inside every target's ball
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const double w = dy0 + s <= YW ? wk[s] : 0.0;   // overshoot steps of the last chunk
+#pragma unroll
+      for (int r = 0; r < kCyR; ++r) {
+        a0[r] = fma(w, Wu[(s + r + 4 * PH) % NW], a0[r]);
+        if (KW) a1[r] = fma(w, Wk[(s + r + 4 * PH) % NW], a1[r]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const double w = wk[s];
+      const int c = c0 + (dy0 + s) * (dy0 + s);
+#pragma unroll
+      for (int r = 0; r < kCyR; ++r) {   // the weight selected to zero outside the target's own ball
+        const double wr = c <= M[r] ? w : 0.0;
+        a0[r] = fma(wr, Wu[(s + r + 4 * PH) % NW], a0[r]);
+        if (KW) a1[r] = fma(wr, Wk[(s + r + 4 * PH) % NW], a1[r]);
+      }
+    }
+  }
+  up += 4 * BW;
+  um += 4 * BW;
+  kp += 4 * BW;
+  km += 4 * BW;
+  wk += 4;
+}
+
+template <bool KW>
+__device__ __forceinline__ void cy_sweep(double (&a0)[kCyR], double (&a1)[kCyR], const int (&M)[kCyR],
+                                         const double* up, const double* um, const double* kp, const double* km,
+                                         int BW, const double* wk, int YW, int YN, int c0) {
+  double Wu[kCyR + 4], Wk[kCyR + 4];
+#pragma unroll
+  for (int i = 0; i < kCyR; ++i) {
+    Wu[i] = up[i * BW] + um[i * BW];
+    if (KW) Wk[i] = kp[i * BW] + km[i * BW];
+  }
+  up += kCyR * BW;
+  um += kCyR * BW;
+  kp += kCyR * BW;
+  km += kCyR * BW;
+  const int nsteps = 2 * YW + 1;
+  int s0 = 0;
+#define NLG_CY_CHUNK(PH)                                                                   \
+  cy_chunk<KW, PH>(a0, a1, M, Wu, Wk, up, um, kp, km, BW, wk, s0 - YW, YW, YN, c0);        \
+  s0 += 4;                                                                                 \
+  if (s0 >= nsteps) break;
+#if NLG_CY_RING
+  for (;;) {
+    NLG_CY_CHUNK(0)
+    NLG_CY_CHUNK(1)
+    NLG_CY_CHUNK(2)
+#if NLG_CY_R == 16
+    NLG_CY_CHUNK(3)
+    NLG_CY_CHUNK(4)
+#endif
+  }
+#else
+  for (;;) {   // one chunk body, the window shifted by register moves
+    NLG_CY_CHUNK(0)
+#pragma unroll
+    for (int i = 0; i < kCyR; ++i) {
+      Wu[i] = Wu[i + 4];
+      if (KW) Wk[i] = Wk[i + 4];
+    }
+  }
+#endif
+#undef NLG_CY_CHUNK
+}
+
+template <int DIM, bool KW>
+__global__ void __launch_bounds__(32 * cy_warps<DIM>(), NLG_CY_MINB)
+    stencil_cy_kernel(const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmk, StArgs a) {
+  constexpr int NWP = cy_warps<DIM>(), NT = 32 * NWP, TY = NWP * kCyR;
+  extern __shared__ __align__(128) double csm[];
+  __shared__ __align__(8) unsigned long long mbar[2];
+  __shared__ int s_bmax;
+  const Geom& g = a.g;
+  const int H = a.H, hs = a.hs, BW = cy_bw(hs), BHl = cy_bhl(hs, NWP), BOX = cy_box(hs, NWP);
+  constexpr int NBOX = (KW ? 2 : 1) * (DIM == 3 ? 2 : 1);
+  double* Tu = csm;
+  double* Tk = KW ? csm + BOX : csm;
+  double* Mu = csm + (KW ? 2 : 1) * BOX;                 // 3-D mirror planes
+  double* Mk = KW ? Mu + BOX : Mu;
+  const int W1 = H + 1, wlen = W1 * a.ws;                // weight rows of one |dz|: [|dx|][dy + H]
+  double* wt = csm + NBOX * BOX;                          // two buffers in 3-D
+  int* isq = reinterpret_cast<int*>(wt + (DIM == 3 ? 2 : 1) * wlen);
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+  const int64_t n = g.n;
+  int64_t x0, y0, z = 0;
+  if (DIM == 2) {
+    x0 = static_cast<int64_t>(blockIdx.x) * 32;
+    y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * TY;
+  } else {
+    const int64_t ntx = (n + 31) / 32;
+    z = g.row_begin + blockIdx.x;
+    x0 = (blockIdx.y % ntx) * 32;
+    y0 = (blockIdx.y / ntx) * TY;
+  }
+  const unsigned mb0 = static_cast<unsigned>(__cvta_generic_to_shared(mbar));
+  const unsigned sTu = static_cast<unsigned>(__cvta_generic_to_shared(Tu));
+  const unsigned sMu = static_cast<unsigned>(__cvta_generic_to_shared(Mu));
+  const unsigned BOXB = static_cast<unsigned>(sizeof(double)) * BOX;
+  const unsigned BYTES = static_cast<unsigned>(sizeof(double)) * BW * BHl * (KW ? 2 : 1);
+  // boxes of one plane (u and kappa) -> dst, dst + BOX, completing on mbar[which]
+  auto issue = [&](unsigned dst, int which, int64_t gz) {
+    const unsigned mb = mb0 + 8u * which;
+    const int cx = static_cast<int>(x0) - hs;
+    const int cy = static_cast<int>(DIM == 2 ? y0 - hs - g.in_begin : y0 - hs);
+    const int cz = DIM == 2 ? 0 : static_cast<int>(gz - g.in_begin);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(BYTES) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(&tmu), "r"(cx), "r"(cy), "r"(cz), "r"(mb)
+        : "memory");
+    if (KW)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst + BOXB),
+          "l"(&tmk), "r"(cx), "r"(cy), "r"(cz), "r"(mb)
+          : "memory");
+  };
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue(sTu, 0, z);
+    s_bmax = -1;
+  }
+  for (int i = tid; i < isq_len(H); i += NT) {
+    int x = static_cast<int>(sqrtf(static_cast<float>(i)));
+    while (x * x > i) --x;
+    while ((x + 1) * (x + 1) <= i) ++x;
+    isq[i] = x;
+  }
+  // the three pad rows below the loaded box are read by overshoot steps only (never used): keep them finite
+  for (int i = tid; i < 3 * BW; i += NT) {
+    Tu[BW * BHl + i] = 0.0;
+    if (KW) Tk[BW * BHl + i] = 0.0;
+  }
+  const int64_t ystop = DIM == 2 ? g.row_end : n;
+  const int64_t ix = x0 + lane;
+  const int64_t iy0 = y0 + wy * kCyR;
+  const double inv_h = 1.0 / g.h;
+  auto in_index = [&](int64_t iy) {
+    return DIM == 2 ? (iy - g.in_begin) * n + ix : ((z - g.in_begin) * n + iy) * n + ix;
+  };
+  int M[kCyR];
+  unsigned tiem = 0;
+  int Mx = -1, Mn = 1 << 20;
+#pragma unroll
+  for (int r = 0; r < kCyR; ++r) {
+    M[r] = -1;
+    const int64_t iy = iy0 + r;
+    if (ix < n && iy < ystop) {
+      const double e = a.delta[in_index(iy)] * inv_h, e2 = e * e;
+      const int mlo = static_cast<int>(ceil(e2 * (1.0 - tie_band_n(inv_h))));
+      const int mhi = static_cast<int>(floor(e2 * (1.0 + tie_band_n(inv_h))));
+      M[r] = mlo <= mhi ? mlo - 1 : mhi;
+      if (mlo <= mhi) tiem |= 1u << r;
+      Mn = min(Mn, M[r]);
+    }
+    Mx = max(Mx, M[r]);
+  }
+  const int MW = __reduce_max_sync(0xffffffffu, Mx);
+  const int MN = __reduce_min_sync(0xffffffffu, Mn);
+  __syncthreads();                                       // s_bmax, isq
+  if (DIM == 3 && lane == 0) atomicMax(&s_bmax, MW);
+  if (DIM == 3) __syncthreads();
+  const int Rz = DIM == 3 ? (s_bmax < 0 ? -1 : isq[s_bmax]) : 0;
+  if (DIM == 3 && tid == 0 && Rz >= 1) {
+    issue(sMu, 1, z - 1);
+  }
+  if (Rz < 0) cy_mbar_wait(mb0, 0u);                     // (no live target: never leave a bulk copy in flight)
+  double a0[kCyR], a1[kCyR];
+#pragma unroll
+  for (int r = 0; r < kCyR; ++r) a0[r] = a1[r] = 0.0;
+  const int colbase = (wy * kCyR + hs) * BW + lane + hs;  // the lane's first target in the box
+  for (int dz = 0; dz <= Rz; ++dz) {
+    // weight rows of this |dz| (row dx = 0 halved: its column is added to itself)
+    double* wd = wt + (DIM == 3 ? (dz & 1) * wlen : 0);
+    {
+      const double* src = a.tab + static_cast<size_t>(dz) * wlen;
+      for (int i = tid; i < wlen; i += NT) wd[i] = (i < a.ws ? 0.5 : 1.0) * __ldg(src + i);
+    }
+    cy_mbar_wait(mb0, static_cast<unsigned>(dz & 1));
+    if (DIM == 3 && dz > 0) cy_mbar_wait(mb0 + 8u, static_cast<unsigned>((dz - 1) & 1));
+    // combine: (u, kappa) [+ mirror] -> (u+ + u-, kappa+ u+ + kappa- u-)
+    {
+      double2* tu2 = reinterpret_cast<double2*>(Tu);
+      double2* tk2 = reinterpret_cast<double2*>(Tk);
+      const double2* mu2 = reinterpret_cast<const double2*>(Mu);
+      const double2* mk2 = reinterpret_cast<const double2*>(Mk);
+      const int ne2 = BW * BHl / 2;
+      if (DIM == 3 && dz > 0) {
+        for (int e = tid; e < ne2; e += NT) {
+          double2 u = tu2[e];
+          const double2 m = mu2[e];
+          if (KW) {
+            double2 k = tk2[e];
+            const double2 km = mk2[e];
+            k.x = fma(km.x, m.x, k.x * u.x);
+            k.y = fma(km.y, m.y, k.y * u.y);
+            tk2[e] = k;
+          }
+          u.x += m.x;
+          u.y += m.y;
+          tu2[e] = u;
+        }
+      } else if (KW) {
+        for (int e = tid; e < ne2; e += NT) {
+          const double2 u = tu2[e];
+          double2 k = tk2[e];
+          k.x *= u.x;
+          k.y *= u.y;
+          tk2[e] = k;
+        }
+      }
+    }
+    __syncthreads();                                     // tile + weights ready; mirror boxes consumed
+    if (DIM == 3 && tid == 0 && dz + 1 <= Rz && dz >= 1) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(sMu, 1, z - (dz + 1));
+    }
+    const int c00 = dz * dz;
+    const int mW = MW - c00;
+    if (mW >= 0) {
+      const int XW = isq[mW];
+      for (int dx = 0; dx <= XW; ++dx) {
+        const int c0 = c00 + dx * dx;
+        const int YW = isq[MW - c0];
+        const int YN = MN >= c0 && MN <= MW ? isq[MN - c0] : -1;
+        const int o = colbase - YW * BW;
+        cy_sweep<KW>(a0, a1, M, Tu + o + dx, Tu + o - dx, Tk + o + dx, Tk + o - dx, BW, wd + dx * a.ws + H - YW, YW, YN,
+                     c0);
+      }
+    }
+    if (DIM == 3 && dz + 1 <= Rz) {
+      __syncthreads();                                   // the tile is consumed
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(sTu, 0, z + dz + 1);
+      }
+    }
+  }
+  // tie bands (rare): offsets with |d|^2 in [mlo, mhi] by the reference's float predicate, from global memory
+  {
+    unsigned tm = tiem;
+    while (tm) {
+      const int rr = __ffs(tm) - 1;
+      tm &= tm - 1;
+      const int64_t iy = iy0 + rr;
+      const double delta = a.delta[in_index(iy)];
+      const double e = delta * inv_h, e2 = e * e;
+      const int mlo = static_cast<int>(ceil(e2 * (1.0 - tie_band_n(inv_h))));
+      const int mhi = static_cast<int>(floor(e2 * (1.0 + tie_band_n(inv_h))));
+      const int64_t ki[3] = {DIM == 2 ? iy : z, DIM == 2 ? ix : iy, ix};
+      const int Rt = isqrt_floor(mhi);
+      double t0 = 0.0, t1 = 0.0;
+      for (int dz = (DIM == 3 ? -Rt : 0); dz <= (DIM == 3 ? Rt : 0); ++dz) {
+        const int Ry = isqrt_floor(mhi - dz * dz);
+        for (int dy = -Ry; dy <= Ry; ++dy) {
+          const int X = isqrt_floor(mhi - dz * dz - dy * dy);
+          const int m = dz * dz + dy * dy + X * X;
+          if (m < mlo || m == 0) continue;
+          for (int sx = -X; sx <= X; sx += (X > 0 ? 2 * X : 1)) {
+            bool in;
+            if (DIM == 2) {
+              const int d[2] = {dy, sx};
+              in = point_in<2>(ki, d, g.h, delta);
+            } else {
+              const int d[3] = {dz, dy, sx};
+              in = point_in<3>(ki, d, g.h, delta);
+            }
+            if (!in) continue;
+            const int64_t gz = z + dz, gy = iy + dy, gx = ix + sx;
+            if (gy < 0 || gy >= n || gx < 0 || gx >= n) continue;
+            if (DIM == 3 && (gz < 0 || gz >= n || gz < g.in_begin || gz >= g.in_end)) continue;
+            if (DIM == 2 && (gy < g.in_begin || gy >= g.in_end)) continue;
+            const int64_t k = DIM == 2 ? (gy - g.in_begin) * n + gx : ((gz - g.in_begin) * n + gy) * n + gx;
+            const int az = dz < 0 ? -dz : dz, ay = dy < 0 ? -dy : dy;
+            const double w = __ldg(a.tab + (static_cast<size_t>(DIM == 3 ? az : 0) * W1 + ay) * a.ws + sx + H);
+            const double uu = a.u[k];
+            t0 = fma(w, uu, t0);
+            if (KW) t1 = fma(w, a.kappa[k] * uu, t1);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kCyR; ++r) {
+        if (r == rr) {
+          a0[r] += t0;
+          a1[r] += t1;
+        }
+      }
+    }
+  }
+  if (ix >= n) return;
+#pragma unroll
+  for (int r = 0; r < kCyR; ++r) {
+    const int64_t iy = iy0 + r;
+    if (iy < ystop) {
+      const int64_t ii = in_index(iy);
+      const int64_t oi = ii - (g.row_begin - g.in_begin) * g.stride0;
+      const double X = KW ? fma(a.kappa[ii], a0[r], a1[r]) : a0[r];
+      a.out[oi] = a.scale[oi] * (X - a.u[ii] * a.diag[oi]);
+    }
+  }
+}
+
 // 1-D fractional apply (horizons below the scan threshold, e.g. cfg0): S
 // lanes per target over a shared-memory tile of the CTA's neighbourhood, lane
 // s summing the offsets k = s mod S of the target's span, then a shuffle
@@ -980,6 +1368,62 @@ void launch(const StArgs& a, cudaStream_t s, size_t smem) {
   }
 }
 
+
+// Tensor map over an input field for the column-lane apply: (x: n, y: n or the
+// input rows, z: input planes or 1), boxes of (32 + 2 hs) x (rows + 2 hs) x 1,
+// zero fill outside.
+bool cy_encode(CUtensorMap* m, const double* base, int dim, int64_t n, int64_t rows_in, int hs, int warps) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess || !fn)
+      return false;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if ((n * 8) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(dim == 2 ? rows_in : n),
+                              static_cast<cuuint64_t>(dim == 2 ? 1 : rows_in)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(n) * 8, static_cast<cuuint64_t>(n) * dims[1] * 8};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(cy_bw(hs)), static_cast<cuuint32_t>(cy_bhl(hs, warps)), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+size_t cy_smem(const StArgs& a, int dim) {
+  const int warps = dim == 2 ? cy_warps<2>() : cy_warps<3>();
+  const int nbox = (a.kw ? 2 : 1) * (dim == 3 ? 2 : 1);
+  const size_t wlen = static_cast<size_t>(a.H + 1) * a.ws;
+  return sizeof(double) * (static_cast<size_t>(nbox) * cy_box(a.hs, warps) + (dim == 3 ? 2 : 1) * wlen) +
+         sizeof(int) * (isq_len(a.H) + 1);
+}
+
+// the column-lane launch; false when the tensor map of u cannot be encoded (the caller falls back)
+bool launch_cy(StencilState& S, const StArgs& a, cudaStream_t s) {
+  const int dim = a.g.dim;
+  const int64_t n = a.g.n, rows_in = a.g.in_end - a.g.in_begin;
+  const int warps = dim == 2 ? cy_warps<2>() : cy_warps<3>();
+  if (S.tmu_base != a.u) {
+    if (!cy_encode(&S.tmu, a.u, dim, n, rows_in, S.hs, warps)) return false;
+    S.tmu_base = a.u;
+  }
+  const size_t sb = cy_smem(a, dim);
+  if (dim == 2) {
+    dim3 grid(static_cast<unsigned>((n + 31) / 32),
+              static_cast<unsigned>((a.g.row_end - a.g.row_begin + warps * kCyR - 1) / (warps * kCyR)));
+    if (a.kw) stencil_cy_kernel<2, true><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmk, a);
+    else stencil_cy_kernel<2, false><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu, a);
+  } else {
+    const int64_t ntx = (n + 31) / 32, nty = (n + warps * kCyR - 1) / (warps * kCyR);
+    dim3 grid(static_cast<unsigned>(a.g.row_end - a.g.row_begin), static_cast<unsigned>(ntx * nty));
+    if (a.kw) stencil_cy_kernel<3, true><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmk, a);
+    else stencil_cy_kernel<3, false><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu, a);
+  }
+  return true;
+}
+
 StArgs make_args(const Plan& P, const StencilState& S, int mode, const double* u, double* out) {
   StArgs a;
   a.g = P.geom;
@@ -988,6 +1432,7 @@ StArgs make_args(const Plan& P, const StencilState& S, int mode, const double* u
   a.collar = P.exterior == 1;
   a.mode = mode;
   a.H = S.H;
+  a.hs = S.hs;
   a.u = u;
   a.pk = reinterpret_cast<const double2*>(S.pack);
   a.delta = P.d_delta;
@@ -1017,6 +1462,10 @@ void allow_smem() {
   smem_attr(stencil_rb_kernel<2, 1, false, kR2Peri>);
   smem_attr(stencil_rb_kernel<3, 0, true, kR3Frac>);
   smem_attr(stencil_rb_kernel<3, 0, false, kR3Frac>);
+  smem_attr(stencil_cy_kernel<2, true>);
+  smem_attr(stencil_cy_kernel<2, false>);
+  smem_attr(stencil_cy_kernel<3, true>);
+  smem_attr(stencil_cy_kernel<3, false>);
   smem_attr(stencil1d_kernel<true, 1>);
   smem_attr(stencil1d_kernel<false, 1>);
   smem_attr(stencil1d_kernel<true, 8>);
@@ -1042,7 +1491,11 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   const Geom& g = P.geom;
   const bool frac = d.family == NLG_FRACTIONAL, peri = d.family == NLG_PERIDYNAMIC;
   if (!frac && !(peri && g.dim == 2)) return;
-  const int H = static_cast<int>(std::floor(P.delta_max / g.h)) + 2;
+  // tile halo: every included offset has |d_a| <= floor(delta_max / h (1 + 1e-12)) <= floor(delta_max / h) + 1
+#ifndef NLG_ST_HPAD
+#define NLG_ST_HPAD 1
+#endif
+  const int H = static_cast<int>(std::floor(P.delta_max / g.h)) + NLG_ST_HPAD;
   if (g.dim >= 2 && H > 16) return;
   if (g.dim == 1 && H > 2048) return;
   auto* S = new StencilState();
@@ -1103,6 +1556,16 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   NLG_CUDA(cudaGetLastError());
   NLG_CUDA(cudaStreamSynchronize(P.stream));
   if (frac && g.dim == 3) S->box = boxfft_setup(P, d.alpha);
+  // column-lane apply: per-node horizons in 2-D / 3-D (NLG_ST_CY=0 keeps the row-lane sweep)
+  S->hs = std::min(H, static_cast<int>(std::floor(P.delta_max / g.h)) + 1);
+  if (frac && g.dim >= 2 && P.d_delta && !S->box) {
+    const char* ce = std::getenv("NLG_ST_CY");
+    const int warps = g.dim == 2 ? cy_warps<2>() : cy_warps<3>();
+    StArgs t = make_args(P, *S, 0, nullptr, nullptr);
+    S->cy = !(ce && std::atoi(ce) == 0) && cy_smem(t, g.dim) <= 200 * 1024 &&
+            (!P.d_kappa || cy_encode(&S->tmk, P.d_kappa, g.dim, g.n, g.in_end - g.in_begin, S->hs, warps)) &&
+            (g.n * 8) % 16 == 0;
+  }
   P.fast_method = 3;
 }
 
@@ -1127,6 +1590,7 @@ void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
         u, P.d_kappa, P.n_in, reinterpret_cast<double2*>(S->pack));
   }
   const StArgs a = make_args(P, *S, 0, u, out);
+  if (S->cy && launch_cy(*S, a, s)) return;
   launch(a, s, S->tab_bytes);
 }
 
@@ -1142,6 +1606,7 @@ void stencil_apply_rows(Plan& P, const double* u, double* out, int64_t a, int64_
   A.g.row_end = P.geom.row_begin + b;
   A.diag = S->diag + off;
   A.scale = S->scale ? S->scale + off : nullptr;
+  if (S->cy && launch_cy(*S, A, s)) return;
   launch(A, s, S->tab_bytes);
 }
 void stencil_box_in(Plan& P, const double* u, int64_t p0, int64_t p1, cudaStream_t s) {
@@ -1155,7 +1620,10 @@ int stencil_reach_rows(const Plan& P) { return P.st_state ? P.st_state->H : 0; }
 // output rows per CTA row of the sweep: row ranges cut at multiples of it keep
 // the CTA tiling (and so every warp's sweep range and summation order) of the
 // one-call apply, so a chunked apply is bit-identical to it
-int stencil_row_tile(const Plan& P) { return P.geom.dim == 2 ? kBY : 1; }
+int stencil_row_tile(const Plan& P) {
+  if (P.geom.dim != 2) return 1;
+  return P.st_state && P.st_state->cy ? std::max(kBY, cy_warps<2>() * kCyR) : kBY;
+}
 int stencil_components(const Plan& P) { return P.st_state ? (P.st_state->kind == 1 ? P.geom.dim : 1) : 1; }
 
 void stencil_free(Plan& P) {
