@@ -49,6 +49,7 @@ struct StencilState {
   bool cy = false;
   int hs = 0;                           // largest offset component any target includes
   CUtensorMap tmu, tmk;                 // boxes of the input planes of u (re-encoded when u moves) and kappa
+  CUtensorMap tmu1;                     // peridynamics: the second displacement component
   const double* tmu_base = nullptr;
 };
 
@@ -859,27 +860,46 @@ __global__ void __launch_bounds__(tile_bx<DIM, KIND>() * kBY / kRX, (kRX == 8 ? 
 // horizon) add their band afterwards from global memory with the reference's
 // float predicate.
 #ifndef NLG_CY_R
-#define NLG_CY_R 16
+#define NLG_CY_R 8
 #endif
-constexpr int kCyR = NLG_CY_R;          // targets per lane: 16 (5 ring phases) or 8 (3)
+constexpr int kCyR = NLG_CY_R;          // targets per lane: 16, 12 or 8 (5, 4, 3 ring phases)
 #ifndef NLG_CY_RING
-#define NLG_CY_RING 0
+#define NLG_CY_RING 1
 #endif
-#ifndef NLG_CY_MINB
-#define NLG_CY_MINB 1
+#ifndef NLG_CY_MINB2
+#define NLG_CY_MINB2 2                  // resident CTAs per SM the register budget allows (2-D, 3-D)
+#endif
+#ifndef NLG_CY_MINB3
+#define NLG_CY_MINB3 3
+#endif
+#ifndef NLG_CY_ONEVAR
+#define NLG_CY_ONEVAR 0                 // 1: every chunk through the per-target select (half the code)
 #endif
 #ifndef NLG_CY_W2
-#define NLG_CY_W2 4
+#define NLG_CY_W2 8
 #endif
 #ifndef NLG_CY_W3
-#define NLG_CY_W3 2
+#define NLG_CY_W3 4
+#endif
+#ifndef NLG_CYP_W
+#define NLG_CYP_W 4                     // peridynamic variant: warps per CTA, resident CTAs
+#endif
+#ifndef NLG_CYP_MINB
+#define NLG_CYP_MINB 3
 #endif
 template <int DIM>
 __host__ __device__ constexpr int cy_warps() { return DIM == 2 ? NLG_CY_W2 : NLG_CY_W3; }
-__host__ __device__ inline int cy_bw(int hs) { return 32 + 2 * hs; }
+inline int cy_warps_rt(int dim, int kind) { return kind == 1 ? NLG_CYP_W : (dim == 2 ? cy_warps<2>() : cy_warps<3>()); }
+// column halo rounded up to even: a box that starts at an odd column (a global address that is not a
+// multiple of 16 bytes) faults ("illegal instruction") on the B200
+__host__ __device__ inline int cy_hx(int hs) { return (hs + 1) & ~1; }
+__host__ __device__ inline int cy_bw(int hs) { return 32 + 2 * cy_hx(hs); }
 __host__ __device__ inline int cy_bhl(int hs, int warps) { return warps * kCyR + 2 * hs; }
-__host__ __device__ inline int cy_box(int hs, int warps) {     // doubles per box, 128-byte multiple
+__host__ __device__ inline int cy_box(int hs, int warps) {     // doubles per swept box (3 pad rows), 128-byte multiple
   return (cy_bw(hs) * (cy_bhl(hs, warps) + 3) + 15) & ~15;
+}
+__host__ __device__ inline int cy_mbox(int hs, int warps) {    // mirror-plane boxes (3-D): no pad rows
+  return (cy_bw(hs) * cy_bhl(hs, warps) + 15) & ~15;
 }
 
 __device__ __forceinline__ void cy_mbar_wait(unsigned mb, unsigned parity) {
@@ -905,7 +925,7 @@ __device__ __forceinline__ void cy_chunk(double (&a0)[kCyR], double (&a1)[kCyR],
     Wu[(kCyR + j + 4 * PH) % NW] = up[j * BW] + um[j * BW];
     if (KW) Wk[(kCyR + j + 4 * PH) % NW] = kp[j * BW] + km[j * BW];
   }
-  if (dy0 >= -YN && min(dy0 + 3, YW) <= YN) {   // every step of the chunk inside every target's ball
+  if (!NLG_CY_ONEVAR && dy0 >= -YN && min(dy0 + 3, YW) <= YN) {   // every step of the chunk inside every target's ball
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const double w = dy0 + s <= YW ? wk[s] : 0.0;   // overshoot steps of the last chunk
@@ -960,8 +980,10 @@ __device__ __forceinline__ void cy_sweep(double (&a0)[kCyR], double (&a1)[kCyR],
     NLG_CY_CHUNK(0)
     NLG_CY_CHUNK(1)
     NLG_CY_CHUNK(2)
-#if NLG_CY_R == 16
+#if NLG_CY_R >= 12
     NLG_CY_CHUNK(3)
+#endif
+#if NLG_CY_R >= 16
     NLG_CY_CHUNK(4)
 #endif
   }
@@ -979,7 +1001,7 @@ __device__ __forceinline__ void cy_sweep(double (&a0)[kCyR], double (&a1)[kCyR],
 }
 
 template <int DIM, bool KW>
-__global__ void __launch_bounds__(32 * cy_warps<DIM>(), NLG_CY_MINB)
+__global__ void __launch_bounds__(32 * cy_warps<DIM>(), DIM == 2 ? NLG_CY_MINB2 : NLG_CY_MINB3)
     stencil_cy_kernel(const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmk, StArgs a) {
   constexpr int NWP = cy_warps<DIM>(), NT = 32 * NWP, TY = NWP * kCyR;
   extern __shared__ __align__(128) double csm[];
@@ -987,14 +1009,14 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), NLG_CY_MINB)
   __shared__ int s_bmax;
   const Geom& g = a.g;
   const int H = a.H, hs = a.hs, BW = cy_bw(hs), BHl = cy_bhl(hs, NWP), BOX = cy_box(hs, NWP);
-  constexpr int NBOX = (KW ? 2 : 1) * (DIM == 3 ? 2 : 1);
   double* Tu = csm;
   double* Tk = KW ? csm + BOX : csm;
+  const int MBOX = cy_mbox(hs, NWP), hx = cy_hx(hs);
   double* Mu = csm + (KW ? 2 : 1) * BOX;                 // 3-D mirror planes
-  double* Mk = KW ? Mu + BOX : Mu;
+  double* Mk = KW ? Mu + MBOX : Mu;
   const int W1 = H + 1, wlen = W1 * a.ws;                // weight rows of one |dz|: [|dx|][dy + H]
-  double* wt = csm + NBOX * BOX;                          // two buffers in 3-D
-  int* isq = reinterpret_cast<int*>(wt + (DIM == 3 ? 2 : 1) * wlen);
+  double* wt = Mu + (DIM == 3 ? (KW ? 2 : 1) * MBOX : 0);   // (rewritten per |dz| behind the tile barrier)
+  int* isq = reinterpret_cast<int*>(wt + wlen);
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
   const int64_t n = g.n;
   int64_t x0, y0, z = 0;
@@ -1010,12 +1032,12 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), NLG_CY_MINB)
   const unsigned mb0 = static_cast<unsigned>(__cvta_generic_to_shared(mbar));
   const unsigned sTu = static_cast<unsigned>(__cvta_generic_to_shared(Tu));
   const unsigned sMu = static_cast<unsigned>(__cvta_generic_to_shared(Mu));
-  const unsigned BOXB = static_cast<unsigned>(sizeof(double)) * BOX;
   const unsigned BYTES = static_cast<unsigned>(sizeof(double)) * BW * BHl * (KW ? 2 : 1);
-  // boxes of one plane (u and kappa) -> dst, dst + BOX, completing on mbar[which]
+  // boxes of one plane (u and kappa) -> dst, dst + box stride, completing on mbar[which]
   auto issue = [&](unsigned dst, int which, int64_t gz) {
     const unsigned mb = mb0 + 8u * which;
-    const int cx = static_cast<int>(x0) - hs;
+    const unsigned BOXB = static_cast<unsigned>(sizeof(double)) * (which ? MBOX : BOX);
+    const int cx = static_cast<int>(x0) - hx;
     const int cy = static_cast<int>(DIM == 2 ? y0 - hs - g.in_begin : y0 - hs);
     const int cz = DIM == 2 ? 0 : static_cast<int>(gz - g.in_begin);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(BYTES) : "memory");
@@ -1058,6 +1080,19 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), NLG_CY_MINB)
   int M[kCyR];
   unsigned tiem = 0;
   int Mx = -1, Mn = 1 << 20;
+  // the epilogue's per-target operands into L2 now (one line per row and array, lanes 0 and 16)
+#ifndef NLG_CY_NOPF
+  if ((lane & 15) == 0 && ix < n) {
+    const int64_t shift = (g.row_begin - g.in_begin) * g.stride0;
+#pragma unroll
+    for (int r = 0; r < kCyR; ++r)
+      if (iy0 + r < ystop) {
+        const int64_t oi = in_index(iy0 + r) - shift;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.scale + oi));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.diag + oi));
+      }
+  }
+#endif
 #pragma unroll
   for (int r = 0; r < kCyR; ++r) {
     M[r] = -1;
@@ -1085,10 +1120,10 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), NLG_CY_MINB)
   double a0[kCyR], a1[kCyR];
 #pragma unroll
   for (int r = 0; r < kCyR; ++r) a0[r] = a1[r] = 0.0;
-  const int colbase = (wy * kCyR + hs) * BW + lane + hs;  // the lane's first target in the box
+  const int colbase = (wy * kCyR + hs) * BW + lane + hx;  // the lane's first target in the box
   for (int dz = 0; dz <= Rz; ++dz) {
     // weight rows of this |dz| (row dx = 0 halved: its column is added to itself)
-    double* wd = wt + (DIM == 3 ? (dz & 1) * wlen : 0);
+    double* wd = wt;
     {
       const double* src = a.tab + static_cast<size_t>(dz) * wlen;
       for (int i = tid; i < wlen; i += NT) wd[i] = (i < a.ws ? 0.5 : 1.0) * __ldg(src + i);
@@ -1214,6 +1249,253 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), NLG_CY_MINB)
       const int64_t oi = ii - (g.row_begin - g.in_begin) * g.stride0;
       const double X = KW ? fma(a.kappa[ii], a0[r], a1[r]) : a0[r];
       a.out[oi] = a.scale[oi] * (X - a.u[ii] * a.diag[oi]);
+    }
+  }
+}
+
+
+// ---- column-lane apply, 2-D peridynamics (cfg3): stencil_cyp_kernel -----------
+// Same blocking as stencil_cy_kernel. M(d) = d d^T / |d|^3: M00 and M11 are
+// even in dx and M01 is odd, so the columns +dx / -dx enter as sums for the
+// even entries and as differences for the odd one (half the FMAs of the
+// row-lane sweep, which cannot pair):
+//   out0 += M00 (u0+ + u0-) + M01 (u1+ - u1-),  out1 += M01 (u0+ - u0-) + M11 (u1+ + u1-),
+// one output component per pass (two windows of kCyR + 4 in registers).
+template <int PH>
+__device__ __forceinline__ void cyp_chunk(double (&acc)[kCyR], const int (&M)[kCyR], double (&Ws)[kCyR + 4],
+                                          double (&Wd)[kCyR + 4], const double*& sp, const double*& sm,
+                                          const double*& dp, const double*& dm, int BW, const double*& wa,
+                                          const double*& wb, int dy0, int YW, int YN, int c0) {
+  constexpr int NW = kCyR + 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    Ws[(kCyR + j + 4 * PH) % NW] = sp[j * BW] + sm[j * BW];
+    Wd[(kCyR + j + 4 * PH) % NW] = dp[j * BW] - dm[j * BW];
+  }
+  if (dy0 >= -YN && min(dy0 + 3, YW) <= YN) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const bool on = dy0 + s <= YW;
+      const double a = on ? wa[s] : 0.0, b = on ? wb[s] : 0.0;
+#pragma unroll
+      for (int r = 0; r < kCyR; ++r)
+        acc[r] = fma(a, Ws[(s + r + 4 * PH) % NW], fma(b, Wd[(s + r + 4 * PH) % NW], acc[r]));
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const double a = wa[s], b = wb[s];
+      const int c = c0 + (dy0 + s) * (dy0 + s);
+#pragma unroll
+      for (int r = 0; r < kCyR; ++r) {
+        const double t = fma(a, Ws[(s + r + 4 * PH) % NW], fma(b, Wd[(s + r + 4 * PH) % NW], acc[r]));
+        acc[r] = c <= M[r] ? t : acc[r];
+      }
+    }
+  }
+  sp += 4 * BW;
+  sm += 4 * BW;
+  dp += 4 * BW;
+  dm += 4 * BW;
+  wa += 4;
+  wb += 4;
+}
+
+__device__ __forceinline__ void cyp_sweep(double (&acc)[kCyR], const int (&M)[kCyR], const double* sp,
+                                          const double* sm, const double* dp, const double* dm, int BW,
+                                          const double* wa, const double* wb, int YW, int YN, int c0) {
+  double Ws[kCyR + 4], Wd[kCyR + 4];
+#pragma unroll
+  for (int i = 0; i < kCyR; ++i) {
+    Ws[i] = sp[i * BW] + sm[i * BW];
+    Wd[i] = dp[i * BW] - dm[i * BW];
+  }
+  sp += kCyR * BW;
+  sm += kCyR * BW;
+  dp += kCyR * BW;
+  dm += kCyR * BW;
+  const int nsteps = 2 * YW + 1;
+  int s0 = 0;
+#define NLG_CYP_CHUNK(PH)                                                             \
+  cyp_chunk<PH>(acc, M, Ws, Wd, sp, sm, dp, dm, BW, wa, wb, s0 - YW, YW, YN, c0);     \
+  s0 += 4;                                                                            \
+  if (s0 >= nsteps) break;
+  for (;;) {
+    NLG_CYP_CHUNK(0)
+    NLG_CYP_CHUNK(1)
+    NLG_CYP_CHUNK(2)
+#if NLG_CY_R >= 12
+    NLG_CYP_CHUNK(3)
+#endif
+#if NLG_CY_R >= 16
+    NLG_CYP_CHUNK(4)
+#endif
+  }
+#undef NLG_CYP_CHUNK
+}
+
+__global__ void __launch_bounds__(32 * NLG_CYP_W, NLG_CYP_MINB)
+    stencil_cyp_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1, StArgs a) {
+  constexpr int NWP = NLG_CYP_W, NT = 32 * NWP, TY = NWP * kCyR;
+  extern __shared__ __align__(128) double csm[];
+  __shared__ __align__(8) unsigned long long mbar;
+  const Geom& g = a.g;
+  const int H = a.H, hs = a.hs, BW = cy_bw(hs), BHl = cy_bhl(hs, NWP), BOX = cy_box(hs, NWP);
+  double* U0 = csm;
+  double* U1 = csm + BOX;
+  const int W1 = H + 1, wlen = W1 * a.ws;                // rows dx = 0..H of one table: [dx][dy + H]
+  double* wt = csm + 2 * BOX;                             // M11 | M01 | M00 of the table (= M00 | M01 | M11 transposed)
+  int* isq = reinterpret_cast<int*>(wt + 3 * wlen);
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+  const int64_t n = g.n;
+  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int64_t y0 = g.row_begin + static_cast<int64_t>(blockIdx.y) * TY;
+  const unsigned mb = static_cast<unsigned>(__cvta_generic_to_shared(&mbar));
+  if (tid == 0) {
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(U0));
+    const unsigned BYTES = static_cast<unsigned>(sizeof(double)) * BW * BHl * 2;
+    const int cx = static_cast<int>(x0) - cy_hx(hs), cy = static_cast<int>(y0 - hs - g.in_begin);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(BYTES) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(&tm0), "r"(cx), "r"(cy), "r"(0), "r"(mb)
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            dst + static_cast<unsigned>(sizeof(double)) * BOX),
+        "l"(&tm1), "r"(cx), "r"(cy), "r"(0), "r"(mb)
+        : "memory");
+  }
+  for (int i = tid; i < isq_len(H); i += NT) {
+    int x = static_cast<int>(sqrtf(static_cast<float>(i)));
+    while (x * x > i) --x;
+    while ((x + 1) * (x + 1) <= i) ++x;
+    isq[i] = x;
+  }
+  for (int i = tid; i < 3 * BW; i += NT) {
+    U0[BW * BHl + i] = 0.0;
+    U1[BW * BHl + i] = 0.0;
+  }
+  // table rows dx >= 0 (row H + dx of the signed table); the dx = 0 rows halved (their column is added to itself)
+  for (int i = tid; i < 3 * wlen; i += NT) {
+    const int t = i / wlen, k = i - t * wlen;
+    wt[i] = (k < a.ws ? 0.5 : 1.0) * __ldg(a.tab + static_cast<size_t>(t) * a.wp + static_cast<size_t>(H) * a.ws + k);
+  }
+  const int64_t ystop = g.row_end;
+  const int64_t ix = x0 + lane;
+  const int64_t iy0 = y0 + wy * kCyR;
+  const double inv_h = 1.0 / g.h;
+  const int64_t nin_total = (g.in_end - g.in_begin) * g.stride0;
+  const int64_t plane_out = (g.row_end - g.row_begin) * n;
+  auto in_index = [&](int64_t iy) { return (iy - g.in_begin) * n + ix; };
+  int M[kCyR];
+  unsigned tiem = 0;
+  int Mx = -1, Mn = 1 << 20;
+  if ((lane & 15) == 0 && ix < n) {
+    const int64_t shift = (g.row_begin - g.in_begin) * g.stride0;
+#pragma unroll
+    for (int r = 0; r < kCyR; ++r)
+      if (iy0 + r < ystop) {
+        const int64_t oi = in_index(iy0 + r) - shift;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.scale + oi));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.diag + oi));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.diag + plane_out + oi));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.diag + 2 * plane_out + oi));
+      }
+  }
+#pragma unroll
+  for (int r = 0; r < kCyR; ++r) {
+    M[r] = -1;
+    const int64_t iy = iy0 + r;
+    if (ix < n && iy < ystop) {
+      const double e = a.delta[in_index(iy)] * inv_h, e2 = e * e;
+      const int mlo = static_cast<int>(ceil(e2 * (1.0 - tie_band_n(inv_h))));
+      const int mhi = static_cast<int>(floor(e2 * (1.0 + tie_band_n(inv_h))));
+      M[r] = mlo <= mhi ? mlo - 1 : mhi;
+      if (mlo <= mhi) tiem |= 1u << r;
+      Mn = min(Mn, M[r]);
+    }
+    Mx = max(Mx, M[r]);
+  }
+  const int MW = __reduce_max_sync(0xffffffffu, Mx);
+  const int MN = __reduce_min_sync(0xffffffffu, Mn);
+  double a0[kCyR], a1[kCyR];
+#pragma unroll
+  for (int r = 0; r < kCyR; ++r) a0[r] = a1[r] = 0.0;
+  __syncthreads();                                       // tables
+  cy_mbar_wait(mb, 0u);
+  const int colbase = (wy * kCyR + hs) * BW + lane + cy_hx(hs);
+  if (MW >= 0) {
+    const int XW = isq[MW];
+    const double* w11 = wt;                               // table 0: dy'^2 / r^3 read transposed = M11(dy, dx)... see below
+    const double* w01 = wt + wlen;
+    const double* w00 = wt + 2 * wlen;
+    // the table stores t0 = dy^2/r^3, t1 = dx dy/r^3, t2 = dx^2/r^3 at [dy + H][dx + H]; read at
+    // [dx + H][dy + H] they are M11, M01, M00 of the offset (dy, dx)
+    for (int dx = 0; dx <= XW; ++dx) {
+      const int c0 = dx * dx;
+      const int YW = isq[MW - c0];
+      const int YN = MN >= c0 && MN <= MW ? isq[MN - c0] : -1;
+      const int o = colbase - YW * BW, wo = dx * a.ws + H - YW;
+      cyp_sweep(a0, M, U0 + o + dx, U0 + o - dx, U1 + o + dx, U1 + o - dx, BW, w00 + wo, w01 + wo, YW, YN, c0);
+      cyp_sweep(a1, M, U1 + o + dx, U1 + o - dx, U0 + o + dx, U0 + o - dx, BW, w11 + wo, w01 + wo, YW, YN, c0);
+    }
+  }
+  // tie bands (rare): from global memory with the reference's float predicate
+  {
+    unsigned tm = tiem;
+    while (tm) {
+      const int rr = __ffs(tm) - 1;
+      tm &= tm - 1;
+      const int64_t iy = iy0 + rr;
+      const double delta = a.delta[in_index(iy)];
+      const double e = delta * inv_h, e2 = e * e;
+      const int mlo = static_cast<int>(ceil(e2 * (1.0 - tie_band_n(inv_h))));
+      const int mhi = static_cast<int>(floor(e2 * (1.0 + tie_band_n(inv_h))));
+      const int64_t ki[3] = {iy, ix, 0};
+      const int Ry = isqrt_floor(mhi);
+      double t0 = 0.0, t1 = 0.0;
+      for (int dy = -Ry; dy <= Ry; ++dy) {
+        const int X = isqrt_floor(mhi - dy * dy);
+        const int m = dy * dy + X * X;
+        if (m < mlo || m == 0) continue;
+        for (int sx = -X; sx <= X; sx += (X > 0 ? 2 * X : 1)) {
+          const int d[2] = {dy, sx};
+          if (!point_in<2>(ki, d, g.h, delta)) continue;
+          const int64_t gy = iy + dy, gx = ix + sx;
+          if (gy < 0 || gy >= n || gx < 0 || gx >= n || gy < g.in_begin || gy >= g.in_end) continue;
+          const int64_t k = (gy - g.in_begin) * n + gx;
+          const int t = (dy + H) * a.ws + sx + H;
+          const double mxx = __ldg(a.tab + t), mxy = __ldg(a.tab + a.wp + t), myy = __ldg(a.tab + 2 * a.wp + t);
+          const double vx = a.u[k], vy = a.u[nin_total + k];
+          t0 = fma(mxx, vx, fma(mxy, vy, t0));
+          t1 = fma(mxy, vx, fma(myy, vy, t1));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kCyR; ++r) {
+        if (r == rr) {
+          a0[r] += t0;
+          a1[r] += t1;
+        }
+      }
+    }
+  }
+  if (ix >= n) return;
+#pragma unroll
+  for (int r = 0; r < kCyR; ++r) {
+    const int64_t iy = iy0 + r;
+    if (iy < ystop) {
+      const int64_t ii = in_index(iy);
+      const int64_t oi = ii - (g.row_begin - g.in_begin) * g.stride0;
+      const double ux = a.u[ii], uy = a.u[nin_total + ii];
+      const double dxx = a.diag[oi], dxy = a.diag[plane_out + oi], dyy = a.diag[2 * plane_out + oi];
+      const double sc = a.scale[oi];
+      a.out[oi] = sc * (a0[r] - (dxx * ux + dxy * uy));
+      a.out[plane_out + oi] = sc * (a1[r] - (dxy * ux + dyy * uy));
     }
   }
 }
@@ -1393,10 +1675,10 @@ bool cy_encode(CUtensorMap* m, const double* base, int dim, int64_t n, int64_t r
 }
 
 size_t cy_smem(const StArgs& a, int dim) {
-  const int warps = dim == 2 ? cy_warps<2>() : cy_warps<3>();
-  const int nbox = (a.kw ? 2 : 1) * (dim == 3 ? 2 : 1);
-  const size_t wlen = static_cast<size_t>(a.H + 1) * a.ws;
-  return sizeof(double) * (static_cast<size_t>(nbox) * cy_box(a.hs, warps) + (dim == 3 ? 2 : 1) * wlen) +
+  const int warps = cy_warps_rt(dim, a.kind);
+  const int nf = a.kind == 1 ? 2 : (a.kw ? 2 : 1);
+  const size_t wlen = static_cast<size_t>(a.H + 1) * a.ws * (a.kind == 1 ? 3 : 1);
+  return sizeof(double) * (static_cast<size_t>(nf) * (cy_box(a.hs, warps) + (dim == 3 ? cy_mbox(a.hs, warps) : 0)) + wlen) +
          sizeof(int) * (isq_len(a.H) + 1);
 }
 
@@ -1404,12 +1686,19 @@ size_t cy_smem(const StArgs& a, int dim) {
 bool launch_cy(StencilState& S, const StArgs& a, cudaStream_t s) {
   const int dim = a.g.dim;
   const int64_t n = a.g.n, rows_in = a.g.in_end - a.g.in_begin;
-  const int warps = dim == 2 ? cy_warps<2>() : cy_warps<3>();
+  const int warps = cy_warps_rt(dim, a.kind);
   if (S.tmu_base != a.u) {
     if (!cy_encode(&S.tmu, a.u, dim, n, rows_in, S.hs, warps)) return false;
+    if (a.kind == 1 && !cy_encode(&S.tmu1, a.u + rows_in * a.g.stride0, dim, n, rows_in, S.hs, warps)) return false;
     S.tmu_base = a.u;
   }
   const size_t sb = cy_smem(a, dim);
+  if (a.kind == 1) {
+    dim3 grid(static_cast<unsigned>((n + 31) / 32),
+              static_cast<unsigned>((a.g.row_end - a.g.row_begin + warps * kCyR - 1) / (warps * kCyR)));
+    stencil_cyp_kernel<<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu1, a);
+    return true;
+  }
   if (dim == 2) {
     dim3 grid(static_cast<unsigned>((n + 31) / 32),
               static_cast<unsigned>((a.g.row_end - a.g.row_begin + warps * kCyR - 1) / (warps * kCyR)));
@@ -1466,6 +1755,7 @@ void allow_smem() {
   smem_attr(stencil_cy_kernel<2, false>);
   smem_attr(stencil_cy_kernel<3, true>);
   smem_attr(stencil_cy_kernel<3, false>);
+  smem_attr(stencil_cyp_kernel);
   smem_attr(stencil1d_kernel<true, 1>);
   smem_attr(stencil1d_kernel<false, 1>);
   smem_attr(stencil1d_kernel<true, 8>);
@@ -1557,10 +1847,19 @@ void stencil_setup(Plan& P, const nlg_desc& d) {
   NLG_CUDA(cudaStreamSynchronize(P.stream));
   if (frac && g.dim == 3) S->box = boxfft_setup(P, d.alpha);
   // column-lane apply: per-node horizons in 2-D / 3-D (NLG_ST_CY=0 keeps the row-lane sweep)
-  S->hs = std::min(H, static_cast<int>(std::floor(P.delta_max / g.h)) + 1);
-  if (frac && g.dim >= 2 && P.d_delta && !S->box) {
+  {   // the largest |d|^2 any target can include (its tie band counted), with a margin on the host rounding
+    const double e = P.delta_max / g.h, m = std::floor(e * e * (1.0 + tie_band(g.h)) * (1.0 + 1e-9));
+    int r = static_cast<int>(std::sqrt(m));
+    while (static_cast<double>(r) * r > m) --r;
+    while (static_cast<double>(r + 1) * (r + 1) <= m) ++r;
+    S->hs = std::min(H, r);
+#ifdef NLG_CY_HSOLD
+    S->hs = H;
+#endif
+  }
+  if ((frac || peri) && g.dim >= 2 && P.d_delta && !S->box) {
     const char* ce = std::getenv("NLG_ST_CY");
-    const int warps = g.dim == 2 ? cy_warps<2>() : cy_warps<3>();
+    const int warps = cy_warps_rt(g.dim, S->kind);
     StArgs t = make_args(P, *S, 0, nullptr, nullptr);
     S->cy = !(ce && std::atoi(ce) == 0) && cy_smem(t, g.dim) <= 200 * 1024 &&
             (!P.d_kappa || cy_encode(&S->tmk, P.d_kappa, g.dim, g.n, g.in_end - g.in_begin, S->hs, warps)) &&
