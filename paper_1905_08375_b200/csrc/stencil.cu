@@ -875,6 +875,9 @@ constexpr int kCyR = NLG_CY_R;          // targets per lane: 16, 12 or 8 (5, 4, 
 #ifndef NLG_CY_ONEVAR
 #define NLG_CY_ONEVAR 0                 // 1: every chunk through the per-target select (half the code)
 #endif
+#ifndef NLG_CY_STEPSEL
+#define NLG_CY_STEPSEL 0                // 1: plain / selected FMAs decided per step (YN carries M_N) instead of per chunk
+#endif
 #ifndef NLG_CY_W2
 #define NLG_CY_W2 8
 #endif
@@ -885,7 +888,7 @@ constexpr int kCyR = NLG_CY_R;          // targets per lane: 16, 12 or 8 (5, 4, 
 #define NLG_CYP_W 4                     // peridynamic variant: warps per CTA, resident CTAs
 #endif
 #ifndef NLG_CYP_MINB
-#define NLG_CYP_MINB 3
+#define NLG_CYP_MINB 4
 #endif
 template <int DIM>
 __host__ __device__ constexpr int cy_warps() { return DIM == 2 ? NLG_CY_W2 : NLG_CY_W3; }
@@ -925,6 +928,30 @@ __device__ __forceinline__ void cy_chunk(double (&a0)[kCyR], double (&a1)[kCyR],
     Wu[(kCyR + j + 4 * PH) % NW] = up[j * BW] + um[j * BW];
     if (KW) Wk[(kCyR + j + 4 * PH) % NW] = kp[j * BW] + km[j * BW];
   }
+#if NLG_CY_STEPSEL
+  // per step: every target of the warp includes it (|d|^2 <= M_N: plain FMAs) or the weight is
+  // selected to zero per target (overshoot steps of the last chunk have |d|^2 > M_W: all zero)
+  (void)YW;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const double w = wk[s];
+    const int c = c0 + (dy0 + s) * (dy0 + s);
+    if (c <= YN) {
+#pragma unroll
+      for (int r = 0; r < kCyR; ++r) {
+        a0[r] = fma(w, Wu[(s + r + 4 * PH) % NW], a0[r]);
+        if (KW) a1[r] = fma(w, Wk[(s + r + 4 * PH) % NW], a1[r]);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < kCyR; ++r) {
+        const double wr = c <= M[r] ? w : 0.0;
+        a0[r] = fma(wr, Wu[(s + r + 4 * PH) % NW], a0[r]);
+        if (KW) a1[r] = fma(wr, Wk[(s + r + 4 * PH) % NW], a1[r]);
+      }
+    }
+  }
+#else
   if (!NLG_CY_ONEVAR && dy0 >= -YN && min(dy0 + 3, YW) <= YN) {   // every step of the chunk inside every target's ball
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
@@ -948,6 +975,7 @@ __device__ __forceinline__ void cy_chunk(double (&a0)[kCyR], double (&a1)[kCyR],
       }
     }
   }
+#endif
   up += 4 * BW;
   um += 4 * BW;
   kp += 4 * BW;
@@ -1174,7 +1202,11 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), DIM == 2 ? NLG_CY_MINB2 
       for (int dx = 0; dx <= XW; ++dx) {
         const int c0 = c00 + dx * dx;
         const int YW = isq[MW - c0];
+#if NLG_CY_STEPSEL
+        const int YN = MN <= MW ? MN : -1;
+#else
         const int YN = MN >= c0 && MN <= MW ? isq[MN - c0] : -1;
+#endif
         const int o = colbase - YW * BW;
         cy_sweep<KW>(a0, a1, M, Tu + o + dx, Tu + o - dx, Tk + o + dx, Tk + o - dx, BW, wd + dx * a.ws + H - YW, YW, YN,
                      c0);
@@ -1440,8 +1472,21 @@ __global__ void __launch_bounds__(32 * NLG_CYP_W, NLG_CYP_MINB)
       const int YW = isq[MW - c0];
       const int YN = MN >= c0 && MN <= MW ? isq[MN - c0] : -1;
       const int o = colbase - YW * BW, wo = dx * a.ws + H - YW;
-      cyp_sweep(a0, M, U0 + o + dx, U0 + o - dx, U1 + o + dx, U1 + o - dx, BW, w00 + wo, w01 + wo, YW, YN, c0);
-      cyp_sweep(a1, M, U1 + o + dx, U1 + o - dx, U0 + o + dx, U0 + o - dx, BW, w11 + wo, w01 + wo, YW, YN, c0);
+      // one inlined sweep for both output components: pass 0 sums into a0 (even entry M00 on u0, odd on u1),
+      // pass 1 into a1 (M11 on u1, odd on u0); the accumulator arrays trade places after each pass
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        const double* S = pass ? U1 : U0;
+        const double* D = pass ? U0 : U1;
+        cyp_sweep(a0, M, S + o + dx, S + o - dx, D + o + dx, D + o - dx, BW, (pass ? w11 : w00) + wo, w01 + wo, YW, YN,
+                  c0);
+#pragma unroll
+        for (int r = 0; r < kCyR; ++r) {
+          const double t = a0[r];
+          a0[r] = a1[r];
+          a1[r] = t;
+        }
+      }
     }
   }
   // tie bands (rare): from global memory with the reference's float predicate
