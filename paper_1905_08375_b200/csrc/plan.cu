@@ -329,15 +329,14 @@ void fast_dev(Plan& P, const double* u, double* out, cudaStream_t s) {
   ++P.fast_applies;
 }
 
-// The chunked host pipeline of nlg_apply_fast: 2-D / 3-D scalar stencil and
-// box-FFT plans of at least 4 Mi nodes. Input rows travel H2D in chunks on one
+// The chunked host pipeline of nlg_apply_fast: 2-D / 3-D stencil (scalar and
+// peridynamic) and box-FFT plans of at least 4 Mi nodes. Input rows travel H2D in chunks on one
 // copy stream; each output row range is computed as soon as every input row
 // it reads (H rows either side) is resident, and travels D2H on a second copy
 // stream while the next chunks copy in and compute: PCIe in, PCIe out and the
 // apply overlap instead of running back to back.
 bool pipelinable(const Plan& P) {
-  return P.fast_method == 3 && P.geom.dim >= 2 && components(P) == 1 && P.n_out >= (int64_t{1} << 22) &&
-         stencil_reach_rows(P) > 0;
+  return P.fast_method == 3 && P.geom.dim >= 2 && P.n_out >= (int64_t{1} << 22) && stencil_reach_rows(P) > 0;
 }
 
 void apply_fast_pipelined(Plan& P, const double* u, double* out) {
@@ -345,6 +344,7 @@ void apply_fast_pipelined(Plan& P, const double* u, double* out) {
   const int64_t st = g.stride0, rows_in = g.in_end - g.in_begin, rows_out = g.row_end - g.row_begin;
   const int64_t H = stencil_reach_rows(P);
   const bool box = stencil_box(P);
+  const int nc = components(P);
   static const int env_chunks = [] { const char* e = std::getenv("NLG_PIPE_CHUNKS"); return e ? std::atoi(e) : 0; }();
   const int nch = static_cast<int>(std::min<int64_t>(env_chunks > 0 ? env_chunks : (box ? 24 : 16), rows_in));
   if (!P.h2d_stream) {
@@ -359,8 +359,9 @@ void apply_fast_pipelined(Plan& P, const double* u, double* out) {
   int64_t q_done = 0;
   for (int k = 0; k < nch; ++k) {
     const int64_t i0 = rows_in * k / nch, i1 = rows_in * (k + 1) / nch;
-    NLG_CUDA(cudaMemcpyAsync(P.d_u + i0 * st, u + i0 * st, sizeof(double) * (i1 - i0) * st, cudaMemcpyHostToDevice,
-                             P.h2d_stream));
+    for (int c = 0; c < nc; ++c)   // (peridynamics: one row chunk per component plane)
+      NLG_CUDA(cudaMemcpyAsync(P.d_u + c * P.n_in + i0 * st, u + c * P.n_in + i0 * st, sizeof(double) * (i1 - i0) * st,
+                               cudaMemcpyHostToDevice, P.h2d_stream));
     NLG_CUDA(cudaEventRecord(P.pipe_ev[k], P.h2d_stream));
     NLG_CUDA(cudaStreamWaitEvent(P.stream, P.pipe_ev[k], 0));
     if (box) stencil_box_in(P, P.d_u, i0, i1, P.stream);
@@ -381,8 +382,9 @@ void apply_fast_pipelined(Plan& P, const double* u, double* out) {
     NLG_CUDA(cudaGetLastError());
     NLG_CUDA(cudaEventRecord(P.pipe_ev[nch + k], P.stream));
     NLG_CUDA(cudaStreamWaitEvent(P.d2h_stream, P.pipe_ev[nch + k], 0));
-    NLG_CUDA(cudaMemcpyAsync(out + q_done * st, P.d_out + q_done * st, sizeof(double) * (q_ready - q_done) * st,
-                             cudaMemcpyDeviceToHost, P.d2h_stream));
+    for (int c = 0; c < nc; ++c)
+      NLG_CUDA(cudaMemcpyAsync(out + c * P.n_out + q_done * st, P.d_out + c * P.n_out + q_done * st,
+                               sizeof(double) * (q_ready - q_done) * st, cudaMemcpyDeviceToHost, P.d2h_stream));
     q_done = q_ready;
   }
   NLG_CUDA(cudaStreamSynchronize(P.d2h_stream));

@@ -61,6 +61,7 @@ struct StArgs {
   Geom g;
   int kind, kw, collar, mode, H;
   int hs;                 // column-lane apply: box halo
+  int64_t plane_out;      // stride between the component planes of out / diag (the plan's n_out, also for row ranges)
   const double* u;        // [comps][n_in]
   const double2* pk;      // (u, kappa u) when kw
   const double* delta;
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kTX * kTY) stencil_kernel(StArgs a) {
     }
   }
   if (!live) return;
-  const int64_t nout = (g.row_end - g.row_begin) * g.stride0;
+  const int64_t nout = a.plane_out;
   if (KIND == 0) {
     if (MODE == 1) {
       a.out[oi] = acc0;
@@ -513,7 +514,7 @@ __global__ void __launch_bounds__(tile_bx<DIM, KIND>() * kBY / kRX, (kRX == 8 ? 
   if (DIM == 3 && yok && x0 + kRX * tx < n) {
     const int64_t i0 = in_index(x0 + kRX * tx), o0 = i0 - (g.row_begin - g.in_begin) * g.stride0;
     const int64_t last = min(static_cast<int64_t>(kRX - 1), n - 1 - (x0 + kRX * tx));
-    const int64_t pout = (g.row_end - g.row_begin) * g.stride0;
+    const int64_t pout = a.plane_out;
     auto pf = [](const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); };
     for (int64_t e : {int64_t(0), last}) {
       pf(a.u + i0 + e);
@@ -821,7 +822,7 @@ __global__ void __launch_bounds__(tile_bx<DIM, KIND>() * kBY / kRX, (kRX == 8 ? 
     }
   }
   if (!yok) return;
-  const int64_t plane_out = DIM == 2 ? (g.row_end - g.row_begin) * n : (g.row_end - g.row_begin) * n * n;
+  const int64_t plane_out = a.plane_out;
 #pragma unroll
   for (int r = 0; r < kRX; ++r) {
     const int64_t ix = x0 + kRX * tx + r;
@@ -1421,7 +1422,7 @@ __global__ void __launch_bounds__(32 * NLG_CYP_W, NLG_CYP_MINB)
   const int64_t iy0 = y0 + wy * kCyR;
   const double inv_h = 1.0 / g.h;
   const int64_t nin_total = (g.in_end - g.in_begin) * g.stride0;
-  const int64_t plane_out = (g.row_end - g.row_begin) * n;
+  const int64_t plane_out = a.plane_out;
   auto in_index = [&](int64_t iy) { return (iy - g.in_begin) * n + ix; };
   int M[kCyR];
   unsigned tiem = 0;
@@ -1767,6 +1768,7 @@ StArgs make_args(const Plan& P, const StencilState& S, int mode, const double* u
   a.mode = mode;
   a.H = S.H;
   a.hs = S.hs;
+  a.plane_out = P.n_out;
   a.u = u;
   a.pk = reinterpret_cast<const double2*>(S.pack);
   a.delta = P.d_delta;
@@ -1939,8 +1941,9 @@ void stencil_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
 }
 
 // Row-range pieces of the apply (the chunked host pipeline of nlg_apply_fast).
-// Output rows [a, b) relative to row_begin; u covers the plan's input rows.
-// Scalar operators only (the peridynamic planes are strided by n_out).
+// Output rows [a, b) relative to row_begin; u covers the plan's input rows
+// (peridynamics: the component planes of u / out / diag stay strided by the
+// plan's n_in / n_out).
 void stencil_apply_rows(Plan& P, const double* u, double* out, int64_t a, int64_t b, cudaStream_t s) {
   StencilState* S = P.st_state;
   if (b <= a) return;

@@ -70,6 +70,25 @@ def test_pipeline_stencil_2d_bitwise(N):
     assert np.array_equal(host, dev)
 
 
+def test_pipeline_peridynamic_2d_bitwise(N):
+    """2-D peridynamics (cfg3 family, two component planes) at 2048^2: the row
+    chunks of both planes travel and are computed per output row range."""
+    import torch
+    from paper_1905_08375_b200 import configs
+    w = configs.cfg3(2048)
+    op = N.NonlocalOperator(2, 2048, **w.op_kwargs())
+    host = op.apply(w.u)
+    plan = op.plan
+    ud = torch.from_numpy(w.u).cuda()
+    od = torch.empty(2 * plan.n_out, dtype=torch.float64, device="cuda")
+    plan.apply_fast_dev(ud.data_ptr(), od.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(host, od.cpu().numpy())
+    tg = np.random.default_rng(3).choice(2048 ** 2, 512, replace=False)
+    ref = op.apply_direct_at(w.u, tg)
+    assert np.max(np.abs(host.reshape(2, -1)[:, tg].reshape(-1) - ref)) <= 1e-10 * np.max(np.abs(ref))
+
+
 def test_pipeline_stencil_3d_variable_bitwise(N):
     """3-D variable horizon (cfg4-B family) at 168^3."""
     from paper_1905_08375_b200 import configs
