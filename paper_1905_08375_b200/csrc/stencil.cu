@@ -891,6 +891,8 @@ constexpr int kCyR = NLG_CY_R;          // targets per lane: 16, 12 or 8 (5, 4, 
 #ifndef NLG_CYP_MINB
 #define NLG_CYP_MINB 4
 #endif
+// box row pitches with their own instantiation: the BASELINE reaches (cfg2: 11 -> 56, cfg4-B: 7 -> 48, cfg3: 8 -> 48)
+constexpr int kCyBW2 = 56, kCyBW3 = 48, kCyBWp = 48;
 template <int DIM>
 __host__ __device__ constexpr int cy_warps() { return DIM == 2 ? NLG_CY_W2 : NLG_CY_W3; }
 inline int cy_warps_rt(int dim, int kind) { return kind == 1 ? NLG_CYP_W : (dim == 2 ? cy_warps<2>() : cy_warps<3>()); }
@@ -918,12 +920,15 @@ __device__ __forceinline__ void cy_mbar_wait(unsigned mb, unsigned parity) {
 // window of kCyR + 4 sources per field lives in registers as a ring: chunk
 // number PH (mod 5) finds logical element i at (i + 4 PH) mod (kCyR + 4), so
 // sliding by four costs no register moves.
-template <bool KW, int PH>
+// BWC: the row pitch of the box as a compile-time constant (the BASELINE reaches: every window load
+// then carries its row offset as an immediate), 0: the run-time pitch bw_rt
+template <bool KW, int PH, int BWC>
 __device__ __forceinline__ void cy_chunk(double (&a0)[kCyR], double (&a1)[kCyR], const int (&M)[kCyR],
                                          double (&Wu)[kCyR + 4], double (&Wk)[kCyR + 4], const double*& up,
-                                         const double*& um, const double*& kp, const double*& km, int BW,
+                                         const double*& um, const double*& kp, const double*& km, int bw_rt,
                                          const double*& wk, int dy0, int YW, int YN, int c0) {
   constexpr int NW = kCyR + 4;
+  const int BW = BWC ? BWC : bw_rt;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     Wu[(kCyR + j + 4 * PH) % NW] = up[j * BW] + um[j * BW];
@@ -984,10 +989,11 @@ __device__ __forceinline__ void cy_chunk(double (&a0)[kCyR], double (&a1)[kCyR],
   wk += 4;
 }
 
-template <bool KW>
+template <bool KW, int BWC>
 __device__ __forceinline__ void cy_sweep(double (&a0)[kCyR], double (&a1)[kCyR], const int (&M)[kCyR],
                                          const double* up, const double* um, const double* kp, const double* km,
-                                         int BW, const double* wk, int YW, int YN, int c0) {
+                                         int bw_rt, const double* wk, int YW, int YN, int c0) {
+  const int BW = BWC ? BWC : bw_rt;
   double Wu[kCyR + 4], Wk[kCyR + 4];
 #pragma unroll
   for (int i = 0; i < kCyR; ++i) {
@@ -1001,7 +1007,7 @@ __device__ __forceinline__ void cy_sweep(double (&a0)[kCyR], double (&a1)[kCyR],
   const int nsteps = 2 * YW + 1;
   int s0 = 0;
 #define NLG_CY_CHUNK(PH)                                                                   \
-  cy_chunk<KW, PH>(a0, a1, M, Wu, Wk, up, um, kp, km, BW, wk, s0 - YW, YW, YN, c0);        \
+  cy_chunk<KW, PH, BWC>(a0, a1, M, Wu, Wk, up, um, kp, km, BW, wk, s0 - YW, YW, YN, c0);   \
   s0 += 4;                                                                                 \
   if (s0 >= nsteps) break;
 #if NLG_CY_RING
@@ -1029,7 +1035,7 @@ __device__ __forceinline__ void cy_sweep(double (&a0)[kCyR], double (&a1)[kCyR],
 #undef NLG_CY_CHUNK
 }
 
-template <int DIM, bool KW>
+template <int DIM, bool KW, int BWC>
 __global__ void __launch_bounds__(32 * cy_warps<DIM>(), DIM == 2 ? NLG_CY_MINB2 : NLG_CY_MINB3)
     stencil_cy_kernel(const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmk, StArgs a) {
   constexpr int NWP = cy_warps<DIM>(), NT = 32 * NWP, TY = NWP * kCyR;
@@ -1037,7 +1043,7 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), DIM == 2 ? NLG_CY_MINB2 
   __shared__ __align__(8) unsigned long long mbar[2];
   __shared__ int s_bmax;
   const Geom& g = a.g;
-  const int H = a.H, hs = a.hs, BW = cy_bw(hs), BHl = cy_bhl(hs, NWP), BOX = cy_box(hs, NWP);
+  const int H = a.H, hs = a.hs, BW = BWC ? BWC : cy_bw(hs), BHl = cy_bhl(hs, NWP), BOX = cy_box(hs, NWP);
   double* Tu = csm;
   double* Tk = KW ? csm + BOX : csm;
   const int MBOX = cy_mbox(hs, NWP), hx = cy_hx(hs);
@@ -1209,8 +1215,8 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), DIM == 2 ? NLG_CY_MINB2 
         const int YN = MN >= c0 && MN <= MW ? isq[MN - c0] : -1;
 #endif
         const int o = colbase - YW * BW;
-        cy_sweep<KW>(a0, a1, M, Tu + o + dx, Tu + o - dx, Tk + o + dx, Tk + o - dx, BW, wd + dx * a.ws + H - YW, YW, YN,
-                     c0);
+        cy_sweep<KW, BWC>(a0, a1, M, Tu + o + dx, Tu + o - dx, Tk + o + dx, Tk + o - dx, BW, wd + dx * a.ws + H - YW, YW,
+                          YN, c0);
       }
     }
     if (DIM == 3 && dz + 1 <= Rz) {
@@ -1294,12 +1300,13 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), DIM == 2 ? NLG_CY_MINB2 
 // row-lane sweep, which cannot pair):
 //   out0 += M00 (u0+ + u0-) + M01 (u1+ - u1-),  out1 += M01 (u0+ - u0-) + M11 (u1+ + u1-),
 // one output component per pass (two windows of kCyR + 4 in registers).
-template <int PH>
+template <int PH, int BWC>
 __device__ __forceinline__ void cyp_chunk(double (&acc)[kCyR], const int (&M)[kCyR], double (&Ws)[kCyR + 4],
                                           double (&Wd)[kCyR + 4], const double*& sp, const double*& sm,
-                                          const double*& dp, const double*& dm, int BW, const double*& wa,
+                                          const double*& dp, const double*& dm, int bw_rt, const double*& wa,
                                           const double*& wb, int dy0, int YW, int YN, int c0) {
   constexpr int NW = kCyR + 4;
+  const int BW = BWC ? BWC : bw_rt;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     Ws[(kCyR + j + 4 * PH) % NW] = sp[j * BW] + sm[j * BW];
@@ -1334,9 +1341,11 @@ __device__ __forceinline__ void cyp_chunk(double (&acc)[kCyR], const int (&M)[kC
   wb += 4;
 }
 
+template <int BWC>
 __device__ __forceinline__ void cyp_sweep(double (&acc)[kCyR], const int (&M)[kCyR], const double* sp,
-                                          const double* sm, const double* dp, const double* dm, int BW,
+                                          const double* sm, const double* dp, const double* dm, int bw_rt,
                                           const double* wa, const double* wb, int YW, int YN, int c0) {
+  const int BW = BWC ? BWC : bw_rt;
   double Ws[kCyR + 4], Wd[kCyR + 4];
 #pragma unroll
   for (int i = 0; i < kCyR; ++i) {
@@ -1350,7 +1359,7 @@ __device__ __forceinline__ void cyp_sweep(double (&acc)[kCyR], const int (&M)[kC
   const int nsteps = 2 * YW + 1;
   int s0 = 0;
 #define NLG_CYP_CHUNK(PH)                                                             \
-  cyp_chunk<PH>(acc, M, Ws, Wd, sp, sm, dp, dm, BW, wa, wb, s0 - YW, YW, YN, c0);     \
+  cyp_chunk<PH, BWC>(acc, M, Ws, Wd, sp, sm, dp, dm, BW, wa, wb, s0 - YW, YW, YN, c0);  \
   s0 += 4;                                                                            \
   if (s0 >= nsteps) break;
   for (;;) {
@@ -1367,13 +1376,14 @@ __device__ __forceinline__ void cyp_sweep(double (&acc)[kCyR], const int (&M)[kC
 #undef NLG_CYP_CHUNK
 }
 
+template <int BWC>
 __global__ void __launch_bounds__(32 * NLG_CYP_W, NLG_CYP_MINB)
     stencil_cyp_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1, StArgs a) {
   constexpr int NWP = NLG_CYP_W, NT = 32 * NWP, TY = NWP * kCyR;
   extern __shared__ __align__(128) double csm[];
   __shared__ __align__(8) unsigned long long mbar;
   const Geom& g = a.g;
-  const int H = a.H, hs = a.hs, BW = cy_bw(hs), BHl = cy_bhl(hs, NWP), BOX = cy_box(hs, NWP);
+  const int H = a.H, hs = a.hs, BW = BWC ? BWC : cy_bw(hs), BHl = cy_bhl(hs, NWP), BOX = cy_box(hs, NWP);
   double* U0 = csm;
   double* U1 = csm + BOX;
   const int W1 = H + 1, wlen = W1 * a.ws;                // rows dx = 0..H of one table: [dx][dy + H]
@@ -1479,8 +1489,8 @@ __global__ void __launch_bounds__(32 * NLG_CYP_W, NLG_CYP_MINB)
       for (int pass = 0; pass < 2; ++pass) {
         const double* S = pass ? U1 : U0;
         const double* D = pass ? U0 : U1;
-        cyp_sweep(a0, M, S + o + dx, S + o - dx, D + o + dx, D + o - dx, BW, (pass ? w11 : w00) + wo, w01 + wo, YW, YN,
-                  c0);
+        cyp_sweep<BWC>(a0, M, S + o + dx, S + o - dx, D + o + dx, D + o - dx, BW, (pass ? w11 : w00) + wo, w01 + wo, YW,
+                       YN, c0);
 #pragma unroll
         for (int r = 0; r < kCyR; ++r) {
           const double t = a0[r];
@@ -1739,22 +1749,34 @@ bool launch_cy(StencilState& S, const StArgs& a, cudaStream_t s) {
     S.tmu_base = a.u;
   }
   const size_t sb = cy_smem(a, dim);
+  const int bw = cy_bw(S.hs);
   if (a.kind == 1) {
     dim3 grid(static_cast<unsigned>((n + 31) / 32),
               static_cast<unsigned>((a.g.row_end - a.g.row_begin + warps * kCyR - 1) / (warps * kCyR)));
-    stencil_cyp_kernel<<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu1, a);
+    if (bw == kCyBWp) stencil_cyp_kernel<kCyBWp><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu1, a);
+    else stencil_cyp_kernel<0><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu1, a);
     return true;
   }
   if (dim == 2) {
     dim3 grid(static_cast<unsigned>((n + 31) / 32),
               static_cast<unsigned>((a.g.row_end - a.g.row_begin + warps * kCyR - 1) / (warps * kCyR)));
-    if (a.kw) stencil_cy_kernel<2, true><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmk, a);
-    else stencil_cy_kernel<2, false><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu, a);
+    if (bw == kCyBW2) {
+      if (a.kw) stencil_cy_kernel<2, true, kCyBW2><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmk, a);
+      else stencil_cy_kernel<2, false, kCyBW2><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu, a);
+    } else {
+      if (a.kw) stencil_cy_kernel<2, true, 0><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmk, a);
+      else stencil_cy_kernel<2, false, 0><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu, a);
+    }
   } else {
     const int64_t ntx = (n + 31) / 32, nty = (n + warps * kCyR - 1) / (warps * kCyR);
     dim3 grid(static_cast<unsigned>(a.g.row_end - a.g.row_begin), static_cast<unsigned>(ntx * nty));
-    if (a.kw) stencil_cy_kernel<3, true><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmk, a);
-    else stencil_cy_kernel<3, false><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu, a);
+    if (bw == kCyBW3) {
+      if (a.kw) stencil_cy_kernel<3, true, kCyBW3><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmk, a);
+      else stencil_cy_kernel<3, false, kCyBW3><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu, a);
+    } else {
+      if (a.kw) stencil_cy_kernel<3, true, 0><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmk, a);
+      else stencil_cy_kernel<3, false, 0><<<grid, 32 * warps, sb, s>>>(S.tmu, S.tmu, a);
+    }
   }
   return true;
 }
@@ -1798,11 +1820,16 @@ void allow_smem() {
   smem_attr(stencil_rb_kernel<2, 1, false, kR2Peri>);
   smem_attr(stencil_rb_kernel<3, 0, true, kR3Frac>);
   smem_attr(stencil_rb_kernel<3, 0, false, kR3Frac>);
-  smem_attr(stencil_cy_kernel<2, true>);
-  smem_attr(stencil_cy_kernel<2, false>);
-  smem_attr(stencil_cy_kernel<3, true>);
-  smem_attr(stencil_cy_kernel<3, false>);
-  smem_attr(stencil_cyp_kernel);
+  smem_attr(stencil_cy_kernel<2, true, 0>);
+  smem_attr(stencil_cy_kernel<2, false, 0>);
+  smem_attr(stencil_cy_kernel<3, true, 0>);
+  smem_attr(stencil_cy_kernel<3, false, 0>);
+  smem_attr(stencil_cy_kernel<2, true, kCyBW2>);
+  smem_attr(stencil_cy_kernel<2, false, kCyBW2>);
+  smem_attr(stencil_cy_kernel<3, true, kCyBW3>);
+  smem_attr(stencil_cy_kernel<3, false, kCyBW3>);
+  smem_attr(stencil_cyp_kernel<0>);
+  smem_attr(stencil_cyp_kernel<kCyBWp>);
   smem_attr(stencil1d_kernel<true, 1>);
   smem_attr(stencil1d_kernel<false, 1>);
   smem_attr(stencil1d_kernel<true, 8>);
