@@ -1,14 +1,15 @@
 """bench.py — fp64 nonlocal-apply throughput (BASELINE.json metric) on B200.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--extra cfg4b,cfg2,cfg3,cfg1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--extra cfg4b,cfg2,cfg3,cfg1,trunc1d,trunc2d]
                   [--impl ours|reference]
 
 One step = one fast apply of the whole workload with the inputs resident in
 HBM. The headline workload is the largest BASELINE configuration that fits one
 B200: configs[4] at 768^3 with the constant horizon delta = 6h (cfg4-A: 3-D,
 kappa-weighted fractional kernel, s = 0.25). cfg4-B (variable horizon), cfg2
-and cfg3 (2-D, 4096^2) and cfg1 (1-D, N = 2^22) are measured in the same run
-and carried under "extra".
+and cfg3 (2-D, 4096^2), cfg1 (1-D, N = 2^22) and the reference's own fast route
+(TruncatedOperator, K = 0: trunc1d at 2^22, trunc2d at 1024^2) are measured in
+the same run and carried under "extra".
 
 N > 1: one process per GPU. Without WORLD_SIZE in the environment bench.py
 re-launches itself under torch.distributed.run with N ranks (and fails loudly
@@ -573,7 +574,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="cfg4")
-    ap.add_argument("--extra", default="cfg4b,cfg2,cfg3,cfg1",
+    ap.add_argument("--extra", default="cfg4b,cfg2,cfg3,cfg1,trunc1d,trunc2d",
                     help="comma-separated workloads measured after the headline ('' for none)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstdlib>
+
 #include "plan.hpp"
 
 namespace nlg {
@@ -172,6 +174,7 @@ struct SpanArgs {
   const double *pref_hi, *pref_lo, *tot_hi, *tot_lo;
   double* out;
   int sym;   // n a power of two: exact coordinates, mirror-symmetric spans
+  int intspan;   // span extents from the integer classification (NLG_SPAN_INT=0: predicate probes)
 };
 
 // global exclusive prefix P(row, p) for p in [0, len] (P(len) = row total)
@@ -266,23 +269,73 @@ __global__ void __launch_bounds__(256) span_eval(SpanArgs a) {
   const int64_t hi0 = DIM > 1 ? min(ki[0] + W, g.n - 1) : 0;
   const int64_t lo1 = DIM > 2 ? max(ki[1] - W, int64_t(0)) : 0;
   const int64_t hi1 = DIM > 2 ? min(ki[1] + W, g.n - 1) : 0;
+  // Integer classification of a source at offset d (the stencils' scheme): Point rule |d|^2 against
+  // (delta/h)^2; Leaf rule 4 dmin / h^2 = sum_{d_a != 0} (2|d_a| - 1)^2 against (2 delta/h)^2 (the
+  // target is a cell centre, the nearest face of cell k lies (|d_a| - 1/2) h away). m < mlo is surely
+  // inside, m > mhi surely outside; only inside the tie band does the reference's float predicate
+  // decide, so a row's extent is one integer square root instead of a few fp64 predicate probes.
+  const double inv_h = 1.0 / h;
+  const double ecell = delta * inv_h;
+  const double E = a.rule == 1 ? ecell * ecell : 4.0 * ecell * ecell;
+  const int64_t mlo = static_cast<int64_t>(ceil(E * (1.0 - tie_band_n(inv_h))));
+  const int64_t mhi = static_cast<int64_t>(floor(E * (1.0 + tie_band_n(inv_h))));
+  auto term = [&](int64_t d) {   // contribution of one axis offset
+    d = d < 0 ? -d : d;
+    if (a.rule == 1) return d * d;
+    return d == 0 ? int64_t(0) : (2 * d - 1) * (2 * d - 1);
+  };
+  auto isqrt64 = [](int64_t m) {
+    int64_t r = static_cast<int64_t>(sqrt(static_cast<double>(m)));
+    while (r * r > m) --r;
+    while ((r + 1) * (r + 1) <= m) ++r;
+    return r;
+  };
   for (int64_t a0 = lo0; a0 <= hi0; ++a0) {
     for (int64_t a1 = lo1; a1 <= hi1; ++a1) {
       if (DIM > 1) k[0] = a0;
       if (DIM > 2) k[1] = a1;
       const int64_t kc = ki[DIM - 1];
       k[DIM - 1] = kc;
-      if (!member<DIM>(a.rule, k, x, h, delta, r2max)) continue;
-      // span estimate from the radius left for this row
-      double q = 0.0;
-      if (DIM > 1) { const double d = fabs(static_cast<double>(a0 - ki[0])); q += d * d; }
-      if (DIM > 2) { const double d = fabs(static_cast<double>(a1 - ki[1])); q += d * d; }
-      const int64_t est = static_cast<int64_t>(sqrt(fmax(rc * rc - q, 0.0)));
-      const int64_t er = span_extent<DIM>(a.rule, k, kc, +1, x, h, delta, r2max, est);
-      // n = 2^L: node coordinates and cell faces are exact dyadics, so the
-      // predicate is mirror-symmetric about the target's cell and the left
-      // extent equals the right one (half the probes)
-      const int64_t el = a.sym ? er : span_extent<DIM>(a.rule, k, kc, -1, x, h, delta, r2max, est);
+      int64_t er, el;
+      if (a.intspan) {
+        int64_t q = 0;
+        if (DIM > 1) q += term(a0 - ki[0]);
+        if (DIM > 2) q += term(a1 - ki[1]);
+        if (q > mhi) continue;
+        if (q >= mlo && !member<DIM>(a.rule, k, x, h, delta, r2max)) continue;
+        int64_t ein = 0;                       // largest e with q + term(e) < mlo
+        if (q < mlo) {
+          const int64_t t = isqrt64(mlo - 1 - q);
+          ein = a.rule == 1 ? t : (t + 1) / 2;
+        }
+        er = el = ein;
+        if (q + term(ein + 1) <= mhi) {        // tie band: the float predicate, each side on its own
+          for (;;) {
+            if (q + term(er + 1) > mhi) break;
+            k[DIM - 1] = kc + er + 1;
+            if (!member<DIM>(a.rule, k, x, h, delta, r2max)) break;
+            ++er;
+          }
+          for (;;) {
+            if (q + term(el + 1) > mhi) break;
+            k[DIM - 1] = kc - (el + 1);
+            if (!member<DIM>(a.rule, k, x, h, delta, r2max)) break;
+            ++el;
+          }
+        }
+      } else {
+        if (!member<DIM>(a.rule, k, x, h, delta, r2max)) continue;
+        // span estimate from the radius left for this row
+        double q = 0.0;
+        if (DIM > 1) { const double d = fabs(static_cast<double>(a0 - ki[0])); q += d * d; }
+        if (DIM > 2) { const double d = fabs(static_cast<double>(a1 - ki[1])); q += d * d; }
+        const int64_t est = static_cast<int64_t>(sqrt(fmax(rc * rc - q, 0.0)));
+        er = span_extent<DIM>(a.rule, k, kc, +1, x, h, delta, r2max, est);
+        // n = 2^L: node coordinates and cell faces are exact dyadics, so the
+        // predicate is mirror-symmetric about the target's cell and the left
+        // extent equals the right one (half the probes)
+        el = a.sym ? er : span_extent<DIM>(a.rule, k, kc, -1, x, h, delta, r2max, est);
+      }
       int64_t lo = kc - el, hi = kc + er;
       lo = max(lo, int64_t(0));
       hi = min(hi, g.n - 1);
@@ -568,6 +621,8 @@ void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   a.tot_lo = P.d_seg_lo;
   a.out = out;
   a.sym = (P.geom.n & (P.geom.n - 1)) == 0;
+  static const bool intspan = [] { const char* e = std::getenv("NLG_SPAN_INT"); return !(e && std::atoi(e) == 0); }();
+  a.intspan = intspan;
   const unsigned blocks = static_cast<unsigned>((P.n_out + 255) / 256);
   switch (P.geom.dim) {
     case 1: span_eval<1><<<blocks, 256, 0, s>>>(a); break;
