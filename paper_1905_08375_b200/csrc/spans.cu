@@ -16,6 +16,7 @@
 #include <vector>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "plan.hpp"
 
@@ -231,8 +232,12 @@ __device__ __forceinline__ int64_t span_extent(int rule, int64_t* k, int64_t kc,
   return e;
 }
 
-template <int DIM>
+// SMALL: (2 delta_max / h)^2 fits 32-bit integers (every 2-D / 3-D horizon of interest): the per-row
+// integer classification runs in int instead of int64_t (64-bit multiplies and compares are several
+// instructions each; the kernel is issue-bound)
+template <int DIM, bool SMALL>
 __global__ void __launch_bounds__(256) span_eval(SpanArgs a) {
+  using I = typename std::conditional<SMALL, int, int64_t>::type;
   const Geom& g = a.g;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nout = (g.row_end - g.row_begin) * g.stride0;
@@ -277,15 +282,16 @@ __global__ void __launch_bounds__(256) span_eval(SpanArgs a) {
   const double inv_h = 1.0 / h;
   const double ecell = delta * inv_h;
   const double E = a.rule == 1 ? ecell * ecell : 4.0 * ecell * ecell;
-  const int64_t mlo = static_cast<int64_t>(ceil(E * (1.0 - tie_band_n(inv_h))));
-  const int64_t mhi = static_cast<int64_t>(floor(E * (1.0 + tie_band_n(inv_h))));
-  auto term = [&](int64_t d) {   // contribution of one axis offset
+  const I mlo = static_cast<I>(ceil(E * (1.0 - tie_band_n(inv_h))));
+  const I mhi = static_cast<I>(floor(E * (1.0 + tie_band_n(inv_h))));
+  const bool point = a.rule == 1;
+  auto term = [&](I d) {   // contribution of one axis offset
     d = d < 0 ? -d : d;
-    if (a.rule == 1) return d * d;
-    return d == 0 ? int64_t(0) : (2 * d - 1) * (2 * d - 1);
+    const I t = point ? d : 2 * d - 1;
+    return d == 0 ? I(0) : t * t;
   };
-  auto isqrt64 = [](int64_t m) {
-    int64_t r = static_cast<int64_t>(sqrt(static_cast<double>(m)));
+  auto isqrt_i = [](I m) {
+    I r = SMALL ? static_cast<I>(sqrtf(static_cast<float>(m))) : static_cast<I>(sqrt(static_cast<double>(m)));
     while (r * r > m) --r;
     while ((r + 1) * (r + 1) <= m) ++r;
     return r;
@@ -298,31 +304,33 @@ __global__ void __launch_bounds__(256) span_eval(SpanArgs a) {
       k[DIM - 1] = kc;
       int64_t er, el;
       if (a.intspan) {
-        int64_t q = 0;
-        if (DIM > 1) q += term(a0 - ki[0]);
-        if (DIM > 2) q += term(a1 - ki[1]);
+        I q = 0;
+        if (DIM > 1) q += term(static_cast<I>(a0 - ki[0]));
+        if (DIM > 2) q += term(static_cast<I>(a1 - ki[1]));
         if (q > mhi) continue;
         if (q >= mlo && !member<DIM>(a.rule, k, x, h, delta, r2max)) continue;
-        int64_t ein = 0;                       // largest e with q + term(e) < mlo
+        I ein = 0;                             // largest e with q + term(e) < mlo
         if (q < mlo) {
-          const int64_t t = isqrt64(mlo - 1 - q);
-          ein = a.rule == 1 ? t : (t + 1) / 2;
+          const I t = isqrt_i(mlo - 1 - q);
+          ein = point ? t : (t + 1) / 2;
         }
-        er = el = ein;
+        I ir = ein, il = ein;
         if (q + term(ein + 1) <= mhi) {        // tie band: the float predicate, each side on its own
           for (;;) {
-            if (q + term(er + 1) > mhi) break;
-            k[DIM - 1] = kc + er + 1;
+            if (q + term(ir + 1) > mhi) break;
+            k[DIM - 1] = kc + ir + 1;
             if (!member<DIM>(a.rule, k, x, h, delta, r2max)) break;
-            ++er;
+            ++ir;
           }
           for (;;) {
-            if (q + term(el + 1) > mhi) break;
-            k[DIM - 1] = kc - (el + 1);
+            if (q + term(il + 1) > mhi) break;
+            k[DIM - 1] = kc - (il + 1);
             if (!member<DIM>(a.rule, k, x, h, delta, r2max)) break;
-            ++el;
+            ++il;
           }
         }
+        er = ir;
+        el = il;
       } else {
         if (!member<DIM>(a.rule, k, x, h, delta, r2max)) continue;
         // span estimate from the radius left for this row
@@ -624,10 +632,12 @@ void spans_apply(Plan& P, const double* u, double* out, cudaStream_t s) {
   static const bool intspan = [] { const char* e = std::getenv("NLG_SPAN_INT"); return !(e && std::atoi(e) == 0); }();
   a.intspan = intspan;
   const unsigned blocks = static_cast<unsigned>((P.n_out + 255) / 256);
+  const double ec = 2.0 * P.delta_max / P.geom.h + 4.0;
+  const bool small = ec * ec * P.geom.dim < 1.0e9;      // every integer of the classification below 2^30
   switch (P.geom.dim) {
-    case 1: span_eval<1><<<blocks, 256, 0, s>>>(a); break;
-    case 2: span_eval<2><<<blocks, 256, 0, s>>>(a); break;
-    default: span_eval<3><<<blocks, 256, 0, s>>>(a); break;
+    case 1: if (small) span_eval<1, true><<<blocks, 256, 0, s>>>(a); else span_eval<1, false><<<blocks, 256, 0, s>>>(a); break;
+    case 2: if (small) span_eval<2, true><<<blocks, 256, 0, s>>>(a); else span_eval<2, false><<<blocks, 256, 0, s>>>(a); break;
+    default: if (small) span_eval<3, true><<<blocks, 256, 0, s>>>(a); else span_eval<3, false><<<blocks, 256, 0, s>>>(a); break;
   }
   stage_end(P, s, kStSpanEval, ev, 1);
 }
