@@ -83,6 +83,9 @@ using namespace stockham;
 
 // Strided passes: C = 4 columns per CTA (64-byte row pieces, two CTAs per SM: 3.6 ms per y pass at
 // 768^3 against 5.2 ms for C = 8 with one CTA per SM); NLG_F3_COLS=8 (plan time) selects 8.
+#ifndef NLG_F3_COLS_MINB
+#define NLG_F3_COLS_MINB(C) (8 / (C))   // resident CTAs per SM the register budget is capped for
+#endif
 constexpr int kF3El = 8;     // elements per thread per stage
 constexpr int kF3MaxG = 7;   // kernel support radius r_f <= 6 (partial spectra per column in registers)
 
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(rows_threads<L, false>(), 5) f3_rows_fwd_multi
 // PB / PD: C adjacent kx columns along y in one plane. PB reads y < n
 // (zero padding above) and writes every ky; PD reads every ky and writes y < n.
 template <int L, bool PD, int C>
-__global__ void __launch_bounds__(cols_threads3<L, C>(), 8 / C) f3_cols(const __grid_constant__ F3Args a) {
+__global__ void __launch_bounds__(cols_threads3<L, C>(), NLG_F3_COLS_MINB(C)) f3_cols(const __grid_constant__ F3Args a) {
   constexpr int T = cols_threads3<L, C>();
   extern __shared__ double2 fsm3[];
   const int tid = threadIdx.x;

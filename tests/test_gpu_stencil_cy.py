@@ -40,7 +40,8 @@ def _fields(dim, n, lo, hi, seed):
 # (dim, n, lowest, highest horizon in cells, kappa weighting)
 SCALAR = [(2, 96, 2.0, 5.5, True), (2, 100, 3.0, 7.9, True), (2, 100, 3.0, 7.9, False), (2, 72, 4.0, 12.0, True),
           (2, 101, 2.0, 6.3, True), (2, 64, 0.4, 3.2, True), (3, 40, 2.0, 4.9, True), (3, 36, 3.0, 5.5, True),
-          (3, 34, 2.0, 4.2, False), (3, 48, 4.0, 8.0, True)]
+          (3, 34, 2.0, 4.2, False), (3, 48, 4.0, 8.0, True),
+          (2, 16, 2.0, 6.0, True), (3, 12, 2.0, 5.0, True)]   # boxes wider than the grid
 
 
 @pytest.mark.parametrize("dim,n,lo,hi,kw", SCALAR)
