@@ -428,7 +428,7 @@ nlg_status nlg_apply_fast_dev_begin(nlg_plan* plan, const double* u_dev, double*
       stencil_box_in(P, u_dev, P.halo_lo, rows_in - P.halo_hi, static_cast<cudaStream_t>(stream));
       NLG_CUDA(cudaGetLastError());
       P.split_begun = true;
-    } else if (P.fast_method == 3 && P.geom.dim >= 2 && components(P) == 1 && (P.halo_lo > 0 || P.halo_hi > 0)) {
+    } else if (P.fast_method == 3 && P.geom.dim >= 2 && (P.halo_lo > 0 || P.halo_hi > 0)) {
       // stencil slab: the output rows whose whole window lies in the owned
       // input rows (r >= H past a lower halo, r < rows_out - H before an upper
       // one), cut at CTA-row multiples so the result is bit-identical

@@ -152,6 +152,40 @@ def test_split_phase_stencil_slab(N, dim, n, rows):
     assert np.array_equal(a, b)
 
 
+def test_split_phase_peridynamic_slab(N):
+    """begin + end on a sharded 2-D peridynamic slab (two component planes,
+    strided by the slab's n_in / n_out) equals the one-call device apply."""
+    import torch
+    from paper_1905_08375_b200 import configs, nonloc as NL
+    n, (rb, re) = 512, (128, 330)
+    w = configs.cfg3(n)
+    dmax = float(w.delta.max())
+    halo = NL.halo_rows(dim=2, n=n, family=5, delta_max=dmax)
+    ib, ie = max(0, rb - halo), min(n, re + halo)
+    sl = slice(ib * n, ie * n)
+    kw = w.op_kwargs()
+    for key in ("delta", "coeff"):
+        kw[key] = kw[key][sl] if kw[key] is not None else None
+    op = N.NonlocalOperator(2, n, row_begin=rb, row_end=re, reach=dmax, **kw)
+    u = np.concatenate([w.u[:n * n][sl], w.u[n * n:][sl]])
+    plan = op.plan
+    ud = torch.from_numpy(u).cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for split in (False, True):
+        od = torch.zeros(2 * plan.n_out, dtype=torch.float64, device="cuda")
+        if split:
+            plan.apply_fast_dev_begin(ud.data_ptr(), od.data_ptr(), s)
+            plan.apply_fast_dev_end(ud.data_ptr(), od.data_ptr(), s)
+        else:
+            plan.apply_fast_dev(ud.data_ptr(), od.data_ptr(), s)
+        torch.cuda.synchronize()
+        outs.append(od.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    whole = N.NonlocalOperator(2, n, **w.op_kwargs()).apply(w.u).reshape(2, n, n)[:, rb:re].reshape(-1)
+    assert np.max(np.abs(outs[0] - whole)) <= 1e-12 * np.max(np.abs(whole))
+
+
 @pytest.mark.parametrize("case", ["box", "stencil3d"])
 def test_pipeline_sharded_slab_bitwise(N, case):
     """The host pipeline on a sharded slab plan (input rows = owned rows +
