@@ -102,5 +102,10 @@ def slab_apply(sl: Slab, plan, u_in, out, stream: int = 0) -> None:
     u_in covers the slab's input rows; only its owned rows need to be valid on
     entry."""
     plan.apply_fast_dev_begin(u_in.data_ptr(), out.data_ptr(), stream)
-    sl.exchange(u_in)
+    comps = int(getattr(plan, "components", 1))
+    if comps == 1:
+        sl.exchange(u_in)
+    else:   # vector fields (peridynamics): SoA component planes of n_in nodes, each with its own halos
+        for c in range(comps):
+            sl.exchange(u_in[c * sl.n_in:(c + 1) * sl.n_in])
     plan.apply_fast_dev_end(u_in.data_ptr(), out.data_ptr(), stream)

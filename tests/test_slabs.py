@@ -237,3 +237,51 @@ def test_cfg1_full_size_slabs_as_in_bench(world, orc):
         parts.append(op.apply(sl.input_slice(w.u)))
     got = np.concatenate(parts)
     assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
+
+def _two_plane_worker(rank, world, port, n, halo, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_1905_08375_b200.slabs import Slab, slab_apply
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    stride = n
+    u = np.random.default_rng(8).standard_normal(2 * n * n)
+    sl = Slab(n, stride, halo, rank, world)
+    own = sl.output_slice()
+    u_in = torch.full((2 * sl.n_in,), float("nan"), dtype=torch.float64)
+    for c in range(2):
+        o = c * sl.n_in + sl.halo_lo * stride
+        u_in[o:o + sl.n_out] = torch.from_numpy(u[c * n * n:(c + 1) * n * n][own])
+
+    class P:
+        components = 2
+
+        def apply_fast_dev_begin(self, *a):
+            pass
+
+        def apply_fast_dev_end(self, *a):
+            pass
+
+    slab_apply(sl, P(), u_in, u_in, 0)
+    want = np.concatenate([u[c * n * n:(c + 1) * n * n][sl.in_begin * stride: sl.in_end * stride] for c in range(2)])
+    q.put((rank, bool(np.array_equal(u_in.numpy(), want))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_two_component_halo_exchange_world2():
+    """slab_apply on a two-component field (peridynamics, SoA planes): every
+    plane's halo rows arrive from the neighbour's owned rows of the same plane."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_plane_worker, args=(r, 2, 29811, 48, 9, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, exact in res:
+        assert exact, f"rank {rank}: halo rows of a component plane differ"
