@@ -867,6 +867,14 @@ constexpr int kCyR = NLG_CY_R;          // targets per lane: 16, 12 or 8 (5, 4, 
 #ifndef NLG_CY_RING
 #define NLG_CY_RING 1
 #endif
+#ifndef NLG_CY_U
+#define NLG_CY_U 4                      // steps per chunk (4 or 2): the window holds kCyR + U sources
+#endif
+#ifndef NLG_CY_U3
+#define NLG_CY_U3 2                     // 3-D scalar kernel: sweeps are ~9 steps, 2-step chunks waste fewer masked steps
+#endif
+constexpr int kCyU = NLG_CY_U;          // 2-D kernels
+#define NLG_CY_NPH ((NLG_CY_R + NLG_CY_U) / NLG_CY_U)   // ring phases (2-D)
 #ifndef NLG_CY_MINB2
 #define NLG_CY_MINB2 2                  // resident CTAs per SM the register budget allows (2-D, 3-D)
 #endif
@@ -922,79 +930,79 @@ __device__ __forceinline__ void cy_mbar_wait(unsigned mb, unsigned parity) {
 // sliding by four costs no register moves.
 // BWC: the row pitch of the box as a compile-time constant (the BASELINE reaches: every window load
 // then carries its row offset as an immediate), 0: the run-time pitch bw_rt
-template <bool KW, int PH, int BWC>
+template <bool KW, int PH, int BWC, int U>
 __device__ __forceinline__ void cy_chunk(double (&a0)[kCyR], double (&a1)[kCyR], const int (&M)[kCyR],
-                                         double (&Wu)[kCyR + 4], double (&Wk)[kCyR + 4], const double*& up,
+                                         double (&Wu)[kCyR + U], double (&Wk)[kCyR + U], const double*& up,
                                          const double*& um, const double*& kp, const double*& km, int bw_rt,
                                          const double*& wk, int dy0, int YW, int YN, int c0) {
-  constexpr int NW = kCyR + 4;
+  constexpr int NW = kCyR + U;
   const int BW = BWC ? BWC : bw_rt;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    Wu[(kCyR + j + 4 * PH) % NW] = up[j * BW] + um[j * BW];
-    if (KW) Wk[(kCyR + j + 4 * PH) % NW] = kp[j * BW] + km[j * BW];
+  for (int j = 0; j < U; ++j) {
+    Wu[(kCyR + j + U * PH) % NW] = up[j * BW] + um[j * BW];
+    if (KW) Wk[(kCyR + j + U * PH) % NW] = kp[j * BW] + km[j * BW];
   }
 #if NLG_CY_STEPSEL
   // per step: every target of the warp includes it (|d|^2 <= M_N: plain FMAs) or the weight is
   // selected to zero per target (overshoot steps of the last chunk have |d|^2 > M_W: all zero)
   (void)YW;
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
+  for (int s = 0; s < U; ++s) {
     const double w = wk[s];
     const int c = c0 + (dy0 + s) * (dy0 + s);
     if (c <= YN) {
 #pragma unroll
       for (int r = 0; r < kCyR; ++r) {
-        a0[r] = fma(w, Wu[(s + r + 4 * PH) % NW], a0[r]);
-        if (KW) a1[r] = fma(w, Wk[(s + r + 4 * PH) % NW], a1[r]);
+        a0[r] = fma(w, Wu[(s + r + U * PH) % NW], a0[r]);
+        if (KW) a1[r] = fma(w, Wk[(s + r + U * PH) % NW], a1[r]);
       }
     } else {
 #pragma unroll
       for (int r = 0; r < kCyR; ++r) {
         const double wr = c <= M[r] ? w : 0.0;
-        a0[r] = fma(wr, Wu[(s + r + 4 * PH) % NW], a0[r]);
-        if (KW) a1[r] = fma(wr, Wk[(s + r + 4 * PH) % NW], a1[r]);
+        a0[r] = fma(wr, Wu[(s + r + U * PH) % NW], a0[r]);
+        if (KW) a1[r] = fma(wr, Wk[(s + r + U * PH) % NW], a1[r]);
       }
     }
   }
 #else
-  if (!NLG_CY_ONEVAR && dy0 >= -YN && min(dy0 + 3, YW) <= YN) {   // every step of the chunk inside every target's ball
+  if (!NLG_CY_ONEVAR && dy0 >= -YN && min(dy0 + U - 1, YW) <= YN) {   // every step of the chunk inside every target's ball
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < U; ++s) {
       const double w = dy0 + s <= YW ? wk[s] : 0.0;   // overshoot steps of the last chunk
 #pragma unroll
       for (int r = 0; r < kCyR; ++r) {
-        a0[r] = fma(w, Wu[(s + r + 4 * PH) % NW], a0[r]);
-        if (KW) a1[r] = fma(w, Wk[(s + r + 4 * PH) % NW], a1[r]);
+        a0[r] = fma(w, Wu[(s + r + U * PH) % NW], a0[r]);
+        if (KW) a1[r] = fma(w, Wk[(s + r + U * PH) % NW], a1[r]);
       }
     }
   } else {
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < U; ++s) {
       const double w = wk[s];
       const int c = c0 + (dy0 + s) * (dy0 + s);
 #pragma unroll
       for (int r = 0; r < kCyR; ++r) {   // the weight selected to zero outside the target's own ball
         const double wr = c <= M[r] ? w : 0.0;
-        a0[r] = fma(wr, Wu[(s + r + 4 * PH) % NW], a0[r]);
-        if (KW) a1[r] = fma(wr, Wk[(s + r + 4 * PH) % NW], a1[r]);
+        a0[r] = fma(wr, Wu[(s + r + U * PH) % NW], a0[r]);
+        if (KW) a1[r] = fma(wr, Wk[(s + r + U * PH) % NW], a1[r]);
       }
     }
   }
 #endif
-  up += 4 * BW;
-  um += 4 * BW;
-  kp += 4 * BW;
-  km += 4 * BW;
-  wk += 4;
+  up += U * BW;
+  um += U * BW;
+  kp += U * BW;
+  km += U * BW;
+  wk += U;
 }
 
-template <bool KW, int BWC>
+template <bool KW, int BWC, int U>
 __device__ __forceinline__ void cy_sweep(double (&a0)[kCyR], double (&a1)[kCyR], const int (&M)[kCyR],
                                          const double* up, const double* um, const double* kp, const double* km,
                                          int bw_rt, const double* wk, int YW, int YN, int c0) {
   const int BW = BWC ? BWC : bw_rt;
-  double Wu[kCyR + 4], Wk[kCyR + 4];
+  double Wu[kCyR + U], Wk[kCyR + U];
 #pragma unroll
   for (int i = 0; i < kCyR; ++i) {
     Wu[i] = up[i * BW] + um[i * BW];
@@ -1007,28 +1015,28 @@ __device__ __forceinline__ void cy_sweep(double (&a0)[kCyR], double (&a1)[kCyR],
   const int nsteps = 2 * YW + 1;
   int s0 = 0;
 #define NLG_CY_CHUNK(PH)                                                                   \
-  cy_chunk<KW, PH, BWC>(a0, a1, M, Wu, Wk, up, um, kp, km, BW, wk, s0 - YW, YW, YN, c0);   \
-  s0 += 4;                                                                                 \
+  cy_chunk<KW, PH, BWC, U>(a0, a1, M, Wu, Wk, up, um, kp, km, BW, wk, s0 - YW, YW, YN, c0);   \
+  s0 += U;                                                                              \
   if (s0 >= nsteps) break;
 #if NLG_CY_RING
   for (;;) {
     NLG_CY_CHUNK(0)
     NLG_CY_CHUNK(1)
     NLG_CY_CHUNK(2)
-#if NLG_CY_R >= 12
-    NLG_CY_CHUNK(3)
-#endif
-#if NLG_CY_R >= 16
-    NLG_CY_CHUNK(4)
-#endif
+    if constexpr ((kCyR + U) / U >= 4) {
+      NLG_CY_CHUNK(3)
+    }
+    if constexpr ((kCyR + U) / U >= 5) {
+      NLG_CY_CHUNK(4)
+    }
   }
 #else
   for (;;) {   // one chunk body, the window shifted by register moves
     NLG_CY_CHUNK(0)
 #pragma unroll
     for (int i = 0; i < kCyR; ++i) {
-      Wu[i] = Wu[i + 4];
-      if (KW) Wk[i] = Wk[i + 4];
+      Wu[i] = Wu[i + U];
+      if (KW) Wk[i] = Wk[i + U];
     }
   }
 #endif
@@ -1215,8 +1223,8 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), DIM == 2 ? NLG_CY_MINB2 
         const int YN = MN >= c0 && MN <= MW ? isq[MN - c0] : -1;
 #endif
         const int o = colbase - YW * BW;
-        cy_sweep<KW, BWC>(a0, a1, M, Tu + o + dx, Tu + o - dx, Tk + o + dx, Tk + o - dx, BW, wd + dx * a.ws + H - YW, YW,
-                          YN, c0);
+        cy_sweep<KW, BWC, (DIM == 3 ? NLG_CY_U3 : NLG_CY_U)>(a0, a1, M, Tu + o + dx, Tu + o - dx, Tk + o + dx,
+                                                              Tk + o - dx, BW, wd + dx * a.ws + H - YW, YW, YN, c0);
       }
     }
     if (DIM == 3 && dz + 1 <= Rz) {
@@ -1301,44 +1309,44 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), DIM == 2 ? NLG_CY_MINB2 
 //   out0 += M00 (u0+ + u0-) + M01 (u1+ - u1-),  out1 += M01 (u0+ - u0-) + M11 (u1+ + u1-),
 // one output component per pass (two windows of kCyR + 4 in registers).
 template <int PH, int BWC>
-__device__ __forceinline__ void cyp_chunk(double (&acc)[kCyR], const int (&M)[kCyR], double (&Ws)[kCyR + 4],
-                                          double (&Wd)[kCyR + 4], const double*& sp, const double*& sm,
+__device__ __forceinline__ void cyp_chunk(double (&acc)[kCyR], const int (&M)[kCyR], double (&Ws)[kCyR + kCyU],
+                                          double (&Wd)[kCyR + kCyU], const double*& sp, const double*& sm,
                                           const double*& dp, const double*& dm, int bw_rt, const double*& wa,
                                           const double*& wb, int dy0, int YW, int YN, int c0) {
-  constexpr int NW = kCyR + 4;
+  constexpr int NW = kCyR + kCyU;
   const int BW = BWC ? BWC : bw_rt;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    Ws[(kCyR + j + 4 * PH) % NW] = sp[j * BW] + sm[j * BW];
-    Wd[(kCyR + j + 4 * PH) % NW] = dp[j * BW] - dm[j * BW];
+  for (int j = 0; j < kCyU; ++j) {
+    Ws[(kCyR + j + kCyU * PH) % NW] = sp[j * BW] + sm[j * BW];
+    Wd[(kCyR + j + kCyU * PH) % NW] = dp[j * BW] - dm[j * BW];
   }
-  if (dy0 >= -YN && min(dy0 + 3, YW) <= YN) {
+  if (dy0 >= -YN && min(dy0 + kCyU - 1, YW) <= YN) {
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < kCyU; ++s) {
       const bool on = dy0 + s <= YW;
       const double a = on ? wa[s] : 0.0, b = on ? wb[s] : 0.0;
 #pragma unroll
       for (int r = 0; r < kCyR; ++r)
-        acc[r] = fma(a, Ws[(s + r + 4 * PH) % NW], fma(b, Wd[(s + r + 4 * PH) % NW], acc[r]));
+        acc[r] = fma(a, Ws[(s + r + kCyU * PH) % NW], fma(b, Wd[(s + r + kCyU * PH) % NW], acc[r]));
     }
   } else {
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < kCyU; ++s) {
       const double a = wa[s], b = wb[s];
       const int c = c0 + (dy0 + s) * (dy0 + s);
 #pragma unroll
       for (int r = 0; r < kCyR; ++r) {
-        const double t = fma(a, Ws[(s + r + 4 * PH) % NW], fma(b, Wd[(s + r + 4 * PH) % NW], acc[r]));
+        const double t = fma(a, Ws[(s + r + kCyU * PH) % NW], fma(b, Wd[(s + r + kCyU * PH) % NW], acc[r]));
         acc[r] = c <= M[r] ? t : acc[r];
       }
     }
   }
-  sp += 4 * BW;
-  sm += 4 * BW;
-  dp += 4 * BW;
-  dm += 4 * BW;
-  wa += 4;
-  wb += 4;
+  sp += kCyU * BW;
+  sm += kCyU * BW;
+  dp += kCyU * BW;
+  dm += kCyU * BW;
+  wa += kCyU;
+  wb += kCyU;
 }
 
 template <int BWC>
@@ -1346,7 +1354,7 @@ __device__ __forceinline__ void cyp_sweep(double (&acc)[kCyR], const int (&M)[kC
                                           const double* sm, const double* dp, const double* dm, int bw_rt,
                                           const double* wa, const double* wb, int YW, int YN, int c0) {
   const int BW = BWC ? BWC : bw_rt;
-  double Ws[kCyR + 4], Wd[kCyR + 4];
+  double Ws[kCyR + kCyU], Wd[kCyR + kCyU];
 #pragma unroll
   for (int i = 0; i < kCyR; ++i) {
     Ws[i] = sp[i * BW] + sm[i * BW];
@@ -1360,16 +1368,16 @@ __device__ __forceinline__ void cyp_sweep(double (&acc)[kCyR], const int (&M)[kC
   int s0 = 0;
 #define NLG_CYP_CHUNK(PH)                                                             \
   cyp_chunk<PH, BWC>(acc, M, Ws, Wd, sp, sm, dp, dm, BW, wa, wb, s0 - YW, YW, YN, c0);  \
-  s0 += 4;                                                                            \
+  s0 += kCyU;                                                                         \
   if (s0 >= nsteps) break;
   for (;;) {
     NLG_CYP_CHUNK(0)
     NLG_CYP_CHUNK(1)
     NLG_CYP_CHUNK(2)
-#if NLG_CY_R >= 12
+#if NLG_CY_NPH >= 4
     NLG_CYP_CHUNK(3)
 #endif
-#if NLG_CY_R >= 16
+#if NLG_CY_NPH >= 5
     NLG_CYP_CHUNK(4)
 #endif
   }
