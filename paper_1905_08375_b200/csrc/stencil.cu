@@ -876,7 +876,7 @@ constexpr int kCyR = NLG_CY_R;          // targets per lane: 16, 12 or 8 (5, 4, 
 constexpr int kCyU = NLG_CY_U;          // 2-D kernels
 #define NLG_CY_NPH ((NLG_CY_R + NLG_CY_U) / NLG_CY_U)   // ring phases (2-D)
 #ifndef NLG_CY_MINB2
-#define NLG_CY_MINB2 2                  // resident CTAs per SM the register budget allows (2-D, 3-D)
+#define NLG_CY_MINB2 4                  // resident CTAs per SM the register budget allows (2-D, 3-D)
 #endif
 #ifndef NLG_CY_MINB3
 #define NLG_CY_MINB3 3
@@ -888,7 +888,7 @@ constexpr int kCyU = NLG_CY_U;          // 2-D kernels
 #define NLG_CY_STEPSEL 0                // 1: plain / selected FMAs decided per step (YN carries M_N) instead of per chunk
 #endif
 #ifndef NLG_CY_W2
-#define NLG_CY_W2 8
+#define NLG_CY_W2 4
 #endif
 #ifndef NLG_CY_W3
 #define NLG_CY_W3 4
@@ -1057,7 +1057,8 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), DIM == 2 ? NLG_CY_MINB2 
   const int MBOX = cy_mbox(hs, NWP), hx = cy_hx(hs);
   double* Mu = csm + (KW ? 2 : 1) * BOX;                 // 3-D mirror planes
   double* Mk = KW ? Mu + MBOX : Mu;
-  const int W1 = H + 1, wlen = W1 * a.ws;                // weight rows of one |dz|: [|dx|][dy + H]
+  const int W1 = H + 1, wfull = W1 * a.ws;               // table rows of one |dz|: [|dx|][dy + H]
+  const int wlen = (hs + 1) * a.ws;                       // rows |dx| <= hs are all a sweep reads
   double* wt = Mu + (DIM == 3 ? (KW ? 2 : 1) * MBOX : 0);   // (rewritten per |dz| behind the tile barrier)
   int* isq = reinterpret_cast<int*>(wt + wlen);
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
@@ -1168,7 +1169,7 @@ __global__ void __launch_bounds__(32 * cy_warps<DIM>(), DIM == 2 ? NLG_CY_MINB2 
     // weight rows of this |dz| (row dx = 0 halved: its column is added to itself)
     double* wd = wt;
     {
-      const double* src = a.tab + static_cast<size_t>(dz) * wlen;
+      const double* src = a.tab + static_cast<size_t>(dz) * wfull;
       for (int i = tid; i < wlen; i += NT) wd[i] = (i < a.ws ? 0.5 : 1.0) * __ldg(src + i);
     }
     cy_mbar_wait(mb0, static_cast<unsigned>(dz & 1));
@@ -1741,7 +1742,7 @@ bool cy_encode(CUtensorMap* m, const double* base, int dim, int64_t n, int64_t r
 size_t cy_smem(const StArgs& a, int dim) {
   const int warps = cy_warps_rt(dim, a.kind);
   const int nf = a.kind == 1 ? 2 : (a.kw ? 2 : 1);
-  const size_t wlen = static_cast<size_t>(a.H + 1) * a.ws * (a.kind == 1 ? 3 : 1);
+  const size_t wlen = a.kind == 1 ? static_cast<size_t>(a.H + 1) * a.ws * 3 : static_cast<size_t>(a.hs + 1) * a.ws;
   return sizeof(double) * (static_cast<size_t>(nf) * (cy_box(a.hs, warps) + (dim == 3 ? cy_mbox(a.hs, warps) : 0)) + wlen) +
          sizeof(int) * (isq_len(a.H) + 1);
 }
