@@ -83,6 +83,9 @@ using namespace stockham;
 
 // Strided passes: C = 4 columns per CTA (64-byte row pieces, two CTAs per SM: 3.6 ms per y pass at
 // 768^3 against 5.2 ms for C = 8 with one CTA per SM); NLG_F3_COLS=8 (plan time) selects 8.
+#ifndef NLG_F3_ROWS_MINB
+#define NLG_F3_ROWS_MINB 1            // row passes: resident CTAs per SM the register budget is capped for
+#endif
 #ifndef NLG_F3_COLS_MINB
 #define NLG_F3_COLS_MINB(C) (8 / (C))   // resident CTAs per SM the register budget is capped for
 #endif
@@ -126,7 +129,7 @@ struct F3Args {
 // AB (inverse only): store (A, B) into the row (the tie pass combines);
 // otherwise the inverse pass applies the combine (and then runs faster at L / 8).
 template <int L, bool INV, bool KW, bool AB = false>
-__global__ void __launch_bounds__(rows_threads<L, INV && !AB>()) f3_rows(const __grid_constant__ F3Args a) {
+__global__ void __launch_bounds__(rows_threads<L, INV && !AB>(), NLG_F3_ROWS_MINB) f3_rows(const __grid_constant__ F3Args a) {
   constexpr int T = rows_threads<L, INV && !AB>();
   __shared__ double2 sm[L + L / 8];
   const int64_t r = blockIdx.x;                      // row within the launch
