@@ -79,18 +79,39 @@ __global__ void __launch_bounds__(kScanThreads) scan_lookback(const double* __re
     v[j] = p < lim ? u[b0 + p] : 0.0;
     run = dd_add(run, {v[j], 0.0});
   }
-  sh[tid] = run.hi;
-  sl[tid] = run.lo;
-  __syncthreads();
-  for (int off = 1; off < kScanThreads; off <<= 1) {
-    dd add{0.0, 0.0};
-    if (tid >= off) add = {sh[tid - off], sl[tid - off]};
-    __syncthreads();
-    if (tid >= off) {
-      const dd cur = dd_add({sh[tid], sl[tid]}, add);
-      sh[tid] = cur.hi;
-      sl[tid] = cur.lo;
+  // inclusive scan of the thread sums over the CTA: warp shuffles, then the warp totals (three
+  // barriers; the shared-memory Hillis-Steele it replaces took sixteen)
+  {
+    constexpr int NWARP = kScanThreads / 32;
+    __shared__ double wh[NWARP], wl[NWARP];
+    const int ln = tid & 31, wp = tid >> 5;
+    dd inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double hi = __shfl_up_sync(0xffffffffu, inc.hi, o), lo = __shfl_up_sync(0xffffffffu, inc.lo, o);
+      if (ln >= o) inc = dd_add(inc, {hi, lo});
     }
+    if (ln == 31) {
+      wh[wp] = inc.hi;
+      wl[wp] = inc.lo;
+    }
+    __syncthreads();
+    if (wp == 0) {
+      dd w = ln < NWARP ? dd{wh[ln], wl[ln]} : dd{0.0, 0.0};
+#pragma unroll
+      for (int o = 1; o < NWARP; o <<= 1) {
+        const double hi = __shfl_up_sync(0xffffffffu, w.hi, o), lo = __shfl_up_sync(0xffffffffu, w.lo, o);
+        if (ln >= o) w = dd_add(w, {hi, lo});
+      }
+      if (ln < NWARP) {
+        wh[ln] = w.hi;
+        wl[ln] = w.lo;
+      }
+    }
+    __syncthreads();
+    if (wp > 0) inc = dd_add({wh[wp - 1], wl[wp - 1]}, inc);
+    sh[tid] = inc.hi;
+    sl[tid] = inc.lo;
     __syncthreads();
   }
   if (tid < 32) {   // warp 0: publish, then look back 32 predecessors at a time
