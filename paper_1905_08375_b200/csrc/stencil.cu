@@ -379,10 +379,6 @@ __host__ __device__ inline int tile2d_q(int H, int bx = kBX) { return bx / 4 + 2
 __host__ __device__ inline int tile2d_rs(int H, int bx = kBX) { return 4 * tile2d_q(H, bx) + 1; }  // row stride in slots (odd)
 __host__ __device__ inline int isq_len(int H) { return (H + 1) * (H + 1) + 1; }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool in) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(in ? 16 : 0) : "memory");
-}
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool in) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(in ? 8 : 0) : "memory");
